@@ -1,0 +1,277 @@
+"""Generate golden fixtures by running the REFERENCE package itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports ``scatterconv`` from /root/reference/pkg/src (numba cache
+redirected to /tmp so nothing is written into the read-only reference tree),
+runs the reference's own entry points on seeded inputs and writes:
+
+  ref_small.npz      ragged random pairs: scatter_convolve, commuted_convolve,
+                     direct_form, skip-zeros outputs (float64, bit-exact)
+  ref_engine.json    scripted ScatterEngine sessions (blocks, samples,
+                     swaps, deferred swaps, flush, state) with every output
+                     recorded as float.hex -- bit-exact goldens
+  ref_configs.npz    per-config reference pins: sha256 of the reference's
+                     output on cfg1/cfg2 in full and cfg3/4/5 prefixes, plus
+                     sampled values and exact direct_form (fsum) samples
+
+The fixtures are committed; the GPU box never needs /root/reference.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import pathlib
+import sys
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+REPO = HERE.parent.parent
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_golden")
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, str(REPO))
+
+from scatterconv import core as rcore  # noqa: E402  (the reference)
+from scatterconv.core import Signal  # noqa: E402
+from scatterconv.engine import EngineConfig, ScatterEngine  # noqa: E402
+
+from paper_2401_01607_b200 import configs  # noqa: E402  (seeded generators only)
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def full(out) -> np.ndarray:
+    return out.concatenated().samples
+
+
+# ----------------------------------------------------------------- small pairs
+
+
+def make_small():
+    rng = np.random.default_rng(20240101)
+    es, hs, kinds, thr = [], [], [], []
+    for i in range(400):
+        ne, nh = int(rng.integers(1, 65)), int(rng.integers(1, 65))
+        e = rng.uniform(-1, 1, ne)
+        h = rng.uniform(-1, 1, nh)
+        kind = i % 4
+        if kind == 1:  # exact zeros sprinkled (skip-zeros cases)
+            e[rng.uniform(0, 1, ne) < 0.3] = 0.0
+        if kind == 2:  # tiny values around a threshold
+            e[rng.uniform(0, 1, ne) < 0.3] *= 1e-3
+        es.append(e)
+        hs.append(h)
+        kinds.append(kind)
+        thr.append(0.0 if kind != 2 else 5e-4)
+    # edge cases: single tap, single sample, -0.0, ints
+    es += [np.array([1.0, 0.0, 0.0, 0.0]), np.array([-0.0, 1.0, -0.0]), np.array([1.0]),
+           np.array([2.0, 3.0])]
+    hs += [np.array([9.0]), np.array([0.5, -0.25, 0.125]), np.array([5.0, 6.0, 7.0]),
+           np.array([1.0])]
+    kinds += [0, 0, 0, 0]
+    thr += [0.0, 0.0, 0.0, 0.0]
+
+    sc, cm, df, sk = [], [], [], []
+    for e, h, t in zip(es, hs, thr):
+        E, H = Signal(e), Signal(h)
+        sc.append(full(rcore.scatter_convolve(E, H)))
+        cm.append(full(rcore.commuted_convolve(E, H)))
+        df.append(rcore.direct_form(E, H).samples)
+        sk.append(full(rcore.scatter_convolve_skip_zeros(E, H, t)))
+
+    def pack(arrs):
+        off = np.cumsum([0] + [len(a) for a in arrs]).astype(np.int64)
+        return np.concatenate(arrs), off
+
+    data = {}
+    for name, arrs in (("e", es), ("h", hs), ("scatter", sc), ("commuted", cm), ("direct", df),
+                       ("skip", sk)):
+        v, off = pack(arrs)
+        data[name] = v
+        data[name + "_off"] = off
+    data["threshold"] = np.asarray(thr)
+    data["kind"] = np.asarray(kinds)
+    np.savez_compressed(HERE / "ref_small.npz", **data)
+    print("ref_small.npz:", len(es), "pairs")
+
+
+# -------------------------------------------------------------- engine sessions
+
+
+def hexlist(a) -> list:
+    return [float(v).hex() for v in np.asarray(a, dtype=np.float64).ravel()]
+
+
+def run_session(h, nb, threshold, ops):
+    """Apply ops to a reference engine; return recorded outputs."""
+    eng = ScatterEngine(Signal(h), EngineConfig(block_size_nb=nb, zero_skip_threshold=threshold))
+    rec = []
+    for op in ops:
+        kind = op[0]
+        if kind == "block":
+            rec.append(hexlist(eng.process_block(Signal(np.asarray(op[1]))).samples))
+        elif kind == "sample":
+            rec.append(hexlist([eng.process_sample(op[1])]))
+        elif kind == "swap":
+            eng.swap_ir(Signal(np.asarray(op[1])))
+            rec.append([])
+        elif kind == "defer":
+            eng.swap_ir_at_next_block(Signal(np.asarray(op[1])))
+            rec.append([])
+        elif kind == "flush":
+            rec.append(hexlist(eng.flush().samples))
+        elif kind == "state":
+            rec.append({"read_index": int(eng.read_index), "ring": hexlist(eng.ring),
+                        "consumed": int(eng.samples_consumed), "live": int(eng._live),
+                        "sched": hexlist(eng._schedule_order())})
+        else:
+            raise ValueError(kind)
+    return rec
+
+
+def make_engine():
+    rng = np.random.default_rng(20240102)
+    sessions = []
+
+    def add(h, nb, thr, ops, tag):
+        ops_json = []
+        for op in ops:
+            if op[0] in ("block", "swap", "defer"):
+                ops_json.append([op[0], hexlist(op[1])])
+            elif op[0] == "sample":
+                ops_json.append([op[0], float(op[1]).hex()])
+            else:
+                ops_json.append([op[0]])
+        sessions.append({"tag": tag, "h": hexlist(h), "nb": nb, "threshold": float(thr).hex(),
+                         "ops": ops_json, "expect": run_session(h, nb, thr, ops)})
+
+    # hand scenarios (test_engine.py:67-71, :216-223, :283-294)
+    add([3.0, 4.0], 8192, 0.0, [("sample", 1.0), ("sample", 2.0), ("flush",)], "hand_3_10_8")
+    add([1.0, 1.0], 8192, 0.0, [("sample", 1.0), ("sample", 0.0), ("swap", [5.0, 5.0]),
+                                ("sample", 0.0), ("sample", 0.0), ("sample", 1.0), ("flush",)],
+        "hand_swap")
+    add([1.0, 2.0, 3.0, 4.0, 5.0, 6.0], 8192, 0.0,
+        [("sample", 1.0), ("swap", [9.0, 9.0]), ("state",), ("sample", 0.0), ("state",),
+         ("flush",), ("state",)], "shrink_drain")
+    add([3.0, 4.0, 5.0], 8192, 0.0, [("sample", 0.0), ("state",), ("sample", -0.0), ("state",)],
+        "zero_untouched")
+    add([1.0, 1.0], 8192, 0.0, [("block", [1.0, np.nan, 2.0]), ("flush",)], "nan_skipped")
+    add([1.0, 0.5], 8192, 0.0, [("block", [np.inf, 1.0]), ("flush",)], "inf_scatters")
+    add([0.5, 0.25], 4, 0.0, [("defer", [2.0, 2.0, 2.0]), ("block", [1.0, 1.0]), ("state",),
+                              ("flush",), ("state",)], "deferred")
+
+    # random sessions: blocks with random cuts, swaps (grow/shrink/same), deferred, samples
+    for s in range(120):
+        nh = int(rng.integers(1, 40))
+        nb = int(rng.integers(1, 70))
+        thr = 0.0 if s % 3 else float(rng.uniform(0, 0.3))
+        h = rng.uniform(-1, 1, nh)
+        ops = []
+        for _ in range(int(rng.integers(1, 9))):
+            r = rng.uniform()
+            if r < 0.55:
+                n = int(rng.integers(0, nb + 1))
+                x = rng.uniform(-1, 1, n)
+                x[rng.uniform(0, 1, n) < 0.2] = 0.0
+                ops.append(("block", x))
+            elif r < 0.7:
+                ops.append(("sample", float(rng.uniform(-1, 1))))
+            elif r < 0.82:
+                ops.append(("swap", rng.uniform(-1, 1, int(rng.integers(1, 50)))))
+            elif r < 0.9:
+                ops.append(("defer", rng.uniform(-1, 1, int(rng.integers(1, 50)))))
+            elif r < 0.95:
+                ops.append(("state",))
+            else:
+                ops.append(("flush",))
+        ops += [("state",), ("flush",), ("state",)]
+        add(h, nb, thr, ops, f"random_{s}")
+    with open(HERE / "ref_engine.json", "w", encoding="utf-8") as fh:
+        json.dump(sessions, fh, separators=(",", ":"))
+    print("ref_engine.json:", len(sessions), "sessions")
+
+
+# ------------------------------------------------------------------- configs
+
+
+def stream_reference(x64, h64, nb):
+    eng = ScatterEngine(Signal(h64), EngineConfig(block_size_nb=nb))
+    outs = [eng.process_block(Signal(x64[i:i + nb])).samples for i in range(0, len(x64), nb)]
+    outs.append(eng.flush().samples)
+    return np.concatenate(outs)
+
+
+def make_configs():
+    out = {}
+    sample_rng = np.random.default_rng(99)
+
+    # cfg1 (float64, full): scatter_convolve, engine and direct_form (fsum)
+    w = configs.cfg1()
+    E, H = Signal(w.x), Signal(w.h)
+    y_sc = full(rcore.scatter_convolve(E, H))
+    y_eng = stream_reference(w.x, w.h, 8192)
+    assert np.array_equal(y_sc, y_eng)
+    idx = np.sort(sample_rng.choice(w.nout, 2048, replace=False))
+    idx[:3] = [0, 1, w.nout - 1]
+    idx = np.unique(idx)
+    y_df = np.array([np.float64(__import__("math").fsum(
+        w.x[m] * w.h[n - m] for m in range(max(0, n - w.nh + 1), min(n, w.ne - 1) + 1)))
+        for n in idx])
+    out["cfg1_sha_scatter"] = sha(y_sc)
+    out["cfg1_idx"] = idx
+    out["cfg1_scatter_at_idx"] = y_sc[idx]
+    out["cfg1_direct_at_idx"] = y_df
+
+    # cfg2 (float32 inputs -> float64 reference): engine nb=256, swap every 100 blocks
+    w = configs.cfg2()
+    x64 = w.x.astype(np.float64)
+    eng = ScatterEngine(Signal(w.irs[0].astype(np.float64)), EngineConfig(block_size_nb=256))
+    outs = []
+    j = 0
+    for b, start in enumerate(range(0, len(x64), 256)):
+        if b > 0 and b % 100 == 0:
+            j += 1
+            eng.swap_ir(Signal(w.irs[j].astype(np.float64)))
+        outs.append(eng.process_block(Signal(x64[start:start + 256])).samples)
+    body = np.concatenate(outs)
+    tail = eng.flush().samples
+    out["cfg2_sha_body"] = sha(body)
+    out["cfg2_sha_tail"] = sha(tail)
+    idx = np.unique(sample_rng.choice(len(body), 4096, replace=False))
+    out["cfg2_idx"] = idx
+    out["cfg2_body_at_idx"] = body[idx]
+    out["cfg2_tail"] = tail.astype(np.float64)
+
+    # cfg3 / cfg4 / cfg5 prefixes through the reference engine (float64 on f32 values)
+    for name, x, h, n_pre in (
+        ("cfg3", configs.cfg3(ne=24000).x, configs.cfg3_h(), 24000),
+        ("cfg5", configs.cfg5_x(ne=6000), configs.cfg5_h(), 6000),
+    ):
+        x64 = x[:n_pre].astype(np.float64)
+        eng = ScatterEngine(Signal(h.astype(np.float64)), EngineConfig(block_size_nb=8192))
+        body = np.concatenate([eng.process_block(Signal(x64[i:i + 8192])).samples
+                               for i in range(0, n_pre, 8192)])
+        out[f"{name}_prefix_len"] = n_pre
+        out[f"{name}_sha_prefix_body"] = sha(body)
+        idx = np.unique(sample_rng.choice(n_pre, 512, replace=False))
+        out[f"{name}_idx"] = idx
+        out[f"{name}_body_at_idx"] = body[idx]
+    w = configs.cfg4(channels=2, ne=30000)
+    for c in range(2):
+        y = stream_reference(w.x[c].astype(np.float64), w.h[c].astype(np.float64), 8192)
+        out[f"cfg4_ch{c}_sha_full_ne30000"] = sha(y)
+    np.savez_compressed(HERE / "ref_configs.npz", **out)
+    print("ref_configs.npz:", sorted(out))
+
+
+if __name__ == "__main__":
+    make_small()
+    make_engine()
+    make_configs()
