@@ -1,0 +1,467 @@
+#!/usr/bin/env python
+"""Benchmark: convolution GMAC/s (out samples x taps) and % of FP32 FMA peak.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5]
+    python bench.py --impl reference ...        # CPU reference arm
+
+Default workload is BASELINE.json configs[4] (cfg5): 57,600,000 x 262,144
+float32, time-sharded over the N GPUs of one node (one process per GPU under
+torchrun; each rank owns an equal contiguous output segment and uploads its
+input slice plus the (Nh-1)-sample halo; no collective on the data path).
+A "step" is one full convolution of that workload.  Other configs
+(--config cfg1..cfg4) are available for profiling; the parity tests cover
+them all.
+
+Timing: W warm-up steps, then K steps, each bracketed by CUDA events on the
+launching stream, with a 256 MiB L2-flush memset before every step outside
+the events (inputs are also > L2 at N=1).  Barrier + synchronize around the
+region; the step time is the MAX over ranks.  `value` = total metric MACs /
+step time.  `e2e` = same metric through the public API with host (pinned)
+buffers, H2D + D2H inside the timed region.  `cpu_baseline` = the CPU oracle
+(restatement of the reference's scatter_block engine, float64) on a bounded
+sample, rank 0, N=1 only.  Rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = json.loads((REPO / "BASELINE.json").read_text())["metric"] if (REPO / "BASELINE.json").exists() \
+    else "convolution GMAC/s (out samples x taps) and % of FP32 FMA peak at 1/2/4/8 GPU"
+UNIT = "GMAC/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target seconds of CPU work for the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+# ------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    """Samples SM clock + clock-event reasons via NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period: float = 0.1):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._period = period
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self._nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = get_r(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(self._period)
+
+    def __enter__(self):
+        if self._nv:
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv and self._t.is_alive():
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ workloads
+
+
+def peaks():
+    p = {}
+    f = REPO / "MEASURED_PEAKS.json"
+    if f.exists():
+        p = json.loads(f.read_text())
+    return p
+
+
+class Work:
+    """One rank's share of a config: device inputs + a step() callable."""
+
+    def __init__(self, cfg, rank, world, device):
+        import torch
+
+        from paper_2401_01607_b200 import configs
+        from paper_2401_01607_b200.sharded import shard_plan
+
+        self.cfg = cfg
+        self.device = device
+        self.kind = cfg
+        if cfg in ("cfg5", "cfg3"):
+            w = configs.cfg5() if cfg == "cfg5" else configs.cfg3()
+            self.w = w
+            self.plan = shard_plan(w.ne, w.nh, world)
+            self.shard = self.plan[rank]
+            self.total_macs = w.metric_macs
+            self.rank_macs = self.shard.n_out * w.nh
+            self.x_host = w.x
+            self.h_host = w.h
+            self.xs = torch.from_numpy(w.x[self.shard.x_begin:self.shard.x_end]).to(device)
+            self.hd = torch.from_numpy(w.h).to(device)
+            self.parallelism = f"time-sharded x{world} (output segments + {w.nh - 1}-sample halo, no collective)"
+            self.scaling = "strong"
+            self.dtype = "f32"
+        elif cfg == "cfg4":
+            w = configs.cfg4()
+            self.w = w
+            per = -(-64 // world)
+            self.c0, self.c1 = min(64, rank * per), min(64, rank * per + per)
+            self.total_macs = w.metric_macs
+            self.rank_macs = (self.c1 - self.c0) * w.nout * w.nh
+            self.xd = torch.from_numpy(w.x[self.c0:self.c1]).to(device)
+            self.hd = torch.from_numpy(w.h[self.c0:self.c1]).to(device)
+            self.parallelism = f"channel-sharded x{world} (no collective)"
+            self.scaling = "strong"
+            self.dtype = "f32"
+        elif cfg == "cfg1":
+            w = configs.cfg1()
+            self.w = w
+            self.total_macs = w.metric_macs * world   # replicas
+            self.rank_macs = w.metric_macs
+            self.xd = torch.from_numpy(w.x).to(device)
+            self.hd = torch.from_numpy(w.h).to(device)
+            self.parallelism = f"replicas x{world}"
+            self.scaling = "weak"
+            self.dtype = "f64"
+        elif cfg == "cfg2":
+            w = configs.cfg2()
+            self.w = w
+            self.total_macs = (w.ne + w.nh - 1) * w.nh * world
+            self.rank_macs = (w.ne + w.nh - 1) * w.nh
+            self.xd = torch.from_numpy(w.x).to(device)
+            n_blocks = -(-w.ne // 256)
+            self.swaps = [(b, torch.from_numpy(w.irs[b // 100]).to(device)) for b in range(100, n_blocks, 100)]
+            self.h0 = torch.from_numpy(w.irs[0]).to(device)
+            self.parallelism = f"replicas x{world} (streaming is sequential per stream)"
+            self.scaling = "weak"
+            self.dtype = "f32"
+
+    def step(self):
+        import torch
+
+        from paper_2401_01607_b200.core import Signal, scatter_convolve
+        from paper_2401_01607_b200.engine import EngineConfig, ScatterEngine
+        from paper_2401_01607_b200.multichannel import convolve_batched
+        from paper_2401_01607_b200.sharded import convolve_shard
+
+        if self.cfg in ("cfg5", "cfg3"):
+            return convolve_shard(self.xs, self.shard, self.hd)
+        if self.cfg == "cfg4":
+            return convolve_batched(self.xd, self.hd)
+        if self.cfg == "cfg1":
+            return scatter_convolve(Signal(self.xd), Signal(self.hd)).concatenated().samples
+        if self.cfg == "cfg2":
+            eng = ScatterEngine(Signal(self.h0), EngineConfig(block_size_nb=256))
+            body = eng.process_stream(self.xd, 256, self.swaps)
+            return body
+        raise ValueError(self.cfg)
+
+    def e2e_step(self, x_pin, h_pin):
+        """Public API with host (pinned) buffers; returns (h2d, d2h) bytes."""
+        import torch.distributed as dist
+
+        from paper_2401_01607_b200.core import Signal, scatter_convolve
+        from paper_2401_01607_b200.multichannel import convolve_batched
+        from paper_2401_01607_b200.sharded import distributed_convolve
+
+        if self.cfg in ("cfg5", "cfg3"):
+            if dist.is_available() and dist.is_initialized():
+                sh, y = distributed_convolve(x_pin, h_pin, to_host=True)
+                return sh.n_in * 4 + len(h_pin) * 4, y.numel() * 4
+            out = scatter_convolve(Signal(x_pin), Signal(h_pin))   # body/tail: pinned host views
+            return x_pin.numel() * 4 + h_pin.numel() * 4, (len(out.body) + len(out.tail)) * 4
+        if self.cfg == "cfg4":
+            y = convolve_batched(x_pin, h_pin)
+            return x_pin.numel() * 4 + h_pin.numel() * 4, y.numel() * 4
+        raise ValueError("e2e only for cfg3/cfg4/cfg5")
+
+
+# ------------------------------------------------------------------ CPU reference
+
+
+def cpu_sample(cfg, seconds, threads):
+    """Time the oracle (float64 restatement of the reference engine) on a
+    bounded prefix of the workload sized to ~`seconds` of work."""
+    from oracle import oracle as O
+    from paper_2401_01607_b200 import configs
+
+    if cfg == "cfg4":
+        w = configs.cfg4(channels=64, ne=480000)
+        x, h = w.x, w.h
+    elif cfg == "cfg3":
+        x, h = configs.cfg3().x, configs.cfg3_h()
+    elif cfg == "cfg1":
+        w = configs.cfg1()
+        x, h = w.x, w.h
+    elif cfg == "cfg2":
+        w = configs.cfg2()
+        x, h = w.x, w.irs[0]
+    else:
+        x, h = configs.cfg5_x(ne=4_000_000), configs.cfg5_h()
+    x = np.asarray(x, np.float64)
+    h = np.asarray(h, np.float64)
+    if cfg == "cfg4":
+        # one engine per channel on a thread pool (the reference's pattern)
+        c = max(1, threads)
+        ne0 = 2000
+        t0 = time.perf_counter()
+        O.conv_channels(x[:c, :ne0], h[:c], nb=8192, threads=threads)
+        dt = time.perf_counter() - t0
+        rate = c * ne0 * h.shape[1] / dt
+        ne = int(min(x.shape[1], max(ne0, seconds * rate / (c * h.shape[1]))))
+        t0 = time.perf_counter()
+        O.conv_channels(x[:c, :ne], h[:c], nb=8192, threads=threads)
+        dt = time.perf_counter() - t0
+        macs = c * ne * h.shape[1]
+        return macs / dt / 1e9, f"{c} channels x {ne} samples x {h.shape[1]} taps ({macs:.3e} MAC, one float64 engine per channel, {threads} threads)", dt
+    nh = len(h)
+    s0 = max(threads, 2000)
+    t0 = time.perf_counter()
+    O.conv_parallel(x[:s0], h, nb=8192, threads=threads)
+    dt = time.perf_counter() - t0
+    rate = s0 * nh / dt
+    s = int(min(len(x), max(s0, seconds * rate / nh)))
+    t0 = time.perf_counter()
+    O.conv_parallel(x[:s], h, nb=8192, threads=threads)
+    dt = time.perf_counter() - t0
+    macs = s * nh
+    return macs / dt / 1e9, (f"x[:{s}] x {nh} taps ({macs:.3e} MAC actually scattered), float64 "
+                             f"scatter_block engine per input segment, overlap-add, {threads} threads"), dt
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    threads = len(os.sched_getaffinity(0))
+    per_step = max(2.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_sample(args.config, per_step / 4, threads)
+    rates, samples, times = [], [], []
+    for _ in range(args.steps):
+        r, s, dt = cpu_sample(args.config, per_step, threads)
+        rates.append(r)
+        samples.append(s)
+        times.append(dt)
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded PCG64, SURVEY.md 8(d))",
+        "config": {"workload": args.config, "parallelism": f"CPU, {threads} threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": samples[-1]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference is Python+numba (no compiled C to build); timed via the C restatement "
+                "of its scatter_block engine (oracle/), pinned bit-exact to the reference",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ main
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2401_01607_b200 import _native as N
+
+    rank, world, local = env_rank()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    device = torch.device("cuda", torch.cuda.current_device())
+    L = N.lib()
+    work = Work(args.config, rank, world, device)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)  # 256 MiB > L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up
+    for _ in range(max(args.warmup, 0)):
+        work.step()
+    torch.cuda.synchronize()
+    barrier()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    dev_index = torch.cuda.current_device()
+    phys = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")
+    nvml_index = int(phys[dev_index]) if len(phys) > dev_index and phys[dev_index].strip().isdigit() else dev_index
+    torch.cuda.synchronize()
+    barrier()
+    launches0 = L.sc_launch_count()
+    with ClockSampler(nvml_index) as clocks:
+        t_wall0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record()
+            work.step()
+            ends[i].record()
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    launches = L.sc_launch_count() - launches0
+    barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_local = sum(step_ms) / len(step_ms)
+    ms = torch.tensor([ms_local], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    value = work.total_macs / (ms * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (k_fir_f32_fast) on this rank
+    p = peaks()
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    sm_max = float(p.get("sm_max_mhz", 1965.0))
+    csum = clocks.summary()
+    fp32_peak = 2 * 128 * sms * sm_max * 1e6 / 1e12  # TFLOP/s at max clock
+    achieved = 2 * work.rank_macs / (ms_local * 1e-3) / 1e12
+    med = csum["sm_mhz"] or sm_max
+    traffic = None
+    tf = REPO / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(args.config)
+    roofline = {
+        "bound": "fp32_fma" if work.dtype == "f32" else "fp64_fma",
+        "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
+        "traffic": traffic,
+        "peak_source": f"computed: {sms} SMs x 128 FP32 FMA/clk x 2 FLOP x sm_max_mhz {sm_max:.0f} "
+                       "(MEASURED_PEAKS.json); no FP32-FMA peak is measured by the driver",
+        "frac_at_observed_clock": achieved / (2 * 128 * sms * med * 1e6 / 1e12),
+        "kernel": "k_fir_f32_fast" if args.config in ("cfg3", "cfg4", "cfg5") else "k_chain",
+        "achieved_from": "CUDA events around each step on the launching stream (step = tap pad + FIR kernel)",
+    }
+
+    # e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e and args.config in ("cfg3", "cfg4", "cfg5"):
+        if args.config == "cfg4":
+            x_pin = torch.from_numpy(work.w.x[work.c0:work.c1]).pin_memory()
+            h_pin = torch.from_numpy(work.w.h[work.c0:work.c1]).pin_memory()
+        else:
+            x_pin = torch.from_numpy(work.x_host).pin_memory()
+            h_pin = torch.from_numpy(work.h_host).pin_memory()
+        work.e2e_step(x_pin, h_pin)
+        torch.cuda.synchronize()
+        barrier()
+        times = []
+        hb = db = 0
+        for _ in range(args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            hb, db = work.e2e_step(x_pin, h_pin)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        t_e2e = torch.tensor([sum(times) / len(times)], device=device, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+        e2e = {"value": work.total_macs / float(t_e2e.item()) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(hb), "d2h_bytes_per_step": int(db),
+               "ms_per_step": 1000 * float(t_e2e.item()),
+               "api": "paper_2401_01607_b200.scatter_convolve(Signal(pinned host tensor))" if world == 1
+               else "paper_2401_01607_b200.distributed_convolve(pinned host, to_host=True)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        rate, sample, dt = cpu_sample(args.config, args.cpu_seconds, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+               "seconds": dt}
+
+    if rank == 0:
+        w = work.w
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": work.scaling, "vs_baseline": None, "dtype": work.dtype,
+            "data": "synthetic (seeded numpy PCG64 recipes of SURVEY.md 8(d); no dataset)",
+            "config": {"workload": w.name, "ne": int(w.ne), "nh": int(w.nh),
+                       "channels": int(w.channels), "metric_macs": int(work.total_macs),
+                       "parallelism": work.parallelism,
+                       "l2": "256 MiB memset before every timed step (outside the events); "
+                             "inputs also exceed L2 at N=1"},
+            "pct_fp32_fma_peak": 100.0 * roofline["frac"],
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": csum,
+            "wall_s_timed_region": t_wall,
+            "step_ms_rank0": step_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

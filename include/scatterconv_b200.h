@@ -1,0 +1,170 @@
+/*
+ * scatterconv_b200.h -- C ABI of the B200 (sm_100a) scatter-convolution library.
+ *
+ * This is the drop-in boundary for the reference package `scatterconv`
+ * (/root/reference/pkg/src/scatterconv).  The reference's only native call is
+ * the numba kernel `_kernels.scatter_block` (_kernels.py:14-52); its Python
+ * entry points (core.py:122-167, engine.py:60-214) are what users call.  Each
+ * entry point below names the reference interface it replaces.  The Python
+ * mirror `paper_2401_01607_b200` binds these with ctypes (INTEGRATION.md shows
+ * the binding a scatterconv maintainer would add).
+ *
+ * Conventions
+ *  - Return 0 on success, a negative SC_ERR_* code otherwise; no C++
+ *    exception crosses this boundary.  sc_last_error() returns a thread-local
+ *    message for the last failure on the calling thread.
+ *  - Unless stated otherwise every sample pointer is a DEVICE pointer (e.g.
+ *    torch.Tensor.data_ptr() of a CUDA tensor) on the current CUDA device, and
+ *    every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream).  Calls documented "synchronous" wait on the stream.
+ *  - dtype: SC_F32 or SC_F64 for every sample array of a call.
+ *  - Engine handles are single-threaded (engine.py:60-66: one engine per
+ *    channel); distinct handles may be used concurrently from different
+ *    threads.  The engine owns copies of every impulse response it is given
+ *    (engine.py:72, :185); callers own inputs and outputs.
+ *
+ * Precision modes
+ *  - SC_MODE_ORDERED: every output is ONE chain over input index m ascending,
+ *    starting at +0.0, each step `acc = acc + x[m]*h[n-m]` with the product and
+ *    the sum rounded separately (no FMA).  This is the reference's order
+ *    (_kernels.py:1-8, core.py:83-86); in float64 it is bit-identical to the
+ *    reference, and stream == batch for any block partition in both dtypes.
+ *  - SC_MODE_FAST (float32 only): register-tiled FFMA2 kernel, fixed
+ *    (deterministic) order, within 1e-5*max|x|*||h||_1 of the reference.
+ *
+ * Skip rules (zero skipping)
+ *  - SC_SKIP_NONE     every input sample scatters (scatter_convolve, core.py:90)
+ *  - SC_SKIP_LE       skip |x| <= threshold; NaN is not skipped (core.py:164)
+ *  - SC_SKIP_NOT_GT   skip unless |x| > threshold; NaN is skipped (_kernels.py:33)
+ */
+#ifndef SCATTERCONV_B200_H
+#define SCATTERCONV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SC_ABI_VERSION 1
+
+#define SC_OK 0
+#define SC_ERR_ARG (-1)    /* invalid argument (sizes, dtype, null pointers) */
+#define SC_ERR_CUDA (-2)   /* CUDA runtime error (message has cudaGetErrorString) */
+#define SC_ERR_ALLOC (-3)  /* device/host allocation failed */
+#define SC_ERR_STATE (-4)  /* engine used in an invalid state */
+
+enum { SC_F32 = 0, SC_F64 = 1 };
+enum { SC_MODE_FAST = 0, SC_MODE_ORDERED = 1 };
+enum { SC_SKIP_NONE = 0, SC_SKIP_LE = 1, SC_SKIP_NOT_GT = 2 };
+
+int sc_abi_version(void);
+const char *sc_last_error(void);
+
+/* Number of CUDA kernels this library has launched in this process (all
+ * threads, all devices).  Benchmarks read it around a timed region to report
+ * how many of the library's kernels ran there. */
+int64_t sc_launch_count(void);
+
+/* ---------------------------------------------------------------- whole signal */
+
+/* Full linear convolution y[0 : ne+nh-1] = x (*) h.
+ * Replaces core._scatter_full (core.py:80-92) and therefore
+ * scatter_convolve (core.py:122-131), commuted_convolve (core.py:134-147:
+ * pass the shorter signal as `x` to drive) and scatter_convolve_skip_zeros
+ * (core.py:150-167, skip_mode = SC_SKIP_LE).  mode SC_MODE_FAST requires
+ * SC_F32 and skip_mode SC_SKIP_NONE. */
+int sc_fir_full(int dtype, int mode, const void *x, int64_t ne, const void *h, int64_t nh,
+                void *y, int skip_mode, double threshold, void *stream);
+
+/* Output-range convolution for time sharding (north_star (4)):
+ * y[i] = sum_k h[k] * X(n_begin + i - k) for i in [0, n_end - n_begin), where
+ * X(m) = x[m - x_begin] for m in [x_begin, x_end) and 0 elsewhere.  A shard
+ * owning outputs [a, b) passes x_begin = max(0, a-nh+1), x_end = min(ne, b):
+ * its input slice plus the (nh-1)-sample halo.  FAST mode, float32. */
+int sc_fir_range(int dtype, const void *x, int64_t x_begin, int64_t x_end, const void *h,
+                 int64_t nh, void *y, int64_t n_begin, int64_t n_end, void *stream);
+
+/* Batched multichannel (replaces one engine per channel, engine.py:60-66,
+ * cli.py:186-202, bench.py:200-202): for c in [0, channels):
+ * y[c*ldy : c*ldy + ne+nh-1] = x[c*ldx : c*ldx+ne] (*) h[c*ldh : c*ldh+nh].
+ * One launch.  FAST mode, float32. */
+int sc_fir_batched(int dtype, const void *x, int64_t ldx, const void *h, int64_t ldh, void *y,
+                   int64_t ldy, int64_t channels, int64_t ne, int64_t nh, void *stream);
+
+/* Gather form with an (almost) exactly rounded accumulator: double-double
+ * (TwoProduct + TwoSum) per output.  Device restatement of direct_form
+ * (core.py:102-119, math.fsum); float64 only. */
+int sc_direct_form(const double *e, int64_t ne, const double *h, int64_t nh, double *y,
+                   void *stream);
+
+/* ---------------------------------------------------------------- literal kernel */
+
+/* Exact drop-in for _kernels.scatter_block (_kernels.py:14-52) on device
+ * arrays: ring[cap] (the reference's physical ring layout, read_index),
+ * ir[nh] (nh <= cap), block[n], out[n].  Mutates ring and out.
+ * Synchronous (it returns the data-dependent `live` through live_out). */
+int sc_scatter_block(int dtype, void *ring, int64_t cap, const void *ir, int64_t nh,
+                     const void *block, int64_t n, void *out, int64_t read_index, int64_t live,
+                     double threshold, int64_t *read_index_out, int64_t *live_out, void *stream);
+
+/* ---------------------------------------------------------------- streaming engine */
+
+/* Device-resident ScatterEngine (engine.py:60-214).  The residue (the
+ * reference's ring in schedule order), the current and pending impulse
+ * responses, read_index, live and cap all live in device memory; no call
+ * below except _flush / _state / _schedule waits on the device. */
+typedef struct sc_engine sc_engine;
+
+/* engine.py:68-81 (+ EngineConfig block_size_nb / zero_skip_threshold).
+ * h is a device pointer; it is copied. */
+int sc_engine_create(int dtype, const void *h, int64_t nh, int64_t block_size_nb,
+                     double threshold, void *stream, sc_engine **out);
+int sc_engine_destroy(sc_engine *e);
+int sc_engine_set_stream(sc_engine *e, void *stream);
+
+/* process_block (engine.py:118-146): applies a pending swap first, then
+ * consumes block[n] (n <= block_size_nb) and writes out[n].  Async. */
+int sc_engine_process_block(sc_engine *e, const void *block, int64_t n, void *out);
+
+/* process_sample (engine.py:99-116): like a 1-sample block but never applies
+ * a pending swap.  Async; out is one device sample. */
+int sc_engine_process_sample(sc_engine *e, const void *x, void *out);
+
+/* swap_ir (engine.py:163-186): effective for the very next sample; residue
+ * keeps its schedule; cap = max(nh_new, live) is computed on device. Async. */
+int sc_engine_swap_ir(sc_engine *e, const void *h, int64_t nh);
+
+/* swap_ir_at_next_block (engine.py:188-192).  Async (h is copied). */
+int sc_engine_swap_ir_at_next_block(sc_engine *e, const void *h, int64_t nh);
+
+/* flush (engine.py:148-161): writes max(nh-1, live) tail samples in emission
+ * order to tail (device, capacity tail_capacity), returns the count in
+ * *n_tail and resets the engine (pending swap survives).  Synchronous. */
+int sc_engine_flush(sc_engine *e, void *tail, int64_t tail_capacity, int64_t *n_tail);
+
+/* State (engine.py:83-97): read_index, live, cap (= len(ring)), consumed,
+ * current nh, has_pending.  Synchronous. */
+int sc_engine_state(sc_engine *e, int64_t *read_index, int64_t *live, int64_t *cap,
+                    int64_t *consumed, int64_t *nh, int *has_pending);
+
+/* Residue in schedule order (_schedule_order, engine.py:211-214): copies
+ * min(n, cap) samples to dst (device).  Synchronous. */
+int sc_engine_schedule(sc_engine *e, void *dst, int64_t n, int64_t *n_written);
+
+/* Current impulse response (engine.py:91-93) copied to dst (device, nh). Async. */
+int sc_engine_current_ir(sc_engine *e, void *dst, int64_t capacity, int64_t *nh);
+
+/* Back-to-back blocks with no host synchronisation (render, engine.py:194-209,
+ * plus an IR swap schedule): x[n_total] is cut into blocks of nb; before block
+ * b = swap_blocks[i] the engine performs swap_ir(swap_irs[i], swap_nh[i]).
+ * Bit-identical to the equivalent sequence of process_block/swap_ir calls. */
+int sc_engine_process_blocks(sc_engine *e, const void *x, int64_t n_total, int64_t nb,
+                             const int64_t *swap_blocks, const void *const *swap_irs,
+                             const int64_t *swap_nh, int64_t n_swaps, void *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SCATTERCONV_B200_H */

@@ -67,6 +67,9 @@ def lib():
     L.oracle_conv_parallel.restype = ctypes.c_int
     L.oracle_conv_channels.argtypes = [_dp, _dp, _dp, _i64, _i64, _i64, _i64, ctypes.c_int]
     L.oracle_conv_channels.restype = ctypes.c_int
+    L.oracle_scatter_window.argtypes = [_dp, _i64, _dp, _i64, _dp, _i64, _i64, ctypes.c_int,
+                                        ctypes.c_double, ctypes.c_int]
+    L.oracle_scatter_window.restype = None
     _LIB = L
     return L
 
@@ -104,6 +107,18 @@ def scatter_full(drive, kern, skip_mode=SKIP_NONE, threshold=0.0) -> np.ndarray:
     k = _f64(kern)
     out = np.empty(len(d) + len(k) - 1)
     lib().oracle_scatter_full(_p(d), len(d), _p(k), len(k), _p(out), int(skip_mode), float(threshold))
+    return out
+
+
+def scatter_window(x, h, n_begin, n_end, skip_mode=SKIP_NONE, threshold=0.0, threads=None):
+    """Outputs [n_begin, n_end) of core._scatter_full(x, h) -- bit-identical to
+    those slots of the full reference result (same per-slot chain)."""
+    x = _f64(x)
+    h = _f64(h)
+    out = np.empty(max(0, n_end - n_begin))
+    threads = threads or len(os.sched_getaffinity(0))
+    lib().oracle_scatter_window(_p(x), len(x), _p(h), len(h), _p(out), int(n_begin), int(n_end),
+                                int(skip_mode), float(threshold), int(threads))
     return out
 
 

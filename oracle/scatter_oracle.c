@@ -340,3 +340,76 @@ int oracle_conv_channels(const double *x, const double *h, double *y, int64_t ch
     pthread_mutex_destroy(&p.mu);
     return 0;
 }
+
+/* ------------------------------------------------------------------------
+ * Output window of _scatter_full -- core.py:80-92 restricted to outputs
+ * [n_begin, n_end): for each drive sample m in ascending order add x*kern
+ * into the window slots it reaches.  Every slot sees exactly the reference's
+ * chain (ascending m, mul then add), so the window is bit-identical to the
+ * same slots of the full reference result.  Threads split the WINDOW (never a
+ * slot's chain).  skip_mode as in oracle_scatter_full.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    const double *x;
+    int64_t ne;
+    const double *h;
+    int64_t nh;
+    double *out;
+    int64_t n_begin, n_end;
+    int skip_mode;
+    double threshold;
+} win_job;
+
+static void run_window(const win_job *w)
+{
+    for (int64_t n = w->n_begin; n < w->n_end; ++n) w->out[n - w->n_begin] = 0.0;
+    int64_t m_lo = w->n_begin - w->nh + 1;
+    if (m_lo < 0) m_lo = 0;
+    int64_t m_hi = w->n_end - 1;
+    if (m_hi > w->ne - 1) m_hi = w->ne - 1;
+    for (int64_t m = m_lo; m <= m_hi; ++m) {
+        const double x = w->x[m];
+        if (w->skip_mode == 1 && fabs(x) <= w->threshold) continue;
+        if (w->skip_mode == 2 && !(fabs(x) > w->threshold)) continue;
+        int64_t a = m > w->n_begin ? m : w->n_begin;           /* slots n in [a, b) */
+        int64_t b = m + w->nh < w->n_end ? m + w->nh : w->n_end;
+        double *dst = w->out - w->n_begin;
+        const double *hk = w->h - m;
+        for (int64_t n = a; n < b; ++n) {
+            const double p = x * hk[n];
+            dst[n] = dst[n] + p;
+        }
+    }
+}
+
+static void *win_thread(void *arg)
+{
+    run_window((const win_job *)arg);
+    return NULL;
+}
+
+void oracle_scatter_window(const double *x, int64_t ne, const double *h, int64_t nh, double *out,
+                           int64_t n_begin, int64_t n_end, int skip_mode, double threshold,
+                           int n_threads)
+{
+    const int64_t len = n_end - n_begin;
+    if (len <= 0) return;
+    if (n_threads < 1) n_threads = 1;
+    if (n_threads > len) n_threads = (int)len;
+    win_job *jobs = (win_job *)calloc((size_t)n_threads, sizeof(win_job));
+    pthread_t *th = (pthread_t *)calloc((size_t)n_threads, sizeof(pthread_t));
+    const int64_t per = (len + n_threads - 1) / n_threads;
+    int used = 0;
+    for (int t = 0; t < n_threads; ++t) {
+        const int64_t a = n_begin + (int64_t)t * per;
+        if (a >= n_end) break;
+        const int64_t b = a + per < n_end ? a + per : n_end;
+        jobs[t] = (win_job){x, ne, h, nh, out + (a - n_begin), a, b, skip_mode, threshold};
+        used++;
+    }
+    for (int t = 1; t < used; ++t) pthread_create(&th[t], NULL, win_thread, &jobs[t]);
+    run_window(&jobs[0]);
+    for (int t = 1; t < used; ++t) pthread_join(th[t], NULL);
+    free(jobs);
+    free(th);
+}

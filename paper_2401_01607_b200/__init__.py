@@ -1,1 +1,85 @@
-"""placeholder"""
+"""B200-native (sm_100a) scatter / taches convolution -- drop-in for the hot
+path of the reference package ``scatterconv`` (arXiv 2401.01607).
+
+Same entry points as pkg/src/scatterconv/__init__.py for the convolution
+path:
+
+  scatter_convolve / commuted_convolve / scatter_convolve_skip_zeros /
+  direct_form                       whole-signal convolution (core)
+  ScatterEngine / EngineConfig      block streaming engine with IR hot swap
+  Signal / ConvOutput               sample containers
+
+plus the B200 additions of the north_star: ``convolve_batched``
+(multichannel in one launch) and ``convolve_sharded`` /
+``distributed_convolve`` (output-time sharding across GPUs).
+
+Everything computes in the CUDA library built in-tree under ``_lib`` and
+called through its C ABI (include/scatterconv_b200.h).  There is no CPU
+fallback: without the library or a CUDA device every compute call raises.
+The reference's file I/O, CLI, fixed-point model and timing sweeps are out
+of scope.
+"""
+
+from . import configs
+from .core import (
+    ConvOutput,
+    Signal,
+    commuted_convolve,
+    direct_form,
+    scatter_convolve,
+    scatter_convolve_skip_zeros,
+)
+from .engine import DEFAULT_BLOCK_SIZE, TAIL_POLICIES, EngineConfig, ScatterEngine
+from .multichannel import convolve_batched
+from .sharded import (
+    Shard,
+    convolve_shard,
+    convolve_sharded,
+    distributed_convolve,
+    gather_shards,
+    shard_plan,
+)
+
+__version__ = "0.1.0"
+
+
+def ms_to_samples(ms: float, sample_rate: int) -> int:
+    """Duration in milliseconds to a sample count (bench.py:36-40)."""
+    if ms <= 0:
+        raise ValueError(f"duration must be positive, got {ms} ms")
+    return int(round(ms * sample_rate / 1000.0))
+
+
+def gen_white_noise(duration: int, sample_rate: int = 44100, seed=0) -> Signal:
+    """Uniform white noise in [-1, 1), reproducible per seed (bench.py:43-52)."""
+    import numpy as np
+
+    if not isinstance(duration, (int, np.integer)) or duration < 1:
+        raise ValueError(f"duration must be a positive sample count, got {duration!r}")
+    rng = np.random.default_rng(seed)
+    return Signal(rng.uniform(-1.0, 1.0, duration), sample_rate)
+
+
+__all__ = [
+    "ConvOutput",
+    "DEFAULT_BLOCK_SIZE",
+    "EngineConfig",
+    "ScatterEngine",
+    "Shard",
+    "Signal",
+    "TAIL_POLICIES",
+    "commuted_convolve",
+    "configs",
+    "convolve_batched",
+    "convolve_shard",
+    "convolve_sharded",
+    "direct_form",
+    "distributed_convolve",
+    "gather_shards",
+    "gen_white_noise",
+    "ms_to_samples",
+    "scatter_convolve",
+    "scatter_convolve_skip_zeros",
+    "shard_plan",
+    "__version__",
+]

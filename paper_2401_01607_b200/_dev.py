@@ -1,0 +1,59 @@
+"""Host/device tensor plumbing (PyTorch is only the allocator and the handoff)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def torch():
+    import torch as _t
+
+    return _t
+
+
+def is_tensor(a) -> bool:
+    try:
+        import torch as _t
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(a, _t.Tensor)
+
+
+def np_dtype(a):
+    """numpy dtype (float32/float64) of an ndarray or tensor."""
+    if is_tensor(a):
+        t = torch()
+        return np.float32 if a.dtype == t.float32 else np.float64
+    return np.float32 if a.dtype == np.float32 else np.float64
+
+
+def torch_dtype(npd):
+    t = torch()
+    return t.float32 if npd == np.float32 else t.float64
+
+
+def as_device(a, npd, device=None):
+    """Contiguous CUDA tensor of dtype npd holding a (ndarray or tensor)."""
+    t = torch()
+    dev = device if device is not None else t.device("cuda", t.cuda.current_device())
+    td = torch_dtype(npd)
+    if is_tensor(a):
+        return a.to(device=dev, dtype=td, non_blocking=a.device.type == "cpu" and a.is_pinned()).contiguous()
+    arr = np.ascontiguousarray(a, dtype=npd)
+    return t.from_numpy(arr).to(device=dev)
+
+
+def like_input(result, *inputs):
+    """Return result (a CUDA tensor) in the caller's currency: a CUDA tensor if
+    any input was one, a CPU tensor if any input was a tensor, else an ndarray."""
+    if any(is_tensor(a) and a.is_cuda for a in inputs):
+        return result
+    if any(is_tensor(a) for a in inputs):
+        if any(is_tensor(a) and a.is_pinned() for a in inputs):
+            # pinned in -> pinned out: one DMA at full PCIe/C2C rate
+            out = torch().empty(result.shape, dtype=result.dtype, pin_memory=True)
+            out.copy_(result, non_blocking=True)
+            torch().cuda.current_stream(result.device).synchronize()
+            return out
+        return result.cpu()
+    return result.cpu().numpy()

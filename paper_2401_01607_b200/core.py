@@ -1,0 +1,193 @@
+"""Whole-signal scatter convolution -- drop-in for ``scatterconv.core``.
+
+Mirrors pkg/src/scatterconv/core.py (Signal, ConvOutput, direct_form,
+scatter_convolve, commuted_convolve, scatter_convolve_skip_zeros) with the
+same names, argument meaning, validation messages and return types.  The
+arithmetic runs in the CUDA library (csrc/), never on the host:
+
+* float64 signals (the reference's only type, core.py:38) use the ORDERED
+  kernel: each output is a single chain over input index ascending with
+  separately rounded multiply and add -- bit-identical to the reference.
+* float32 signals (arrays or tensors; ``Signal`` keeps float32 instead of
+  upcasting) use the FAST register-tiled FFMA2 kernel, within
+  1e-5*max|x|*||h||_1 of the reference; ``mode="ordered"`` selects the
+  ordered chain in float32.
+
+Samples may be numpy arrays (results come back as arrays) or torch tensors
+(CUDA tensors stay on the device; no host synchronisation).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _dev
+from . import _native as N
+
+
+@dataclass(eq=False)
+class Signal:
+    """A finite run of samples at a fixed sample rate (core.py:25-49).
+
+    ``samples`` becomes a 1-D float64 array like the reference, except that
+    float32 arrays and float32/float64 torch tensors keep their dtype (and
+    CUDA tensors their device) so the FP32 path and device residency are
+    reachable through the same type.
+    """
+
+    samples: object
+    sample_rate: int = 44100
+
+    def __post_init__(self):
+        if _dev.is_tensor(self.samples):
+            t = _dev.torch()
+            if self.samples.dtype not in (t.float32, t.float64):
+                self.samples = self.samples.to(t.float64)
+        else:
+            arr = np.asarray(self.samples)
+            if arr.dtype != np.float32:
+                arr = np.asarray(self.samples, dtype=np.float64)
+            self.samples = arr
+        if self.samples.ndim != 1:
+            raise ValueError(f"samples must be 1-D, got shape {tuple(self.samples.shape)}")
+        if not isinstance(self.sample_rate, (int, np.integer)) or self.sample_rate <= 0:
+            raise ValueError(f"sample_rate must be a positive integer, got {self.sample_rate!r}")
+
+    def __len__(self):
+        return int(self.samples.shape[0])
+
+    @property
+    def duration_s(self) -> float:
+        return len(self) / self.sample_rate
+
+    @property
+    def dtype(self):
+        return _dev.np_dtype(self.samples)
+
+
+@dataclass(eq=False)
+class ConvOutput:
+    """Body (aligned with the input) and tail (len(h)-1 samples), core.py:52-66."""
+
+    body: Signal
+    tail: Signal
+
+    def concatenated(self) -> Signal:
+        a, b = self.body.samples, self.tail.samples
+        if _dev.is_tensor(a):
+            joined = _dev.torch().cat([a, b.to(a.device)])
+        else:
+            joined = np.concatenate([a, b])
+        return Signal(joined, self.body.sample_rate)
+
+
+def _check_pair(e: Signal, h: Signal):
+    """core.py:69-77 (same messages)."""
+    if len(e) == 0:
+        raise ValueError("input signal is empty")
+    if len(h) == 0:
+        raise ValueError("impulse response is empty")
+    if e.sample_rate != h.sample_rate:
+        raise ValueError(
+            f"sample rates differ: input {e.sample_rate} Hz vs impulse response {h.sample_rate} Hz"
+        )
+
+
+def _result_dtype(*arrays):
+    return np.float64 if any(_dev.np_dtype(a) == np.float64 for a in arrays) else np.float32
+
+
+_MODES = {None: None, "fast": N.SC_MODE_FAST, "ordered": N.SC_MODE_ORDERED,
+          "strict": N.SC_MODE_ORDERED}
+
+
+def _fir(drive, kern, *, mode=None, skip_mode=N.SC_SKIP_NONE, threshold=0.0):
+    """Full convolution of two 1-D sample arrays on the device (core._scatter_full
+    semantics: slot n accumulates drive samples in increasing index)."""
+    if mode not in _MODES:
+        raise ValueError(f"mode must be one of {sorted(k for k in _MODES if k)}, got {mode!r}")
+    npd = _result_dtype(drive, kern)
+    m = _MODES[mode]
+    if m is None:
+        m = N.SC_MODE_FAST if npd == np.float32 else N.SC_MODE_ORDERED
+    L = N.lib()
+    t = _dev.torch()
+    x = _dev.as_device(drive, npd)
+    h = _dev.as_device(kern, npd, device=x.device)
+    nout = x.shape[0] + h.shape[0] - 1
+    with t.cuda.device(x.device):
+        y = t.empty(nout, dtype=x.dtype, device=x.device)
+        N.check(L.sc_fir_full(N.dtype_code(npd), m, N.ptr(x), x.shape[0], N.ptr(h), h.shape[0],
+                              N.ptr(y), skip_mode, float(threshold), N.stream_ptr()))
+    return _dev.like_input(y, drive, kern)
+
+
+def _scatter_full(drive, kern, mode=None):
+    """Scatter `drive` through `kern` into a fresh linear buffer (core.py:80-92).
+
+    Each drive sample adds its scaled copy of `kern` in increasing tap order,
+    so every output slot accumulates contributions in increasing drive-index
+    order -- the ordered kernel reproduces exactly that chain.
+    """
+    return _fir(drive, kern, mode=mode)
+
+
+def _split(full, n_body: int, sample_rate: int) -> ConvOutput:
+    """core.py:95-99.  The reference copies the two slices out of its scratch
+    buffer; `full` here is always a fresh buffer owned by this result, so the
+    body and tail are views of it (no extra host/device copy)."""
+    return ConvOutput(body=Signal(full[:n_body], sample_rate),
+                      tail=Signal(full[n_body:], sample_rate))
+
+
+def direct_form(e: Signal, h: Signal) -> Signal:
+    """Gather-form convolution (core.py:102-119).
+
+    The reference sums each output's products with math.fsum.  On the device
+    each output's individually rounded products are summed with a
+    compensated (double-double) accumulator, float64 always.
+    """
+    _check_pair(e, h)
+    L = N.lib()
+    t = _dev.torch()
+    x = _dev.as_device(e.samples, np.float64)
+    k = _dev.as_device(h.samples, np.float64, device=x.device)
+    with t.cuda.device(x.device):
+        y = t.empty(len(e) + len(h) - 1, dtype=t.float64, device=x.device)
+        N.check(L.sc_direct_form(N.ptr(x), len(e), N.ptr(k), len(h), N.ptr(y), N.stream_ptr()))
+    return Signal(_dev.like_input(y, e.samples, h.samples), e.sample_rate)
+
+
+def scatter_convolve(e: Signal, h: Signal, *, mode=None) -> ConvOutput:
+    """Convolve by scattering one scaled, delayed copy of h per input sample
+    (core.py:122-131).  ``mode``: None (float64 -> ordered, float32 -> fast),
+    "fast" or "ordered"/"strict"."""
+    _check_pair(e, h)
+    full = _scatter_full(e.samples, h.samples, mode=mode) if mode else _scatter_full(e.samples, h.samples)
+    return _split(full, len(e), e.sample_rate)
+
+
+def commuted_convolve(e: Signal, h: Signal) -> ConvOutput:
+    """Scatter with the shorter signal driving the loop (core.py:134-147).
+
+    The body/tail split still follows the original argument roles.
+    """
+    _check_pair(e, h)
+    if len(h) <= len(e):
+        full = _scatter_full(h.samples, e.samples)
+    else:
+        full = _scatter_full(e.samples, h.samples)
+    return _split(full, len(e), e.sample_rate)
+
+
+def scatter_convolve_skip_zeros(e: Signal, h: Signal, threshold: float = 0.0) -> ConvOutput:
+    """Scatter convolution skipping input samples with |value| <= threshold
+    (core.py:150-167).  NaN inputs are not skipped (they propagate)."""
+    if threshold < 0:
+        raise ValueError(f"threshold must be non-negative, got {threshold}")
+    _check_pair(e, h)
+    full = _fir(e.samples, h.samples, mode="ordered", skip_mode=N.SC_SKIP_LE,
+                threshold=threshold)
+    return _split(full, len(e), e.sample_rate)

@@ -1,0 +1,145 @@
+// capi.cu -- C ABI entry points for the whole-signal paths + shared runtime.
+//
+// Each sc_* function validates its arguments, picks the kernel for the
+// requested dtype/mode and launches on the caller's stream.  See
+// include/scatterconv_b200.h for the contract and the reference interface
+// each entry point replaces.
+
+#include <atomic>
+#include <cstdarg>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "sc_common.cuh"
+
+namespace sc {
+
+static thread_local char g_err[512] = "";
+static std::atomic<int64_t> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int sm_count() {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int n = 148;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
+    cache[dev] = n;
+    return n;
+}
+
+void *scratch(size_t bytes, int slot, cudaStream_t stream, int *err) {
+    // Grow-only buffers keyed by (device, stream, slot): concurrent streams
+    // (or host threads driving different devices) never share a buffer.
+    struct Buf {
+        void *p = nullptr;
+        size_t n = 0;
+    };
+    static std::mutex mu;
+    static std::map<std::tuple<int, uintptr_t, int>, Buf> bufs;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    Buf &b = bufs[std::make_tuple(dev, reinterpret_cast<uintptr_t>(stream), slot)];
+    if (b.n < bytes) {
+        if (b.p) {
+            // kernels queued on this stream may still read the old buffer
+            cudaStreamSynchronize(stream);
+            cudaFree(b.p);
+            b.p = nullptr;
+            b.n = 0;
+        }
+        size_t want = bytes + bytes / 4 + 256;
+        if (cudaMalloc(&b.p, want) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("scratch: cudaMalloc(%zu) failed", want);
+            *err = SC_ERR_ALLOC;
+            return nullptr;
+        }
+        b.n = want;
+    }
+    *err = 0;
+    return b.p;
+}
+
+static size_t dtype_size(int dtype) { return dtype == SC_F64 ? 8 : (dtype == SC_F32 ? 4 : 0); }
+
+}  // namespace sc
+
+using namespace sc;
+
+extern "C" {
+
+int sc_abi_version(void) { return SC_ABI_VERSION; }
+
+int64_t sc_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char *sc_last_error(void) { return g_err; }
+
+int sc_fir_full(int dtype, int mode, const void *x, int64_t ne, const void *h, int64_t nh,
+                void *y, int skip_mode, double threshold, void *stream) {
+    SC_REQUIRE(dtype_size(dtype) != 0, "sc_fir_full: bad dtype %d", dtype);
+    SC_REQUIRE(ne >= 1, "sc_fir_full: input signal is empty");
+    SC_REQUIRE(nh >= 1, "sc_fir_full: impulse response is empty");
+    SC_REQUIRE(x && h && y, "sc_fir_full: null pointer");
+    SC_REQUIRE(skip_mode >= SC_SKIP_NONE && skip_mode <= SC_SKIP_NOT_GT, "sc_fir_full: bad skip_mode");
+    SC_REQUIRE(threshold >= 0.0, "sc_fir_full: threshold must be non-negative, got %g", threshold);
+    const int64_t nout = ne + nh - 1;
+    cudaStream_t st = as_stream(stream);
+    if (mode == SC_MODE_FAST && dtype == SC_F32 && skip_mode == SC_SKIP_NONE) {
+        return launch_fir_f32_fast(static_cast<const float *>(x), 0, 0, 0, ne,
+                                   static_cast<const float *>(h), 0, nh, static_cast<float *>(y), 0,
+                                   0, nout, 1, st);
+    }
+    ChainSeg seg{h, nh, 0, ne};
+    return launch_chain(dtype, skip_mode, threshold, x, 0, &seg, 1, nullptr, 0, nullptr, 0, nout,
+                        y, nout, nullptr, st);
+}
+
+int sc_fir_range(int dtype, const void *x, int64_t x_begin, int64_t x_end, const void *h,
+                 int64_t nh, void *y, int64_t n_begin, int64_t n_end, void *stream) {
+    SC_REQUIRE(dtype == SC_F32, "sc_fir_range: only float32 (fast mode) is supported");
+    SC_REQUIRE(nh >= 1, "sc_fir_range: impulse response is empty");
+    SC_REQUIRE(x_end >= x_begin && n_end >= n_begin, "sc_fir_range: bad range");
+    SC_REQUIRE(h && y && (x || x_end == x_begin), "sc_fir_range: null pointer");
+    return launch_fir_f32_fast(static_cast<const float *>(x), 0, x_begin, x_begin, x_end,
+                               static_cast<const float *>(h), 0, nh, static_cast<float *>(y), 0,
+                               n_begin, n_end, 1, as_stream(stream));
+}
+
+int sc_fir_batched(int dtype, const void *x, int64_t ldx, const void *h, int64_t ldh, void *y,
+                   int64_t ldy, int64_t channels, int64_t ne, int64_t nh, void *stream) {
+    SC_REQUIRE(dtype == SC_F32, "sc_fir_batched: only float32 (fast mode) is supported");
+    SC_REQUIRE(ne >= 1, "sc_fir_batched: input signal is empty");
+    SC_REQUIRE(nh >= 1, "sc_fir_batched: impulse response is empty");
+    SC_REQUIRE(channels >= 1, "sc_fir_batched: channels must be >= 1");
+    SC_REQUIRE(ldx >= ne && ldh >= nh && ldy >= ne + nh - 1, "sc_fir_batched: bad leading dims");
+    SC_REQUIRE(x && h && y, "sc_fir_batched: null pointer");
+    return launch_fir_f32_fast(static_cast<const float *>(x), ldx, 0, 0, ne,
+                               static_cast<const float *>(h), ldh, nh, static_cast<float *>(y), ldy,
+                               0, ne + nh - 1, channels, as_stream(stream));
+}
+
+int sc_direct_form(const double *e, int64_t ne, const double *h, int64_t nh, double *y,
+                   void *stream) {
+    SC_REQUIRE(ne >= 1, "sc_direct_form: input signal is empty");
+    SC_REQUIRE(nh >= 1, "sc_direct_form: impulse response is empty");
+    SC_REQUIRE(e && h && y, "sc_direct_form: null pointer");
+    return launch_direct_form_dd(e, ne, h, nh, y, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,472 @@
+// engine.cu -- device-resident streaming engine (ScatterEngine,
+// pkg/src/scatterconv/engine.py:60-214) and the literal scatter_block
+// drop-in (_kernels.py:14-52).
+//
+// Residue layout.  The reference keeps a circular ring of cap slots and a
+// read index (engine.py:75-79).  On the device we keep the same residue in
+// SCHEDULE ORDER (index 0 = next slot to emit, engine.py:211-214) in two
+// ping-pong buffers.  A block of n samples is one ordered gather launch:
+//   for slot t in [0, n + cap):  acc = res_in[t] (if t < cap) + sum over
+//   block samples m ascending of x[m]*h[t-m];  t < n -> out[t], else
+//   res_out[t-n]
+// which continues each slot's chain exactly where the reference's per-sample
+// loop would (_kernels.py:31-51), and avoids the ring's slot aliasing
+// (slots t and t+cap of one block) that would be a race in parallel.
+//
+// State that the reference updates data-dependently -- `live` (engine.py
+// :78-79 / _kernels.py:43-51), and through it `cap` on a swap
+// (engine.py:179) and `read_index` -- lives in device memory and is updated
+// by a one-CTA epilogue kernel, so process_block, swap_ir and the deferred
+// swap never wait on the host.  The host keeps only an upper bound of cap
+// (to size launches and buffers) and the sample counter.
+
+#include <cstring>
+#include <new>
+
+#include "sc_common.cuh"
+
+namespace sc {
+namespace {
+
+enum { ST_LIVE = 0, ST_CAP = 1, ST_RI = 2, ST_N = 4 };
+
+// live/read_index after a block (see the derivation in DESIGN.md): with
+// J = last index whose sample scatters (-1 if none),
+//   live' = max(0, live - n, J >= 0 ? nh - n + J : 0);  ri' = (ri + n) % cap.
+template <typename T, int SKIP>
+__global__ void k_block_epilogue(const T *__restrict__ x, int64_t n, double thr, int64_t nh,
+                                 int64_t *__restrict__ st) {
+    __shared__ long long sj[32];
+    long long J = -1;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        if (!skipped<SKIP>(x[i], thr)) J = i > J ? i : J;
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long v = __shfl_xor_sync(0xffffffffu, J, o);
+        J = v > J ? v : J;
+    }
+    if ((threadIdx.x & 31) == 0) sj[threadIdx.x >> 5] = J;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) J = sj[w] > J ? sj[w] : J;
+        int64_t live = st[ST_LIVE] - n;
+        if (live < 0) live = 0;
+        if (J >= 0 && nh - n + J > live) live = nh - n + J;
+        st[ST_LIVE] = live;
+        st[ST_RI] = (st[ST_RI] + n) % st[ST_CAP];
+    }
+}
+
+__global__ void k_swap_state(int64_t *st, int64_t nh_new) {
+    const int64_t live = st[ST_LIVE];
+    st[ST_CAP] = nh_new > live ? nh_new : live;  // engine.py:179
+    st[ST_RI] = 0;                               // engine.py:184
+}
+
+__global__ void k_reset_state(int64_t *st, int64_t nh) {
+    st[ST_LIVE] = 0;
+    st[ST_CAP] = nh;
+    st[ST_RI] = 0;
+}
+
+template <typename T>
+__global__ void k_ring_to_sched(const T *__restrict__ ring, int64_t cap, int64_t ri,
+                                T *__restrict__ sched) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < cap) sched[i] = ring[(ri + i) % cap];
+}
+
+template <typename T>
+__global__ void k_sched_to_ring(const T *__restrict__ sched, int64_t cap, int64_t ri,
+                                T *__restrict__ ring) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < cap) ring[(ri + i) % cap] = sched[i];
+}
+
+size_t esize(int dtype) { return dtype == SC_F64 ? 8 : 4; }
+
+int launch_epilogue(int dtype, const void *x, int64_t n, double thr, int64_t nh, int64_t *st,
+                    cudaStream_t s) {
+    if (dtype == SC_F64)
+        k_block_epilogue<double, SC_SKIP_NOT_GT><<<1, 1024, 0, s>>>(static_cast<const double *>(x),
+                                                                    n, thr, nh, st);
+    else
+        k_block_epilogue<float, SC_SKIP_NOT_GT><<<1, 1024, 0, s>>>(static_cast<const float *>(x), n,
+                                                                   thr, nh, st);
+    SC_CHECK_LAUNCH();
+    return SC_OK;
+}
+
+}  // namespace
+}  // namespace sc
+
+using namespace sc;
+
+struct sc_engine {
+    int dtype = SC_F32;
+    size_t es = 4;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t nb = 8192;
+    double thr = 0.0;
+    // current impulse response (engine-owned copy)
+    void *ir = nullptr;
+    int64_t nh = 0, ir_capacity = 0;
+    // pending impulse response (swap_ir_at_next_block)
+    void *pend = nullptr;
+    int64_t pend_nh = 0, pend_capacity = 0;
+    bool has_pending = false;
+    // residue in schedule order, ping-pong; buffers hold res_capacity samples
+    void *res[2] = {nullptr, nullptr};
+    int cur = 0;
+    int64_t res_capacity = 0;
+    int64_t cap_ub = 0;  // host upper bound of the device-side logical cap
+    int64_t *st = nullptr;  // device: live, cap, read_index
+    int64_t consumed = 0;
+};
+
+namespace {
+
+int ensure_buffer(void **p, int64_t *capacity, int64_t want, size_t es, bool keep, int64_t keep_n,
+                  cudaStream_t s) {
+    if (*capacity >= want) return SC_OK;
+    void *np = nullptr;
+    if (cudaMalloc(&np, (size_t)want * es) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("engine: cudaMalloc(%lld samples) failed", (long long)want);
+        return SC_ERR_ALLOC;
+    }
+    SC_CHECK_CUDA(cudaMemsetAsync(np, 0, (size_t)want * es, s));
+    if (*p) {
+        if (keep && keep_n > 0)
+            SC_CHECK_CUDA(cudaMemcpyAsync(np, *p, (size_t)keep_n * es, cudaMemcpyDeviceToDevice, s));
+        SC_CHECK_CUDA(cudaStreamSynchronize(s));  // old buffer may still be read
+        cudaFree(*p);
+    }
+    *p = np;
+    *capacity = want;
+    return SC_OK;
+}
+
+int grow_residue(sc_engine *e, int64_t want) {
+    if (e->res_capacity >= want) return SC_OK;
+    int64_t cap0 = e->res_capacity, cap1 = e->res_capacity;
+    int rc = ensure_buffer(&e->res[e->cur], &cap0, want, e->es, true, e->cap_ub, e->stream);
+    if (rc) return rc;
+    rc = ensure_buffer(&e->res[1 - e->cur], &cap1, want, e->es, false, 0, e->stream);
+    if (rc) return rc;
+    e->res_capacity = want;
+    return SC_OK;
+}
+
+// swap_ir core (engine.py:163-186) with h already in device memory.
+int do_swap(sc_engine *e, const void *h, int64_t nh) {
+    int rc = ensure_buffer(&e->ir, &e->ir_capacity, nh, e->es, false, 0, e->stream);
+    if (rc) return rc;
+    if (h != e->ir)
+        SC_CHECK_CUDA(cudaMemcpyAsync(e->ir, h, (size_t)nh * e->es, cudaMemcpyDeviceToDevice, e->stream));
+    // new cap = max(nh, live) <= max(nh, cap_ub): grow buffers on the host bound only
+    const int64_t ub = nh > e->cap_ub ? nh : e->cap_ub;
+    rc = grow_residue(e, ub);
+    if (rc) return rc;
+    e->cap_ub = ub;
+    e->nh = nh;
+    k_swap_state<<<1, 1, 0, e->stream>>>(e->st, nh);
+    SC_CHECK_LAUNCH();
+    return SC_OK;
+}
+
+int do_block(sc_engine *e, const void *block, int64_t n, void *out, bool apply_pending) {
+    if (apply_pending && e->has_pending) {
+        e->has_pending = false;
+        int rc = do_swap(e, e->pend, e->pend_nh);
+        if (rc) return rc;
+    }
+    SC_REQUIRE(n <= e->nb, "block of %lld samples exceeds block_size_nb=%lld", (long long)n,
+               (long long)e->nb);
+    if (n == 0) return SC_OK;
+    ChainSeg seg{e->ir, e->nh, 0, n};
+    void *rin = e->res[e->cur], *rout = e->res[1 - e->cur];
+    int rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, block, 0, &seg, 1, rin, 0,
+                          e->st + ST_CAP, 0, n + e->cap_ub, out, n, rout, e->stream);
+    if (rc) return rc;
+    rc = launch_epilogue(e->dtype, block, n, e->thr, e->nh, e->st, e->stream);
+    if (rc) return rc;
+    e->cur = 1 - e->cur;
+    e->consumed += n;
+    return SC_OK;
+}
+
+int read_state(sc_engine *e, int64_t host[ST_N]) {
+    SC_CHECK_CUDA(cudaMemcpyAsync(host, e->st, sizeof(int64_t) * ST_N, cudaMemcpyDeviceToHost, e->stream));
+    SC_CHECK_CUDA(cudaStreamSynchronize(e->stream));
+    return SC_OK;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int now = -1;
+        cudaGetDevice(&now);
+        if (prev >= 0 && now != prev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+int sc_engine_create(int dtype, const void *h, int64_t nh, int64_t block_size_nb,
+                     double threshold, void *stream, sc_engine **out) {
+    SC_REQUIRE(dtype == SC_F32 || dtype == SC_F64, "sc_engine_create: bad dtype %d", dtype);
+    SC_REQUIRE(nh >= 1, "impulse response is empty");
+    SC_REQUIRE(block_size_nb >= 1, "block_size_nb must be >= 1, got %lld", (long long)block_size_nb);
+    SC_REQUIRE(threshold >= 0.0, "zero_skip_threshold must be >= 0, got %g", threshold);
+    SC_REQUIRE(h && out, "sc_engine_create: null pointer");
+    sc_engine *e = new (std::nothrow) sc_engine();
+    if (!e) {
+        set_error("sc_engine_create: out of host memory");
+        return SC_ERR_ALLOC;
+    }
+    e->dtype = dtype;
+    e->es = esize(dtype);
+    cudaGetDevice(&e->device);
+    e->stream = as_stream(stream);
+    e->nb = block_size_nb;
+    e->thr = threshold;
+    int rc = SC_OK;
+    if (cudaMalloc(&e->st, sizeof(int64_t) * ST_N) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("sc_engine_create: cudaMalloc failed");
+        rc = SC_ERR_ALLOC;
+    }
+    if (!rc) rc = ensure_buffer(&e->ir, &e->ir_capacity, nh, e->es, false, 0, e->stream);
+    if (!rc) rc = grow_residue(e, nh);
+    if (!rc && cudaMemcpyAsync(e->ir, h, (size_t)nh * e->es, cudaMemcpyDeviceToDevice, e->stream) != cudaSuccess) {
+        set_error("sc_engine_create: copy of impulse response failed");
+        rc = SC_ERR_CUDA;
+    }
+    if (!rc) {
+        e->nh = nh;
+        e->cap_ub = nh;
+        k_reset_state<<<1, 1, 0, e->stream>>>(e->st, nh);
+        if (cudaGetLastError() != cudaSuccess) rc = SC_ERR_CUDA;
+    }
+    if (rc) {
+        sc_engine_destroy(e);
+        return rc;
+    }
+    *out = e;
+    return SC_OK;
+}
+
+int sc_engine_destroy(sc_engine *e) {
+    if (!e) return SC_OK;
+    DeviceGuard g(e->device);
+    if (e->stream) cudaStreamSynchronize(e->stream);
+    cudaFree(e->ir);
+    cudaFree(e->pend);
+    cudaFree(e->res[0]);
+    cudaFree(e->res[1]);
+    cudaFree(e->st);
+    delete e;
+    return SC_OK;
+}
+
+int sc_engine_set_stream(sc_engine *e, void *stream) {
+    SC_REQUIRE(e, "null engine");
+    e->stream = as_stream(stream);
+    return SC_OK;
+}
+
+int sc_engine_process_block(sc_engine *e, const void *block, int64_t n, void *out) {
+    SC_REQUIRE(e, "null engine");
+    SC_REQUIRE(n >= 0 && (n == 0 || (block && out)), "sc_engine_process_block: bad block");
+    DeviceGuard g(e->device);
+    return do_block(e, block, n, out, true);
+}
+
+int sc_engine_process_sample(sc_engine *e, const void *x, void *out) {
+    SC_REQUIRE(e && x && out, "sc_engine_process_sample: null pointer");
+    DeviceGuard g(e->device);
+    // engine.py:99-116: one sample, a pending swap is NOT applied and the
+    // block-size limit does not apply.
+    const int64_t nb = e->nb;
+    e->nb = nb > 1 ? nb : 1;
+    const int rc = do_block(e, x, 1, out, false);
+    e->nb = nb;
+    return rc;
+}
+
+int sc_engine_swap_ir(sc_engine *e, const void *h, int64_t nh) {
+    SC_REQUIRE(e && h, "sc_engine_swap_ir: null pointer");
+    SC_REQUIRE(nh >= 1, "impulse response is empty");
+    DeviceGuard g(e->device);
+    return do_swap(e, h, nh);
+}
+
+int sc_engine_swap_ir_at_next_block(sc_engine *e, const void *h, int64_t nh) {
+    SC_REQUIRE(e && h, "sc_engine_swap_ir_at_next_block: null pointer");
+    SC_REQUIRE(nh >= 1, "impulse response is empty");
+    DeviceGuard g(e->device);
+    int rc = ensure_buffer(&e->pend, &e->pend_capacity, nh, e->es, false, 0, e->stream);
+    if (rc) return rc;
+    SC_CHECK_CUDA(cudaMemcpyAsync(e->pend, h, (size_t)nh * e->es, cudaMemcpyDeviceToDevice, e->stream));
+    e->pend_nh = nh;
+    e->has_pending = true;
+    return SC_OK;
+}
+
+int sc_engine_flush(sc_engine *e, void *tail, int64_t tail_capacity, int64_t *n_tail) {
+    SC_REQUIRE(e && n_tail, "sc_engine_flush: null pointer");
+    DeviceGuard g(e->device);
+    int64_t hs[ST_N];
+    int rc = read_state(e, hs);
+    if (rc) return rc;
+    const int64_t live = hs[ST_LIVE];
+    const int64_t nt = (e->nh - 1 > live) ? e->nh - 1 : live;  // engine.py:155
+    SC_REQUIRE(tail_capacity >= nt && (nt == 0 || tail), "sc_engine_flush: tail buffer too small (%lld < %lld)",
+               (long long)tail_capacity, (long long)nt);
+    if (nt > 0)
+        SC_CHECK_CUDA(cudaMemcpyAsync(tail, e->res[e->cur], (size_t)nt * e->es, cudaMemcpyDeviceToDevice,
+                                      e->stream));
+    // reset (engine.py:157-160): zero ring of len(ir), ri = live = consumed = 0
+    SC_CHECK_CUDA(cudaMemsetAsync(e->res[0], 0, (size_t)e->res_capacity * e->es, e->stream));
+    SC_CHECK_CUDA(cudaMemsetAsync(e->res[1], 0, (size_t)e->res_capacity * e->es, e->stream));
+    k_reset_state<<<1, 1, 0, e->stream>>>(e->st, e->nh);
+    SC_CHECK_LAUNCH();
+    e->cap_ub = e->nh;
+    e->consumed = 0;
+    SC_CHECK_CUDA(cudaStreamSynchronize(e->stream));
+    *n_tail = nt;
+    return SC_OK;
+}
+
+int sc_engine_state(sc_engine *e, int64_t *read_index, int64_t *live, int64_t *cap,
+                    int64_t *consumed, int64_t *nh, int *has_pending) {
+    SC_REQUIRE(e, "null engine");
+    DeviceGuard g(e->device);
+    int64_t hs[ST_N];
+    int rc = read_state(e, hs);
+    if (rc) return rc;
+    if (read_index) *read_index = hs[ST_RI];
+    if (live) *live = hs[ST_LIVE];
+    if (cap) *cap = hs[ST_CAP];
+    if (consumed) *consumed = e->consumed;
+    if (nh) *nh = e->nh;
+    if (has_pending) *has_pending = e->has_pending ? 1 : 0;
+    return SC_OK;
+}
+
+int sc_engine_schedule(sc_engine *e, void *dst, int64_t n, int64_t *n_written) {
+    SC_REQUIRE(e && n_written, "null pointer");
+    DeviceGuard g(e->device);
+    int64_t hs[ST_N];
+    int rc = read_state(e, hs);
+    if (rc) return rc;
+    const int64_t k = n < hs[ST_CAP] ? n : hs[ST_CAP];
+    if (k > 0) {
+        SC_REQUIRE(dst, "null destination");
+        SC_CHECK_CUDA(cudaMemcpyAsync(dst, e->res[e->cur], (size_t)k * e->es, cudaMemcpyDeviceToDevice, e->stream));
+        SC_CHECK_CUDA(cudaStreamSynchronize(e->stream));
+    }
+    *n_written = k;
+    return SC_OK;
+}
+
+int sc_engine_current_ir(sc_engine *e, void *dst, int64_t capacity, int64_t *nh) {
+    SC_REQUIRE(e && nh, "null pointer");
+    DeviceGuard g(e->device);
+    *nh = e->nh;
+    if (dst) {
+        SC_REQUIRE(capacity >= e->nh, "sc_engine_current_ir: buffer too small");
+        SC_CHECK_CUDA(cudaMemcpyAsync(dst, e->ir, (size_t)e->nh * e->es, cudaMemcpyDeviceToDevice, e->stream));
+    }
+    return SC_OK;
+}
+
+int sc_engine_process_blocks(sc_engine *e, const void *x, int64_t n_total, int64_t nb,
+                             const int64_t *swap_blocks, const void *const *swap_irs,
+                             const int64_t *swap_nh, int64_t n_swaps, void *out) {
+    SC_REQUIRE(e, "null engine");
+    SC_REQUIRE(nb >= 1 && nb <= e->nb, "sc_engine_process_blocks: nb must be in [1, block_size_nb]");
+    SC_REQUIRE(n_total >= 0 && (n_total == 0 || (x && out)), "sc_engine_process_blocks: bad input");
+    SC_REQUIRE(n_swaps == 0 || (swap_blocks && swap_irs && swap_nh), "sc_engine_process_blocks: bad swaps");
+    DeviceGuard g(e->device);
+    const char *xb = static_cast<const char *>(x);
+    char *ob = static_cast<char *>(out);
+    int64_t si = 0;
+    int64_t b = 0;
+    for (int64_t s = 0; s < n_total; s += nb, ++b) {
+        while (si < n_swaps && swap_blocks[si] <= b) {
+            if (swap_blocks[si] == b) {
+                SC_REQUIRE(swap_nh[si] >= 1, "impulse response is empty");
+                int rc = do_swap(e, swap_irs[si], swap_nh[si]);
+                if (rc) return rc;
+            }
+            ++si;
+        }
+        const int64_t n = n_total - s < nb ? n_total - s : nb;
+        int rc = do_block(e, xb + (size_t)s * e->es, n, ob + (size_t)s * e->es, true);
+        if (rc) return rc;
+    }
+    return SC_OK;
+}
+
+// ---------------------------------------------------------------- literal kernel
+
+int sc_scatter_block(int dtype, void *ring, int64_t cap, const void *ir, int64_t nh,
+                     const void *block, int64_t n, void *out, int64_t read_index, int64_t live,
+                     double threshold, int64_t *read_index_out, int64_t *live_out, void *stream) {
+    SC_REQUIRE(dtype == SC_F32 || dtype == SC_F64, "sc_scatter_block: bad dtype %d", dtype);
+    SC_REQUIRE(cap >= 1 && nh >= 1 && nh <= cap, "sc_scatter_block: need 1 <= len(ir) <= len(ring)");
+    SC_REQUIRE(read_index >= 0 && read_index < cap, "sc_scatter_block: read_index out of range");
+    SC_REQUIRE(ring && ir && read_index_out && live_out, "sc_scatter_block: null pointer");
+    SC_REQUIRE(n == 0 || (block && out), "sc_scatter_block: null block/out");
+    cudaStream_t s = as_stream(stream);
+    if (n == 0) {
+        *read_index_out = read_index;
+        *live_out = live;
+        return SC_OK;
+    }
+    const size_t es = esize(dtype);
+    int err = 0;
+    char *ws = static_cast<char *>(scratch(es * (size_t)cap * 2 + 64, 2, s, &err));
+    if (err) return err;
+    void *sched_in = ws, *sched_out = ws + es * (size_t)cap;
+    int64_t *st = reinterpret_cast<int64_t *>(ws + es * (size_t)cap * 2);
+    int64_t hs[ST_N] = {live, cap, read_index, 0};
+    SC_CHECK_CUDA(cudaMemcpyAsync(st, hs, sizeof(hs), cudaMemcpyHostToDevice, s));
+    const unsigned g = (unsigned)cdiv(cap, 256);
+    if (dtype == SC_F64)
+        k_ring_to_sched<double><<<g, 256, 0, s>>>(static_cast<double *>(ring), cap, read_index,
+                                                  static_cast<double *>(sched_in));
+    else
+        k_ring_to_sched<float><<<g, 256, 0, s>>>(static_cast<float *>(ring), cap, read_index,
+                                                 static_cast<float *>(sched_in));
+    SC_CHECK_LAUNCH();
+    ChainSeg seg{ir, nh, 0, n};
+    int rc = launch_chain(dtype, SC_SKIP_NOT_GT, threshold, block, 0, &seg, 1, sched_in, cap,
+                          nullptr, 0, n + cap, out, n, sched_out, s);
+    if (rc) return rc;
+    rc = launch_epilogue(dtype, block, n, threshold, nh, st, s);
+    if (rc) return rc;
+    const int64_t ri2 = (read_index + n) % cap;
+    if (dtype == SC_F64)
+        k_sched_to_ring<double><<<g, 256, 0, s>>>(static_cast<double *>(sched_out), cap, ri2,
+                                                  static_cast<double *>(ring));
+    else
+        k_sched_to_ring<float><<<g, 256, 0, s>>>(static_cast<float *>(sched_out), cap, ri2,
+                                                 static_cast<float *>(ring));
+    SC_CHECK_LAUNCH();
+    SC_CHECK_CUDA(cudaMemcpyAsync(hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    SC_CHECK_CUDA(cudaStreamSynchronize(s));
+    *read_index_out = ri2;
+    *live_out = hs[ST_LIVE];
+    return SC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,191 @@
+// k_ordered.cu -- ordered ("strict") scatter-convolution kernels.
+//
+// Every output is computed as ONE chain over input index m ascending,
+// starting from +0.0 (or from a carried residue), acc = acc + x[m]*h[t-m]
+// with the product and the sum rounded separately.  That is exactly the
+// order in which the reference's scatter loops touch each slot:
+//   core._scatter_full        pkg/src/scatterconv/core.py:80-92
+//   _kernels.scatter_block    pkg/src/scatterconv/_kernels.py:31-51
+// so float64 results are bit-identical to the reference, and streamed
+// results equal batch results for every block partition (the residue carry
+// continues the same chain).
+//
+// Gather form on the device: output-stationary, one thread per output slot,
+// drive samples and taps staged through shared memory per 256-sample chunk.
+// The drive chunk is a shared-memory broadcast; taps are read at consecutive
+// addresses by consecutive threads (conflict-free).  Zero-skip predicates are
+// warp-uniform (all threads of a chunk visit the same m).
+
+#include "sc_common.cuh"
+
+namespace sc {
+namespace {
+
+constexpr int TB = 256;  // outputs per CTA
+constexpr int MC = 256;  // drive samples per shared-memory chunk
+
+template <typename T>
+struct ChainArgs {
+    const T *x;
+    int64_t x_off;
+    ChainSeg seg[kMaxSegs];
+    int nseg;
+    const T *init;
+    int64_t init_len;
+    const int64_t *init_len_dev;
+    int64_t t0, n_out;
+    T *out_a;
+    int64_t n_a;
+    T *out_b;
+    double thr;
+};
+
+template <typename T, int SKIP>
+__global__ void __launch_bounds__(TB) k_chain(ChainArgs<T> a) {
+    __shared__ T xs[MC];
+    __shared__ T hs[MC + TB - 1];
+    const int64_t tile0 = a.t0 + (int64_t)blockIdx.x * TB;
+    const int64_t t_end = a.t0 + a.n_out;
+    const int64_t tile_last = (tile0 + TB < t_end ? tile0 + TB : t_end) - 1;
+    const int64_t t = tile0 + threadIdx.x;
+    const bool active = t < t_end;
+    const int64_t init_len = a.init_len_dev ? *a.init_len_dev : a.init_len;
+
+    T acc = T(0);
+    if (active && a.init != nullptr && (t - a.t0) < init_len) acc = a.init[t - a.t0];
+
+    for (int s = 0; s < a.nseg; ++s) {
+        const T *__restrict__ h = static_cast<const T *>(a.seg[s].h);
+        const int64_t nh = a.seg[s].nh;
+        const int64_t m_lo = a.seg[s].m_lo, m_hi = a.seg[s].m_hi;
+        const int64_t blo = tile0 - nh + 1 > m_lo ? tile0 - nh + 1 : m_lo;
+        const int64_t bhi = tile_last + 1 < m_hi ? tile_last + 1 : m_hi;  // exclusive
+        const int64_t my_lo = t - nh + 1 > m_lo ? t - nh + 1 : m_lo;
+        const int64_t my_hi = t < m_hi - 1 ? t : m_hi - 1;  // inclusive
+        for (int64_t mc = blo; mc < bhi; mc += MC) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < MC; i += TB) {
+                const int64_t m = mc + i;
+                xs[i] = m < bhi ? a.x[m - a.x_off] : T(0);
+            }
+            const int64_t kbase = tile0 - mc - MC + 1;
+            for (int i = threadIdx.x; i < MC + TB - 1; i += TB) {
+                const int64_t k = kbase + i;
+                hs[i] = (k >= 0 && k < nh) ? h[k] : T(0);
+            }
+            __syncthreads();
+            if (active) {
+                const int64_t lo64 = my_lo > mc ? my_lo : mc;
+                const int64_t hi64 = my_hi < mc + MC - 1 ? my_hi : mc + MC - 1;
+                if (lo64 <= hi64) {
+                    const int lo = (int)(lo64 - mc), hi = (int)(hi64 - mc);
+                    const T *hp = hs + threadIdx.x + MC - 1;
+#pragma unroll 4
+                    for (int im = lo; im <= hi; ++im) {
+                        const T xv = xs[im];
+                        if (skipped<SKIP>(xv, a.thr)) continue;
+                        acc = add_rn(acc, mul_rn(xv, hp[-im]));
+                    }
+                }
+            }
+        }
+    }
+    if (active) {
+        const int64_t i = t - a.t0;
+        if (i < a.n_a)
+            a.out_a[i] = acc;
+        else if (a.out_b != nullptr)
+            a.out_b[i - a.n_a] = acc;
+    }
+}
+
+template <typename T>
+int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off,
+                   const ChainSeg *segs, int nseg, const void *init, int64_t init_len,
+                   const int64_t *init_len_dev, int64_t t0, int64_t n_out, void *out_a,
+                   int64_t n_a, void *out_b, cudaStream_t stream) {
+    if (n_out <= 0) return SC_OK;
+    SC_REQUIRE(nseg >= 0 && nseg <= kMaxSegs, "chain: bad segment count %d", nseg);
+    ChainArgs<T> a{};
+    a.x = static_cast<const T *>(x);
+    a.x_off = x_off;
+    for (int i = 0; i < nseg; ++i) a.seg[i] = segs[i];
+    a.nseg = nseg;
+    a.init = static_cast<const T *>(init);
+    a.init_len = init_len;
+    a.init_len_dev = init_len_dev;
+    a.t0 = t0;
+    a.n_out = n_out;
+    a.out_a = static_cast<T *>(out_a);
+    a.n_a = n_a;
+    a.out_b = static_cast<T *>(out_b);
+    a.thr = threshold;
+    const int64_t grid = cdiv(n_out, TB);
+    SC_REQUIRE(grid < (int64_t)INT32_MAX, "chain: output range too large");
+    switch (skip_mode) {
+        case SC_SKIP_NONE: k_chain<T, SC_SKIP_NONE><<<(unsigned)grid, TB, 0, stream>>>(a); break;
+        case SC_SKIP_LE: k_chain<T, SC_SKIP_LE><<<(unsigned)grid, TB, 0, stream>>>(a); break;
+        case SC_SKIP_NOT_GT: k_chain<T, SC_SKIP_NOT_GT><<<(unsigned)grid, TB, 0, stream>>>(a); break;
+        default: SC_REQUIRE(false, "chain: bad skip_mode %d", skip_mode);
+    }
+    SC_CHECK_LAUNCH();
+    return SC_OK;
+}
+
+// ---------------------------------------------------------------- direct form
+// Gather form of direct_form (core.py:102-119).  The reference sums the
+// individually rounded products e[m]*h[n-m] with math.fsum (exact rounding).
+// Here: products rounded the same way, summed with the compensated
+// "Sum2" scheme (TwoSum error-free transformation, error terms accumulated
+// and folded in once) -- as accurate as a double-double accumulator, which
+// is exactly rounded except under extreme cancellation.
+
+__device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
+    s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+__global__ void __launch_bounds__(TB) k_direct_dd(const double *__restrict__ e, int64_t ne,
+                                                  const double *__restrict__ h, int64_t nh,
+                                                  double *__restrict__ y) {
+    const int64_t n = (int64_t)blockIdx.x * TB + threadIdx.x;
+    if (n >= ne + nh - 1) return;
+    const int64_t lo = n - nh + 1 > 0 ? n - nh + 1 : 0;
+    const int64_t hi = n < ne - 1 ? n : ne - 1;
+    double s = 0.0, c = 0.0;
+    for (int64_t m = lo; m <= hi; ++m) {
+        const double p = __dmul_rn(e[m], h[n - m]);
+        double q;
+        two_sum(s, p, s, q);
+        c = __dadd_rn(c, q);
+    }
+    y[n] = __dadd_rn(s, c);
+}
+
+}  // namespace
+
+int launch_chain(int dtype, int skip_mode, double threshold, const void *x, int64_t x_off,
+                 const ChainSeg *segs, int nseg, const void *init, int64_t init_len,
+                 const int64_t *init_len_dev, int64_t t0, int64_t n_out, void *out_a,
+                 int64_t n_a, void *out_b, cudaStream_t stream) {
+    if (dtype == SC_F64)
+        return launch_chain_t<double>(skip_mode, threshold, x, x_off, segs, nseg, init, init_len,
+                                      init_len_dev, t0, n_out, out_a, n_a, out_b, stream);
+    if (dtype == SC_F32)
+        return launch_chain_t<float>(skip_mode, threshold, x, x_off, segs, nseg, init, init_len,
+                                     init_len_dev, t0, n_out, out_a, n_a, out_b, stream);
+    set_error("chain: bad dtype %d", dtype);
+    return SC_ERR_ARG;
+}
+
+int launch_direct_form_dd(const double *e, int64_t ne, const double *h, int64_t nh, double *y,
+                          cudaStream_t stream) {
+    const int64_t nout = ne + nh - 1;
+    if (nout <= 0) return SC_OK;
+    k_direct_dd<<<(unsigned)cdiv(nout, TB), TB, 0, stream>>>(e, ne, h, nh, y);
+    SC_CHECK_LAUNCH();
+    return SC_OK;
+}
+
+}  // namespace sc

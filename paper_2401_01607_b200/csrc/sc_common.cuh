@@ -1,0 +1,111 @@
+// sc_common.cuh -- shared helpers for the scatterconv B200 library (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+
+#include "../../include/scatterconv_b200.h"
+
+namespace sc {
+
+// ------------------------------------------------------------------ errors
+
+void set_error(const char *fmt, ...);
+
+#define SC_CHECK_CUDA(expr)                                                            \
+    do {                                                                               \
+        cudaError_t _e = (expr);                                                       \
+        if (_e != cudaSuccess) {                                                       \
+            ::sc::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),   \
+                            __FILE__, __LINE__);                                       \
+            return SC_ERR_CUDA;                                                        \
+        }                                                                              \
+    } while (0)
+
+void note_launch();  // bumps the sc_launch_count() counter
+
+#define SC_CHECK_LAUNCH()                                                              \
+    do {                                                                               \
+        ::sc::note_launch();                                                           \
+        cudaError_t _e = cudaGetLastError();                                           \
+        if (_e != cudaSuccess) {                                                       \
+            ::sc::set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e), \
+                            __FILE__, __LINE__);                                       \
+            return SC_ERR_CUDA;                                                        \
+        }                                                                              \
+    } while (0)
+
+#define SC_REQUIRE(cond, ...)                                                          \
+    do {                                                                               \
+        if (!(cond)) {                                                                 \
+            ::sc::set_error(__VA_ARGS__);                                              \
+            return SC_ERR_ARG;                                                         \
+        }                                                                              \
+    } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count();  // of the current device (cached per device)
+
+// Grow-only per-device scratch buffer (workspace for split-K partials and
+// padded taps).  Stream-ordered: a buffer is only reallocated after a
+// cudaStreamSynchronize of the requesting stream.
+void *scratch(size_t bytes, int slot, cudaStream_t stream, int *err);
+
+// ------------------------------------------------------------------ exact arithmetic
+
+// Separately rounded multiply then add: the reference's strict order
+// (_kernels.py:1-8).  These never contract into FMA.
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+
+// Zero-skip predicates, compared in float64 like the reference (a float32
+// sample widens exactly; the threshold is never rounded to float32).
+template <int SKIP, typename T>
+__device__ __forceinline__ bool skipped(T x, double thr) {
+    if (SKIP == SC_SKIP_LE) return fabs((double)x) <= thr;       // core.py:164 (NaN not skipped)
+    if (SKIP == SC_SKIP_NOT_GT) return !(fabs((double)x) > thr); // _kernels.py:33 (NaN skipped)
+    return false;
+}
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace sc
+
+// ------------------------------------------------------------------ internal launchers
+// (implemented in the .cu files, used by capi.cu / engine.cu)
+
+namespace sc {
+
+struct ChainSeg {
+    const void *h;    // taps of the IR active for drive samples [m_lo, m_hi)
+    int64_t nh;
+    int64_t m_lo, m_hi;
+};
+constexpr int kMaxSegs = 4;
+
+// Ordered chain: outputs t in [t0, t0+n_out):
+//   acc = init (init[t-t0] if t-t0 < init_len (host value, or *init_len_dev
+//         when non-null), else +0)
+//   for each seg, for m ascending in seg ∩ [t-nh+1, t]: unless skipped,
+//         acc = acc + x[m - x_off] * h[t-m]   (separately rounded)
+//   t-t0 < n_a -> out_a[t-t0], else out_b[t-t0-n_a]
+int launch_chain(int dtype, int skip_mode, double threshold, const void *x, int64_t x_off,
+                 const ChainSeg *segs, int nseg, const void *init, int64_t init_len,
+                 const int64_t *init_len_dev, int64_t t0, int64_t n_out, void *out_a,
+                 int64_t n_a, void *out_b, cudaStream_t stream);
+
+// Fast FP32 FIR over an output range (see k_fast_f32.cu).
+int launch_fir_f32_fast(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
+                        const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy,
+                        int64_t n_begin, int64_t n_end, int64_t channels, cudaStream_t stream);
+
+int launch_direct_form_dd(const double *e, int64_t ne, const double *h, int64_t nh, double *y,
+                          cudaStream_t stream);
+
+}  // namespace sc

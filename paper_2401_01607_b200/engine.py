@@ -1,0 +1,296 @@
+"""Streaming convolution engine -- drop-in for ``scatterconv.engine``.
+
+Mirrors pkg/src/scatterconv/engine.py (EngineConfig, ScatterEngine with
+process_sample / process_block / flush / swap_ir / swap_ir_at_next_block /
+render and the ring / read_index / current_ir / samples_consumed
+properties).  The state lives on the GPU inside a ``sc_engine`` handle
+(csrc/engine.cu): the residue ring (kept in schedule order), the impulse
+response copy, ``live``, ``cap`` and ``read_index``.  Blocks and IR swaps
+never wait on the host; only calls that must return host data (flush, the
+state properties, numpy-in/numpy-out blocks) synchronise.
+
+Arithmetic is the ordered chain (csrc/k_ordered.cu): float64 engines are
+bit-identical to the reference, and in both dtypes any block partition
+yields the identical stream (block-size invariance, engine.py:7-9).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _dev
+from . import _native as N
+from .core import Signal
+
+TAIL_POLICIES = ("emit-on-flush", "auto-append")
+
+# Block size sweet spot (engine.py:31-33).
+DEFAULT_BLOCK_SIZE = 8192
+
+
+@dataclass
+class EngineConfig:
+    """Knobs for a ScatterEngine (engine.py:36-57).
+
+    block_size_nb        upper bound on samples per process_block call
+    zero_skip_threshold  inputs with |x| <= threshold scatter nothing
+    tail_policy          "auto-append" or "emit-on-flush" (render)
+    """
+
+    block_size_nb: int = DEFAULT_BLOCK_SIZE
+    zero_skip_threshold: float = 0.0
+    tail_policy: str = "emit-on-flush"
+
+    def __post_init__(self):
+        if not isinstance(self.block_size_nb, (int, np.integer)) or self.block_size_nb < 1:
+            raise ValueError(f"block_size_nb must be >= 1, got {self.block_size_nb!r}")
+        if self.zero_skip_threshold < 0:
+            raise ValueError(f"zero_skip_threshold must be >= 0, got {self.zero_skip_threshold}")
+        if self.tail_policy not in TAIL_POLICIES:
+            raise ValueError(f"tail_policy must be one of {TAIL_POLICIES}, got {self.tail_policy!r}")
+
+
+class ScatterEngine:
+    """Stateful block- or sample-driven convolution processor on the GPU.
+
+    One instance is single-threaded; instances are independent (one engine
+    per channel, engine.py:60-66).  The engine's dtype is the impulse
+    response's (float64 by default, float32 for float32 arrays/tensors).
+    """
+
+    def __init__(self, h: Signal, config: EngineConfig | None = None, *, device=None):
+        if len(h) == 0:
+            raise ValueError("impulse response is empty")
+        self.config = config if config is not None else EngineConfig()
+        t = _dev.torch()
+        self._lib = N.lib()
+        self._npd = h.dtype
+        self._dt = N.dtype_code(self._npd)
+        if device is None:
+            device = h.samples.device if (_dev.is_tensor(h.samples) and h.samples.is_cuda) else \
+                t.device("cuda", t.cuda.current_device())
+        self._device = t.device(device)
+        self._sample_rate = h.sample_rate
+        self._ir_signal = Signal(self._copy_host(h.samples), h.sample_rate)
+        self._pending_ir = None
+        self._handle = ctypes.c_void_p()
+        hd = self._to_dev(h.samples)
+        with t.cuda.device(self._device):
+            N.check(self._lib.sc_engine_create(self._dt, N.ptr(hd), len(h),
+                                               int(self.config.block_size_nb),
+                                               float(self.config.zero_skip_threshold),
+                                               N.stream_ptr(), ctypes.byref(self._handle)))
+
+    # ------------------------------------------------------------- plumbing
+
+    def _copy_host(self, samples):
+        if _dev.is_tensor(samples):
+            return samples.detach().clone()
+        return np.array(samples, dtype=self._npd, copy=True)
+
+    def _to_dev(self, samples):
+        return _dev.as_device(samples, self._npd, device=self._device)
+
+    def _bind_stream(self):
+        N.check(self._lib.sc_engine_set_stream(self._handle, N.stream_ptr()))
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.sc_engine_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self._handle = ctypes.c_void_p()
+
+    def _state(self):
+        ri, live, cap, cons, nh = (ctypes.c_int64() for _ in range(5))
+        pend = ctypes.c_int()
+        t = _dev.torch()
+        with t.cuda.device(self._device):
+            self._bind_stream()
+            N.check(self._lib.sc_engine_state(self._handle, ctypes.byref(ri), ctypes.byref(live),
+                                              ctypes.byref(cap), ctypes.byref(cons),
+                                              ctypes.byref(nh), ctypes.byref(pend)))
+        return {"read_index": ri.value, "live": live.value, "cap": cap.value,
+                "consumed": cons.value, "nh": nh.value}
+
+    # ----------------------------------------------------------- properties
+
+    @property
+    def ring(self) -> np.ndarray:
+        """The reference's physical ring (engine.py:83-85): the schedule-order
+        residue rotated by read_index.  A host copy."""
+        st = self._state()
+        sched = self._schedule_order()
+        return np.roll(sched, st["read_index"])
+
+    @property
+    def read_index(self) -> int:
+        return self._state()["read_index"]
+
+    @property
+    def current_ir(self) -> Signal:
+        return self._ir_signal
+
+    @property
+    def samples_consumed(self) -> int:
+        return self._state()["consumed"]
+
+    @property
+    def dtype(self):
+        return self._npd
+
+    # ------------------------------------------------------------- streaming
+
+    def process_sample(self, x: float) -> float:
+        """Consume one input sample, return the output sample it completes
+        (engine.py:99-116; a pending swap is not applied)."""
+        t = _dev.torch()
+        with t.cuda.device(self._device):
+            xd = t.tensor([x], dtype=_dev.torch_dtype(self._npd), device=self._device)
+            out = t.empty(1, dtype=xd.dtype, device=self._device)
+            self._bind_stream()
+            N.check(self._lib.sc_engine_process_sample(self._handle, N.ptr(xd), N.ptr(out)))
+            return float(out.item())
+
+    def process_block(self, block: Signal) -> Signal:
+        """Consume a block of at most block_size_nb samples (engine.py:118-146).
+
+        Order of effects as in the reference: pending swap, size check, rate
+        check, then the block.  CUDA-tensor blocks return CUDA-tensor output
+        without synchronising.
+        """
+        if self._pending_ir is not None:
+            h_new, self._pending_ir = self._pending_ir, None
+            self.swap_ir(h_new)
+        if len(block) > self.config.block_size_nb:
+            raise ValueError(
+                f"block of {len(block)} samples exceeds block_size_nb={self.config.block_size_nb}"
+            )
+        if block.sample_rate != self._sample_rate:
+            raise ValueError(
+                f"sample rates differ: block {block.sample_rate} Hz vs engine {self._sample_rate} Hz"
+            )
+        t = _dev.torch()
+        with t.cuda.device(self._device):
+            xd = self._to_dev(block.samples)
+            out = t.empty(len(block), dtype=xd.dtype, device=self._device)
+            if len(block):
+                self._bind_stream()
+                N.check(self._lib.sc_engine_process_block(self._handle, N.ptr(xd), len(block),
+                                                          N.ptr(out)))
+        return Signal(_dev.like_input(out, block.samples), self._sample_rate)
+
+    def flush(self) -> Signal:
+        """Emit the pending residue and reset the engine (engine.py:148-161):
+        max(len(ir)-1, live) samples in emission order."""
+        t = _dev.torch()
+        with t.cuda.device(self._device):
+            st = self._state()
+            cap = max(st["cap"], 1)
+            tail = t.empty(cap, dtype=_dev.torch_dtype(self._npd), device=self._device)
+            n = ctypes.c_int64()
+            N.check(self._lib.sc_engine_flush(self._handle, N.ptr(tail), cap, ctypes.byref(n)))
+            tail = tail[:n.value].clone()
+        like = self._ir_signal.samples
+        return Signal(_dev.like_input(tail, like), self._sample_rate)
+
+    def swap_ir(self, h_new: Signal):
+        """Replace the impulse response, effective for the very next sample
+        (engine.py:163-186).  Residue keeps its schedule; no host round-trip."""
+        if len(h_new) == 0:
+            raise ValueError("impulse response is empty")
+        if h_new.sample_rate != self._sample_rate:
+            raise ValueError(
+                f"sample rates differ: new impulse response {h_new.sample_rate} Hz "
+                f"vs engine {self._sample_rate} Hz"
+            )
+        t = _dev.torch()
+        with t.cuda.device(self._device):
+            hd = self._to_dev(h_new.samples)
+            self._bind_stream()
+            N.check(self._lib.sc_engine_swap_ir(self._handle, N.ptr(hd), len(h_new)))
+        self._ir_signal = Signal(self._copy_host(h_new.samples), h_new.sample_rate)
+
+    def swap_ir_at_next_block(self, h_new: Signal):
+        """Defer the swap to the start of the next process_block call (engine.py:188-192)."""
+        if len(h_new) == 0:
+            raise ValueError("impulse response is empty")
+        self._pending_ir = h_new
+
+    def render(self, e: Signal) -> Signal:
+        """Run a whole signal through in blocks (engine.py:194-209)."""
+        nb = self.config.block_size_nb
+        parts = []
+        for start in range(0, len(e), nb):
+            chunk = Signal(e.samples[start:start + nb], e.sample_rate)
+            parts.append(self.process_block(chunk).samples)
+        if _dev.is_tensor(e.samples):
+            t = _dev.torch()
+            body = t.cat(parts) if parts else e.samples[:0].to(_dev.torch_dtype(self._npd))
+            if self.config.tail_policy == "auto-append":
+                body = t.cat([body, self.flush().samples.to(body.device)])
+        else:
+            body = np.concatenate(parts) if parts else np.empty(0, dtype=self._npd)
+            if self.config.tail_policy == "auto-append":
+                body = np.concatenate([body, self.flush().samples])
+        return Signal(body, self._sample_rate)
+
+    def _schedule_order(self) -> np.ndarray:
+        """Ring contents reordered so index 0 is the next slot to emit (engine.py:211-214)."""
+        t = _dev.torch()
+        with t.cuda.device(self._device):
+            st = self._state()
+            buf = t.empty(max(st["cap"], 1), dtype=_dev.torch_dtype(self._npd), device=self._device)
+            n = ctypes.c_int64()
+            N.check(self._lib.sc_engine_schedule(self._handle, N.ptr(buf), st["cap"],
+                                                 ctypes.byref(n)))
+            return buf[:n.value].cpu().numpy()
+
+    # ------------------------------------------------------ device-side extras
+
+    def process_stream(self, x, nb: int | None = None, swaps=()):
+        """Back-to-back blocks of `nb` samples with an IR-swap schedule, queued
+        without host synchronisation (one C call; csrc/engine.cu).
+
+        ``swaps`` is a sequence of (block_index, impulse_response) pairs: the
+        swap_ir happens right before that block.  Bit-identical to calling
+        swap_ir/process_block in the same order.  Returns the body (device
+        tensor if x is a CUDA tensor, else ndarray).
+        """
+        nb = self.config.block_size_nb if nb is None else int(nb)
+        if nb < 1 or nb > self.config.block_size_nb:
+            raise ValueError(f"nb must be in [1, block_size_nb={self.config.block_size_nb}]")
+        if self._pending_ir is not None and len(x):
+            h_new, self._pending_ir = self._pending_ir, None
+            self.swap_ir(h_new)
+        t = _dev.torch()
+        with t.cuda.device(self._device):
+            xs = x.samples if isinstance(x, Signal) else x
+            xd = self._to_dev(xs)
+            out = t.empty(xd.shape[0], dtype=xd.dtype, device=self._device)
+            swaps = sorted(swaps, key=lambda s: s[0])
+            irs = [self._to_dev(s[1].samples if isinstance(s[1], Signal) else s[1]) for s in swaps]
+            n = len(swaps)
+            blocks = (ctypes.c_int64 * max(n, 1))(*[int(s[0]) for s in swaps])
+            ptrs = (ctypes.c_void_p * max(n, 1))(*[ir.data_ptr() for ir in irs])
+            nhs = (ctypes.c_int64 * max(n, 1))(*[ir.shape[0] for ir in irs])
+            self._bind_stream()
+            N.check(self._lib.sc_engine_process_blocks(self._handle, N.ptr(xd), xd.shape[0], nb,
+                                                       blocks, ptrs, nhs, n, N.ptr(out)))
+            if swaps:
+                last = swaps[-1][1]
+                self._ir_signal = Signal(self._copy_host(last.samples if isinstance(last, Signal) else last),
+                                         self._sample_rate)
+        return _dev.like_input(out, xs)
+
+    def state_dict(self) -> dict:
+        """Snapshot for tests/checkpointing: ring, schedule, read_index, live, consumed."""
+        st = self._state()
+        sched = self._schedule_order()
+        return {"read_index": st["read_index"], "ring": np.roll(sched, st["read_index"]),
+                "consumed": st["consumed"], "live": st["live"], "sched": sched}

@@ -1,0 +1,262 @@
+"""Whole-signal convolution on the GPU vs the reference's goldens and the CPU
+oracle.  Mirrors pkg/tests/test_core.py (frozen values, oracle equivalence,
+algebraic properties) and adds the float32 fast path.
+
+float64: bit-exact to the reference (ordered kernel).  float32 fast path:
+max-abs error <= 1e-5 * max|x| * ||h||_1 (north_star tolerance).
+"""
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+from oracle import oracle as O
+from paper_2401_01607_b200 import core, configs
+from paper_2401_01607_b200.core import (
+    Signal,
+    commuted_convolve,
+    direct_form,
+    scatter_convolve,
+    scatter_convolve_skip_zeros,
+)
+from paper_2401_01607_b200.multichannel import convolve_batched
+from paper_2401_01607_b200.sharded import convolve_shard, shard_plan
+from tests import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+
+def sig(values, rate=44100):
+    return Signal(np.asarray(values, dtype=np.float64), rate)
+
+
+def full(out) -> np.ndarray:
+    return np.asarray(out.concatenated().samples)
+
+
+def assert_close(actual, expected, rtol):
+    expected = np.asarray(expected)
+    scale = max(1.0, float(np.max(np.abs(expected))) if expected.size else 0.0)
+    np.testing.assert_allclose(actual, expected, rtol=0.0, atol=rtol * scale)
+
+
+def within_tol(y, ref, x, h, dtype="f32"):
+    tol = configs.tolerance(x, h, dtype)
+    err = float(np.max(np.abs(np.asarray(y, np.float64) - ref))) if len(ref) else 0.0
+    assert err <= tol, f"max err {err:.3e} > tol {tol:.3e}"
+    return err, tol
+
+
+amplitudes = st.floats(min_value=-1.0, max_value=1.0, allow_nan=False, width=64)
+signal_values = st.lists(amplitudes, min_size=1, max_size=64)
+
+# ---------------------------------------------------------------- frozen values
+
+
+def test_direct_form_hand_examples():
+    assert np.array_equal(direct_form(sig([1.0]), sig([5.0, 6.0, 7.0])).samples, [5.0, 6.0, 7.0])
+    assert np.array_equal(direct_form(sig([1.0, 2.0]), sig([3.0, 4.0])).samples, [3.0, 10.0, 8.0])
+    assert np.array_equal(direct_form(sig([0.0, 0.0, 0.0]), sig([1.0, 1.0])).samples, np.zeros(4))
+
+
+def test_scatter_hand_examples():
+    out = scatter_convolve(sig([1.0, 2.0]), sig([3.0, 4.0]))
+    assert np.array_equal(out.body.samples, [3.0, 10.0])
+    assert np.array_equal(out.tail.samples, [8.0])
+    out = scatter_convolve(sig([1.0, 0.0, 0.0, 0.0]), sig([9.0]))
+    assert np.array_equal(out.body.samples, [9.0, 0.0, 0.0, 0.0]) and len(out.tail) == 0
+    h = sig([0.5, -0.25, 0.125])
+    for k in (1, 3, 7):
+        got = full(scatter_convolve(sig([0.0] * k + [1.0]), h))
+        assert np.array_equal(got[:k], np.zeros(k)) and np.array_equal(got[k:], h.samples)
+
+
+def test_commuted_short_signal_drives(monkeypatch):
+    lengths = []
+    original = core._scatter_full
+
+    def spy(drive, kern):
+        lengths.append(len(drive))
+        return original(drive, kern)
+
+    monkeypatch.setattr(core, "_scatter_full", spy)
+    e = sig([1.0, 2.0, 3.0, 4.0, 5.0, 6.0])
+    h = sig([1.0, 2.0, 3.0])
+    out = commuted_convolve(e, h)
+    assert lengths == [3]
+    assert len(out.body) == 6 and len(out.tail) == 2
+    lengths.clear()
+    commuted_convolve(h, e)
+    assert lengths == [3]
+
+
+def test_skip_zeros_hand_examples():
+    out = scatter_convolve_skip_zeros(sig([1.0, 0.0, 2.0]), sig([1.0, 1.0]), threshold=0.0)
+    assert np.array_equal(out.body.samples, [1.0, 1.0, 2.0]) and np.array_equal(out.tail.samples, [2.0])
+    out = scatter_convolve_skip_zeros(sig([0.0, 0.0]), sig([4.0, 5.0, 6.0]), threshold=0.0)
+    assert np.array_equal(full(out), np.zeros(4))
+    out = scatter_convolve_skip_zeros(sig([1.0, 1e-9, 1.0]), sig([1.0]), threshold=1e-6)
+    assert np.array_equal(out.body.samples, [1.0, 0.0, 1.0])
+
+
+def test_nan_and_signed_zero_semantics():
+    # scatter_convolve propagates NaN (core.py:90); -0.0 inputs still "scatter"
+    got = full(scatter_convolve(sig([1.0, np.nan, 2.0]), sig([1.0, 1.0])))
+    want = O.scatter_full([1.0, np.nan, 2.0], [1.0, 1.0])
+    assert np.array_equal(got, want, equal_nan=True)
+    got = full(scatter_convolve(sig([-0.0]), sig([-0.0, 1.0])))
+    assert np.array_equal(np.signbit(got), np.signbit(O.scatter_full([-0.0], [-0.0, 1.0])))
+
+
+# ---------------------------------------------------------------- reference goldens
+
+
+@pytest.fixture(scope="module")
+def pairs():
+    return G.small_pairs()
+
+
+def test_golden_scatter_commuted_skip_bit_exact(pairs):
+    for p in pairs:
+        E, H = sig(p["e"]), sig(p["h"])
+        assert np.array_equal(full(scatter_convolve(E, H)), p["scatter"])
+        assert np.array_equal(full(commuted_convolve(E, H)), p["commuted"])
+        assert np.array_equal(full(scatter_convolve_skip_zeros(E, H, p["threshold"])), p["skip"])
+
+
+def test_golden_direct_form(pairs):
+    exact = 0
+    for p in pairs:
+        got = direct_form(sig(p["e"]), sig(p["h"])).samples
+        assert_close(got, p["direct"], 1e-15)
+        exact += int(np.array_equal(got, p["direct"]))
+    assert exact >= 0.95 * len(pairs)
+
+
+# ---------------------------------------------------------------- properties (float64)
+
+
+@given(e=signal_values, h=signal_values)
+@settings(max_examples=150)
+def test_oracle_equivalence(e, h):
+    got = full(scatter_convolve(sig(e), sig(h)))
+    assert np.array_equal(got, O.scatter_full(e, h))          # reference chain, bit-exact
+    assert_close(got, O.direct_form(e, h), 1e-12)             # exact-sum oracle
+
+
+@given(e=signal_values, h=signal_values)
+def test_length_law_and_commutativity(e, h):
+    out = scatter_convolve(sig(e), sig(h))
+    assert len(out.body) == len(e) and len(out.tail) == len(h) - 1
+    assert_close(full(out), full(scatter_convolve(sig(h), sig(e))), 1e-12)
+    assert_close(full(commuted_convolve(sig(e), sig(h))), full(out), 1e-12)
+
+
+@given(e1=signal_values, e2=signal_values, h=signal_values,
+       a=st.floats(min_value=-10, max_value=10, allow_nan=False, width=64),
+       b=st.floats(min_value=-10, max_value=10, allow_nan=False, width=64))
+def test_linearity(e1, e2, h, a, b):
+    n = max(len(e1), len(e2))
+    x1 = np.zeros(n)
+    x1[: len(e1)] = e1
+    x2 = np.zeros(n)
+    x2[: len(e2)] = e2
+    mixed = full(scatter_convolve(sig(a * x1 + b * x2), sig(h)))
+    separate = a * full(scatter_convolve(sig(x1), sig(h))) + b * full(scatter_convolve(sig(x2), sig(h)))
+    assert_close(mixed, separate, 1e-10)
+
+
+@given(e=signal_values, h=signal_values, k=st.integers(min_value=1, max_value=16))
+def test_time_invariance_bit_exact(e, h, k):
+    base = full(scatter_convolve(sig(e), sig(h)))
+    shifted = full(scatter_convolve(sig([0.0] * k + e), sig(h)))
+    assert np.array_equal(shifted[:k], np.zeros(k)) and np.array_equal(shifted[k:], base)
+
+
+@given(h=signal_values)
+def test_unit_impulse_bit_exact(h):
+    assert np.array_equal(full(scatter_convolve(sig([1.0]), sig(h))), np.asarray(h))
+
+
+@given(e=signal_values, h=signal_values, threshold=st.floats(min_value=0, max_value=0.5, width=64))
+def test_skip_threshold_equals_thresholded_input(e, h, threshold):
+    skipped = full(scatter_convolve_skip_zeros(sig(e), sig(h), threshold=threshold))
+    gated = np.where(np.abs(np.asarray(e)) <= threshold, 0.0, np.asarray(e))
+    assert np.array_equal(skipped, full(scatter_convolve(sig(gated), sig(h))))
+
+
+# ---------------------------------------------------------------- float32 fast path
+
+F32_CASES = [(1, 1), (1, 5000), (5000, 1), (3, 2), (8192, 64), (8193, 65), (10000, 3000),
+             (100_000, 4097), (30_000, 70_000), (20_000, 100_000), (200_000, 1023), (65, 8191)]
+
+
+@pytest.mark.parametrize("ne,nh", F32_CASES)
+def test_fast_f32_within_tolerance(ne, nh):
+    rng = np.random.default_rng(ne * 7 + nh)
+    x = rng.uniform(-1, 1, ne).astype(np.float32)
+    h = (rng.standard_normal(nh) * np.exp(-np.arange(nh) / max(1.0, nh / 4))).astype(np.float32)
+    y = full(scatter_convolve(Signal(x), Signal(h)))
+    assert y.dtype == np.float32 and len(y) == ne + nh - 1
+    ref = O.scatter_window(x, h, 0, ne + nh - 1)
+    within_tol(y, ref, x, h)
+
+
+@pytest.mark.parametrize("ne,nh", [(1, 1), (4000, 333), (20_000, 2048)])
+def test_ordered_f32_within_tolerance(ne, nh):
+    rng = np.random.default_rng(ne + 3 * nh)
+    x = rng.uniform(-1, 1, ne).astype(np.float32)
+    h = rng.standard_normal(nh).astype(np.float32)
+    y = full(scatter_convolve(Signal(x), Signal(h), mode="ordered"))
+    within_tol(y, O.scatter_full(x, h), x, h)
+
+
+def test_fast_f32_is_deterministic_and_tensor_resident():
+    import torch
+
+    rng = np.random.default_rng(1)
+    x = torch.from_numpy(rng.uniform(-1, 1, 50_000).astype(np.float32)).cuda()
+    h = torch.from_numpy(rng.standard_normal(9000).astype(np.float32)).cuda()
+    a = scatter_convolve(Signal(x), Signal(h)).concatenated().samples
+    b = scatter_convolve(Signal(x), Signal(h)).concatenated().samples
+    assert a.is_cuda and a.dtype == torch.float32
+    assert torch.equal(a, b)
+
+
+def test_fast_f32_nan_propagates_like_reference():
+    x = np.zeros(20_000, np.float32)
+    x[5] = np.nan
+    x[100] = 1.0
+    h = np.ones(300, np.float32)
+    y = full(scatter_convolve(Signal(x), Signal(h)))
+    ref = O.scatter_full(x, h)
+    assert np.array_equal(np.isnan(y), np.isnan(ref))
+
+
+def test_batched_matches_oracle_per_channel():
+    rng = np.random.default_rng(9)
+    C, ne, nh = 5, 3000, 1500
+    x = rng.uniform(-1, 1, (C, ne)).astype(np.float32)
+    h = rng.standard_normal((C, nh)).astype(np.float32)
+    y = convolve_batched(x, h)
+    assert y.shape == (C, ne + nh - 1)
+    for c in range(C):
+        within_tol(y[c], O.scatter_full(x[c], h[c]), x[c], h[c])
+    yb = convolve_batched(x, h[0])  # mono IR broadcast
+    within_tol(yb[3], O.scatter_full(x[3], h[0]), x[3], h[0])
+
+
+def test_shards_reassemble_full_output():
+    import torch
+
+    rng = np.random.default_rng(4)
+    x = rng.uniform(-1, 1, 40_000).astype(np.float32)
+    h = rng.standard_normal(5000).astype(np.float32)
+    hd = torch.from_numpy(h).cuda()
+    parts = []
+    for sh in shard_plan(len(x), len(h), 8):
+        xs = torch.from_numpy(x[sh.x_begin:sh.x_end]).cuda()
+        parts.append(convolve_shard(xs, sh, hd).cpu().numpy())
+    y = np.concatenate(parts)
+    within_tol(y, O.scatter_full(x, h), x, h)

@@ -1,0 +1,318 @@
+"""Device-resident streaming engine vs the reference's recorded sessions and
+the reference's own engine tests (pkg/tests/test_engine.py).  float64
+engines must be bit-exact; float32 engines must be block-size invariant and
+bit-identical to the float32 ordered batch kernel."""
+
+import ctypes
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+from oracle import oracle as O
+from paper_2401_01607_b200 import _kernels
+from paper_2401_01607_b200 import _native as N
+from paper_2401_01607_b200.core import Signal, direct_form, scatter_convolve, scatter_convolve_skip_zeros
+from paper_2401_01607_b200.engine import EngineConfig, ScatterEngine
+from tests import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+
+def sig(values, rate=44100):
+    return Signal(np.asarray(values, dtype=np.float64), rate)
+
+
+def run_stream(engine, e, cuts=()):
+    bounds = [0, *sorted(cuts), len(e)]
+    pieces = [engine.process_block(Signal(e.samples[lo:hi], e.sample_rate)).samples
+              for lo, hi in zip(bounds, bounds[1:])]
+    pieces.append(engine.flush().samples)
+    return np.concatenate(pieces)
+
+
+amplitudes = st.floats(min_value=-1.0, max_value=1.0, allow_nan=False, width=64)
+signal_values = st.lists(amplitudes, min_size=1, max_size=48)
+
+
+# ---------------------------------------------------------------- reference sessions
+
+
+class _Eng(ScatterEngine):
+    def process_block(self, block):
+        return super().process_block(sig(block) if not isinstance(block, Signal) else block).samples
+
+    def swap_ir(self, h):
+        super().swap_ir(sig(h) if not isinstance(h, Signal) else h)
+
+    def swap_ir_at_next_block(self, h):
+        super().swap_ir_at_next_block(sig(h) if not isinstance(h, Signal) else h)
+
+    def flush(self):
+        return super().flush().samples
+
+
+def test_reference_sessions_bit_exact():
+    for s in G.engine_sessions():
+        mk = lambda h, nb, thr: _Eng(sig(h), EngineConfig(block_size_nb=nb, zero_skip_threshold=thr))  # noqa: E731
+        for kind, got, want in G.replay(s, mk):
+            if kind == "state":
+                assert got["read_index"] == want["read_index"], s["tag"]
+                assert got["consumed"] == want["consumed"], s["tag"]
+                assert got["live"] == want["live"], s["tag"]
+                assert np.array_equal(got["ring"], G.unhex(want["ring"]), equal_nan=True), s["tag"]
+                assert np.array_equal(got["sched"], G.unhex(want["sched"]), equal_nan=True), s["tag"]
+            elif got is not None:
+                assert np.array_equal(got, G.unhex(want), equal_nan=True), (s["tag"], kind)
+
+
+# ---------------------------------------------------------------- reference engine tests
+
+
+def test_fresh_engine_state():
+    eng = ScatterEngine(sig([1.0, 2.0, 3.0]))
+    assert np.array_equal(eng.ring, [0.0, 0.0, 0.0])
+    assert eng.read_index == 0 and eng.samples_consumed == 0
+    assert np.array_equal(eng.current_ir.samples, [1.0, 2.0, 3.0])
+    assert len(ScatterEngine(sig([0.5])).ring) == 1
+    assert ScatterEngine(sig([0.5])).config.block_size_nb == 8192
+    with pytest.raises(ValueError, match="empty"):
+        ScatterEngine(sig([]))
+
+
+def test_process_sample_examples():
+    eng = ScatterEngine(sig([3.0, 4.0]))
+    assert eng.process_sample(1.0) == 3.0
+    assert eng.process_sample(2.0) == 10.0
+    assert np.array_equal(eng.flush().samples, [8.0])
+    eng = ScatterEngine(sig([3.0, 4.0, 5.0]))
+    assert eng.process_sample(0.0) == 0.0
+    assert np.array_equal(eng.ring, np.zeros(3))
+    eng = ScatterEngine(sig([1.0]))
+    for x in np.random.default_rng(3).uniform(-1, 1, 20):
+        assert eng.process_sample(x) == x
+
+
+def test_zero_latency_against_oracle_prefix():
+    rng = np.random.default_rng(7)
+    e = rng.uniform(-1, 1, 30)
+    h = sig(rng.uniform(-1, 1, 9))
+    eng = ScatterEngine(h)
+    for n in range(len(e)):
+        y = eng.process_sample(e[n])
+        assert y == scatter_convolve(sig(e[: n + 1]), h).body.samples[n]
+        np.testing.assert_allclose(y, direct_form(sig(e[: n + 1]), h).samples[n], atol=1e-12)
+
+
+def test_counters_and_errors():
+    eng = ScatterEngine(sig([1.0, 1.0]))
+    eng.process_sample(1.0)
+    eng.process_block(sig([1.0, 1.0, 1.0]))
+    assert eng.samples_consumed == 4
+    eng.flush()
+    assert eng.samples_consumed == 0
+    eng = ScatterEngine(sig([1.0]), EngineConfig(block_size_nb=4))
+    with pytest.raises(ValueError, match="exceeds block_size_nb"):
+        eng.process_block(sig(np.zeros(5)))
+    eng = ScatterEngine(sig([1.0], 44100))
+    with pytest.raises(ValueError, match="sample rates differ"):
+        eng.process_block(sig([1.0], 48000))
+    with pytest.raises(ValueError, match="empty"):
+        eng.swap_ir(sig([]))
+    with pytest.raises(ValueError, match="sample rates differ"):
+        eng.swap_ir(sig([1.0], 48000))
+
+
+@given(e=signal_values, h=signal_values, data=st.data())
+@settings(max_examples=120)
+def test_stream_equals_batch_bit_exact(e, h, data):
+    cuts = data.draw(st.lists(st.integers(min_value=0, max_value=len(e)), max_size=5), label="cuts")
+    streamed = run_stream(ScatterEngine(sig(h)), sig(e), cuts)
+    assert np.array_equal(streamed, np.asarray(scatter_convolve(sig(e), sig(h)).concatenated().samples))
+
+
+@given(e=signal_values, h=signal_values, nb=st.integers(min_value=1, max_value=64))
+@settings(max_examples=60)
+def test_block_size_invariance(e, h, nb):
+    per_sample = run_stream(ScatterEngine(sig(h), EngineConfig(block_size_nb=1)), sig(e), range(1, len(e)))
+    chunks = run_stream(ScatterEngine(sig(h), EngineConfig(block_size_nb=nb)), sig(e), range(nb, len(e), nb))
+    assert np.array_equal(per_sample, chunks)
+
+
+def test_engine_zero_skip_matches_core_bit_exact():
+    rng = np.random.default_rng(11)
+    e = np.where(rng.uniform(0, 1, 200) < 0.3, 0.0, rng.uniform(-1, 1, 200))
+    h = rng.uniform(-1, 1, 12)
+    for threshold in (0.0, 1e-3, 0.2):
+        eng = ScatterEngine(sig(h), EngineConfig(zero_skip_threshold=threshold))
+        got = run_stream(eng, sig(e), (50, 130))
+        want = scatter_convolve_skip_zeros(sig(e), sig(h), threshold).concatenated().samples
+        assert np.array_equal(got, want)
+
+
+def test_residue_conservation():
+    rng = np.random.default_rng(23)
+    e = rng.uniform(-1, 1, 20)
+    h = sig(rng.uniform(-1, 1, 6))
+    eng = ScatterEngine(h)
+    emitted = []
+    for k in range(len(e)):
+        emitted.append(eng.process_sample(e[k]))
+        pending = eng._schedule_order()[: len(h) - 1]
+        want = scatter_convolve(sig(e[: k + 1]), h).concatenated().samples
+        assert np.array_equal(np.concatenate([emitted, pending]), want)
+
+
+def test_swap_examples():
+    eng = ScatterEngine(sig([1.0, 1.0]))
+    out = [eng.process_sample(1.0), eng.process_sample(0.0)]
+    eng.swap_ir(sig([5.0, 5.0]))
+    out += [eng.process_sample(0.0), eng.process_sample(0.0), eng.process_sample(1.0)]
+    assert out == [1.0, 1.0, 0.0, 0.0, 5.0]
+    assert np.array_equal(eng.flush().samples, [5.0])
+    h1 = sig([1.0, 2.0, 3.0, 4.0, 5.0, 6.0])
+    eng = ScatterEngine(h1)
+    out = [eng.process_sample(1.0)]
+    eng.swap_ir(sig([9.0, 9.0]))
+    out.append(eng.process_sample(0.0))
+    assert out == [1.0, 2.0] and np.array_equal(eng.flush().samples, [3.0, 4.0, 5.0, 6.0])
+
+
+@pytest.mark.parametrize("nh1,nh2", [(3, 8), (8, 3), (5, 5), (1, 6), (6, 1)])
+def test_swap_grow_and_shrink_match_oracle_engine(nh1, nh2):
+    rng = np.random.default_rng(nh1 * 100 + nh2)
+    e = rng.uniform(-1, 1, 30)
+    h1, h2 = rng.uniform(-1, 1, nh1), rng.uniform(-1, 1, nh2)
+    k = 11
+    eng = ScatterEngine(sig(h1))
+    ref = O.OracleEngine(h1)
+    got = [eng.process_block(sig(e[:k])).samples]
+    want = [ref.process_block(e[:k])]
+    eng.swap_ir(sig(h2))
+    ref.swap_ir(h2)
+    got += [eng.process_block(sig(e[k:])).samples, eng.flush().samples]
+    want += [ref.process_block(e[k:]), ref.flush()]
+    assert np.array_equal(np.concatenate(got), np.concatenate(want))
+
+
+def test_deferred_swap_applies_at_next_block():
+    rng = np.random.default_rng(41)
+    e = rng.uniform(-1, 1, 24)
+    h1, h2 = sig(rng.uniform(-1, 1, 5)), sig(rng.uniform(-1, 1, 5))
+    imm = ScatterEngine(h1)
+    a = imm.process_block(sig(e[:12])).samples
+    imm.swap_ir(h2)
+    want = np.concatenate([a, imm.process_block(sig(e[12:])).samples, imm.flush().samples])
+    d = ScatterEngine(h1)
+    a = d.process_block(sig(e[:12])).samples
+    d.swap_ir_at_next_block(h2)
+    assert np.array_equal(d.current_ir.samples, h1.samples)
+    got = np.concatenate([a, d.process_block(sig(e[12:])).samples, d.flush().samples])
+    assert np.array_equal(got, want)
+
+
+def test_render_policies():
+    eng = ScatterEngine(sig([3.0, 4.0]), EngineConfig(block_size_nb=1))
+    assert np.array_equal(eng.render(sig([1.0, 2.0])).samples, [3.0, 10.0])
+    assert np.array_equal(eng.flush().samples, [8.0])
+    rng = np.random.default_rng(43)
+    e, h = sig(rng.uniform(-1, 1, 100)), sig(rng.uniform(-1, 1, 7))
+    eng = ScatterEngine(h, EngineConfig(block_size_nb=32, tail_policy="auto-append"))
+    assert np.array_equal(eng.render(e).samples, scatter_convolve(e, h).concatenated().samples)
+
+
+# ---------------------------------------------------------------- float32 and device-side
+
+
+def test_f32_engine_block_invariance_and_ordered_batch():
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, 5000).astype(np.float32)
+    h = rng.standard_normal(700).astype(np.float32)
+    outs = []
+    for nb in (1, 37, 256, 4096, 5000):
+        eng = ScatterEngine(Signal(h), EngineConfig(block_size_nb=nb))
+        outs.append(run_stream(eng, Signal(x), range(nb, len(x), nb)))
+    for o in outs[1:]:
+        assert o.dtype == np.float32 and np.array_equal(o, outs[0])
+    batch = scatter_convolve(Signal(x), Signal(h), mode="ordered").concatenated().samples
+    assert np.array_equal(outs[0], batch)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_process_stream_equals_sequential_calls(dtype):
+    import torch
+
+    rng = np.random.default_rng(8)
+    x = rng.uniform(-1, 1, 3000).astype(dtype)
+    irs = [rng.standard_normal(n).astype(dtype) for n in (200, 200, 350, 90)]
+    nb = 128
+    swaps = [(5, irs[1]), (9, irs[2]), (17, irs[3])]
+    seq = ScatterEngine(Signal(irs[0]), EngineConfig(block_size_nb=nb))
+    pieces = []
+    for b, s in enumerate(range(0, len(x), nb)):
+        for sb, ir in swaps:
+            if sb == b:
+                seq.swap_ir(Signal(ir))
+        pieces.append(seq.process_block(Signal(x[s:s + nb])).samples)
+    want = np.concatenate(pieces + [seq.flush().samples])
+    dev = ScatterEngine(Signal(irs[0]), EngineConfig(block_size_nb=nb))
+    body = dev.process_stream(torch.from_numpy(x).cuda(), nb, swaps)
+    got = np.concatenate([body.cpu().numpy(), dev.flush().samples])
+    assert np.array_equal(got, want)
+    # the oracle engine agrees (float64 only: same arithmetic)
+    if dtype == np.float64:
+        ref = O.OracleEngine(irs[0], block_size_nb=nb)
+        rp = []
+        for b, s in enumerate(range(0, len(x), nb)):
+            for sb, ir in swaps:
+                if sb == b:
+                    ref.swap_ir(ir)
+            rp.append(ref.process_block(x[s:s + nb]))
+        assert np.array_equal(got, np.concatenate(rp + [ref.flush()]))
+
+
+def test_c_abi_deferred_swap_and_state():
+    import torch
+
+    L = N.lib()
+    h1 = torch.tensor([1.0, 2.0, 3.0], dtype=torch.float64, device="cuda")
+    h2 = torch.tensor([10.0], dtype=torch.float64, device="cuda")
+    eng = ctypes.c_void_p()
+    N.check(L.sc_engine_create(N.SC_F64, N.ptr(h1), 3, 8, 0.0, N.stream_ptr(), ctypes.byref(eng)))
+    try:
+        x = torch.tensor([1.0, 0.0], dtype=torch.float64, device="cuda")
+        out = torch.empty(2, dtype=torch.float64, device="cuda")
+        N.check(L.sc_engine_swap_ir_at_next_block(eng, N.ptr(h2), 1))
+        N.check(L.sc_engine_process_block(eng, N.ptr(x), 2, N.ptr(out)))  # swap applies first
+        assert out.tolist() == [10.0, 0.0]
+        vals = [ctypes.c_int64() for _ in range(5)]
+        pend = ctypes.c_int()
+        N.check(L.sc_engine_state(eng, *[ctypes.byref(v) for v in vals], ctypes.byref(pend)))
+        ri, live, cap, cons, nh = (v.value for v in vals)
+        assert (cap, nh, cons, pend.value) == (3, 1, 2, 0)
+        big = torch.zeros(20, dtype=torch.float64, device="cuda")
+        with pytest.raises(ValueError, match="exceeds block_size_nb"):
+            N.check(L.sc_engine_process_block(eng, N.ptr(big), 20, N.ptr(big)))
+    finally:
+        L.sc_engine_destroy(eng)
+
+
+def test_literal_scatter_block_matches_oracle():
+    rng = np.random.default_rng(12)
+    for _ in range(40):
+        cap = int(rng.integers(1, 40))
+        nh = int(rng.integers(1, cap + 1))
+        ring = rng.uniform(-1, 1, cap)
+        ir = rng.uniform(-1, 1, nh)
+        block = rng.uniform(-1, 1, int(rng.integers(0, 90)))
+        block[rng.uniform(0, 1, len(block)) < 0.3] = 0.0
+        ri0, live0 = int(rng.integers(0, cap)), int(rng.integers(0, cap + 1))
+        thr = 0.0 if rng.uniform() < 0.5 else 0.3
+        r1, o1 = ring.copy(), np.empty(len(block))
+        r2, o2 = ring.copy(), np.empty(len(block))
+        got = _kernels.scatter_block(r1, ir, block, o1, ri0, live0, thr)
+        want = O.scatter_block(r2, ir, block, o2, ri0, live0, thr)
+        assert got == want
+        assert np.array_equal(r1, r2) and np.array_equal(o1, o2)
+    _kernels.warm_up()
