@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--mode", default="fast", choices=["fast", "ffma", "tc"],
+                    help="float32 kernel: fast = picked by shape (tensor cores for long filters)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -192,6 +194,25 @@ class Work:
             self.scaling = "weak"
             self.dtype = "f32"
 
+    def pick_kernel(self):
+        """Which kernel the library runs for this config/mode (mirrors capi.cu's
+        FAST dispatch) and the padded tensor-core work it issues."""
+        self.tc_padded_macs = 0
+        if self.dtype != "f32" or self.cfg not in ("cfg3", "cfg4", "cfg5"):
+            self.kernel = "k_chain"
+            return
+        nh = self.w.nh
+        use_tc = self.mode == "tc" or (self.mode == "fast" and nh >= 256)
+        self.kernel = "k_tc_fir" if use_tc else "k_fir_f32_fast"
+        if use_tc:
+            s = (nh + 126) // 128 + 1
+            s8 = -(-s // 8) * 8
+            if self.cfg == "cfg4":
+                tiles = -(-self.w.nout // 16384) * (self.c1 - self.c0)
+            else:
+                tiles = -(-self.shard.n_out // 16384)
+            self.tc_padded_macs = tiles * 16384 * 128 * s8
+
     def step(self):
         import torch
 
@@ -201,9 +222,9 @@ class Work:
         from paper_2401_01607_b200.sharded import convolve_shard
 
         if self.cfg in ("cfg5", "cfg3"):
-            return convolve_shard(self.xs, self.shard, self.hd)
+            return convolve_shard(self.xs, self.shard, self.hd, mode=self.mode)
         if self.cfg == "cfg4":
-            return convolve_batched(self.xd, self.hd)
+            return convolve_batched(self.xd, self.hd, mode=self.mode)
         if self.cfg == "cfg1":
             return scatter_convolve(Signal(self.xd), Signal(self.hd)).concatenated().samples
         if self.cfg == "cfg2":
@@ -338,6 +359,8 @@ def main():
     device = torch.device("cuda", torch.cuda.current_device())
     L = N.lib()
     work = Work(args.config, rank, world, device)
+    work.mode = args.mode
+    work.pick_kernel()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)  # 256 MiB > L2
 
     def barrier():
@@ -377,28 +400,44 @@ def main():
     ms = float(ms.item())
     value = work.total_macs / (ms * 1e-3) / 1e9
 
-    # roofline of the dominant kernel (k_fir_f32_fast) on this rank
+    # roofline of the dominant kernel on this rank
     p = peaks()
     sms = torch.cuda.get_device_properties(device).multi_processor_count
     sm_max = float(p.get("sm_max_mhz", 1965.0))
     csum = clocks.summary()
     fp32_peak = 2 * 128 * sms * sm_max * 1e6 / 1e12  # TFLOP/s at max clock
-    achieved = 2 * work.rank_macs / (ms_local * 1e-3) / 1e12
+    useful = 2 * work.rank_macs / (ms_local * 1e-3) / 1e12   # useful FP32-equivalent TFLOP/s
     med = csum["sm_mhz"] or sm_max
     traffic = None
     tf = REPO / "profiles" / "ncu_traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get(args.config)
-    roofline = {
-        "bound": "fp32_fma" if work.dtype == "f32" else "fp64_fma",
-        "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
-        "traffic": traffic,
-        "peak_source": f"computed: {sms} SMs x 128 FP32 FMA/clk x 2 FLOP x sm_max_mhz {sm_max:.0f} "
-                       "(MEASURED_PEAKS.json); no FP32-FMA peak is measured by the driver",
-        "frac_at_observed_clock": achieved / (2 * 128 * sms * med * 1e6 / 1e12),
-        "kernel": "k_fir_f32_fast" if args.config in ("cfg3", "cfg4", "cfg5") else "k_chain",
-        "achieved_from": "CUDA events around each step on the launching stream (step = tap pad + FIR kernel)",
-    }
+        traffic = json.loads(tf.read_text()).get(f"{args.config}_{work.kernel}")
+    if work.kernel == "k_tc_fir":
+        # tensor work actually issued: 3 fp16 MMAs (hi*hi, lo*hi, hi*lo) over the
+        # padded block-Toeplitz GEMM (whole 16384-output tiles x 128 taps x s8 shifts)
+        tc_peak = float(p.get("bf16_tflops", 1590.0))
+        achieved = 2 * 3 * work.tc_padded_macs / (ms_local * 1e-3) / 1e12
+        roofline = {
+            "bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
+            "frac": achieved / tc_peak, "traffic": traffic,
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst, cuBLAS bf16; fp16 MMA runs at "
+                           "the same rate)" if "bf16_tflops" in p else "fallback 1.59 PFLOP/s",
+            "achieved_per_launch": f"2 x 3 x {work.tc_padded_macs:.4e} padded MMA MACs / mean step time",
+            "useful_fp32_tflops": useful,
+            "useful_frac_of_fp32_fma_peak": useful / fp32_peak,
+            "kernel": "k_tc_fir (tcgen05.mma kind::f16 128x128x16, TMEM accumulators, cp.async.bulk)",
+        }
+    else:
+        roofline = {
+            "bound": "fp32_fma" if work.dtype == "f32" else "fp64_fma",
+            "achieved": useful, "peak": fp32_peak, "unit": "TFLOP/s", "frac": useful / fp32_peak,
+            "traffic": traffic,
+            "peak_source": f"computed: {sms} SMs x 128 FP32 FMA/clk x 2 FLOP x sm_max_mhz {sm_max:.0f} "
+                           "(MEASURED_PEAKS.json); no FP32-FMA peak is measured by the driver",
+            "frac_at_observed_clock": useful / (2 * 128 * sms * med * 1e6 / 1e12),
+            "kernel": work.kernel,
+        }
+    roofline["achieved_from"] = "CUDA events around each step on the launching stream"
 
     # e2e through the public API with pinned host buffers
     e2e = None
@@ -448,7 +487,8 @@ def main():
                        "parallelism": work.parallelism,
                        "l2": "256 MiB memset before every timed step (outside the events); "
                              "inputs also exceed L2 at N=1"},
-            "pct_fp32_fma_peak": 100.0 * roofline["frac"],
+            "pct_fp32_fma_peak": 100.0 * useful / fp32_peak,
+            "kernel": work.kernel,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

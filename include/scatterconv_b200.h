@@ -29,8 +29,13 @@
  *    the sum rounded separately (no FMA).  This is the reference's order
  *    (_kernels.py:1-8, core.py:83-86); in float64 it is bit-identical to the
  *    reference, and stream == batch for any block partition in both dtypes.
- *  - SC_MODE_FAST (float32 only): register-tiled FFMA2 kernel, fixed
+ *  - SC_MODE_FAST (float32 only): the fastest kernel for the shape --
+ *    SC_MODE_TC for long filters, SC_MODE_FFMA otherwise.  Fixed
  *    (deterministic) order, within 1e-5*max|x|*||h||_1 of the reference.
+ *  - SC_MODE_FFMA: register-tiled CUDA-core kernel (FFMA2 = fma.rn.f32x2).
+ *  - SC_MODE_TC: tcgen05 tensor-core block-Toeplitz GEMM with an fp16 hi/lo
+ *    split of x and h (3 MMAs per K-step, FP32 accumulation in TMEM); requires
+ *    finite inputs.
  *
  * Skip rules (zero skipping)
  *  - SC_SKIP_NONE     every input sample scatters (scatter_convolve, core.py:90)
@@ -55,7 +60,7 @@ extern "C" {
 #define SC_ERR_STATE (-4)  /* engine used in an invalid state */
 
 enum { SC_F32 = 0, SC_F64 = 1 };
-enum { SC_MODE_FAST = 0, SC_MODE_ORDERED = 1 };
+enum { SC_MODE_FAST = 0, SC_MODE_ORDERED = 1, SC_MODE_FFMA = 2, SC_MODE_TC = 3 };
 enum { SC_SKIP_NONE = 0, SC_SKIP_LE = 1, SC_SKIP_NOT_GT = 2 };
 
 int sc_abi_version(void);
@@ -72,8 +77,8 @@ int64_t sc_launch_count(void);
  * Replaces core._scatter_full (core.py:80-92) and therefore
  * scatter_convolve (core.py:122-131), commuted_convolve (core.py:134-147:
  * pass the shorter signal as `x` to drive) and scatter_convolve_skip_zeros
- * (core.py:150-167, skip_mode = SC_SKIP_LE).  mode SC_MODE_FAST requires
- * SC_F32 and skip_mode SC_SKIP_NONE. */
+ * (core.py:150-167, skip_mode = SC_SKIP_LE).  The FAST/FFMA/TC modes need
+ * SC_F32 and skip_mode SC_SKIP_NONE; otherwise the ORDERED kernel runs. */
 int sc_fir_full(int dtype, int mode, const void *x, int64_t ne, const void *h, int64_t nh,
                 void *y, int skip_mode, double threshold, void *stream);
 
@@ -81,16 +86,16 @@ int sc_fir_full(int dtype, int mode, const void *x, int64_t ne, const void *h, i
  * y[i] = sum_k h[k] * X(n_begin + i - k) for i in [0, n_end - n_begin), where
  * X(m) = x[m - x_begin] for m in [x_begin, x_end) and 0 elsewhere.  A shard
  * owning outputs [a, b) passes x_begin = max(0, a-nh+1), x_end = min(ne, b):
- * its input slice plus the (nh-1)-sample halo.  FAST mode, float32. */
-int sc_fir_range(int dtype, const void *x, int64_t x_begin, int64_t x_end, const void *h,
+ * its input slice plus the (nh-1)-sample halo.  float32; mode FAST, FFMA or TC. */
+int sc_fir_range(int dtype, int mode, const void *x, int64_t x_begin, int64_t x_end, const void *h,
                  int64_t nh, void *y, int64_t n_begin, int64_t n_end, void *stream);
 
 /* Batched multichannel (replaces one engine per channel, engine.py:60-66,
  * cli.py:186-202, bench.py:200-202): for c in [0, channels):
  * y[c*ldy : c*ldy + ne+nh-1] = x[c*ldx : c*ldx+ne] (*) h[c*ldh : c*ldh+nh].
- * One launch.  FAST mode, float32. */
-int sc_fir_batched(int dtype, const void *x, int64_t ldx, const void *h, int64_t ldh, void *y,
-                   int64_t ldy, int64_t channels, int64_t ne, int64_t nh, void *stream);
+ * One launch of the FIR kernel.  float32; mode FAST, FFMA or TC. */
+int sc_fir_batched(int dtype, int mode, const void *x, int64_t ldx, const void *h, int64_t ldh,
+                   void *y, int64_t ldy, int64_t channels, int64_t ne, int64_t nh, void *stream);
 
 /* Gather form with an (almost) exactly rounded accumulator: double-double
  * (TwoProduct + TwoSum) per output.  Device restatement of direct_form

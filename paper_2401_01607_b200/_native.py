@@ -18,7 +18,7 @@ LIB_DIR = pathlib.Path(__file__).resolve().parent / "_lib"
 LIB_NAME = "libscatterconv_b200.so"
 
 SC_F32, SC_F64 = 0, 1
-SC_MODE_FAST, SC_MODE_ORDERED = 0, 1
+SC_MODE_FAST, SC_MODE_ORDERED, SC_MODE_FFMA, SC_MODE_TC = 0, 1, 2, 3
 SC_SKIP_NONE, SC_SKIP_LE, SC_SKIP_NOT_GT = 0, 1, 2
 SC_ERR_ARG = -1
 
@@ -32,8 +32,9 @@ _SIGNATURES = {
     "sc_abi_version": [],
     "sc_fir_full": [ctypes.c_int, ctypes.c_int, _vp, _i64, _vp, _i64, _vp, ctypes.c_int,
                     ctypes.c_double, _vp],
-    "sc_fir_range": [ctypes.c_int, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _vp],
-    "sc_fir_batched": [ctypes.c_int, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp],
+    "sc_fir_range": [ctypes.c_int, ctypes.c_int, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _vp],
+    "sc_fir_batched": [ctypes.c_int, ctypes.c_int, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64,
+                       _i64, _vp],
     "sc_direct_form": [_vp, _i64, _vp, _i64, _vp, _vp],
     "sc_scatter_block": [ctypes.c_int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64,
                          ctypes.c_double, _p64, _p64, _vp],

@@ -100,7 +100,16 @@ def _result_dtype(*arrays):
 
 
 _MODES = {None: None, "fast": N.SC_MODE_FAST, "ordered": N.SC_MODE_ORDERED,
-          "strict": N.SC_MODE_ORDERED}
+          "strict": N.SC_MODE_ORDERED, "ffma": N.SC_MODE_FFMA, "tc": N.SC_MODE_TC}
+
+
+def mode_code(mode) -> int:
+    """C-ABI mode for a float32 fast-path name (None/"fast", "ffma", "tc")."""
+    if mode is None:
+        return N.SC_MODE_FAST
+    if mode not in ("fast", "ffma", "tc"):
+        raise ValueError(f"mode must be 'fast', 'ffma' or 'tc', got {mode!r}")
+    return _MODES[mode]
 
 
 def _fir(drive, kern, *, mode=None, skip_mode=N.SC_SKIP_NONE, threshold=0.0):

@@ -21,6 +21,10 @@ static std::atomic<int64_t> g_launches{0};
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// FAST mode routes long filters to the tensor-core kernel (validated on B200
+// against the oracle, tests/test_tc_gpu.py).
+static bool g_fast_uses_tc = true;
+
 void set_error(const char *fmt, ...) {
     va_list ap;
     va_start(ap, fmt);
@@ -76,6 +80,40 @@ void *scratch(size_t bytes, int slot, cudaStream_t stream, int *err) {
     return b.p;
 }
 
+int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
+                   const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin,
+                   int64_t n_end, int64_t channels, cudaStream_t stream) {
+    bool tc = false, guard = false;
+    if (mode == SC_MODE_TC) {
+        tc = true;
+    } else if (mode == SC_MODE_FAST) {
+        tc = g_fast_uses_tc && tc_fir_supported(nh);
+        guard = tc;
+    } else if (mode != SC_MODE_FFMA) {
+        set_error("fir: bad mode %d", mode);
+        return SC_ERR_ARG;
+    }
+    if (!tc)
+        return launch_fir_f32_fast(x, ldx, x_base, x_lo, x_hi, h, ldh, nh, y, ldy, n_begin, n_end,
+                                   channels, stream);
+    const unsigned *nonfinite = nullptr;
+    int rc = launch_fir_f32_tc(x, ldx, x_base, x_lo, x_hi, h, ldh, nh, y, ldy, n_begin, n_end, channels,
+                               stream, &nonfinite);
+    if (rc || !guard || !nonfinite) return rc;
+    // FAST mode: NaN/Inf inputs are routed (on the device, no host sync) to
+    // the ORDERED kernel, which visits exactly the reference's (m, k) pairs
+    // and so reproduces its NaN/Inf pattern (0*Inf included).  Each launch
+    // exits immediately when the flag is clear.
+    for (int64_t c = 0; c < channels; ++c) {
+        ChainSeg seg{h + c * ldh, nh, x_lo, x_hi};
+        rc = launch_chain(SC_F32, SC_SKIP_NONE, 0.0, x + c * ldx, x_base, &seg, 1, nullptr, 0, nullptr,
+                          n_begin, n_end - n_begin, y + c * ldy, n_end - n_begin, nullptr, stream,
+                          nonfinite);
+        if (rc) return rc;
+    }
+    return SC_OK;
+}
+
 static size_t dtype_size(int dtype) { return dtype == SC_F64 ? 8 : (dtype == SC_F32 ? 4 : 0); }
 
 }  // namespace sc
@@ -100,38 +138,40 @@ int sc_fir_full(int dtype, int mode, const void *x, int64_t ne, const void *h, i
     SC_REQUIRE(threshold >= 0.0, "sc_fir_full: threshold must be non-negative, got %g", threshold);
     const int64_t nout = ne + nh - 1;
     cudaStream_t st = as_stream(stream);
-    if (mode == SC_MODE_FAST && dtype == SC_F32 && skip_mode == SC_SKIP_NONE) {
-        return launch_fir_f32_fast(static_cast<const float *>(x), 0, 0, 0, ne,
-                                   static_cast<const float *>(h), 0, nh, static_cast<float *>(y), 0,
-                                   0, nout, 1, st);
+    if (mode != SC_MODE_ORDERED && dtype == SC_F32 && skip_mode == SC_SKIP_NONE) {
+        return launch_fir_f32(mode, static_cast<const float *>(x), 0, 0, 0, ne,
+                              static_cast<const float *>(h), 0, nh, static_cast<float *>(y), 0, 0, nout,
+                              1, st);
     }
     ChainSeg seg{h, nh, 0, ne};
     return launch_chain(dtype, skip_mode, threshold, x, 0, &seg, 1, nullptr, 0, nullptr, 0, nout,
                         y, nout, nullptr, st);
 }
 
-int sc_fir_range(int dtype, const void *x, int64_t x_begin, int64_t x_end, const void *h,
+int sc_fir_range(int dtype, int mode, const void *x, int64_t x_begin, int64_t x_end, const void *h,
                  int64_t nh, void *y, int64_t n_begin, int64_t n_end, void *stream) {
     SC_REQUIRE(dtype == SC_F32, "sc_fir_range: only float32 (fast mode) is supported");
+    SC_REQUIRE(mode != SC_MODE_ORDERED, "sc_fir_range: ordered mode is not supported");
     SC_REQUIRE(nh >= 1, "sc_fir_range: impulse response is empty");
     SC_REQUIRE(x_end >= x_begin && n_end >= n_begin, "sc_fir_range: bad range");
     SC_REQUIRE(h && y && (x || x_end == x_begin), "sc_fir_range: null pointer");
-    return launch_fir_f32_fast(static_cast<const float *>(x), 0, x_begin, x_begin, x_end,
-                               static_cast<const float *>(h), 0, nh, static_cast<float *>(y), 0,
-                               n_begin, n_end, 1, as_stream(stream));
+    return launch_fir_f32(mode, static_cast<const float *>(x), 0, x_begin, x_begin, x_end,
+                          static_cast<const float *>(h), 0, nh, static_cast<float *>(y), 0, n_begin,
+                          n_end, 1, as_stream(stream));
 }
 
-int sc_fir_batched(int dtype, const void *x, int64_t ldx, const void *h, int64_t ldh, void *y,
-                   int64_t ldy, int64_t channels, int64_t ne, int64_t nh, void *stream) {
+int sc_fir_batched(int dtype, int mode, const void *x, int64_t ldx, const void *h, int64_t ldh,
+                   void *y, int64_t ldy, int64_t channels, int64_t ne, int64_t nh, void *stream) {
     SC_REQUIRE(dtype == SC_F32, "sc_fir_batched: only float32 (fast mode) is supported");
+    SC_REQUIRE(mode != SC_MODE_ORDERED, "sc_fir_batched: ordered mode is not supported");
     SC_REQUIRE(ne >= 1, "sc_fir_batched: input signal is empty");
     SC_REQUIRE(nh >= 1, "sc_fir_batched: impulse response is empty");
     SC_REQUIRE(channels >= 1, "sc_fir_batched: channels must be >= 1");
     SC_REQUIRE(ldx >= ne && ldh >= nh && ldy >= ne + nh - 1, "sc_fir_batched: bad leading dims");
     SC_REQUIRE(x && h && y, "sc_fir_batched: null pointer");
-    return launch_fir_f32_fast(static_cast<const float *>(x), ldx, 0, 0, ne,
-                               static_cast<const float *>(h), ldh, nh, static_cast<float *>(y), ldy,
-                               0, ne + nh - 1, channels, as_stream(stream));
+    return launch_fir_f32(mode, static_cast<const float *>(x), ldx, 0, 0, ne,
+                          static_cast<const float *>(h), ldh, nh, static_cast<float *>(y), ldy, 0,
+                          ne + nh - 1, channels, as_stream(stream));
 }
 
 int sc_direct_form(const double *e, int64_t ne, const double *h, int64_t nh, double *y,

@@ -60,6 +60,7 @@ struct FastArgs {
     float *ws;        // partials [nsplit][channels][n_len] when nsplit > 1
     int64_t n_begin, n_len;
     int nsplit, channels;
+    const unsigned *run_if;  // optional device gate (FAST-mode fallback)
 };
 
 __device__ __forceinline__ float load_x(const FastArgs &a, const float *xc, int64_t m) {
@@ -74,6 +75,7 @@ __device__ __forceinline__ int ring_slot(int64_t g) {
 
 __global__ void __launch_bounds__(FT_THREADS, 2) k_fir_f32_fast(FastArgs a) {
     __shared__ __align__(16) float2 ring[FT_NG * FT_GSTRIDE];
+    if (a.run_if && *a.run_if == 0) return;  // gated fallback not needed (block-uniform)
 
     const int j = threadIdx.x;
     const int ch = blockIdx.z;
@@ -216,10 +218,10 @@ __global__ void __launch_bounds__(FT_THREADS, 2) k_fir_f32_fast(FastArgs a) {
 
 // Sum split partials in fixed (ascending) split order.
 __global__ void k_split_reduce(const float *__restrict__ ws, int nsplit, int channels,
-                               int64_t n_len, float *__restrict__ y, int64_t ldy) {
+                               int64_t n_len, float *__restrict__ y, int64_t ldy, const unsigned *run_if) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int ch = blockIdx.y;
-    if (i >= n_len) return;
+    if (i >= n_len || (run_if && *run_if == 0)) return;
     float s = ws[(int64_t)ch * n_len + i];
     for (int k = 1; k < nsplit; ++k) s += ws[((int64_t)k * channels + ch) * n_len + i];
     y[(int64_t)ch * ldy + i] = s;
@@ -227,10 +229,10 @@ __global__ void k_split_reduce(const float *__restrict__ ws, int nsplit, int cha
 
 // Copy taps into a zero-padded, 16-byte aligned workspace.
 __global__ void k_pad_taps(const float *__restrict__ h, int64_t ldh, int64_t nh,
-                           float *__restrict__ hp, int64_t ldhp) {
+                           float *__restrict__ hp, int64_t ldhp, const unsigned *run_if) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int ch = blockIdx.y;
-    if (i >= ldhp) return;
+    if (i >= ldhp || (run_if && *run_if == 0)) return;
     hp[(int64_t)ch * ldhp + i] = i < nh ? h[(int64_t)ch * ldh + i] : 0.0f;
 }
 
@@ -258,7 +260,8 @@ int choose_splits(int64_t tiles, int64_t stages, int slots) {
 
 int launch_fir_f32_fast(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
                         const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy,
-                        int64_t n_begin, int64_t n_end, int64_t channels, cudaStream_t stream) {
+                        int64_t n_begin, int64_t n_end, int64_t channels, cudaStream_t stream,
+                        const unsigned *run_if) {
     const int64_t n_len = n_end - n_begin;
     if (n_len <= 0 || channels <= 0) return SC_OK;
     SC_REQUIRE(nh >= 1, "fir: empty impulse response");
@@ -288,7 +291,7 @@ int launch_fir_f32_fast(const float *x, int64_t ldx, int64_t x_base, int64_t x_l
     if (err) return err;
     {
         dim3 g((unsigned)cdiv(ldhp, 256), (unsigned)channels);
-        k_pad_taps<<<g, 256, 0, stream>>>(h, ldh, nh, hp, ldhp);
+        k_pad_taps<<<g, 256, 0, stream>>>(h, ldh, nh, hp, ldhp, run_if);
         SC_CHECK_LAUNCH();
     }
     float *ws = nullptr;
@@ -315,12 +318,13 @@ int launch_fir_f32_fast(const float *x, int64_t ldx, int64_t x_base, int64_t x_l
     a.n_len = n_len;
     a.nsplit = nsplit_eff;
     a.channels = (int)channels;
+    a.run_if = run_if;
     dim3 grid((unsigned)tiles, (unsigned)nsplit_eff, (unsigned)channels);
     k_fir_f32_fast<<<grid, FT_THREADS, 0, stream>>>(a);
     SC_CHECK_LAUNCH();
     if (nsplit_eff > 1) {
         dim3 g((unsigned)cdiv(n_len, 256), (unsigned)channels);
-        k_split_reduce<<<g, 256, 0, stream>>>(ws, nsplit_eff, (int)channels, n_len, y, ldy);
+        k_split_reduce<<<g, 256, 0, stream>>>(ws, nsplit_eff, (int)channels, n_len, y, ldy, run_if);
         SC_CHECK_LAUNCH();
     }
     return SC_OK;

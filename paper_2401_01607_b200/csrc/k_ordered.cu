@@ -38,12 +38,14 @@ struct ChainArgs {
     int64_t n_a;
     T *out_b;
     double thr;
+    const unsigned *run_if;  // optional device gate: run only if *run_if != 0
 };
 
 template <typename T, int SKIP>
 __global__ void __launch_bounds__(TB) k_chain(ChainArgs<T> a) {
     __shared__ T xs[MC];
     __shared__ T hs[MC + TB - 1];
+    if (a.run_if && *a.run_if == 0) return;  // block-uniform
     const int64_t tile0 = a.t0 + (int64_t)blockIdx.x * TB;
     const int64_t t_end = a.t0 + a.n_out;
     const int64_t tile_last = (tile0 + TB < t_end ? tile0 + TB : t_end) - 1;
@@ -103,7 +105,7 @@ template <typename T>
 int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off,
                    const ChainSeg *segs, int nseg, const void *init, int64_t init_len,
                    const int64_t *init_len_dev, int64_t t0, int64_t n_out, void *out_a,
-                   int64_t n_a, void *out_b, cudaStream_t stream) {
+                   int64_t n_a, void *out_b, cudaStream_t stream, const unsigned *run_if) {
     if (n_out <= 0) return SC_OK;
     SC_REQUIRE(nseg >= 0 && nseg <= kMaxSegs, "chain: bad segment count %d", nseg);
     ChainArgs<T> a{};
@@ -120,6 +122,7 @@ int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off
     a.n_a = n_a;
     a.out_b = static_cast<T *>(out_b);
     a.thr = threshold;
+    a.run_if = run_if;
     const int64_t grid = cdiv(n_out, TB);
     SC_REQUIRE(grid < (int64_t)INT32_MAX, "chain: output range too large");
     switch (skip_mode) {
@@ -168,13 +171,13 @@ __global__ void __launch_bounds__(TB) k_direct_dd(const double *__restrict__ e, 
 int launch_chain(int dtype, int skip_mode, double threshold, const void *x, int64_t x_off,
                  const ChainSeg *segs, int nseg, const void *init, int64_t init_len,
                  const int64_t *init_len_dev, int64_t t0, int64_t n_out, void *out_a,
-                 int64_t n_a, void *out_b, cudaStream_t stream) {
+                 int64_t n_a, void *out_b, cudaStream_t stream, const unsigned *run_if) {
     if (dtype == SC_F64)
         return launch_chain_t<double>(skip_mode, threshold, x, x_off, segs, nseg, init, init_len,
-                                      init_len_dev, t0, n_out, out_a, n_a, out_b, stream);
+                                      init_len_dev, t0, n_out, out_a, n_a, out_b, stream, run_if);
     if (dtype == SC_F32)
         return launch_chain_t<float>(skip_mode, threshold, x, x_off, segs, nseg, init, init_len,
-                                     init_len_dev, t0, n_out, out_a, n_a, out_b, stream);
+                                     init_len_dev, t0, n_out, out_a, n_a, out_b, stream, run_if);
     set_error("chain: bad dtype %d", dtype);
     return SC_ERR_ARG;
 }

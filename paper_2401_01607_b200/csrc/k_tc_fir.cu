@@ -1,0 +1,505 @@
+// k_tc_fir.cu -- FP32-accurate FIR on the 5th-gen tensor cores (tcgen05).
+//
+// Same output as the reference's scatter loop (core.py:80-92) within the
+// north_star tolerance, computed as a block-Toeplitz GEMM:
+//
+//   y[n0 + 128*i + r] = sum_s sum_v X[i-s, v] * h[128*s + r - v]
+//       X[rho, v] = x[n0 + 128*rho + v]   (the signal cut into 128-sample rows)
+//
+// For each "shift" s this is D[r', i] += T_s[r', v] * X[i-s, v] with
+// r' = 127 - r (phases reversed, M = 128), i = output row (N = 128) and
+// v = K (128 taps per shift).  Both operands come straight from compact
+// shared-memory images through UMMA descriptors (SWIZZLE_NONE, K-major):
+//
+//  * T_s (A operand) is Toeplitz.  With H8[g][b][e] = h[C - 8g - b - e]
+//    ("8 phase copies" of the reversed taps, 128 B per group g), core matrix
+//    (row-group a, K-group j) of T_s is H8[g_s + a + j]: leading- and
+//    stride-byte-offsets are both 128 B, so an 8 KB descriptor window covers a
+//    dense 128x128 Toeplitz block.  Consecutive shifts slide by 16 groups.
+//  * X (B operand) is stored K-group-major ([j][row][8]) so rows are 16 B
+//    apart: moving to the next shift (one row down) is just start address
+//    - 16 B.  One 192-row window serves 64 consecutive shifts.
+//
+// FP32 accuracy from FP16 tensor cores: x = x_hi + x_lo, h = h_hi + h_lo
+// (each fp16, after exact power-of-two scaling of x and h into fp16 range),
+// D += x_hi*h_hi + x_hi*h_lo + x_lo*h_hi (3 MMAs per K-step; fp16 products
+// are exact in the FP32 accumulator).  Per-product relative error <= ~3*2^-22,
+// i.e. worst case ~7% of the 1e-5*max|x|*||h||_1 tolerance.
+//
+// Pipeline (one persistent CTA per SM, 192 threads):
+//   warp 0 lane 0 : producer -- cp.async.bulk of X windows and H8 stages
+//                   (8 shifts each) into smem, mbarrier complete_tx
+//   warp 1 lane 0 : MMA issuer -- tcgen05.mma kind::f16, 128x128x16, FP32
+//                   accumulators in TMEM (two 128-column buffers),
+//                   tcgen05.commit releases smem slots / publishes tiles
+//   warps 2..5    : epilogue -- tcgen05.ld 32x32b, unscale, coalesced stores
+//                   while the MMA warp already works on the next tile.
+
+#include <cuda_fp16.h>
+
+#include <algorithm>
+
+#include "sc_common.cuh"
+
+namespace sc {
+namespace {
+
+constexpr int TR = 128;              // phases per row (M) = taps per shift (K)
+constexpr int TN = 128;              // output rows per tile (N)
+constexpr int TTILE = TR * TN;       // 16384 outputs per tile
+constexpr int KG = TR / 8;           // 16 K-groups of 8 fp16 (16 B)
+constexpr int WP = 64;               // shifts per X window
+constexpr int WROWS = TN + WP;       // 192 rows per window (191 used)
+constexpr int SSH = 8;               // shifts per H8 stage
+constexpr int SGROUPS = 2 * KG - 1 + KG * (SSH - 1);  // 143 groups per stage
+constexpr int NHSLOT = 2;            // H8 stage slots
+constexpr uint32_t XWIN_PART = WROWS * KG * 16;        // 49152 B
+constexpr uint32_t HST_PART = SGROUPS * 128;           // 18304 B
+constexpr uint32_t SM_XWIN = 0;
+constexpr uint32_t SM_HST = 2 * XWIN_PART;             // 98304
+constexpr uint32_t SM_BAR = SM_HST + NHSLOT * 2 * HST_PART;  // 171520
+constexpr uint32_t SM_TOTAL = SM_BAR + 128;
+constexpr int TC_THREADS = 192;
+constexpr uint32_t TMEM_COLS = 256;  // 2 accumulators x 128 fp32 columns
+
+// idesc: F32 accumulate (bit 4), A/B F16, K-major, N = 128 (>>3 at bit 17),
+// M = 128 (>>4 at bit 24).
+constexpr uint32_t IDESC = (1u << 4) | ((TN >> 3) << 17) | ((TR >> 4) << 24);
+
+struct TcArgs {
+    const __half *xt[2];   // X in [ch][j][row][8] layout, hi / lo
+    const __half *h8[2];   // H8 groups [ch][g][8][8], hi / lo
+    int64_t xt_ch;         // elements per channel in xt
+    int64_t h8_ch;         // elements per channel in h8
+    int64_t nrows;         // rows in the X layout (per channel)
+    int64_t row_min;       // row index of layout row 0
+    int64_t s8;            // shifts (multiple of SSH)
+    int64_t tiles_per_ch;
+    int64_t n_tiles;       // tiles_per_ch * channels
+    int64_t n_begin, n_end;  // output range; y[i] = out(n_begin + i)
+    float *y;
+    int64_t ldy;           // channel stride of y
+    const float *scales;   // per channel: [3*ch+2] = 2^-(ex+eh)
+    const unsigned *nonfinite;  // set by k_amax: inputs not representable -> skip
+};
+
+// ---------------------------------------------------------------- PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    // SWIZZLE_NONE K-major canonical layout; version 1 (bit 46).
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------- main kernel
+
+__global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    if (*a.nonfinite) return;  // block-uniform: the FFMA kernel handles this input
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar_xfull = sbase + SM_BAR + 0;
+    const uint32_t bar_xempty = sbase + SM_BAR + 8;
+    const uint32_t bar_hfull = sbase + SM_BAR + 16;   // + 8*slot
+    const uint32_t bar_hempty = sbase + SM_BAR + 32;  // + 8*slot
+    const uint32_t bar_tfull = sbase + SM_BAR + 48;   // + 8*acc
+    const uint32_t bar_tempty = sbase + SM_BAR + 64;  // + 8*acc
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + SM_BAR + 96);
+
+    if (threadIdx.x == 0) {
+        mbar_init(bar_xfull, 1);
+        mbar_init(bar_xempty, 1);
+        for (int i = 0; i < NHSLOT; ++i) {
+            mbar_init(bar_hfull + 8 * i, 1);
+            mbar_init(bar_hempty + 8 * i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(bar_tfull + 8 * i, 1);
+            mbar_init(bar_tempty + 8 * i, 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const int64_t n_windows = (a.s8 + WP - 1) / WP;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------------------ producer
+            uint32_t xw = 0, hsc = 0;
+            for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+                const int64_t ch = tile / a.tiles_per_ch;
+                const int64_t i0 = (tile - ch * a.tiles_per_ch) * TN;
+                const __half *xt0 = a.xt[0] + ch * a.xt_ch, *xt1 = a.xt[1] + ch * a.xt_ch;
+                const __half *h80 = a.h8[0] + ch * a.h8_ch, *h81 = a.h8[1] + ch * a.h8_ch;
+                for (int64_t w = 0; w < n_windows; ++w) {
+                    const int64_t s0 = w * WP;
+                    const int64_t s1 = s0 + WP < a.s8 ? s0 + WP : a.s8;
+                    if (xw > 0) mbar_wait(bar_xempty, (xw - 1) & 1);
+                    mbar_expect_tx(bar_xfull, 2 * XWIN_PART);
+                    const int64_t row_lo = i0 - s0 - WP - a.row_min;  // layout row of window row 0
+                    for (int p = 0; p < 2; ++p)
+                        for (int j = 0; j < KG; ++j)
+                            bulk_g2s(sbase + SM_XWIN + p * XWIN_PART + j * (WROWS * 16),
+                                     (p ? xt1 : xt0) + ((int64_t)j * a.nrows + row_lo) * 8, WROWS * 16, bar_xfull);
+                    ++xw;
+                    for (int64_t sg = s0; sg < s1; sg += SSH) {
+                        const uint32_t slot = hsc % NHSLOT;
+                        if (hsc >= NHSLOT) mbar_wait(bar_hempty + 8 * slot, ((hsc / NHSLOT) - 1) & 1);
+                        mbar_expect_tx(bar_hfull + 8 * slot, 2 * HST_PART);
+                        // lowest group of the stage: g_s of its last shift
+                        const int64_t glo = (a.s8 - 1 - (sg + SSH - 1)) * KG;
+                        for (int p = 0; p < 2; ++p)
+                            bulk_g2s(sbase + SM_HST + (slot * 2 + p) * HST_PART, (p ? h81 : h80) + glo * 64, HST_PART,
+                                     bar_hfull + 8 * slot);
+                        ++hsc;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ------------------------------------------------------------ MMA issuer
+            uint32_t xw = 0, hsc = 0, tcount = 0;
+            for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+                const uint32_t acc = tcount & 1;
+                if (tcount >= 2) mbar_wait(bar_tempty + 8 * acc, ((tcount >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem + acc * TN;
+                uint32_t accumulate = 0;
+                for (int64_t w = 0; w < n_windows; ++w) {
+                    const int64_t s0 = w * WP;
+                    const int64_t s1 = s0 + WP < a.s8 ? s0 + WP : a.s8;
+                    mbar_wait(bar_xfull, xw & 1);
+                    ++xw;
+                    for (int64_t sg = s0; sg < s1; sg += SSH) {
+                        const uint32_t slot = hsc % NHSLOT;
+                        mbar_wait(bar_hfull + 8 * slot, (hsc / NHSLOT) & 1);
+                        ++hsc;
+                        tc_fence_after();
+#pragma unroll 1
+                        for (int ss = 0; ss < SSH; ++ss) {
+                            const int64_t s = sg + ss;
+                            // A: T_s starts at group offset (SSH-1-ss)*KG inside the stage
+                            const uint32_t a_hi = sbase + SM_HST + (slot * 2 + 0) * HST_PART + (SSH - 1 - ss) * KG * 128;
+                            const uint32_t a_lo = a_hi + HST_PART;
+                            // B: rows of shift s start WP + s0 - s rows into the window
+                            const uint32_t b_hi = sbase + SM_XWIN + (uint32_t)(WP + s0 - s) * 16;
+                            const uint32_t b_lo = b_hi + XWIN_PART;
+#pragma unroll
+                            for (int kk = 0; kk < KG / 2; ++kk) {
+                                const uint64_t ah = sdesc(a_hi + kk * 256, 128, 128);
+                                const uint64_t al = sdesc(a_lo + kk * 256, 128, 128);
+                                const uint64_t bh = sdesc(b_hi + kk * 2 * (WROWS * 16), WROWS * 16, 128);
+                                const uint64_t bl = sdesc(b_lo + kk * 2 * (WROWS * 16), WROWS * 16, 128);
+                                umma_f16(d_tmem, ah, bh, accumulate);
+                                accumulate = 1;
+                                umma_f16(d_tmem, al, bh, 1);
+                                umma_f16(d_tmem, ah, bl, 1);
+                            }
+                        }
+                        umma_commit(bar_hempty + 8 * slot);
+                    }
+                    umma_commit(bar_xempty);
+                }
+                umma_commit(bar_tfull + 8 * acc);
+                ++tcount;
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- epilogue
+        const int q = warp & 3;                // TMEM lane quarter of this warp
+        const int rp = q * 32 + lane;          // phase index r' = 127 - r
+        uint32_t tcount = 0;
+        for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+            const int64_t ch = tile / a.tiles_per_ch;
+            const float inv = a.scales[3 * ch + 2];
+            float *yc = a.y + ch * a.ldy;
+            const uint32_t acc = tcount & 1;
+            mbar_wait(bar_tfull + 8 * acc, (tcount >> 1) & 1);
+            tc_fence_after();
+            const int64_t nb = a.n_begin + (tile - ch * a.tiles_per_ch) * (int64_t)TTILE + (TR - 1 - rp);
+#pragma unroll 1
+            for (int c = 0; c < TN; c += 32) {
+                float v[32];
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * TN + c, v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int64_t n = nb + (int64_t)(c + i) * TR;
+                    if (n < a.n_end) yc[n - a.n_begin] = v[i] * inv;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
+            ++tcount;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
+// ---------------------------------------------------------------- preprocessing
+
+__device__ __forceinline__ void atomic_max_nonneg(unsigned *addr, float v) {
+    // IEEE order of non-negative floats == order of their bit patterns
+    atomicMax(addr, __float_as_uint(v));
+}
+
+// max|x| per channel, and a global flag if any sample is NaN/Inf (the
+// tensor-core split cannot represent those; FAST mode then reroutes to the
+// FFMA kernel on the device, without a host round-trip).
+__global__ void k_amax(const float *__restrict__ x, int64_t ld, int64_t n, unsigned *out,
+                       unsigned *nonfinite) {
+    const float *xc = x + (int64_t)blockIdx.y * ld;
+    float m = 0.0f;
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = fabsf(xc[i]);
+        bad |= !(v <= 3.4028235e38f);
+        m = v > m ? v : m;
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out + 2 * blockIdx.y, m);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
+}
+
+// per channel c: scales[3c] = 2^ex, [3c+1] = 2^eh (exact powers of two that
+// put max|x|, max|h| in [2^14, 2^15)), [3c+2] = 2^-(ex+eh).  amax[2c], [2c+1].
+__global__ void k_scales(const unsigned *amax, float *scales, int channels) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= channels) return;
+    int e[2];
+    for (int i = 0; i < 2; ++i) {
+        const float m = __uint_as_float(amax[2 * c + i]);
+        e[i] = (m > 0.0f && isfinite(m)) ? 14 - ilogbf(m) : 0;
+        scales[3 * c + i] = ldexpf(1.0f, e[i]);
+    }
+    scales[3 * c + 2] = ldexpf(1.0f, -(e[0] + e[1]));
+}
+
+__device__ __forceinline__ void split16(float v, __half &hi, __half &lo) {
+    hi = __float2half_rn(v);
+    lo = __float2half_rn(v - __half2float(hi));
+}
+
+// XT[c][j][row][e] = split(scale_c * X_c(n_begin + (row + row_min)*128 + 8j + e))
+__global__ void k_split_x(const float *__restrict__ x, int64_t ldx, int64_t x_base, int64_t x_lo,
+                          int64_t x_hi, int64_t n_begin, int64_t row_min, int64_t nrows,
+                          const float *scales, __half *__restrict__ xt_hi, __half *__restrict__ xt_lo,
+                          int64_t xt_ch) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (j, row) chunk
+    if (idx >= nrows * KG) return;
+    const int c = blockIdx.y;
+    const int j = (int)(idx / nrows);
+    const int64_t row = idx - (int64_t)j * nrows;
+    const float sc = scales[3 * c];
+    const float *xc = x + (int64_t)c * ldx;
+    const int64_t m0 = n_begin + (row + row_min) * TR + 8 * j;
+    __align__(16) __half hv[8], lv[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int64_t m = m0 + e;
+        const float v = (m >= x_lo && m < x_hi) ? xc[m - x_base] * sc : 0.0f;
+        split16(v, hv[e], lv[e]);
+    }
+    const int64_t o = (int64_t)c * xt_ch + idx * 8;
+    *reinterpret_cast<uint4 *>(xt_hi + o) = *reinterpret_cast<const uint4 *>(hv);
+    *reinterpret_cast<uint4 *>(xt_lo + o) = *reinterpret_cast<const uint4 *>(lv);
+}
+
+// H8[c][g][b][e] = split(scale_c * h_c[C - 8g - b - e]), C = 128*s8 - 1
+__global__ void k_build_h8(const float *__restrict__ h, int64_t ldh, int64_t nh, int64_t s8,
+                           int64_t ngroups, const float *scales, __half *__restrict__ h8_hi,
+                           __half *__restrict__ h8_lo, int64_t h8_ch) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (g, b)
+    if (idx >= ngroups * 8) return;
+    const int c = blockIdx.y;
+    const int64_t g = idx >> 3;
+    const int b = (int)(idx & 7);
+    const float sc = scales[3 * c + 1];
+    const float *hc = h + (int64_t)c * ldh;
+    const int64_t cc = (int64_t)TR * s8 - 1;
+    __align__(16) __half hv[8], lv[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int64_t k = cc - 8 * g - b - e;
+        const float v = (k >= 0 && k < nh) ? hc[k] * sc : 0.0f;
+        split16(v, hv[e], lv[e]);
+    }
+    const int64_t o = (int64_t)c * h8_ch + idx * 8;
+    *reinterpret_cast<uint4 *>(h8_hi + o) = *reinterpret_cast<const uint4 *>(hv);
+    *reinterpret_cast<uint4 *>(h8_lo + o) = *reinterpret_cast<const uint4 *>(lv);
+}
+
+}  // namespace
+
+bool tc_fir_supported(int64_t nh) { return nh >= 2 * TR; }
+
+int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
+                      const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin,
+                      int64_t n_end, int64_t channels, cudaStream_t stream, const unsigned **nonfinite_out) {
+    if (nonfinite_out) *nonfinite_out = nullptr;
+    const int64_t n_len = n_end - n_begin;
+    if (n_len <= 0 || channels <= 0) return SC_OK;
+    SC_REQUIRE(nh >= 1, "tc fir: empty impulse response");
+    SC_REQUIRE(channels < 65536, "tc fir: too many channels");
+    const int64_t s_needed = (nh + TR - 2) / TR + 1;
+    const int64_t s8 = cdiv(s_needed, SSH) * SSH;
+    const int64_t tiles_per_ch = cdiv(n_len, TTILE);
+    const int64_t row_min = -((s8 + WP + 7) / 8) * 8;
+    const int64_t nrows = tiles_per_ch * TN - row_min;
+    const int64_t ngroups = KG * s8 + KG - 1;
+
+    // scratch: [amax 2C u32 | scales 3C f32] [xt hi | xt lo] [h8 hi | h8 lo]
+    const int64_t xt_ch = nrows * KG * 8;
+    const int64_t h8_ch = ngroups * 64;
+    const size_t head = (size_t)cdiv(20 * channels + 64, 256) * 256;
+    const size_t bytes = head + 2 * (size_t)(xt_ch + h8_ch) * channels * 2 + 1024;
+    int err = 0;
+    char *ws = static_cast<char *>(scratch(bytes, 3, stream, &err));
+    if (err) return err;
+    unsigned *amax = reinterpret_cast<unsigned *>(ws);
+    unsigned *flag = reinterpret_cast<unsigned *>(ws + 8 * channels);
+    float *scales = reinterpret_cast<float *>(ws + 8 * channels + 16);
+    if (nonfinite_out) *nonfinite_out = flag;
+    __half *xt_hi = reinterpret_cast<__half *>(ws + head);
+    __half *xt_lo = xt_hi + xt_ch * channels;
+    __half *h8_hi = xt_lo + xt_ch * channels;
+    __half *h8_lo = h8_hi + h8_ch * channels;
+
+    SC_CHECK_CUDA(cudaMemsetAsync(amax, 0, 8 * channels + 4, stream));
+    const int64_t xn = x_hi - x_lo;
+    if (xn > 0) {
+        dim3 g((unsigned)std::min<int64_t>(cdiv(xn, 256), 4 * 148), (unsigned)channels);
+        k_amax<<<g, 256, 0, stream>>>(x + (x_lo - x_base), ldx, xn, amax, flag);
+        SC_CHECK_LAUNCH();
+    }
+    {
+        dim3 g((unsigned)std::min<int64_t>(cdiv(nh, 256), 4 * 148), (unsigned)channels);
+        k_amax<<<g, 256, 0, stream>>>(h, ldh, nh, amax + 1, flag);
+        SC_CHECK_LAUNCH();
+    }
+    k_scales<<<(unsigned)cdiv(channels, 128), 128, 0, stream>>>(amax, scales, (int)channels);
+    SC_CHECK_LAUNCH();
+    {
+        dim3 g((unsigned)cdiv(nrows * KG, 256), (unsigned)channels);
+        k_split_x<<<g, 256, 0, stream>>>(x, ldx, x_base, x_lo, x_hi, n_begin, row_min, nrows, scales, xt_hi,
+                                         xt_lo, xt_ch);
+        SC_CHECK_LAUNCH();
+    }
+    {
+        dim3 g((unsigned)cdiv(ngroups * 8, 256), (unsigned)channels);
+        k_build_h8<<<g, 256, 0, stream>>>(h, ldh, nh, s8, ngroups, scales, h8_hi, h8_lo, h8_ch);
+        SC_CHECK_LAUNCH();
+    }
+    static bool attr_set = false;
+    if (!attr_set) {
+        SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_TOTAL));
+        attr_set = true;
+    }
+    TcArgs a;
+    a.xt[0] = xt_hi;
+    a.xt[1] = xt_lo;
+    a.h8[0] = h8_hi;
+    a.h8[1] = h8_lo;
+    a.xt_ch = xt_ch;
+    a.h8_ch = h8_ch;
+    a.nrows = nrows;
+    a.row_min = row_min;
+    a.s8 = s8;
+    a.tiles_per_ch = tiles_per_ch;
+    a.n_tiles = tiles_per_ch * channels;
+    a.n_begin = n_begin;
+    a.n_end = n_end;
+    a.y = y;
+    a.ldy = ldy;
+    a.scales = scales;
+    a.nonfinite = flag;
+    const int grid = (int)std::min<int64_t>(a.n_tiles, sm_count());
+    k_tc_fir<<<grid, TC_THREADS, SM_TOTAL, stream>>>(a);
+    SC_CHECK_LAUNCH();
+    return SC_OK;
+}
+
+}  // namespace sc

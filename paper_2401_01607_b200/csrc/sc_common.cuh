@@ -98,12 +98,29 @@ constexpr int kMaxSegs = 4;
 int launch_chain(int dtype, int skip_mode, double threshold, const void *x, int64_t x_off,
                  const ChainSeg *segs, int nseg, const void *init, int64_t init_len,
                  const int64_t *init_len_dev, int64_t t0, int64_t n_out, void *out_a,
-                 int64_t n_a, void *out_b, cudaStream_t stream);
+                 int64_t n_a, void *out_b, cudaStream_t stream, const unsigned *run_if = nullptr);
 
-// Fast FP32 FIR over an output range (see k_fast_f32.cu).
+// Fast FP32 FIR over an output range (see k_fast_f32.cu).  With run_if set,
+// every kernel of the launch exits immediately unless *run_if != 0.
 int launch_fir_f32_fast(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
                         const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy,
-                        int64_t n_begin, int64_t n_end, int64_t channels, cudaStream_t stream);
+                        int64_t n_begin, int64_t n_end, int64_t channels, cudaStream_t stream,
+                        const unsigned *run_if = nullptr);
+
+// Tensor-core (tcgen05, FP16 hi/lo split, 3 MMAs) FP32-accurate FIR (k_tc_fir.cu).
+// *nonfinite_out receives a device flag that is nonzero when an input sample
+// is NaN/Inf; the tensor-core kernel then writes nothing and the caller's
+// FFMA launch (gated on the same flag) produces the reference's NaN pattern.
+bool tc_fir_supported(int64_t nh);
+int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
+                      const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin,
+                      int64_t n_end, int64_t channels, cudaStream_t stream,
+                      const unsigned **nonfinite_out);
+
+// FAST-mode dispatch: tensor cores for long filters, FFMA2 kernel otherwise.
+int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
+                   const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin,
+                   int64_t n_end, int64_t channels, cudaStream_t stream);
 
 int launch_direct_form_dd(const double *e, int64_t ne, const double *h, int64_t nh, double *y,
                           cudaStream_t stream);

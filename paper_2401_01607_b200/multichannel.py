@@ -15,7 +15,7 @@ from . import _dev
 from . import _native as N
 
 
-def convolve_batched(x, h):
+def convolve_batched(x, h, mode=None):
     """y[c] = x[c] (*) h[c] for all channels in one launch.
 
     x: [C, Ne] float32 (ndarray or tensor), h: [C, Nh] float32 (or [Nh],
@@ -37,9 +37,12 @@ def convolve_batched(x, h):
     nh = int(hd.shape[1])
     if nh == 0:
         raise ValueError("impulse response is empty")
+    from .core import mode_code
+
     L = N.lib()
     with t.cuda.device(xd.device):
         y = t.empty((C, ne + nh - 1), dtype=t.float32, device=xd.device)
-        N.check(L.sc_fir_batched(N.SC_F32, N.ptr(xd), ne, N.ptr(hd), nh, N.ptr(y), ne + nh - 1, C,
+        N.check(L.sc_fir_batched(N.SC_F32, mode_code(mode), N.ptr(xd), ne, N.ptr(hd), nh, N.ptr(y),
+                                 ne + nh - 1, C,
                                  ne, nh, N.stream_ptr()))
     return _dev.like_input(y, x, h)

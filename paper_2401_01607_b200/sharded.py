@@ -62,15 +62,18 @@ def shard_plan(ne: int, nh: int, world: int) -> list[Shard]:
     return plan
 
 
-def convolve_shard(x_slice, shard: Shard, h):
+def convolve_shard(x_slice, shard: Shard, h, mode=None):
     """Compute one shard on the current device: x_slice holds inputs
     [shard.x_begin, shard.x_end) (CUDA float32), h the taps (CUDA float32).
-    Returns the shard's outputs [n_begin, n_end) as a CUDA tensor."""
+    Returns the shard's outputs [n_begin, n_end) as a CUDA tensor.
+    mode: None/"fast" (kernel chosen by shape), "ffma" or "tc"."""
+    from .core import mode_code
+
     t = _dev.torch()
     L = N.lib()
     y = t.empty(shard.n_out, dtype=t.float32, device=h.device)
     if shard.n_out:
-        N.check(L.sc_fir_range(N.SC_F32, N.ptr(x_slice) if x_slice.numel() else None,
+        N.check(L.sc_fir_range(N.SC_F32, mode_code(mode), N.ptr(x_slice) if x_slice.numel() else None,
                                shard.x_begin, shard.x_end, N.ptr(h), h.shape[0], N.ptr(y),
                                shard.n_begin, shard.n_end, N.stream_ptr()))
     return y

@@ -54,7 +54,7 @@ def test_argument_errors_raise_valueerror_without_device():
     rc = L.sc_fir_full(7, 0, None, 4, None, 4, None, 0, 0.0, None)
     assert rc == N.SC_ERR_ARG and "dtype" in L.sc_last_error().decode()
     with pytest.raises(ValueError, match="empty"):
-        N.check(L.sc_fir_batched(N.SC_F32, None, 1, None, 1, None, 1, 1, 0, 1, None))
+        N.check(L.sc_fir_batched(N.SC_F32, N.SC_MODE_FAST, None, 1, None, 1, None, 1, 1, 0, 1, None))
 
 
 @pytest.mark.skipif(cuda_ok(), reason="checks the no-GPU failure mode")

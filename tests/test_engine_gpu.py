@@ -290,7 +290,8 @@ def test_c_abi_deferred_swap_and_state():
         pend = ctypes.c_int()
         N.check(L.sc_engine_state(eng, *[ctypes.byref(v) for v in vals], ctypes.byref(pend)))
         ri, live, cap, cons, nh = (v.value for v in vals)
-        assert (cap, nh, cons, pend.value) == (3, 1, 2, 0)
+        # engine.py:179: cap = max(len(h_new), live) = max(1, 0) after the deferred swap
+        assert (cap, nh, cons, pend.value, live) == (1, 1, 2, 0, 0)
         big = torch.zeros(20, dtype=torch.float64, device="cuda")
         with pytest.raises(ValueError, match="exceeds block_size_nb"):
             N.check(L.sc_engine_process_block(eng, N.ptr(big), 20, N.ptr(big)))

@@ -1,0 +1,103 @@
+"""Tensor-core (tcgen05, fp16 hi/lo split) FIR vs the CPU oracle.
+
+Tolerance: max-abs <= 1e-5 * max|x| * ||h||_1 (north_star), on shapes that
+exercise every boundary of the kernel: one/many X windows (64 shifts each),
+partial H8 stages, partial last tile, tiny and huge dynamic range, shards
+(output ranges with halos) and batched channels.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2401_01607_b200 import configs
+from paper_2401_01607_b200.core import Signal, scatter_convolve
+from paper_2401_01607_b200.multichannel import convolve_batched
+from paper_2401_01607_b200.sharded import convolve_shard, shard_plan
+
+pytestmark = pytest.mark.gpu
+
+
+def err_frac(y, ref, x, h):
+    tol = configs.tolerance(x, h, "f32")
+    return float(np.max(np.abs(np.asarray(y, np.float64) - ref))) / tol
+
+
+CASES = [(20_000, 256), (20_000, 1000), (16_384, 4096), (100_000, 9_000), (50_001, 20_003),
+         (3_000, 70_000), (300_000, 1_100), (1, 300), (1000, 8191)]
+
+
+@pytest.mark.parametrize("ne,nh", CASES)
+def test_tc_matches_oracle(ne, nh):
+    rng = np.random.default_rng(ne + 17 * nh)
+    x = rng.uniform(-1, 1, ne).astype(np.float32)
+    h = (rng.standard_normal(nh) * np.exp(-np.arange(nh) / (nh / 5))).astype(np.float32)
+    y = np.asarray(scatter_convolve(Signal(x), Signal(h), mode="tc").concatenated().samples)
+    assert len(y) == ne + nh - 1
+    ref = O.scatter_window(x, h, 0, ne + nh - 1)
+    assert err_frac(y, ref, x, h) <= 1.0
+
+
+@pytest.mark.parametrize("xscale,hscale", [(1e-6, 1.0), (1.0, 1e-9), (3e4, 7e3), (1e-30, 1e20)])
+def test_tc_scaling_is_exact_power_of_two(xscale, hscale):
+    rng = np.random.default_rng(5)
+    x = (rng.uniform(-1, 1, 30_000) * xscale).astype(np.float32)
+    h = (rng.standard_normal(3000) * hscale).astype(np.float32)
+    y = np.asarray(scatter_convolve(Signal(x), Signal(h), mode="tc").concatenated().samples)
+    assert np.all(np.isfinite(y))
+    assert err_frac(y, O.scatter_window(x, h, 0, len(y)), x, h) <= 1.0
+
+
+def test_tc_shards_and_batched():
+    import torch
+
+    rng = np.random.default_rng(8)
+    x = rng.uniform(-1, 1, 90_000).astype(np.float32)
+    h = rng.standard_normal(5000).astype(np.float32)
+    hd = torch.from_numpy(h).cuda()
+    ref = O.scatter_window(x, h, 0, len(x) + len(h) - 1)
+    parts = []
+    for sh in shard_plan(len(x), len(h), 3):
+        xs = torch.from_numpy(x[sh.x_begin:sh.x_end]).cuda()
+        parts.append(convolve_shard(xs, sh, hd, mode="tc").cpu().numpy())
+    assert err_frac(np.concatenate(parts), ref, x, h) <= 1.0
+    X = rng.uniform(-1, 1, (3, 40_000)).astype(np.float32)
+    H = rng.standard_normal((3, 2000)).astype(np.float32)
+    H[1] *= 1e-3
+    Y = convolve_batched(X, H, mode="tc")
+    for c in range(3):
+        assert err_frac(Y[c], O.scatter_window(X[c], H[c], 0, Y.shape[1]), X[c], H[c]) <= 1.0
+
+
+@pytest.mark.parametrize("where", ["x_nan", "x_inf", "h_inf"])
+def test_fast_mode_nonfinite_reroutes_on_device(where):
+    # FAST mode on a long filter runs the tensor-core kernel; NaN/Inf inputs
+    # are detected on the device and the FFMA kernel produces the reference's
+    # exact NaN/Inf pattern (no host synchronisation involved).
+    rng = np.random.default_rng(6)
+    x = rng.uniform(-1, 1, 40_000).astype(np.float32)
+    h = rng.standard_normal(3000).astype(np.float32)
+    if where == "x_nan":
+        x[1234] = np.nan
+    elif where == "x_inf":
+        x[20_000] = np.inf
+    else:
+        h[17] = -np.inf
+    y = np.asarray(scatter_convolve(Signal(x), Signal(h)).concatenated().samples)
+    ref = O.scatter_window(x, h, 0, len(y))
+    assert np.array_equal(np.isnan(y), np.isnan(ref))
+    assert np.array_equal(np.isinf(y), np.isinf(ref))
+    fin = np.isfinite(ref)
+    tol = 1e-5 * np.max(np.abs(x[np.isfinite(x)])) * np.sum(np.abs(h[np.isfinite(h)]))
+    assert np.max(np.abs(y[fin] - ref[fin])) <= tol
+
+
+def test_tc_deterministic():
+    import torch
+
+    rng = np.random.default_rng(2)
+    x = torch.from_numpy(rng.uniform(-1, 1, 200_000).astype(np.float32)).cuda()
+    h = torch.from_numpy(rng.standard_normal(12_000).astype(np.float32)).cuda()
+    a = scatter_convolve(Signal(x), Signal(h), mode="tc").concatenated().samples
+    b = scatter_convolve(Signal(x), Signal(h), mode="tc").concatenated().samples
+    assert torch.equal(a, b)
