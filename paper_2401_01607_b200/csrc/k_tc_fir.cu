@@ -236,13 +236,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
     } else if (warp == 1) {
         if (lane == 0) {
             // ------------------------------------------------------------ MMA issuer
-            uint32_t xw = 0, hsc = 0, tcount = 0;
+            // Every H8 stage (8 shifts) accumulates into a fresh TMEM buffer
+            // (alternating), which the epilogue drains into FP32 registers.
+            // The tensor core's FP32 accumulation truncates; bounding each
+            // accumulator's chain to 8 shifts x 8 K-steps x 3 MMAs keeps the
+            // truncation drift ~1e-6 relative (it reached ~1.5e-3 over a full
+            // 262k-tap chain).
+            uint32_t xw = 0, hsc = 0, dc = 0;
             for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
-                const uint32_t acc = tcount & 1;
-                if (tcount >= 2) mbar_wait(bar_tempty + 8 * acc, ((tcount >> 1) - 1) & 1);
-                tc_fence_after();
-                const uint32_t d_tmem = tmem + acc * TN;
-                uint32_t accumulate = 0;
                 for (int64_t w = 0; w < n_windows; ++w) {
                     const int64_t s0 = w * WP;
                     const int64_t s1 = s0 + WP < a.s8 ? s0 + WP : a.s8;
@@ -252,7 +253,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
                         const uint32_t slot = hsc % NHSLOT;
                         mbar_wait(bar_hfull + 8 * slot, (hsc / NHSLOT) & 1);
                         ++hsc;
+                        const uint32_t acc = dc & 1;
+                        if (dc >= 2) mbar_wait(bar_tempty + 8 * acc, ((dc >> 1) - 1) & 1);
                         tc_fence_after();
+                        const uint32_t d_tmem = tmem + acc * TN;
+                        uint32_t accumulate = 0;
 #pragma unroll 1
                         for (int ss = 0; ss < SSH; ++ss) {
                             const int64_t s = sg + ss;
@@ -275,40 +280,51 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
                             }
                         }
                         umma_commit(bar_hempty + 8 * slot);
+                        umma_commit(bar_tfull + 8 * acc);
+                        ++dc;
                     }
                     umma_commit(bar_xempty);
                 }
-                umma_commit(bar_tfull + 8 * acc);
-                ++tcount;
             }
         }
     } else {
         // ---------------------------------------------------------------- epilogue
         const int q = warp & 3;                // TMEM lane quarter of this warp
         const int rp = q * 32 + lane;          // phase index r' = 127 - r
-        uint32_t tcount = 0;
+        const int64_t n_stages = a.s8 / SSH;
+        uint32_t dc = 0;
         for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
             const int64_t ch = tile / a.tiles_per_ch;
             const float inv = a.scales[3 * ch + 2];
             float *yc = a.y + ch * a.ldy;
-            const uint32_t acc = tcount & 1;
-            mbar_wait(bar_tfull + 8 * acc, (tcount >> 1) & 1);
-            tc_fence_after();
-            const int64_t nb = a.n_begin + (tile - ch * a.tiles_per_ch) * (int64_t)TTILE + (TR - 1 - rp);
-#pragma unroll 1
-            for (int c = 0; c < TN; c += 32) {
-                float v[32];
-                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * TN + c, v);
+            // this thread's 128 outputs (one phase r', all 128 rows), summed
+            // over the stage partials in FP32 round-to-nearest
+            float sum[TN];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int64_t n = nb + (int64_t)(c + i) * TR;
-                    if (n < a.n_end) yc[n - a.n_begin] = v[i] * inv;
+            for (int i = 0; i < TN; ++i) sum[i] = 0.0f;
+#pragma unroll 1
+            for (int64_t st = 0; st < n_stages; ++st, ++dc) {
+                const uint32_t acc = dc & 1;
+                mbar_wait(bar_tfull + 8 * acc, (dc >> 1) & 1);
+                tc_fence_after();
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * TN;
+#pragma unroll
+                for (int c = 0; c < TN; c += 32) {
+                    float v[32];
+                    tmem_ld32(taddr + c, v);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) sum[c + i] += v[i];
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
-            ++tcount;
+            const int64_t nb = a.n_begin + (tile - ch * a.tiles_per_ch) * (int64_t)TTILE + (TR - 1 - rp);
+#pragma unroll
+            for (int i = 0; i < TN; ++i) {
+                const int64_t n = nb + (int64_t)i * TR;
+                if (n < a.n_end) yc[n - a.n_begin] = sum[i] * inv;
+            }
         }
     }
     tc_fence_before();

@@ -24,7 +24,7 @@ def err_frac(y, ref, x, h):
 
 
 CASES = [(20_000, 256), (20_000, 1000), (16_384, 4096), (100_000, 9_000), (50_001, 20_003),
-         (3_000, 70_000), (300_000, 1_100), (1, 300), (1000, 8191)]
+         (3_000, 70_000), (300_000, 1_100), (1, 300), (1000, 8191), (40_000, 262_144)]
 
 
 @pytest.mark.parametrize("ne,nh", CASES)
