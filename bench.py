@@ -125,6 +125,20 @@ class ClockSampler:
 # ------------------------------------------------------------------ workloads
 
 
+def max_over_ranks(v: float, world: int, device) -> float:
+    """MAX of a per-rank float over all ranks (device tensor under NCCL,
+    host tensor under gloo)."""
+    if world == 1:
+        return float(v)
+    import torch
+    import torch.distributed as dist
+
+    dev = device if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def peaks():
     p = {}
     f = REPO / "MEASURED_PEAKS.json"
@@ -352,8 +366,16 @@ def main():
 
     rank, world, local = env_rank()
     if world > 1:
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # SC_DIST_BACKEND=gloo lets the multi-rank timing/sharding logic run
+        # with several ranks on one GPU (NCCL refuses duplicate devices); the
+        # data path has no collective either way -- only barrier/max-reduce.
+        backend = os.environ.get("SC_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     device = torch.device("cuda", torch.cuda.current_device())
@@ -394,10 +416,7 @@ def main():
     barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms_local = sum(step_ms) / len(step_ms)
-    ms = torch.tensor([ms_local], device=device, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+    ms = max_over_ranks(ms_local, world, device)
     value = work.total_macs / (ms * 1e-3) / 1e9
 
     # roofline of the dominant kernel on this rank
@@ -459,12 +478,10 @@ def main():
             hb, db = work.e2e_step(x_pin, h_pin)
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
-        t_e2e = torch.tensor([sum(times) / len(times)], device=device, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-        e2e = {"value": work.total_macs / float(t_e2e.item()) / 1e9, "unit": UNIT,
+        t_e2e = max_over_ranks(sum(times) / len(times), world, device)
+        e2e = {"value": work.total_macs / t_e2e / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(hb), "d2h_bytes_per_step": int(db),
-               "ms_per_step": 1000 * float(t_e2e.item()),
+               "ms_per_step": 1000 * t_e2e,
                "api": "paper_2401_01607_b200.scatter_convolve(Signal(pinned host tensor))" if world == 1
                else "paper_2401_01607_b200.distributed_convolve(pinned host, to_host=True)"}
 
