@@ -104,14 +104,10 @@ int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_
     // the ORDERED kernel, which visits exactly the reference's (m, k) pairs
     // and so reproduces its NaN/Inf pattern (0*Inf included).  Each launch
     // exits immediately when the flag is clear.
-    for (int64_t c = 0; c < channels; ++c) {
-        ChainSeg seg{h + c * ldh, nh, x_lo, x_hi};
-        rc = launch_chain(SC_F32, SC_SKIP_NONE, 0.0, x + c * ldx, x_base, &seg, 1, nullptr, 0, nullptr,
-                          n_begin, n_end - n_begin, y + c * ldy, n_end - n_begin, nullptr, stream,
-                          nonfinite);
-        if (rc) return rc;
-    }
-    return SC_OK;
+    ChainSeg seg{h, nh, x_lo, x_hi};
+    ChainBatch batch{channels, ldx, ldh, ldy};
+    return launch_chain(SC_F32, SC_SKIP_NONE, 0.0, x, x_base, &seg, 1, nullptr, 0, nullptr, n_begin,
+                        n_end - n_begin, y, n_end - n_begin, nullptr, stream, nonfinite, &batch);
 }
 
 static size_t dtype_size(int dtype) { return dtype == SC_F64 ? 8 : (dtype == SC_F32 ? 4 : 0); }

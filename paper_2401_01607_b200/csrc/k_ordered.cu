@@ -16,6 +16,8 @@
 // addresses by consecutive threads (conflict-free).  Zero-skip predicates are
 // warp-uniform (all threads of a chunk visit the same m).
 
+#include <algorithm>
+
 #include "sc_common.cuh"
 
 namespace sc {
@@ -39,6 +41,7 @@ struct ChainArgs {
     T *out_b;
     double thr;
     const unsigned *run_if;  // optional device gate: run only if *run_if != 0
+    int64_t ldx, ldh, ldo;   // channel strides (grid.y = channel); 0 = one channel
 };
 
 template <typename T, int SKIP>
@@ -46,7 +49,15 @@ __global__ void __launch_bounds__(TB) k_chain(ChainArgs<T> a) {
     __shared__ T xs[MC];
     __shared__ T hs[MC + TB - 1];
     if (a.run_if && *a.run_if == 0) return;  // block-uniform
-    const int64_t tile0 = a.t0 + (int64_t)blockIdx.x * TB;
+    if (blockIdx.y) {  // batched channel: shift the channel's base pointers
+        a.x += blockIdx.y * a.ldx;
+        a.out_a += blockIdx.y * a.ldo;
+        for (int s = 0; s < a.nseg; ++s) a.seg[s].h = static_cast<const T *>(a.seg[s].h) + blockIdx.y * a.ldh;
+    }
+    const int64_t n_tiles = (a.n_out + TB - 1) / TB;
+    for (int64_t tb = blockIdx.x; tb < n_tiles; tb += gridDim.x) {
+    __syncthreads();  // smem reuse across tiles of this CTA
+    const int64_t tile0 = a.t0 + tb * TB;
     const int64_t t_end = a.t0 + a.n_out;
     const int64_t tile_last = (tile0 + TB < t_end ? tile0 + TB : t_end) - 1;
     const int64_t t = tile0 + threadIdx.x;
@@ -99,13 +110,15 @@ __global__ void __launch_bounds__(TB) k_chain(ChainArgs<T> a) {
         else if (a.out_b != nullptr)
             a.out_b[i - a.n_a] = acc;
     }
+    }  // tiles
 }
 
 template <typename T>
 int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off,
                    const ChainSeg *segs, int nseg, const void *init, int64_t init_len,
                    const int64_t *init_len_dev, int64_t t0, int64_t n_out, void *out_a,
-                   int64_t n_a, void *out_b, cudaStream_t stream, const unsigned *run_if) {
+                   int64_t n_a, void *out_b, cudaStream_t stream, const unsigned *run_if,
+                   const ChainBatch *batch) {
     if (n_out <= 0) return SC_OK;
     SC_REQUIRE(nseg >= 0 && nseg <= kMaxSegs, "chain: bad segment count %d", nseg);
     ChainArgs<T> a{};
@@ -123,12 +136,23 @@ int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off
     a.out_b = static_cast<T *>(out_b);
     a.thr = threshold;
     a.run_if = run_if;
-    const int64_t grid = cdiv(n_out, TB);
-    SC_REQUIRE(grid < (int64_t)INT32_MAX, "chain: output range too large");
+    int64_t channels = 1;
+    if (batch) {
+        channels = batch->channels;
+        a.ldx = batch->ldx;
+        a.ldh = batch->ldh;
+        a.ldo = batch->ldo;
+        SC_REQUIRE(channels >= 1 && channels < 65536 && out_b == nullptr, "chain: bad batch");
+    }
+    // Grid-stride over 256-output tiles.  A device-gated launch (run_if) is
+    // usually a no-op, so it gets a small grid that exits in microseconds.
+    const int64_t cap = run_if ? std::max<int64_t>(1, 4 * (int64_t)sm_count() / channels)
+                               : (int64_t)INT32_MAX - 1;
+    const dim3 grid((unsigned)std::min<int64_t>(cdiv(n_out, TB), cap), (unsigned)channels);
     switch (skip_mode) {
-        case SC_SKIP_NONE: k_chain<T, SC_SKIP_NONE><<<(unsigned)grid, TB, 0, stream>>>(a); break;
-        case SC_SKIP_LE: k_chain<T, SC_SKIP_LE><<<(unsigned)grid, TB, 0, stream>>>(a); break;
-        case SC_SKIP_NOT_GT: k_chain<T, SC_SKIP_NOT_GT><<<(unsigned)grid, TB, 0, stream>>>(a); break;
+        case SC_SKIP_NONE: k_chain<T, SC_SKIP_NONE><<<grid, TB, 0, stream>>>(a); break;
+        case SC_SKIP_LE: k_chain<T, SC_SKIP_LE><<<grid, TB, 0, stream>>>(a); break;
+        case SC_SKIP_NOT_GT: k_chain<T, SC_SKIP_NOT_GT><<<grid, TB, 0, stream>>>(a); break;
         default: SC_REQUIRE(false, "chain: bad skip_mode %d", skip_mode);
     }
     SC_CHECK_LAUNCH();
@@ -171,13 +195,14 @@ __global__ void __launch_bounds__(TB) k_direct_dd(const double *__restrict__ e, 
 int launch_chain(int dtype, int skip_mode, double threshold, const void *x, int64_t x_off,
                  const ChainSeg *segs, int nseg, const void *init, int64_t init_len,
                  const int64_t *init_len_dev, int64_t t0, int64_t n_out, void *out_a,
-                 int64_t n_a, void *out_b, cudaStream_t stream, const unsigned *run_if) {
+                 int64_t n_a, void *out_b, cudaStream_t stream, const unsigned *run_if,
+                 const ChainBatch *batch) {
     if (dtype == SC_F64)
         return launch_chain_t<double>(skip_mode, threshold, x, x_off, segs, nseg, init, init_len,
-                                      init_len_dev, t0, n_out, out_a, n_a, out_b, stream, run_if);
+                                      init_len_dev, t0, n_out, out_a, n_a, out_b, stream, run_if, batch);
     if (dtype == SC_F32)
         return launch_chain_t<float>(skip_mode, threshold, x, x_off, segs, nseg, init, init_len,
-                                     init_len_dev, t0, n_out, out_a, n_a, out_b, stream, run_if);
+                                     init_len_dev, t0, n_out, out_a, n_a, out_b, stream, run_if, batch);
     set_error("chain: bad dtype %d", dtype);
     return SC_ERR_ARG;
 }

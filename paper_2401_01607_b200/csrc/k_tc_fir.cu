@@ -81,6 +81,11 @@ struct TcArgs {
     int64_t ldy;           // channel stride of y
     const float *scales;   // per channel: [3*ch+2] = 2^-(ex+eh)
     const unsigned *nonfinite;  // set by k_amax: inputs not representable -> skip
+    int64_t nsplit;        // shift-range splits per tile
+    int64_t sps;           // shifts per split (multiple of SSH)
+    int64_t n_units;       // n_tiles * nsplit
+    int64_t channels;
+    float *ws;             // partials [nsplit][channels][n_end-n_begin] when nsplit > 1
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -197,20 +202,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    const int64_t n_windows = (a.s8 + WP - 1) / WP;
-
+    // Work unit u = (tile, split): the split's shift range [sb, se) of that
+    // tile (splits > 1 only when tiles alone leave SMs idle, e.g. cfg3).
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------------------ producer
             uint32_t xw = 0, hsc = 0;
-            for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+            for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+                const int64_t tile = u / a.nsplit;
+                const int64_t sb = (u - tile * a.nsplit) * a.sps;
+                const int64_t se = sb + a.sps < a.s8 ? sb + a.sps : a.s8;
                 const int64_t ch = tile / a.tiles_per_ch;
                 const int64_t i0 = (tile - ch * a.tiles_per_ch) * TN;
                 const __half *xt0 = a.xt[0] + ch * a.xt_ch, *xt1 = a.xt[1] + ch * a.xt_ch;
                 const __half *h80 = a.h8[0] + ch * a.h8_ch, *h81 = a.h8[1] + ch * a.h8_ch;
-                for (int64_t w = 0; w < n_windows; ++w) {
-                    const int64_t s0 = w * WP;
-                    const int64_t s1 = s0 + WP < a.s8 ? s0 + WP : a.s8;
+                for (int64_t s0 = sb; s0 < se; s0 += WP) {
+                    const int64_t s1 = s0 + WP < se ? s0 + WP : se;
                     if (xw > 0) mbar_wait(bar_xempty, (xw - 1) & 1);
                     mbar_expect_tx(bar_xfull, 2 * XWIN_PART);
                     const int64_t row_lo = i0 - s0 - WP - a.row_min;  // layout row of window row 0
@@ -243,10 +250,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
             // truncation drift ~1e-6 relative (it reached ~1.5e-3 over a full
             // 262k-tap chain).
             uint32_t xw = 0, hsc = 0, dc = 0;
-            for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
-                for (int64_t w = 0; w < n_windows; ++w) {
-                    const int64_t s0 = w * WP;
-                    const int64_t s1 = s0 + WP < a.s8 ? s0 + WP : a.s8;
+            for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+                const int64_t tile = u / a.nsplit;
+                const int64_t sb = (u - tile * a.nsplit) * a.sps;
+                const int64_t se = sb + a.sps < a.s8 ? sb + a.sps : a.s8;
+                for (int64_t s0 = sb; s0 < se; s0 += WP) {
+                    const int64_t s1 = s0 + WP < se ? s0 + WP : se;
                     mbar_wait(bar_xfull, xw & 1);
                     ++xw;
                     for (int64_t sg = s0; sg < s1; sg += SSH) {
@@ -291,12 +300,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
         // ---------------------------------------------------------------- epilogue
         const int q = warp & 3;                // TMEM lane quarter of this warp
         const int rp = q * 32 + lane;          // phase index r' = 127 - r
-        const int64_t n_stages = a.s8 / SSH;
         uint32_t dc = 0;
-        for (int64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+        for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+            const int64_t tile = u / a.nsplit;
+            const int64_t sp = u - tile * a.nsplit;
+            const int64_t sb = sp * a.sps;
+            const int64_t se = sb + a.sps < a.s8 ? sb + a.sps : a.s8;
+            const int64_t n_stages = (se - sb) / SSH;
             const int64_t ch = tile / a.tiles_per_ch;
             const float inv = a.scales[3 * ch + 2];
-            float *yc = a.y + ch * a.ldy;
+            // with splits, each writes its (rescaled) partial to ws[sp][ch][.];
+            // k_tc_split_reduce sums them in fixed split order (deterministic)
+            float *yc = a.nsplit == 1 ? a.y + ch * a.ldy
+                                      : a.ws + (sp * a.channels + ch) * (a.n_end - a.n_begin);
             // this thread's 128 outputs (one phase r', all 128 rows), summed
             // over the stage partials in FP32 round-to-nearest
             float sum[TN];
@@ -350,8 +366,23 @@ __global__ void k_amax(const float *__restrict__ x, int64_t ld, int64_t n, unsig
     const float *xc = x + (int64_t)blockIdx.y * ld;
     float m = 0.0f;
     bool bad = false;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const float v = fabsf(xc[i]);
+    // scalar head up to 16-byte alignment, float4 body, scalar tail
+    const int64_t mis = (int64_t)((16 - (reinterpret_cast<uintptr_t>(xc) & 15)) & 15) / 4;
+    const int64_t head = mis < n ? mis : n;
+    const int64_t n4 = (n - head) / 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const float4 *x4 = reinterpret_cast<const float4 *>(xc + head);
+    for (int64_t i = tid; i < n4; i += stride) {
+        const float4 q = x4[i];
+        const float a = fmaxf(fmaxf(fabsf(q.x), fabsf(q.y)), fmaxf(fabsf(q.z), fabsf(q.w)));
+        bad |= !(fabsf(q.x) <= 3.4028235e38f) || !(fabsf(q.y) <= 3.4028235e38f) ||
+               !(fabsf(q.z) <= 3.4028235e38f) || !(fabsf(q.w) <= 3.4028235e38f);
+        m = a > m ? a : m;
+    }
+    for (int64_t i = tid; i < head + (n - head - 4 * n4); i += stride) {
+        const int64_t k = i < head ? i : head + 4 * n4 + (i - head);
+        const float v = fabsf(xc[k]);
         bad |= !(v <= 3.4028235e38f);
         m = v > m ? v : m;
     }
@@ -384,27 +415,62 @@ __global__ void k_split_x(const float *__restrict__ x, int64_t ldx, int64_t x_ba
                           int64_t x_hi, int64_t n_begin, int64_t row_min, int64_t nrows,
                           const float *scales, __half *__restrict__ xt_hi, __half *__restrict__ xt_lo,
                           int64_t xt_ch) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (j, row) chunk
-    if (idx >= nrows * KG) return;
+    // One CTA = 32 consecutive rows = 4096 contiguous samples: coalesced
+    // float4 loads into a padded smem tile (row pitch 132 floats), then each
+    // K-group j writes its 32 rows x 16 B = 512 B contiguous (fp16 hi and lo).
+    __shared__ __align__(16) float s[32][132];
     const int c = blockIdx.y;
-    const int j = (int)(idx / nrows);
-    const int64_t row = idx - (int64_t)j * nrows;
+    const int64_t row0 = (int64_t)blockIdx.x * 32;
     const float sc = scales[3 * c];
     const float *xc = x + (int64_t)c * ldx;
-    const int64_t m0 = n_begin + (row + row_min) * TR + 8 * j;
-    __align__(16) __half hv[8], lv[8];
+    const int64_t m0 = n_begin + (row0 + row_min) * TR;  // first sample of the tile
+    const bool inside = m0 >= x_lo && m0 + 4096 <= x_hi &&
+                        ((reinterpret_cast<uintptr_t>(xc + (m0 - x_base)) & 15) == 0);
+    if (inside) {
+        const float4 *src = reinterpret_cast<const float4 *>(xc + (m0 - x_base));
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        const int64_t m = m0 + e;
-        const float v = (m >= x_lo && m < x_hi) ? xc[m - x_base] * sc : 0.0f;
-        split16(v, hv[e], lv[e]);
+        for (int k = 0; k < 4; ++k) {
+            const int f = threadIdx.x + 256 * k;  // float4 index in the tile
+            const float4 q = src[f];
+            float *d = &s[f >> 5][(f & 31) * 4];
+            d[0] = q.x * sc;
+            d[1] = q.y * sc;
+            d[2] = q.z * sc;
+            d[3] = q.w * sc;
+        }
+    } else {
+        for (int f = threadIdx.x; f < 4096; f += 256) {
+            const int64_t m = m0 + f;
+            s[f >> 7][f & 127] = (m >= x_lo && m < x_hi) ? xc[m - x_base] * sc : 0.0f;
+        }
     }
-    const int64_t o = (int64_t)c * xt_ch + idx * 8;
-    *reinterpret_cast<uint4 *>(xt_hi + o) = *reinterpret_cast<const uint4 *>(hv);
-    *reinterpret_cast<uint4 *>(xt_lo + o) = *reinterpret_cast<const uint4 *>(lv);
+    __syncthreads();
+    const int r = threadIdx.x & 31;
+    if (row0 + r >= nrows) return;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+        const int j = (threadIdx.x >> 5) + 8 * pass;
+        __align__(16) __half hv[8], lv[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) split16(s[r][8 * j + e], hv[e], lv[e]);
+        const int64_t o = (int64_t)c * xt_ch + ((int64_t)j * nrows + row0 + r) * 8;
+        *reinterpret_cast<uint4 *>(xt_hi + o) = *reinterpret_cast<const uint4 *>(hv);
+        *reinterpret_cast<uint4 *>(xt_lo + o) = *reinterpret_cast<const uint4 *>(lv);
+    }
 }
 
 // H8[c][g][b][e] = split(scale_c * h_c[C - 8g - b - e]), C = 128*s8 - 1
+// y = sum of the split partials in ascending split order (deterministic).
+__global__ void k_tc_split_reduce(const float *__restrict__ ws, int nsplit, int channels, int64_t n_len,
+                                  float *__restrict__ y, int64_t ldy, const unsigned *nonfinite) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int ch = blockIdx.y;
+    if (i >= n_len || *nonfinite) return;
+    float s = ws[(int64_t)ch * n_len + i];
+    for (int k = 1; k < nsplit; ++k) s += ws[((int64_t)k * channels + ch) * n_len + i];
+    y[(int64_t)ch * ldy + i] = s;
+}
+
 __global__ void k_build_h8(const float *__restrict__ h, int64_t ldh, int64_t nh, int64_t s8,
                            int64_t ngroups, const float *scales, __half *__restrict__ h8_hi,
                            __half *__restrict__ h8_lo, int64_t h8_ch) {
@@ -467,7 +533,9 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     SC_CHECK_CUDA(cudaMemsetAsync(amax, 0, 8 * channels + 4, stream));
     const int64_t xn = x_hi - x_lo;
     if (xn > 0) {
-        dim3 g((unsigned)std::min<int64_t>(cdiv(xn, 256), 4 * 148), (unsigned)channels);
+        // ~8 resident CTAs per SM across all channels, float4 per thread
+        const int64_t per_ch = std::max<int64_t>(1, 8 * (int64_t)sm_count() / channels);
+        dim3 g((unsigned)std::min<int64_t>(cdiv(xn, 1024), per_ch), (unsigned)channels);
         k_amax<<<g, 256, 0, stream>>>(x + (x_lo - x_base), ldx, xn, amax, flag);
         SC_CHECK_LAUNCH();
     }
@@ -479,7 +547,7 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     k_scales<<<(unsigned)cdiv(channels, 128), 128, 0, stream>>>(amax, scales, (int)channels);
     SC_CHECK_LAUNCH();
     {
-        dim3 g((unsigned)cdiv(nrows * KG, 256), (unsigned)channels);
+        dim3 g((unsigned)cdiv(nrows, 32), (unsigned)channels);
         k_split_x<<<g, 256, 0, stream>>>(x, ldx, x_base, x_lo, x_hi, n_begin, row_min, nrows, scales, xt_hi,
                                          xt_lo, xt_ch);
         SC_CHECK_LAUNCH();
@@ -512,9 +580,44 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     a.ldy = ldy;
     a.scales = scales;
     a.nonfinite = flag;
-    const int grid = (int)std::min<int64_t>(a.n_tiles, sm_count());
+    a.channels = channels;
+    // Shift-range splits fill idle SMs when whole tiles leave the last wave
+    // mostly empty (cfg3: 182 tiles on 148 SMs); each split keeps >= 2 X
+    // windows so its window load stays amortised.
+    const int sms = sm_count();
+    const int64_t stages = s8 / SSH;
+    int64_t nsplit = 1;
+    {
+        double best = 0.0;
+        for (int64_t s = 1; s <= 16 && s * 2 * (WP / SSH) <= stages; ++s) {
+            const int64_t units = a.n_tiles * s;
+            const int64_t waves = (units + sms - 1) / sms;
+            const double eff = (double)units / (double)(waves * sms);
+            if (eff > best + 0.03) {
+                best = eff;
+                nsplit = s;
+            }
+            if (best > 0.95) break;
+        }
+    }
+    const int64_t sps = cdiv(stages, nsplit) * SSH;
+    nsplit = cdiv(s8, sps);
+    a.nsplit = nsplit;
+    a.sps = sps;
+    a.n_units = a.n_tiles * nsplit;
+    a.ws = nullptr;
+    if (nsplit > 1) {
+        a.ws = static_cast<float *>(scratch(sizeof(float) * (size_t)n_len * channels * nsplit, 4, stream, &err));
+        if (err) return err;
+    }
+    const int grid = (int)std::min<int64_t>(a.n_units, sms);
     k_tc_fir<<<grid, TC_THREADS, SM_TOTAL, stream>>>(a);
     SC_CHECK_LAUNCH();
+    if (nsplit > 1) {
+        dim3 g((unsigned)cdiv(n_len, 256), (unsigned)channels);
+        k_tc_split_reduce<<<g, 256, 0, stream>>>(a.ws, (int)nsplit, (int)channels, n_len, y, ldy, flag);
+        SC_CHECK_LAUNCH();
+    }
     return SC_OK;
 }
 

@@ -98,7 +98,14 @@ constexpr int kMaxSegs = 4;
 int launch_chain(int dtype, int skip_mode, double threshold, const void *x, int64_t x_off,
                  const ChainSeg *segs, int nseg, const void *init, int64_t init_len,
                  const int64_t *init_len_dev, int64_t t0, int64_t n_out, void *out_a,
-                 int64_t n_a, void *out_b, cudaStream_t stream, const unsigned *run_if = nullptr);
+                 int64_t n_a, void *out_b, cudaStream_t stream, const unsigned *run_if = nullptr,
+                 const struct ChainBatch *batch = nullptr);
+
+// Optional channel batching for launch_chain (single-segment use): channel c
+// reads x + c*ldx and taps + c*ldh, and writes out_a + c*ldo.
+struct ChainBatch {
+    int64_t channels, ldx, ldh, ldo;
+};
 
 // Fast FP32 FIR over an output range (see k_fast_f32.cu).  With run_if set,
 // every kernel of the launch exits immediately unless *run_if != 0.
