@@ -49,7 +49,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--config", default="cfg5",
+                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "short8", "short16", "short32",
+                             "short64", "short128"])
     ap.add_argument("--mode", default="fast", choices=["fast", "ffma", "tc"],
                     help="float32 kernel: fast = picked by shape (tensor cores for long filters)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -195,6 +197,20 @@ class Work:
             self.parallelism = f"replicas x{world}"
             self.scaling = "weak"
             self.dtype = "f64"
+        elif cfg.startswith("short"):
+            # short-filter HBM sanity sweep: Ne = 2^26, Nh = 8..64
+            nh = int(cfg[5:])
+            rng = np.random.default_rng(77)
+            x = rng.uniform(-1, 1, 1 << 26).astype(np.float32)
+            h = rng.standard_normal(nh).astype(np.float32)
+            self.w = configs.Workload(f"short_f32_67108864x{nh}", "f32", x, h)
+            self.total_macs = self.w.metric_macs * world
+            self.rank_macs = self.w.metric_macs
+            self.xd = torch.from_numpy(x).to(device)
+            self.hd = torch.from_numpy(h).to(device)
+            self.parallelism = f"replicas x{world}"
+            self.scaling = "weak"
+            self.dtype = "f32"
         elif cfg == "cfg2":
             w = configs.cfg2()
             self.w = w
@@ -202,8 +218,14 @@ class Work:
             self.rank_macs = (w.ne + w.nh - 1) * w.nh
             self.xd = torch.from_numpy(w.x).to(device)
             n_blocks = -(-w.ne // 256)
-            self.swaps = [(b, torch.from_numpy(w.irs[b // 100]).to(device)) for b in range(100, n_blocks, 100)]
             self.h0 = torch.from_numpy(w.irs[0]).to(device)
+            # block 0 re-selects IR 0 so every step replays the identical stream
+            self.swaps = [(0, self.h0)] + [(b, torch.from_numpy(w.irs[b // 100]).to(device))
+                                           for b in range(100, n_blocks, 100)]
+            from paper_2401_01607_b200.core import Signal
+            from paper_2401_01607_b200.engine import EngineConfig, ScatterEngine
+
+            self.eng = ScatterEngine(Signal(self.h0), EngineConfig(block_size_nb=256))
             self.parallelism = f"replicas x{world} (streaming is sequential per stream)"
             self.scaling = "weak"
             self.dtype = "f32"
@@ -212,6 +234,10 @@ class Work:
         """Which kernel the library runs for this config/mode (mirrors capi.cu's
         FAST dispatch) and the padded tensor-core work it issues."""
         self.tc_padded_macs = 0
+        if self.cfg.startswith("short"):
+            self.kernel = "k_fir_f32_fast" if self.w.nh < 256 else "k_tc_fir"
+            self.hbm_bound = True
+            return
         if self.dtype != "f32" or self.cfg not in ("cfg3", "cfg4", "cfg5"):
             self.kernel = "k_chain"
             return
@@ -240,11 +266,17 @@ class Work:
         if self.cfg == "cfg4":
             return convolve_batched(self.xd, self.hd, mode=self.mode)
         if self.cfg == "cfg1":
-            return scatter_convolve(Signal(self.xd), Signal(self.hd)).concatenated().samples
+            # the full Ne+Nh-1 result (ConvOutput body/tail are views of it)
+            return scatter_convolve(Signal(self.xd), Signal(self.hd)).body.samples
         if self.cfg == "cfg2":
-            eng = ScatterEngine(Signal(self.h0), EngineConfig(block_size_nb=256))
-            body = eng.process_stream(self.xd, 256, self.swaps)
+            # 1,875 blocks of 256 with 18 IR swaps, then the flush of the tail
+            # (engine.py:148-161) -- the whole stream, no host round-trip until
+            # the flush (which returns the data-dependent tail length).
+            body = self.eng.process_stream(self.xd, 256, self.swaps)
+            self.eng.flush()
             return body
+        if self.cfg.startswith("short"):
+            return scatter_convolve(Signal(self.xd), Signal(self.hd), mode=self.mode).body.samples
         raise ValueError(self.cfg)
 
     def e2e_step(self, x_pin, h_pin):
@@ -431,7 +463,15 @@ def main():
     tf = REPO / "profiles" / "ncu_traffic.json"
     if tf.exists():
         traffic = json.loads(tf.read_text()).get(f"{args.config}_{work.kernel}")
-    if work.kernel == "k_tc_fir":
+    if getattr(work, "hbm_bound", False):
+        # short filters: the kernel should stream x in and y out at HBM speed
+        hbm = float(p.get("hbm_gbs", 6650.0))
+        alg_bytes = 4 * (work.w.ne + work.w.nh + work.w.nout)
+        gbs = alg_bytes / (ms_local * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                    "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "alg_bytes_per_launch": alg_bytes, "kernel": work.kernel}
+    elif work.kernel == "k_tc_fir":
         # tensor work actually issued: 3 fp16 MMAs (hi*hi, lo*hi, hi*lo) over the
         # padded block-Toeplitz GEMM (whole 16384-output tiles x 128 taps x s8 shifts)
         tc_peak = float(p.get("bf16_tflops", 1590.0))

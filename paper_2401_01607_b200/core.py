@@ -112,6 +112,57 @@ def mode_code(mode) -> int:
     return _MODES[mode]
 
 
+_PIPELINE_MIN_MACS = 1 << 36   # host-resident inputs this large are streamed in chunks
+_PIPELINE_CHUNKS = 8
+_PIPE_STREAMS: dict = {}
+
+
+def _fir_host_pipelined(x_pin, kern, mode):
+    """Pinned-host float32 input: overlap the H2D upload, the FIR and the D2H
+    download chunk by chunk (one stream each, event-chained).  Chunk c owns
+    outputs [a_c, b_c) and needs inputs up to min(Ne, b_c); it is computed with
+    sc_fir_range over the device copy of x (its halo is already there).
+    Returns a pinned host tensor with the full Ne+Nh-1 result."""
+    t = _dev.torch()
+    L = N.lib()
+    dev = t.device("cuda", t.cuda.current_device())
+    ne = x_pin.shape[0]
+    h = _dev.as_device(kern, np.float32, device=dev)
+    nh = h.shape[0]
+    nout = ne + nh - 1
+    out = t.empty(nout, dtype=t.float32, pin_memory=True)
+    xd = t.empty(ne, dtype=t.float32, device=dev)
+    yd = t.empty(nout, dtype=t.float32, device=dev)
+    main = t.cuda.current_stream(dev)
+    # persistent per-device streams: the library's scratch buffers are keyed
+    # by stream, so fresh streams would re-allocate every call
+    if dev.index not in _PIPE_STREAMS:
+        _PIPE_STREAMS[dev.index] = tuple(t.cuda.Stream(dev) for _ in range(3))
+    s_in, s_cmp, s_out = _PIPE_STREAMS[dev.index]
+    for s in (s_in, s_cmp, s_out):
+        s.wait_stream(main)   # h upload / allocations are ordered on main
+    per = -(-nout // _PIPELINE_CHUNKS)
+    uploaded = 0
+    for c in range(_PIPELINE_CHUNKS):
+        a, b = c * per, min(nout, (c + 1) * per)
+        if a >= b:
+            break
+        need = min(ne, b)
+        if need > uploaded:
+            with t.cuda.stream(s_in):
+                xd[uploaded:need].copy_(x_pin[uploaded:need], non_blocking=True)
+            uploaded = need
+        s_cmp.wait_stream(s_in)
+        xb = max(0, a - nh + 1)
+        N.check(L.sc_fir_range(N.SC_F32, mode, N.ptr(xd[xb:]) if need > xb else None, xb, max(xb, need),
+                               N.ptr(h), nh, N.ptr(yd[a:]), a, b, N.stream_ptr(s_cmp)))
+        s_out.wait_stream(s_cmp)
+        with t.cuda.stream(s_out):
+            out[a:b].copy_(yd[a:b], non_blocking=True)
+    s_out.synchronize()   # the result lives in host memory: wait for the last D2H
+    return out
+
+
 def _fir(drive, kern, *, mode=None, skip_mode=N.SC_SKIP_NONE, threshold=0.0):
     """Full convolution of two 1-D sample arrays on the device (core._scatter_full
     semantics: slot n accumulates drive samples in increasing index)."""
@@ -123,6 +174,10 @@ def _fir(drive, kern, *, mode=None, skip_mode=N.SC_SKIP_NONE, threshold=0.0):
         m = N.SC_MODE_FAST if npd == np.float32 else N.SC_MODE_ORDERED
     L = N.lib()
     t = _dev.torch()
+    if (npd == np.float32 and m != N.SC_MODE_ORDERED and skip_mode == N.SC_SKIP_NONE
+            and _dev.is_tensor(drive) and drive.device.type == "cpu" and drive.is_pinned()
+            and drive.dtype == t.float32 and drive.shape[0] * int(np.shape(kern)[0]) >= _PIPELINE_MIN_MACS):
+        return _fir_host_pipelined(drive, kern, m)
     x = _dev.as_device(drive, npd)
     h = _dev.as_device(kern, npd, device=x.device)
     nout = x.shape[0] + h.shape[0] - 1

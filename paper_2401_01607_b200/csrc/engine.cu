@@ -22,6 +22,7 @@
 
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "sc_common.cuh"
 
@@ -84,6 +85,66 @@ __global__ void k_sched_to_ring(const T *__restrict__ sched, int64_t cap, int64_
 
 size_t esize(int dtype) { return dtype == SC_F64 ? 8 : 4; }
 
+// ---- fused multi-block streaming (sc_engine_process_blocks)
+
+constexpr int kMaxEvents = kMaxSegs - 1;  // IR changes per fused launch
+
+struct StreamEvents {
+    int64_t n;                     // number of events
+    int64_t block[kMaxEvents];     // block index the swap precedes (ascending)
+    int64_t nh[kMaxEvents];        // new IR length
+};
+
+// J[b] = last index (within block b) whose sample scatters, -1 if none.
+template <typename T>
+__global__ void k_blocks_last_scatter(const T *__restrict__ x, int64_t n_total, int64_t nb, double thr,
+                                      int64_t *__restrict__ J) {
+    const int64_t b = blockIdx.x;
+    const int64_t s = b * nb;
+    const int64_t n = n_total - s < nb ? n_total - s : nb;
+    long long j = -1;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        if (!skipped<SC_SKIP_NOT_GT>(x[s + i], thr)) j = i > j ? i : j;
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long v = __shfl_xor_sync(0xffffffffu, j, o);
+        j = v > j ? v : j;
+    }
+    __shared__ long long sj[8];
+    if ((threadIdx.x & 31) == 0) sj[threadIdx.x >> 5] = j;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) j = sj[w] > j ? sj[w] : j;
+        J[b] = j;
+    }
+}
+
+// Replays engine.py's bookkeeping over all blocks of the call: each swap
+// (cap = max(nh, live), ri = 0; engine.py:179-184) and each block
+// (live' = max(0, live - n, J >= 0 ? nh - n + J : 0), ri' = (ri + n) % cap).
+__global__ void k_stream_state(const int64_t *__restrict__ J, int64_t n_blocks, int64_t nb, int64_t n_total,
+                               int64_t nh0, StreamEvents ev, int64_t *st) {
+    int64_t live = st[0], cap = st[1], ri = st[2], nh = nh0;
+    int64_t k = 0;
+    for (int64_t b = 0; b < n_blocks; ++b) {
+        while (k < ev.n && ev.block[k] == b) {
+            nh = ev.nh[k];
+            cap = nh > live ? nh : live;
+            ri = 0;
+            ++k;
+        }
+        const int64_t n = n_total - b * nb < nb ? n_total - b * nb : nb;
+        const int64_t j = J[b];
+        int64_t l = live - n;
+        if (l < 0) l = 0;
+        if (j >= 0 && nh - n + j > l) l = nh - n + j;
+        live = l;
+        ri = (ri + n) % cap;
+    }
+    st[0] = live;
+    st[1] = cap;
+    st[2] = ri;
+}
+
 int launch_epilogue(int dtype, const void *x, int64_t n, double thr, int64_t nh, int64_t *st,
                     cudaStream_t s) {
     if (dtype == SC_F64)
@@ -122,6 +183,11 @@ struct sc_engine {
     int64_t cap_ub = 0;  // host upper bound of the device-side logical cap
     int64_t *st = nullptr;  // device: live, cap, read_index
     int64_t consumed = 0;
+    // staging copies of the IRs of one fused process_blocks call
+    void *stage = nullptr;
+    int64_t stage_capacity = 0;
+    int64_t *jbuf = nullptr;  // per-block last-scatter index (device)
+    int64_t jbuf_capacity = 0;
 };
 
 namespace {
@@ -272,6 +338,8 @@ int sc_engine_destroy(sc_engine *e) {
     cudaFree(e->res[0]);
     cudaFree(e->res[1]);
     cudaFree(e->st);
+    cudaFree(e->stage);
+    cudaFree(e->jbuf);
     delete e;
     return SC_OK;
 }
@@ -395,24 +463,116 @@ int sc_engine_process_blocks(sc_engine *e, const void *x, int64_t n_total, int64
     SC_REQUIRE(nb >= 1 && nb <= e->nb, "sc_engine_process_blocks: nb must be in [1, block_size_nb]");
     SC_REQUIRE(n_total >= 0 && (n_total == 0 || (x && out)), "sc_engine_process_blocks: bad input");
     SC_REQUIRE(n_swaps == 0 || (swap_blocks && swap_irs && swap_nh), "sc_engine_process_blocks: bad swaps");
-    DeviceGuard g(e->device);
-    const char *xb = static_cast<const char *>(x);
-    char *ob = static_cast<char *>(out);
-    int64_t si = 0;
-    int64_t b = 0;
-    for (int64_t s = 0; s < n_total; s += nb, ++b) {
-        while (si < n_swaps && swap_blocks[si] <= b) {
-            if (swap_blocks[si] == b) {
-                SC_REQUIRE(swap_nh[si] >= 1, "impulse response is empty");
-                int rc = do_swap(e, swap_irs[si], swap_nh[si]);
-                if (rc) return rc;
-            }
-            ++si;
-        }
-        const int64_t n = n_total - s < nb ? n_total - s : nb;
-        int rc = do_block(e, xb + (size_t)s * e->es, n, ob + (size_t)s * e->es, true);
-        if (rc) return rc;
+    for (int64_t i = 0; i < n_swaps; ++i) {
+        SC_REQUIRE(swap_nh[i] >= 1, "impulse response is empty");
+        SC_REQUIRE(i == 0 || swap_blocks[i] >= swap_blocks[i - 1], "swap_blocks must be ascending");
     }
+    DeviceGuard g(e->device);
+    if (n_total == 0) return SC_OK;
+    const int64_t n_blocks = cdiv(n_total, nb);
+    // IR timeline: (block, h, nh); a pending deferred swap acts right before
+    // block 0, after any explicit swap scheduled there (engine.py:124-126).
+    struct Ev {
+        int64_t block;
+        const void *h;
+        int64_t nh;
+    };
+    std::vector<Ev> ev;
+    for (int64_t i = 0; i < n_swaps; ++i)
+        if (swap_blocks[i] >= 0 && swap_blocks[i] < n_blocks) ev.push_back({swap_blocks[i], swap_irs[i], swap_nh[i]});
+    if (e->has_pending) {
+        size_t pos = 0;
+        while (pos < ev.size() && ev[pos].block == 0) ++pos;
+        ev.insert(ev.begin() + pos, Ev{0, e->pend, e->pend_nh});
+        e->has_pending = false;
+    }
+    // Too many IR changes for one launch: process in consecutive block ranges.
+    if ((int64_t)ev.size() > kMaxEvents) {
+        int64_t b0 = 0;
+        size_t k = 0;
+        while (b0 < n_blocks) {
+            size_t k1 = std::min(ev.size(), k + kMaxEvents);
+            int64_t b1 = k1 < ev.size() ? ev[k1].block : n_blocks;
+            if (b1 <= b0) b1 = b0 + 1;
+            std::vector<int64_t> sb;
+            std::vector<const void *> sh;
+            std::vector<int64_t> sn;
+            for (size_t q = k; q < ev.size() && ev[q].block < b1; ++q, ++k) {
+                sb.push_back(ev[q].block - b0);
+                sh.push_back(ev[q].h);
+                sn.push_back(ev[q].nh);
+            }
+            const int64_t s0 = b0 * nb, s1 = std::min(n_total, b1 * nb);
+            int rc = sc_engine_process_blocks(e, static_cast<const char *>(x) + (size_t)s0 * e->es, s1 - s0, nb,
+                                              sb.data(), sh.data(), sn.data(), (int64_t)sb.size(),
+                                              static_cast<char *>(out) + (size_t)s0 * e->es);
+            if (rc) return rc;
+            b0 = b1;
+        }
+        return SC_OK;
+    }
+    // Stage every IR of the timeline in engine-owned memory (the kernels run
+    // after this call returns; callers may free their buffers).
+    int64_t tot = e->nh;
+    for (const Ev &v : ev) tot += v.nh;
+    int rc = ensure_buffer(&e->stage, &e->stage_capacity, tot, e->es, false, 0, e->stream);
+    if (rc) return rc;
+    rc = ensure_buffer(reinterpret_cast<void **>(&e->jbuf), &e->jbuf_capacity, n_blocks, 8, false, 0, e->stream);
+    if (rc) return rc;
+    char *stage = static_cast<char *>(e->stage);
+    SC_CHECK_CUDA(cudaMemcpyAsync(stage, e->ir, (size_t)e->nh * e->es, cudaMemcpyDeviceToDevice, e->stream));
+    ChainSeg segs[kMaxSegs];
+    int nseg = 0;
+    segs[nseg++] = ChainSeg{stage, e->nh, 0, n_total};
+    int64_t off = e->nh, ub = e->cap_ub;
+    StreamEvents sev{};
+    sev.n = 0;
+    for (const Ev &v : ev) {
+        char *dst = stage + (size_t)off * e->es;
+        SC_CHECK_CUDA(cudaMemcpyAsync(dst, v.h, (size_t)v.nh * e->es, cudaMemcpyDeviceToDevice, e->stream));
+        const int64_t m = v.block * nb;
+        if (segs[nseg - 1].m_lo == m) {
+            segs[nseg - 1].h = dst;  // a later swap before the same block wins
+            segs[nseg - 1].nh = v.nh;
+        } else {
+            segs[nseg - 1].m_hi = m;
+            segs[nseg++] = ChainSeg{dst, v.nh, m, n_total};
+        }
+        sev.block[sev.n] = v.block;
+        sev.nh[sev.n] = v.nh;
+        ++sev.n;
+        off += v.nh;
+        ub = v.nh > ub ? v.nh : ub;
+    }
+    rc = grow_residue(e, ub);
+    if (rc) return rc;
+    // One ordered launch for every block: slot t accumulates its drive samples
+    // in ascending order across blocks and IR segments -- the same chain as
+    // block-by-block processing (bit-identical), continued from the residue.
+    void *rin = e->res[e->cur], *rout = e->res[1 - e->cur];
+    rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, x, 0, segs, nseg, rin, 0, e->st + ST_CAP, 0, n_total + ub,
+                      out, n_total, rout, e->stream);
+    if (rc) return rc;
+    if (e->dtype == SC_F64)
+        k_blocks_last_scatter<double><<<(unsigned)n_blocks, 256, 0, e->stream>>>(static_cast<const double *>(x), n_total,
+                                                                             nb, e->thr, e->jbuf);
+    else
+        k_blocks_last_scatter<float><<<(unsigned)n_blocks, 256, 0, e->stream>>>(static_cast<const float *>(x), n_total,
+                                                                            nb, e->thr, e->jbuf);
+    SC_CHECK_LAUNCH();
+    k_stream_state<<<1, 1, 0, e->stream>>>(e->jbuf, n_blocks, nb, n_total, e->nh, sev, e->st);
+    SC_CHECK_LAUNCH();
+    // host-side bookkeeping: last IR becomes current (engine-owned copy)
+    const ChainSeg &last = segs[nseg - 1];
+    if (last.h != stage) {
+        rc = ensure_buffer(&e->ir, &e->ir_capacity, last.nh, e->es, false, 0, e->stream);
+        if (rc) return rc;
+        SC_CHECK_CUDA(cudaMemcpyAsync(e->ir, last.h, (size_t)last.nh * e->es, cudaMemcpyDeviceToDevice, e->stream));
+        e->nh = last.nh;
+    }
+    e->cap_ub = ub;
+    e->cur = 1 - e->cur;
+    e->consumed += n_total;
     return SC_OK;
 }
 

@@ -236,6 +236,113 @@ __global__ void k_pad_taps(const float *__restrict__ h, int64_t ldh, int64_t nh,
     hp[(int64_t)ch * ldhp + i] = i < nh ? h[(int64_t)ch * ldh + i] : 0.0f;
 }
 
+// ---------------------------------------------------------------- short filters
+// Nh <= 256: the ring/split machinery above is overhead.  Each CTA stages one
+// contiguous x tile (4096 outputs + Nh-1 halo, float4 loads) and the taps in
+// smem; each thread computes 16 consecutive outputs.  Per 4 taps a thread
+// reads its 20-float input window with 5 LDS.128 plus the 4 taps with one
+// broadcast LDS.128 and issues 64 FFMA; the stage starts Nh rounded up to 4
+// before the tile so every window is float4-aligned and the window shift is
+// pure register renaming.
+// The x stage is padded by 4 floats every 16 (row pitch 80 B) so the 64 B
+// stride between lanes is bank-conflict-free.  HBM-bound for short filters
+// (8 B per output), FMA-bound beyond ~40 taps.  Edge tiles (touching the ends
+// of the valid input range) only multiply taps whose input exists, so
+// non-finite taps propagate exactly as in the reference.
+constexpr int SH_THREADS = 256;
+constexpr int SH_R = 16;
+constexpr int SH_TILE = SH_THREADS * SH_R;  // 4096
+constexpr int SH_MAXNH = 256;
+
+__device__ __forceinline__ int sh_pos(int i) { return i + ((i >> 4) << 2); }
+
+__global__ void __launch_bounds__(SH_THREADS) k_fir_short(const float *__restrict__ x, int64_t ldx, int64_t x_base,
+                                                          int64_t x_lo, int64_t x_hi, const float *__restrict__ h,
+                                                          int64_t ldh, int nh, float *__restrict__ y, int64_t ldy,
+                                                          int64_t n_begin, int64_t n_end, const unsigned *run_if) {
+    // xs[i] = X(n0 - nh_pad + 1 + i) with nh_pad = nh rounded up to 4 (so the
+    // tile start is float4-aligned whenever n0 is), i in [0, 4096 + nh_pad + 4)
+    constexpr int XS = SH_TILE + SH_MAXNH + 8;
+    __shared__ __align__(16) float xs[XS + XS / 4];
+    __shared__ __align__(16) float hsm[SH_MAXNH + 4];
+    if (run_if && *run_if == 0) return;
+    const int ch = blockIdx.y;
+    const float *xc = x + (int64_t)ch * ldx;
+    const float *hc = h + (int64_t)ch * ldh;
+    float *yc = y + (int64_t)ch * ldy;
+    const int nhp = (nh + 3) & ~3;
+    const int64_t n0 = n_begin + (int64_t)blockIdx.x * SH_TILE;
+    const int64_t m0 = n0 - nhp;  // input index of xs[0] (float4-aligned with n0)
+    const int nx = SH_TILE + nhp;
+    for (int k = threadIdx.x; k < SH_MAXNH + 4; k += SH_THREADS) hsm[k] = k < nh ? hc[k] : 0.0f;
+    const bool edge = m0 < x_lo || n0 + SH_TILE > x_hi;
+    const float *src = xc + (m0 - x_base);
+    if (!edge && m0 + nx <= x_hi && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        for (int i4 = threadIdx.x; i4 < nx / 4; i4 += SH_THREADS)
+            *reinterpret_cast<float4 *>(&xs[sh_pos(4 * i4)]) = __ldg(reinterpret_cast<const float4 *>(src) + i4);
+    } else {
+        for (int i = threadIdx.x; i < nx; i += SH_THREADS) {
+            const int64_t m = m0 + i;
+            xs[sh_pos(i)] = (m >= x_lo && m < x_hi) ? __ldg(xc + (m - x_base)) : 0.0f;
+        }
+    }
+    __syncthreads();
+    float acc[SH_R];
+#pragma unroll
+    for (int r = 0; r < SH_R; ++r) acc[r] = 0.0f;
+    const int j16 = threadIdx.x * SH_R;
+    const int64_t t0 = n0 + j16;  // this thread's first output
+    // output t0+r, tap k reads X(t0 + r - k) = xs[j16 + r - k + nhp]
+    for (int k0 = 0; k0 < nh; k0 += 4) {
+        // window: xs[b .. b+20) with b = j16 + nhp - 4 - k0 (a multiple of 4,
+        // so both the staging and the window loads are float4-aligned);
+        // tap k0+u, output r -> w[r - u + 4]
+        const int b = j16 + nhp - 4 - k0;
+        float w[20];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+            const float4 q = *reinterpret_cast<const float4 *>(&xs[sh_pos(b + 4 * c)]);
+            w[4 * c] = q.x;
+            w[4 * c + 1] = q.y;
+            w[4 * c + 2] = q.z;
+            w[4 * c + 3] = q.w;
+        }
+        const float4 hq = *reinterpret_cast<const float4 *>(&hsm[k0]);
+        const float hk[4] = {hq.x, hq.y, hq.z, hq.w};
+        if (!edge) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (k0 + u < nh) {
+#pragma unroll
+                    for (int r = 0; r < SH_R; ++r) acc[r] = fmaf(w[r - u + 4], hk[u], acc[r]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = k0 + u;
+                if (k < nh) {
+#pragma unroll
+                    for (int r = 0; r < SH_R; ++r) {
+                        const int64_t m = t0 + r - k;
+                        if (m >= x_lo && m < x_hi) acc[r] = fmaf(w[r - u + 4], hk[u], acc[r]);
+                    }
+                }
+            }
+        }
+    }
+    float *d = yc + (t0 - n_begin);
+    if (t0 + SH_R <= n_end && (reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+#pragma unroll
+        for (int c = 0; c < SH_R / 4; ++c)
+            reinterpret_cast<float4 *>(d)[c] = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
+    } else {
+#pragma unroll
+        for (int r = 0; r < SH_R; ++r)
+            if (t0 + r < n_end) d[r] = acc[r];
+    }
+}
+
 int choose_splits(int64_t tiles, int64_t stages, int slots) {
     // Pick the split count (over tap stages) that best fills whole waves of
     // `slots` resident CTAs; each split keeps >= 16 stages (1024 taps) so
@@ -266,6 +373,15 @@ int launch_fir_f32_fast(const float *x, int64_t ldx, int64_t x_base, int64_t x_l
     if (n_len <= 0 || channels <= 0) return SC_OK;
     SC_REQUIRE(nh >= 1, "fir: empty impulse response");
     SC_REQUIRE(channels < 65536, "fir: too many channels");
+    if (nh <= SH_MAXNH) {
+        const int64_t tiles = cdiv(n_len, SH_TILE);
+        SC_REQUIRE(tiles < (int64_t)INT32_MAX, "fir: output range too large");
+        dim3 g((unsigned)tiles, (unsigned)channels);
+        k_fir_short<<<g, SH_THREADS, 0, stream>>>(x, ldx, x_base, x_lo, x_hi, h, ldh, (int)nh, y, ldy, n_begin,
+                                                  n_end, run_if);
+        SC_CHECK_LAUNCH();
+        return SC_OK;
+    }
     const int64_t nh_pad = cdiv(nh, FT_STAGE_TAPS) * FT_STAGE_TAPS;
     const int64_t tiles = cdiv(n_len, FT_TILE);
     SC_REQUIRE(tiles < (int64_t)INT32_MAX, "fir: output range too large");

@@ -49,11 +49,11 @@ __global__ void __launch_bounds__(TB) k_chain(ChainArgs<T> a) {
     __shared__ T xs[MC];
     __shared__ T hs[MC + TB - 1];
     if (a.run_if && *a.run_if == 0) return;  // block-uniform
-    if (blockIdx.y) {  // batched channel: shift the channel's base pointers
-        a.x += blockIdx.y * a.ldx;
-        a.out_a += blockIdx.y * a.ldo;
-        for (int s = 0; s < a.nseg; ++s) a.seg[s].h = static_cast<const T *>(a.seg[s].h) + blockIdx.y * a.ldh;
-    }
+    // batched channel (grid.y): channel-local base pointers (the param struct
+    // itself is never written, so it stays in the constant bank)
+    const T *xb = a.x + blockIdx.y * a.ldx;
+    T *outa = a.out_a + blockIdx.y * a.ldo;
+    const int64_t hoff = blockIdx.y * a.ldh;
     const int64_t n_tiles = (a.n_out + TB - 1) / TB;
     for (int64_t tb = blockIdx.x; tb < n_tiles; tb += gridDim.x) {
     __syncthreads();  // smem reuse across tiles of this CTA
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(TB) k_chain(ChainArgs<T> a) {
     if (active && a.init != nullptr && (t - a.t0) < init_len) acc = a.init[t - a.t0];
 
     for (int s = 0; s < a.nseg; ++s) {
-        const T *__restrict__ h = static_cast<const T *>(a.seg[s].h);
+        const T *__restrict__ h = static_cast<const T *>(a.seg[s].h) + hoff;
         const int64_t nh = a.seg[s].nh;
         const int64_t m_lo = a.seg[s].m_lo, m_hi = a.seg[s].m_hi;
         const int64_t blo = tile0 - nh + 1 > m_lo ? tile0 - nh + 1 : m_lo;
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(TB) k_chain(ChainArgs<T> a) {
             __syncthreads();
             for (int i = threadIdx.x; i < MC; i += TB) {
                 const int64_t m = mc + i;
-                xs[i] = m < bhi ? a.x[m - a.x_off] : T(0);
+                xs[i] = m < bhi ? xb[m - a.x_off] : T(0);
             }
             const int64_t kbase = tile0 - mc - MC + 1;
             for (int i = threadIdx.x; i < MC + TB - 1; i += TB) {
@@ -106,11 +106,117 @@ __global__ void __launch_bounds__(TB) k_chain(ChainArgs<T> a) {
     if (active) {
         const int64_t i = t - a.t0;
         if (i < a.n_a)
-            a.out_a[i] = acc;
+            outa[i] = acc;
         else if (a.out_b != nullptr)
             a.out_b[i - a.n_a] = acc;
     }
     }  // tiles
+}
+
+// ---------------------------------------------------------------- register-tiled chain
+// Same arithmetic and order as k_chain (each output: one ascending-m chain of
+// separately rounded mul/add), but each thread carries RT_R consecutive
+// outputs: per drive sample m the tap window slides by one, so with a
+// rotating register window of RT_R + RT_U - 1 taps one shared-memory load
+// feeds RT_R/ (RT_R+RT_U-1) * RT_U MACs instead of one.  Used for large
+// ordered launches (whole signals in float64, fused streaming).  The tap
+// stage is padded (one slot every 32 floats / 16 doubles) so the stride-RT_R
+// accesses of a warp hit distinct banks.
+constexpr int RT_TB = 128;
+constexpr int RT_R = 8;
+constexpr int RT_TILE = RT_TB * RT_R;  // 1024 outputs per CTA
+constexpr int RT_MC = 128;            // drive samples per smem chunk
+constexpr int RT_U = 8;               // m-steps per register window
+
+template <typename T>
+__device__ __forceinline__ int rt_pos(int i) {
+    return sizeof(T) == 8 ? i + (i >> 4) : i + (i >> 5);
+}
+
+template <typename T, int SKIP>
+__global__ void __launch_bounds__(RT_TB) k_chain_rt(ChainArgs<T> a) {
+    constexpr int HS = RT_TILE + RT_MC - 1;
+    __shared__ T xs[RT_MC];
+    __shared__ T hs[HS + HS / 16 + 2];
+    if (a.run_if && *a.run_if == 0) return;
+    // batched channel (grid.y): channel-local base pointers (the param struct
+    // itself is never written, so it stays in the constant bank)
+    const T *xb = a.x + blockIdx.y * a.ldx;
+    T *outa = a.out_a + blockIdx.y * a.ldo;
+    const int64_t hoff = blockIdx.y * a.ldh;
+    const int64_t n_tiles = (a.n_out + RT_TILE - 1) / RT_TILE;
+    const int64_t t_end = a.t0 + a.n_out;
+    const int64_t init_len = a.init_len_dev ? *a.init_len_dev : a.init_len;
+    for (int64_t tb = blockIdx.x; tb < n_tiles; tb += gridDim.x) {
+        __syncthreads();
+        const int64_t tile0 = a.t0 + tb * RT_TILE;
+        const int64_t tile_last = (tile0 + RT_TILE < t_end ? tile0 + RT_TILE : t_end) - 1;
+        const int64_t tj = tile0 + (int64_t)threadIdx.x * RT_R;  // this thread's first output
+        T acc[RT_R];
+#pragma unroll
+        for (int r = 0; r < RT_R; ++r) {
+            const int64_t t = tj + r;
+            acc[r] = (a.init != nullptr && t < t_end && (t - a.t0) < init_len) ? a.init[t - a.t0] : T(0);
+        }
+        for (int s = 0; s < a.nseg; ++s) {
+            const T *__restrict__ h = static_cast<const T *>(a.seg[s].h) + hoff;
+            const int64_t nh = a.seg[s].nh;
+            const int64_t m_lo = a.seg[s].m_lo, m_hi = a.seg[s].m_hi;
+            const int64_t blo = tile0 - nh + 1 > m_lo ? tile0 - nh + 1 : m_lo;
+            const int64_t bhi = tile_last + 1 < m_hi ? tile_last + 1 : m_hi;
+            for (int64_t mc = blo; mc < bhi; mc += RT_MC) {
+                __syncthreads();
+                for (int i = threadIdx.x; i < RT_MC; i += RT_TB) {
+                    const int64_t m = mc + i;
+                    xs[i] = m < bhi ? xb[m - a.x_off] : T(0);
+                }
+                const int64_t kbase = tile0 - mc - RT_MC + 1;
+                for (int i = threadIdx.x; i < HS; i += RT_TB) {
+                    const int64_t k = kbase + i;
+                    hs[rt_pos<T>(i)] = (k >= 0 && k < nh) ? h[k] : T(0);
+                }
+                __syncthreads();
+                const int mcount = (int)(bhi - mc < RT_MC ? bhi - mc : RT_MC);
+                // every (output of the tile, m of the chunk) pair is a valid tap
+                const bool full = (mc >= tile_last - nh + 1) && (mc + mcount - 1 <= tile0);
+                const int hb = threadIdx.x * RT_R + RT_MC - 1;  // hs index of tap for (r=0, im=0)
+                for (int im0 = 0; im0 < mcount; im0 += RT_U) {
+                    T w[RT_R + RT_U - 1];  // w[q] = hs[hb - im0 - (RT_U-1) + q]
+#pragma unroll
+                    for (int q = 0; q < RT_R + RT_U - 1; ++q) w[q] = hs[rt_pos<T>(hb - im0 - (RT_U - 1) + q)];
+#pragma unroll
+                    for (int u = 0; u < RT_U; ++u) {
+                        const int im = im0 + u;
+                        if (im >= mcount) break;
+                        const T xv = xs[im];
+                        if (skipped<SKIP>(xv, a.thr)) continue;
+                        const int64_t m = mc + im;
+                        if (full) {
+#pragma unroll
+                            for (int r = 0; r < RT_R; ++r) acc[r] = add_rn(acc[r], mul_rn(xv, w[r - u + RT_U - 1]));
+                        } else {
+#pragma unroll
+                            for (int r = 0; r < RT_R; ++r) {
+                                const int64_t t = tj + r;
+                                if (m <= t && m > t - nh) acc[r] = add_rn(acc[r], mul_rn(xv, w[r - u + RT_U - 1]));
+                            }
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RT_R; ++r) {
+            const int64_t t = tj + r;
+            if (t < t_end) {
+                const int64_t i = t - a.t0;
+                if (i < a.n_a)
+                    outa[i] = acc[r];
+                else if (a.out_b != nullptr)
+                    a.out_b[i - a.n_a] = acc[r];
+            }
+        }
+    }
 }
 
 template <typename T>
@@ -148,6 +254,23 @@ int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off
     // usually a no-op, so it gets a small grid that exits in microseconds.
     const int64_t cap = run_if ? std::max<int64_t>(1, 4 * (int64_t)sm_count() / channels)
                                : (int64_t)INT32_MAX - 1;
+    // Large launches: register-tiled variant (8 outputs/thread).  Small ones
+    // (one streaming block) keep one output per thread for parallelism.
+    static const int64_t rt_min = [] {
+        const char *v = getenv("SC_CHAIN_RT_MIN");  // experiment knob (outputs)
+        return v ? (int64_t)atoll(v) : (int64_t)2 * 148 * RT_TILE;
+    }();
+    if (n_out >= rt_min) {
+        const dim3 grid((unsigned)std::min<int64_t>(cdiv(n_out, RT_TILE), cap), (unsigned)channels);
+        switch (skip_mode) {
+            case SC_SKIP_NONE: k_chain_rt<T, SC_SKIP_NONE><<<grid, RT_TB, 0, stream>>>(a); break;
+            case SC_SKIP_LE: k_chain_rt<T, SC_SKIP_LE><<<grid, RT_TB, 0, stream>>>(a); break;
+            case SC_SKIP_NOT_GT: k_chain_rt<T, SC_SKIP_NOT_GT><<<grid, RT_TB, 0, stream>>>(a); break;
+            default: SC_REQUIRE(false, "chain: bad skip_mode %d", skip_mode);
+        }
+        SC_CHECK_LAUNCH();
+        return SC_OK;
+    }
     const dim3 grid((unsigned)std::min<int64_t>(cdiv(n_out, TB), cap), (unsigned)channels);
     switch (skip_mode) {
         case SC_SKIP_NONE: k_chain<T, SC_SKIP_NONE><<<grid, TB, 0, stream>>>(a); break;

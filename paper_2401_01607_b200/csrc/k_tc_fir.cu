@@ -48,16 +48,19 @@ constexpr int TR = 128;              // phases per row (M) = taps per shift (K)
 constexpr int TN = 128;              // output rows per tile (N)
 constexpr int TTILE = TR * TN;       // 16384 outputs per tile
 constexpr int KG = TR / 8;           // 16 K-groups of 8 fp16 (16 B)
-constexpr int WP = 64;               // shifts per X window
-constexpr int WROWS = TN + WP;       // 192 rows per window (191 used)
+#ifndef SC_TC_WP
+#define SC_TC_WP 128
+#endif
+constexpr int WP = SC_TC_WP;         // shifts per X window (window reloads stall the MMAs)
+constexpr int WROWS = TN + WP;       // rows per window (WROWS-1 used)
 constexpr int SSH = 8;               // shifts per H8 stage
 constexpr int SGROUPS = 2 * KG - 1 + KG * (SSH - 1);  // 143 groups per stage
 constexpr int NHSLOT = 2;            // H8 stage slots
-constexpr uint32_t XWIN_PART = WROWS * KG * 16;        // 49152 B
-constexpr uint32_t HST_PART = SGROUPS * 128;           // 18304 B
+constexpr uint32_t XWIN_PART = WROWS * KG * 16;        // one X window, one part (64 KB at WP=128)
+constexpr uint32_t HST_PART = SGROUPS * 128;           // one H8 stage, one part (18304 B)
 constexpr uint32_t SM_XWIN = 0;
-constexpr uint32_t SM_HST = 2 * XWIN_PART;             // 98304
-constexpr uint32_t SM_BAR = SM_HST + NHSLOT * 2 * HST_PART;  // 171520
+constexpr uint32_t SM_HST = 2 * XWIN_PART;
+constexpr uint32_t SM_BAR = SM_HST + NHSLOT * 2 * HST_PART;  // 204288 B at WP=128
 constexpr uint32_t SM_TOTAL = SM_BAR + 128;
 constexpr int TC_THREADS = 192;
 constexpr uint32_t TMEM_COLS = 256;  // 2 accumulators x 128 fp32 columns
@@ -589,7 +592,7 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     int64_t nsplit = 1;
     {
         double best = 0.0;
-        for (int64_t s = 1; s <= 16 && s * 2 * (WP / SSH) <= stages; ++s) {
+        for (int64_t s = 1; s <= 16 && s * (WP / SSH) <= stages; ++s) {
             const int64_t units = a.n_tiles * s;
             const int64_t waves = (units + sms - 1) / sms;
             const double eff = (double)units / (double)(waves * sms);

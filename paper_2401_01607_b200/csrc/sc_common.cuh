@@ -87,7 +87,7 @@ struct ChainSeg {
     int64_t nh;
     int64_t m_lo, m_hi;
 };
-constexpr int kMaxSegs = 4;
+constexpr int kMaxSegs = 32;
 
 // Ordered chain: outputs t in [t0, t0+n_out):
 //   acc = init (init[t-t0] if t-t0 < init_len (host value, or *init_len_dev

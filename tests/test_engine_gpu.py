@@ -272,6 +272,45 @@ def test_process_stream_equals_sequential_calls(dtype):
         assert np.array_equal(got, np.concatenate(rp + [ref.flush()]))
 
 
+@pytest.mark.parametrize("dtype,n_swaps,thr", [(np.float64, 45, 0.0), (np.float32, 45, 0.3),
+                                               (np.float64, 3, 0.25)])
+def test_fused_stream_many_swaps_matches_oracle_engine(dtype, n_swaps, thr):
+    """process_stream is ONE fused launch per <=31 IR changes; with 45 swaps
+    (grow, shrink, same length, several before one block) it must equal the
+    block-by-block reference engine bit-for-bit (float64) and its state."""
+    import torch
+
+    rng = np.random.default_rng(100 + n_swaps)
+    nb = 64
+    x = rng.uniform(-1, 1, 64 * 70 + 17)
+    x[rng.uniform(0, 1, len(x)) < 0.2] = 0.0
+    x[5] = np.nan
+    x = x.astype(dtype)
+    h0 = rng.standard_normal(90).astype(dtype)
+    blocks = np.sort(rng.integers(0, 71, n_swaps))
+    swaps = [(int(b), rng.standard_normal(int(rng.integers(1, 300))).astype(dtype)) for b in blocks]
+    eng = ScatterEngine(Signal(h0), EngineConfig(block_size_nb=nb, zero_skip_threshold=thr))
+    body = eng.process_stream(torch.from_numpy(x).cuda(), nb, swaps).cpu().numpy()
+    st = eng.state_dict()
+    tail = eng.flush().samples
+    ref = O.OracleEngine(h0, block_size_nb=nb, zero_skip_threshold=thr)
+    outs = []
+    for b, s in enumerate(range(0, len(x), nb)):
+        for sb, ir in swaps:
+            if sb == b:
+                ref.swap_ir(ir)
+        outs.append(ref.process_block(x[s:s + nb]))
+    assert st["live"] == ref.live and st["read_index"] == ref.read_index
+    want = np.concatenate(outs + [ref.flush()])
+    got = np.concatenate([body, tail])
+    if dtype == np.float64:
+        assert np.array_equal(got, want, equal_nan=True)
+    else:
+        assert np.array_equal(np.isnan(got), np.isnan(want))
+        ok = ~np.isnan(want)
+        assert np.max(np.abs(got[ok] - want[ok])) <= 1e-5 * 1.0 * 300 * 4
+
+
 def test_c_abi_deferred_swap_and_state():
     import torch
 

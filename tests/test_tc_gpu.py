@@ -69,6 +69,25 @@ def test_tc_shards_and_batched():
         assert err_frac(Y[c], O.scatter_window(X[c], H[c], 0, Y.shape[1]), X[c], H[c]) <= 1.0
 
 
+@pytest.mark.parametrize("nh", [5, 200])
+@pytest.mark.parametrize("where", ["x_nan", "h_inf"])
+def test_short_filter_nonfinite_exact(nh, where):
+    # the short-filter kernel multiplies only taps whose input exists, so
+    # 0*Inf never appears at the signal edges (reference semantics)
+    rng = np.random.default_rng(nh)
+    x = rng.uniform(-1, 1, 10_000).astype(np.float32)
+    h = rng.standard_normal(nh).astype(np.float32)
+    if where == "x_nan":
+        x[[0, 4000, 9999]] = np.nan
+    else:
+        h[nh // 2] = np.inf
+    y = np.asarray(scatter_convolve(Signal(x), Signal(h)).concatenated().samples)
+    ref = O.scatter_full(x, h)
+    assert np.array_equal(np.isnan(y), np.isnan(ref)) and np.array_equal(np.isinf(y), np.isinf(ref))
+    fin = np.isfinite(ref)
+    assert np.max(np.abs(y[fin] - ref[fin])) <= 1e-5 * np.sum(np.abs(h[np.isfinite(h)])) + 1e-6
+
+
 @pytest.mark.parametrize("where", ["x_nan", "x_inf", "h_inf"])
 def test_fast_mode_nonfinite_reroutes_on_device(where):
     # FAST mode on a long filter runs the tensor-core kernel; NaN/Inf inputs
@@ -90,6 +109,25 @@ def test_fast_mode_nonfinite_reroutes_on_device(where):
     fin = np.isfinite(ref)
     tol = 1e-5 * np.max(np.abs(x[np.isfinite(x)])) * np.sum(np.abs(h[np.isfinite(h)]))
     assert np.max(np.abs(y[fin] - ref[fin])) <= tol
+
+
+@pytest.mark.parametrize("mode", [None, "ffma"])
+def test_pinned_host_pipeline(monkeypatch, mode):
+    """Pinned host input -> chunked H2D / FIR / D2H overlap (core._fir_host_pipelined)."""
+    import torch
+
+    from paper_2401_01607_b200 import core
+
+    monkeypatch.setattr(core, "_PIPELINE_MIN_MACS", 0)
+    monkeypatch.setattr(core, "_PIPELINE_CHUNKS", 5)
+    rng = np.random.default_rng(44)
+    x = rng.uniform(-1, 1, 70_001).astype(np.float32)
+    h = rng.standard_normal(3_333).astype(np.float32)
+    xp = torch.from_numpy(x).pin_memory()
+    out = scatter_convolve(Signal(xp), Signal(torch.from_numpy(h)), mode=mode)
+    assert out.body.samples.is_pinned() and len(out.body) == len(x) and len(out.tail) == len(h) - 1
+    y = out.concatenated().samples
+    assert err_frac(y.numpy(), O.scatter_window(x, h, 0, len(y)), x, h) <= 1.0
 
 
 def test_tc_deterministic():
