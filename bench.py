@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="cfg5",
                     choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "short8", "short16", "short32",
-                             "short64", "short128"])
+                             "short64", "short128", "mstream"])
     ap.add_argument("--mode", default="fast", choices=["fast", "ffma", "tc"],
                     help="float32 kernel: fast = picked by shape (tensor cores for long filters)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -211,6 +211,26 @@ class Work:
             self.parallelism = f"replicas x{world}"
             self.scaling = "weak"
             self.dtype = "f32"
+        elif cfg == "mstream":
+            # cfg4's 64 channels streamed through ONE
+            # multichannel engine (blocks of 8192 = the reference default,
+            # engine.py:33), ordered chain, IR swapped halfway (cli.py --swap-ir)
+            w = configs.cfg4()
+            self.w = w
+            self.total_macs = w.metric_macs * world
+            self.rank_macs = w.metric_macs
+            self.xd = torch.from_numpy(w.x).to(device)
+            self.hd = torch.from_numpy(w.h).to(device)
+            self.hd2 = torch.flip(self.hd, dims=[1]).contiguous()
+            n_blocks = -(-w.ne // 8192)
+            self.swaps = [(0, self.hd), (n_blocks // 2, self.hd2)]
+            from paper_2401_01607_b200.engine import EngineConfig
+            from paper_2401_01607_b200.multichannel import MultiChannelEngine
+
+            self.eng = MultiChannelEngine(self.hd, EngineConfig(block_size_nb=8192))
+            self.parallelism = f"replicas x{world} (one 64-channel engine per GPU)"
+            self.scaling = "weak"
+            self.dtype = "f32"
         elif cfg == "cfg2":
             w = configs.cfg2()
             self.w = w
@@ -277,6 +297,10 @@ class Work:
             return body
         if self.cfg.startswith("short"):
             return scatter_convolve(Signal(self.xd), Signal(self.hd), mode=self.mode).body.samples
+        if self.cfg == "mstream":
+            body = self.eng.process_stream(self.xd, 8192, self.swaps)
+            self.eng.flush()
+            return body
         raise ValueError(self.cfg)
 
     def e2e_step(self, x_pin, h_pin):

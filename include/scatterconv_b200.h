@@ -125,6 +125,17 @@ typedef struct sc_engine sc_engine;
  * h is a device pointer; it is copied. */
 int sc_engine_create(int dtype, const void *h, int64_t nh, int64_t block_size_nb,
                      double threshold, void *stream, sc_engine **out);
+
+/* C engines that advance together (one per channel -- the reference's
+ * multichannel pattern, engine.py:60-66, cli.py:186-202 -- in one launch per
+ * block).  h is [channels][nh] row-major.  Every
+ * sample array of the calls below is then [channels][n] row-major, and the
+ * per-channel outputs of _flush / _state / _schedule (n_tail, read_index,
+ * live, cap, n_written) are arrays of `channels` entries; each channel keeps
+ * its own live / cap / read_index.  channels = 1 is sc_engine_create. */
+int sc_engine_create_multi(int dtype, const void *h, int64_t nh, int64_t channels,
+                           int64_t block_size_nb, double threshold, void *stream, sc_engine **out);
+int sc_engine_channels(sc_engine *e, int64_t *channels);
 int sc_engine_destroy(sc_engine *e);
 int sc_engine_set_stream(sc_engine *e, void *stream);
 

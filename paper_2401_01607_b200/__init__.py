@@ -30,7 +30,7 @@ from .core import (
     scatter_convolve_skip_zeros,
 )
 from .engine import DEFAULT_BLOCK_SIZE, TAIL_POLICIES, EngineConfig, ScatterEngine
-from .multichannel import convolve_batched
+from .multichannel import MultiChannelEngine, convolve_batched
 from .sharded import (
     Shard,
     convolve_shard,
@@ -64,6 +64,7 @@ __all__ = [
     "ConvOutput",
     "DEFAULT_BLOCK_SIZE",
     "EngineConfig",
+    "MultiChannelEngine",
     "ScatterEngine",
     "Shard",
     "Signal",

@@ -40,6 +40,9 @@ _SIGNATURES = {
                          ctypes.c_double, _p64, _p64, _vp],
     "sc_engine_create": [ctypes.c_int, _vp, _i64, _i64, ctypes.c_double, _vp,
                          ctypes.POINTER(_vp)],
+    "sc_engine_create_multi": [ctypes.c_int, _vp, _i64, _i64, _i64, ctypes.c_double, _vp,
+                               ctypes.POINTER(_vp)],
+    "sc_engine_channels": [_vp, _p64],
     "sc_engine_destroy": [_vp],
     "sc_engine_set_stream": [_vp, _vp],
     "sc_engine_process_block": [_vp, _vp, _i64, _vp],

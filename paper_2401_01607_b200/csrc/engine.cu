@@ -1,6 +1,7 @@
 // engine.cu -- device-resident streaming engine (ScatterEngine,
-// pkg/src/scatterconv/engine.py:60-214) and the literal scatter_block
-// drop-in (_kernels.py:14-52).
+// pkg/src/scatterconv/engine.py:60-214), its multichannel batch (SURVEY.md
+// 8(f)1: one engine per channel, engine.py:60-66 / cli.py:186-202, in ONE
+// launch per block), and the literal scatter_block drop-in (_kernels.py:14-52).
 //
 // Residue layout.  The reference keeps a circular ring of cap slots and a
 // read index (engine.py:75-79).  On the device we keep the same residue in
@@ -16,10 +17,16 @@
 // State that the reference updates data-dependently -- `live` (engine.py
 // :78-79 / _kernels.py:43-51), and through it `cap` on a swap
 // (engine.py:179) and `read_index` -- lives in device memory and is updated
-// by a one-CTA epilogue kernel, so process_block, swap_ir and the deferred
+// by small epilogue kernels, so process_block, swap_ir and the deferred
 // swap never wait on the host.  The host keeps only an upper bound of cap
 // (to size launches and buffers) and the sample counter.
+//
+// Channels: every per-engine array is [C][ld] (ld = its capacity) and every
+// kernel runs grid.y = C (or one thread per channel), so C engines that share
+// block size, IR length and swap times -- the reference CLI's per-channel
+// loop -- advance together.  Each channel keeps its own live/cap/read_index.
 
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -31,16 +38,19 @@ namespace {
 
 enum { ST_LIVE = 0, ST_CAP = 1, ST_RI = 2, ST_N = 4 };
 
-// live/read_index after a block (see the derivation in DESIGN.md): with
-// J = last index whose sample scatters (-1 if none),
+// live/read_index after a block (derivation in DESIGN.md): with J = last
+// index whose sample scatters (-1 if none),
 //   live' = max(0, live - n, J >= 0 ? nh - n + J : 0);  ri' = (ri + n) % cap.
+// One CTA per channel.
 template <typename T, int SKIP>
-__global__ void k_block_epilogue(const T *__restrict__ x, int64_t n, double thr, int64_t nh,
+__global__ void k_block_epilogue(const T *__restrict__ x, int64_t ldx, int64_t n, double thr, int64_t nh,
                                  int64_t *__restrict__ st) {
+    const T *xc = x + blockIdx.x * ldx;
+    int64_t *s = st + blockIdx.x * ST_N;
     __shared__ long long sj[32];
     long long J = -1;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
-        if (!skipped<SKIP>(x[i], thr)) J = i > J ? i : J;
+        if (!skipped<SKIP>(xc[i], thr)) J = i > J ? i : J;
     for (int o = 16; o > 0; o >>= 1) {
         const long long v = __shfl_xor_sync(0xffffffffu, J, o);
         J = v > J ? v : J;
@@ -49,24 +59,30 @@ __global__ void k_block_epilogue(const T *__restrict__ x, int64_t n, double thr,
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) J = sj[w] > J ? sj[w] : J;
-        int64_t live = st[ST_LIVE] - n;
+        int64_t live = s[ST_LIVE] - n;
         if (live < 0) live = 0;
         if (J >= 0 && nh - n + J > live) live = nh - n + J;
-        st[ST_LIVE] = live;
-        st[ST_RI] = (st[ST_RI] + n) % st[ST_CAP];
+        s[ST_LIVE] = live;
+        s[ST_RI] = (s[ST_RI] + n) % s[ST_CAP];
     }
 }
 
-__global__ void k_swap_state(int64_t *st, int64_t nh_new) {
-    const int64_t live = st[ST_LIVE];
-    st[ST_CAP] = nh_new > live ? nh_new : live;  // engine.py:179
-    st[ST_RI] = 0;                               // engine.py:184
+__global__ void k_swap_state(int64_t *st, int64_t nh_new, int64_t C) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    int64_t *s = st + c * ST_N;
+    const int64_t live = s[ST_LIVE];
+    s[ST_CAP] = nh_new > live ? nh_new : live;  // engine.py:179
+    s[ST_RI] = 0;                               // engine.py:184
 }
 
-__global__ void k_reset_state(int64_t *st, int64_t nh) {
-    st[ST_LIVE] = 0;
-    st[ST_CAP] = nh;
-    st[ST_RI] = 0;
+__global__ void k_reset_state(int64_t *st, int64_t nh, int64_t C) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    int64_t *s = st + c * ST_N;
+    s[ST_LIVE] = 0;
+    s[ST_CAP] = nh;
+    s[ST_RI] = 0;
 }
 
 template <typename T>
@@ -85,6 +101,18 @@ __global__ void k_sched_to_ring(const T *__restrict__ sched, int64_t cap, int64_
 
 size_t esize(int dtype) { return dtype == SC_F64 ? 8 : 4; }
 
+int launch_epilogue(int dtype, const void *x, int64_t ldx, int64_t n, double thr, int64_t nh, int64_t *st,
+                    int64_t C, cudaStream_t s) {
+    if (dtype == SC_F64)
+        k_block_epilogue<double, SC_SKIP_NOT_GT><<<(unsigned)C, 1024, 0, s>>>(static_cast<const double *>(x), ldx,
+                                                                             n, thr, nh, st);
+    else
+        k_block_epilogue<float, SC_SKIP_NOT_GT><<<(unsigned)C, 1024, 0, s>>>(static_cast<const float *>(x), ldx, n,
+                                                                            thr, nh, st);
+    SC_CHECK_LAUNCH();
+    return SC_OK;
+}
+
 // ---- fused multi-block streaming (sc_engine_process_blocks)
 
 constexpr int kMaxEvents = kMaxSegs - 1;  // IR changes per fused launch
@@ -95,16 +123,18 @@ struct StreamEvents {
     int64_t nh[kMaxEvents];        // new IR length
 };
 
-// J[b] = last index (within block b) whose sample scatters, -1 if none.
+// J[c*n_blocks + b] = last index (within block b of channel c) whose sample
+// scatters, -1 if none.  grid (n_blocks, C).
 template <typename T>
-__global__ void k_blocks_last_scatter(const T *__restrict__ x, int64_t n_total, int64_t nb, double thr,
-                                      int64_t *__restrict__ J) {
+__global__ void k_blocks_last_scatter(const T *__restrict__ x, int64_t ldx, int64_t n_total, int64_t nb,
+                                      double thr, int64_t n_blocks, int64_t *__restrict__ J) {
     const int64_t b = blockIdx.x;
+    const T *xc = x + blockIdx.y * ldx;
     const int64_t s = b * nb;
     const int64_t n = n_total - s < nb ? n_total - s : nb;
     long long j = -1;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
-        if (!skipped<SC_SKIP_NOT_GT>(x[s + i], thr)) j = i > j ? i : j;
+        if (!skipped<SC_SKIP_NOT_GT>(xc[s + i], thr)) j = i > j ? i : j;
     for (int o = 16; o > 0; o >>= 1) {
         const long long v = __shfl_xor_sync(0xffffffffu, j, o);
         j = v > j ? v : j;
@@ -114,16 +144,21 @@ __global__ void k_blocks_last_scatter(const T *__restrict__ x, int64_t n_total, 
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) j = sj[w] > j ? sj[w] : j;
-        J[b] = j;
+        J[blockIdx.y * n_blocks + b] = j;
     }
 }
 
-// Replays engine.py's bookkeeping over all blocks of the call: each swap
-// (cap = max(nh, live), ri = 0; engine.py:179-184) and each block
-// (live' = max(0, live - n, J >= 0 ? nh - n + J : 0), ri' = (ri + n) % cap).
+// Replays engine.py's bookkeeping over all blocks of the call, one thread per
+// channel: each swap (cap = max(nh, live), ri = 0; engine.py:179-184) and
+// each block (live' = max(0, live - n, J >= 0 ? nh - n + J : 0),
+// ri' = (ri + n) % cap).
 __global__ void k_stream_state(const int64_t *__restrict__ J, int64_t n_blocks, int64_t nb, int64_t n_total,
-                               int64_t nh0, StreamEvents ev, int64_t *st) {
-    int64_t live = st[0], cap = st[1], ri = st[2], nh = nh0;
+                               int64_t nh0, StreamEvents ev, int64_t *st, int64_t C) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    int64_t *s = st + c * ST_N;
+    const int64_t *Jc = J + c * n_blocks;
+    int64_t live = s[ST_LIVE], cap = s[ST_CAP], ri = s[ST_RI], nh = nh0;
     int64_t k = 0;
     for (int64_t b = 0; b < n_blocks; ++b) {
         while (k < ev.n && ev.block[k] == b) {
@@ -133,28 +168,16 @@ __global__ void k_stream_state(const int64_t *__restrict__ J, int64_t n_blocks, 
             ++k;
         }
         const int64_t n = n_total - b * nb < nb ? n_total - b * nb : nb;
-        const int64_t j = J[b];
+        const int64_t j = Jc[b];
         int64_t l = live - n;
         if (l < 0) l = 0;
         if (j >= 0 && nh - n + j > l) l = nh - n + j;
         live = l;
         ri = (ri + n) % cap;
     }
-    st[0] = live;
-    st[1] = cap;
-    st[2] = ri;
-}
-
-int launch_epilogue(int dtype, const void *x, int64_t n, double thr, int64_t nh, int64_t *st,
-                    cudaStream_t s) {
-    if (dtype == SC_F64)
-        k_block_epilogue<double, SC_SKIP_NOT_GT><<<1, 1024, 0, s>>>(static_cast<const double *>(x),
-                                                                    n, thr, nh, st);
-    else
-        k_block_epilogue<float, SC_SKIP_NOT_GT><<<1, 1024, 0, s>>>(static_cast<const float *>(x), n,
-                                                                   thr, nh, st);
-    SC_CHECK_LAUNCH();
-    return SC_OK;
+    s[ST_LIVE] = live;
+    s[ST_CAP] = cap;
+    s[ST_RI] = ri;
 }
 
 }  // namespace
@@ -167,103 +190,122 @@ struct sc_engine {
     size_t es = 4;
     int device = 0;
     cudaStream_t stream = nullptr;
+    int64_t C = 1;  // channels
     int64_t nb = 8192;
     double thr = 0.0;
-    // current impulse response (engine-owned copy)
+    // current impulse response, engine-owned copy: [C][ir_ld]
     void *ir = nullptr;
-    int64_t nh = 0, ir_capacity = 0;
-    // pending impulse response (swap_ir_at_next_block)
+    int64_t nh = 0, ir_ld = 0;
+    // pending impulse response (swap_ir_at_next_block): [C][pend_ld]
     void *pend = nullptr;
-    int64_t pend_nh = 0, pend_capacity = 0;
+    int64_t pend_nh = 0, pend_ld = 0;
     bool has_pending = false;
-    // residue in schedule order, ping-pong; buffers hold res_capacity samples
+    // residue in schedule order, ping-pong: [C][res_ld]
     void *res[2] = {nullptr, nullptr};
     int cur = 0;
-    int64_t res_capacity = 0;
-    int64_t cap_ub = 0;  // host upper bound of the device-side logical cap
-    int64_t *st = nullptr;  // device: live, cap, read_index
+    int64_t res_ld = 0;
+    int64_t cap_ub = 0;     // host upper bound of every channel's logical cap
+    int64_t *st = nullptr;  // device [C][ST_N]: live, cap, read_index
     int64_t consumed = 0;
-    // staging copies of the IRs of one fused process_blocks call
+    // staging copies of the IRs of one fused process_blocks call: [C][stage_ld]
     void *stage = nullptr;
-    int64_t stage_capacity = 0;
-    int64_t *jbuf = nullptr;  // per-block last-scatter index (device)
-    int64_t jbuf_capacity = 0;
+    int64_t stage_ld = 0;
+    int64_t *jbuf = nullptr;  // [C][n_blocks] last-scatter index per block
+    int64_t jbuf_ld = 0;
 };
 
 namespace {
 
-int ensure_buffer(void **p, int64_t *capacity, int64_t want, size_t es, bool keep, int64_t keep_n,
-                  cudaStream_t s) {
-    if (*capacity >= want) return SC_OK;
+// Grow a [C][ld] buffer to [C][want], keeping the first keep_n samples of
+// every row; new samples are zero.
+int ensure_2d(void **p, int64_t *ld, int64_t want, size_t es, int64_t C, int64_t keep_n, cudaStream_t s) {
+    if (*ld >= want) return SC_OK;
     void *np = nullptr;
-    if (cudaMalloc(&np, (size_t)want * es) != cudaSuccess) {
+    if (cudaMalloc(&np, (size_t)want * es * C) != cudaSuccess) {
         cudaGetLastError();
-        set_error("engine: cudaMalloc(%lld samples) failed", (long long)want);
+        set_error("engine: cudaMalloc(%lld x %lld samples) failed", (long long)C, (long long)want);
         return SC_ERR_ALLOC;
     }
-    SC_CHECK_CUDA(cudaMemsetAsync(np, 0, (size_t)want * es, s));
+    SC_CHECK_CUDA(cudaMemsetAsync(np, 0, (size_t)want * es * C, s));
     if (*p) {
-        if (keep && keep_n > 0)
-            SC_CHECK_CUDA(cudaMemcpyAsync(np, *p, (size_t)keep_n * es, cudaMemcpyDeviceToDevice, s));
+        if (keep_n > 0)
+            SC_CHECK_CUDA(cudaMemcpy2DAsync(np, (size_t)want * es, *p, (size_t)(*ld) * es, (size_t)keep_n * es,
+                                            (size_t)C, cudaMemcpyDeviceToDevice, s));
         SC_CHECK_CUDA(cudaStreamSynchronize(s));  // old buffer may still be read
         cudaFree(*p);
     }
     *p = np;
-    *capacity = want;
+    *ld = want;
     return SC_OK;
 }
+
+// rows of n samples: dst[c*dld + i] = src[c*sld + i]
+int copy_rows(sc_engine *e, void *dst, int64_t dld, const void *src, int64_t sld, int64_t n) {
+    if (n <= 0) return SC_OK;
+    SC_CHECK_CUDA(cudaMemcpy2DAsync(dst, (size_t)dld * e->es, src, (size_t)sld * e->es, (size_t)n * e->es,
+                                    (size_t)e->C, cudaMemcpyDeviceToDevice, e->stream));
+    return SC_OK;
+}
+
+unsigned cgrid(int64_t C) { return (unsigned)cdiv(C, 128); }
 
 int grow_residue(sc_engine *e, int64_t want) {
-    if (e->res_capacity >= want) return SC_OK;
-    int64_t cap0 = e->res_capacity, cap1 = e->res_capacity;
-    int rc = ensure_buffer(&e->res[e->cur], &cap0, want, e->es, true, e->cap_ub, e->stream);
+    if (e->res_ld >= want) return SC_OK;
+    int64_t ld0 = e->res_ld, ld1 = e->res_ld;
+    int rc = ensure_2d(&e->res[e->cur], &ld0, want, e->es, e->C, e->cap_ub, e->stream);
     if (rc) return rc;
-    rc = ensure_buffer(&e->res[1 - e->cur], &cap1, want, e->es, false, 0, e->stream);
+    rc = ensure_2d(&e->res[1 - e->cur], &ld1, want, e->es, e->C, 0, e->stream);
     if (rc) return rc;
-    e->res_capacity = want;
+    e->res_ld = want;
     return SC_OK;
 }
 
-// swap_ir core (engine.py:163-186) with h already in device memory.
-int do_swap(sc_engine *e, const void *h, int64_t nh) {
-    int rc = ensure_buffer(&e->ir, &e->ir_capacity, nh, e->es, false, 0, e->stream);
-    if (rc) return rc;
-    if (h != e->ir)
-        SC_CHECK_CUDA(cudaMemcpyAsync(e->ir, h, (size_t)nh * e->es, cudaMemcpyDeviceToDevice, e->stream));
+// swap_ir core (engine.py:163-186): h is [C][h_ld] in device memory.
+int do_swap(sc_engine *e, const void *h, int64_t h_ld, int64_t nh) {
+    if (h != e->ir) {
+        int rc = ensure_2d(&e->ir, &e->ir_ld, nh, e->es, e->C, 0, e->stream);
+        if (rc) return rc;
+        rc = copy_rows(e, e->ir, e->ir_ld, h, h_ld, nh);
+        if (rc) return rc;
+    }
     // new cap = max(nh, live) <= max(nh, cap_ub): grow buffers on the host bound only
     const int64_t ub = nh > e->cap_ub ? nh : e->cap_ub;
-    rc = grow_residue(e, ub);
+    int rc = grow_residue(e, ub);
     if (rc) return rc;
     e->cap_ub = ub;
     e->nh = nh;
-    k_swap_state<<<1, 1, 0, e->stream>>>(e->st, nh);
+    k_swap_state<<<cgrid(e->C), 128, 0, e->stream>>>(e->st, nh, e->C);
     SC_CHECK_LAUNCH();
     return SC_OK;
 }
 
-int do_block(sc_engine *e, const void *block, int64_t n, void *out, bool apply_pending) {
+// One block of n samples per channel: block/out are [C][ld].
+int do_block(sc_engine *e, const void *block, int64_t ldx, int64_t n, void *out, int64_t ldo, bool apply_pending) {
     if (apply_pending && e->has_pending) {
         e->has_pending = false;
-        int rc = do_swap(e, e->pend, e->pend_nh);
+        int rc = do_swap(e, e->pend, e->pend_ld, e->pend_nh);
         if (rc) return rc;
     }
     SC_REQUIRE(n <= e->nb, "block of %lld samples exceeds block_size_nb=%lld", (long long)n,
                (long long)e->nb);
     if (n == 0) return SC_OK;
     ChainSeg seg{e->ir, e->nh, 0, n};
+    ChainBatch batch{e->C, ldx, e->ir_ld, ldo, e->res_ld, e->res_ld, ST_N};
     void *rin = e->res[e->cur], *rout = e->res[1 - e->cur];
-    int rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, block, 0, &seg, 1, rin, 0,
-                          e->st + ST_CAP, 0, n + e->cap_ub, out, n, rout, e->stream);
+    int rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, block, 0, &seg, 1, rin, 0, e->st + ST_CAP, 0,
+                          n + e->cap_ub, out, n, rout, e->stream, nullptr, &batch);
     if (rc) return rc;
-    rc = launch_epilogue(e->dtype, block, n, e->thr, e->nh, e->st, e->stream);
+    rc = launch_epilogue(e->dtype, block, ldx, n, e->thr, e->nh, e->st, e->C, e->stream);
     if (rc) return rc;
     e->cur = 1 - e->cur;
     e->consumed += n;
     return SC_OK;
 }
 
-int read_state(sc_engine *e, int64_t host[ST_N]) {
-    SC_CHECK_CUDA(cudaMemcpyAsync(host, e->st, sizeof(int64_t) * ST_N, cudaMemcpyDeviceToHost, e->stream));
+int read_state(sc_engine *e, std::vector<int64_t> &host) {
+    host.assign((size_t)(ST_N * e->C), 0);
+    SC_CHECK_CUDA(cudaMemcpyAsync(host.data(), e->st, sizeof(int64_t) * ST_N * e->C, cudaMemcpyDeviceToHost,
+                                  e->stream));
     SC_CHECK_CUDA(cudaStreamSynchronize(e->stream));
     return SC_OK;
 }
@@ -281,14 +323,134 @@ struct DeviceGuard {
     }
 };
 
+// Fused back-to-back blocks (see sc_engine_process_blocks); x/out are
+// [C][ldx]/[C][ldo] rows of n_total samples.
+int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64_t nb,
+                        const int64_t *swap_blocks, const void *const *swap_irs, const int64_t *swap_nh,
+                        const int64_t *swap_ld, int64_t n_swaps, void *out, int64_t ldo) {
+    if (n_total == 0) return SC_OK;
+    const int64_t n_blocks = cdiv(n_total, nb);
+    // IR timeline: (block, h [C][nh], nh); a pending deferred swap acts right
+    // before block 0, after any explicit swap scheduled there (engine.py:124-126).
+    struct Ev {
+        int64_t block;
+        const void *h;
+        int64_t ld, nh;
+    };
+    std::vector<Ev> ev;
+    for (int64_t i = 0; i < n_swaps; ++i)
+        if (swap_blocks[i] >= 0 && swap_blocks[i] < n_blocks)
+            ev.push_back({swap_blocks[i], swap_irs[i], swap_ld ? swap_ld[i] : swap_nh[i], swap_nh[i]});
+    if (e->has_pending) {
+        size_t pos = 0;
+        while (pos < ev.size() && ev[pos].block == 0) ++pos;
+        ev.insert(ev.begin() + pos, Ev{0, e->pend, e->pend_ld, e->pend_nh});
+        e->has_pending = false;
+    }
+    // Too many IR changes for one launch: process consecutive block ranges.
+    if ((int64_t)ev.size() > kMaxEvents) {
+        int64_t b0 = 0;
+        size_t k = 0;
+        while (b0 < n_blocks) {
+            const size_t k1 = std::min(ev.size(), k + kMaxEvents);
+            int64_t b1 = k1 < ev.size() ? ev[k1].block : n_blocks;
+            if (b1 <= b0) b1 = b0 + 1;
+            std::vector<int64_t> sb, sn, sl;
+            std::vector<const void *> sh;
+            for (; k < ev.size() && ev[k].block < b1; ++k) {
+                sb.push_back(ev[k].block - b0);
+                sh.push_back(ev[k].h);
+                sn.push_back(ev[k].nh);
+                sl.push_back(ev[k].ld);  // the pending IR lives in a pitched buffer
+            }
+            const int64_t s0 = b0 * nb, s1 = std::min(n_total, b1 * nb);
+            int rc = process_blocks_impl(e, static_cast<const char *>(x) + (size_t)s0 * e->es, ldx, s1 - s0, nb,
+                                         sb.data(), sh.data(), sn.data(), sl.data(), (int64_t)sb.size(),
+                                         static_cast<char *>(out) + (size_t)s0 * e->es, ldo);
+            if (rc) return rc;
+            b0 = b1;
+        }
+        return SC_OK;
+    }
+    // Stage every IR of the timeline in engine-owned memory (the kernels run
+    // after this call returns; callers may free their buffers): [C][stage_ld].
+    int64_t tot = e->nh;
+    for (const Ev &v : ev) tot += v.nh;
+    int rc = ensure_2d(&e->stage, &e->stage_ld, tot, e->es, e->C, 0, e->stream);
+    if (rc) return rc;
+    rc = ensure_2d(reinterpret_cast<void **>(&e->jbuf), &e->jbuf_ld, n_blocks * e->C, 8, 1, 0, e->stream);
+    if (rc) return rc;
+    char *stage = static_cast<char *>(e->stage);
+    rc = copy_rows(e, stage, e->stage_ld, e->ir, e->ir_ld, e->nh);
+    if (rc) return rc;
+    ChainSeg segs[kMaxSegs];
+    int nseg = 0;
+    segs[nseg++] = ChainSeg{stage, e->nh, 0, n_total};
+    int64_t off = e->nh, ub = e->cap_ub;
+    StreamEvents sev{};
+    sev.n = 0;
+    for (const Ev &v : ev) {
+        char *dst = stage + (size_t)off * e->es;
+        rc = copy_rows(e, dst, e->stage_ld, v.h, v.ld, v.nh);
+        if (rc) return rc;
+        const int64_t m = v.block * nb;
+        if (segs[nseg - 1].m_lo == m) {
+            segs[nseg - 1].h = dst;  // a later swap before the same block wins
+            segs[nseg - 1].nh = v.nh;
+        } else {
+            segs[nseg - 1].m_hi = m;
+            segs[nseg++] = ChainSeg{dst, v.nh, m, n_total};
+        }
+        sev.block[sev.n] = v.block;
+        sev.nh[sev.n] = v.nh;
+        ++sev.n;
+        off += v.nh;
+        ub = v.nh > ub ? v.nh : ub;
+    }
+    rc = grow_residue(e, ub);
+    if (rc) return rc;
+    // One ordered launch for every block: slot t accumulates its drive samples
+    // in ascending order across blocks and IR segments -- the same chain as
+    // block-by-block processing (bit-identical), continued from the residue.
+    void *rin = e->res[e->cur], *rout = e->res[1 - e->cur];
+    ChainBatch batch{e->C, ldx, e->stage_ld, ldo, e->res_ld, e->res_ld, ST_N};
+    rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, x, 0, segs, nseg, rin, 0, e->st + ST_CAP, 0, n_total + ub,
+                      out, n_total, rout, e->stream, nullptr, &batch);
+    if (rc) return rc;
+    const dim3 gj((unsigned)n_blocks, (unsigned)e->C);
+    if (e->dtype == SC_F64)
+        k_blocks_last_scatter<double><<<gj, 256, 0, e->stream>>>(static_cast<const double *>(x), ldx, n_total, nb,
+                                                                e->thr, n_blocks, e->jbuf);
+    else
+        k_blocks_last_scatter<float><<<gj, 256, 0, e->stream>>>(static_cast<const float *>(x), ldx, n_total, nb,
+                                                               e->thr, n_blocks, e->jbuf);
+    SC_CHECK_LAUNCH();
+    k_stream_state<<<cgrid(e->C), 128, 0, e->stream>>>(e->jbuf, n_blocks, nb, n_total, e->nh, sev, e->st, e->C);
+    SC_CHECK_LAUNCH();
+    // host-side bookkeeping: the last IR becomes current (engine-owned copy)
+    const ChainSeg &last = segs[nseg - 1];
+    if (last.h != stage) {
+        rc = ensure_2d(&e->ir, &e->ir_ld, last.nh, e->es, e->C, 0, e->stream);
+        if (rc) return rc;
+        rc = copy_rows(e, e->ir, e->ir_ld, last.h, e->stage_ld, last.nh);
+        if (rc) return rc;
+        e->nh = last.nh;
+    }
+    e->cap_ub = ub;
+    e->cur = 1 - e->cur;
+    e->consumed += n_total;
+    return SC_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
-int sc_engine_create(int dtype, const void *h, int64_t nh, int64_t block_size_nb,
-                     double threshold, void *stream, sc_engine **out) {
+int sc_engine_create_multi(int dtype, const void *h, int64_t nh, int64_t channels, int64_t block_size_nb,
+                           double threshold, void *stream, sc_engine **out) {
     SC_REQUIRE(dtype == SC_F32 || dtype == SC_F64, "sc_engine_create: bad dtype %d", dtype);
     SC_REQUIRE(nh >= 1, "impulse response is empty");
+    SC_REQUIRE(channels >= 1 && channels < 65536, "channels must be in [1, 65535], got %lld", (long long)channels);
     SC_REQUIRE(block_size_nb >= 1, "block_size_nb must be >= 1, got %lld", (long long)block_size_nb);
     SC_REQUIRE(threshold >= 0.0, "zero_skip_threshold must be >= 0, got %g", threshold);
     SC_REQUIRE(h && out, "sc_engine_create: null pointer");
@@ -301,24 +463,22 @@ int sc_engine_create(int dtype, const void *h, int64_t nh, int64_t block_size_nb
     e->es = esize(dtype);
     cudaGetDevice(&e->device);
     e->stream = as_stream(stream);
+    e->C = channels;
     e->nb = block_size_nb;
     e->thr = threshold;
     int rc = SC_OK;
-    if (cudaMalloc(&e->st, sizeof(int64_t) * ST_N) != cudaSuccess) {
+    if (cudaMalloc(&e->st, sizeof(int64_t) * ST_N * channels) != cudaSuccess) {
         cudaGetLastError();
         set_error("sc_engine_create: cudaMalloc failed");
         rc = SC_ERR_ALLOC;
     }
-    if (!rc) rc = ensure_buffer(&e->ir, &e->ir_capacity, nh, e->es, false, 0, e->stream);
+    if (!rc) rc = ensure_2d(&e->ir, &e->ir_ld, nh, e->es, e->C, 0, e->stream);
     if (!rc) rc = grow_residue(e, nh);
-    if (!rc && cudaMemcpyAsync(e->ir, h, (size_t)nh * e->es, cudaMemcpyDeviceToDevice, e->stream) != cudaSuccess) {
-        set_error("sc_engine_create: copy of impulse response failed");
-        rc = SC_ERR_CUDA;
-    }
+    if (!rc) rc = copy_rows(e, e->ir, e->ir_ld, h, nh, nh);
     if (!rc) {
         e->nh = nh;
         e->cap_ub = nh;
-        k_reset_state<<<1, 1, 0, e->stream>>>(e->st, nh);
+        k_reset_state<<<cgrid(channels), 128, 0, e->stream>>>(e->st, nh, channels);
         if (cudaGetLastError() != cudaSuccess) rc = SC_ERR_CUDA;
     }
     if (rc) {
@@ -326,6 +486,17 @@ int sc_engine_create(int dtype, const void *h, int64_t nh, int64_t block_size_nb
         return rc;
     }
     *out = e;
+    return SC_OK;
+}
+
+int sc_engine_create(int dtype, const void *h, int64_t nh, int64_t block_size_nb, double threshold,
+                     void *stream, sc_engine **out) {
+    return sc_engine_create_multi(dtype, h, nh, 1, block_size_nb, threshold, stream, out);
+}
+
+int sc_engine_channels(sc_engine *e, int64_t *channels) {
+    SC_REQUIRE(e && channels, "null pointer");
+    *channels = e->C;
     return SC_OK;
 }
 
@@ -354,35 +525,31 @@ int sc_engine_process_block(sc_engine *e, const void *block, int64_t n, void *ou
     SC_REQUIRE(e, "null engine");
     SC_REQUIRE(n >= 0 && (n == 0 || (block && out)), "sc_engine_process_block: bad block");
     DeviceGuard g(e->device);
-    return do_block(e, block, n, out, true);
+    return do_block(e, block, n, n, out, n, true);
 }
 
 int sc_engine_process_sample(sc_engine *e, const void *x, void *out) {
     SC_REQUIRE(e && x && out, "sc_engine_process_sample: null pointer");
     DeviceGuard g(e->device);
-    // engine.py:99-116: one sample, a pending swap is NOT applied and the
-    // block-size limit does not apply.
-    const int64_t nb = e->nb;
-    e->nb = nb > 1 ? nb : 1;
-    const int rc = do_block(e, x, 1, out, false);
-    e->nb = nb;
-    return rc;
+    // engine.py:99-116: one sample per channel; a pending swap is NOT applied
+    return do_block(e, x, 1, 1, out, 1, false);
 }
 
 int sc_engine_swap_ir(sc_engine *e, const void *h, int64_t nh) {
     SC_REQUIRE(e && h, "sc_engine_swap_ir: null pointer");
     SC_REQUIRE(nh >= 1, "impulse response is empty");
     DeviceGuard g(e->device);
-    return do_swap(e, h, nh);
+    return do_swap(e, h, nh, nh);
 }
 
 int sc_engine_swap_ir_at_next_block(sc_engine *e, const void *h, int64_t nh) {
     SC_REQUIRE(e && h, "sc_engine_swap_ir_at_next_block: null pointer");
     SC_REQUIRE(nh >= 1, "impulse response is empty");
     DeviceGuard g(e->device);
-    int rc = ensure_buffer(&e->pend, &e->pend_capacity, nh, e->es, false, 0, e->stream);
+    int rc = ensure_2d(&e->pend, &e->pend_ld, nh, e->es, e->C, 0, e->stream);
     if (rc) return rc;
-    SC_CHECK_CUDA(cudaMemcpyAsync(e->pend, h, (size_t)nh * e->es, cudaMemcpyDeviceToDevice, e->stream));
+    rc = copy_rows(e, e->pend, e->pend_ld, h, nh, nh);
+    if (rc) return rc;
     e->pend_nh = nh;
     e->has_pending = true;
     return SC_OK;
@@ -391,38 +558,43 @@ int sc_engine_swap_ir_at_next_block(sc_engine *e, const void *h, int64_t nh) {
 int sc_engine_flush(sc_engine *e, void *tail, int64_t tail_capacity, int64_t *n_tail) {
     SC_REQUIRE(e && n_tail, "sc_engine_flush: null pointer");
     DeviceGuard g(e->device);
-    int64_t hs[ST_N];
+    std::vector<int64_t> hs;
     int rc = read_state(e, hs);
     if (rc) return rc;
-    const int64_t live = hs[ST_LIVE];
-    const int64_t nt = (e->nh - 1 > live) ? e->nh - 1 : live;  // engine.py:155
-    SC_REQUIRE(tail_capacity >= nt && (nt == 0 || tail), "sc_engine_flush: tail buffer too small (%lld < %lld)",
-               (long long)tail_capacity, (long long)nt);
-    if (nt > 0)
-        SC_CHECK_CUDA(cudaMemcpyAsync(tail, e->res[e->cur], (size_t)nt * e->es, cudaMemcpyDeviceToDevice,
-                                      e->stream));
+    int64_t nt_max = 0;
+    for (int64_t c = 0; c < e->C; ++c) {
+        const int64_t live = hs[c * ST_N + ST_LIVE];
+        n_tail[c] = (e->nh - 1 > live) ? e->nh - 1 : live;  // engine.py:155
+        nt_max = std::max(nt_max, n_tail[c]);
+    }
+    SC_REQUIRE(tail_capacity >= nt_max && (nt_max == 0 || tail), "sc_engine_flush: tail buffer too small (%lld < %lld)",
+               (long long)tail_capacity, (long long)nt_max);
+    // entries past a channel's own tail length are zero (beyond its live slots)
+    rc = copy_rows(e, tail, tail_capacity, e->res[e->cur], e->res_ld, nt_max);
+    if (rc) return rc;
     // reset (engine.py:157-160): zero ring of len(ir), ri = live = consumed = 0
-    SC_CHECK_CUDA(cudaMemsetAsync(e->res[0], 0, (size_t)e->res_capacity * e->es, e->stream));
-    SC_CHECK_CUDA(cudaMemsetAsync(e->res[1], 0, (size_t)e->res_capacity * e->es, e->stream));
-    k_reset_state<<<1, 1, 0, e->stream>>>(e->st, e->nh);
+    SC_CHECK_CUDA(cudaMemsetAsync(e->res[0], 0, (size_t)e->res_ld * e->es * e->C, e->stream));
+    SC_CHECK_CUDA(cudaMemsetAsync(e->res[1], 0, (size_t)e->res_ld * e->es * e->C, e->stream));
+    k_reset_state<<<cgrid(e->C), 128, 0, e->stream>>>(e->st, e->nh, e->C);
     SC_CHECK_LAUNCH();
     e->cap_ub = e->nh;
     e->consumed = 0;
     SC_CHECK_CUDA(cudaStreamSynchronize(e->stream));
-    *n_tail = nt;
     return SC_OK;
 }
 
-int sc_engine_state(sc_engine *e, int64_t *read_index, int64_t *live, int64_t *cap,
-                    int64_t *consumed, int64_t *nh, int *has_pending) {
+int sc_engine_state(sc_engine *e, int64_t *read_index, int64_t *live, int64_t *cap, int64_t *consumed,
+                    int64_t *nh, int *has_pending) {
     SC_REQUIRE(e, "null engine");
     DeviceGuard g(e->device);
-    int64_t hs[ST_N];
+    std::vector<int64_t> hs;
     int rc = read_state(e, hs);
     if (rc) return rc;
-    if (read_index) *read_index = hs[ST_RI];
-    if (live) *live = hs[ST_LIVE];
-    if (cap) *cap = hs[ST_CAP];
+    for (int64_t c = 0; c < e->C; ++c) {
+        if (read_index) read_index[c] = hs[c * ST_N + ST_RI];
+        if (live) live[c] = hs[c * ST_N + ST_LIVE];
+        if (cap) cap[c] = hs[c * ST_N + ST_CAP];
+    }
     if (consumed) *consumed = e->consumed;
     if (nh) *nh = e->nh;
     if (has_pending) *has_pending = e->has_pending ? 1 : 0;
@@ -432,16 +604,20 @@ int sc_engine_state(sc_engine *e, int64_t *read_index, int64_t *live, int64_t *c
 int sc_engine_schedule(sc_engine *e, void *dst, int64_t n, int64_t *n_written) {
     SC_REQUIRE(e && n_written, "null pointer");
     DeviceGuard g(e->device);
-    int64_t hs[ST_N];
+    std::vector<int64_t> hs;
     int rc = read_state(e, hs);
     if (rc) return rc;
-    const int64_t k = n < hs[ST_CAP] ? n : hs[ST_CAP];
-    if (k > 0) {
+    int64_t kmax = 0;
+    for (int64_t c = 0; c < e->C; ++c) {
+        n_written[c] = std::min(n, hs[c * ST_N + ST_CAP]);
+        kmax = std::max(kmax, n_written[c]);
+    }
+    if (kmax > 0) {
         SC_REQUIRE(dst, "null destination");
-        SC_CHECK_CUDA(cudaMemcpyAsync(dst, e->res[e->cur], (size_t)k * e->es, cudaMemcpyDeviceToDevice, e->stream));
+        rc = copy_rows(e, dst, n, e->res[e->cur], e->res_ld, kmax);
+        if (rc) return rc;
         SC_CHECK_CUDA(cudaStreamSynchronize(e->stream));
     }
-    *n_written = k;
     return SC_OK;
 }
 
@@ -451,7 +627,7 @@ int sc_engine_current_ir(sc_engine *e, void *dst, int64_t capacity, int64_t *nh)
     *nh = e->nh;
     if (dst) {
         SC_REQUIRE(capacity >= e->nh, "sc_engine_current_ir: buffer too small");
-        SC_CHECK_CUDA(cudaMemcpyAsync(dst, e->ir, (size_t)e->nh * e->es, cudaMemcpyDeviceToDevice, e->stream));
+        return copy_rows(e, dst, capacity, e->ir, e->ir_ld, e->nh);
     }
     return SC_OK;
 }
@@ -468,112 +644,8 @@ int sc_engine_process_blocks(sc_engine *e, const void *x, int64_t n_total, int64
         SC_REQUIRE(i == 0 || swap_blocks[i] >= swap_blocks[i - 1], "swap_blocks must be ascending");
     }
     DeviceGuard g(e->device);
-    if (n_total == 0) return SC_OK;
-    const int64_t n_blocks = cdiv(n_total, nb);
-    // IR timeline: (block, h, nh); a pending deferred swap acts right before
-    // block 0, after any explicit swap scheduled there (engine.py:124-126).
-    struct Ev {
-        int64_t block;
-        const void *h;
-        int64_t nh;
-    };
-    std::vector<Ev> ev;
-    for (int64_t i = 0; i < n_swaps; ++i)
-        if (swap_blocks[i] >= 0 && swap_blocks[i] < n_blocks) ev.push_back({swap_blocks[i], swap_irs[i], swap_nh[i]});
-    if (e->has_pending) {
-        size_t pos = 0;
-        while (pos < ev.size() && ev[pos].block == 0) ++pos;
-        ev.insert(ev.begin() + pos, Ev{0, e->pend, e->pend_nh});
-        e->has_pending = false;
-    }
-    // Too many IR changes for one launch: process in consecutive block ranges.
-    if ((int64_t)ev.size() > kMaxEvents) {
-        int64_t b0 = 0;
-        size_t k = 0;
-        while (b0 < n_blocks) {
-            size_t k1 = std::min(ev.size(), k + kMaxEvents);
-            int64_t b1 = k1 < ev.size() ? ev[k1].block : n_blocks;
-            if (b1 <= b0) b1 = b0 + 1;
-            std::vector<int64_t> sb;
-            std::vector<const void *> sh;
-            std::vector<int64_t> sn;
-            for (size_t q = k; q < ev.size() && ev[q].block < b1; ++q, ++k) {
-                sb.push_back(ev[q].block - b0);
-                sh.push_back(ev[q].h);
-                sn.push_back(ev[q].nh);
-            }
-            const int64_t s0 = b0 * nb, s1 = std::min(n_total, b1 * nb);
-            int rc = sc_engine_process_blocks(e, static_cast<const char *>(x) + (size_t)s0 * e->es, s1 - s0, nb,
-                                              sb.data(), sh.data(), sn.data(), (int64_t)sb.size(),
-                                              static_cast<char *>(out) + (size_t)s0 * e->es);
-            if (rc) return rc;
-            b0 = b1;
-        }
-        return SC_OK;
-    }
-    // Stage every IR of the timeline in engine-owned memory (the kernels run
-    // after this call returns; callers may free their buffers).
-    int64_t tot = e->nh;
-    for (const Ev &v : ev) tot += v.nh;
-    int rc = ensure_buffer(&e->stage, &e->stage_capacity, tot, e->es, false, 0, e->stream);
-    if (rc) return rc;
-    rc = ensure_buffer(reinterpret_cast<void **>(&e->jbuf), &e->jbuf_capacity, n_blocks, 8, false, 0, e->stream);
-    if (rc) return rc;
-    char *stage = static_cast<char *>(e->stage);
-    SC_CHECK_CUDA(cudaMemcpyAsync(stage, e->ir, (size_t)e->nh * e->es, cudaMemcpyDeviceToDevice, e->stream));
-    ChainSeg segs[kMaxSegs];
-    int nseg = 0;
-    segs[nseg++] = ChainSeg{stage, e->nh, 0, n_total};
-    int64_t off = e->nh, ub = e->cap_ub;
-    StreamEvents sev{};
-    sev.n = 0;
-    for (const Ev &v : ev) {
-        char *dst = stage + (size_t)off * e->es;
-        SC_CHECK_CUDA(cudaMemcpyAsync(dst, v.h, (size_t)v.nh * e->es, cudaMemcpyDeviceToDevice, e->stream));
-        const int64_t m = v.block * nb;
-        if (segs[nseg - 1].m_lo == m) {
-            segs[nseg - 1].h = dst;  // a later swap before the same block wins
-            segs[nseg - 1].nh = v.nh;
-        } else {
-            segs[nseg - 1].m_hi = m;
-            segs[nseg++] = ChainSeg{dst, v.nh, m, n_total};
-        }
-        sev.block[sev.n] = v.block;
-        sev.nh[sev.n] = v.nh;
-        ++sev.n;
-        off += v.nh;
-        ub = v.nh > ub ? v.nh : ub;
-    }
-    rc = grow_residue(e, ub);
-    if (rc) return rc;
-    // One ordered launch for every block: slot t accumulates its drive samples
-    // in ascending order across blocks and IR segments -- the same chain as
-    // block-by-block processing (bit-identical), continued from the residue.
-    void *rin = e->res[e->cur], *rout = e->res[1 - e->cur];
-    rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, x, 0, segs, nseg, rin, 0, e->st + ST_CAP, 0, n_total + ub,
-                      out, n_total, rout, e->stream);
-    if (rc) return rc;
-    if (e->dtype == SC_F64)
-        k_blocks_last_scatter<double><<<(unsigned)n_blocks, 256, 0, e->stream>>>(static_cast<const double *>(x), n_total,
-                                                                             nb, e->thr, e->jbuf);
-    else
-        k_blocks_last_scatter<float><<<(unsigned)n_blocks, 256, 0, e->stream>>>(static_cast<const float *>(x), n_total,
-                                                                            nb, e->thr, e->jbuf);
-    SC_CHECK_LAUNCH();
-    k_stream_state<<<1, 1, 0, e->stream>>>(e->jbuf, n_blocks, nb, n_total, e->nh, sev, e->st);
-    SC_CHECK_LAUNCH();
-    // host-side bookkeeping: last IR becomes current (engine-owned copy)
-    const ChainSeg &last = segs[nseg - 1];
-    if (last.h != stage) {
-        rc = ensure_buffer(&e->ir, &e->ir_capacity, last.nh, e->es, false, 0, e->stream);
-        if (rc) return rc;
-        SC_CHECK_CUDA(cudaMemcpyAsync(e->ir, last.h, (size_t)last.nh * e->es, cudaMemcpyDeviceToDevice, e->stream));
-        e->nh = last.nh;
-    }
-    e->cap_ub = ub;
-    e->cur = 1 - e->cur;
-    e->consumed += n_total;
-    return SC_OK;
+    return process_blocks_impl(e, x, n_total, n_total, nb, swap_blocks, swap_irs, swap_nh, nullptr, n_swaps, out,
+                               n_total);
 }
 
 // ---------------------------------------------------------------- literal kernel
@@ -612,7 +684,7 @@ int sc_scatter_block(int dtype, void *ring, int64_t cap, const void *ir, int64_t
     int rc = launch_chain(dtype, SC_SKIP_NOT_GT, threshold, block, 0, &seg, 1, sched_in, cap,
                           nullptr, 0, n + cap, out, n, sched_out, s);
     if (rc) return rc;
-    rc = launch_epilogue(dtype, block, n, threshold, nh, st, s);
+    rc = launch_epilogue(dtype, block, n, n, threshold, nh, st, 1, s);
     if (rc) return rc;
     const int64_t ri2 = (read_index + n) % cap;
     if (dtype == SC_F64)

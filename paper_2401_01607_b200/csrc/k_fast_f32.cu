@@ -387,14 +387,11 @@ int launch_fir_f32_fast(const float *x, int64_t ldx, int64_t x_base, int64_t x_l
     SC_REQUIRE(tiles < (int64_t)INT32_MAX, "fir: output range too large");
     const int64_t stages = nh_pad / FT_STAGE_TAPS;
 
-    static int slots_per_sm = -1;
-    if (slots_per_sm < 0) {
-        int nb = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fir_f32_fast, FT_THREADS, 0) !=
-                cudaSuccess || nb < 1)
-            nb = 1;
-        slots_per_sm = nb;
-    }
+    // queried per launch (cheap, host-only): thread-safe and per-device
+    int slots_per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&slots_per_sm, k_fir_f32_fast, FT_THREADS, 0) !=
+            cudaSuccess || slots_per_sm < 1)
+        slots_per_sm = 1;
     const int slots = sm_count() * slots_per_sm;
     const int nsplit = choose_splits(tiles * channels, stages, slots);
     const int64_t stages_per_split = cdiv(stages, nsplit);

@@ -42,6 +42,7 @@ struct ChainArgs {
     double thr;
     const unsigned *run_if;  // optional device gate: run only if *run_if != 0
     int64_t ldx, ldh, ldo;   // channel strides (grid.y = channel); 0 = one channel
+    int64_t ld_init, ld_outb, ld_st;
 };
 
 template <typename T, int SKIP>
@@ -54,7 +55,10 @@ __global__ void __launch_bounds__(TB) k_chain(ChainArgs<T> a) {
     const T *xb = a.x + blockIdx.y * a.ldx;
     T *outa = a.out_a + blockIdx.y * a.ldo;
     const int64_t hoff = blockIdx.y * a.ldh;
+    const T *initc = a.init ? a.init + blockIdx.y * a.ld_init : nullptr;
+    T *outb = a.out_b ? a.out_b + blockIdx.y * a.ld_outb : nullptr;
     const int64_t n_tiles = (a.n_out + TB - 1) / TB;
+    const int64_t init_len = a.init_len_dev ? a.init_len_dev[blockIdx.y * a.ld_st] : a.init_len;
     for (int64_t tb = blockIdx.x; tb < n_tiles; tb += gridDim.x) {
     __syncthreads();  // smem reuse across tiles of this CTA
     const int64_t tile0 = a.t0 + tb * TB;
@@ -62,10 +66,9 @@ __global__ void __launch_bounds__(TB) k_chain(ChainArgs<T> a) {
     const int64_t tile_last = (tile0 + TB < t_end ? tile0 + TB : t_end) - 1;
     const int64_t t = tile0 + threadIdx.x;
     const bool active = t < t_end;
-    const int64_t init_len = a.init_len_dev ? *a.init_len_dev : a.init_len;
 
     T acc = T(0);
-    if (active && a.init != nullptr && (t - a.t0) < init_len) acc = a.init[t - a.t0];
+    if (active && initc != nullptr && (t - a.t0) < init_len) acc = initc[t - a.t0];
 
     for (int s = 0; s < a.nseg; ++s) {
         const T *__restrict__ h = static_cast<const T *>(a.seg[s].h) + hoff;
@@ -107,8 +110,8 @@ __global__ void __launch_bounds__(TB) k_chain(ChainArgs<T> a) {
         const int64_t i = t - a.t0;
         if (i < a.n_a)
             outa[i] = acc;
-        else if (a.out_b != nullptr)
-            a.out_b[i - a.n_a] = acc;
+        else if (outb != nullptr)
+            outb[i - a.n_a] = acc;
     }
     }  // tiles
 }
@@ -144,9 +147,11 @@ __global__ void __launch_bounds__(RT_TB) k_chain_rt(ChainArgs<T> a) {
     const T *xb = a.x + blockIdx.y * a.ldx;
     T *outa = a.out_a + blockIdx.y * a.ldo;
     const int64_t hoff = blockIdx.y * a.ldh;
+    const T *initc = a.init ? a.init + blockIdx.y * a.ld_init : nullptr;
+    T *outb = a.out_b ? a.out_b + blockIdx.y * a.ld_outb : nullptr;
     const int64_t n_tiles = (a.n_out + RT_TILE - 1) / RT_TILE;
     const int64_t t_end = a.t0 + a.n_out;
-    const int64_t init_len = a.init_len_dev ? *a.init_len_dev : a.init_len;
+    const int64_t init_len = a.init_len_dev ? a.init_len_dev[blockIdx.y * a.ld_st] : a.init_len;
     for (int64_t tb = blockIdx.x; tb < n_tiles; tb += gridDim.x) {
         __syncthreads();
         const int64_t tile0 = a.t0 + tb * RT_TILE;
@@ -156,7 +161,7 @@ __global__ void __launch_bounds__(RT_TB) k_chain_rt(ChainArgs<T> a) {
 #pragma unroll
         for (int r = 0; r < RT_R; ++r) {
             const int64_t t = tj + r;
-            acc[r] = (a.init != nullptr && t < t_end && (t - a.t0) < init_len) ? a.init[t - a.t0] : T(0);
+            acc[r] = (initc != nullptr && t < t_end && (t - a.t0) < init_len) ? initc[t - a.t0] : T(0);
         }
         for (int s = 0; s < a.nseg; ++s) {
             const T *__restrict__ h = static_cast<const T *>(a.seg[s].h) + hoff;
@@ -212,8 +217,8 @@ __global__ void __launch_bounds__(RT_TB) k_chain_rt(ChainArgs<T> a) {
                 const int64_t i = t - a.t0;
                 if (i < a.n_a)
                     outa[i] = acc[r];
-                else if (a.out_b != nullptr)
-                    a.out_b[i - a.n_a] = acc[r];
+                else if (outb != nullptr)
+                    outb[i - a.n_a] = acc[r];
             }
         }
     }
@@ -248,7 +253,10 @@ int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off
         a.ldx = batch->ldx;
         a.ldh = batch->ldh;
         a.ldo = batch->ldo;
-        SC_REQUIRE(channels >= 1 && channels < 65536 && out_b == nullptr, "chain: bad batch");
+        a.ld_init = batch->ld_init;
+        a.ld_outb = batch->ld_outb;
+        a.ld_st = batch->ld_st;
+        SC_REQUIRE(channels >= 1 && channels < 65536, "chain: bad batch");
     }
     // Grid-stride over 256-output tiles.  A device-gated launch (run_if) is
     // usually a no-op, so it gets a small grid that exits in microseconds.

@@ -560,11 +560,9 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
         k_build_h8<<<g, 256, 0, stream>>>(h, ldh, nh, s8, ngroups, scales, h8_hi, h8_lo, h8_ch);
         SC_CHECK_LAUNCH();
     }
-    static bool attr_set = false;
-    if (!attr_set) {
-        SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_TOTAL));
-        attr_set = true;
-    }
+    // function attributes are per device (context): set on every launch so
+    // multi-GPU drivers (one host thread per device) never miss it
+    SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_TOTAL));
     TcArgs a;
     a.xt[0] = xt_hi;
     a.xt[1] = xt_lo;

@@ -101,10 +101,13 @@ int launch_chain(int dtype, int skip_mode, double threshold, const void *x, int6
                  int64_t n_a, void *out_b, cudaStream_t stream, const unsigned *run_if = nullptr,
                  const struct ChainBatch *batch = nullptr);
 
-// Optional channel batching for launch_chain (single-segment use): channel c
-// reads x + c*ldx and taps + c*ldh, and writes out_a + c*ldo.
+// Optional channel batching for launch_chain (grid.y = channel): channel c
+// reads x + c*ldx, every segment's taps + c*ldh, its residue init + c*ld_init
+// with length *(init_len_dev + c*ld_st), and writes out_a + c*ldo and
+// out_b + c*ld_outb.
 struct ChainBatch {
     int64_t channels, ldx, ldh, ldo;
+    int64_t ld_init = 0, ld_outb = 0, ld_st = 0;
 };
 
 // Fast FP32 FIR over an output range (see k_fast_f32.cu).  With run_if set,

@@ -46,3 +46,176 @@ def convolve_batched(x, h, mode=None):
                                  ne + nh - 1, C,
                                  ne, nh, N.stream_ptr()))
     return _dev.like_input(y, x, h)
+
+
+class MultiChannelEngine:
+    """C streaming engines that advance together, one per channel.
+
+    The reference runs one ``ScatterEngine`` per channel and loops over them
+    (engine.py:60-66; the CLI's per-channel loop, cli.py:186-202, with the
+    mono-IR broadcast of cli.py:147-155).  Here all channels share one
+    device engine: one launch per block for every channel, each channel with
+    its own residue, ``live``, ``cap`` and ``read_index`` (SURVEY.md 8(f)
+    row 1).  Semantics per channel are exactly ``ScatterEngine``'s
+    (bit-identical in float64).
+
+    h: [C, Nh] (or [Nh] with ``channels=C`` to broadcast a mono IR).
+    Blocks are [C, n] arrays/tensors; outputs come back in the same currency.
+    """
+
+    def __init__(self, h, config=None, *, channels=None, device=None):
+        import ctypes
+
+        from .engine import EngineConfig
+
+        t = _dev.torch()
+        self.config = config if config is not None else EngineConfig()
+        hd = h if _dev.is_tensor(h) else np.asarray(h)
+        npd = _dev.np_dtype(hd) if (_dev.is_tensor(hd) or hd.dtype in (np.float32, np.float64)) else np.float64
+        if hd.ndim == 1:
+            if channels is None:
+                raise ValueError("a 1-D impulse response needs channels=C to broadcast")
+            hd = hd[None, :].repeat(channels, 0) if not _dev.is_tensor(hd) else hd[None, :].expand(channels, -1)
+        if hd.shape[-1] == 0:
+            raise ValueError("impulse response is empty")
+        self._npd = npd
+        self._dt = N.dtype_code(npd)
+        self._device = t.device(device) if device is not None else t.device("cuda", t.cuda.current_device())
+        self._lib = N.lib()
+        self._C = int(hd.shape[0])
+        self._pending = None
+        h_dev = _dev.as_device(hd, npd, device=self._device).contiguous()
+        self._handle = ctypes.c_void_p()
+        with t.cuda.device(self._device):
+            N.check(self._lib.sc_engine_create_multi(self._dt, N.ptr(h_dev), h_dev.shape[1], self._C,
+                                                     int(self.config.block_size_nb),
+                                                     float(self.config.zero_skip_threshold),
+                                                     N.stream_ptr(), ctypes.byref(self._handle)))
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.sc_engine_destroy(h)
+            except Exception:  # pragma: no cover
+                pass
+            self._handle = None
+
+    @property
+    def channels(self) -> int:
+        return self._C
+
+    def _bind(self):
+        N.check(self._lib.sc_engine_set_stream(self._handle, N.stream_ptr()))
+
+    def _rows(self, a, n_expected=None):
+        d = _dev.as_device(a, self._npd, device=self._device)
+        if d.ndim == 1 and self._C == 1:
+            d = d[None, :]
+        if d.ndim != 2 or d.shape[0] != self._C:
+            raise ValueError(f"expected [channels={self._C}, n] samples, got shape {tuple(d.shape)}")
+        return d.contiguous()
+
+    def _ir_rows(self, h):
+        hd = h if _dev.is_tensor(h) else np.asarray(h)
+        if hd.ndim == 1:
+            hd = hd[None, :].repeat(self._C, 0) if not _dev.is_tensor(hd) else hd[None, :].expand(self._C, -1)
+        if hd.shape[-1] == 0:
+            raise ValueError("impulse response is empty")
+        return self._rows(hd)
+
+    def process_block(self, block):
+        """[C, n] in, [C, n] out (engine.py:118-146 per channel)."""
+        t = _dev.torch()
+        if self._pending is not None:
+            h_new, self._pending = self._pending, None
+            self.swap_ir(h_new)
+        with t.cuda.device(self._device):
+            xd = self._rows(block)
+            n = xd.shape[1]
+            if n > self.config.block_size_nb:
+                raise ValueError(f"block of {n} samples exceeds block_size_nb={self.config.block_size_nb}")
+            out = t.empty_like(xd)
+            if n:
+                self._bind()
+                N.check(self._lib.sc_engine_process_block(self._handle, N.ptr(xd), n, N.ptr(out)))
+        return _dev.like_input(out, block)
+
+    def process_sample(self, x):
+        """One sample per channel ([C]) -> [C] outputs (engine.py:99-116)."""
+        t = _dev.torch()
+        with t.cuda.device(self._device):
+            xd = _dev.as_device(np.asarray(x, dtype=self._npd).reshape(self._C, 1), self._npd, device=self._device)
+            out = t.empty_like(xd)
+            self._bind()
+            N.check(self._lib.sc_engine_process_sample(self._handle, N.ptr(xd), N.ptr(out)))
+            return out[:, 0].cpu().numpy()
+
+    def swap_ir(self, h_new):
+        """Every channel swaps to its row of h_new (or a broadcast mono IR)."""
+        t = _dev.torch()
+        with t.cuda.device(self._device):
+            hd = self._ir_rows(h_new)
+            self._bind()
+            N.check(self._lib.sc_engine_swap_ir(self._handle, N.ptr(hd), hd.shape[1]))
+
+    def swap_ir_at_next_block(self, h_new):
+        self._ir_rows(h_new)  # validate now (engine.py:188-192)
+        self._pending = h_new
+
+    def flush(self):
+        """Per-channel tails (max(len(ir)-1, live_c) samples each) as a list."""
+        import ctypes
+
+        t = _dev.torch()
+        with t.cuda.device(self._device):
+            st = self.state()
+            cap = max(max(st["cap"]), 1)
+            tail = t.empty((self._C, cap), dtype=_dev.torch_dtype(self._npd), device=self._device)
+            n = (ctypes.c_int64 * self._C)()
+            self._bind()
+            N.check(self._lib.sc_engine_flush(self._handle, N.ptr(tail), cap, n))
+            host = tail.cpu().numpy()
+        return [host[c, :n[c]].copy() for c in range(self._C)]
+
+    def state(self) -> dict:
+        import ctypes
+
+        C = self._C
+        ri, live, cap = (ctypes.c_int64 * C)(), (ctypes.c_int64 * C)(), (ctypes.c_int64 * C)()
+        cons, nh = ctypes.c_int64(), ctypes.c_int64()
+        pend = ctypes.c_int()
+        t = _dev.torch()
+        with t.cuda.device(self._device):
+            self._bind()
+            N.check(self._lib.sc_engine_state(self._handle, ri, live, cap, ctypes.byref(cons), ctypes.byref(nh),
+                                              ctypes.byref(pend)))
+        return {"read_index": list(ri), "live": list(live), "cap": list(cap), "consumed": cons.value,
+                "nh": nh.value}
+
+    def process_stream(self, x, nb=None, swaps=()):
+        """[C, N] through back-to-back blocks of nb with an IR-swap schedule
+        ((block_index, IR) pairs, applied to every channel) in one fused
+        launch per <= 31 swaps; bit-identical to the block-by-block calls."""
+        import ctypes
+
+        t = _dev.torch()
+        nb = self.config.block_size_nb if nb is None else int(nb)
+        if nb < 1 or nb > self.config.block_size_nb:
+            raise ValueError(f"nb must be in [1, block_size_nb={self.config.block_size_nb}]")
+        if self._pending is not None:
+            h_new, self._pending = self._pending, None
+            self.swap_ir(h_new)
+        with t.cuda.device(self._device):
+            xd = self._rows(x)
+            out = t.empty_like(xd)
+            swaps = sorted(swaps, key=lambda s: s[0])
+            irs = [self._ir_rows(s[1]) for s in swaps]
+            k = len(swaps)
+            blocks = (ctypes.c_int64 * max(k, 1))(*[int(s[0]) for s in swaps])
+            ptrs = (ctypes.c_void_p * max(k, 1))(*[ir.data_ptr() for ir in irs])
+            nhs = (ctypes.c_int64 * max(k, 1))(*[ir.shape[1] for ir in irs])
+            self._bind()
+            N.check(self._lib.sc_engine_process_blocks(self._handle, N.ptr(xd), xd.shape[1], nb, blocks, ptrs,
+                                                       nhs, k, N.ptr(out)))
+        return _dev.like_input(out, x)

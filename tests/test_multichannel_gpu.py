@@ -1,0 +1,104 @@
+"""Multichannel streaming engine vs one reference
+engine per channel (the oracle restatement of engine.py, pinned to the
+reference).  float64: bit-exact per channel, including per-channel `live`
+(one channel goes silent so its tail is shorter), swaps, deferred swaps,
+process_sample and the fused process_stream."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2401_01607_b200 import EngineConfig, MultiChannelEngine
+
+pytestmark = pytest.mark.gpu
+
+
+def _inputs(rng, C, n, dtype):
+    x = rng.uniform(-1, 1, (C, n)).astype(dtype)
+    x[rng.uniform(0, 1, (C, n)) < 0.15] = 0.0
+    x[1, n // 2:] = 0.0          # channel 1 falls silent: its live drains early
+    x[2, 7] = np.nan             # NaN input is skipped by the engine (_kernels.py:33)
+    return x
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_blocks_swaps_flush_per_channel(dtype):
+    rng = np.random.default_rng(3)
+    C, nb = 4, 50
+    h1 = rng.standard_normal((C, 40)).astype(dtype)
+    h2 = rng.standard_normal((C, 90)).astype(dtype)
+    h3 = rng.standard_normal((C, 15)).astype(dtype)
+    x = _inputs(rng, C, 600, dtype)
+    eng = MultiChannelEngine(h1, EngineConfig(block_size_nb=nb, zero_skip_threshold=0.05))
+    refs = [O.OracleEngine(h1[c], nb, 0.05) for c in range(C)]
+    got, want = [], [[] for _ in range(C)]
+    for b, s in enumerate(range(0, 600, nb)):
+        if b == 3:
+            eng.swap_ir(h2)
+            for c in range(C):
+                refs[c].swap_ir(h2[c])
+        if b == 7:
+            eng.swap_ir_at_next_block(h3)   # applied by the next process_block
+            for c in range(C):
+                refs[c].swap_ir_at_next_block(h3[c])
+        got.append(np.asarray(eng.process_block(x[:, s:s + nb])))
+        for c in range(C):
+            want[c].append(refs[c].process_block(x[c, s:s + nb]))
+    st = eng.state()
+    assert st["live"] == [r.live for r in refs]
+    assert st["read_index"] == [r.read_index for r in refs]
+    tails = eng.flush()
+    body = np.concatenate(got, axis=1)
+    for c in range(C):
+        w = np.concatenate(want[c])
+        wt = refs[c].flush()
+        assert len(tails[c]) == len(wt)
+        if dtype == np.float64:
+            assert np.array_equal(body[c], w) and np.array_equal(tails[c], wt)
+        else:
+            tol = 1e-5 * np.sum(np.abs(h2[c])) * 2
+            assert np.max(np.abs(body[c] - w)) <= tol and np.max(np.abs(tails[c] - wt), initial=0) <= tol
+
+
+def test_fused_stream_and_samples_f64():
+    import torch
+
+    rng = np.random.default_rng(9)
+    C, nb = 3, 32
+    h0 = rng.standard_normal((C, 70))
+    irs = [rng.standard_normal((C, n)) for n in (20, 150, 70)]
+    x = _inputs(rng, C, 32 * 40 + 5, np.float64)
+    swaps = [(4, irs[0]), (10, irs[1]), (10, irs[2]), (25, irs[0])]
+    eng = MultiChannelEngine(h0, EngineConfig(block_size_nb=nb))
+    # a few per-sample steps first (never apply pending swaps)
+    s0 = [eng.process_sample(x[:, i]) for i in range(3)]
+    body = eng.process_stream(torch.from_numpy(x[:, 3:]).cuda(), nb, swaps).cpu().numpy()
+    tails = eng.flush()
+    for c in range(C):
+        ref = O.OracleEngine(h0[c], nb)
+        w = [ref.process_sample(x[c, i]) for i in range(3)]
+        assert np.array_equal([s[c] for s in s0], w)
+        outs = []
+        for b, s in enumerate(range(3, x.shape[1], nb)):
+            for sb, ir in swaps:
+                if sb == b:
+                    ref.swap_ir(ir[c])
+            outs.append(ref.process_block(x[c, s:s + nb]))
+        assert np.array_equal(body[c], np.concatenate(outs))
+        assert np.array_equal(tails[c], ref.flush())
+
+
+def test_mono_ir_broadcast_and_errors():
+    rng = np.random.default_rng(1)
+    h = rng.standard_normal(33)
+    eng = MultiChannelEngine(h, channels=2)
+    x = rng.uniform(-1, 1, (2, 100))
+    y = eng.process_block(x)
+    for c in range(2):
+        assert np.array_equal(y[c], O.OracleEngine(h).process_block(x[c]))
+    with pytest.raises(ValueError, match="exceeds block_size_nb"):
+        MultiChannelEngine(h, EngineConfig(block_size_nb=4), channels=2).process_block(np.zeros((2, 5)))
+    with pytest.raises(ValueError, match="channels"):
+        eng.process_block(np.zeros((3, 5)))
+    with pytest.raises(ValueError, match="empty"):
+        eng.swap_ir(np.zeros((2, 0)))
