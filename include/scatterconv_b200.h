@@ -25,10 +25,11 @@
  *
  * Precision modes
  *  - SC_MODE_ORDERED: every output is ONE chain over input index m ascending,
- *    starting at +0.0, each step `acc = acc + x[m]*h[n-m]` with the product and
- *    the sum rounded separately (no FMA).  This is the reference's order
- *    (_kernels.py:1-8, core.py:83-86); in float64 it is bit-identical to the
- *    reference, and stream == batch for any block partition in both dtypes.
+ *    starting at +0.0, each step `acc = acc + x[m]*h[n-m]` -- the reference's
+ *    order (_kernels.py:1-8, core.py:83-86).  float64: product and sum rounded
+ *    separately (no FMA), bit-identical to the reference.  float32: one fused
+ *    multiply-add per step.  In both dtypes stream == batch for any block
+ *    partition.
  *  - SC_MODE_FAST (float32 only): the fastest kernel for the shape --
  *    SC_MODE_TC for long filters, SC_MODE_FFMA otherwise.  Fixed
  *    (deterministic) order, within 1e-5*max|x|*||h||_1 of the reference.

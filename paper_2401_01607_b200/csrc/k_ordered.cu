@@ -2,7 +2,8 @@
 //
 // Every output is computed as ONE chain over input index m ascending,
 // starting from +0.0 (or from a carried residue), acc = acc + x[m]*h[t-m]
-// with the product and the sum rounded separately.  That is exactly the
+// (float64: product and sum rounded separately; float32: fused, see
+// mac_rn in sc_common.cuh).  That is exactly the
 // order in which the reference's scatter loops touch each slot:
 //   core._scatter_full        pkg/src/scatterconv/core.py:80-92
 //   _kernels.scatter_block    pkg/src/scatterconv/_kernels.py:31-51
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(TB) k_chain(ChainArgs<T> a) {
                     for (int im = lo; im <= hi; ++im) {
                         const T xv = xs[im];
                         if (skipped<SKIP>(xv, a.thr)) continue;
-                        acc = add_rn(acc, mul_rn(xv, hp[-im]));
+                        acc = mac_rn(acc, xv, hp[-im]);
                     }
                 }
             }
@@ -130,6 +131,8 @@ constexpr int RT_R = 8;
 constexpr int RT_TILE = RT_TB * RT_R;  // 1024 outputs per CTA
 constexpr int RT_MC = 128;            // drive samples per smem chunk
 constexpr int RT_U = 8;               // m-steps per register window
+static_assert(RT_MC == RT_TB, "one staged drive sample per thread (the scatter-mask ballot)");
+static_assert(32 % RT_U == 0, "a u-block's scatter bits sit in one mask word");
 
 template <typename T>
 __device__ __forceinline__ int rt_pos(int i) {
@@ -140,6 +143,7 @@ template <typename T, int SKIP>
 __global__ void __launch_bounds__(RT_TB) k_chain_rt(ChainArgs<T> a) {
     constexpr int HS = RT_TILE + RT_MC - 1;
     __shared__ T xs[RT_MC];
+    __shared__ unsigned xmask[RT_MC / 32];
     __shared__ T hs[HS + HS / 16 + 2];
     if (a.run_if && *a.run_if == 0) return;
     // batched channel (grid.y): channel-local base pointers (the param struct
@@ -171,9 +175,15 @@ __global__ void __launch_bounds__(RT_TB) k_chain_rt(ChainArgs<T> a) {
             const int64_t bhi = tile_last + 1 < m_hi ? tile_last + 1 : m_hi;
             for (int64_t mc = blo; mc < bhi; mc += RT_MC) {
                 __syncthreads();
+                // stage the drive chunk and, by warp ballot, a bit per sample
+                // that scatters (the zero-skip test runs once per sample, not
+                // once per thread and sample)
                 for (int i = threadIdx.x; i < RT_MC; i += RT_TB) {
                     const int64_t m = mc + i;
-                    xs[i] = m < bhi ? xb[m - a.x_off] : T(0);
+                    const T v = m < bhi ? xb[m - a.x_off] : T(0);
+                    xs[i] = v;
+                    const unsigned live_bits = __ballot_sync(0xffffffffu, m < bhi && !skipped<SKIP>(v, a.thr));
+                    if ((i & 31) == 0) xmask[i >> 5] = live_bits;
                 }
                 const int64_t kbase = tile0 - mc - RT_MC + 1;
                 for (int i = threadIdx.x; i < HS; i += RT_TB) {
@@ -184,26 +194,33 @@ __global__ void __launch_bounds__(RT_TB) k_chain_rt(ChainArgs<T> a) {
                 const int mcount = (int)(bhi - mc < RT_MC ? bhi - mc : RT_MC);
                 // every (output of the tile, m of the chunk) pair is a valid tap
                 const bool full = (mc >= tile_last - nh + 1) && (mc + mcount - 1 <= tile0);
+                // edge chunks: output r takes sample im iff lo_r <= im <= hi_r
+                // (int32, relative to the chunk): m <= t and m > t - nh
+                const int rel = (int)(tj - mc);  // t - m = rel + r - im
                 const int hb = threadIdx.x * RT_R + RT_MC - 1;  // hs index of tap for (r=0, im=0)
                 for (int im0 = 0; im0 < mcount; im0 += RT_U) {
                     T w[RT_R + RT_U - 1];  // w[q] = hs[hb - im0 - (RT_U-1) + q]
 #pragma unroll
                     for (int q = 0; q < RT_R + RT_U - 1; ++q) w[q] = hs[rt_pos<T>(hb - im0 - (RT_U - 1) + q)];
+                    // scatter bits of samples im0..im0+7 (RT_U = 8 divides 32)
+                    const unsigned bits = (xmask[im0 >> 5] >> (im0 & 31)) & 0xFFu;
+                    if (full) {
 #pragma unroll
-                    for (int u = 0; u < RT_U; ++u) {
-                        const int im = im0 + u;
-                        if (im >= mcount) break;
-                        const T xv = xs[im];
-                        if (skipped<SKIP>(xv, a.thr)) continue;
-                        const int64_t m = mc + im;
-                        if (full) {
+                        for (int u = 0; u < RT_U; ++u) {
+                            if (!(bits & (1u << u))) continue;
+                            const T xv = xs[im0 + u];
 #pragma unroll
-                            for (int r = 0; r < RT_R; ++r) acc[r] = add_rn(acc[r], mul_rn(xv, w[r - u + RT_U - 1]));
-                        } else {
+                            for (int r = 0; r < RT_R; ++r) acc[r] = mac_rn(acc[r], xv, w[r - u + RT_U - 1]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < RT_U; ++u) {
+                            if (!(bits & (1u << u))) continue;
+                            const T xv = xs[im0 + u];
 #pragma unroll
                             for (int r = 0; r < RT_R; ++r) {
-                                const int64_t t = tj + r;
-                                if (m <= t && m > t - nh) acc[r] = add_rn(acc[r], mul_rn(xv, w[r - u + RT_U - 1]));
+                                const int d = rel + r - (im0 + u);  // = t - m
+                                if (d >= 0 && d < nh) acc[r] = mac_rn(acc[r], xv, w[r - u + RT_U - 1]);
                             }
                         }
                     }

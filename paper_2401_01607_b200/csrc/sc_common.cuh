@@ -64,6 +64,15 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 
+// One step of an ordered chain, acc + x*h.  float64: product and sum rounded
+// separately -- the reference's exact arithmetic, hence bit-identical results.
+// float32 (no bit-exact reference exists; the reference computes in float64):
+// one fused multiply-add, i.e. a single rounding per step -- every float32
+// ordered kernel uses this same step, so stream == batch and block-size
+// invariance stay bit-exact in float32 too.
+__device__ __forceinline__ double mac_rn(double acc, double x, double h) { return __dadd_rn(acc, __dmul_rn(x, h)); }
+__device__ __forceinline__ float mac_rn(float acc, float x, float h) { return __fmaf_rn(x, h, acc); }
+
 // Zero-skip predicates, compared in float64 like the reference (a float32
 // sample widens exactly; the threshold is never rounded to float32).
 template <int SKIP, typename T>
