@@ -204,7 +204,15 @@ __global__ void __launch_bounds__(RT_TB) k_chain_rt(ChainArgs<T> a) {
                     for (int q = 0; q < RT_R + RT_U - 1; ++q) w[q] = hs[rt_pos<T>(hb - im0 - (RT_U - 1) + q)];
                     // scatter bits of samples im0..im0+7 (RT_U = 8 divides 32)
                     const unsigned bits = (xmask[im0 >> 5] >> (im0 & 31)) & 0xFFu;
-                    if (full) {
+                    if (full && bits == 0xFFu) {
+                        // common case (dense signal, interior chunk): no tests at all
+#pragma unroll
+                        for (int u = 0; u < RT_U; ++u) {
+                            const T xv = xs[im0 + u];
+#pragma unroll
+                            for (int r = 0; r < RT_R; ++r) acc[r] = mac_rn(acc[r], xv, w[r - u + RT_U - 1]);
+                        }
+                    } else if (full) {
 #pragma unroll
                         for (int u = 0; u < RT_U; ++u) {
                             if (!(bits & (1u << u))) continue;
