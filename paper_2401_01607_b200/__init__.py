@@ -40,27 +40,29 @@ from .sharded import (
     shard_plan,
 )
 
+from .sweeps import (
+    BenchReport,
+    BenchRow,
+    LinearFit,
+    SweepSpec,
+    find_realtime_limit,
+    gen_white_noise,
+    ms_to_samples,
+    run_ir_sweep,
+    run_nb_sweep,
+)
+
 __version__ = "0.1.0"
 
 
-def ms_to_samples(ms: float, sample_rate: int) -> int:
-    """Duration in milliseconds to a sample count (bench.py:36-40)."""
-    if ms <= 0:
-        raise ValueError(f"duration must be positive, got {ms} ms")
-    return int(round(ms * sample_rate / 1000.0))
-
-
-def gen_white_noise(duration: int, sample_rate: int = 44100, seed=0) -> Signal:
-    """Uniform white noise in [-1, 1), reproducible per seed (bench.py:43-52)."""
-    import numpy as np
-
-    if not isinstance(duration, (int, np.integer)) or duration < 1:
-        raise ValueError(f"duration must be a positive sample count, got {duration!r}")
-    rng = np.random.default_rng(seed)
-    return Signal(rng.uniform(-1.0, 1.0, duration), sample_rate)
-
-
 __all__ = [
+    "BenchReport",
+    "BenchRow",
+    "LinearFit",
+    "SweepSpec",
+    "find_realtime_limit",
+    "run_ir_sweep",
+    "run_nb_sweep",
     "ConvOutput",
     "DEFAULT_BLOCK_SIZE",
     "EngineConfig",

@@ -271,7 +271,29 @@ def make_configs():
     print("ref_configs.npz:", sorted(out))
 
 
+def make_sweeps():
+    """Digests of the reference's own sweeps (bench.py:182-257): the outputs
+    are deterministic, so a device harness with float64 engines must match."""
+    from scatterconv.bench import SweepSpec, gen_white_noise, run_ir_sweep, run_nb_sweep
+
+    x = gen_white_noise(3000, 8000, seed=(77, 1))
+    ir = run_ir_sweep(SweepSpec([20, 45, 130], x, repetitions=1, rng_seed=5))
+    nbs = run_nb_sweep(SweepSpec([64], x, nb_values=[17, 256, 4096], repetitions=1, rng_seed=6))
+    out = {"ir_sweep": {"ir_lengths": [20, 45, 130], "n": 3000, "rate": 8000, "seed": [77, 1],
+                        "rng_seed": 5, "digest": ir.output_digest},
+           "nb_sweep": {"ir_lengths": [64], "nb_values": [17, 256, 4096], "rng_seed": 6,
+                        "digest": nbs.output_digest}}
+    with open(HERE / "ref_sweeps.json", "w", encoding="utf-8") as fh:
+        json.dump(out, fh, indent=1)
+    print("ref_sweeps.json:", out)
+
+
 if __name__ == "__main__":
-    make_small()
-    make_engine()
-    make_configs()
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[f"make_{name}"]()
+    else:
+        make_small()
+        make_engine()
+        make_configs()
+        make_sweeps()
