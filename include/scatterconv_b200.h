@@ -180,6 +180,24 @@ int sc_engine_process_blocks(sc_engine *e, const void *x, int64_t n_total, int64
                              const int64_t *swap_blocks, const void *const *swap_irs,
                              const int64_t *swap_nh, int64_t n_swaps, void *out);
 
+/* ---------------------------------------------------------------- WAV on device */
+
+/* SURVEY.md 8(f) row 3.  encoding: 0 pcm16, 1 pcm24, 2 float32 (the three
+ * encodings of wavio.py).  Decode the raw interleaved data-chunk bytes
+ * (device) into out[channels][frames] (wavio.py:118-130: PCM / 2^(bits-1)). */
+int sc_wav_decode(int encoding, const void *raw, int64_t frames, int64_t channels, int out_dtype,
+                  void *out, void *stream);
+
+/* Encode in[channels][ld] * gain into interleaved bytes (device); integer PCM
+ * rounds half-to-even and saturates, adding the number of clipped samples to
+ * *clipped (a device counter) -- wavio.py:133-198 semantics. */
+int sc_wav_encode(int encoding, int in_dtype, const void *in, int64_t ld, int64_t frames,
+                  int64_t channels, double gain, void *raw, unsigned long long *clipped, void *stream);
+
+/* max |x| over n samples into *peak_bits (device; the float64 bit pattern,
+ * initialise to 0) -- the --normalize peak of cli.py:204-210. */
+int sc_peak_abs(int dtype, const void *x, int64_t n, unsigned long long *peak_bits, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -288,6 +288,58 @@ def make_sweeps():
     print("ref_sweeps.json:", out)
 
 
+def make_wav():
+    """Reference CLI runs (cli.py `convolve`) on small synthetic WAV files: the
+    inputs are committed under tests/golden/wav/ and the sha256 of every
+    output file (plus exit code) is recorded."""
+    import contextlib
+    import io
+
+    from scatterconv.cli import main
+    from scatterconv.wavio import WavSpec, write_wav
+
+    d = HERE / "wav"
+    d.mkdir(exist_ok=True)
+    rng = np.random.default_rng(2026)
+    rate = 8000
+    x = rng.uniform(-0.5, 0.5, (2, 12000))
+    x[0, 3000:3400] = 0.0
+    write_wav(d / "in_pcm16_stereo.wav", [Signal(x[0], rate), Signal(x[1], rate)], WavSpec(rate, 2, "pcm16"))
+    h = rng.standard_normal((2, 1500)) * np.exp(-np.arange(1500) / 300.0) * 0.1
+    write_wav(d / "ir_f32_stereo.wav", [Signal(h[0], rate), Signal(h[1], rate)], WavSpec(rate, 2, "float32"))
+    hs = rng.standard_normal(900) * np.exp(-np.arange(900) / 200.0) * 0.1
+    write_wav(d / "swap_pcm24_mono.wav", [Signal(hs, rate)], WavSpec(rate, 1, "pcm24"))
+    hm = rng.standard_normal(700) * 0.05
+    write_wav(d / "ir_pcm16_mono.wav", [Signal(hm, rate)], WavSpec(rate, 1, "pcm16"))
+    runs = {
+        "default": ["in_pcm16_stereo.wav", "ir_f32_stereo.wav"],
+        "swap_norm_pcm24": ["in_pcm16_stereo.wav", "ir_f32_stereo.wav", "--nb", "256", "--swap-ir",
+                            "swap_pcm24_mono.wav@5000", "--normalize", "0.9", "--encoding", "pcm24"],
+        "skip_notail_pcm16": ["in_pcm16_stereo.wav", "ir_pcm16_mono.wav", "--zero-skip", "0.01", "--no-tail",
+                              "--encoding", "pcm16", "--nb", "1000"],
+        "two_swaps_loud_pcm16": ["in_pcm16_stereo.wav", "ir_pcm16_mono.wav", "--swap-ir",
+                                 "ir_f32_stereo.wav@100", "--swap-ir", "swap_pcm24_mono.wav@11999",
+                                 "--encoding", "pcm16", "--nb", "4096"],
+    }
+    out = {}
+    for name, args in runs.items():
+        argv = ["convolve", str(d / args[0]), str(d / args[1]), f"/tmp/golden_{name}.wav"]
+        rest = list(args[2:])
+        for i, a in enumerate(rest):
+            if a.endswith(".wav") or "@" in a:
+                p, sep, at = a.partition("@")
+                rest[i] = str(d / p) + sep + at
+        buf_o, buf_e = io.StringIO(), io.StringIO()
+        with contextlib.redirect_stdout(buf_o), contextlib.redirect_stderr(buf_e):
+            rc = main(argv + rest)
+        blob = open(f"/tmp/golden_{name}.wav", "rb").read()
+        out[name] = {"args": args, "rc": rc, "sha256": hashlib.sha256(blob).hexdigest(), "bytes": len(blob),
+                     "stderr": buf_e.getvalue()}
+    with open(HERE / "ref_wav.json", "w", encoding="utf-8") as fh:
+        json.dump(out, fh, indent=1)
+    print("ref_wav.json:", {k: (v["rc"], v["bytes"]) for k, v in out.items()})
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -297,3 +349,4 @@ if __name__ == "__main__":
         make_engine()
         make_configs()
         make_sweeps()
+        make_wav()
