@@ -198,6 +198,28 @@ int sc_wav_encode(int encoding, int in_dtype, const void *in, int64_t ld, int64_
  * initialise to 0) -- the --normalize peak of cli.py:204-210. */
 int sc_peak_abs(int dtype, const void *x, int64_t n, unsigned long long *peak_bits, void *stream);
 
+/* ---------------------------------------------------------------- fixed point */
+
+/* bit-true fixed-point simulation (quantize.py).
+ * Quantise n float64 samples (device) to a word_bits two's-complement
+ * fractional grid: k = clamp(rint(x * 2^(word_bits-1))), NaN -> INT64_MIN
+ * (quantize.py:137-143).  xq (optional) receives k / 2^(word_bits-1)
+ * (quantize.py:146-147).  stats[0] += samples outside [-1, 1) (the caller
+ * raises ValueError), stats[1] = max(stats[1], max |k|); both device
+ * counters, initialise to 0.  word_bits in [2, 64]. */
+int sc_fixed_quantize(const double *x, int64_t n, int word_bits, int64_t *k, double *xq,
+                      unsigned long long *stats, void *stream);
+
+/* Exact-integer convolution of quantised ke[ne], kh[nh] (device) under one
+ * requantisation scheme (0 "ideal": one half-even rounding per output;
+ * 1 "mac": rounding after every multiply-accumulate), y[ne+nh-1] = result /
+ * 2^(word_bits-1) in float64 -- fixed_point_convolve, quantize.py:163-195.
+ * Intermediates are __int128; the caller guarantees bitlen(max|ke|) +
+ * bitlen(max|kh|) + ceil(log2(min(ne, nh))) <= 126.  wide != 0 selects
+ * 64x64->128 products (needed once max|k| > 2^31). */
+int sc_fixed_convolve(const int64_t *ke, int64_t ne, const int64_t *kh, int64_t nh, int word_bits, int scheme,
+                      int wide, double *y, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,6 +70,11 @@ def lib():
     L.oracle_scatter_window.argtypes = [_dp, _i64, _dp, _i64, _dp, _i64, _i64, ctypes.c_int,
                                         ctypes.c_double, ctypes.c_int]
     L.oracle_scatter_window.restype = None
+    _ip = ctypes.POINTER(_i64)
+    L.oracle_fixed_quantize.argtypes = [_dp, _i64, ctypes.c_int, _ip]
+    L.oracle_fixed_quantize.restype = _i64
+    L.oracle_fixed_conv.argtypes = [_ip, _i64, _ip, _i64, ctypes.c_int, ctypes.c_int, _dp]
+    L.oracle_fixed_conv.restype = None
     _LIB = L
     return L
 
@@ -247,3 +252,26 @@ def stream_with_swaps(x, irs, nb, swap_every_blocks):
         outs.append(eng.process_block(x[start:start + nb]))
     tail = eng.flush()
     return np.concatenate(outs), tail
+
+
+def fixed_quantize(x, word_bits):
+    """quantize._quantize_ints (quantize.py:137-143): int64 grid indices;
+    raises ValueError like the reference on samples outside [-1, 1)."""
+    x = _f64(x)
+    k = np.empty(len(x), dtype=np.int64)
+    bad = lib().oracle_fixed_quantize(_p(x), len(x), int(word_bits) - 1,
+                                      k.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+    if bad:
+        raise ValueError("samples outside the representable range [-1, 1)")
+    return k
+
+
+def fixed_convolve(e, h, word_bits, scheme):
+    """quantize.fixed_point_convolve (quantize.py:163-195) on raw sample arrays."""
+    ke = fixed_quantize(e, word_bits)
+    kh = fixed_quantize(h, word_bits)
+    out = np.empty(len(ke) + len(kh) - 1)
+    ip = ctypes.POINTER(ctypes.c_int64)
+    lib().oracle_fixed_conv(ke.ctypes.data_as(ip), len(ke), kh.ctypes.data_as(ip), len(kh), int(word_bits) - 1,
+                            {"ideal": 0, "mac": 1}[scheme], _p(out))
+    return out

@@ -413,3 +413,61 @@ void oracle_scatter_window(const double *x, int64_t ne, const double *h, int64_t
     free(jobs);
     free(th);
 }
+
+/* ------------------------------------------------------------------ fixed point
+ * Bit-true fixed-point simulation, restating quantize.py:137-195.  Samples
+ * quantise to k = clamp(round_half_even(x * 2^frac)), NaN -> INT64_MIN (what
+ * numpy's float->int64 cast gives on x86).  Convolution is exact in __int128;
+ * "ideal" (scheme 0) rounds the exact sum once, "mac" (scheme 1) rounds after
+ * every multiply-accumulate with the first product kept exact until it joins
+ * the second.  Valid while every intermediate fits 127 bits (the callers'
+ * word lengths are <= 32 bits). */
+
+int64_t oracle_fixed_quantize(const double *x, int64_t n, int frac, int64_t *k)
+{
+    const double scale = ldexp(1.0, frac);
+    int64_t bad = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const double v = x[i];
+        if (v < -1.0 || v >= 1.0) bad++;
+        if (isnan(v)) {
+            k[i] = INT64_MIN;
+            continue;
+        }
+        double r = nearbyint(v * scale); /* default rounding mode: half to even */
+        if (r < -scale) r = -scale;
+        if (r > scale - 1.0) r = scale - 1.0;
+        k[i] = (int64_t)r;
+    }
+    return bad;
+}
+
+static __int128 rshe(__int128 t, int s)
+{
+    const __int128 q = t >> s;
+    const unsigned __int128 r = (unsigned __int128)t & (((unsigned __int128)1 << s) - 1);
+    const unsigned __int128 half = (unsigned __int128)1 << (s - 1);
+    return q + ((r > half || (r == half && (q & 1))) ? 1 : 0);
+}
+
+void oracle_fixed_conv(const int64_t *ke, int64_t ne, const int64_t *kh, int64_t nh, int frac, int scheme,
+                       double *out)
+{
+    for (int64_t n = 0; n < ne + nh - 1; ++n) {
+        const int64_t lo = n - nh + 1 > 0 ? n - nh + 1 : 0;
+        const int64_t hi = n < ne - 1 ? n : ne - 1;
+        __int128 c;
+        if (scheme == 0) {
+            __int128 acc = 0;
+            for (int64_t m = lo; m <= hi; ++m) acc += (__int128)ke[m] * kh[n - m];
+            c = rshe(acc, frac);
+        } else if (lo == hi) {
+            c = rshe((__int128)ke[lo] * kh[n - lo], frac);
+        } else {
+            c = rshe((__int128)ke[lo] * kh[n - lo] + (__int128)ke[lo + 1] * kh[n - lo - 1], frac);
+            for (int64_t m = lo + 2; m <= hi; ++m)
+                c = rshe((__int128)((unsigned __int128)c << frac) + (__int128)ke[m] * kh[n - m], frac);
+        }
+        out[n] = ldexp((double)c, -frac); /* libgcc int128->double rounds to nearest */
+    }
+}

@@ -340,6 +340,98 @@ def make_wav():
     print("ref_wav.json:", {k: (v["rc"], v["bytes"]) for k, v in out.items()})
 
 
+FIXED_BITS = (2, 3, 8, 12, 16, 24, 32)
+
+
+def _fixed_cases():
+    """(name, e, h) inputs for the fixed-point fixtures: random, grid edges
+    (-1, values that round up to +1 and saturate, exact half steps) and the
+    single-sample shapes the mac scheme special-cases."""
+    rng = np.random.default_rng(1607)
+    cases = [("rand", rng.uniform(-1, 1, 37), rng.uniform(-1, 1, 11)),
+             ("ne1", rng.uniform(-1, 1, 1), rng.uniform(-1, 1, 6)),
+             ("nh1", rng.uniform(-1, 1, 9), rng.uniform(-1, 1, 1)),
+             ("nh2", rng.uniform(-1, 1, 13), rng.uniform(-1, 1, 2)),
+             ("long_ir", rng.uniform(-1, 1, 20), rng.uniform(-1, 1, 64))]
+    edge = np.array([-1.0, 1.0 - 2.0 ** -40, 0.5, -0.5, 0.0, -0.0, 0.25 + 2.0 ** -10, 0.375, -0.625, 0.999])
+    cases.append(("edges", edge, edge[::-1].copy()))
+    cases.append(("loud", np.full(24, 1.0 - 2.0 ** -45), np.full(24, -1.0)))
+    return cases
+
+
+def make_fixed():
+    """Reference quantize.py runs: fixed_point_convolve outputs for every case x
+    word length x scheme, simulate reports, and the `quant` CLI's stdout."""
+    import contextlib
+    import io
+
+    import importlib
+
+    q = importlib.import_module("scatterconv.quantize")  # the package re-exports a function of that name
+    from scatterconv.cli import main
+
+    arrays, meta = {}, {"reports": {}, "cli": {}}
+    for name, e, h in _fixed_cases():
+        arrays[f"{name}/e"] = e
+        arrays[f"{name}/h"] = h
+        for bits in FIXED_BITS:
+            fmt = q.FixedPointFormat(bits)
+            for scheme in q.SCHEMES:
+                y = q.fixed_point_convolve(Signal(e, 48000), Signal(h, 48000), fmt, scheme).samples
+                arrays[f"{name}/{bits}/{scheme}"] = y
+                if name in ("rand", "long_ir"):
+                    r = q.simulate_fixed_point_conv(Signal(e, 48000), Signal(h, 48000), fmt, scheme)
+                    meta["reports"][f"{name}/{bits}/{scheme}"] = [r.operations_count, r.bits_removed_per_op,
+                                                                  r.rms_error, r.max_error]
+    runs = {"b16_ir32_sim": ["quant", "--bits", "16", "--ir-len", "32", "--simulate", "--seed", "3"],
+            "b8_ir5": ["quant", "--bits", "8", "--ir-len", "5"],
+            "b24_ir100_sim": ["quant", "--bits", "24", "--ir-len", "100", "--simulate", "--len", "64"],
+            "b2_ir1_sim": ["quant", "--bits", "2", "--ir-len", "1", "--simulate", "--len", "5"],
+            "b32_ir7_sim": ["quant", "--bits", "32", "--ir-len", "7", "--simulate", "--seed", "11", "--len", "300"],
+            "bad_bits": ["quant", "--bits", "1", "--ir-len", "4"],
+            "bad_len": ["quant", "--bits", "8", "--ir-len", "4", "--simulate", "--len", "0"],
+            "bad_ir": ["quant", "--bits", "8", "--ir-len", "0"]}
+    for name, argv in runs.items():
+        o, e = io.StringIO(), io.StringIO()
+        with contextlib.redirect_stdout(o), contextlib.redirect_stderr(e):
+            rc = main(argv)
+        meta["cli"][name] = {"argv": argv, "rc": rc, "stdout": o.getvalue(), "stderr": e.getvalue()}
+    np.savez_compressed(HERE / "ref_fixed.npz", **arrays)
+    with open(HERE / "ref_fixed.json", "w", encoding="utf-8") as fh:
+        json.dump(meta, fh, indent=1)
+    print("ref_fixed:", len(arrays), "arrays;", {k: v["rc"] for k, v in meta["cli"].items()})
+
+
+def make_cli_bench():
+    """The reference `bench` CLI: timing lines vary, the output digests and
+    row counts do not."""
+    import contextlib
+    import io
+
+    from scatterconv.cli import main
+
+    runs = {"ir_nb": ["bench", "--ir-sweep", "1:3:1", "--input", "noise:0.05", "--reps", "1", "--nb-sweep",
+                      "64,100", "--ir-ms", "2", "--csv", "{tmp}/x.csv", "--plot-data", "{tmp}/p.dat"],
+            "ir_only_seed": ["bench", "--ir-sweep", "0.5:0.5:1", "--input", "noise:0.02", "--seed", "5",
+                             "--rate", "8000", "--nb", "33", "--reps", "2"],
+            "nothing": ["bench", "--input", "noise:0.01"],
+            "bad_input": ["bench", "--ir-sweep", "1:2:1", "--input", "noise:abc"],
+            "plot_needs_ir": ["bench", "--nb-sweep", "8", "--ir-ms", "1", "--input", "noise:0.01",
+                              "--plot-data", "{tmp}/p.dat"]}
+    out = {}
+    for name, argv in runs.items():
+        o, e = io.StringIO(), io.StringIO()
+        with contextlib.redirect_stdout(o), contextlib.redirect_stderr(e):
+            rc = main([a.replace("{tmp}", "/tmp") for a in argv])
+        stable = [ln for ln in o.getvalue().splitlines()
+                  if "sha256" in ln or ln.startswith("wrote") or ln.startswith("nb sweep at")]
+        out[name] = {"argv": argv, "rc": rc, "stable": [ln.split(": wall-time")[0] for ln in stable],
+                     "stderr": e.getvalue()}
+    with open(HERE / "ref_cli_bench.json", "w", encoding="utf-8") as fh:
+        json.dump(out, fh, indent=1)
+    print("ref_cli_bench.json:", {k: v["rc"] for k, v in out.items()})
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -350,3 +442,5 @@ if __name__ == "__main__":
         make_configs()
         make_sweeps()
         make_wav()
+        make_fixed()
+        make_cli_bench()
