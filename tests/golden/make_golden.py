@@ -16,7 +16,14 @@ runs the reference's own entry points on seeded inputs and writes:
   ref_configs.npz    per-config reference pins: sha256 of the reference's
                      output on cfg1/cfg2 in full and cfg3/4/5 prefixes, plus
                      sampled values and exact direct_form (fsum) samples
+  ref_sweeps.json    bench.py sweep reports (digests, row shapes)
+  wav/, ref_wav.json WAV inputs + sha256 of the reference CLI `convolve`
+                     outputs for four flag sets
+  ref_fixed.*        quantize.py fixed_point_convolve outputs, simulate
+                     reports and `quant` CLI stdout
+  ref_cli_bench.json the `bench` CLI's timing-independent lines
 
+`python tests/golden/make_golden.py NAME...` regenerates only make_NAME().
 The fixtures are committed; the GPU box never needs /root/reference.
 """
 
