@@ -156,9 +156,16 @@ int sc_engine_swap_ir(sc_engine *e, const void *h, int64_t nh);
 int sc_engine_swap_ir_at_next_block(sc_engine *e, const void *h, int64_t nh);
 
 /* flush (engine.py:148-161): writes max(nh-1, live) tail samples in emission
- * order to tail (device, capacity tail_capacity), returns the count in
- * *n_tail and resets the engine (pending swap survives).  Synchronous. */
+ * order to tail (device, capacity tail_capacity; per channel for a
+ * multichannel engine), returns the count(s) in n_tail and resets the engine
+ * (pending swap survives).  Waits for the state read (the tail length is
+ * data dependent); the tail itself is written asynchronously on the engine
+ * stream. */
 int sc_engine_flush(sc_engine *e, void *tail, int64_t tail_capacity, int64_t *n_tail);
+
+/* Host-side upper bound of every channel's tail length (no synchronisation):
+ * a tail_capacity that always suffices for sc_engine_flush. */
+int sc_engine_tail_bound(sc_engine *e, int64_t *bound);
 
 /* State (engine.py:83-97): read_index, live, cap (= len(ring)), consumed,
  * current nh, has_pending.  Synchronous. */

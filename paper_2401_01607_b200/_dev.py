@@ -35,8 +35,13 @@ def torch_dtype(npd):
 def as_device(a, npd, device=None):
     """Contiguous CUDA tensor of dtype npd holding a (ndarray or tensor)."""
     t = torch()
-    dev = device if device is not None else t.device("cuda", t.cuda.current_device())
     td = torch_dtype(npd)
+    if is_tensor(a) and a.is_cuda and a.dtype == td and a.is_contiguous():
+        # already in place: skip the .to() dispatch (hot in fused streaming calls)
+        want = t.device(device).index if device is not None else t.cuda.current_device()
+        if a.device.index == want:
+            return a
+    dev = device if device is not None else t.device("cuda", t.cuda.current_device())
     if is_tensor(a):
         return a.to(device=dev, dtype=td, non_blocking=a.device.type == "cpu" and a.is_pinned()).contiguous()
     arr = np.ascontiguousarray(a, dtype=npd)

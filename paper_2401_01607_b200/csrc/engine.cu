@@ -148,36 +148,127 @@ __global__ void k_blocks_last_scatter(const T *__restrict__ x, int64_t ldx, int6
     }
 }
 
-// Replays engine.py's bookkeeping over all blocks of the call, one thread per
-// channel: each swap (cap = max(nh, live), ri = 0; engine.py:179-184) and
-// each block (live' = max(0, live - n, J >= 0 ? nh - n + J : 0),
-// ri' = (ri + n) % cap).
-__global__ void k_stream_state(const int64_t *__restrict__ J, int64_t n_blocks, int64_t nb, int64_t n_total,
-                               int64_t nh0, StreamEvents ev, int64_t *st, int64_t C) {
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= C) return;
+// Staging of every IR of a fused call in ONE launch (instead of one
+// cudaMemcpy2DAsync per IR): copy j moves [C][nh_j] from src_j (row pitch
+// sld_j) to stage + off_j (row pitch dld).  grid (x: 256-sample chunks of
+// the longest IR, y: copy, z: channel).
+struct StageCopies {
+    int n;
+    const void *src[kMaxSegs];
+    int64_t sld[kMaxSegs], off[kMaxSegs], nh[kMaxSegs];
+};
+
+template <typename T>
+__global__ void k_stage_irs(StageCopies c, T *__restrict__ stage, int64_t dld) {
+    const int j = blockIdx.y;
+    const int64_t ch = blockIdx.z;
+    const T *src = static_cast<const T *>(c.src[j]) + ch * c.sld[j];
+    T *dst = stage + ch * dld + c.off[j];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.nh[j]; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+// Replays engine.py's bookkeeping over all blocks of the call: each swap
+// (cap = max(nh, live), ri = 0; engine.py:179-184) and each block
+// (live' = max(0, live - n, J >= 0 ? nh - n + J : 0), ri' = (ri + n) % cap).
+// Per block b the live-length update is  live' = max(live - n_b, c_b)  with
+// c_b = max(0, J_b >= 0 ? nh_b - n_b + J_b : 0): a max-plus map
+// l -> max(l + A, B).  Such maps compose associatively,
+// (A1,B1) then (A2,B2) = (A1 + A2, max(B1 + A2, B2)), so the state after n
+// blocks is an ordered reduction, not a serial walk.  Swaps only reset cap
+// (= max(nh, live at the swap)) and read_index (= 0), so the final state
+// needs live at the LAST swap and at the end:
+//   cap = max(nh_last, live(b_last)),  ri = (samples since b_last) mod cap,
+// or, without swaps, ri = (ri0 + n_total) mod cap.  One CTA per channel.
+constexpr int64_t kMaxPlusNegInf = INT64_MIN / 4;
+constexpr int SS_TB = 256;
+
+__device__ __forceinline__ void mp_then(int64_t &A, int64_t &B, int64_t A2, int64_t B2) {
+    const int64_t b1 = B <= kMaxPlusNegInf ? kMaxPlusNegInf : B + A2;
+    A += A2;
+    B = b1 > B2 ? b1 : B2;
+}
+
+// ordered composition of the maps of blocks [lo, hi) across the CTA
+__device__ void mp_reduce(const int64_t *__restrict__ Jc, int64_t lo, int64_t hi, int64_t nb, int64_t n_total,
+                          int64_t nh0, const StreamEvents &ev, int64_t &A_out, int64_t &B_out) {
+    __shared__ int64_t sA[SS_TB / 32], sB[SS_TB / 32];
+    const int64_t cnt = hi - lo;
+    const int64_t per = (cnt + SS_TB - 1) / SS_TB;
+    const int64_t b0 = lo + threadIdx.x * per;
+    const int64_t b1 = b0 + per < hi ? b0 + per : hi;
+    int64_t A = 0, B = kMaxPlusNegInf;
+    if (b0 < b1) {
+        // IR length in force at block b0: the last event at or before it
+        int64_t nh = nh0;
+        int k = 0;
+        while (k < ev.n && ev.block[k] <= b0) nh = ev.nh[k++];
+        for (int64_t b = b0; b < b1; ++b) {
+            while (k < ev.n && ev.block[k] == b) nh = ev.nh[k++];
+            const int64_t n = n_total - b * nb < nb ? n_total - b * nb : nb;
+            const int64_t j = Jc[b];
+            int64_t c = j >= 0 ? nh - n + j : 0;
+            c = c > 0 ? c : 0;
+            mp_then(A, B, -n, c);
+        }
+    }
+    // in-order tree over lanes, then over warps
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t A2 = __shfl_down_sync(0xffffffffu, A, o);
+        const int64_t B2 = __shfl_down_sync(0xffffffffu, B, o);
+        if ((lane & (2 * o - 1)) == 0) mp_then(A, B, A2, B2);
+    }
+    if (lane == 0) {
+        sA[warp] = A;
+        sB[warp] = B;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        A = sA[0];
+        B = sB[0];
+        for (int w = 1; w < SS_TB / 32; ++w) mp_then(A, B, sA[w], sB[w]);
+        A_out = A;
+        B_out = B;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(SS_TB) k_stream_state(const int64_t *__restrict__ J, int64_t n_blocks, int64_t nb,
+                                                        int64_t n_total, int64_t nh0, StreamEvents ev, int64_t *st) {
+    const int64_t c = blockIdx.x;
     int64_t *s = st + c * ST_N;
     const int64_t *Jc = J + c * n_blocks;
-    int64_t live = s[ST_LIVE], cap = s[ST_CAP], ri = s[ST_RI], nh = nh0;
-    int64_t k = 0;
-    for (int64_t b = 0; b < n_blocks; ++b) {
-        while (k < ev.n && ev.block[k] == b) {
-            nh = ev.nh[k];
-            cap = nh > live ? nh : live;
-            ri = 0;
-            ++k;
-        }
-        const int64_t n = n_total - b * nb < nb ? n_total - b * nb : nb;
-        const int64_t j = Jc[b];
-        int64_t l = live - n;
-        if (l < 0) l = 0;
-        if (j >= 0 && nh - n + j > l) l = nh - n + j;
-        live = l;
-        ri = (ri + n) % cap;
+    int last = -1;  // last event that precedes a processed block
+    for (int k = 0; k < ev.n; ++k)
+        if (ev.block[k] < n_blocks) last = k;
+    const int64_t b_last = last >= 0 ? ev.block[last] : 0;
+    __shared__ int64_t red[2];
+    int64_t A, B;
+    mp_reduce(Jc, 0, b_last, nb, n_total, nh0, ev, A, B);
+    if (threadIdx.x == 0) {
+        red[0] = A;
+        red[1] = B;
     }
-    s[ST_LIVE] = live;
-    s[ST_CAP] = cap;
-    s[ST_RI] = ri;
+    mp_reduce(Jc, b_last, n_blocks, nb, n_total, nh0, ev, A, B);
+    if (threadIdx.x == 0) {
+        const int64_t live0 = s[ST_LIVE];
+        int64_t live = live0 + red[0];
+        live = live > red[1] ? live : red[1];
+        int64_t cap = s[ST_CAP], ri = s[ST_RI];
+        const int64_t since = n_total - b_last * nb;
+        if (last >= 0) {
+            const int64_t nh_last = ev.nh[last];
+            cap = nh_last > live ? nh_last : live;
+            ri = since % cap;
+        } else {
+            ri = (ri + since) % cap;
+        }
+        int64_t fin = live + A;
+        s[ST_LIVE] = fin > B ? fin : B;
+        s[ST_CAP] = cap;
+        s[ST_RI] = ri;
+    }
 }
 
 }  // namespace
@@ -381,8 +472,9 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
     rc = ensure_2d(reinterpret_cast<void **>(&e->jbuf), &e->jbuf_ld, n_blocks * e->C, 8, 1, 0, e->stream);
     if (rc) return rc;
     char *stage = static_cast<char *>(e->stage);
-    rc = copy_rows(e, stage, e->stage_ld, e->ir, e->ir_ld, e->nh);
-    if (rc) return rc;
+    StageCopies cp{};
+    int64_t max_nh = e->nh;
+    cp.src[0] = e->ir, cp.sld[0] = e->ir_ld, cp.off[0] = 0, cp.nh[0] = e->nh, cp.n = 1;
     ChainSeg segs[kMaxSegs];
     int nseg = 0;
     segs[nseg++] = ChainSeg{stage, e->nh, 0, n_total};
@@ -391,8 +483,8 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
     sev.n = 0;
     for (const Ev &v : ev) {
         char *dst = stage + (size_t)off * e->es;
-        rc = copy_rows(e, dst, e->stage_ld, v.h, v.ld, v.nh);
-        if (rc) return rc;
+        cp.src[cp.n] = v.h, cp.sld[cp.n] = v.ld, cp.off[cp.n] = off, cp.nh[cp.n] = v.nh, ++cp.n;
+        max_nh = v.nh > max_nh ? v.nh : max_nh;
         const int64_t m = v.block * nb;
         if (segs[nseg - 1].m_lo == m) {
             segs[nseg - 1].h = dst;  // a later swap before the same block wins
@@ -406,6 +498,14 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
         ++sev.n;
         off += v.nh;
         ub = v.nh > ub ? v.nh : ub;
+    }
+    {
+        const dim3 gs((unsigned)std::min<int64_t>(cdiv(max_nh, 256), 64), (unsigned)cp.n, (unsigned)e->C);
+        if (e->dtype == SC_F64)
+            k_stage_irs<double><<<gs, 256, 0, e->stream>>>(cp, static_cast<double *>(e->stage), e->stage_ld);
+        else
+            k_stage_irs<float><<<gs, 256, 0, e->stream>>>(cp, static_cast<float *>(e->stage), e->stage_ld);
+        SC_CHECK_LAUNCH();
     }
     rc = grow_residue(e, ub);
     if (rc) return rc;
@@ -425,7 +525,7 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
         k_blocks_last_scatter<float><<<gj, 256, 0, e->stream>>>(static_cast<const float *>(x), ldx, n_total, nb,
                                                                e->thr, n_blocks, e->jbuf);
     SC_CHECK_LAUNCH();
-    k_stream_state<<<cgrid(e->C), 128, 0, e->stream>>>(e->jbuf, n_blocks, nb, n_total, e->nh, sev, e->st, e->C);
+    k_stream_state<<<(unsigned)e->C, SS_TB, 0, e->stream>>>(e->jbuf, n_blocks, nb, n_total, e->nh, sev, e->st);
     SC_CHECK_LAUNCH();
     // host-side bookkeeping: the last IR becomes current (engine-owned copy)
     const ChainSeg &last = segs[nseg - 1];
@@ -579,7 +679,12 @@ int sc_engine_flush(sc_engine *e, void *tail, int64_t tail_capacity, int64_t *n_
     SC_CHECK_LAUNCH();
     e->cap_ub = e->nh;
     e->consumed = 0;
-    SC_CHECK_CUDA(cudaStreamSynchronize(e->stream));
+    return SC_OK;
+}
+
+int sc_engine_tail_bound(sc_engine *e, int64_t *bound) {
+    SC_REQUIRE(e && bound, "sc_engine_tail_bound: null pointer");
+    *bound = std::max<int64_t>(e->cap_ub, 1);  // live <= cap <= cap_ub; nh - 1 < cap_ub
     return SC_OK;
 }
 

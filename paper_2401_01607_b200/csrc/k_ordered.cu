@@ -24,8 +24,7 @@
 namespace sc {
 namespace {
 
-constexpr int TB = 256;  // outputs per CTA
-constexpr int MC = 256;  // drive samples per shared-memory chunk
+constexpr int TB = 256;  // direct-form CTA size
 
 template <typename T>
 struct ChainArgs {
@@ -46,197 +45,215 @@ struct ChainArgs {
     int64_t ld_init, ld_outb, ld_st;
 };
 
-template <typename T, int SKIP>
-__global__ void __launch_bounds__(TB) k_chain(ChainArgs<T> a) {
-    __shared__ T xs[MC];
-    __shared__ T hs[MC + TB - 1];
+// ---------------------------------------------------------------- windowed chain
+// One kernel for every ordered launch.  A CTA of 128 threads owns a tile of
+// 128*R consecutive outputs, thread j the R consecutive outputs tj..tj+R-1
+// (R = 8, 4, 2 or 1, picked per launch so the grid keeps every SM sub-
+// partition busy).  Drive samples go through shared memory in chunks of 128
+// (one per thread), the taps of the chunk x tile in a padded stage (see
+// cw_pos: the stride-R reads of a warp hit distinct banks).  Per 8-sample "u-block" a thread keeps a register
+// window of R+7 taps; sliding to the next u-block reuses R-1 of them, so a
+// u-block costs 8 tap loads and two (float) / four (double) broadcast
+// vector loads of the drive for 8R MACs.  Interior chunks of a dense drive
+// (every (output, sample) pair valid, nothing skipped) run a fully unrolled
+// path with no tests; edge u-blocks test validity per thread and only the
+// u-blocks that straddle an edge pay per-MAC predicates.  The next chunk's
+// drive and taps are loaded into registers while the current chunk is
+// computed (double-buffered stage, one barrier per chunk).
+constexpr int CW_TB = 128;
+constexpr int CW_MC = 128;  // drive samples per chunk (= CW_TB: one staged per thread)
+constexpr int CW_U = 8;     // samples per u-block
+static_assert(CW_MC == CW_TB, "one staged drive sample per thread (scatter-mask ballot)");
+static_assert(32 % CW_U == 0, "a u-block's scatter bits sit in one mask word");
+
+// Tap stage layout: one pad element after every R taps (none for R = 1).
+// Lane l of a warp reads stage index l*R + c, i.e. padded word offset
+// (R+1)*l*(es/4) + ..., which lands on distinct banks for R = 2, 4, 8 (odd
+// strides 3, 5, 9 words for float; for double, 6, 10, 18 words across a
+// half-warp).  Because the thread's base index l*R is a multiple of R, the
+// padded address splits into a per-thread base (R+1)*l plus cw_pos(c) of the
+// compile-time (or 8-aligned) offset c: every tap load is [reg + imm].
+template <int R>
+__host__ __device__ constexpr int cw_pos(int i) {
+    return R == 1 ? i : i + i / R;
+}
+
+template <typename T, int SKIP, int R>
+__global__ void __launch_bounds__(CW_TB, 4) k_chain_w(ChainArgs<T> a) {
+    constexpr int TILE = CW_TB * R;
+    constexpr int HS = TILE + CW_MC - 1;  // taps per stage
+    constexpr int HSP = cw_pos<R>(HS - 1) + 1;
+    constexpr int HPT = (HS + CW_TB - 1) / CW_TB;  // tap loads per thread per chunk
+    constexpr int W = R + CW_U - 1;
+    constexpr int XV = 16 / (int)sizeof(T);  // drive samples per vector load
+    __shared__ __align__(16) T xs[2][CW_MC];
+    __shared__ unsigned xmask[2][CW_MC / 32];
+    __shared__ T hs[2][HSP];
     if (a.run_if && *a.run_if == 0) return;  // block-uniform
-    // batched channel (grid.y): channel-local base pointers (the param struct
-    // itself is never written, so it stays in the constant bank)
+    // channel-local base pointers (the param struct stays in the constant bank)
     const T *xb = a.x + blockIdx.y * a.ldx;
     T *outa = a.out_a + blockIdx.y * a.ldo;
     const int64_t hoff = blockIdx.y * a.ldh;
     const T *initc = a.init ? a.init + blockIdx.y * a.ld_init : nullptr;
     T *outb = a.out_b ? a.out_b + blockIdx.y * a.ld_outb : nullptr;
-    const int64_t n_tiles = (a.n_out + TB - 1) / TB;
-    const int64_t init_len = a.init_len_dev ? a.init_len_dev[blockIdx.y * a.ld_st] : a.init_len;
-    for (int64_t tb = blockIdx.x; tb < n_tiles; tb += gridDim.x) {
-    __syncthreads();  // smem reuse across tiles of this CTA
-    const int64_t tile0 = a.t0 + tb * TB;
-    const int64_t t_end = a.t0 + a.n_out;
-    const int64_t tile_last = (tile0 + TB < t_end ? tile0 + TB : t_end) - 1;
-    const int64_t t = tile0 + threadIdx.x;
-    const bool active = t < t_end;
-
-    T acc = T(0);
-    if (active && initc != nullptr && (t - a.t0) < init_len) acc = initc[t - a.t0];
-
-    for (int s = 0; s < a.nseg; ++s) {
-        const T *__restrict__ h = static_cast<const T *>(a.seg[s].h) + hoff;
-        const int64_t nh = a.seg[s].nh;
-        const int64_t m_lo = a.seg[s].m_lo, m_hi = a.seg[s].m_hi;
-        const int64_t blo = tile0 - nh + 1 > m_lo ? tile0 - nh + 1 : m_lo;
-        const int64_t bhi = tile_last + 1 < m_hi ? tile_last + 1 : m_hi;  // exclusive
-        const int64_t my_lo = t - nh + 1 > m_lo ? t - nh + 1 : m_lo;
-        const int64_t my_hi = t < m_hi - 1 ? t : m_hi - 1;  // inclusive
-        for (int64_t mc = blo; mc < bhi; mc += MC) {
-            __syncthreads();
-            for (int i = threadIdx.x; i < MC; i += TB) {
-                const int64_t m = mc + i;
-                xs[i] = m < bhi ? xb[m - a.x_off] : T(0);
-            }
-            const int64_t kbase = tile0 - mc - MC + 1;
-            for (int i = threadIdx.x; i < MC + TB - 1; i += TB) {
-                const int64_t k = kbase + i;
-                hs[i] = (k >= 0 && k < nh) ? h[k] : T(0);
-            }
-            __syncthreads();
-            if (active) {
-                const int64_t lo64 = my_lo > mc ? my_lo : mc;
-                const int64_t hi64 = my_hi < mc + MC - 1 ? my_hi : mc + MC - 1;
-                if (lo64 <= hi64) {
-                    const int lo = (int)(lo64 - mc), hi = (int)(hi64 - mc);
-                    const T *hp = hs + threadIdx.x + MC - 1;
-#pragma unroll 4
-                    for (int im = lo; im <= hi; ++im) {
-                        const T xv = xs[im];
-                        if (skipped<SKIP>(xv, a.thr)) continue;
-                        acc = mac_rn(acc, xv, hp[-im]);
-                    }
-                }
-            }
-        }
-    }
-    if (active) {
-        const int64_t i = t - a.t0;
-        if (i < a.n_a)
-            outa[i] = acc;
-        else if (outb != nullptr)
-            outb[i - a.n_a] = acc;
-    }
-    }  // tiles
-}
-
-// ---------------------------------------------------------------- register-tiled chain
-// Same arithmetic and order as k_chain (each output: one ascending-m chain of
-// separately rounded mul/add), but each thread carries RT_R consecutive
-// outputs: per drive sample m the tap window slides by one, so with a
-// rotating register window of RT_R + RT_U - 1 taps one shared-memory load
-// feeds RT_R/ (RT_R+RT_U-1) * RT_U MACs instead of one.  Used for large
-// ordered launches (whole signals in float64, fused streaming).  The tap
-// stage is padded (one slot every 32 floats / 16 doubles) so the stride-RT_R
-// accesses of a warp hit distinct banks.
-constexpr int RT_TB = 128;
-constexpr int RT_R = 8;
-constexpr int RT_TILE = RT_TB * RT_R;  // 1024 outputs per CTA
-constexpr int RT_MC = 128;            // drive samples per smem chunk
-constexpr int RT_U = 8;               // m-steps per register window
-static_assert(RT_MC == RT_TB, "one staged drive sample per thread (the scatter-mask ballot)");
-static_assert(32 % RT_U == 0, "a u-block's scatter bits sit in one mask word");
-
-template <typename T>
-__device__ __forceinline__ int rt_pos(int i) {
-    return sizeof(T) == 8 ? i + (i >> 4) : i + (i >> 5);
-}
-
-template <typename T, int SKIP>
-__global__ void __launch_bounds__(RT_TB) k_chain_rt(ChainArgs<T> a) {
-    constexpr int HS = RT_TILE + RT_MC - 1;
-    __shared__ T xs[RT_MC];
-    __shared__ unsigned xmask[RT_MC / 32];
-    __shared__ T hs[HS + HS / 16 + 2];
-    if (a.run_if && *a.run_if == 0) return;
-    // batched channel (grid.y): channel-local base pointers (the param struct
-    // itself is never written, so it stays in the constant bank)
-    const T *xb = a.x + blockIdx.y * a.ldx;
-    T *outa = a.out_a + blockIdx.y * a.ldo;
-    const int64_t hoff = blockIdx.y * a.ldh;
-    const T *initc = a.init ? a.init + blockIdx.y * a.ld_init : nullptr;
-    T *outb = a.out_b ? a.out_b + blockIdx.y * a.ld_outb : nullptr;
-    const int64_t n_tiles = (a.n_out + RT_TILE - 1) / RT_TILE;
+    const int64_t n_tiles = (a.n_out + TILE - 1) / TILE;
     const int64_t t_end = a.t0 + a.n_out;
     const int64_t init_len = a.init_len_dev ? a.init_len_dev[blockIdx.y * a.ld_st] : a.init_len;
+    const int tid = threadIdx.x;
+    // the tap for (r, im) sits at stage index tid*R + (CW_MC - 1) + r - im
+    const int hth = R == 1 ? tid : (R + 1) * tid;  // padded base of this thread
+
     for (int64_t tb = blockIdx.x; tb < n_tiles; tb += gridDim.x) {
-        __syncthreads();
-        const int64_t tile0 = a.t0 + tb * RT_TILE;
-        const int64_t tile_last = (tile0 + RT_TILE < t_end ? tile0 + RT_TILE : t_end) - 1;
-        const int64_t tj = tile0 + (int64_t)threadIdx.x * RT_R;  // this thread's first output
-        T acc[RT_R];
+        const int64_t tile0 = a.t0 + tb * TILE;
+        const int64_t tile_last = (tile0 + TILE < t_end ? tile0 + TILE : t_end) - 1;
+        const int64_t tj = tile0 + (int64_t)tid * R;
+        T acc[R];
 #pragma unroll
-        for (int r = 0; r < RT_R; ++r) {
+        for (int r = 0; r < R; ++r) {
             const int64_t t = tj + r;
             acc[r] = (initc != nullptr && t < t_end && (t - a.t0) < init_len) ? initc[t - a.t0] : T(0);
         }
-        for (int s = 0; s < a.nseg; ++s) {
+        // chunk range of segment s for this tile: [blo, bhi)
+        auto seg_lo = [&](int s) {
+            const int64_t v = tile0 - a.seg[s].nh + 1;
+            return v > a.seg[s].m_lo ? v : a.seg[s].m_lo;
+        };
+        auto seg_hi = [&](int s) { return tile_last + 1 < a.seg[s].m_hi ? tile_last + 1 : a.seg[s].m_hi; };
+        // first chunk
+        int cs = 0;
+        int64_t cmc = 0;
+        while (cs < a.nseg && seg_lo(cs) >= seg_hi(cs)) ++cs;
+        if (cs < a.nseg) cmc = seg_lo(cs);
+        // register prefetch of one chunk
+        T px;
+        bool pbit;
+        T ph[HPT];
+        auto fetch = [&](int s, int64_t mc) {
+            const int64_t bhi = seg_hi(s);
+            const int64_t m = mc + tid;
+            px = m < bhi ? xb[m - a.x_off] : T(0);
+            pbit = m < bhi && !skipped<SKIP>(px, a.thr);
             const T *__restrict__ h = static_cast<const T *>(a.seg[s].h) + hoff;
             const int64_t nh = a.seg[s].nh;
-            const int64_t m_lo = a.seg[s].m_lo, m_hi = a.seg[s].m_hi;
-            const int64_t blo = tile0 - nh + 1 > m_lo ? tile0 - nh + 1 : m_lo;
-            const int64_t bhi = tile_last + 1 < m_hi ? tile_last + 1 : m_hi;
-            for (int64_t mc = blo; mc < bhi; mc += RT_MC) {
-                __syncthreads();
-                // stage the drive chunk and, by warp ballot, a bit per sample
-                // that scatters (the zero-skip test runs once per sample, not
-                // once per thread and sample)
-                for (int i = threadIdx.x; i < RT_MC; i += RT_TB) {
-                    const int64_t m = mc + i;
-                    const T v = m < bhi ? xb[m - a.x_off] : T(0);
-                    xs[i] = v;
-                    const unsigned live_bits = __ballot_sync(0xffffffffu, m < bhi && !skipped<SKIP>(v, a.thr));
-                    if ((i & 31) == 0) xmask[i >> 5] = live_bits;
-                }
-                const int64_t kbase = tile0 - mc - RT_MC + 1;
-                for (int i = threadIdx.x; i < HS; i += RT_TB) {
-                    const int64_t k = kbase + i;
-                    hs[rt_pos<T>(i)] = (k >= 0 && k < nh) ? h[k] : T(0);
-                }
-                __syncthreads();
-                const int mcount = (int)(bhi - mc < RT_MC ? bhi - mc : RT_MC);
-                // every (output of the tile, m of the chunk) pair is a valid tap
-                const bool full = (mc >= tile_last - nh + 1) && (mc + mcount - 1 <= tile0);
-                // edge chunks: output r takes sample im iff lo_r <= im <= hi_r
-                // (int32, relative to the chunk): m <= t and m > t - nh
-                const int rel = (int)(tj - mc);  // t - m = rel + r - im
-                const int hb = threadIdx.x * RT_R + RT_MC - 1;  // hs index of tap for (r=0, im=0)
-                for (int im0 = 0; im0 < mcount; im0 += RT_U) {
-                    T w[RT_R + RT_U - 1];  // w[q] = hs[hb - im0 - (RT_U-1) + q]
+            const int64_t kbase = tile0 - mc - CW_MC + 1;
 #pragma unroll
-                    for (int q = 0; q < RT_R + RT_U - 1; ++q) w[q] = hs[rt_pos<T>(hb - im0 - (RT_U - 1) + q)];
-                    // scatter bits of samples im0..im0+7 (RT_U = 8 divides 32)
-                    const unsigned bits = (xmask[im0 >> 5] >> (im0 & 31)) & 0xFFu;
-                    if (full && bits == 0xFFu) {
-                        // common case (dense signal, interior chunk): no tests at all
+            for (int j = 0; j < HPT; ++j) {
+                const int i = tid + j * CW_TB;
+                const int64_t k = kbase + i;
+                ph[j] = (i < HS && k >= 0 && k < nh) ? h[k] : T(0);
+            }
+        };
+        auto stash = [&](int buf) {
+            xs[buf][tid] = px;
+            const unsigned bits = __ballot_sync(0xffffffffu, pbit);
+            if ((tid & 31) == 0) xmask[buf][tid >> 5] = bits;
 #pragma unroll
-                        for (int u = 0; u < RT_U; ++u) {
-                            const T xv = xs[im0 + u];
+            for (int j = 0; j < HPT; ++j) {
+                const int i = tid + j * CW_TB;
+                if (i < HS) hs[buf][cw_pos<R>(i)] = ph[j];
+            }
+        };
+        if (cs < a.nseg) {
+            fetch(cs, cmc);
+            stash(0);
+        }
+        __syncthreads();
+        int buf = 0;
+        while (cs < a.nseg) {
+            // next chunk
+            int ns = cs;
+            int64_t nmc = cmc + CW_MC;
+            if (nmc >= seg_hi(ns)) {
+                ++ns;
+                while (ns < a.nseg && seg_lo(ns) >= seg_hi(ns)) ++ns;
+                if (ns < a.nseg) nmc = seg_lo(ns);
+            }
+            if (ns < a.nseg) fetch(ns, nmc);  // global loads in flight during the compute below
+
+            const int64_t nh = a.seg[cs].nh;
+            const int64_t bhi = seg_hi(cs);
+            const int mcount = (int)(bhi - cmc < CW_MC ? bhi - cmc : CW_MC);
+            const T *xsb = xs[buf];
+            const T *hsb = hs[buf];
+            const bool full = (cmc >= tile_last - nh + 1) && (cmc + mcount - 1 <= tile0);
+            const bool dense = mcount == CW_MC && (xmask[buf][0] & xmask[buf][1] & xmask[buf][2] & xmask[buf][3]) == ~0u;
+            if (full && dense) {
+                // interior: every (output, sample) pair valid, nothing skipped
+                T w[W];
 #pragma unroll
-                            for (int r = 0; r < RT_R; ++r) acc[r] = mac_rn(acc[r], xv, w[r - u + RT_U - 1]);
+                for (int q = 0; q < W; ++q) w[q] = hsb[hth + cw_pos<R>(CW_MC - CW_U + q)];
+#pragma unroll
+                for (int ub = 0; ub < CW_MC / CW_U; ++ub) {
+                    if (ub > 0) {
+#pragma unroll
+                        for (int p = R - 2; p >= 0; --p) w[CW_U + p] = w[p];
+#pragma unroll
+                        for (int q = 0; q < CW_U; ++q) w[q] = hsb[hth + cw_pos<R>(CW_MC - CW_U - ub * CW_U + q)];
+                    }
+                    T xv[CW_U];
+#pragma unroll
+                    for (int v = 0; v < CW_U; v += XV) {
+                        if (sizeof(T) == 4) {
+                            const float4 f = *reinterpret_cast<const float4 *>(&xsb[ub * CW_U + v]);
+                            xv[v] = (T)f.x, xv[v + 1] = (T)f.y, xv[v + 2] = (T)f.z, xv[v + 3] = (T)f.w;
+                        } else {
+                            const double2 d = *reinterpret_cast<const double2 *>(&xsb[ub * CW_U + v]);
+                            xv[v] = (T)d.x, xv[v + 1] = (T)d.y;
                         }
-                    } else if (full) {
+                    }
 #pragma unroll
-                        for (int u = 0; u < RT_U; ++u) {
-                            if (!(bits & (1u << u))) continue;
-                            const T xv = xs[im0 + u];
+                    for (int u = 0; u < CW_U; ++u)
 #pragma unroll
-                            for (int r = 0; r < RT_R; ++r) acc[r] = mac_rn(acc[r], xv, w[r - u + RT_U - 1]);
+                        for (int r = 0; r < R; ++r) acc[r] = mac_rn(acc[r], xv[u], w[r - u + CW_U - 1]);
+                }
+            } else {
+                // t - m = rel + r - im.  Only u-blocks with at least one valid
+                // (output, sample) pair are visited: im0 in (rel - nh - 7 + R... ]
+                // i.e. rel + R - 1 - im0 >= 0 and rel - im0 - 7 < nh.
+                const int64_t rel = tj - cmc;
+                int64_t ilo = rel - nh - (CW_U - 1) + 1;  // smallest im0 with rel - im0 - 7 < nh
+                int64_t ihi = rel + R - 1;                // largest im0 with rel + R - 1 - im0 >= 0
+                ilo = ilo < 0 ? 0 : (ilo + CW_U - 1) / CW_U * CW_U;
+                ihi = ihi > mcount - 1 ? mcount - 1 : ihi;
+                const int nh32 = (int)(nh < INT32_MAX ? nh : INT32_MAX);
+                for (int im0 = (int)ilo; im0 <= (int)ihi; im0 += CW_U) {
+                    T w[W];
+                    // c0 = CW_MC - CW_U - im0 is a multiple of 8, so cw_pos(c0 + q) = cw_pos(c0) + cw_pos(q)
+                    const T *hp = hsb + hth + cw_pos<R>(CW_MC - CW_U - im0);
+#pragma unroll
+                    for (int q = 0; q < W; ++q) w[q] = hp[cw_pos<R>(q)];
+                    // samples im0..im0+7 (bits past mcount are 0: m >= bhi)
+                    const unsigned bits = (xmask[buf][im0 >> 5] >> (im0 & 31)) & 0xFFu;
+                    const int e = (int)(rel - im0);  // |e| < nh + 8 here
+                    const bool inside = (e - (CW_U - 1) >= 0) && (e + R - 1 < nh32);
+                    if (bits == 0xFFu && inside) {
+#pragma unroll
+                        for (int u = 0; u < CW_U; ++u) {
+                            const T xv = xsb[im0 + u];
+#pragma unroll
+                            for (int r = 0; r < R; ++r) acc[r] = mac_rn(acc[r], xv, w[r - u + CW_U - 1]);
                         }
                     } else {
 #pragma unroll
-                        for (int u = 0; u < RT_U; ++u) {
+                        for (int u = 0; u < CW_U; ++u) {
                             if (!(bits & (1u << u))) continue;
-                            const T xv = xs[im0 + u];
+                            const T xv = xsb[im0 + u];
 #pragma unroll
-                            for (int r = 0; r < RT_R; ++r) {
-                                const int d = rel + r - (im0 + u);  // = t - m
-                                if (d >= 0 && d < nh) acc[r] = mac_rn(acc[r], xv, w[r - u + RT_U - 1]);
-                            }
+                            for (int r = 0; r < R; ++r)  // 0 <= t - m < nh
+                                if ((unsigned)(e + r - u) < (unsigned)nh32)
+                                    acc[r] = mac_rn(acc[r], xv, w[r - u + CW_U - 1]);
                         }
                     }
                 }
             }
+            if (ns < a.nseg) stash(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
+            cs = ns;
+            cmc = nmc;
         }
 #pragma unroll
-        for (int r = 0; r < RT_R; ++r) {
+        for (int r = 0; r < R; ++r) {
             const int64_t t = tj + r;
             if (t < t_end) {
                 const int64_t i = t - a.t0;
@@ -247,6 +264,33 @@ __global__ void __launch_bounds__(RT_TB) k_chain_rt(ChainArgs<T> a) {
             }
         }
     }
+}
+
+template <typename T, int SKIP>
+int launch_chain_r(int R, dim3 grid, cudaStream_t stream, const ChainArgs<T> &a) {
+    switch (R) {
+        case 8: k_chain_w<T, SKIP, 8><<<grid, CW_TB, 0, stream>>>(a); break;
+        case 4: k_chain_w<T, SKIP, 4><<<grid, CW_TB, 0, stream>>>(a); break;
+        case 2: k_chain_w<T, SKIP, 2><<<grid, CW_TB, 0, stream>>>(a); break;
+        default: k_chain_w<T, SKIP, 1><<<grid, CW_TB, 0, stream>>>(a); break;
+    }
+    return SC_OK;
+}
+
+// Outputs per thread: the largest R that still gives every SM about 16 warps
+// (two per sub-partition, each carrying R independent chains).
+int pick_r(int64_t n_out, int64_t channels, size_t es) {
+    static const int forced = [] {
+        const char *v = getenv("SC_CHAIN_R");  // experiment knob
+        return v ? atoi(v) : 0;
+    }();
+    if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
+    (void)es;
+    const int64_t warps_per_sm = 16;
+    const int64_t want_threads = (int64_t)sm_count() * warps_per_sm * 32;
+    for (int R = 8; R > 1; R >>= 1)
+        if (channels * cdiv(n_out, R) >= want_threads) return R;
+    return 1;
 }
 
 template <typename T>
@@ -283,32 +327,16 @@ int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off
         a.ld_st = batch->ld_st;
         SC_REQUIRE(channels >= 1 && channels < 65536, "chain: bad batch");
     }
-    // Grid-stride over 256-output tiles.  A device-gated launch (run_if) is
-    // usually a no-op, so it gets a small grid that exits in microseconds.
+    const int R = pick_r(n_out, channels, sizeof(T));
+    // Grid-stride over tiles.  A device-gated launch (run_if) is usually a
+    // no-op, so it gets a small grid that exits in microseconds.
     const int64_t cap = run_if ? std::max<int64_t>(1, 4 * (int64_t)sm_count() / channels)
                                : (int64_t)INT32_MAX - 1;
-    // Large launches: register-tiled variant (8 outputs/thread).  Small ones
-    // (one streaming block) keep one output per thread for parallelism.
-    static const int64_t rt_min = [] {
-        const char *v = getenv("SC_CHAIN_RT_MIN");  // experiment knob (outputs)
-        return v ? (int64_t)atoll(v) : (int64_t)2 * 148 * RT_TILE;
-    }();
-    if (n_out >= rt_min) {
-        const dim3 grid((unsigned)std::min<int64_t>(cdiv(n_out, RT_TILE), cap), (unsigned)channels);
-        switch (skip_mode) {
-            case SC_SKIP_NONE: k_chain_rt<T, SC_SKIP_NONE><<<grid, RT_TB, 0, stream>>>(a); break;
-            case SC_SKIP_LE: k_chain_rt<T, SC_SKIP_LE><<<grid, RT_TB, 0, stream>>>(a); break;
-            case SC_SKIP_NOT_GT: k_chain_rt<T, SC_SKIP_NOT_GT><<<grid, RT_TB, 0, stream>>>(a); break;
-            default: SC_REQUIRE(false, "chain: bad skip_mode %d", skip_mode);
-        }
-        SC_CHECK_LAUNCH();
-        return SC_OK;
-    }
-    const dim3 grid((unsigned)std::min<int64_t>(cdiv(n_out, TB), cap), (unsigned)channels);
+    const dim3 grid((unsigned)std::min<int64_t>(cdiv(n_out, (int64_t)CW_TB * R), cap), (unsigned)channels);
     switch (skip_mode) {
-        case SC_SKIP_NONE: k_chain<T, SC_SKIP_NONE><<<grid, TB, 0, stream>>>(a); break;
-        case SC_SKIP_LE: k_chain<T, SC_SKIP_LE><<<grid, TB, 0, stream>>>(a); break;
-        case SC_SKIP_NOT_GT: k_chain<T, SC_SKIP_NOT_GT><<<grid, TB, 0, stream>>>(a); break;
+        case SC_SKIP_NONE: launch_chain_r<T, SC_SKIP_NONE>(R, grid, stream, a); break;
+        case SC_SKIP_LE: launch_chain_r<T, SC_SKIP_LE>(R, grid, stream, a); break;
+        case SC_SKIP_NOT_GT: launch_chain_r<T, SC_SKIP_NOT_GT>(R, grid, stream, a); break;
         default: SC_REQUIRE(false, "chain: bad skip_mode %d", skip_mode);
     }
     SC_CHECK_LAUNCH();

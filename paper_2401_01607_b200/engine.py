@@ -190,12 +190,13 @@ class ScatterEngine:
         max(len(ir)-1, live) samples in emission order."""
         t = _dev.torch()
         with t.cuda.device(self._device):
-            st = self._state()
-            cap = max(st["cap"], 1)
-            tail = t.empty(cap, dtype=_dev.torch_dtype(self._npd), device=self._device)
+            self._bind_stream()
+            cap = ctypes.c_int64()
+            N.check(self._lib.sc_engine_tail_bound(self._handle, ctypes.byref(cap)))
+            tail = t.empty(cap.value, dtype=_dev.torch_dtype(self._npd), device=self._device)
             n = ctypes.c_int64()
-            N.check(self._lib.sc_engine_flush(self._handle, N.ptr(tail), cap, ctypes.byref(n)))
-            tail = tail[:n.value].clone()
+            N.check(self._lib.sc_engine_flush(self._handle, N.ptr(tail), cap.value, ctypes.byref(n)))
+            tail = tail[:n.value]
         like = self._ir_signal.samples
         return Signal(_dev.like_input(tail, like), self._sample_rate)
 

@@ -169,12 +169,12 @@ class MultiChannelEngine:
 
         t = _dev.torch()
         with t.cuda.device(self._device):
-            st = self.state()
-            cap = max(max(st["cap"]), 1)
-            tail = t.empty((self._C, cap), dtype=_dev.torch_dtype(self._npd), device=self._device)
-            n = (ctypes.c_int64 * self._C)()
             self._bind()
-            N.check(self._lib.sc_engine_flush(self._handle, N.ptr(tail), cap, n))
+            cap = ctypes.c_int64()
+            N.check(self._lib.sc_engine_tail_bound(self._handle, ctypes.byref(cap)))
+            tail = t.empty((self._C, cap.value), dtype=_dev.torch_dtype(self._npd), device=self._device)
+            n = (ctypes.c_int64 * self._C)()
+            N.check(self._lib.sc_engine_flush(self._handle, N.ptr(tail), cap.value, n))
             host = tail.cpu().numpy()
         return [host[c, :n[c]].copy() for c in range(self._C)]
 
