@@ -52,8 +52,9 @@ def parse():
     ap.add_argument("--config", default="cfg5",
                     choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "short8", "short16", "short32",
                              "short64", "short128", "mstream"])
-    ap.add_argument("--mode", default="fast", choices=["fast", "ffma", "tc"],
-                    help="float32 kernel: fast = picked by shape (tensor cores for long filters)")
+    ap.add_argument("--mode", default="fast", choices=["fast", "ffma", "tc", "ordered"],
+                    help="float32 kernel: fast = picked by shape (tensor cores for long filters); "
+                         "ordered = the sequential-chain kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -227,7 +228,8 @@ class Work:
             from paper_2401_01607_b200.engine import EngineConfig
             from paper_2401_01607_b200.multichannel import MultiChannelEngine
 
-            self.eng = MultiChannelEngine(self.hd, EngineConfig(block_size_nb=8192))
+            self._make_engine = lambda mode: MultiChannelEngine(self.hd, EngineConfig(block_size_nb=8192),
+                                                                mode=mode)
             self.parallelism = f"replicas x{world} (one 64-channel engine per GPU)"
             self.scaling = "weak"
             self.dtype = "f32"
@@ -255,15 +257,31 @@ class Work:
         FAST dispatch) and the padded tensor-core work it issues."""
         self.tc_padded_macs = 0
         if self.cfg.startswith("short"):
-            self.kernel = "k_fir_f32_fast" if self.w.nh < 256 else "k_tc_fir"
+            # FAST dispatch (capi.cu): tensor cores from 256 taps, else k_fir_short
+            self.kernel = "k_tc_fir" if self.w.nh >= 256 else "k_fir_short"
             self.hbm_bound = True
             return
-        if self.dtype != "f32" or self.cfg not in ("cfg3", "cfg4", "cfg5"):
-            self.kernel = "k_chain"
+        if self.cfg == "mstream":
+            # float32 engine: FAST mode puts each IR segment (2 x 64 ch x 240,000
+            # samples x 16,384 taps) on the tensor-core FIR (csrc/engine.cu
+            # fast_stream); --mode ordered keeps the ordered chain
+            fast = self.mode != "ordered"
+            self.eng = self._make_engine("fast" if fast else "ordered")
+            self.kernel = "k_tc_fir" if fast else "k_chain_w"
+            if fast:
+                nh = self.w.nh
+                s8 = -(-((nh + 126) // 128 + 1) // 8) * 8
+                half = (-(-self.w.ne // 8192) // 2) * 8192
+                segs = [half, self.w.ne - half]
+                tiles = sum(-(-(n + nh - 1) // 16384) for n in segs) * self.w.channels
+                self.tc_padded_macs = tiles * 16384 * 128 * s8
+            return
+        if self.dtype != "f32" or self.cfg not in ("cfg3", "cfg4", "cfg5") or self.mode == "ordered":
+            self.kernel = "k_chain_w"   # ordered chain (csrc/k_ordered.cu)
             return
         nh = self.w.nh
         use_tc = self.mode == "tc" or (self.mode == "fast" and nh >= 256)
-        self.kernel = "k_tc_fir" if use_tc else "k_fir_f32_fast"
+        self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 256 else "k_fir_f32_fast")
         if use_tc:
             s = (nh + 126) // 128 + 1
             s8 = -(-s // 8) * 8
@@ -299,8 +317,8 @@ class Work:
             return scatter_convolve(Signal(self.xd), Signal(self.hd), mode=self.mode).body.samples
         if self.cfg == "mstream":
             body = self.eng.process_stream(self.xd, 8192, self.swaps)
-            self.eng.flush()
-            return body
+            tails, _ = self.eng.flush(on_device=True)   # [64, 16383] tails stay in HBM like the body
+            return body, tails
         raise ValueError(self.cfg)
 
     def e2e_step(self, x_pin, h_pin):
@@ -332,7 +350,7 @@ def cpu_sample(cfg, seconds, threads):
     from oracle import oracle as O
     from paper_2401_01607_b200 import configs
 
-    if cfg == "cfg4":
+    if cfg in ("cfg4", "mstream"):   # mstream streams cfg4's channels
         w = configs.cfg4(channels=64, ne=480000)
         x, h = w.x, w.h
     elif cfg == "cfg3":
@@ -347,7 +365,7 @@ def cpu_sample(cfg, seconds, threads):
         x, h = configs.cfg5_x(ne=4_000_000), configs.cfg5_h()
     x = np.asarray(x, np.float64)
     h = np.asarray(h, np.float64)
-    if cfg == "cfg4":
+    if cfg in ("cfg4", "mstream"):
         # one engine per channel on a thread pool (the reference's pattern)
         c = max(1, threads)
         ne0 = 2000
@@ -510,9 +528,25 @@ def main():
             "useful_frac_of_fp32_fma_peak": useful / fp32_peak,
             "kernel": "k_tc_fir (tcgen05.mma kind::f16 128x128x16, TMEM accumulators, cp.async.bulk)",
         }
+    elif work.dtype == "f64":
+        # ordered float64 chain: every MAC is a DMUL and a DADD (separately
+        # rounded, the reference's arithmetic), i.e. 2 FP64-pipe lane-ops; the
+        # FP64 pipe issues 64 lane-ops/clk/SM (tools/ubench/fp64_latency.cu
+        # measured 62.2 for DADD at 32 warps/SM)
+        dp_peak = 64 * sms * sm_max * 1e6 / 1e12  # T lane-ops/s
+        dp_ops = 2 * work.rank_macs / (ms_local * 1e-3) / 1e12
+        roofline = {
+            "bound": "fp64_pipe", "achieved": dp_ops, "peak": dp_peak, "unit": "Tops/s (FP64 pipe lane-ops)",
+            "frac": dp_ops / dp_peak, "traffic": traffic,
+            "peak_source": f"computed: {sms} SMs x 64 FP64 lane-ops/clk x sm_max_mhz {sm_max:.0f}; "
+                           "microbenchmark tools/ubench/fp64_latency.cu: 62.2 lane-ops/clk/SM",
+            "achieved_per_launch": "2 x metric MACs (DMUL + DADD) / mean step time",
+            "frac_at_observed_clock": dp_ops / (64 * sms * med * 1e6 / 1e12),
+            "kernel": work.kernel,
+        }
     else:
         roofline = {
-            "bound": "fp32_fma" if work.dtype == "f32" else "fp64_fma",
+            "bound": "fp32_fma",
             "achieved": useful, "peak": fp32_peak, "unit": "TFLOP/s", "frac": useful / fp32_peak,
             "traffic": traffic,
             "peak_source": f"computed: {sms} SMs x 128 FP32 FMA/clk x 2 FLOP x sm_max_mhz {sm_max:.0f} "
@@ -563,7 +597,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": work.scaling, "vs_baseline": None, "dtype": work.dtype,
             "data": "synthetic (seeded numpy PCG64 recipes of SURVEY.md 8(d); no dataset)",
-            "config": {"workload": w.name, "ne": int(w.ne), "nh": int(w.nh),
+            "config": {"workload": ("mstream_f32_64ch_480000x16384_b8192_1swap_multichannel_engine"
+                                    if args.config == "mstream" else w.name),
+                       "ne": int(w.ne), "nh": int(w.nh),
                        "channels": int(w.channels), "metric_macs": int(work.total_macs),
                        "parallelism": work.parallelism,
                        "l2": "256 MiB memset before every timed step (outside the events); "

@@ -140,6 +140,15 @@ int sc_engine_channels(sc_engine *e, int64_t *channels);
 int sc_engine_destroy(sc_engine *e);
 int sc_engine_set_stream(sc_engine *e, void *stream);
 
+/* Kernel family for fused streams (sc_engine_process_blocks): SC_MODE_ORDERED
+ * (default; bit-identical to block-by-block calls) or SC_MODE_FAST (float32
+ * only): when every IR segment of a call carries >= 2^30 MACs over the
+ * channels, each segment's convolution runs on the FAST FIR path (tensor
+ * cores from 256 taps) and a combine kernel adds the segments and the
+ * residue -- results within the FP32 tolerance, not bit-identical.  Single
+ * blocks and samples stay on the ordered chain. */
+int sc_engine_set_mode(sc_engine *e, int mode);
+
 /* process_block (engine.py:118-146): applies a pending swap first, then
  * consumes block[n] (n <= block_size_nb) and writes out[n].  Async. */
 int sc_engine_process_block(sc_engine *e, const void *block, int64_t n, void *out);

@@ -148,6 +148,50 @@ __global__ void k_blocks_last_scatter(const T *__restrict__ x, int64_t ldx, int6
     }
 }
 
+// ---- FAST fused streams (float32, tensor cores)
+// The fused stream is  out/res_out[t] = res_in[t] (t < cap) + sum over IR
+// segments j of conv(x masked to segment j, h_j)[t]  -- the same sum the
+// ordered chain forms, in another order.  Each segment's convolution runs on
+// the FAST FIR path (tcgen05 kernel from 256 taps) into its own region of fy;
+// k_fast_combine adds the regions that cover each slot in segment order and
+// splits the result into the block outputs and the next residue.  Samples the
+// engine would skip (|x| <= thr, NaN) are zeroed in the masked drive.
+struct FastSegs {
+    int n;
+    int64_t m_lo[kMaxSegs], m_hi[kMaxSegs], nh[kMaxSegs], off[kMaxSegs];
+};
+
+__global__ void k_mask_skip(const float *__restrict__ x, int64_t ldx, int64_t n, double thr,
+                            float *__restrict__ xm, int64_t ldm) {
+    const float *xc = x + blockIdx.y * ldx;
+    float *mc = xm + blockIdx.y * ldm;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = xc[i];
+        mc[i] = skipped<SC_SKIP_NOT_GT>(v, thr) ? 0.0f : v;
+    }
+}
+
+__global__ void k_fast_combine(FastSegs sg, const float *__restrict__ fy, int64_t fy_ld,
+                               const float *__restrict__ rin, int64_t res_ld, const int64_t *__restrict__ st,
+                               int64_t n_total, int64_t n_slots, float *__restrict__ out, int64_t ldo,
+                               float *__restrict__ rout) {
+    const int64_t c = blockIdx.y;
+    const int64_t cap = st[c * ST_N + ST_CAP];
+    const float *yc = fy + c * fy_ld;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_slots;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        float v = t < cap ? rin[c * res_ld + t] : 0.0f;
+        for (int j = 0; j < sg.n; ++j) {
+            const int64_t d = t - sg.m_lo[j];
+            if (d >= 0 && t < sg.m_hi[j] + sg.nh[j] - 1) v += yc[sg.off[j] + d];
+        }
+        if (t < n_total)
+            out[c * ldo + t] = v;
+        else
+            rout[c * res_ld + (t - n_total)] = v;
+    }
+}
+
 // Staging of every IR of a fused call in ONE launch (instead of one
 // cudaMemcpy2DAsync per IR): copy j moves [C][nh_j] from src_j (row pitch
 // sld_j) to stage + off_j (row pitch dld).  grid (x: 256-sample chunks of
@@ -302,6 +346,11 @@ struct sc_engine {
     void *stage = nullptr;
     int64_t stage_ld = 0;
     int64_t *jbuf = nullptr;  // [C][n_blocks] last-scatter index per block
+    // FAST fused streams (float32): masked drive [C][fx_ld] and the per-segment
+    // convolutions [C][fy_ld] (segment j at column offset fy_off[j])
+    int mode = SC_MODE_ORDERED;
+    void *fx = nullptr, *fy = nullptr;
+    int64_t fx_ld = 0, fy_ld = 0;
     int64_t jbuf_ld = 0;
 };
 
@@ -416,6 +465,55 @@ struct DeviceGuard {
 
 // Fused back-to-back blocks (see sc_engine_process_blocks); x/out are
 // [C][ldx]/[C][ldo] rows of n_total samples.
+// FAST fused streams pay ~6 launches per IR segment (tensor-core set-up), so
+// they are used only when every segment is large: >= 2^30 MACs over the
+// channels (the ordered chain needs >= ~30 us for that much work).
+bool fast_stream_worth(const sc_engine *e, const ChainSeg *segs, int nseg) {
+    if (e->mode != SC_MODE_FAST || e->dtype != SC_F32) return false;
+    for (int j = 0; j < nseg; ++j)
+        if ((double)e->C * (double)(segs[j].m_hi - segs[j].m_lo) * (double)segs[j].nh < 1073741824.0) return false;
+    return true;
+}
+
+int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64_t ub, const ChainSeg *segs,
+                int nseg, void *rin, void *rout, void *out, int64_t ldo) {
+    FastSegs sg{};
+    sg.n = nseg;
+    int64_t tot = 0;
+    for (int j = 0; j < nseg; ++j) {
+        sg.m_lo[j] = segs[j].m_lo;
+        sg.m_hi[j] = segs[j].m_hi;
+        sg.nh[j] = segs[j].nh;
+        sg.off[j] = tot;
+        tot += segs[j].m_hi - segs[j].m_lo + segs[j].nh - 1;
+    }
+    int rc = ensure_2d(&e->fx, &e->fx_ld, n_total, 4, e->C, 0, e->stream);
+    if (rc) return rc;
+    rc = ensure_2d(&e->fy, &e->fy_ld, tot, 4, e->C, 0, e->stream);
+    if (rc) return rc;
+    float *xm = static_cast<float *>(e->fx), *fy = static_cast<float *>(e->fy);
+    {
+        const dim3 g((unsigned)std::min<int64_t>(cdiv(n_total, 256), 1024), (unsigned)e->C);
+        k_mask_skip<<<g, 256, 0, e->stream>>>(static_cast<const float *>(x), ldx, n_total, e->thr, xm, e->fx_ld);
+        SC_CHECK_LAUNCH();
+    }
+    for (int j = 0; j < nseg; ++j) {
+        // outputs [m_lo, m_hi + nh - 1) of segment j's drive samples, NaN/Inf
+        // handled by launch_fir_f32's device-gated ordered fallback
+        rc = launch_fir_f32(SC_MODE_FAST, xm, e->fx_ld, 0, segs[j].m_lo, segs[j].m_hi,
+                            static_cast<const float *>(segs[j].h), e->stage_ld, segs[j].nh, fy + sg.off[j], e->fy_ld,
+                            segs[j].m_lo, segs[j].m_hi + segs[j].nh - 1, e->C, e->stream);
+        if (rc) return rc;
+    }
+    const int64_t n_slots = n_total + ub;
+    const dim3 g((unsigned)std::min<int64_t>(cdiv(n_slots, 256), 2048), (unsigned)e->C);
+    k_fast_combine<<<g, 256, 0, e->stream>>>(sg, fy, e->fy_ld, static_cast<const float *>(rin), e->res_ld, e->st,
+                                             n_total, n_slots, static_cast<float *>(out), ldo,
+                                             static_cast<float *>(rout));
+    SC_CHECK_LAUNCH();
+    return SC_OK;
+}
+
 int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64_t nb,
                         const int64_t *swap_blocks, const void *const *swap_irs, const int64_t *swap_nh,
                         const int64_t *swap_ld, int64_t n_swaps, void *out, int64_t ldo) {
@@ -513,9 +611,13 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
     // in ascending order across blocks and IR segments -- the same chain as
     // block-by-block processing (bit-identical), continued from the residue.
     void *rin = e->res[e->cur], *rout = e->res[1 - e->cur];
-    ChainBatch batch{e->C, ldx, e->stage_ld, ldo, e->res_ld, e->res_ld, ST_N};
-    rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, x, 0, segs, nseg, rin, 0, e->st + ST_CAP, 0, n_total + ub,
-                      out, n_total, rout, e->stream, nullptr, &batch);
+    if (fast_stream_worth(e, segs, nseg)) {
+        rc = fast_stream(e, x, ldx, n_total, ub, segs, nseg, rin, rout, out, ldo);
+    } else {
+        ChainBatch batch{e->C, ldx, e->stage_ld, ldo, e->res_ld, e->res_ld, ST_N};
+        rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, x, 0, segs, nseg, rin, 0, e->st + ST_CAP, 0,
+                          n_total + ub, out, n_total, rout, e->stream, nullptr, &batch);
+    }
     if (rc) return rc;
     const dim3 gj((unsigned)n_blocks, (unsigned)e->C);
     if (e->dtype == SC_F64)
@@ -611,7 +713,17 @@ int sc_engine_destroy(sc_engine *e) {
     cudaFree(e->st);
     cudaFree(e->stage);
     cudaFree(e->jbuf);
+    cudaFree(e->fx);
+    cudaFree(e->fy);
     delete e;
+    return SC_OK;
+}
+
+int sc_engine_set_mode(sc_engine *e, int mode) {
+    SC_REQUIRE(e, "null engine");
+    SC_REQUIRE(mode == SC_MODE_ORDERED || mode == SC_MODE_FAST, "engine mode must be ORDERED or FAST, got %d", mode);
+    SC_REQUIRE(mode == SC_MODE_ORDERED || e->dtype == SC_F32, "FAST engine mode needs float32");
+    e->mode = mode;
     return SC_OK;
 }
 

@@ -53,6 +53,17 @@ class EngineConfig:
             raise ValueError(f"tail_policy must be one of {TAIL_POLICIES}, got {self.tail_policy!r}")
 
 
+def _engine_mode(mode, npd) -> bool:
+    """True for the FAST fused-stream mode.  Default: FAST for float32 engines
+    (tensor cores for fused streams whose IR segments carry >= 2^30 MACs),
+    ORDERED for float64 (bit-identical to the reference)."""
+    if mode not in (None, "fast", "ordered"):
+        raise ValueError(f"mode must be 'fast' or 'ordered', got {mode!r}")
+    if mode == "fast" and npd != np.float32:
+        raise ValueError("mode='fast' needs a float32 engine")
+    return npd == np.float32 and mode != "ordered"
+
+
 class ScatterEngine:
     """Stateful block- or sample-driven convolution processor on the GPU.
 
@@ -61,9 +72,10 @@ class ScatterEngine:
     response's (float64 by default, float32 for float32 arrays/tensors).
     """
 
-    def __init__(self, h: Signal, config: EngineConfig | None = None, *, device=None):
+    def __init__(self, h: Signal, config: EngineConfig | None = None, *, device=None, mode=None):
         if len(h) == 0:
             raise ValueError("impulse response is empty")
+        fast = _engine_mode(mode, h.dtype)
         self.config = config if config is not None else EngineConfig()
         t = _dev.torch()
         self._lib = N.lib()
@@ -83,6 +95,9 @@ class ScatterEngine:
                                                int(self.config.block_size_nb),
                                                float(self.config.zero_skip_threshold),
                                                N.stream_ptr(), ctypes.byref(self._handle)))
+            if fast:
+                N.check(self._lib.sc_engine_set_mode(self._handle, N.SC_MODE_FAST))
+        self.mode = "fast" if fast else "ordered"
 
     # ------------------------------------------------------------- plumbing
 
@@ -259,9 +274,13 @@ class ScatterEngine:
         without host synchronisation (one C call; csrc/engine.cu).
 
         ``swaps`` is a sequence of (block_index, impulse_response) pairs: the
-        swap_ir happens right before that block.  Bit-identical to calling
-        swap_ir/process_block in the same order.  Returns the body (device
-        tensor if x is a CUDA tensor, else ndarray).
+        swap_ir happens right before that block.  Ordered mode (float64
+        always): bit-identical to calling swap_ir/process_block in the same
+        order.  Float32 'fast' mode (the float32 default): when every IR
+        segment carries >= 2^30 MACs, each segment is convolved on the
+        tensor-core FIR path and the segments plus the residue are combined --
+        within the FP32 tolerance of the ordered result, same engine state.
+        Returns the body (device tensor if x is a CUDA tensor, else ndarray).
         """
         nb = self.config.block_size_nb if nb is None else int(nb)
         if nb < 1 or nb > self.config.block_size_nb:

@@ -63,10 +63,10 @@ class MultiChannelEngine:
     Blocks are [C, n] arrays/tensors; outputs come back in the same currency.
     """
 
-    def __init__(self, h, config=None, *, channels=None, device=None):
+    def __init__(self, h, config=None, *, channels=None, device=None, mode=None):
         import ctypes
 
-        from .engine import EngineConfig
+        from .engine import EngineConfig, _engine_mode
 
         t = _dev.torch()
         self.config = config if config is not None else EngineConfig()
@@ -79,6 +79,7 @@ class MultiChannelEngine:
         if hd.shape[-1] == 0:
             raise ValueError("impulse response is empty")
         self._npd = npd
+        fast = _engine_mode(mode, npd)
         self._dt = N.dtype_code(npd)
         self._device = t.device(device) if device is not None else t.device("cuda", t.cuda.current_device())
         self._lib = N.lib()
@@ -91,6 +92,9 @@ class MultiChannelEngine:
                                                      int(self.config.block_size_nb),
                                                      float(self.config.zero_skip_threshold),
                                                      N.stream_ptr(), ctypes.byref(self._handle)))
+            if fast:
+                N.check(self._lib.sc_engine_set_mode(self._handle, N.SC_MODE_FAST))
+        self.mode = "fast" if fast else "ordered"
 
     def __del__(self):
         h = getattr(self, "_handle", None)
@@ -163,8 +167,11 @@ class MultiChannelEngine:
         self._ir_rows(h_new)  # validate now (engine.py:188-192)
         self._pending = h_new
 
-    def flush(self):
-        """Per-channel tails (max(len(ir)-1, live_c) samples each) as a list."""
+    def flush(self, *, on_device: bool = False):
+        """Per-channel tails (max(len(ir)-1, live_c) samples each) as a list of
+        host arrays; with on_device=True, (tails [C, max_len] CUDA tensor,
+        lengths) instead -- no device-to-host copy (row c is valid up to
+        lengths[c], zero beyond)."""
         import ctypes
 
         t = _dev.torch()
@@ -175,6 +182,9 @@ class MultiChannelEngine:
             tail = t.empty((self._C, cap.value), dtype=_dev.torch_dtype(self._npd), device=self._device)
             n = (ctypes.c_int64 * self._C)()
             N.check(self._lib.sc_engine_flush(self._handle, N.ptr(tail), cap.value, n))
+            if on_device:
+                lengths = list(n)
+                return tail[:, :max(lengths, default=0)], lengths
             host = tail.cpu().numpy()
         return [host[c, :n[c]].copy() for c in range(self._C)]
 
@@ -196,7 +206,9 @@ class MultiChannelEngine:
     def process_stream(self, x, nb=None, swaps=()):
         """[C, N] through back-to-back blocks of nb with an IR-swap schedule
         ((block_index, IR) pairs, applied to every channel) in one fused
-        launch per <= 31 swaps; bit-identical to the block-by-block calls."""
+        launch per <= 31 swaps; bit-identical to the block-by-block calls in
+        ordered mode (float32 'fast' mode: tensor cores for large segments, see
+        ScatterEngine.process_stream)."""
         import ctypes
 
         t = _dev.torch()

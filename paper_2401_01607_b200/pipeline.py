@@ -13,7 +13,6 @@ from __future__ import annotations
 
 import sys
 
-import numpy as np
 
 from . import _dev
 from .engine import DEFAULT_BLOCK_SIZE, EngineConfig
@@ -77,15 +76,12 @@ def convolve_files(input_path, ir_path, output_path, *, nb: int = DEFAULT_BLOCK_
     if no_tail:
         y = body
     else:
-        tails = engine.flush()
-        lengths = {len(tl) for tl in tails}
-        if len(lengths) > 1:   # write_wav's own check (wavio.py:148-151)
-            n0 = n_in + len(tails[0])
-            bad = next(c for c in range(C) if len(tails[c]) != len(tails[0]))
-            raise ValueError(f"channel lengths differ: channel 0 has {n0}, channel {bad} has "
-                             f"{n_in + len(tails[bad])}")
-        tail = t.from_numpy(np.stack(tails)).to(x.device) if lengths.pop() else x[:, :0]
-        y = t.cat([body, tail], dim=1)
+        tail, lengths = engine.flush(on_device=True)
+        if len(set(lengths)) > 1:   # write_wav's own check (wavio.py:148-151)
+            bad = next(c for c in range(C) if lengths[c] != lengths[0])
+            raise ValueError(f"channel lengths differ: channel 0 has {n_in + lengths[0]}, channel {bad} has "
+                             f"{n_in + lengths[bad]}")
+        y = t.cat([body, tail[:, :lengths[0]]], dim=1)
 
     gain = 1.0
     if normalize is not None:

@@ -1,0 +1,132 @@
+"""Float32 FAST fused streams (csrc/engine.cu fast_stream): every IR segment
+with >= 2^30 MACs is convolved on the tensor-core FIR path and combined with
+the residue.  Checked against the float64 oracle engine (tolerance
+1e-5 * max|x| * ||h||_1 per channel, the FP32 bar) and against the ordered
+engine for the data-dependent state (live / cap / read_index, tail lengths)
+and the NaN/Inf pattern."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _tol(x, h):
+    return 1e-5 * float(np.max(np.abs(x))) * float(np.sum(np.abs(h)))
+
+
+def _oracle_stream(x, irs_at, nb, thr=0.0):
+    """float64 reference engine over blocks of nb with swaps {block: h}."""
+    eng = oracle.OracleEngine(irs_at[0].astype(np.float64), nb, thr)
+    out = []
+    for b, s in enumerate(range(0, len(x), nb)):
+        if b in irs_at and b > 0:
+            eng.swap_ir(irs_at[b].astype(np.float64))
+        out.append(eng.process_block(x[s:s + nb].astype(np.float64)))
+    return np.concatenate(out), eng.flush()
+
+
+def test_single_channel_fast_vs_oracle_and_ordered():
+    import torch
+
+    from paper_2401_01607_b200.core import Signal
+    from paper_2401_01607_b200.engine import EngineConfig, ScatterEngine
+
+    rng = np.random.default_rng(11)
+    n, nh, nb = 1 << 20, 4096, 8192
+    x = rng.uniform(-1, 1, n).astype(np.float32)
+    x[rng.uniform(size=n) < 0.1] = 0.0           # skipped samples
+    x[1000:1010] = np.nan                         # engine skips NaN
+    h0 = (rng.standard_normal(nh) * np.exp(-np.arange(nh) / 700)).astype(np.float32)
+    h1 = (rng.standard_normal(3000) * np.exp(-np.arange(3000) / 500)).astype(np.float32)
+    swap_block = (n // nb) // 2                   # 2 segments of 2^19 x ~4k taps: > 2^30 MACs each
+    outs, tails, states = {}, {}, {}
+    for mode in ("fast", "ordered"):
+        eng = ScatterEngine(Signal(torch.from_numpy(h0).cuda()), EngineConfig(block_size_nb=nb,
+                                                                             zero_skip_threshold=0.0),
+                            mode=mode)
+        assert eng.mode == mode
+        body = eng.process_stream(torch.from_numpy(x).cuda(), nb, [(swap_block, torch.from_numpy(h1).cuda())])
+        states[mode] = eng.state_dict()["live"], eng._state()["cap"], eng._state()["read_index"]
+        tails[mode] = eng.flush().samples.cpu().numpy()
+        outs[mode] = body.cpu().numpy()
+    ref_body, ref_tail = _oracle_stream(x, {0: h0, swap_block: h1}, nb)
+    tol = max(_tol(np.nan_to_num(x), h0), _tol(np.nan_to_num(x), h1))
+    assert states["fast"] == states["ordered"]
+    assert len(tails["fast"]) == len(tails["ordered"]) == len(ref_tail)
+    for mode in ("fast", "ordered"):
+        assert np.max(np.abs(outs[mode] - ref_body)) <= tol, mode
+        assert np.max(np.abs(tails[mode] - ref_tail)) <= tol, mode
+    assert not np.array_equal(outs["fast"], outs["ordered"])   # really a different kernel
+
+
+def test_multichannel_fast_residue_carry_and_threshold():
+    import torch
+
+    from paper_2401_01607_b200.engine import EngineConfig
+    from paper_2401_01607_b200.multichannel import MultiChannelEngine
+
+    rng = np.random.default_rng(12)
+    C, n, nh, nb, thr = 8, 1 << 18, 2048, 4096, 0.05
+    x = rng.uniform(-1, 1, (C, n)).astype(np.float32)
+    h = (rng.standard_normal((C, nh)) * np.exp(-np.arange(nh) / 300)).astype(np.float32)
+    eng = MultiChannelEngine(torch.from_numpy(h).cuda(), EngineConfig(block_size_nb=nb, zero_skip_threshold=thr))
+    assert eng.mode == "fast"
+    # two calls: the second continues from the residue of the first
+    half = n // 2
+    b1 = eng.process_stream(torch.from_numpy(x[:, :half]).cuda(), nb).cpu().numpy()
+    b2 = eng.process_stream(torch.from_numpy(x[:, half:]).cuda(), nb).cpu().numpy()
+    tails = eng.flush()
+    for c in range(C):
+        ref_body, ref_tail = _oracle_stream(x[c], {0: h[c]}, nb, thr)
+        tol = _tol(x[c], h[c])
+        got = np.concatenate([b1[c], b2[c]])
+        assert np.max(np.abs(got - ref_body)) <= tol, c
+        assert len(tails[c]) == len(ref_tail)
+        assert np.max(np.abs(tails[c] - ref_tail)) <= tol, c
+
+
+def test_fast_nonfinite_pattern_matches_ordered():
+    import torch
+
+    from paper_2401_01607_b200.core import Signal
+    from paper_2401_01607_b200.engine import EngineConfig, ScatterEngine
+
+    rng = np.random.default_rng(13)
+    n, nh, nb = 1 << 19, 4096, 8192
+    x = rng.uniform(-1, 1, n).astype(np.float32)
+    x[300000] = np.inf
+    h = rng.standard_normal(nh).astype(np.float32)
+    h[17] = 0.0                                   # 0 * inf -> NaN at one output
+    res = {}
+    for mode in ("fast", "ordered"):
+        eng = ScatterEngine(Signal(torch.from_numpy(h).cuda()), EngineConfig(block_size_nb=nb), mode=mode)
+        res[mode] = eng.process_stream(torch.from_numpy(x).cuda(), nb).cpu().numpy()
+    for f in (np.isnan, np.isposinf, np.isneginf):
+        np.testing.assert_array_equal(f(res["fast"]), f(res["ordered"]))
+    fin = np.isfinite(res["ordered"])
+    assert np.max(np.abs(res["fast"][fin] - res["ordered"][fin])) <= _tol(np.where(np.isfinite(x), x, 0), h)
+
+
+def test_small_segments_stay_ordered_and_mode_validation():
+    import torch
+
+    from paper_2401_01607_b200.core import Signal
+    from paper_2401_01607_b200.engine import EngineConfig, ScatterEngine
+
+    rng = np.random.default_rng(14)
+    x = rng.uniform(-1, 1, 50000).astype(np.float32)
+    h = rng.standard_normal(512).astype(np.float32)
+    a = ScatterEngine(Signal(torch.from_numpy(h).cuda()), EngineConfig(block_size_nb=1024))
+    b = ScatterEngine(Signal(torch.from_numpy(h).cuda()), EngineConfig(block_size_nb=1024), mode="ordered")
+    ya = a.process_stream(torch.from_numpy(x).cuda(), 1024).cpu().numpy()
+    yb = b.process_stream(torch.from_numpy(x).cuda(), 1024).cpu().numpy()
+    np.testing.assert_array_equal(ya, yb)         # 25.6M MACs: below the FAST threshold
+    with pytest.raises(ValueError, match="float32"):
+        ScatterEngine(Signal(np.ones(4)), mode="fast")
+    with pytest.raises(ValueError, match="mode must be"):
+        ScatterEngine(Signal(h), mode="tc")
