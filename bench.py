@@ -257,9 +257,12 @@ class Work:
         FAST dispatch) and the padded tensor-core work it issues."""
         self.tc_padded_macs = 0
         if self.cfg.startswith("short"):
-            # FAST dispatch (capi.cu): tensor cores from 256 taps, else k_fir_short
-            self.kernel = "k_tc_fir" if self.w.nh >= 256 else "k_fir_short"
-            self.hbm_bound = True
+            # FAST dispatch (capi.cu / k_fast_f32.cu): tensor cores from 256
+            # taps, the streaming k_fir_short up to 32 (HBM-bound), the smem
+            # k_fir_short_smem in between (FMA-bound)
+            nh = self.w.nh
+            self.kernel = "k_tc_fir" if nh >= 256 else ("k_fir_short" if nh <= 32 else "k_fir_short_smem")
+            self.hbm_bound = nh <= 32
             return
         if self.cfg == "mstream":
             # float32 engine: FAST mode puts each IR segment (2 x 64 ch x 240,000
@@ -281,7 +284,8 @@ class Work:
             return
         nh = self.w.nh
         use_tc = self.mode == "tc" or (self.mode == "fast" and nh >= 256)
-        self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 256 else "k_fir_f32_fast")
+        self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 32 else
+                                                 "k_fir_short_smem" if nh <= 256 else "k_fir_f32_fast")
         if use_tc:
             s = (nh + 126) // 128 + 1
             s8 = -(-s // 8) * 8
@@ -463,8 +467,9 @@ def main():
         if world > 1:
             dist.barrier()
 
-    # warm-up
+    # warm-up (same sequence as a timed step: L2 flush, then the step)
     for _ in range(max(args.warmup, 0)):
+        flush.zero_()
         work.step()
     torch.cuda.synchronize()
     barrier()
@@ -479,6 +484,10 @@ def main():
     launches0 = L.sc_launch_count()
     with ClockSampler(nvml_index) as clocks:
         t_wall0 = time.perf_counter()
+        # ~1 ms of device-side spin ahead of the first step, so the host's
+        # enqueue of step 0 does not show up as idle time inside its events
+        # (later steps are enqueued while the previous one runs)
+        torch.cuda._sleep(2_000_000)
         for i in range(args.steps):
             flush.zero_()
             starts[i].record()

@@ -236,8 +236,103 @@ __global__ void k_pad_taps(const float *__restrict__ h, int64_t ldh, int64_t nh,
     hp[(int64_t)ch * ldhp + i] = i < nh ? h[(int64_t)ch * ldh + i] : 0.0f;
 }
 
-// ---------------------------------------------------------------- short filters
-// Nh <= 256: the ring/split machinery above is overhead.  Each CTA stages one
+// ---------------------------------------------------------------- short filters, HBM-bound (Nh <= 32)
+// Nh <= 32 (HBM-bound up to ~40 taps; longer filters use k_fir_short_smem
+// below, whose smem window feeds more FMAs per L1 wavefront): no staging of x at
+// all.  Each thread owns 8 consecutive outputs t0..t0+7 and slides a
+// 12-float register window over x in float4 steps: for the 4 taps
+// 4kb..4kb+3 it needs x[t0-4kb-3 .. t0-4kb+7], and moving to the next 4 taps
+// drops the top float4 and loads one new float4 below (renaming only: the
+// tap-block loop is unrolled at compile time, NKB = ceil(Nh/4) blocks).  So
+// a thread issues NKB+2 LDG.128 (L1 hits for all but ~1/3: neighbouring
+// threads share windows), one broadcast LDS.128 of taps and 32 FFMA per 4
+// taps, and two float4 stores.  Each output accumulates taps in ascending
+// order (fmaf), identical in interior and edge tiles.  Taps past Nh (zero
+// padding of the last block) are never multiplied, so NaN/Inf inputs next to
+// them cannot leak.  Tiles whose window leaves the valid input range [x_lo,
+// x_hi) (the first and last few) take a guarded scalar path that multiplies
+// only taps whose input exists -- the reference's edge semantics.
+constexpr int SH_THREADS = 256;
+constexpr int SH_R = 8;
+constexpr int SH_TILE = SH_THREADS * SH_R;  // 2048 outputs per CTA
+constexpr int SH_MAXNH = 256;
+
+template <int NKB>
+__global__ void __launch_bounds__(SH_THREADS) k_fir_short(const float *__restrict__ x, int64_t ldx, int64_t x_base,
+                                                          int64_t x_lo, int64_t x_hi, const float *__restrict__ h,
+                                                          int64_t ldh, int nh, float *__restrict__ y, int64_t ldy,
+                                                          int64_t n_begin, int64_t n_end, const unsigned *run_if) {
+    __shared__ __align__(16) float hsm[4 * NKB];
+    if (run_if && *run_if == 0) return;
+    const int ch = blockIdx.y;
+    const float *xc = x + (int64_t)ch * ldx;
+    const float *hc = h + (int64_t)ch * ldh;
+    float *yc = y + (int64_t)ch * ldy;
+    for (int k = threadIdx.x; k < 4 * NKB; k += SH_THREADS) hsm[k] = k < nh ? hc[k] : 0.0f;
+    __syncthreads();
+    const int64_t n0 = n_begin + (int64_t)blockIdx.x * SH_TILE;
+    const int64_t t0 = n0 + (int64_t)threadIdx.x * SH_R;
+    const int nkb = (nh + 3) >> 2;
+    const int nfull = nh >> 2;  // blocks whose 4 taps all exist
+    float acc[SH_R];
+#pragma unroll
+    for (int r = 0; r < SH_R; ++r) acc[r] = 0.0f;
+    // CTA-uniform: every float4 the window reads lies in [x_lo, x_hi), is
+    // aligned, and the tile is whole
+    const float *xt = xc + (n0 - x_base);
+    const bool interior = n0 - 4 * nkb >= x_lo && n0 + SH_TILE <= x_hi && n0 + SH_TILE <= n_end &&
+                          ((reinterpret_cast<uintptr_t>(xt) | reinterpret_cast<uintptr_t>(yc + (n0 - n_begin)) |
+                            (uintptr_t)(ldx * 4) | (uintptr_t)(ldy * 4)) & 15) == 0;
+    if (interior) {
+        const float4 *xp = reinterpret_cast<const float4 *>(xc + (t0 - x_base));  // x[t0 .. t0+3]
+        float4 g2 = __ldg(xp + 1), g1 = __ldg(xp), g0 = __ldg(xp - 1);        // x[t0-4 .. t0+7]
+        const float4 *h4 = reinterpret_cast<const float4 *>(hsm);
+#pragma unroll
+        for (int kb = 0; kb < NKB; ++kb) {
+            if (kb < nkb) {
+                const float w[12] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, g2.y, g2.z, g2.w};
+                const float4 hq = h4[kb];
+                const float hk[4] = {hq.x, hq.y, hq.z, hq.w};
+                // next window (x[t0-4kb-8 .. t0-4kb-5]) in flight during the FMAs
+                const float4 gn = kb + 1 < nkb ? __ldg(xp - (kb + 2)) : g0;
+                if (kb < nfull) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int r = 0; r < SH_R; ++r) acc[r] = fmaf(w[r - u + 4], hk[u], acc[r]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (4 * kb + u < nh)
+#pragma unroll
+                            for (int r = 0; r < SH_R; ++r) acc[r] = fmaf(w[r - u + 4], hk[u], acc[r]);
+                }
+                g2 = g1;
+                g1 = g0;
+                g0 = gn;
+            }
+        }
+        float4 *d = reinterpret_cast<float4 *>(yc + (t0 - n_begin));
+        d[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        d[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        return;
+    }
+    // edge tiles: scalar, only taps whose input exists, k ascending
+    for (int k = 0; k < nh; ++k) {
+        const float hk = hsm[k];
+#pragma unroll
+        for (int r = 0; r < SH_R; ++r) {
+            const int64_t m = t0 + r - k;
+            if (m >= x_lo && m < x_hi) acc[r] = fmaf(__ldg(xc + (m - x_base)), hk, acc[r]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < SH_R; ++r)
+        if (t0 + r < n_end) yc[t0 + r - n_begin] = acc[r];
+}
+
+// ---------------------------------------------------------------- short filters, FMA-bound (32 < Nh <= 256)
+// 32 < Nh <= 256 (FMA-bound): the ring/split machinery above is overhead.  Each CTA stages one
 // contiguous x tile (4096 outputs + Nh-1 halo, float4 loads) and the taps in
 // smem; each thread computes 16 consecutive outputs.  Per 4 taps a thread
 // reads its 20-float input window with 5 LDS.128 plus the 4 taps with one
@@ -249,20 +344,19 @@ __global__ void k_pad_taps(const float *__restrict__ h, int64_t ldh, int64_t nh,
 // (8 B per output), FMA-bound beyond ~40 taps.  Edge tiles (touching the ends
 // of the valid input range) only multiply taps whose input exists, so
 // non-finite taps propagate exactly as in the reference.
-constexpr int SH_THREADS = 256;
-constexpr int SH_R = 16;
-constexpr int SH_TILE = SH_THREADS * SH_R;  // 4096
-constexpr int SH_MAXNH = 256;
+constexpr int SM_THREADS = 256;
+constexpr int SM_R = 16;
+constexpr int SM_TILE = SM_THREADS * SM_R;  // 4096
 
 __device__ __forceinline__ int sh_pos(int i) { return i + ((i >> 4) << 2); }
 
-__global__ void __launch_bounds__(SH_THREADS) k_fir_short(const float *__restrict__ x, int64_t ldx, int64_t x_base,
+__global__ void __launch_bounds__(SM_THREADS) k_fir_short_smem(const float *__restrict__ x, int64_t ldx, int64_t x_base,
                                                           int64_t x_lo, int64_t x_hi, const float *__restrict__ h,
                                                           int64_t ldh, int nh, float *__restrict__ y, int64_t ldy,
                                                           int64_t n_begin, int64_t n_end, const unsigned *run_if) {
     // xs[i] = X(n0 - nh_pad + 1 + i) with nh_pad = nh rounded up to 4 (so the
     // tile start is float4-aligned whenever n0 is), i in [0, 4096 + nh_pad + 4)
-    constexpr int XS = SH_TILE + SH_MAXNH + 8;
+    constexpr int XS = SM_TILE + SH_MAXNH + 8;
     __shared__ __align__(16) float xs[XS + XS / 4];
     __shared__ __align__(16) float hsm[SH_MAXNH + 4];
     if (run_if && *run_if == 0) return;
@@ -271,26 +365,26 @@ __global__ void __launch_bounds__(SH_THREADS) k_fir_short(const float *__restric
     const float *hc = h + (int64_t)ch * ldh;
     float *yc = y + (int64_t)ch * ldy;
     const int nhp = (nh + 3) & ~3;
-    const int64_t n0 = n_begin + (int64_t)blockIdx.x * SH_TILE;
+    const int64_t n0 = n_begin + (int64_t)blockIdx.x * SM_TILE;
     const int64_t m0 = n0 - nhp;  // input index of xs[0] (float4-aligned with n0)
-    const int nx = SH_TILE + nhp;
-    for (int k = threadIdx.x; k < SH_MAXNH + 4; k += SH_THREADS) hsm[k] = k < nh ? hc[k] : 0.0f;
-    const bool edge = m0 < x_lo || n0 + SH_TILE > x_hi;
+    const int nx = SM_TILE + nhp;
+    for (int k = threadIdx.x; k < SH_MAXNH + 4; k += SM_THREADS) hsm[k] = k < nh ? hc[k] : 0.0f;
+    const bool edge = m0 < x_lo || n0 + SM_TILE > x_hi;
     const float *src = xc + (m0 - x_base);
     if (!edge && m0 + nx <= x_hi && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-        for (int i4 = threadIdx.x; i4 < nx / 4; i4 += SH_THREADS)
+        for (int i4 = threadIdx.x; i4 < nx / 4; i4 += SM_THREADS)
             *reinterpret_cast<float4 *>(&xs[sh_pos(4 * i4)]) = __ldg(reinterpret_cast<const float4 *>(src) + i4);
     } else {
-        for (int i = threadIdx.x; i < nx; i += SH_THREADS) {
+        for (int i = threadIdx.x; i < nx; i += SM_THREADS) {
             const int64_t m = m0 + i;
             xs[sh_pos(i)] = (m >= x_lo && m < x_hi) ? __ldg(xc + (m - x_base)) : 0.0f;
         }
     }
     __syncthreads();
-    float acc[SH_R];
+    float acc[SM_R];
 #pragma unroll
-    for (int r = 0; r < SH_R; ++r) acc[r] = 0.0f;
-    const int j16 = threadIdx.x * SH_R;
+    for (int r = 0; r < SM_R; ++r) acc[r] = 0.0f;
+    const int j16 = threadIdx.x * SM_R;
     const int64_t t0 = n0 + j16;  // this thread's first output
     // output t0+r, tap k reads X(t0 + r - k) = xs[j16 + r - k + nhp]
     for (int k0 = 0; k0 < nh; k0 += 4) {
@@ -314,7 +408,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_fir_short(const float *__restric
             for (int u = 0; u < 4; ++u) {
                 if (k0 + u < nh) {
 #pragma unroll
-                    for (int r = 0; r < SH_R; ++r) acc[r] = fmaf(w[r - u + 4], hk[u], acc[r]);
+                    for (int r = 0; r < SM_R; ++r) acc[r] = fmaf(w[r - u + 4], hk[u], acc[r]);
                 }
             }
         } else {
@@ -323,7 +417,7 @@ __global__ void __launch_bounds__(SH_THREADS) k_fir_short(const float *__restric
                 const int k = k0 + u;
                 if (k < nh) {
 #pragma unroll
-                    for (int r = 0; r < SH_R; ++r) {
+                    for (int r = 0; r < SM_R; ++r) {
                         const int64_t m = t0 + r - k;
                         if (m >= x_lo && m < x_hi) acc[r] = fmaf(w[r - u + 4], hk[u], acc[r]);
                     }
@@ -332,13 +426,13 @@ __global__ void __launch_bounds__(SH_THREADS) k_fir_short(const float *__restric
         }
     }
     float *d = yc + (t0 - n_begin);
-    if (t0 + SH_R <= n_end && (reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+    if (t0 + SM_R <= n_end && (reinterpret_cast<uintptr_t>(d) & 15) == 0) {
 #pragma unroll
-        for (int c = 0; c < SH_R / 4; ++c)
+        for (int c = 0; c < SM_R / 4; ++c)
             reinterpret_cast<float4 *>(d)[c] = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
     } else {
 #pragma unroll
-        for (int r = 0; r < SH_R; ++r)
+        for (int r = 0; r < SM_R; ++r)
             if (t0 + r < n_end) d[r] = acc[r];
     }
 }
@@ -373,12 +467,26 @@ int launch_fir_f32_fast(const float *x, int64_t ldx, int64_t x_base, int64_t x_l
     if (n_len <= 0 || channels <= 0) return SC_OK;
     SC_REQUIRE(nh >= 1, "fir: empty impulse response");
     SC_REQUIRE(channels < 65536, "fir: too many channels");
+    if (nh > 32 && nh <= SH_MAXNH) {
+        const int64_t tiles = cdiv(n_len, SM_TILE);
+        SC_REQUIRE(tiles < (int64_t)INT32_MAX, "fir: output range too large");
+        dim3 g((unsigned)tiles, (unsigned)channels);
+        k_fir_short_smem<<<g, SM_THREADS, 0, stream>>>(x, ldx, x_base, x_lo, x_hi, h, ldh, (int)nh, y, ldy, n_begin,
+                                                       n_end, run_if);
+        SC_CHECK_LAUNCH();
+        return SC_OK;
+    }
     if (nh <= SH_MAXNH) {
         const int64_t tiles = cdiv(n_len, SH_TILE);
         SC_REQUIRE(tiles < (int64_t)INT32_MAX, "fir: output range too large");
         dim3 g((unsigned)tiles, (unsigned)channels);
-        k_fir_short<<<g, SH_THREADS, 0, stream>>>(x, ldx, x_base, x_lo, x_hi, h, ldh, (int)nh, y, ldy, n_begin,
-                                                  n_end, run_if);
+#define SC_SHORT(NKB) k_fir_short<NKB><<<g, SH_THREADS, 0, stream>>>(x, ldx, x_base, x_lo, x_hi, h, ldh, (int)nh, \
+                                                                   y, ldy, n_begin, n_end, run_if)
+        if (nh <= 4) SC_SHORT(1);
+        else if (nh <= 8) SC_SHORT(2);
+        else if (nh <= 16) SC_SHORT(4);
+        else SC_SHORT(8);
+#undef SC_SHORT
         SC_CHECK_LAUNCH();
         return SC_OK;
     }
