@@ -161,16 +161,57 @@ struct FastSegs {
     int64_t m_lo[kMaxSegs], m_hi[kMaxSegs], nh[kMaxSegs], off[kMaxSegs];
 };
 
-__global__ void k_mask_skip(const float *__restrict__ x, int64_t ldx, int64_t n, double thr,
-                            float *__restrict__ xm, int64_t ldm) {
-    const float *xc = x + blockIdx.y * ldx;
-    float *mc = xm + blockIdx.y * ldm;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+// One CTA per (engine block, channel): zero the samples the engine skips and
+// record the block's last scattering index J (the k_blocks_last_scatter
+// result, from the same pass over x).  The engine's test !(|x| > thr) is done
+// in float against keep = the smallest float above thr (|x| > thr  <=>
+// |x| >= keep for float x; NaN fails both), float4-wide when aligned.
+__global__ void k_mask_skip(const float *__restrict__ x, int64_t ldx, int64_t n_total, int64_t nb, float keep,
+                            float *__restrict__ xm, int64_t ldm, int64_t n_blocks, int64_t *__restrict__ J,
+                            bool vec4) {
+    const int64_t b = blockIdx.x;
+    const float *xc = x + blockIdx.y * ldx + b * nb;
+    float *mc = xm + blockIdx.y * ldm + b * nb;
+    const int64_t n = n_total - b * nb < nb ? n_total - b * nb : nb;
+    long long j = -1;
+    int64_t i0 = 0;
+    if (vec4) {
+        const int64_t n4 = n >> 2;
+        for (int64_t q = threadIdx.x; q < n4; q += blockDim.x) {
+            float4 v = reinterpret_cast<const float4 *>(xc)[q];
+            const bool k0 = fabsf(v.x) >= keep, k1 = fabsf(v.y) >= keep, k2 = fabsf(v.z) >= keep,
+                       k3 = fabsf(v.w) >= keep;
+            v.x = k0 ? v.x : 0.0f, v.y = k1 ? v.y : 0.0f, v.z = k2 ? v.z : 0.0f, v.w = k3 ? v.w : 0.0f;
+            reinterpret_cast<float4 *>(mc)[q] = v;
+            const long long base = 4 * q;
+            if (k3) j = base + 3;
+            else if (k2) j = base + 2;
+            else if (k1) j = base + 1;
+            else if (k0) j = base;
+        }
+        i0 = n4 << 2;
+    }
+    for (int64_t i = i0 + threadIdx.x; i < n; i += blockDim.x) {
         const float v = xc[i];
-        mc[i] = skipped<SC_SKIP_NOT_GT>(v, thr) ? 0.0f : v;
+        const bool keepv = fabsf(v) >= keep;
+        mc[i] = keepv ? v : 0.0f;
+        if (keepv) j = i;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long v = __shfl_xor_sync(0xffffffffu, j, o);
+        j = v > j ? v : j;
+    }
+    __shared__ long long sj[32];
+    if ((threadIdx.x & 31) == 0) sj[threadIdx.x >> 5] = j;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) j = sj[w] > j ? sj[w] : j;
+        J[blockIdx.y * n_blocks + b] = j;
     }
 }
 
+// 4 consecutive slots per thread; segments that miss the 4 slots are skipped
+// with one test.
 __global__ void k_fast_combine(FastSegs sg, const float *__restrict__ fy, int64_t fy_ld,
                                const float *__restrict__ rin, int64_t res_ld, const int64_t *__restrict__ st,
                                int64_t n_total, int64_t n_slots, float *__restrict__ out, int64_t ldo,
@@ -178,17 +219,27 @@ __global__ void k_fast_combine(FastSegs sg, const float *__restrict__ fy, int64_
     const int64_t c = blockIdx.y;
     const int64_t cap = st[c * ST_N + ST_CAP];
     const float *yc = fy + c * fy_ld;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_slots;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        float v = t < cap ? rin[c * res_ld + t] : 0.0f;
+    for (int64_t t4 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; t4 < n_slots;
+         t4 += (int64_t)gridDim.x * blockDim.x * 4) {
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = t4 + q < cap && t4 + q < n_slots ? rin[c * res_ld + t4 + q] : 0.0f;
         for (int j = 0; j < sg.n; ++j) {
-            const int64_t d = t - sg.m_lo[j];
-            if (d >= 0 && t < sg.m_hi[j] + sg.nh[j] - 1) v += yc[sg.off[j] + d];
+            const int64_t lo = sg.m_lo[j], hi = sg.m_hi[j] + sg.nh[j] - 1;
+            if (t4 + 3 < lo || t4 >= hi) continue;
+            const float *src = yc + sg.off[j] - lo;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (t4 + q >= lo && t4 + q < hi) v[q] += src[t4 + q];
         }
-        if (t < n_total)
-            out[c * ldo + t] = v;
-        else
-            rout[c * res_ld + (t - n_total)] = v;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t t = t4 + q;
+            if (t < n_total)
+                out[c * ldo + t] = v[q];
+            else if (t < n_slots)
+                rout[c * res_ld + (t - n_total)] = v[q];
+        }
     }
 }
 
@@ -475,8 +526,10 @@ bool fast_stream_worth(const sc_engine *e, const ChainSeg *segs, int nseg) {
     return true;
 }
 
-int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64_t ub, const ChainSeg *segs,
-                int nseg, void *rin, void *rout, void *out, int64_t ldo) {
+// Also fills e->jbuf (last scattering index per block) from its mask pass.
+int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64_t nb, int64_t ub,
+                const ChainSeg *segs, int nseg, void *rin, void *rout, void *out, int64_t ldo) {
+    const int64_t n_blocks = cdiv(n_total, nb);
     FastSegs sg{};
     sg.n = nseg;
     int64_t tot = 0;
@@ -493,8 +546,14 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
     if (rc) return rc;
     float *xm = static_cast<float *>(e->fx), *fy = static_cast<float *>(e->fy);
     {
-        const dim3 g((unsigned)std::min<int64_t>(cdiv(n_total, 256), 1024), (unsigned)e->C);
-        k_mask_skip<<<g, 256, 0, e->stream>>>(static_cast<const float *>(x), ldx, n_total, e->thr, xm, e->fx_ld);
+        const dim3 g((unsigned)n_blocks, (unsigned)e->C);
+        // smallest float strictly above thr (thr >= 0): |x| > thr <=> |x| >= keep
+        float keep = (float)e->thr;
+        if ((double)keep <= e->thr) keep = nextafterf(keep, INFINITY);
+        const bool vec4 = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(xm)) & 15) == 0 &&
+                          ldx % 4 == 0 && e->fx_ld % 4 == 0 && nb % 4 == 0;
+        k_mask_skip<<<g, 256, 0, e->stream>>>(static_cast<const float *>(x), ldx, n_total, nb, keep, xm, e->fx_ld,
+                                              n_blocks, e->jbuf, vec4);
         SC_CHECK_LAUNCH();
     }
     for (int j = 0; j < nseg; ++j) {
@@ -506,7 +565,7 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
         if (rc) return rc;
     }
     const int64_t n_slots = n_total + ub;
-    const dim3 g((unsigned)std::min<int64_t>(cdiv(n_slots, 256), 2048), (unsigned)e->C);
+    const dim3 g((unsigned)std::min<int64_t>(cdiv(n_slots, 1024), 4096), (unsigned)e->C);
     k_fast_combine<<<g, 256, 0, e->stream>>>(sg, fy, e->fy_ld, static_cast<const float *>(rin), e->res_ld, e->st,
                                              n_total, n_slots, static_cast<float *>(out), ldo,
                                              static_cast<float *>(rout));
@@ -612,21 +671,22 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
     // block-by-block processing (bit-identical), continued from the residue.
     void *rin = e->res[e->cur], *rout = e->res[1 - e->cur];
     if (fast_stream_worth(e, segs, nseg)) {
-        rc = fast_stream(e, x, ldx, n_total, ub, segs, nseg, rin, rout, out, ldo);
+        rc = fast_stream(e, x, ldx, n_total, nb, ub, segs, nseg, rin, rout, out, ldo);
+        if (rc) return rc;
     } else {
         ChainBatch batch{e->C, ldx, e->stage_ld, ldo, e->res_ld, e->res_ld, ST_N};
         rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, x, 0, segs, nseg, rin, 0, e->st + ST_CAP, 0,
                           n_total + ub, out, n_total, rout, e->stream, nullptr, &batch);
+        if (rc) return rc;
+        const dim3 gj((unsigned)n_blocks, (unsigned)e->C);
+        if (e->dtype == SC_F64)
+            k_blocks_last_scatter<double><<<gj, 256, 0, e->stream>>>(static_cast<const double *>(x), ldx, n_total,
+                                                                    nb, e->thr, n_blocks, e->jbuf);
+        else
+            k_blocks_last_scatter<float><<<gj, 256, 0, e->stream>>>(static_cast<const float *>(x), ldx, n_total,
+                                                                   nb, e->thr, n_blocks, e->jbuf);
+        SC_CHECK_LAUNCH();
     }
-    if (rc) return rc;
-    const dim3 gj((unsigned)n_blocks, (unsigned)e->C);
-    if (e->dtype == SC_F64)
-        k_blocks_last_scatter<double><<<gj, 256, 0, e->stream>>>(static_cast<const double *>(x), ldx, n_total, nb,
-                                                                e->thr, n_blocks, e->jbuf);
-    else
-        k_blocks_last_scatter<float><<<gj, 256, 0, e->stream>>>(static_cast<const float *>(x), ldx, n_total, nb,
-                                                               e->thr, n_blocks, e->jbuf);
-    SC_CHECK_LAUNCH();
     k_stream_state<<<(unsigned)e->C, SS_TB, 0, e->stream>>>(e->jbuf, n_blocks, nb, n_total, e->nh, sev, e->st);
     SC_CHECK_LAUNCH();
     // host-side bookkeeping: the last IR becomes current (engine-owned copy)
