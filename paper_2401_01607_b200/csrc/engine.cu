@@ -399,9 +399,10 @@ struct sc_engine {
     int64_t *jbuf = nullptr;  // [C][n_blocks] last-scatter index per block
     // FAST fused streams (float32): masked drive [C][fx_ld] and the per-segment
     // convolutions [C][fy_ld] (segment j at column offset fy_off[j])
+    // (flat buffers; the row pitch is chosen per call)
     int mode = SC_MODE_ORDERED;
-    void *fx = nullptr, *fy = nullptr;
-    int64_t fx_ld = 0, fy_ld = 0;
+    void *fx = nullptr, *fy = nullptr, *fh = nullptr;
+    int64_t fx_cap = 0, fy_cap = 0, fh_cap = 0;
     int64_t jbuf_ld = 0;
 };
 
@@ -516,20 +517,47 @@ struct DeviceGuard {
 
 // Fused back-to-back blocks (see sc_engine_process_blocks); x/out are
 // [C][ldx]/[C][ldo] rows of n_total samples.
-// FAST fused streams pay ~6 launches per IR segment (tensor-core set-up), so
-// they are used only when every segment is large: >= 2^30 MACs over the
-// channels (the ordered chain needs >= ~30 us for that much work).
+// Segments of one length L (the last may be shorter) and one IR length NH --
+// periodic swaps, the CLI's and cfg2's pattern -- are convolved in ONE
+// batched FIR launch: batch (channel c, segment j) reads the masked drive at
+// (c*S + j)*L (row pitch S*L, zero padded past the stream), its IR staged at
+// (c*S + j)*NH and writes (c*S + j)*(L + NH - 1).
+bool uniform_segs(const ChainSeg *segs, int nseg, int64_t *L, int64_t *NH) {
+    *L = segs[0].m_hi - segs[0].m_lo;
+    *NH = segs[0].nh;
+    if (nseg < 2) return false;
+    for (int j = 0; j < nseg; ++j) {
+        const int64_t len = segs[j].m_hi - segs[j].m_lo;
+        if (segs[j].nh != *NH || (j < nseg - 1 ? len != *L : len > *L)) return false;
+    }
+    return true;
+}
+
+// FAST fused streams go to the FIR kernels when the work amortises their
+// set-up: a batched launch (uniform segments) from 2^28 MACs in total,
+// otherwise ~6 launches per segment, so every segment needs >= 2^30 MACs
+// over the channels (the ordered chain needs >= ~30 us for that much work).
 bool fast_stream_worth(const sc_engine *e, const ChainSeg *segs, int nseg) {
     if (e->mode != SC_MODE_FAST || e->dtype != SC_F32) return false;
-    for (int j = 0; j < nseg; ++j)
-        if ((double)e->C * (double)(segs[j].m_hi - segs[j].m_lo) * (double)segs[j].nh < 1073741824.0) return false;
-    return true;
+    int64_t L, NH;
+    double total = 0.0;
+    bool each = true;
+    for (int j = 0; j < nseg; ++j) {
+        const double w = (double)e->C * (double)(segs[j].m_hi - segs[j].m_lo) * (double)segs[j].nh;
+        total += w;
+        each = each && w >= 1073741824.0;
+    }
+    if (uniform_segs(segs, nseg, &L, &NH) && (double)e->C * nseg < 65536.0 && total >= 268435456.0) return true;
+    return each;
 }
 
 // Also fills e->jbuf (last scattering index per block) from its mask pass.
 int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64_t nb, int64_t ub,
                 const ChainSeg *segs, int nseg, void *rin, void *rout, void *out, int64_t ldo) {
     const int64_t n_blocks = cdiv(n_total, nb);
+    int64_t L, NH;
+    const bool batched = uniform_segs(segs, nseg, &L, &NH) && e->C * nseg < 65536;
+    const int64_t Lo = L + NH - 1;
     FastSegs sg{};
     sg.n = nseg;
     int64_t tot = 0;
@@ -537,12 +565,14 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
         sg.m_lo[j] = segs[j].m_lo;
         sg.m_hi[j] = segs[j].m_hi;
         sg.nh[j] = segs[j].nh;
-        sg.off[j] = tot;
+        sg.off[j] = batched ? j * Lo : tot;
         tot += segs[j].m_hi - segs[j].m_lo + segs[j].nh - 1;
     }
-    int rc = ensure_2d(&e->fx, &e->fx_ld, n_total, 4, e->C, 0, e->stream);
+    const int64_t xpitch = batched ? nseg * L : n_total;  // per channel
+    const int64_t ypitch = batched ? nseg * Lo : tot;
+    int rc = ensure_2d(&e->fx, &e->fx_cap, e->C * xpitch, 4, 1, 0, e->stream);
     if (rc) return rc;
-    rc = ensure_2d(&e->fy, &e->fy_ld, tot, 4, e->C, 0, e->stream);
+    rc = ensure_2d(&e->fy, &e->fy_cap, e->C * ypitch, 4, 1, 0, e->stream);
     if (rc) return rc;
     float *xm = static_cast<float *>(e->fx), *fy = static_cast<float *>(e->fy);
     {
@@ -551,22 +581,40 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
         float keep = (float)e->thr;
         if ((double)keep <= e->thr) keep = nextafterf(keep, INFINITY);
         const bool vec4 = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(xm)) & 15) == 0 &&
-                          ldx % 4 == 0 && e->fx_ld % 4 == 0 && nb % 4 == 0;
-        k_mask_skip<<<g, 256, 0, e->stream>>>(static_cast<const float *>(x), ldx, n_total, nb, keep, xm, e->fx_ld,
+                          ldx % 4 == 0 && xpitch % 4 == 0 && nb % 4 == 0;
+        k_mask_skip<<<g, 256, 0, e->stream>>>(static_cast<const float *>(x), ldx, n_total, nb, keep, xm, xpitch,
                                               n_blocks, e->jbuf, vec4);
         SC_CHECK_LAUNCH();
+        if (xpitch > n_total)  // zero padding of the last (short) segment
+            SC_CHECK_CUDA(cudaMemset2DAsync(xm + n_total, (size_t)xpitch * 4, 0, (size_t)(xpitch - n_total) * 4,
+                                            (size_t)e->C, e->stream));
     }
-    for (int j = 0; j < nseg; ++j) {
-        // outputs [m_lo, m_hi + nh - 1) of segment j's drive samples, NaN/Inf
-        // handled by launch_fir_f32's device-gated ordered fallback
-        rc = launch_fir_f32(SC_MODE_FAST, xm, e->fx_ld, 0, segs[j].m_lo, segs[j].m_hi,
-                            static_cast<const float *>(segs[j].h), e->stage_ld, segs[j].nh, fy + sg.off[j], e->fy_ld,
-                            segs[j].m_lo, segs[j].m_hi + segs[j].nh - 1, e->C, e->stream);
+    // NaN/Inf in x or h: launch_fir_f32's device-gated ordered fallback
+    if (batched) {
+        rc = ensure_2d(&e->fh, &e->fh_cap, e->C * nseg * NH, 4, 1, 0, e->stream);
         if (rc) return rc;
+        StageCopies cp{};
+        cp.n = nseg;
+        for (int j = 0; j < nseg; ++j)
+            cp.src[j] = segs[j].h, cp.sld[j] = e->stage_ld, cp.off[j] = j * NH, cp.nh[j] = NH;
+        const dim3 gs((unsigned)std::min<int64_t>(cdiv(NH, 256), 64), (unsigned)nseg, (unsigned)e->C);
+        k_stage_irs<float><<<gs, 256, 0, e->stream>>>(cp, static_cast<float *>(e->fh), nseg * NH);
+        SC_CHECK_LAUNCH();
+        rc = launch_fir_f32(SC_MODE_FAST, xm, L, 0, 0, L, static_cast<const float *>(e->fh), NH, NH, fy, Lo, 0, Lo,
+                            e->C * nseg, e->stream);
+        if (rc) return rc;
+    } else {
+        for (int j = 0; j < nseg; ++j) {
+            // outputs [m_lo, m_hi + nh - 1) of segment j's drive samples
+            rc = launch_fir_f32(SC_MODE_FAST, xm, xpitch, 0, segs[j].m_lo, segs[j].m_hi,
+                                static_cast<const float *>(segs[j].h), e->stage_ld, segs[j].nh, fy + sg.off[j],
+                                ypitch, segs[j].m_lo, segs[j].m_hi + segs[j].nh - 1, e->C, e->stream);
+            if (rc) return rc;
+        }
     }
     const int64_t n_slots = n_total + ub;
     const dim3 g((unsigned)std::min<int64_t>(cdiv(n_slots, 1024), 4096), (unsigned)e->C);
-    k_fast_combine<<<g, 256, 0, e->stream>>>(sg, fy, e->fy_ld, static_cast<const float *>(rin), e->res_ld, e->st,
+    k_fast_combine<<<g, 256, 0, e->stream>>>(sg, fy, ypitch, static_cast<const float *>(rin), e->res_ld, e->st,
                                              n_total, n_slots, static_cast<float *>(out), ldo,
                                              static_cast<float *>(rout));
     SC_CHECK_LAUNCH();
@@ -775,6 +823,7 @@ int sc_engine_destroy(sc_engine *e) {
     cudaFree(e->jbuf);
     cudaFree(e->fx);
     cudaFree(e->fy);
+    cudaFree(e->fh);
     delete e;
     return SC_OK;
 }

@@ -86,7 +86,8 @@ class ScatterEngine:
                 t.device("cuda", t.cuda.current_device())
         self._device = t.device(device)
         self._sample_rate = h.sample_rate
-        self._ir_signal = Signal(self._copy_host(h.samples), h.sample_rate)
+        self._ir_like = h.samples[:0]   # currency of returned signals (host / device / pinned)
+        self._nh = len(h)
         self._pending_ir = None
         self._handle = ctypes.c_void_p()
         hd = self._to_dev(h.samples)
@@ -100,11 +101,6 @@ class ScatterEngine:
         self.mode = "fast" if fast else "ordered"
 
     # ------------------------------------------------------------- plumbing
-
-    def _copy_host(self, samples):
-        if _dev.is_tensor(samples):
-            return samples.detach().clone()
-        return np.array(samples, dtype=self._npd, copy=True)
 
     def _to_dev(self, samples):
         return _dev.as_device(samples, self._npd, device=self._device)
@@ -149,7 +145,15 @@ class ScatterEngine:
 
     @property
     def current_ir(self) -> Signal:
-        return self._ir_signal
+        """The impulse response in force (engine.py:91-93): read back from the
+        engine's own device copy, in the currency of the IR last given."""
+        t = _dev.torch()
+        with t.cuda.device(self._device):
+            buf = t.empty(self._nh, dtype=_dev.torch_dtype(self._npd), device=self._device)
+            n = ctypes.c_int64()
+            self._bind_stream()
+            N.check(self._lib.sc_engine_current_ir(self._handle, N.ptr(buf), self._nh, ctypes.byref(n)))
+        return Signal(_dev.like_input(buf[:n.value], self._ir_like), self._sample_rate)
 
     @property
     def samples_consumed(self) -> int:
@@ -212,7 +216,7 @@ class ScatterEngine:
             n = ctypes.c_int64()
             N.check(self._lib.sc_engine_flush(self._handle, N.ptr(tail), cap.value, ctypes.byref(n)))
             tail = tail[:n.value]
-        like = self._ir_signal.samples
+        like = self._ir_like
         return Signal(_dev.like_input(tail, like), self._sample_rate)
 
     def swap_ir(self, h_new: Signal):
@@ -230,7 +234,8 @@ class ScatterEngine:
             hd = self._to_dev(h_new.samples)
             self._bind_stream()
             N.check(self._lib.sc_engine_swap_ir(self._handle, N.ptr(hd), len(h_new)))
-        self._ir_signal = Signal(self._copy_host(h_new.samples), h_new.sample_rate)
+        self._ir_like = h_new.samples[:0]
+        self._nh = len(h_new)
 
     def swap_ir_at_next_block(self, h_new: Signal):
         """Defer the swap to the start of the next process_block call (engine.py:188-192)."""
@@ -304,8 +309,9 @@ class ScatterEngine:
                                                        blocks, ptrs, nhs, n, N.ptr(out)))
             if swaps:
                 last = swaps[-1][1]
-                self._ir_signal = Signal(self._copy_host(last.samples if isinstance(last, Signal) else last),
-                                         self._sample_rate)
+                last = last.samples if isinstance(last, Signal) else last
+                self._ir_like = last[:0]
+                self._nh = len(last)
         return _dev.like_input(out, xs)
 
     def state_dict(self) -> dict:

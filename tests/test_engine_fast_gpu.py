@@ -130,3 +130,51 @@ def test_small_segments_stay_ordered_and_mode_validation():
         ScatterEngine(Signal(np.ones(4)), mode="fast")
     with pytest.raises(ValueError, match="mode must be"):
         ScatterEngine(Signal(h), mode="tc")
+
+
+@pytest.mark.parametrize("channels", [1, 3])
+def test_periodic_swaps_batched_path(channels):
+    """cfg2's pattern: equal segments (the last one shorter), one IR length --
+    all segments in one batched tensor-core launch; vs the oracle engine."""
+    import torch
+
+    from paper_2401_01607_b200.engine import EngineConfig
+    from paper_2401_01607_b200.multichannel import MultiChannelEngine
+
+    rng = np.random.default_rng(15 + channels)
+    n, nh, nb, every = 150_000 + 77, 4096, 256, 100          # 6 segments of 25,600, last 22,077
+    x = rng.uniform(-1, 1, (channels, n)).astype(np.float32)
+    n_blocks = -(-n // nb)
+    irs = [(rng.standard_normal((channels, nh)) * np.exp(-np.arange(nh) / 800)).astype(np.float32)
+           for _ in range(-(-n_blocks // every))]
+    eng = MultiChannelEngine(torch.from_numpy(irs[0]).cuda(), EngineConfig(block_size_nb=nb, zero_skip_threshold=0.01))
+    swaps = [(b, torch.from_numpy(irs[b // every]).cuda()) for b in range(every, n_blocks, every)]
+    body = eng.process_stream(torch.from_numpy(x).cuda(), nb, swaps).cpu().numpy()
+    tails = eng.flush()
+    for c in range(channels):
+        ref_body, ref_tail = _oracle_stream(x[c], {b: irs[b // every][c] for b in range(0, n_blocks, every)}, nb, 0.01)
+        tol = max(_tol(x[c], ir[c]) for ir in irs)
+        assert np.max(np.abs(body[c] - ref_body)) <= tol, c
+        assert len(tails[c]) == len(ref_tail)
+        assert np.max(np.abs(tails[c] - ref_tail)) <= tol, c
+
+
+def test_unequal_segments_per_segment_path():
+    """Large segments of different IR lengths: one FIR launch per segment."""
+    import torch
+
+    from paper_2401_01607_b200.core import Signal
+    from paper_2401_01607_b200.engine import EngineConfig, ScatterEngine
+
+    rng = np.random.default_rng(21)
+    n, nb = 1 << 20, 8192
+    x = rng.uniform(-1, 1, n).astype(np.float32)
+    h0 = rng.standard_normal(4096).astype(np.float32) * 0.1
+    h1 = rng.standard_normal(6000).astype(np.float32) * 0.1
+    eng = ScatterEngine(Signal(torch.from_numpy(h0).cuda()), EngineConfig(block_size_nb=nb))
+    body = eng.process_stream(torch.from_numpy(x).cuda(), nb, [(40, torch.from_numpy(h1).cuda())]).cpu().numpy()
+    tail = eng.flush().samples.cpu().numpy()
+    ref_body, ref_tail = _oracle_stream(x, {0: h0, 40: h1}, nb)
+    tol = max(_tol(x, h0), _tol(x, h1))
+    assert np.max(np.abs(body - ref_body)) <= tol
+    assert len(tail) == len(ref_tail) and np.max(np.abs(tail - ref_tail)) <= tol

@@ -51,3 +51,16 @@ for it in range(6):
     print(f"iter {it}: enqueue process_stream {1e3*(t1-t0):.3f} ms, flush {1e3*(t2-t1):.3f} ms, "
           f"device stream {e0.elapsed_time(e1):.3f} ms, device total {e0.elapsed_time(e2):.3f} ms, "
           f"wall {1e3*(t3-t0):.3f} ms")
+
+if len(sys.argv) > 2 and sys.argv[2] == "cprofile":
+    import cProfile
+    import pstats
+
+    pr = cProfile.Profile()
+    pr.enable()
+    for _ in range(50):
+        eng.process_stream(xd, nb, swaps)
+        eng.flush()
+    torch.cuda.synchronize()
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(14)
