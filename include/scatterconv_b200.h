@@ -145,8 +145,9 @@ int sc_engine_set_stream(sc_engine *e, void *stream);
  * only): when every IR segment of a call carries >= 2^30 MACs over the
  * channels, each segment's convolution runs on the FAST FIR path (tensor
  * cores from 256 taps) and a combine kernel adds the segments and the
- * residue -- results within the FP32 tolerance, not bit-identical.  Single
- * blocks and samples stay on the ordered chain. */
+ * residue -- results within the FP32 tolerance, not bit-identical.  A single
+ * block (sc_engine_process_block) with >= 2^30 MACs takes the same path;
+ * smaller blocks and samples stay on the ordered chain. */
 int sc_engine_set_mode(sc_engine *e, int mode);
 
 /* process_block (engine.py:118-146): applies a pending swap first, then

@@ -846,6 +846,13 @@ int sc_engine_process_block(sc_engine *e, const void *block, int64_t n, void *ou
     SC_REQUIRE(e, "null engine");
     SC_REQUIRE(n >= 0 && (n == 0 || (block && out)), "sc_engine_process_block: bad block");
     DeviceGuard g(e->device);
+    // FAST mode: a block big enough for the tensor-core FIR (>= 2^30 MACs over
+    // the channels, with the IR that will be in force) goes through the fused
+    // path as a one-block stream (same state updates, pending swap included)
+    const int64_t nh_next = e->has_pending ? e->pend_nh : e->nh;
+    if (n > 0 && n <= e->nb && e->mode == SC_MODE_FAST && e->dtype == SC_F32 &&
+        (double)e->C * (double)n * (double)nh_next >= 1073741824.0)
+        return process_blocks_impl(e, block, n, n, n, nullptr, nullptr, nullptr, nullptr, 0, out, n);
     return do_block(e, block, n, n, out, n, true);
 }
 

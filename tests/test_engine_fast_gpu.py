@@ -178,3 +178,31 @@ def test_unequal_segments_per_segment_path():
     tol = max(_tol(x, h0), _tol(x, h1))
     assert np.max(np.abs(body - ref_body)) <= tol
     assert len(tail) == len(ref_tail) and np.max(np.abs(tail - ref_tail)) <= tol
+
+
+def test_fast_process_block_large_blocks_with_pending_swap():
+    """FAST mode routes a single block with >= 2^30 MACs through the fused
+    tensor-core path (pending swap applied first, as in engine.py:124-126)."""
+    import torch
+
+    from paper_2401_01607_b200.engine import EngineConfig
+    from paper_2401_01607_b200.multichannel import MultiChannelEngine
+
+    rng = np.random.default_rng(31)
+    C, nb, nh = 8, 8192, 16384
+    x = rng.uniform(-1, 1, (C, 5 * nb - 100)).astype(np.float32)
+    h0 = (rng.standard_normal((C, nh)) * np.exp(-np.arange(nh) / 3000)).astype(np.float32)
+    h1 = (rng.standard_normal((C, nh)) * np.exp(-np.arange(nh) / 2000)).astype(np.float32)
+    eng = MultiChannelEngine(torch.from_numpy(h0).cuda(), EngineConfig(block_size_nb=nb))
+    outs = []
+    for b, s in enumerate(range(0, x.shape[1], nb)):
+        if b == 3:
+            eng.swap_ir_at_next_block(torch.from_numpy(h1).cuda())
+        outs.append(eng.process_block(torch.from_numpy(x[:, s:s + nb]).cuda()).cpu().numpy())
+    body = np.concatenate(outs, axis=1)
+    tails = eng.flush()
+    for c in range(C):
+        ref_body, ref_tail = _oracle_stream(x[c], {0: h0[c], 3: h1[c]}, nb)
+        tol = max(_tol(x[c], h0[c]), _tol(x[c], h1[c]))
+        assert np.max(np.abs(body[c] - ref_body)) <= tol, c
+        assert len(tails[c]) == len(ref_tail) and np.max(np.abs(tails[c] - ref_tail)) <= tol, c
