@@ -247,7 +247,8 @@ class Work:
             from paper_2401_01607_b200.core import Signal
             from paper_2401_01607_b200.engine import EngineConfig, ScatterEngine
 
-            self.eng = ScatterEngine(Signal(self.h0), EngineConfig(block_size_nb=256))
+            self._make_engine = lambda mode: ScatterEngine(Signal(self.h0), EngineConfig(block_size_nb=256),
+                                                           mode=mode)
             self.parallelism = f"replicas x{world} (streaming is sequential per stream)"
             self.scaling = "weak"
             self.dtype = "f32"
@@ -263,6 +264,18 @@ class Work:
             nh = self.w.nh
             self.kernel = "k_tc_fir" if nh >= 256 else ("k_fir_short" if nh <= 32 else "k_fir_short_smem")
             self.hbm_bound = nh <= 32
+            return
+        if self.cfg == "cfg2":
+            # float32 engine: FAST mode convolves the 19 equal IR segments in one
+            # batched tensor-core launch; --mode ordered keeps the ordered chain
+            fast = self.mode != "ordered"
+            self.eng = self._make_engine("fast" if fast else "ordered")
+            self.kernel = "k_tc_fir" if fast else "k_chain_w"
+            if fast:
+                nh, seg = self.w.nh, 100 * 256
+                s8 = -(-((nh + 126) // 128 + 1) // 8) * 8
+                nseg = -(-self.w.ne // seg)
+                self.tc_padded_macs = nseg * (-(-(seg + nh - 1) // 16384)) * 16384 * 128 * s8
             return
         if self.cfg == "mstream":
             # float32 engine: FAST mode puts each IR segment (2 x 64 ch x 240,000

@@ -79,7 +79,7 @@ __host__ __device__ constexpr int cw_pos(int i) {
 }
 
 template <typename T, int SKIP, int R>
-__global__ void __launch_bounds__(CW_TB, 4) k_chain_w(ChainArgs<T> a) {
+__global__ void __launch_bounds__(CW_TB, sizeof(T) == 4 ? 6 : 4) k_chain_w(ChainArgs<T> a) {
     constexpr int TILE = CW_TB * R;
     constexpr int HS = TILE + CW_MC - 1;  // taps per stage
     constexpr int HSP = cw_pos<R>(HS - 1) + 1;
