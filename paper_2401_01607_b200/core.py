@@ -21,6 +21,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from . import _dev
@@ -113,7 +115,8 @@ def mode_code(mode) -> int:
 
 
 _PIPELINE_MIN_MACS = 1 << 36   # host-resident inputs this large are streamed in chunks
-_PIPELINE_CHUNKS = 8
+_PIPELINE_CHUNK_MACS = 1 << 36   # each pipelined chunk carries at least this much work...
+_PIPELINE_MAX_CHUNKS = 12        # ...up to 12 chunks (cfg3: 4 chunks, cfg5: 12; measured best)
 _PIPE_STREAMS: dict = {}
 
 
@@ -141,9 +144,11 @@ def _fir_host_pipelined(x_pin, kern, mode):
     s_in, s_cmp, s_out = _PIPE_STREAMS[dev.index]
     for s in (s_in, s_cmp, s_out):
         s.wait_stream(main)   # h upload / allocations are ordered on main
-    per = -(-nout // _PIPELINE_CHUNKS)
+    chunks = int(os.environ.get("SC_PIPE_CHUNKS", "0")) or \
+        max(2, min(_PIPELINE_MAX_CHUNKS, (nout * nh) // _PIPELINE_CHUNK_MACS))
+    per = -(-nout // chunks)
     uploaded = 0
-    for c in range(_PIPELINE_CHUNKS):
+    for c in range(chunks):
         a, b = c * per, min(nout, (c + 1) * per)
         if a >= b:
             break

@@ -119,7 +119,7 @@ def test_pinned_host_pipeline(monkeypatch, mode):
     from paper_2401_01607_b200 import core
 
     monkeypatch.setattr(core, "_PIPELINE_MIN_MACS", 0)
-    monkeypatch.setattr(core, "_PIPELINE_CHUNKS", 5)
+    monkeypatch.setattr(core, "_PIPELINE_CHUNK_MACS", 70_001 * 3_333 // 5)   # 5 chunks
     rng = np.random.default_rng(44)
     x = rng.uniform(-1, 1, 70_001).astype(np.float32)
     h = rng.standard_normal(3_333).astype(np.float32)
