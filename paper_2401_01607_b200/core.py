@@ -120,6 +120,16 @@ _PIPELINE_MAX_CHUNKS = 12        # ...up to 12 chunks (cfg3: 4 chunks, cfg5: 12;
 _PIPE_STREAMS: dict = {}
 
 
+def pipe_streams(dev):
+    """(upload, compute, download) streams of a device, created once: the
+    library's scratch buffers are keyed by stream, so fresh streams would
+    re-allocate every call."""
+    t = _dev.torch()
+    if dev.index not in _PIPE_STREAMS:
+        _PIPE_STREAMS[dev.index] = tuple(t.cuda.Stream(dev) for _ in range(3))
+    return _PIPE_STREAMS[dev.index]
+
+
 def _fir_host_pipelined(x_pin, kern, mode):
     """Pinned-host float32 input: overlap the H2D upload, the FIR and the D2H
     download chunk by chunk (one stream each, event-chained).  Chunk c owns
@@ -137,11 +147,7 @@ def _fir_host_pipelined(x_pin, kern, mode):
     xd = t.empty(ne, dtype=t.float32, device=dev)
     yd = t.empty(nout, dtype=t.float32, device=dev)
     main = t.cuda.current_stream(dev)
-    # persistent per-device streams: the library's scratch buffers are keyed
-    # by stream, so fresh streams would re-allocate every call
-    if dev.index not in _PIPE_STREAMS:
-        _PIPE_STREAMS[dev.index] = tuple(t.cuda.Stream(dev) for _ in range(3))
-    s_in, s_cmp, s_out = _PIPE_STREAMS[dev.index]
+    s_in, s_cmp, s_out = pipe_streams(dev)
     for s in (s_in, s_cmp, s_out):
         s.wait_stream(main)   # h upload / allocations are ordered on main
     chunks = int(os.environ.get("SC_PIPE_CHUNKS", "0")) or \

@@ -20,7 +20,9 @@ def convolve_batched(x, h, mode=None):
 
     x: [C, Ne] float32 (ndarray or tensor), h: [C, Nh] float32 (or [Nh],
     broadcast to every channel like the CLI's mono IR, cli.py:147-155).
-    Returns [C, Ne+Nh-1] float32 in the caller's currency.
+    Returns [C, Ne+Nh-1] float32 in the caller's currency.  A large pinned
+    host input streams channel groups through upload / FIR / download on
+    three overlapping streams (pinned host output).
     """
     t = _dev.torch()
     if x.ndim != 2:
@@ -28,8 +30,10 @@ def convolve_batched(x, h, mode=None):
     C, ne = int(x.shape[0]), int(x.shape[1])
     if ne == 0:
         raise ValueError("input signal is empty")
-    xd = _dev.as_device(x, np.float32)
-    hd = _dev.as_device(h, np.float32, device=xd.device)
+    pinned_in = _dev.is_tensor(x) and x.device.type == "cpu" and x.is_pinned()
+    dev = t.device("cuda", t.cuda.current_device())
+    xd = None if pinned_in else _dev.as_device(x, np.float32)
+    hd = _dev.as_device(h, np.float32, device=xd.device if xd is not None else dev)
     if hd.ndim == 1:
         hd = hd.unsqueeze(0).expand(C, -1).contiguous()
     if hd.shape[0] != C:
@@ -40,12 +44,58 @@ def convolve_batched(x, h, mode=None):
     from .core import mode_code
 
     L = N.lib()
+    if (_dev.is_tensor(x) and x.device.type == "cpu" and x.is_pinned() and x.dtype == t.float32
+            and x.is_contiguous() and mode_code(mode) != N.SC_MODE_ORDERED and C >= 2
+            and C * ne * nh >= _PIPELINE_MIN_MACS):
+        return _batched_host_pipelined(x, hd, mode_code(mode))
+    if xd is None:
+        xd = _dev.as_device(x, np.float32, device=hd.device)
     with t.cuda.device(xd.device):
         y = t.empty((C, ne + nh - 1), dtype=t.float32, device=xd.device)
         N.check(L.sc_fir_batched(N.SC_F32, mode_code(mode), N.ptr(xd), ne, N.ptr(hd), nh, N.ptr(y),
                                  ne + nh - 1, C,
                                  ne, nh, N.stream_ptr()))
     return _dev.like_input(y, x, h)
+
+
+_PIPELINE_MIN_MACS = 1 << 34   # pinned-host batches this large overlap H2D / FIR / D2H
+
+
+def _batched_host_pipelined(x_pin, hd, mode):
+    """Pinned-host [C, Ne] input: channel groups flow through upload, FIR and
+    download on three streams (event-chained), so the PCIe/C2C transfers of
+    one group overlap the tensor-core work of another.  Returns a pinned host
+    [C, Ne+Nh-1] tensor."""
+    from .core import pipe_streams
+
+    t = _dev.torch()
+    L = N.lib()
+    dev = hd.device
+    C, ne = int(x_pin.shape[0]), int(x_pin.shape[1])
+    nh = int(hd.shape[1])
+    nout = ne + nh - 1
+    out = t.empty((C, nout), dtype=t.float32, pin_memory=True)
+    with t.cuda.device(dev):
+        xd = t.empty((C, ne), dtype=t.float32, device=dev)
+        yd = t.empty((C, nout), dtype=t.float32, device=dev)
+        main = t.cuda.current_stream(dev)
+        s_in, s_cmp, s_out = pipe_streams(dev)
+        for s in (s_in, s_cmp, s_out):
+            s.wait_stream(main)
+        groups = max(2, min(C, 8, (C * ne * nh) >> 35))
+        per = -(-C // groups)
+        for c0 in range(0, C, per):
+            c1 = min(C, c0 + per)
+            with t.cuda.stream(s_in):
+                xd[c0:c1].copy_(x_pin[c0:c1], non_blocking=True)
+            s_cmp.wait_stream(s_in)
+            N.check(L.sc_fir_batched(N.SC_F32, mode, N.ptr(xd[c0]), ne, N.ptr(hd[c0]), nh, N.ptr(yd[c0]), nout,
+                                     c1 - c0, ne, nh, N.stream_ptr(s_cmp)))
+            s_out.wait_stream(s_cmp)
+            with t.cuda.stream(s_out):
+                out[c0:c1].copy_(yd[c0:c1], non_blocking=True)
+        s_out.synchronize()
+    return out
 
 
 class MultiChannelEngine:

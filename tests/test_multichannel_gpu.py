@@ -102,3 +102,22 @@ def test_mono_ir_broadcast_and_errors():
         eng.process_block(np.zeros((3, 5)))
     with pytest.raises(ValueError, match="empty"):
         eng.swap_ir(np.zeros((2, 0)))
+
+
+def test_batched_pinned_host_pipeline(monkeypatch):
+    """Pinned host [C, Ne] -> channel groups overlapped over three streams."""
+    import torch
+
+    from oracle import oracle as O
+    from paper_2401_01607_b200 import multichannel
+
+    monkeypatch.setattr(multichannel, "_PIPELINE_MIN_MACS", 0)
+    rng = np.random.default_rng(77)
+    X = rng.uniform(-1, 1, (11, 20_011)).astype(np.float32)
+    H = rng.standard_normal((11, 1_500)).astype(np.float32)
+    y = multichannel.convolve_batched(torch.from_numpy(X).pin_memory(), torch.from_numpy(H))
+    assert y.is_pinned() and tuple(y.shape) == (11, 20_011 + 1_499)
+    for c in range(11):
+        ref = O.scatter_full(X[c], H[c])
+        tol = 1e-5 * np.max(np.abs(X[c])) * np.sum(np.abs(H[c]))
+        assert np.max(np.abs(y[c].numpy().astype(np.float64) - ref)) <= tol
