@@ -52,8 +52,9 @@ def parse():
     ap.add_argument("--config", default="cfg5",
                     choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "short8", "short16", "short32",
                              "short64", "short128", "mstream"])
-    ap.add_argument("--mode", default="fast", choices=["fast", "ffma", "tc", "ordered"],
-                    help="float32 kernel: fast = picked by shape (tensor cores for long filters); "
+    ap.add_argument("--mode", default="auto", choices=["auto", "fast", "ffma", "tc", "ordered"],
+                    help="auto = the library default (float32: fast, tensor cores for long filters; "
+                         "float64: ordered, bit-exact); fast on a float64 config = fused-FMA chain; "
                          "ordered = the sequential-chain kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -296,7 +297,7 @@ class Work:
             self.kernel = "k_chain_w"   # ordered chain (csrc/k_ordered.cu)
             return
         nh = self.w.nh
-        use_tc = self.mode == "tc" or (self.mode == "fast" and nh >= 256)
+        use_tc = self.mode == "tc" or (self.mode in ("fast", "auto") and nh >= 256)
         self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 32 else
                                                  "k_fir_short_smem" if nh <= 256 else "k_fir_f32_fast")
         if use_tc:
@@ -317,12 +318,13 @@ class Work:
         from paper_2401_01607_b200.sharded import convolve_shard
 
         if self.cfg in ("cfg5", "cfg3"):
-            return convolve_shard(self.xs, self.shard, self.hd, mode=self.mode)
+            return convolve_shard(self.xs, self.shard, self.hd, mode=self.lib_mode)
         if self.cfg == "cfg4":
-            return convolve_batched(self.xd, self.hd, mode=self.mode)
+            return convolve_batched(self.xd, self.hd, mode=self.lib_mode)
         if self.cfg == "cfg1":
-            # the full Ne+Nh-1 result (ConvOutput body/tail are views of it)
-            return scatter_convolve(Signal(self.xd), Signal(self.hd)).body.samples
+            # the full Ne+Nh-1 result (ConvOutput body/tail are views of it);
+            # auto = ordered (bit-exact), --mode fast = fused-FMA chain
+            return scatter_convolve(Signal(self.xd), Signal(self.hd), mode=self.lib_mode).body.samples
         if self.cfg == "cfg2":
             # 1,875 blocks of 256 with 18 IR swaps, then the flush of the tail
             # (engine.py:148-161) -- the whole stream, no host round-trip until
@@ -331,7 +333,7 @@ class Work:
             self.eng.flush()
             return body
         if self.cfg.startswith("short"):
-            return scatter_convolve(Signal(self.xd), Signal(self.hd), mode=self.mode).body.samples
+            return scatter_convolve(Signal(self.xd), Signal(self.hd), mode=self.lib_mode).body.samples
         if self.cfg == "mstream":
             body = self.eng.process_stream(self.xd, 8192, self.swaps)
             tails, _ = self.eng.flush(on_device=True)   # [64, 16383] tails stay in HBM like the body
@@ -473,6 +475,7 @@ def main():
     L = N.lib()
     work = Work(args.config, rank, world, device)
     work.mode = args.mode
+    work.lib_mode = None if args.mode == "auto" else args.mode
     work.pick_kernel()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)  # 256 MiB > L2
 
@@ -556,13 +559,14 @@ def main():
         # FP64 pipe issues 64 lane-ops/clk/SM (tools/ubench/fp64_latency.cu
         # measured 62.2 for DADD at 32 warps/SM)
         dp_peak = 64 * sms * sm_max * 1e6 / 1e12  # T lane-ops/s
-        dp_ops = 2 * work.rank_macs / (ms_local * 1e-3) / 1e12
+        ops_per_mac = 1 if args.mode == "fast" else 2   # DFMA vs DMUL + DADD
+        dp_ops = ops_per_mac * work.rank_macs / (ms_local * 1e-3) / 1e12
         roofline = {
             "bound": "fp64_pipe", "achieved": dp_ops, "peak": dp_peak, "unit": "Tops/s (FP64 pipe lane-ops)",
             "frac": dp_ops / dp_peak, "traffic": traffic,
             "peak_source": f"computed: {sms} SMs x 64 FP64 lane-ops/clk x sm_max_mhz {sm_max:.0f}; "
                            "microbenchmark tools/ubench/fp64_latency.cu: 62.2 lane-ops/clk/SM",
-            "achieved_per_launch": "2 x metric MACs (DMUL + DADD) / mean step time",
+            "achieved_per_launch": f"{ops_per_mac} x metric MACs ({'DFMA' if ops_per_mac == 1 else 'DMUL + DADD'}) / mean step time",
             "frac_at_observed_clock": dp_ops / (64 * sms * med * 1e6 / 1e12),
             "kernel": work.kernel,
         }

@@ -30,9 +30,13 @@
  *    separately (no FMA), bit-identical to the reference.  float32: one fused
  *    multiply-add per step.  In both dtypes stream == batch for any block
  *    partition.
- *  - SC_MODE_FAST (float32 only): the fastest kernel for the shape --
- *    SC_MODE_TC for long filters, SC_MODE_FFMA otherwise.  Fixed
- *    (deterministic) order, within 1e-5*max|x|*||h||_1 of the reference.
+ *  - SC_MODE_FAST: float32 -- the fastest kernel for the shape, SC_MODE_TC
+ *    for long filters, SC_MODE_FFMA otherwise; fixed (deterministic) order,
+ *    within 1e-5*max|x|*||h||_1 of the reference.  float64 (any non-ORDERED
+ *    mode) -- the ordered chain with one fused multiply-add per step: same
+ *    order, one rounding fewer per MAC, twice the FP64 throughput, within
+ *    1e-12*max|x|*||h||_1 (north_star's FP64 bar); stream == batch still
+ *    holds within the mode.
  *  - SC_MODE_FFMA: register-tiled CUDA-core kernel (FFMA2 = fma.rn.f32x2).
  *  - SC_MODE_TC: tcgen05 tensor-core block-Toeplitz GEMM with an fp16 hi/lo
  *    split of x and h (3 MMAs per K-step, FP32 accumulation in TMEM); requires
@@ -140,9 +144,12 @@ int sc_engine_channels(sc_engine *e, int64_t *channels);
 int sc_engine_destroy(sc_engine *e);
 int sc_engine_set_stream(sc_engine *e, void *stream);
 
-/* Kernel family for fused streams (sc_engine_process_blocks): SC_MODE_ORDERED
- * (default; bit-identical to block-by-block calls) or SC_MODE_FAST (float32
- * only): when every IR segment of a call carries >= 2^30 MACs over the
+/* Kernel family: SC_MODE_ORDERED (default; bit-identical to block-by-block
+ * calls and, in float64, to the reference) or SC_MODE_FAST.  float64 FAST:
+ * every launch uses the fused-multiply-add chain (see SC_MODE_FAST above).
+ * float32 FAST, fused streams (sc_engine_process_blocks): when the IR
+ * segments of a call carry enough work (one batched launch for equal
+ * segments from 2^28 MACs; otherwise >= 2^30 MACs per segment) over the
  * channels, each segment's convolution runs on the FAST FIR path (tensor
  * cores from 256 taps) and a combine kernel adds the segments and the
  * residue -- results within the FP32 tolerance, not bit-identical.  A single

@@ -139,9 +139,10 @@ int sc_fir_full(int dtype, int mode, const void *x, int64_t ne, const void *h, i
                               static_cast<const float *>(h), 0, nh, static_cast<float *>(y), 0, 0, nout,
                               1, st);
     }
+    // float64 outside ORDERED mode: the same chain with fused multiply-adds
     ChainSeg seg{h, nh, 0, ne};
     return launch_chain(dtype, skip_mode, threshold, x, 0, &seg, 1, nullptr, 0, nullptr, 0, nout,
-                        y, nout, nullptr, st);
+                        y, nout, nullptr, st, nullptr, nullptr, dtype == SC_F64 && mode != SC_MODE_ORDERED);
 }
 
 int sc_fir_range(int dtype, int mode, const void *x, int64_t x_begin, int64_t x_end, const void *h,

@@ -472,6 +472,9 @@ int do_swap(sc_engine *e, const void *h, int64_t h_ld, int64_t nh) {
 }
 
 // One block of n samples per channel: block/out are [C][ld].
+// float64 engines in FAST mode run the ordered chain with fused multiply-adds
+bool fused_chain(const sc_engine *e) { return e->dtype == SC_F64 && e->mode == SC_MODE_FAST; }
+
 int do_block(sc_engine *e, const void *block, int64_t ldx, int64_t n, void *out, int64_t ldo, bool apply_pending) {
     if (apply_pending && e->has_pending) {
         e->has_pending = false;
@@ -485,7 +488,7 @@ int do_block(sc_engine *e, const void *block, int64_t ldx, int64_t n, void *out,
     ChainBatch batch{e->C, ldx, e->ir_ld, ldo, e->res_ld, e->res_ld, ST_N};
     void *rin = e->res[e->cur], *rout = e->res[1 - e->cur];
     int rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, block, 0, &seg, 1, rin, 0, e->st + ST_CAP, 0,
-                          n + e->cap_ub, out, n, rout, e->stream, nullptr, &batch);
+                          n + e->cap_ub, out, n, rout, e->stream, nullptr, &batch, fused_chain(e));
     if (rc) return rc;
     rc = launch_epilogue(e->dtype, block, ldx, n, e->thr, e->nh, e->st, e->C, e->stream);
     if (rc) return rc;
@@ -724,7 +727,7 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
     } else {
         ChainBatch batch{e->C, ldx, e->stage_ld, ldo, e->res_ld, e->res_ld, ST_N};
         rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, x, 0, segs, nseg, rin, 0, e->st + ST_CAP, 0,
-                          n_total + ub, out, n_total, rout, e->stream, nullptr, &batch);
+                          n_total + ub, out, n_total, rout, e->stream, nullptr, &batch, fused_chain(e));
         if (rc) return rc;
         const dim3 gj((unsigned)n_blocks, (unsigned)e->C);
         if (e->dtype == SC_F64)
@@ -831,7 +834,6 @@ int sc_engine_destroy(sc_engine *e) {
 int sc_engine_set_mode(sc_engine *e, int mode) {
     SC_REQUIRE(e, "null engine");
     SC_REQUIRE(mode == SC_MODE_ORDERED || mode == SC_MODE_FAST, "engine mode must be ORDERED or FAST, got %d", mode);
-    SC_REQUIRE(mode == SC_MODE_ORDERED || e->dtype == SC_F32, "FAST engine mode needs float32");
     e->mode = mode;
     return SC_OK;
 }

@@ -11,11 +11,12 @@
 // results equal batch results for every block partition (the residue carry
 // continues the same chain).
 //
-// Gather form on the device: output-stationary, one thread per output slot,
-// drive samples and taps staged through shared memory per 256-sample chunk.
-// The drive chunk is a shared-memory broadcast; taps are read at consecutive
-// addresses by consecutive threads (conflict-free).  Zero-skip predicates are
-// warp-uniform (all threads of a chunk visit the same m).
+// Gather form on the device: output-stationary, each thread owns R
+// consecutive output slots (k_chain_w below); drive samples and taps are
+// staged through shared memory per 128-sample chunk, the drive as a
+// broadcast, the taps through a per-thread register window.  Zero-skip tests
+// run once per staged sample (a warp-ballot scatter mask).  The direct-form
+// oracle restatement (k_direct_dd) closes the file.
 
 #include <algorithm>
 
@@ -78,7 +79,7 @@ __host__ __device__ constexpr int cw_pos(int i) {
     return R == 1 ? i : i + i / R;
 }
 
-template <typename T, int SKIP, int R>
+template <typename T, int SKIP, int R, bool FUSED>
 __global__ void __launch_bounds__(CW_TB, sizeof(T) == 4 ? 6 : 4) k_chain_w(ChainArgs<T> a) {
     constexpr int TILE = CW_TB * R;
     constexpr int HS = TILE + CW_MC - 1;  // taps per stage
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(CW_TB, sizeof(T) == 4 ? 6 : 4) k_chain_w(Chain
 #pragma unroll
                     for (int u = 0; u < CW_U; ++u)
 #pragma unroll
-                        for (int r = 0; r < R; ++r) acc[r] = mac_rn(acc[r], xv[u], w[r - u + CW_U - 1]);
+                        for (int r = 0; r < R; ++r) acc[r] = mac_step<FUSED>(acc[r], xv[u], w[r - u + CW_U - 1]);
                 }
             } else {
                 // t - m = rel + r - im.  Only u-blocks with at least one valid
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(CW_TB, sizeof(T) == 4 ? 6 : 4) k_chain_w(Chain
                         for (int u = 0; u < CW_U; ++u) {
                             const T xv = xsb[im0 + u];
 #pragma unroll
-                            for (int r = 0; r < R; ++r) acc[r] = mac_rn(acc[r], xv, w[r - u + CW_U - 1]);
+                            for (int r = 0; r < R; ++r) acc[r] = mac_step<FUSED>(acc[r], xv, w[r - u + CW_U - 1]);
                         }
                     } else {
 #pragma unroll
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(CW_TB, sizeof(T) == 4 ? 6 : 4) k_chain_w(Chain
 #pragma unroll
                             for (int r = 0; r < R; ++r)  // 0 <= t - m < nh
                                 if ((unsigned)(e + r - u) < (unsigned)nh32)
-                                    acc[r] = mac_rn(acc[r], xv, w[r - u + CW_U - 1]);
+                                    acc[r] = mac_step<FUSED>(acc[r], xv, w[r - u + CW_U - 1]);
                         }
                     }
                 }
@@ -266,15 +267,22 @@ __global__ void __launch_bounds__(CW_TB, sizeof(T) == 4 ? 6 : 4) k_chain_w(Chain
     }
 }
 
-template <typename T, int SKIP>
-int launch_chain_r(int R, dim3 grid, cudaStream_t stream, const ChainArgs<T> &a) {
+template <typename T, int SKIP, bool FUSED>
+int launch_chain_rf(int R, dim3 grid, cudaStream_t stream, const ChainArgs<T> &a) {
     switch (R) {
-        case 8: k_chain_w<T, SKIP, 8><<<grid, CW_TB, 0, stream>>>(a); break;
-        case 4: k_chain_w<T, SKIP, 4><<<grid, CW_TB, 0, stream>>>(a); break;
-        case 2: k_chain_w<T, SKIP, 2><<<grid, CW_TB, 0, stream>>>(a); break;
-        default: k_chain_w<T, SKIP, 1><<<grid, CW_TB, 0, stream>>>(a); break;
+        case 8: k_chain_w<T, SKIP, 8, FUSED><<<grid, CW_TB, 0, stream>>>(a); break;
+        case 4: k_chain_w<T, SKIP, 4, FUSED><<<grid, CW_TB, 0, stream>>>(a); break;
+        case 2: k_chain_w<T, SKIP, 2, FUSED><<<grid, CW_TB, 0, stream>>>(a); break;
+        default: k_chain_w<T, SKIP, 1, FUSED><<<grid, CW_TB, 0, stream>>>(a); break;
     }
     return SC_OK;
+}
+
+// float chains are always fused (one instantiation); double picks per call
+template <typename T, int SKIP>
+int launch_chain_r(int R, dim3 grid, cudaStream_t stream, const ChainArgs<T> &a, bool fused) {
+    if (sizeof(T) == 8 && fused) return launch_chain_rf<T, SKIP, true>(R, grid, stream, a);
+    return launch_chain_rf<T, SKIP, false>(R, grid, stream, a);
 }
 
 // Outputs per thread: the largest R that still gives every SM about 16 warps
@@ -298,7 +306,7 @@ int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off
                    const ChainSeg *segs, int nseg, const void *init, int64_t init_len,
                    const int64_t *init_len_dev, int64_t t0, int64_t n_out, void *out_a,
                    int64_t n_a, void *out_b, cudaStream_t stream, const unsigned *run_if,
-                   const ChainBatch *batch) {
+                   const ChainBatch *batch, bool fused) {
     if (n_out <= 0) return SC_OK;
     SC_REQUIRE(nseg >= 0 && nseg <= kMaxSegs, "chain: bad segment count %d", nseg);
     ChainArgs<T> a{};
@@ -334,9 +342,9 @@ int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off
                                : (int64_t)INT32_MAX - 1;
     const dim3 grid((unsigned)std::min<int64_t>(cdiv(n_out, (int64_t)CW_TB * R), cap), (unsigned)channels);
     switch (skip_mode) {
-        case SC_SKIP_NONE: launch_chain_r<T, SC_SKIP_NONE>(R, grid, stream, a); break;
-        case SC_SKIP_LE: launch_chain_r<T, SC_SKIP_LE>(R, grid, stream, a); break;
-        case SC_SKIP_NOT_GT: launch_chain_r<T, SC_SKIP_NOT_GT>(R, grid, stream, a); break;
+        case SC_SKIP_NONE: launch_chain_r<T, SC_SKIP_NONE>(R, grid, stream, a, fused); break;
+        case SC_SKIP_LE: launch_chain_r<T, SC_SKIP_LE>(R, grid, stream, a, fused); break;
+        case SC_SKIP_NOT_GT: launch_chain_r<T, SC_SKIP_NOT_GT>(R, grid, stream, a, fused); break;
         default: SC_REQUIRE(false, "chain: bad skip_mode %d", skip_mode);
     }
     SC_CHECK_LAUNCH();
@@ -380,13 +388,13 @@ int launch_chain(int dtype, int skip_mode, double threshold, const void *x, int6
                  const ChainSeg *segs, int nseg, const void *init, int64_t init_len,
                  const int64_t *init_len_dev, int64_t t0, int64_t n_out, void *out_a,
                  int64_t n_a, void *out_b, cudaStream_t stream, const unsigned *run_if,
-                 const ChainBatch *batch) {
+                 const ChainBatch *batch, bool fused) {
     if (dtype == SC_F64)
         return launch_chain_t<double>(skip_mode, threshold, x, x_off, segs, nseg, init, init_len,
-                                      init_len_dev, t0, n_out, out_a, n_a, out_b, stream, run_if, batch);
+                                      init_len_dev, t0, n_out, out_a, n_a, out_b, stream, run_if, batch, fused);
     if (dtype == SC_F32)
         return launch_chain_t<float>(skip_mode, threshold, x, x_off, segs, nseg, init, init_len,
-                                     init_len_dev, t0, n_out, out_a, n_a, out_b, stream, run_if, batch);
+                                     init_len_dev, t0, n_out, out_a, n_a, out_b, stream, run_if, batch, fused);
     set_error("chain: bad dtype %d", dtype);
     return SC_ERR_ARG;
 }

@@ -72,6 +72,14 @@ __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, 
 // invariance stay bit-exact in float32 too.
 __device__ __forceinline__ double mac_rn(double acc, double x, double h) { return __dadd_rn(acc, __dmul_rn(x, h)); }
 __device__ __forceinline__ float mac_rn(float acc, float x, float h) { return __fmaf_rn(x, h, acc); }
+// FUSED = true: one rounding per step (fma) for double too -- the float64
+// FAST mode (chain order kept, product rounding dropped; within 1e-12).
+template <bool FUSED>
+__device__ __forceinline__ double mac_step(double acc, double x, double h) {
+    return FUSED ? __fma_rn(x, h, acc) : mac_rn(acc, x, h);
+}
+template <bool FUSED>
+__device__ __forceinline__ float mac_step(float acc, float x, float h) { return mac_rn(acc, x, h); }
 
 // Zero-skip predicates, compared in float64 like the reference (a float32
 // sample widens exactly; the threshold is never rounded to float32).
@@ -108,7 +116,7 @@ int launch_chain(int dtype, int skip_mode, double threshold, const void *x, int6
                  const ChainSeg *segs, int nseg, const void *init, int64_t init_len,
                  const int64_t *init_len_dev, int64_t t0, int64_t n_out, void *out_a,
                  int64_t n_a, void *out_b, cudaStream_t stream, const unsigned *run_if = nullptr,
-                 const struct ChainBatch *batch = nullptr);
+                 const struct ChainBatch *batch = nullptr, bool fused = false);
 
 // Optional channel batching for launch_chain (grid.y = channel): channel c
 // reads x + c*ldx, every segment's taps + c*ldh, its residue init + c*ld_init
