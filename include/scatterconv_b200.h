@@ -204,6 +204,21 @@ int sc_engine_process_blocks(sc_engine *e, const void *x, int64_t n_total, int64
                              const int64_t *swap_blocks, const void *const *swap_irs,
                              const int64_t *swap_nh, int64_t n_swaps, void *out);
 
+/* ---------------------------------------------------------------- multi-GPU */
+
+/* Whole-signal convolution of a HOST signal x[ne] (pinned or pageable) with
+ * h[nh] (host), partitioned by output time segment over ngpu devices
+ * (devices[]; repeats allowed): device g computes outputs [a_g, b_g) from
+ * its input slice plus the (nh-1)-sample halo -- no MAC repeated, no partial
+ * sums exchanged, no reduction (SURVEY.md 8(b) sc_fir_sharded, north_star
+ * (4)).  y[ne+nh-1] is a host pointer when gather_device < 0, else a device
+ * pointer on gather_device filled by peer copies.  One host thread per shard;
+ * synchronous.  mode as sc_fir_full; ORDERED float64 stays bit-identical to
+ * the reference at any device count (every output's chain runs on one
+ * device). */
+int sc_fir_sharded(int dtype, int mode, const void *x_host, int64_t ne, const void *h_host, int64_t nh, void *y,
+                   int ngpu, const int *devices, int gather_device);
+
 /* ---------------------------------------------------------------- WAV on device */
 
 /* SURVEY.md 8(f) row 3.  encoding: 0 pcm16, 1 pcm24, 2 float32 (the three

@@ -44,6 +44,8 @@ _SIGNATURES = {
     "sc_wav_encode": [ctypes.c_int, ctypes.c_int, _vp, _i64, _i64, _i64, ctypes.c_double, _vp, _vp, _vp],
     "sc_peak_abs": [ctypes.c_int, _vp, _i64, _vp, _vp],
     "sc_engine_tail_bound": [_vp, _p64],
+    "sc_fir_sharded": [ctypes.c_int, ctypes.c_int, _vp, _i64, _vp, _i64, _vp, ctypes.c_int,
+                       ctypes.POINTER(ctypes.c_int), ctypes.c_int],
     "sc_engine_set_mode": [_vp, ctypes.c_int],
     "sc_fixed_quantize": [_vp, _i64, ctypes.c_int, _vp, _vp, _vp, _vp],
     "sc_fixed_convolve": [_vp, _i64, _vp, _i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp],

@@ -18,7 +18,7 @@ import sys
 PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "_lib" / "libscatterconv_b200.so"
-SOURCES = ["capi.cu", "k_ordered.cu", "k_fast_f32.cu", "k_tc_fir.cu", "engine.cu", "k_wav.cu", "k_fixed.cu"]
+SOURCES = ["capi.cu", "k_ordered.cu", "k_fast_f32.cu", "k_tc_fir.cu", "engine.cu", "k_wav.cu", "k_fixed.cu", "sharded.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -124,6 +124,48 @@ def convolve_sharded(x, h, devices=None, gather: str | None = "host"):
     return t.cat([o.to(dst) for o in outs])
 
 
+def fir_sharded(x, h, devices=None, *, mode=None, gather_device=None):
+    """The C-ABI multi-GPU entry (``sc_fir_sharded``): host x [Ne] and h [Nh]
+    (float32 or float64), outputs partitioned over ``devices`` (repeats
+    allowed) by one native host thread per shard.  Returns the full
+    Ne+Nh-1 result as an ndarray, or as a CUDA tensor on ``gather_device``
+    (filled by peer copies).  mode as ``scatter_convolve``: float64 defaults
+    to ORDERED, bit-identical to the reference at any device count."""
+    import ctypes
+
+    from .core import _MODES, _result_dtype
+
+    t = _dev.torch()
+    devices = list(devices) if devices is not None else list(range(t.cuda.device_count()))
+    npd = _result_dtype(x, h)
+    xa = np.ascontiguousarray(x.cpu().numpy() if _dev.is_tensor(x) else x, dtype=npd)
+    ha = np.ascontiguousarray(h.cpu().numpy() if _dev.is_tensor(h) else h, dtype=npd)
+    if xa.ndim != 1 or ha.ndim != 1:
+        raise ValueError("x and h must be 1-D")
+    if len(xa) == 0:
+        raise ValueError("input signal is empty")
+    if len(ha) == 0:
+        raise ValueError("impulse response is empty")
+    if mode not in _MODES:
+        raise ValueError(f"mode must be one of {sorted(k for k in _MODES if k)}, got {mode!r}")
+    m = _MODES[mode]
+    if m is None:
+        m = N.SC_MODE_FAST if npd == np.float32 else N.SC_MODE_ORDERED
+    nout = len(xa) + len(ha) - 1
+    if gather_device is None:
+        y = np.empty(nout, dtype=npd)
+        yp, gd = y.ctypes.data, -1
+    else:
+        gd = t.device(gather_device).index if not isinstance(gather_device, int) else gather_device
+        y = t.empty(nout, dtype=_dev.torch_dtype(npd), device=t.device("cuda", gd))
+        yp = y.data_ptr()
+    devs = (ctypes.c_int * len(devices))(*devices)
+    N.check(N.lib().sc_fir_sharded(N.dtype_code(npd), m, ctypes.c_void_p(xa.ctypes.data), len(xa),
+                                   ctypes.c_void_p(ha.ctypes.data), len(ha), ctypes.c_void_p(yp),
+                                   len(devices), devs, gd))
+    return y
+
+
 def distributed_convolve(x, h, *, rank=None, world=None, compute=None, device=None,
                          to_host=False):
     """One shard per process (torchrun / torch.distributed initialised).

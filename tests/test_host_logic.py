@@ -185,3 +185,15 @@ def test_distributed_world2_gloo():
         p.join(120)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=5) is True
+
+
+def test_fir_sharded_validation_without_gpu():
+    """Argument errors surface before any device work (ValueError)."""
+    from paper_2401_01607_b200.sharded import fir_sharded
+
+    with pytest.raises(ValueError, match="input signal is empty"):
+        fir_sharded(np.zeros(0), np.ones(3), devices=[0])
+    with pytest.raises(ValueError, match="impulse response is empty"):
+        fir_sharded(np.ones(3), np.zeros(0), devices=[0])
+    with pytest.raises(ValueError, match="mode must be one of"):
+        fir_sharded(np.ones(3), np.ones(3), devices=[0], mode="bogus")
