@@ -58,7 +58,7 @@ def parse():
                          "ordered = the sequential-chain kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+    ap.add_argument("--cpu-seconds", type=float, default=20.0,
                     help="target seconds of CPU work for the cpu_baseline sample")
     return ap.parse_args()
 

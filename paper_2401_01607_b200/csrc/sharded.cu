@@ -6,8 +6,10 @@
 // and receives only its input slice plus the (Nh-1)-sample halo,
 // [max(0, a_g-Nh+1), min(Ne, b_g)).  No MAC is repeated and no partial sum
 // crosses devices, so there is no reduction: each device writes its segment
-// straight into the host result (or, with a gather device, into that
-// device's buffer over NVLink peer copies).  One host thread per shard
+// straight into the host result or, with a gather device, into that
+// device's buffer: the FIR epilogue stores there directly over NVLink when
+// peer access is available (compute and gather in one pass), else through a
+// peer copy.  One host thread per shard
 // drives its device (upload on its own stream, FIR, download), so the
 // uploads and kernels of all devices overlap.  Output-segment sharding keeps
 // every output's whole chain on one device: ORDERED float64 stays
@@ -85,21 +87,40 @@ int run_shard(ShardJob &j, int slot, int dtype, int mode, const void *x_host, co
             fail(SC_ERR_CUDA);
             break;
         }
+        // With a gather device reachable by peer access (or the same device),
+        // the kernel's epilogue stores its segment straight into the gather
+        // buffer -- over NVLink for a peer -- so compute and gather are one
+        // pass; otherwise the segment is staged and copied.
+        void *dst = yd;
+        bool direct = false;
+        if (gather_device >= 0) {
+            int can = gather_device == j.device;
+            if (!can) cudaDeviceCanAccessPeer(&can, j.device, gather_device);
+            if (can && gather_device != j.device) {
+                const cudaError_t pe = cudaDeviceEnablePeerAccess(gather_device, 0);
+                if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) can = 0;
+                cudaGetLastError();
+            }
+            if (can) {
+                dst = static_cast<char *>(y) + (size_t)j.a * es;
+                direct = true;
+            }
+        }
         if (dtype == SC_F32 && mode != SC_MODE_ORDERED) {
             rc = launch_fir_f32(mode, static_cast<const float *>(xd), 0, j.xb, j.xb, j.xe,
-                                static_cast<const float *>(hd), 0, nh, static_cast<float *>(yd), 0, j.a, j.b, 1, s);
+                                static_cast<const float *>(hd), 0, nh, static_cast<float *>(dst), 0, j.a, j.b, 1, s);
         } else {
             // the ordered chain of every output of [a, b) reads only [xb, xe)
             ChainSeg seg{hd, nh, j.xb, j.xe};
-            rc = launch_chain(dtype, SC_SKIP_NONE, 0.0, xd, j.xb, &seg, 1, nullptr, 0, nullptr, j.a, ny, yd, ny,
+            rc = launch_chain(dtype, SC_SKIP_NONE, 0.0, xd, j.xb, &seg, 1, nullptr, 0, nullptr, j.a, ny, dst, ny,
                               nullptr, s, nullptr, nullptr, dtype == SC_F64 && mode != SC_MODE_ORDERED);
         }
         if (rc) break;
-        cudaError_t e;
+        cudaError_t e = cudaSuccess;
         if (gather_device < 0)
             e = cudaMemcpyAsync(static_cast<char *>(y) + (size_t)j.a * es, yd, (size_t)ny * es,
                                 cudaMemcpyDeviceToHost, s);
-        else
+        else if (!direct)
             e = cudaMemcpyPeerAsync(static_cast<char *>(y) + (size_t)j.a * es, gather_device, yd, j.device,
                                     (size_t)ny * es, s);
         if (e != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) {
