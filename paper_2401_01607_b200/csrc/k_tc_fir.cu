@@ -361,20 +361,17 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned *addr, float v) {
     atomicMax(addr, __float_as_uint(v));
 }
 
-// max|x| per channel, and a global flag if any sample is NaN/Inf (the
-// tensor-core split cannot represent those; FAST mode then reroutes to the
-// FFMA kernel on the device, without a host round-trip).
-__global__ void k_amax(const float *__restrict__ x, int64_t ld, int64_t n, unsigned *out,
-                       unsigned *nonfinite) {
-    const float *xc = x + (int64_t)blockIdx.y * ld;
+// max|v| over one channel's n samples into *out, and a global flag if any
+// sample is NaN/Inf (the tensor-core split cannot represent those; FAST mode
+// then reroutes to the ordered kernel on the device, no host round-trip).
+__device__ __forceinline__ void amax_body(const float *__restrict__ xc, int64_t n, int64_t tid, int64_t stride,
+                                          unsigned *out, unsigned *nonfinite) {
     float m = 0.0f;
     bool bad = false;
     // scalar head up to 16-byte alignment, float4 body, scalar tail
     const int64_t mis = (int64_t)((16 - (reinterpret_cast<uintptr_t>(xc) & 15)) & 15) / 4;
     const int64_t head = mis < n ? mis : n;
     const int64_t n4 = (n - head) / 4;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const float4 *x4 = reinterpret_cast<const float4 *>(xc + head);
     for (int64_t i = tid; i < n4; i += stride) {
         const float4 q = x4[i];
@@ -390,22 +387,32 @@ __global__ void k_amax(const float *__restrict__ x, int64_t ld, int64_t n, unsig
         m = v > m ? v : m;
     }
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out + 2 * blockIdx.y, m);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out, m);
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
 }
 
-// per channel c: scales[3c] = 2^ex, [3c+1] = 2^eh (exact powers of two that
-// put max|x|, max|h| in [2^14, 2^15)), [3c+2] = 2^-(ex+eh).  amax[2c], [2c+1].
-__global__ void k_scales(const unsigned *amax, float *scales, int channels) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= channels) return;
+// One launch for both operands: blocks [0, gx) reduce x (amax[2c]), blocks
+// [gx, gridDim.x) reduce h (amax[2c+1]); grid.y = channel.
+__global__ void k_amax2(const float *__restrict__ x, int64_t ldx, int64_t nx, int gx, const float *__restrict__ h,
+                        int64_t ldh, int64_t nh, unsigned *amax, unsigned *nonfinite) {
+    const int c = blockIdx.y;
+    if ((int)blockIdx.x < gx)
+        amax_body(x + (int64_t)c * ldx, nx, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                  (int64_t)gx * blockDim.x, amax + 2 * c, nonfinite);
+    else
+        amax_body(h + (int64_t)c * ldh, nh, (int64_t)(blockIdx.x - gx) * blockDim.x + threadIdx.x,
+                  (int64_t)(gridDim.x - gx) * blockDim.x, amax + 2 * c + 1, nonfinite);
+}
+
+// per channel c: exact powers of two that put max|x|, max|h| in [2^14, 2^15):
+// 2^ex, 2^eh, and the epilogue's unscale 2^-(ex+eh).  From amax[2c], [2c+1].
+__device__ __forceinline__ float3 channel_scales(const unsigned *amax, int c) {
     int e[2];
     for (int i = 0; i < 2; ++i) {
         const float m = __uint_as_float(amax[2 * c + i]);
         e[i] = (m > 0.0f && isfinite(m)) ? 14 - ilogbf(m) : 0;
-        scales[3 * c + i] = ldexpf(1.0f, e[i]);
     }
-    scales[3 * c + 2] = ldexpf(1.0f, -(e[0] + e[1]));
+    return make_float3(ldexpf(1.0f, e[0]), ldexpf(1.0f, e[1]), ldexpf(1.0f, -(e[0] + e[1])));
 }
 
 __device__ __forceinline__ void split16(float v, __half &hi, __half &lo) {
@@ -414,17 +421,15 @@ __device__ __forceinline__ void split16(float v, __half &hi, __half &lo) {
 }
 
 // XT[c][j][row][e] = split(scale_c * X_c(n_begin + (row + row_min)*128 + 8j + e))
-__global__ void k_split_x(const float *__restrict__ x, int64_t ldx, int64_t x_base, int64_t x_lo,
-                          int64_t x_hi, int64_t n_begin, int64_t row_min, int64_t nrows,
-                          const float *scales, __half *__restrict__ xt_hi, __half *__restrict__ xt_lo,
-                          int64_t xt_ch) {
+__device__ __forceinline__ void split_x_tile(const float *__restrict__ x, int64_t ldx, int64_t x_base, int64_t x_lo,
+                                             int64_t x_hi, int64_t n_begin, int64_t row_min, int64_t nrows,
+                                             float sc, __half *__restrict__ xt_hi, __half *__restrict__ xt_lo,
+                                             int64_t xt_ch, int64_t tile, float (*s)[132]) {
     // One CTA = 32 consecutive rows = 4096 contiguous samples: coalesced
     // float4 loads into a padded smem tile (row pitch 132 floats), then each
     // K-group j writes its 32 rows x 16 B = 512 B contiguous (fp16 hi and lo).
-    __shared__ __align__(16) float s[32][132];
     const int c = blockIdx.y;
-    const int64_t row0 = (int64_t)blockIdx.x * 32;
-    const float sc = scales[3 * c];
+    const int64_t row0 = tile * 32;
     const float *xc = x + (int64_t)c * ldx;
     const int64_t m0 = n_begin + (row0 + row_min) * TR;  // first sample of the tile
     const bool inside = m0 >= x_lo && m0 + 4096 <= x_hi &&
@@ -474,15 +479,14 @@ __global__ void k_tc_split_reduce(const float *__restrict__ ws, int nsplit, int 
     y[(int64_t)ch * ldy + i] = s;
 }
 
-__global__ void k_build_h8(const float *__restrict__ h, int64_t ldh, int64_t nh, int64_t s8,
-                           int64_t ngroups, const float *scales, __half *__restrict__ h8_hi,
-                           __half *__restrict__ h8_lo, int64_t h8_ch) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (g, b)
+__device__ __forceinline__ void build_h8_part(const float *__restrict__ h, int64_t ldh, int64_t nh, int64_t s8,
+                                              int64_t ngroups, float sc, __half *__restrict__ h8_hi,
+                                              __half *__restrict__ h8_lo, int64_t h8_ch, int64_t part) {
+    const int64_t idx = part * blockDim.x + threadIdx.x;  // (g, b)
     if (idx >= ngroups * 8) return;
     const int c = blockIdx.y;
     const int64_t g = idx >> 3;
     const int b = (int)(idx & 7);
-    const float sc = scales[3 * c + 1];
     const float *hc = h + (int64_t)c * ldh;
     const int64_t cc = (int64_t)TR * s8 - 1;
     __align__(16) __half hv[8], lv[8];
@@ -495,6 +499,31 @@ __global__ void k_build_h8(const float *__restrict__ h, int64_t ldh, int64_t nh,
     const int64_t o = (int64_t)c * h8_ch + idx * 8;
     *reinterpret_cast<uint4 *>(h8_hi + o) = *reinterpret_cast<const uint4 *>(hv);
     *reinterpret_cast<uint4 *>(h8_lo + o) = *reinterpret_cast<const uint4 *>(lv);
+}
+
+// One launch for the operand images: blocks [0, gsplit) split x tiles,
+// the rest build H8; each derives its channel's power-of-two scales from
+// amax (block (0, c) also stores them for the tensor-core epilogue).
+__global__ void __launch_bounds__(256) k_tc_prep(const float *__restrict__ x, int64_t ldx, int64_t x_base,
+                                                 int64_t x_lo, int64_t x_hi, int64_t n_begin, int64_t row_min,
+                                                 int64_t nrows, int gsplit, const float *__restrict__ h, int64_t ldh,
+                                                 int64_t nh, int64_t s8, int64_t ngroups, const unsigned *amax,
+                                                 float *scales, __half *__restrict__ xt_hi,
+                                                 __half *__restrict__ xt_lo, int64_t xt_ch,
+                                                 __half *__restrict__ h8_hi, __half *__restrict__ h8_lo,
+                                                 int64_t h8_ch) {
+    __shared__ __align__(16) float s[32][132];
+    const int c = blockIdx.y;
+    const float3 sc = channel_scales(amax, c);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        scales[3 * c] = sc.x;
+        scales[3 * c + 1] = sc.y;
+        scales[3 * c + 2] = sc.z;
+    }
+    if ((int)blockIdx.x < gsplit)
+        split_x_tile(x, ldx, x_base, x_lo, x_hi, n_begin, row_min, nrows, sc.x, xt_hi, xt_lo, xt_ch, blockIdx.x, s);
+    else
+        build_h8_part(h, ldh, nh, s8, ngroups, sc.y, h8_hi, h8_lo, h8_ch, (int64_t)blockIdx.x - gsplit);
 }
 
 }  // namespace
@@ -534,30 +563,22 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     __half *h8_lo = h8_hi + h8_ch * channels;
 
     SC_CHECK_CUDA(cudaMemsetAsync(amax, 0, 8 * channels + 4, stream));
-    const int64_t xn = x_hi - x_lo;
-    if (xn > 0) {
-        // ~8 resident CTAs per SM across all channels, float4 per thread
+    {
+        // ~8 resident CTAs per SM across all channels for x, float4 per thread
+        const int64_t xn = x_hi - x_lo;
         const int64_t per_ch = std::max<int64_t>(1, 8 * (int64_t)sm_count() / channels);
-        dim3 g((unsigned)std::min<int64_t>(cdiv(xn, 1024), per_ch), (unsigned)channels);
-        k_amax<<<g, 256, 0, stream>>>(x + (x_lo - x_base), ldx, xn, amax, flag);
+        const int gx = xn > 0 ? (int)std::min<int64_t>(cdiv(xn, 1024), per_ch) : 0;
+        const int gh = (int)std::min<int64_t>(cdiv(nh, 1024), std::max<int64_t>(1, per_ch / 4));
+        dim3 g((unsigned)(gx + gh), (unsigned)channels);
+        k_amax2<<<g, 256, 0, stream>>>(x + (x_lo - x_base), ldx, xn, gx, h, ldh, nh, amax, flag);
         SC_CHECK_LAUNCH();
     }
     {
-        dim3 g((unsigned)std::min<int64_t>(cdiv(nh, 256), 4 * 148), (unsigned)channels);
-        k_amax<<<g, 256, 0, stream>>>(h, ldh, nh, amax + 1, flag);
-        SC_CHECK_LAUNCH();
-    }
-    k_scales<<<(unsigned)cdiv(channels, 128), 128, 0, stream>>>(amax, scales, (int)channels);
-    SC_CHECK_LAUNCH();
-    {
-        dim3 g((unsigned)cdiv(nrows, 32), (unsigned)channels);
-        k_split_x<<<g, 256, 0, stream>>>(x, ldx, x_base, x_lo, x_hi, n_begin, row_min, nrows, scales, xt_hi,
-                                         xt_lo, xt_ch);
-        SC_CHECK_LAUNCH();
-    }
-    {
-        dim3 g((unsigned)cdiv(ngroups * 8, 256), (unsigned)channels);
-        k_build_h8<<<g, 256, 0, stream>>>(h, ldh, nh, s8, ngroups, scales, h8_hi, h8_lo, h8_ch);
+        const int gsplit = (int)cdiv(nrows, 32);
+        const int gh8 = (int)cdiv(ngroups * 8, 256);
+        dim3 g((unsigned)(gsplit + gh8), (unsigned)channels);
+        k_tc_prep<<<g, 256, 0, stream>>>(x, ldx, x_base, x_lo, x_hi, n_begin, row_min, nrows, gsplit, h, ldh, nh,
+                                         s8, ngroups, amax, scales, xt_hi, xt_lo, xt_ch, h8_hi, h8_lo, h8_ch);
         SC_CHECK_LAUNCH();
     }
     // function attributes are per device (context): set on every launch so
