@@ -11,7 +11,7 @@ from paper_2401_01607_b200.sweeps import (
     BenchReport,
     BenchRow,
     SweepSpec,
-    _fit_line,
+    _least_squares as _fit_line,
     find_realtime_limit,
     gen_white_noise,
     ms_to_samples,
