@@ -30,35 +30,57 @@ SCHEMES = ("ideal", "mac")
 _SCHEME_CODE = {"ideal": 0, "mac": 1}
 
 
+def _int_at_least(v, lo: int) -> bool:
+    return isinstance(v, (int, np.integer)) and v >= lo
+
+
+def _one_of(value, allowed, what: str):
+    if value not in allowed:
+        raise ValueError(f"{what} must be one of {allowed}, got {value!r}")
+
+
 @dataclass(frozen=True)
 class FixedPointFormat:
     """Two's-complement fraction: one sign bit and word_bits-1 fractional bits
-    (quantize.py:34-70)."""
+    (quantize.py:34-70).  Rounds to nearest-even; saturates where samples are
+    stored."""
 
     word_bits: int
     rounding: str = "nearest-even"
     overflow: str = "saturate"
 
     def __post_init__(self):
-        if not isinstance(self.word_bits, (int, np.integer)) or self.word_bits < 2:
+        if not _int_at_least(self.word_bits, 2):
             raise ValueError(f"word_bits must be an integer >= 2, got {self.word_bits!r}")
-        if self.rounding not in ROUNDING_MODES:
-            raise ValueError(f"rounding must be one of {ROUNDING_MODES}, got {self.rounding!r}")
-        if self.overflow not in OVERFLOW_MODES:
-            raise ValueError(f"overflow must be one of {OVERFLOW_MODES}, got {self.overflow!r}")
+        _one_of(self.rounding, ROUNDING_MODES, "rounding")
+        _one_of(self.overflow, OVERFLOW_MODES, "overflow")
 
-    fractional_bits = property(lambda self: self.word_bits - 1)
-    scale = property(lambda self: 1 << (self.word_bits - 1))
-    min_int = property(lambda self: -(1 << (self.word_bits - 1)))
-    max_int = property(lambda self: (1 << (self.word_bits - 1)) - 1)
-    ulp = property(lambda self: 1.0 / (1 << (self.word_bits - 1)))
+    @property
+    def fractional_bits(self) -> int:
+        return self.word_bits - 1
+
+    @property
+    def scale(self) -> int:                 # 2^fractional_bits
+        return 1 << self.fractional_bits
+
+    @property
+    def min_int(self) -> int:
+        return -self.scale
+
+    @property
+    def max_int(self) -> int:
+        return self.scale - 1
+
+    @property
+    def ulp(self) -> float:
+        return 1.0 / self.scale
 
 
 @dataclass
 class RequantReport:
-    """Error statistics of one simulated scheme (quantize.py:73-100):
-    rounding events per output, bits removed per event, and rms / max error
-    against the exact-product result on the same quantised inputs."""
+    """What one simulated scheme did (quantize.py:73-100): rounding events
+    per output sample and the bits each removes, plus rms / max deviation from
+    the exact-product result on the same quantised inputs."""
 
     scheme: str
     operations_count: int
@@ -67,9 +89,8 @@ class RequantReport:
     max_error: float
 
     def __post_init__(self):
-        if self.scheme not in SCHEMES:
-            raise ValueError(f"scheme must be one of {SCHEMES}, got {self.scheme!r}")
-        if self.operations_count < 0 or self.bits_removed_per_op < 0:
+        _one_of(self.scheme, SCHEMES, "scheme")
+        if min(self.operations_count, self.bits_removed_per_op) < 0:
             raise ValueError("counts must be non-negative")
         if self.rms_error > self.max_error:
             raise ValueError(f"rms_error {self.rms_error} exceeds max_error {self.max_error}")
@@ -78,30 +99,31 @@ class RequantReport:
 # ------------------------------------------------------------------ closed forms
 
 
-def _check_bits(n_bits, ir_len):
-    if not isinstance(n_bits, (int, np.integer)) or n_bits < 2:
+def _budget_args(n_bits, ir_len):
+    if not _int_at_least(n_bits, 2):
         raise ValueError(f"word length must be an integer >= 2 bits, got {n_bits!r}")
-    if not isinstance(ir_len, (int, np.integer)) or ir_len < 1:
+    if not _int_at_least(ir_len, 1):
         raise ValueError(f"impulse response length must be a positive integer, got {ir_len!r}")
+    return int(n_bits), int(ir_len)
 
 
 def ideal_accumulator_bits(n_bits: int, ir_len: int) -> int:
-    """Overflow-proof accumulator width, 2*n_bits + ir_len - 1 (one carry bit
-    per added term: the reference's deliberately conservative budget)."""
-    _check_bits(n_bits, ir_len)
-    return 2 * n_bits + ir_len - 1
+    """Overflow-proof accumulator width: two N-bit operands per product plus
+    one carry bit per added term (the reference's conservative budget)."""
+    n, L = _budget_args(n_bits, ir_len)
+    return 2 * n + L - 1
 
 
 def ideal_bits_removed(n_bits: int, ir_len: int) -> int:
-    """Bits the single final rounding of the ideal scheme drops."""
-    _check_bits(n_bits, ir_len)
-    return n_bits + ir_len - 1
+    """Bits the ideal scheme's single final rounding drops."""
+    n, L = _budget_args(n_bits, ir_len)
+    return n + L - 1
 
 
 def mac_requant_count(n_bits: int, ir_len: int) -> tuple[int, int]:
-    """(rounding events, bits each) of the round-after-every-MAC scheme."""
-    _check_bits(n_bits, ir_len)
-    return ir_len - 1, n_bits
+    """(rounding events, bits per event) when every MAC is rounded back."""
+    n, L = _budget_args(n_bits, ir_len)
+    return L - 1, n
 
 
 # ------------------------------------------------------------------ device simulation
@@ -134,15 +156,18 @@ def quantize(values, fmt: FixedPointFormat):
     return _dev.like_input(xq, values)
 
 
-def fixed_point_convolve(e: Signal, h: Signal, fmt: FixedPointFormat, scheme: str) -> Signal:
-    """Quantise both signals, convolve exactly in integers, requantise per
-    scheme (quantize.py:163-195).  Float64 outputs on the format's grid."""
-    if scheme not in SCHEMES:
-        raise ValueError(f"scheme must be one of {SCHEMES}, got {scheme!r}")
-    if len(e) == 0 or len(h) == 0:
+def _check_pair(e: Signal, h: Signal, scheme: str):
+    _one_of(scheme, SCHEMES, "scheme")
+    if min(len(e), len(h)) == 0:
         raise ValueError("empty signal")
     if e.sample_rate != h.sample_rate:
         raise ValueError("sample rates differ")
+
+
+def fixed_point_convolve(e: Signal, h: Signal, fmt: FixedPointFormat, scheme: str) -> Signal:
+    """Quantise both signals, convolve exactly in integers, requantise per
+    scheme (quantize.py:163-195).  Float64 outputs on the format's grid."""
+    _check_pair(e, h, scheme)
     y = _fixed_conv_device(e, h, fmt, scheme)[0]
     return Signal(_dev.like_input(y, e.samples, h.samples), e.sample_rate)
 
@@ -167,12 +192,7 @@ def _fixed_conv_device(e: Signal, h: Signal, fmt: FixedPointFormat, scheme: str)
 def simulate_fixed_point_conv(e: Signal, h: Signal, fmt: FixedPointFormat, scheme: str) -> RequantReport:
     """Run one scheme and measure it against direct_form on the quantised
     inputs, isolating requantisation damage (quantize.py:198-222)."""
-    if scheme not in SCHEMES:
-        raise ValueError(f"scheme must be one of {SCHEMES}, got {scheme!r}")
-    if len(e) == 0 or len(h) == 0:
-        raise ValueError("empty signal")
-    if e.sample_rate != h.sample_rate:
-        raise ValueError("sample rates differ")
+    _check_pair(e, h, scheme)
     y, eq, hq = _fixed_conv_device(e, h, fmt, scheme)
     ref = direct_form(Signal(eq, e.sample_rate), Signal(hq, h.sample_rate)).samples
     # the two summary statistics are numpy reductions of the device results
