@@ -27,15 +27,15 @@ from tests import _golden as G
 pytestmark = pytest.mark.gpu
 
 
-def sig(values, rate=44100):
+def _sig(values, rate=44100):
     return Signal(np.asarray(values, dtype=np.float64), rate)
 
 
-def full(out) -> np.ndarray:
+def _whole(out) -> np.ndarray:
     return np.asarray(out.concatenated().samples)
 
 
-def assert_close(actual, expected, rtol):
+def _near(actual, expected, rtol):
     expected = np.asarray(expected)
     scale = max(1.0, float(np.max(np.abs(expected))) if expected.size else 0.0)
     np.testing.assert_allclose(actual, expected, rtol=0.0, atol=rtol * scale)
@@ -48,27 +48,27 @@ def within_tol(y, ref, x, h, dtype="f32"):
     return err, tol
 
 
-amplitudes = st.floats(min_value=-1.0, max_value=1.0, allow_nan=False, width=64)
-signal_values = st.lists(amplitudes, min_size=1, max_size=64)
+_AMP = st.floats(min_value=-1.0, max_value=1.0, allow_nan=False, width=64)
+_SEQ = st.lists(_AMP, min_size=1, max_size=64)
 
 # ---------------------------------------------------------------- frozen values
 
 
 def test_direct_form_hand_examples():
-    assert np.array_equal(direct_form(sig([1.0]), sig([5.0, 6.0, 7.0])).samples, [5.0, 6.0, 7.0])
-    assert np.array_equal(direct_form(sig([1.0, 2.0]), sig([3.0, 4.0])).samples, [3.0, 10.0, 8.0])
-    assert np.array_equal(direct_form(sig([0.0, 0.0, 0.0]), sig([1.0, 1.0])).samples, np.zeros(4))
+    assert np.array_equal(direct_form(_sig([1.0]), _sig([5.0, 6.0, 7.0])).samples, [5.0, 6.0, 7.0])
+    assert np.array_equal(direct_form(_sig([1.0, 2.0]), _sig([3.0, 4.0])).samples, [3.0, 10.0, 8.0])
+    assert np.array_equal(direct_form(_sig([0.0, 0.0, 0.0]), _sig([1.0, 1.0])).samples, np.zeros(4))
 
 
 def test_scatter_hand_examples():
-    out = scatter_convolve(sig([1.0, 2.0]), sig([3.0, 4.0]))
+    out = scatter_convolve(_sig([1.0, 2.0]), _sig([3.0, 4.0]))
     assert np.array_equal(out.body.samples, [3.0, 10.0])
     assert np.array_equal(out.tail.samples, [8.0])
-    out = scatter_convolve(sig([1.0, 0.0, 0.0, 0.0]), sig([9.0]))
+    out = scatter_convolve(_sig([1.0, 0.0, 0.0, 0.0]), _sig([9.0]))
     assert np.array_equal(out.body.samples, [9.0, 0.0, 0.0, 0.0]) and len(out.tail) == 0
-    h = sig([0.5, -0.25, 0.125])
+    h = _sig([0.5, -0.25, 0.125])
     for k in (1, 3, 7):
-        got = full(scatter_convolve(sig([0.0] * k + [1.0]), h))
+        got = _whole(scatter_convolve(_sig([0.0] * k + [1.0]), h))
         assert np.array_equal(got[:k], np.zeros(k)) and np.array_equal(got[k:], h.samples)
 
 
@@ -81,8 +81,8 @@ def test_commuted_short_signal_drives(monkeypatch):
         return original(drive, kern)
 
     monkeypatch.setattr(core, "_scatter_full", spy)
-    e = sig([1.0, 2.0, 3.0, 4.0, 5.0, 6.0])
-    h = sig([1.0, 2.0, 3.0])
+    e = _sig([1.0, 2.0, 3.0, 4.0, 5.0, 6.0])
+    h = _sig([1.0, 2.0, 3.0])
     out = commuted_convolve(e, h)
     assert lengths == [3]
     assert len(out.body) == 6 and len(out.tail) == 2
@@ -92,20 +92,20 @@ def test_commuted_short_signal_drives(monkeypatch):
 
 
 def test_skip_zeros_hand_examples():
-    out = scatter_convolve_skip_zeros(sig([1.0, 0.0, 2.0]), sig([1.0, 1.0]), threshold=0.0)
+    out = scatter_convolve_skip_zeros(_sig([1.0, 0.0, 2.0]), _sig([1.0, 1.0]), threshold=0.0)
     assert np.array_equal(out.body.samples, [1.0, 1.0, 2.0]) and np.array_equal(out.tail.samples, [2.0])
-    out = scatter_convolve_skip_zeros(sig([0.0, 0.0]), sig([4.0, 5.0, 6.0]), threshold=0.0)
-    assert np.array_equal(full(out), np.zeros(4))
-    out = scatter_convolve_skip_zeros(sig([1.0, 1e-9, 1.0]), sig([1.0]), threshold=1e-6)
+    out = scatter_convolve_skip_zeros(_sig([0.0, 0.0]), _sig([4.0, 5.0, 6.0]), threshold=0.0)
+    assert np.array_equal(_whole(out), np.zeros(4))
+    out = scatter_convolve_skip_zeros(_sig([1.0, 1e-9, 1.0]), _sig([1.0]), threshold=1e-6)
     assert np.array_equal(out.body.samples, [1.0, 0.0, 1.0])
 
 
 def test_nan_and_signed_zero_semantics():
     # scatter_convolve propagates NaN (core.py:90); -0.0 inputs still "scatter"
-    got = full(scatter_convolve(sig([1.0, np.nan, 2.0]), sig([1.0, 1.0])))
+    got = _whole(scatter_convolve(_sig([1.0, np.nan, 2.0]), _sig([1.0, 1.0])))
     want = O.scatter_full([1.0, np.nan, 2.0], [1.0, 1.0])
     assert np.array_equal(got, want, equal_nan=True)
-    got = full(scatter_convolve(sig([-0.0]), sig([-0.0, 1.0])))
+    got = _whole(scatter_convolve(_sig([-0.0]), _sig([-0.0, 1.0])))
     assert np.array_equal(np.signbit(got), np.signbit(O.scatter_full([-0.0], [-0.0, 1.0])))
 
 
@@ -119,17 +119,17 @@ def pairs():
 
 def test_golden_scatter_commuted_skip_bit_exact(pairs):
     for p in pairs:
-        E, H = sig(p["e"]), sig(p["h"])
-        assert np.array_equal(full(scatter_convolve(E, H)), p["scatter"])
-        assert np.array_equal(full(commuted_convolve(E, H)), p["commuted"])
-        assert np.array_equal(full(scatter_convolve_skip_zeros(E, H, p["threshold"])), p["skip"])
+        E, H = _sig(p["e"]), _sig(p["h"])
+        assert np.array_equal(_whole(scatter_convolve(E, H)), p["scatter"])
+        assert np.array_equal(_whole(commuted_convolve(E, H)), p["commuted"])
+        assert np.array_equal(_whole(scatter_convolve_skip_zeros(E, H, p["threshold"])), p["skip"])
 
 
 def test_golden_direct_form(pairs):
     exact = 0
     for p in pairs:
-        got = direct_form(sig(p["e"]), sig(p["h"])).samples
-        assert_close(got, p["direct"], 1e-15)
+        got = direct_form(_sig(p["e"]), _sig(p["h"])).samples
+        _near(got, p["direct"], 1e-15)
         exact += int(np.array_equal(got, p["direct"]))
     assert exact >= 0.95 * len(pairs)
 
@@ -137,23 +137,23 @@ def test_golden_direct_form(pairs):
 # ---------------------------------------------------------------- properties (float64)
 
 
-@given(e=signal_values, h=signal_values)
+@given(e=_SEQ, h=_SEQ)
 @settings(max_examples=150)
 def test_oracle_equivalence(e, h):
-    got = full(scatter_convolve(sig(e), sig(h)))
+    got = _whole(scatter_convolve(_sig(e), _sig(h)))
     assert np.array_equal(got, O.scatter_full(e, h))          # reference chain, bit-exact
-    assert_close(got, O.direct_form(e, h), 1e-12)             # exact-sum oracle
+    _near(got, O.direct_form(e, h), 1e-12)             # exact-sum oracle
 
 
-@given(e=signal_values, h=signal_values)
+@given(e=_SEQ, h=_SEQ)
 def test_length_law_and_commutativity(e, h):
-    out = scatter_convolve(sig(e), sig(h))
+    out = scatter_convolve(_sig(e), _sig(h))
     assert len(out.body) == len(e) and len(out.tail) == len(h) - 1
-    assert_close(full(out), full(scatter_convolve(sig(h), sig(e))), 1e-12)
-    assert_close(full(commuted_convolve(sig(e), sig(h))), full(out), 1e-12)
+    _near(_whole(out), _whole(scatter_convolve(_sig(h), _sig(e))), 1e-12)
+    _near(_whole(commuted_convolve(_sig(e), _sig(h))), _whole(out), 1e-12)
 
 
-@given(e1=signal_values, e2=signal_values, h=signal_values,
+@given(e1=_SEQ, e2=_SEQ, h=_SEQ,
        a=st.floats(min_value=-10, max_value=10, allow_nan=False, width=64),
        b=st.floats(min_value=-10, max_value=10, allow_nan=False, width=64))
 def test_linearity(e1, e2, h, a, b):
@@ -162,28 +162,28 @@ def test_linearity(e1, e2, h, a, b):
     x1[: len(e1)] = e1
     x2 = np.zeros(n)
     x2[: len(e2)] = e2
-    mixed = full(scatter_convolve(sig(a * x1 + b * x2), sig(h)))
-    separate = a * full(scatter_convolve(sig(x1), sig(h))) + b * full(scatter_convolve(sig(x2), sig(h)))
-    assert_close(mixed, separate, 1e-10)
+    mixed = _whole(scatter_convolve(_sig(a * x1 + b * x2), _sig(h)))
+    separate = a * _whole(scatter_convolve(_sig(x1), _sig(h))) + b * _whole(scatter_convolve(_sig(x2), _sig(h)))
+    _near(mixed, separate, 1e-10)
 
 
-@given(e=signal_values, h=signal_values, k=st.integers(min_value=1, max_value=16))
+@given(e=_SEQ, h=_SEQ, k=st.integers(min_value=1, max_value=16))
 def test_time_invariance_bit_exact(e, h, k):
-    base = full(scatter_convolve(sig(e), sig(h)))
-    shifted = full(scatter_convolve(sig([0.0] * k + e), sig(h)))
+    base = _whole(scatter_convolve(_sig(e), _sig(h)))
+    shifted = _whole(scatter_convolve(_sig([0.0] * k + e), _sig(h)))
     assert np.array_equal(shifted[:k], np.zeros(k)) and np.array_equal(shifted[k:], base)
 
 
-@given(h=signal_values)
+@given(h=_SEQ)
 def test_unit_impulse_bit_exact(h):
-    assert np.array_equal(full(scatter_convolve(sig([1.0]), sig(h))), np.asarray(h))
+    assert np.array_equal(_whole(scatter_convolve(_sig([1.0]), _sig(h))), np.asarray(h))
 
 
-@given(e=signal_values, h=signal_values, threshold=st.floats(min_value=0, max_value=0.5, width=64))
+@given(e=_SEQ, h=_SEQ, threshold=st.floats(min_value=0, max_value=0.5, width=64))
 def test_skip_threshold_equals_thresholded_input(e, h, threshold):
-    skipped = full(scatter_convolve_skip_zeros(sig(e), sig(h), threshold=threshold))
+    skipped = _whole(scatter_convolve_skip_zeros(_sig(e), _sig(h), threshold=threshold))
     gated = np.where(np.abs(np.asarray(e)) <= threshold, 0.0, np.asarray(e))
-    assert np.array_equal(skipped, full(scatter_convolve(sig(gated), sig(h))))
+    assert np.array_equal(skipped, _whole(scatter_convolve(_sig(gated), _sig(h))))
 
 
 # ---------------------------------------------------------------- float32 fast path
@@ -197,7 +197,7 @@ def test_fast_f32_within_tolerance(ne, nh):
     rng = np.random.default_rng(ne * 7 + nh)
     x = rng.uniform(-1, 1, ne).astype(np.float32)
     h = (rng.standard_normal(nh) * np.exp(-np.arange(nh) / max(1.0, nh / 4))).astype(np.float32)
-    y = full(scatter_convolve(Signal(x), Signal(h)))
+    y = _whole(scatter_convolve(Signal(x), Signal(h)))
     assert y.dtype == np.float32 and len(y) == ne + nh - 1
     ref = O.scatter_window(x, h, 0, ne + nh - 1)
     within_tol(y, ref, x, h)
@@ -208,7 +208,7 @@ def test_ordered_f32_within_tolerance(ne, nh):
     rng = np.random.default_rng(ne + 3 * nh)
     x = rng.uniform(-1, 1, ne).astype(np.float32)
     h = rng.standard_normal(nh).astype(np.float32)
-    y = full(scatter_convolve(Signal(x), Signal(h), mode="ordered"))
+    y = _whole(scatter_convolve(Signal(x), Signal(h), mode="ordered"))
     within_tol(y, O.scatter_full(x, h), x, h)
 
 
@@ -229,7 +229,7 @@ def test_fast_f32_nan_propagates_like_reference():
     x[5] = np.nan
     x[100] = 1.0
     h = np.ones(300, np.float32)
-    y = full(scatter_convolve(Signal(x), Signal(h)))
+    y = _whole(scatter_convolve(Signal(x), Signal(h)))
     ref = O.scatter_full(x, h)
     assert np.array_equal(np.isnan(y), np.isnan(ref))
 
