@@ -413,6 +413,23 @@ def cpu_sample(cfg, seconds, threads):
                              f"scatter_block engine per input segment, overlap-add, {threads} threads"), dt
 
 
+def workload_config(cfg: str) -> dict:
+    """The `config` object of a bench line for `cfg` (same keys on both arms;
+    host-only, no device)."""
+    from paper_2401_01607_b200 import configs
+
+    if cfg.startswith("short"):
+        nh = int(cfg[5:])
+        ne, ch, name = 1 << 26, 1, f"short_f32_67108864x{nh}"
+    else:
+        w = configs.ALL["cfg4" if cfg == "mstream" else cfg]()
+        ne, nh, ch, name = w.ne, w.nh, w.channels, w.name
+        if cfg == "mstream":
+            name = "mstream_f32_64ch_480000x16384_b8192_1swap_multichannel_engine"
+    return {"workload": name, "ne": int(ne), "nh": int(nh), "channels": int(ch),
+            "metric_macs": int(ch * (ne + nh - 1) * nh)}
+
+
 def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
@@ -431,9 +448,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(times),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.config in ("cfg3", "cfg4", "cfg5") else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded PCG64, SURVEY.md 8(d))",
-        "config": {"workload": args.config, "parallelism": f"CPU, {threads} threads"},
+        "config": {**workload_config(args.config), "parallelism": f"CPU, {threads} threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": samples[-1]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
