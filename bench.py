@@ -387,7 +387,7 @@ def cpu_sample(cfg, seconds, threads):
     if cfg in ("cfg4", "mstream"):
         # one engine per channel on a thread pool (the reference's pattern)
         c = max(1, threads)
-        ne0 = 2000
+        ne0 = 8192
         t0 = time.perf_counter()
         O.conv_channels(x[:c, :ne0], h[:c], nb=8192, threads=threads)
         dt = time.perf_counter() - t0
@@ -399,7 +399,7 @@ def cpu_sample(cfg, seconds, threads):
         macs = c * ne * h.shape[1]
         return macs / dt / 1e9, f"{c} channels x {ne} samples x {h.shape[1]} taps ({macs:.3e} MAC, one float64 engine per channel, {threads} threads)", dt
     nh = len(h)
-    s0 = max(threads, 2000)
+    s0 = min(len(x), max(2000, 2048 * threads))   # probe big enough to amortise thread start-up
     t0 = time.perf_counter()
     O.conv_parallel(x[:s0], h, nb=8192, threads=threads)
     dt = time.perf_counter() - t0
