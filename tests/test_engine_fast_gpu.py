@@ -204,3 +204,26 @@ def test_fast_process_block_large_blocks_with_pending_swap():
         tol = max(_tol(x[c], h0[c]), _tol(x[c], h1[c]))
         assert np.max(np.abs(body[c] - ref_body)) <= tol, c
         assert len(tails[c]) == len(ref_tail) and np.max(np.abs(tails[c] - ref_tail)) <= tol, c
+
+
+def test_fast_many_swaps_chunked_calls():
+    """45 IR changes: the fused call is split into launches of <= 31 events,
+    each of which takes the batched tensor-core path (uniform segments)."""
+    import torch
+
+    from paper_2401_01607_b200.core import Signal
+    from paper_2401_01607_b200.engine import EngineConfig, ScatterEngine
+
+    rng = np.random.default_rng(45)
+    nb, every, nh = 256, 10, 4096
+    n = nb * every * 46
+    x = rng.uniform(-1, 1, n).astype(np.float32)
+    irs = [(rng.standard_normal(nh) * np.exp(-np.arange(nh) / 600)).astype(np.float32) for _ in range(46)]
+    eng = ScatterEngine(Signal(torch.from_numpy(irs[0]).cuda()), EngineConfig(block_size_nb=nb))
+    swaps = [(every * j, torch.from_numpy(irs[j]).cuda()) for j in range(1, 46)]
+    body = eng.process_stream(torch.from_numpy(x).cuda(), nb, swaps).cpu().numpy()
+    tail = eng.flush().samples.cpu().numpy()
+    ref_body, ref_tail = _oracle_stream(x, {every * j: irs[j] for j in range(46)}, nb)
+    tol = max(_tol(x, h) for h in irs)
+    assert np.max(np.abs(body - ref_body)) <= tol
+    assert len(tail) == len(ref_tail) and np.max(np.abs(tail - ref_tail)) <= tol
