@@ -554,7 +554,7 @@ def main():
         alg_bytes = 4 * (work.w.ne + work.w.nh + work.w.nout)
         gbs = alg_bytes / (ms_local * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
-                    "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                     "alg_bytes_per_launch": alg_bytes, "kernel": work.kernel}
     elif work.kernel == "k_tc_fir":
         # tensor work actually issued: 3 fp16 MMAs (hi*hi, lo*hi, hi*lo) over the
