@@ -281,7 +281,9 @@ int launch_chain_rf(int R, dim3 grid, cudaStream_t stream, const ChainArgs<T> &a
 // float chains are always fused (one instantiation); double picks per call
 template <typename T, int SKIP>
 int launch_chain_r(int R, dim3 grid, cudaStream_t stream, const ChainArgs<T> &a, bool fused) {
-    if (sizeof(T) == 8 && fused) return launch_chain_rf<T, SKIP, true>(R, grid, stream, a);
+    if constexpr (sizeof(T) == 8) {
+        if (fused) return launch_chain_rf<T, SKIP, true>(R, grid, stream, a);
+    }
     return launch_chain_rf<T, SKIP, false>(R, grid, stream, a);
 }
 
