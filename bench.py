@@ -259,12 +259,16 @@ class Work:
         FAST dispatch) and the padded tensor-core work it issues."""
         self.tc_padded_macs = 0
         if self.cfg.startswith("short"):
-            # FAST dispatch (capi.cu / k_fast_f32.cu): tensor cores from 256
-            # taps, the streaming k_fir_short up to 32 (HBM-bound), the smem
-            # k_fir_short_smem in between (FMA-bound)
+            # FAST dispatch (capi.cu / k_fast_f32.cu): tensor cores from 80
+            # taps at this size, the streaming k_fir_short up to 32
+            # (HBM-bound), the smem k_fir_short_smem in between (FMA-bound)
             nh = self.w.nh
-            self.kernel = "k_tc_fir" if nh >= 256 else ("k_fir_short" if nh <= 32 else "k_fir_short_smem")
-            self.hbm_bound = nh <= 32
+            use_tc = self.mode == "tc" or (self.mode in ("fast", "auto") and nh >= 80)
+            self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 32 else "k_fir_short_smem")
+            self.hbm_bound = nh <= 32 and not use_tc
+            if use_tc:
+                s8 = 2 if (nh + 126) // 128 + 1 <= 2 else -(-((nh + 126) // 128 + 1) // 8) * 8
+                self.tc_padded_macs = -(-self.w.nout // 16384) * 16384 * 128 * s8
             return
         if self.cfg == "cfg2":
             # float32 engine: FAST mode convolves the 19 equal IR segments in one

@@ -9,6 +9,7 @@ point raises immediately.
 from __future__ import annotations
 
 import ctypes
+import os
 import pathlib
 import threading
 
@@ -72,7 +73,9 @@ _lib = None
 
 
 def library_path() -> pathlib.Path:
-    return LIB_DIR / LIB_NAME
+    # SC_B200_LIB: an alternative build of the same library (A/B timing)
+    alt = os.environ.get("SC_B200_LIB")
+    return pathlib.Path(alt) if alt else LIB_DIR / LIB_NAME
 
 
 def load_library() -> ctypes.CDLL:

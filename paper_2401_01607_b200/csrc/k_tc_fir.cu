@@ -53,15 +53,21 @@ constexpr int KG = TR / 8;           // 16 K-groups of 8 fp16 (16 B)
 #endif
 constexpr int WP = SC_TC_WP;         // shifts per X window (window reloads stall the MMAs)
 constexpr int WROWS = TN + WP;       // rows per window (WROWS-1 used)
-constexpr int SSH = 8;               // shifts per H8 stage
-constexpr int SGROUPS = 2 * KG - 1 + KG * (SSH - 1);  // 143 groups per stage
 constexpr int NHSLOT = 2;            // H8 stage slots
 constexpr uint32_t XWIN_PART = WROWS * KG * 16;        // one X window, one part (64 KB at WP=128)
-constexpr uint32_t HST_PART = SGROUPS * 128;           // one H8 stage, one part (18304 B)
 constexpr uint32_t SM_XWIN = 0;
 constexpr uint32_t SM_HST = 2 * XWIN_PART;
-constexpr uint32_t SM_BAR = SM_HST + NHSLOT * 2 * HST_PART;  // 204288 B at WP=128
-constexpr uint32_t SM_TOTAL = SM_BAR + 128;
+
+// SSH = shifts per H8 stage = shifts per TMEM accumulator (drain period).
+// 8 for long filters; 2 when the filter needs at most two 128-tap shifts,
+// so short filters are not padded to 8 shifts.
+template <int SSH>
+struct TcStage {
+    static constexpr int SGROUPS = 2 * KG - 1 + KG * (SSH - 1);  // 143 groups per stage at SSH = 8
+    static constexpr uint32_t HST_PART = SGROUPS * 128;            // one H8 stage, one part (18304 B)
+    static constexpr uint32_t SM_BAR = SM_HST + NHSLOT * 2 * HST_PART;  // 204288 B at WP=128, SSH=8
+    static constexpr uint32_t SM_TOTAL = SM_BAR + 128;
+};
 constexpr int TC_THREADS = 192;
 constexpr uint32_t TMEM_COLS = 256;  // 2 accumulators x 128 fp32 columns
 
@@ -168,7 +174,10 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 
 // ---------------------------------------------------------------- main kernel
 
+template <int SSH>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
+    constexpr uint32_t HST_PART = TcStage<SSH>::HST_PART;
+    constexpr uint32_t SM_BAR = TcStage<SSH>::SM_BAR;
     extern __shared__ __align__(1024) uint8_t smem[];
     if (*a.nonfinite) return;  // block-uniform: the FFMA kernel handles this input
     const int warp = threadIdx.x >> 5;
@@ -222,12 +231,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
                 for (int64_t s0 = sb; s0 < se; s0 += WP) {
                     const int64_t s1 = s0 + WP < se ? s0 + WP : se;
                     if (xw > 0) mbar_wait(bar_xempty, (xw - 1) & 1);
-                    mbar_expect_tx(bar_xfull, 2 * XWIN_PART);
-                    const int64_t row_lo = i0 - s0 - WP - a.row_min;  // layout row of window row 0
+                    // only the rows the window's shifts read: [WP - n_sh + 1, WROWS),
+                    // rounded down to 8 rows (128 B) so the copies stay aligned
+                    const int n_sh = (int)(s1 - s0);
+                    const int r_first = ((WP - n_sh + 1) / 8) * 8;
+                    const uint32_t rbytes = (uint32_t)(WROWS - r_first) * 16;
+                    mbar_expect_tx(bar_xfull, 2 * KG * rbytes);
+                    const int64_t row_lo = i0 - s0 - WP - a.row_min + r_first;  // layout row of window row r_first
                     for (int p = 0; p < 2; ++p)
                         for (int j = 0; j < KG; ++j)
-                            bulk_g2s(sbase + SM_XWIN + p * XWIN_PART + j * (WROWS * 16),
-                                     (p ? xt1 : xt0) + ((int64_t)j * a.nrows + row_lo) * 8, WROWS * 16, bar_xfull);
+                            bulk_g2s(sbase + SM_XWIN + p * XWIN_PART + j * (WROWS * 16) + r_first * 16,
+                                     (p ? xt1 : xt0) + ((int64_t)j * a.nrows + row_lo) * 8, rbytes, bar_xfull);
                     ++xw;
                     for (int64_t sg = s0; sg < s1; sg += SSH) {
                         const uint32_t slot = hsc % NHSLOT;
@@ -539,6 +553,7 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     SC_REQUIRE(nh >= 1, "tc fir: empty impulse response");
     SC_REQUIRE(channels < 65536, "tc fir: too many channels");
     const int64_t s_needed = (nh + TR - 2) / TR + 1;
+    const int SSH = s_needed <= 2 ? 2 : 8;  // drain period: see TcStage
     const int64_t s8 = cdiv(s_needed, SSH) * SSH;
     const int64_t tiles_per_ch = cdiv(n_len, TTILE);
     const int64_t row_min = -((s8 + WP + 7) / 8) * 8;
@@ -583,7 +598,11 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     }
     // function attributes are per device (context): set on every launch so
     // multi-GPU drivers (one host thread per device) never miss it
-    SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_TOTAL));
+    const uint32_t sm_total = SSH == 2 ? TcStage<2>::SM_TOTAL : TcStage<8>::SM_TOTAL;
+    if (SSH == 2)
+        SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_total));
+    else
+        SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_total));
     TcArgs a;
     a.xt[0] = xt_hi;
     a.xt[1] = xt_lo;
@@ -633,7 +652,10 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
         if (err) return err;
     }
     const int grid = (int)std::min<int64_t>(a.n_units, sms);
-    k_tc_fir<<<grid, TC_THREADS, SM_TOTAL, stream>>>(a);
+    if (SSH == 2)
+        k_tc_fir<2><<<grid, TC_THREADS, sm_total, stream>>>(a);
+    else
+        k_tc_fir<8><<<grid, TC_THREADS, sm_total, stream>>>(a);
     SC_CHECK_LAUNCH();
     if (nsplit > 1) {
         dim3 g((unsigned)cdiv(n_len, 256), (unsigned)channels);

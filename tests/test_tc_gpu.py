@@ -24,7 +24,9 @@ def err_frac(y, ref, x, h):
 
 
 CASES = [(20_000, 256), (20_000, 1000), (16_384, 4096), (100_000, 9_000), (50_001, 20_003),
-         (3_000, 70_000), (300_000, 1_100), (1, 300), (1000, 8191), (40_000, 262_144)]
+         (3_000, 70_000), (300_000, 1_100), (1, 300), (1000, 8191), (40_000, 262_144),
+         # <= 2 shifts: the 2-shift drain variant (k_tc_fir<2>)
+         (50_001, 64), (20_000, 129), (7, 3), (33_333, 1), (70_000, 100)]
 
 
 @pytest.mark.parametrize("ne,nh", CASES)
