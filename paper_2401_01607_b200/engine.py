@@ -17,7 +17,7 @@ yields the identical stream (block-size invariance, engine.py:7-9).
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
