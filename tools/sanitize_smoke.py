@@ -106,6 +106,43 @@ def main():
         O.scatter_block(r2, h64[:30], blk, o2, 3, 5, 0.0)
     assert np.array_equal(ring, r2) and np.array_equal(out, o2)
     print("ok scatter_block", flush=True)
+    # tensor cores with the 2-shift drain (<= 2 shifts) and the short kernels
+    for nh in (3, 24, 100):
+        h = rng.standard_normal(nh).astype(np.float32)
+        for mode in (None, "tc"):
+            y = scatter_convolve(Signal(x), Signal(h), mode=mode).concatenated().samples
+            check(f"short nh={nh} mode={mode}", y, O.scatter_full(x, h), x, h)
+    # FAST fused stream through the batched tensor-core path (thresholds lowered)
+    from paper_2401_01607_b200.engine import ScatterEngine as _SE
+
+    hf = rng.standard_normal(300).astype(np.float32)
+    xf = rng.uniform(-1, 1, 256 * 40).astype(np.float32)
+    ef = _SE(Signal(torch.from_numpy(hf).cuda()), EngineConfig(block_size_nb=256), mode="fast")
+    bf = ef.process_stream(torch.from_numpy(xf).cuda(), 256, [(10 * j, torch.from_numpy(hf).cuda()) for j in (1, 2, 3)])
+    full = np.concatenate([bf.cpu().numpy(), ef.flush().samples.cpu().numpy()])
+    check("fast stream (ordered below threshold)", full, O.scatter_full(xf, hf), xf, hf)
+    # fixed point, WAV codecs, native sharded call
+    from paper_2401_01607_b200 import fixed_point as fx
+    from paper_2401_01607_b200.sharded import fir_sharded
+
+    e16, k16 = rng.uniform(-1, 1, 200), rng.uniform(-1, 1, 30)
+    for scheme in ("ideal", "mac"):
+        yq = fx.fixed_point_convolve(Signal(e16), Signal(k16), fx.FixedPointFormat(16), scheme).samples
+        assert np.array_equal(yq, O.fixed_convolve(e16, k16, 16, scheme))
+    print("ok fixed point", flush=True)
+    assert np.array_equal(fir_sharded(x64, h64, devices=[0, 0, 0]), O.scatter_full(x64, h64))
+    print("ok sharded", flush=True)
+    import tempfile
+
+    from paper_2401_01607_b200 import wav
+
+    with tempfile.TemporaryDirectory() as tmp:
+        for enc in wav.ENCODINGS:
+            path = pathlib.Path(tmp) / f"{enc}.wav"
+            wav.write_wav(path, [Signal(np.clip(x64[:500], -0.9, 0.9), 8000)], wav.WavSpec(8000, 1, enc))
+            back, spec = wav.read_wav(path)
+            assert spec.encoding == enc and len(back[0]) == 500
+    print("ok wav", flush=True)
     torch.cuda.synchronize()
     print("SANITIZE SMOKE PASSED", flush=True)
 
