@@ -166,12 +166,25 @@ struct FastSegs {
 // result, from the same pass over x).  The engine's test !(|x| > thr) is done
 // in float against keep = the smallest float above thr (|x| > thr  <=>
 // |x| >= keep for float x; NaN fails both), float4-wide when aligned.
+// Segment remap of the masked copy: block b of segment j (sm.m_lo[j] <=
+// b*nb) lands at sm.dst[j] + (b*nb - sm.m_lo[j]); sm.n == 0 keeps the layout.
+struct SegMap {
+    int n;
+    int64_t m_lo[kMaxSegs], dst[kMaxSegs];
+};
+
 __global__ void k_mask_skip(const float *__restrict__ x, int64_t ldx, int64_t n_total, int64_t nb, float keep,
                             float *__restrict__ xm, int64_t ldm, int64_t n_blocks, int64_t *__restrict__ J,
-                            bool vec4) {
+                            bool vec4, SegMap sm) {
     const int64_t b = blockIdx.x;
     const float *xc = x + blockIdx.y * ldx + b * nb;
-    float *mc = xm + blockIdx.y * ldm + b * nb;
+    int64_t dst = b * nb;
+    if (sm.n > 0) {
+        int j = 0;
+        while (j + 1 < sm.n && sm.m_lo[j + 1] <= b * nb) ++j;
+        dst = sm.dst[j] + (b * nb - sm.m_lo[j]);
+    }
+    float *mc = xm + blockIdx.y * ldm + dst;
     const int64_t n = n_total - b * nb < nb ? n_total - b * nb : nb;
     long long j = -1;
     int64_t i0 = 0;
@@ -208,6 +221,14 @@ __global__ void k_mask_skip(const float *__restrict__ x, int64_t ldx, int64_t n_
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) j = sj[w] > j ? sj[w] : j;
         J[blockIdx.y * n_blocks + b] = j;
     }
+}
+
+// zero [len_j, L) of every padded segment j of the masked copy (grid nseg x C)
+__global__ void k_zero_tails(float *__restrict__ xm, int64_t ldm, int64_t L, FastSegs sg) {
+    const int j = blockIdx.x;
+    const int64_t len = sg.m_hi[j] - sg.m_lo[j];
+    float *row = xm + blockIdx.y * ldm + (int64_t)j * L;
+    for (int64_t i = len + threadIdx.x; i < L; i += blockDim.x) row[i] = 0.0f;
 }
 
 // 4 consecutive slots per thread; segments that miss the 4 slots are skipped
@@ -520,20 +541,23 @@ struct DeviceGuard {
 
 // Fused back-to-back blocks (see sc_engine_process_blocks); x/out are
 // [C][ldx]/[C][ldo] rows of n_total samples.
-// Segments of one length L (the last may be shorter) and one IR length NH --
-// periodic swaps, the CLI's and cfg2's pattern -- are convolved in ONE
-// batched FIR launch: batch (channel c, segment j) reads the masked drive at
-// (c*S + j)*L (row pitch S*L, zero padded past the stream), its IR staged at
+// Segments sharing one IR length NH (periodic swaps -- the CLI's, cfg2's and
+// mstream's pattern) are convolved in ONE batched FIR launch: each segment is
+// padded with zeros to the longest length L, batch (channel c, segment j)
+// reads the masked drive at (c*S + j)*L (row pitch S*L), its IR staged at
 // (c*S + j)*NH and writes (c*S + j)*(L + NH - 1).
 bool uniform_segs(const ChainSeg *segs, int nseg, int64_t *L, int64_t *NH) {
-    *L = segs[0].m_hi - segs[0].m_lo;
+    // one IR length; segments padded to the longest, <= 25 % padding
     *NH = segs[0].nh;
-    if (nseg < 2) return false;
+    *L = 0;
+    int64_t total = 0;
     for (int j = 0; j < nseg; ++j) {
         const int64_t len = segs[j].m_hi - segs[j].m_lo;
-        if (segs[j].nh != *NH || (j < nseg - 1 ? len != *L : len > *L)) return false;
+        if (segs[j].nh != *NH) return false;
+        *L = len > *L ? len : *L;
+        total += len;
     }
-    return true;
+    return nseg >= 2 && 4 * (*L * nseg - total) <= total;
 }
 
 // FAST fused streams go to the FIR kernels when the work amortises their
@@ -583,14 +607,20 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
         // smallest float strictly above thr (thr >= 0): |x| > thr <=> |x| >= keep
         float keep = (float)e->thr;
         if ((double)keep <= e->thr) keep = nextafterf(keep, INFINITY);
+        SegMap sm{};
+        if (batched) {
+            sm.n = nseg;
+            for (int j = 0; j < nseg; ++j) sm.m_lo[j] = segs[j].m_lo, sm.dst[j] = j * L;
+        }
         const bool vec4 = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(xm)) & 15) == 0 &&
-                          ldx % 4 == 0 && xpitch % 4 == 0 && nb % 4 == 0;
+                          ldx % 4 == 0 && xpitch % 4 == 0 && nb % 4 == 0 && (!batched || L % 4 == 0);
         k_mask_skip<<<g, 256, 0, e->stream>>>(static_cast<const float *>(x), ldx, n_total, nb, keep, xm, xpitch,
-                                              n_blocks, e->jbuf, vec4);
+                                              n_blocks, e->jbuf, vec4, sm);
         SC_CHECK_LAUNCH();
-        if (xpitch > n_total)  // zero padding of the last (short) segment
-            SC_CHECK_CUDA(cudaMemset2DAsync(xm + n_total, (size_t)xpitch * 4, 0, (size_t)(xpitch - n_total) * 4,
-                                            (size_t)e->C, e->stream));
+        if (batched && xpitch > n_total) {  // zero padding of the shorter segments
+            k_zero_tails<<<dim3((unsigned)nseg, (unsigned)e->C), 256, 0, e->stream>>>(xm, xpitch, L, sg);
+            SC_CHECK_LAUNCH();
+        }
     }
     // NaN/Inf in x or h: launch_fir_f32's device-gated ordered fallback
     if (batched) {

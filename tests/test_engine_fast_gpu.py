@@ -227,3 +227,29 @@ def test_fast_many_swaps_chunked_calls():
     tol = max(_tol(x, h) for h in irs)
     assert np.max(np.abs(body - ref_body)) <= tol
     assert len(tail) == len(ref_tail) and np.max(np.abs(tail - ref_tail)) <= tol
+
+
+def test_unequal_segments_padded_batched_path():
+    """Segments of one IR length but different lengths (44, 46, 38 blocks):
+    padded to the longest and convolved in one batched launch."""
+    import torch
+
+    from paper_2401_01607_b200.engine import EngineConfig
+    from paper_2401_01607_b200.multichannel import MultiChannelEngine
+
+    rng = np.random.default_rng(52)
+    C, nb, nh = 2, 4096, 4096
+    n = nb * 128 - 1000
+    x = rng.uniform(-1, 1, (C, n)).astype(np.float32)
+    x[:, 5000:5100] = np.nan
+    irs = [(rng.standard_normal((C, nh)) * np.exp(-np.arange(nh) / 900)).astype(np.float32) for _ in range(3)]
+    eng = MultiChannelEngine(torch.from_numpy(irs[0]).cuda(), EngineConfig(block_size_nb=nb, zero_skip_threshold=0.02))
+    swaps = [(44, torch.from_numpy(irs[1]).cuda()), (90, torch.from_numpy(irs[2]).cuda())]
+    body = eng.process_stream(torch.from_numpy(x).cuda(), nb, swaps).cpu().numpy()
+    tails = eng.flush()
+    for c in range(C):
+        ref_body, ref_tail = _oracle_stream(x[c], {0: irs[0][c], 44: irs[1][c], 90: irs[2][c]}, nb, 0.02)
+        xc = np.nan_to_num(x[c])
+        tol = max(_tol(xc, ir[c]) for ir in irs)
+        assert np.max(np.abs(body[c] - ref_body)) <= tol, c
+        assert len(tails[c]) == len(ref_tail) and np.max(np.abs(tails[c] - ref_tail)) <= tol, c
