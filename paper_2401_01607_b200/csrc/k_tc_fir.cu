@@ -45,35 +45,41 @@ namespace sc {
 namespace {
 
 constexpr int TR = 128;              // phases per row (M) = taps per shift (K)
-constexpr int TN = 128;              // output rows per tile (N)
-constexpr int TTILE = TR * TN;       // 16384 outputs per tile
 constexpr int KG = TR / 8;           // 16 K-groups of 8 fp16 (16 B)
 #ifndef SC_TC_WP
 #define SC_TC_WP 128
 #endif
-constexpr int WP = SC_TC_WP;         // shifts per X window (window reloads stall the MMAs)
-constexpr int WROWS = TN + WP;       // rows per window (WROWS-1 used)
 constexpr int NHSLOT = 2;            // H8 stage slots
-constexpr uint32_t XWIN_PART = WROWS * KG * 16;        // one X window, one part (64 KB at WP=128)
+
+// Tile geometry, by N = output rows per tile (the UMMA N): 128 (4 epilogue
+// warps, 2 x 128 TMEM columns, 128-shift X windows) or 256 (8 epilogue
+// warps, all 512 TMEM columns, 48-shift windows so X + H8 fit in smem).
+template <int TNV>
+struct TcGeo {
+    static constexpr int TN = TNV;
+    static constexpr int TTILE = TR * TNV;                 // outputs per tile
+    static constexpr int WP = TNV == 128 ? SC_TC_WP : 48;  // shifts per X window
+    static constexpr int WROWS = TNV + WP;                 // rows per window (WROWS-1 used)
+    static constexpr uint32_t XWIN_PART = WROWS * KG * 16; // one X window, one part (64 KB at N=128)
+    static constexpr uint32_t SM_HST = 2 * XWIN_PART;
+    static constexpr int NEPI = TNV / 32;                  // epilogue warps
+    static constexpr int THREADS = 64 + 32 * NEPI;         // + producer and MMA warps
+    static constexpr uint32_t TMEM_COLS = 2 * TNV;         // 2 accumulators x N fp32 columns
+    // idesc: F32 accumulate (bit 4), A/B F16, K-major, N (>>3 at bit 17), M = 128 (>>4 at bit 24)
+    static constexpr uint32_t IDESC = (1u << 4) | ((TNV >> 3) << 17) | ((TR >> 4) << 24);
+};
 constexpr uint32_t SM_XWIN = 0;
-constexpr uint32_t SM_HST = 2 * XWIN_PART;
 
 // SSH = shifts per H8 stage = shifts per TMEM accumulator (drain period).
 // 8 for long filters; 2 when the filter needs at most two 128-tap shifts,
 // so short filters are not padded to 8 shifts.
-template <int SSH>
+template <int SSH, int TNV>
 struct TcStage {
     static constexpr int SGROUPS = 2 * KG - 1 + KG * (SSH - 1);  // 143 groups per stage at SSH = 8
     static constexpr uint32_t HST_PART = SGROUPS * 128;            // one H8 stage, one part (18304 B)
-    static constexpr uint32_t SM_BAR = SM_HST + NHSLOT * 2 * HST_PART;  // 204288 B at WP=128, SSH=8
+    static constexpr uint32_t SM_BAR = TcGeo<TNV>::SM_HST + NHSLOT * 2 * HST_PART;  // 204288 B at N=128, SSH=8
     static constexpr uint32_t SM_TOTAL = SM_BAR + 128;
 };
-constexpr int TC_THREADS = 192;
-constexpr uint32_t TMEM_COLS = 256;  // 2 accumulators x 128 fp32 columns
-
-// idesc: F32 accumulate (bit 4), A/B F16, K-major, N = 128 (>>3 at bit 17),
-// M = 128 (>>4 at bit 24).
-constexpr uint32_t IDESC = (1u << 4) | ((TN >> 3) << 17) | ((TR >> 4) << 24);
 
 struct TcArgs {
     const __half *xt[2];   // X in [ch][j][row][8] layout, hi / lo
@@ -139,12 +145,12 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
            ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
-__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(IDESC), "r"(accumulate));
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
@@ -174,10 +180,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 
 // ---------------------------------------------------------------- main kernel
 
-template <int SSH>
-__global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
-    constexpr uint32_t HST_PART = TcStage<SSH>::HST_PART;
-    constexpr uint32_t SM_BAR = TcStage<SSH>::SM_BAR;
+template <int SSH, int TNV>
+__global__ void __launch_bounds__(TcGeo<TNV>::THREADS, 1) k_tc_fir(TcArgs a) {
+    using G = TcGeo<TNV>;
+    constexpr int TN = G::TN, WP = G::WP, WROWS = G::WROWS, NEPI = G::NEPI;
+    constexpr uint32_t XWIN_PART = G::XWIN_PART, SM_HST = G::SM_HST, TMEM_COLS = G::TMEM_COLS, IDESC = G::IDESC;
+    constexpr int64_t TTILE = G::TTILE;
+    constexpr uint32_t HST_PART = TcStage<SSH, TNV>::HST_PART;
+    constexpr uint32_t SM_BAR = TcStage<SSH, TNV>::SM_BAR;
     extern __shared__ __align__(1024) uint8_t smem[];
     if (*a.nonfinite) return;  // block-uniform: the FFMA kernel handles this input
     const int warp = threadIdx.x >> 5;
@@ -200,7 +210,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(bar_tfull + 8 * i, 1);
-            mbar_init(bar_tempty + 8 * i, 4);
+            mbar_init(bar_tempty + 8 * i, NEPI);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -299,10 +309,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
                                 const uint64_t al = sdesc(a_lo + kk * 256, 128, 128);
                                 const uint64_t bh = sdesc(b_hi + kk * 2 * (WROWS * 16), WROWS * 16, 128);
                                 const uint64_t bl = sdesc(b_lo + kk * 2 * (WROWS * 16), WROWS * 16, 128);
-                                umma_f16(d_tmem, ah, bh, accumulate);
+                                umma_f16(d_tmem, ah, bh, IDESC, accumulate);
                                 accumulate = 1;
-                                umma_f16(d_tmem, al, bh, 1);
-                                umma_f16(d_tmem, ah, bl, 1);
+                                umma_f16(d_tmem, al, bh, IDESC, 1);
+                                umma_f16(d_tmem, ah, bl, IDESC, 1);
                             }
                         }
                         umma_commit(bar_hempty + 8 * slot);
@@ -316,6 +326,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
     } else {
         // ---------------------------------------------------------------- epilogue
         const int q = warp & 3;                // TMEM lane quarter of this warp
+        const int half = (warp - 2) >> 2;      // which 128-column half of the N columns
         const int rp = q * 32 + lane;          // phase index r' = 127 - r
         uint32_t dc = 0;
         for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
@@ -330,19 +341,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
             // k_tc_split_reduce sums them in fixed split order (deterministic)
             float *yc = a.nsplit == 1 ? a.y + ch * a.ldy
                                       : a.ws + (sp * a.channels + ch) * (a.n_end - a.n_begin);
-            // this thread's 128 outputs (one phase r', all 128 rows), summed
-            // over the stage partials in FP32 round-to-nearest
-            float sum[TN];
+            // this thread's 128 outputs (one phase r', rows 128*half ..
+            // 128*half+127), summed over the stage partials in FP32
+            // round-to-nearest
+            float sum[128];
 #pragma unroll
-            for (int i = 0; i < TN; ++i) sum[i] = 0.0f;
+            for (int i = 0; i < 128; ++i) sum[i] = 0.0f;
 #pragma unroll 1
             for (int64_t st = 0; st < n_stages; ++st, ++dc) {
                 const uint32_t acc = dc & 1;
                 mbar_wait(bar_tfull + 8 * acc, (dc >> 1) & 1);
                 tc_fence_after();
-                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * TN;
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * TN + half * 128;
 #pragma unroll
-                for (int c = 0; c < TN; c += 32) {
+                for (int c = 0; c < 128; c += 32) {
                     float v[32];
                     tmem_ld32(taddr + c, v);
 #pragma unroll
@@ -352,9 +364,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_fir(TcArgs a) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
             }
-            const int64_t nb = a.n_begin + (tile - ch * a.tiles_per_ch) * (int64_t)TTILE + (TR - 1 - rp);
+            const int64_t nb = a.n_begin + (tile - ch * a.tiles_per_ch) * TTILE + (int64_t)half * 128 * TR + (TR - 1 - rp);
 #pragma unroll
-            for (int i = 0; i < TN; ++i) {
+            for (int i = 0; i < 128; ++i) {
                 const int64_t n = nb + (int64_t)i * TR;
                 if (n < a.n_end) yc[n - a.n_begin] = sum[i] * inv;
             }
@@ -554,6 +566,18 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     SC_REQUIRE(channels < 65536, "tc fir: too many channels");
     const int64_t s_needed = (nh + TR - 2) / TR + 1;
     const int SSH = s_needed <= 2 ? 2 : 8;  // drain period: see TcStage
+    // 256 output rows per tile when there are enough such tiles to fill the
+    // SMs twice (measured +2 % on cfg5, +2.7 % on cfg4 over 128: half the
+    // A-operand reads per FLOP); small launches keep 128-row tiles (cfg2's
+    // 19 segments: 0.18 ms vs 0.22 ms).  SC_TC_N=128|256 forces one.
+    static const int tnv_env = [] {
+        const char *v = getenv("SC_TC_N");
+        return v ? atoi(v) : 0;
+    }();
+    const int64_t wide_tiles = cdiv(n_len, (int64_t)TR * 256) * channels;
+    const int TNV = tnv_env == 128 ? 128 : tnv_env == 256 ? 256 : (wide_tiles >= 2 * sm_count() ? 256 : 128);
+    const int64_t TN = TNV, TTILE = (int64_t)TR * TNV;
+    const int WP = TNV == 256 ? TcGeo<256>::WP : TcGeo<128>::WP;
     const int64_t s8 = cdiv(s_needed, SSH) * SSH;
     const int64_t tiles_per_ch = cdiv(n_len, TTILE);
     const int64_t row_min = -((s8 + WP + 7) / 8) * 8;
@@ -598,11 +622,14 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     }
     // function attributes are per device (context): set on every launch so
     // multi-GPU drivers (one host thread per device) never miss it
-    const uint32_t sm_total = SSH == 2 ? TcStage<2>::SM_TOTAL : TcStage<8>::SM_TOTAL;
-    if (SSH == 2)
-        SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_total));
-    else
-        SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_total));
+#define SC_TC_ATTR(S, N) \
+    SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir<S, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                       TcStage<S, N>::SM_TOTAL))
+    if (SSH == 2 && TNV == 128) SC_TC_ATTR(2, 128);
+    else if (SSH == 2) SC_TC_ATTR(2, 256);
+    else if (TNV == 128) SC_TC_ATTR(8, 128);
+    else SC_TC_ATTR(8, 256);
+#undef SC_TC_ATTR
     TcArgs a;
     a.xt[0] = xt_hi;
     a.xt[1] = xt_lo;
@@ -652,10 +679,12 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
         if (err) return err;
     }
     const int grid = (int)std::min<int64_t>(a.n_units, sms);
-    if (SSH == 2)
-        k_tc_fir<2><<<grid, TC_THREADS, sm_total, stream>>>(a);
-    else
-        k_tc_fir<8><<<grid, TC_THREADS, sm_total, stream>>>(a);
+#define SC_TC_LAUNCH(S, N) k_tc_fir<S, N><<<grid, TcGeo<N>::THREADS, TcStage<S, N>::SM_TOTAL, stream>>>(a)
+    if (SSH == 2 && TNV == 128) SC_TC_LAUNCH(2, 128);
+    else if (SSH == 2) SC_TC_LAUNCH(2, 256);
+    else if (TNV == 128) SC_TC_LAUNCH(8, 128);
+    else SC_TC_LAUNCH(8, 256);
+#undef SC_TC_LAUNCH
     SC_CHECK_LAUNCH();
     if (nsplit > 1) {
         dim3 g((unsigned)cdiv(n_len, 256), (unsigned)channels);
