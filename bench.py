@@ -254,6 +254,18 @@ class Work:
             self.scaling = "weak"
             self.dtype = "f32"
 
+    @staticmethod
+    def tc_padded(n_lens, channels, nh, sms=148):
+        """Padded MMA MACs of one k_tc_fir launch over batches of output
+        lengths n_lens (x channels), mirroring the library's tile choice
+        (256-row tiles when they fill the SMs twice, else 128) and drain
+        period (2 shifts for <= 2-shift filters, else 8)."""
+        s_needed = (nh + 126) // 128 + 1
+        s8 = 2 if s_needed <= 2 else -(-s_needed // 8) * 8
+        wide = sum(-(-n // 32768) for n in n_lens) * channels >= 2 * sms
+        tile = 32768 if wide else 16384
+        return sum(-(-n // tile) for n in n_lens) * channels * tile * 128 * s8
+
     def pick_kernel(self):
         """Which kernel the library runs for this config/mode (mirrors capi.cu's
         FAST dispatch) and the padded tensor-core work it issues."""
@@ -267,8 +279,7 @@ class Work:
             self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 32 else "k_fir_short_smem")
             self.hbm_bound = nh <= 32 and not use_tc
             if use_tc:
-                s8 = 2 if (nh + 126) // 128 + 1 <= 2 else -(-((nh + 126) // 128 + 1) // 8) * 8
-                self.tc_padded_macs = -(-self.w.nout // 16384) * 16384 * 128 * s8
+                self.tc_padded_macs = self.tc_padded([self.w.nout], 1, nh)
             return
         if self.cfg == "cfg2":
             # float32 engine: FAST mode convolves the 19 equal IR segments in one
@@ -278,9 +289,8 @@ class Work:
             self.kernel = "k_tc_fir" if fast else "k_chain_w"
             if fast:
                 nh, seg = self.w.nh, 100 * 256
-                s8 = -(-((nh + 126) // 128 + 1) // 8) * 8
                 nseg = -(-self.w.ne // seg)
-                self.tc_padded_macs = nseg * (-(-(seg + nh - 1) // 16384)) * 16384 * 128 * s8
+                self.tc_padded_macs = self.tc_padded([seg + nh - 1] * nseg, 1, nh)
             return
         if self.cfg == "mstream":
             # float32 engine: FAST mode puts each IR segment (2 x 64 ch x 240,000
@@ -291,11 +301,10 @@ class Work:
             self.kernel = "k_tc_fir" if fast else "k_chain_w"
             if fast:
                 nh = self.w.nh
-                s8 = -(-((nh + 126) // 128 + 1) // 8) * 8
                 half = (-(-self.w.ne // 8192) // 2) * 8192
                 segs = [half, self.w.ne - half]
-                tiles = sum(-(-(n + nh - 1) // 16384) for n in segs) * self.w.channels
-                self.tc_padded_macs = tiles * 16384 * 128 * s8
+                # the two segments are padded to the longer one and batched
+                self.tc_padded_macs = self.tc_padded([max(segs) + nh - 1] * 2, self.w.channels, nh)
             return
         if self.dtype != "f32" or self.cfg not in ("cfg3", "cfg4", "cfg5") or self.mode == "ordered":
             self.kernel = "k_chain_w"   # ordered chain (csrc/k_ordered.cu)
@@ -305,13 +314,10 @@ class Work:
         self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 32 else
                                                  "k_fir_short_smem" if nh <= 256 else "k_fir_f32_fast")
         if use_tc:
-            s = (nh + 126) // 128 + 1
-            s8 = -(-s // 8) * 8
             if self.cfg == "cfg4":
-                tiles = -(-self.w.nout // 16384) * (self.c1 - self.c0)
+                self.tc_padded_macs = self.tc_padded([self.w.nout], self.c1 - self.c0, nh)
             else:
-                tiles = -(-self.shard.n_out // 16384)
-            self.tc_padded_macs = tiles * 16384 * 128 * s8
+                self.tc_padded_macs = self.tc_padded([self.shard.n_out], 1, nh)
 
     def step(self):
         import torch
@@ -562,7 +568,7 @@ def main():
                     "alg_bytes_per_launch": alg_bytes, "kernel": work.kernel}
     elif work.kernel == "k_tc_fir":
         # tensor work actually issued: 3 fp16 MMAs (hi*hi, lo*hi, hi*lo) over the
-        # padded block-Toeplitz GEMM (whole 16384-output tiles x 128 taps x s8 shifts)
+        # padded block-Toeplitz GEMM (whole 32768- or 16384-output tiles x 128 taps x s8 shifts)
         tc_peak = float(p.get("bf16_tflops", 1590.0))
         achieved = 2 * 3 * work.tc_padded_macs / (ms_local * 1e-3) / 1e12
         roofline = {
