@@ -566,19 +566,21 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     SC_REQUIRE(channels < 65536, "tc fir: too many channels");
     const int64_t s_needed = (nh + TR - 2) / TR + 1;
     const int SSH = s_needed <= 2 ? 2 : 8;  // drain period: see TcStage
-    // 256 output rows per tile when there are enough such tiles to fill the
-    // SMs twice (measured +2 % on cfg5, +2.7 % on cfg4 over 128: half the
-    // A-operand reads per FLOP); small launches keep 128-row tiles (cfg2's
-    // 19 segments: 0.18 ms vs 0.22 ms).  SC_TC_N=128|256 forces one.
+    const int64_t s8 = cdiv(s_needed, SSH) * SSH;
+    // 256 output rows per tile (measured +2 % on cfg5, +2.7 % on cfg4, +3 %
+    // on cfg3 end to end over 128: half the A-operand reads per FLOP) unless
+    // the launch is too small to fill the SMs with 256-row work units (tiles
+    // x shift-range splits of >= 48 shifts): cfg2's 19 short segments keep
+    // 128-row tiles (0.18 ms vs 0.22 ms).  SC_TC_N=128|256 forces one.
     static const int tnv_env = [] {
         const char *v = getenv("SC_TC_N");
         return v ? atoi(v) : 0;
     }();
-    const int64_t wide_tiles = cdiv(n_len, (int64_t)TR * 256) * channels;
-    const int TNV = tnv_env == 128 ? 128 : tnv_env == 256 ? 256 : (wide_tiles >= 2 * sm_count() ? 256 : 128);
+    const int64_t wide_units = cdiv(n_len, (int64_t)TR * 256) * channels *
+                               std::max<int64_t>(1, s8 / TcGeo<256>::WP);
+    const int TNV = tnv_env == 128 ? 128 : tnv_env == 256 ? 256 : (wide_units >= sm_count() ? 256 : 128);
     const int64_t TN = TNV, TTILE = (int64_t)TR * TNV;
     const int WP = TNV == 256 ? TcGeo<256>::WP : TcGeo<128>::WP;
-    const int64_t s8 = cdiv(s_needed, SSH) * SSH;
     const int64_t tiles_per_ch = cdiv(n_len, TTILE);
     const int64_t row_min = -((s8 + WP + 7) / 8) * 8;
     const int64_t nrows = tiles_per_ch * TN - row_min;
