@@ -52,16 +52,12 @@ constexpr int KG = TR / 8;           // 16 K-groups of 8 fp16 (16 B)
 constexpr int NHSLOT = 2;            // H8 stage slots
 
 // Tile geometry, by N = output rows per tile (the UMMA N): 128 (4 epilogue
-// warps, 2 x 128 TMEM columns, 128-shift X windows) or 256 (8 epilogue
-// warps, all 512 TMEM columns, 48-shift windows so X + H8 fit in smem).
+// warps, 2 x 128 TMEM columns) or 256 (8 epilogue warps, all 512 TMEM
+// columns).
 template <int TNV>
 struct TcGeo {
     static constexpr int TN = TNV;
     static constexpr int TTILE = TR * TNV;                 // outputs per tile
-    static constexpr int WP = TNV == 128 ? SC_TC_WP : 48;  // shifts per X window
-    static constexpr int WROWS = TNV + WP;                 // rows per window (WROWS-1 used)
-    static constexpr uint32_t XWIN_PART = WROWS * KG * 16; // one X window, one part (64 KB at N=128)
-    static constexpr uint32_t SM_HST = 2 * XWIN_PART;
     static constexpr int NEPI = TNV / 32;                  // epilogue warps
     static constexpr int THREADS = 64 + 32 * NEPI;         // + producer and MMA warps
     static constexpr uint32_t TMEM_COLS = 2 * TNV;         // 2 accumulators x N fp32 columns
@@ -69,16 +65,26 @@ struct TcGeo {
     static constexpr uint32_t IDESC = (1u << 4) | ((TNV >> 3) << 17) | ((TR >> 4) << 24);
 };
 constexpr uint32_t SM_XWIN = 0;
+constexpr uint32_t SMEM_MAX = 232448;  // dynamic smem per CTA on sm_100
 
-// SSH = shifts per H8 stage = shifts per TMEM accumulator (drain period).
-// 8 for long filters; 2 when the filter needs at most two 128-tap shifts,
-// so short filters are not padded to 8 shifts.
+// Per (SSH, N): SSH = shifts per H8 stage = shifts per TMEM accumulator
+// (drain period; 8 for long filters at N = 128, 4 at N = 256, 2 for filters
+// of at most two 128-tap shifts), and the X window: the most shifts WP (<=
+// 128, a multiple of 8) whose window of N + WP rows fits beside two H8
+// stages.
 template <int SSH, int TNV>
 struct TcStage {
     static constexpr int SGROUPS = 2 * KG - 1 + KG * (SSH - 1);  // 143 groups per stage at SSH = 8
     static constexpr uint32_t HST_PART = SGROUPS * 128;            // one H8 stage, one part (18304 B)
-    static constexpr uint32_t SM_BAR = TcGeo<TNV>::SM_HST + NHSLOT * 2 * HST_PART;  // 204288 B at N=128, SSH=8
+    static constexpr int WP_FIT = (int)((SMEM_MAX - 128 - NHSLOT * 2 * HST_PART) / (2 * KG * 16)) - TNV;
+    static constexpr int WP = (WP_FIT < SC_TC_WP ? WP_FIT : SC_TC_WP) / 8 * 8;  // shifts per X window
+    static constexpr int WROWS = TNV + WP;                         // rows per window (WROWS-1 used)
+    static constexpr uint32_t XWIN_PART = WROWS * KG * 16;         // one X window, one part
+    static constexpr uint32_t SM_HST = 2 * XWIN_PART;
+    static constexpr uint32_t SM_BAR = SM_HST + NHSLOT * 2 * HST_PART;  // 204288 B at N=128, SSH=8
     static constexpr uint32_t SM_TOTAL = SM_BAR + 128;
+    static_assert(WP >= 8 && WP % SSH == 0, "X window too small");
+    static_assert(SM_TOTAL <= SMEM_MAX, "smem");
 };
 
 struct TcArgs {
@@ -183,11 +189,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 template <int SSH, int TNV>
 __global__ void __launch_bounds__(TcGeo<TNV>::THREADS, 1) k_tc_fir(TcArgs a) {
     using G = TcGeo<TNV>;
-    constexpr int TN = G::TN, WP = G::WP, WROWS = G::WROWS, NEPI = G::NEPI;
-    constexpr uint32_t XWIN_PART = G::XWIN_PART, SM_HST = G::SM_HST, TMEM_COLS = G::TMEM_COLS, IDESC = G::IDESC;
+    using S = TcStage<SSH, TNV>;
+    constexpr int TN = G::TN, WP = S::WP, WROWS = S::WROWS, NEPI = G::NEPI;
+    constexpr uint32_t XWIN_PART = S::XWIN_PART, SM_HST = S::SM_HST, TMEM_COLS = G::TMEM_COLS, IDESC = G::IDESC;
     constexpr int64_t TTILE = G::TTILE;
-    constexpr uint32_t HST_PART = TcStage<SSH, TNV>::HST_PART;
-    constexpr uint32_t SM_BAR = TcStage<SSH, TNV>::SM_BAR;
+    constexpr uint32_t HST_PART = S::HST_PART;
+    constexpr uint32_t SM_BAR = S::SM_BAR;
     extern __shared__ __align__(1024) uint8_t smem[];
     if (*a.nonfinite) return;  // block-uniform: the FFMA kernel handles this input
     const int warp = threadIdx.x >> 5;
@@ -565,8 +572,10 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     SC_REQUIRE(nh >= 1, "tc fir: empty impulse response");
     SC_REQUIRE(channels < 65536, "tc fir: too many channels");
     const int64_t s_needed = (nh + TR - 2) / TR + 1;
-    const int SSH = s_needed <= 2 ? 2 : 8;  // drain period: see TcStage
-    const int64_t s8 = cdiv(s_needed, SSH) * SSH;
+    static const int wide_ssh = [] {
+        const char *v = getenv("SC_TC_WIDE_SSH");  // experiment knob: 4 or 8
+        return v && atoi(v) == 8 ? 8 : 4;
+    }();
     // 256 output rows per tile (measured +2 % on cfg5, +2.7 % on cfg4, +3 %
     // on cfg3 end to end over 128: half the A-operand reads per FLOP) unless
     // the launch is too small to fill the SMs with 256-row work units (tiles
@@ -576,11 +585,16 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
         const char *v = getenv("SC_TC_N");
         return v ? atoi(v) : 0;
     }();
-    const int64_t wide_units = cdiv(n_len, (int64_t)TR * 256) * channels *
-                               std::max<int64_t>(1, s8 / TcGeo<256>::WP);
+    const int ssh_wide = s_needed <= 2 ? 2 : wide_ssh;
+    const int wp_wide = ssh_wide == 2 ? TcStage<2, 256>::WP : ssh_wide == 4 ? TcStage<4, 256>::WP : TcStage<8, 256>::WP;
+    const int64_t s8_wide = cdiv(s_needed, ssh_wide) * ssh_wide;
+    const int64_t wide_units = cdiv(n_len, (int64_t)TR * 256) * channels * std::max<int64_t>(1, s8_wide / wp_wide);
     const int TNV = tnv_env == 128 ? 128 : tnv_env == 256 ? 256 : (wide_units >= sm_count() ? 256 : 128);
+    const int SSH = TNV == 256 ? ssh_wide : (s_needed <= 2 ? 2 : 8);  // drain period: see TcStage
+    const int64_t s8 = cdiv(s_needed, SSH) * SSH;
     const int64_t TN = TNV, TTILE = (int64_t)TR * TNV;
-    const int WP = TNV == 256 ? TcGeo<256>::WP : TcGeo<128>::WP;
+    const int WP = TNV == 128 ? (SSH == 2 ? TcStage<2, 128>::WP : TcStage<8, 128>::WP)
+                              : (SSH == 2 ? TcStage<2, 256>::WP : SSH == 4 ? TcStage<4, 256>::WP : TcStage<8, 256>::WP);
     const int64_t tiles_per_ch = cdiv(n_len, TTILE);
     const int64_t row_min = -((s8 + WP + 7) / 8) * 8;
     const int64_t nrows = tiles_per_ch * TN - row_min;
@@ -627,9 +641,10 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
 #define SC_TC_ATTR(S, N) \
     SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir<S, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                        TcStage<S, N>::SM_TOTAL))
-    if (SSH == 2 && TNV == 128) SC_TC_ATTR(2, 128);
-    else if (SSH == 2) SC_TC_ATTR(2, 256);
+    if (TNV == 128 && SSH == 2) SC_TC_ATTR(2, 128);
     else if (TNV == 128) SC_TC_ATTR(8, 128);
+    else if (SSH == 2) SC_TC_ATTR(2, 256);
+    else if (SSH == 4) SC_TC_ATTR(4, 256);
     else SC_TC_ATTR(8, 256);
 #undef SC_TC_ATTR
     TcArgs a;
@@ -682,9 +697,10 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     }
     const int grid = (int)std::min<int64_t>(a.n_units, sms);
 #define SC_TC_LAUNCH(S, N) k_tc_fir<S, N><<<grid, TcGeo<N>::THREADS, TcStage<S, N>::SM_TOTAL, stream>>>(a)
-    if (SSH == 2 && TNV == 128) SC_TC_LAUNCH(2, 128);
-    else if (SSH == 2) SC_TC_LAUNCH(2, 256);
+    if (TNV == 128 && SSH == 2) SC_TC_LAUNCH(2, 128);
     else if (TNV == 128) SC_TC_LAUNCH(8, 128);
+    else if (SSH == 2) SC_TC_LAUNCH(2, 256);
+    else if (SSH == 4) SC_TC_LAUNCH(4, 256);
     else SC_TC_LAUNCH(8, 256);
 #undef SC_TC_LAUNCH
     SC_CHECK_LAUNCH();
