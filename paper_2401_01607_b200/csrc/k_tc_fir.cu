@@ -573,8 +573,9 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     SC_REQUIRE(channels < 65536, "tc fir: too many channels");
     const int64_t s_needed = (nh + TR - 2) / TR + 1;
     static const int wide_ssh = [] {
-        const char *v = getenv("SC_TC_WIDE_SSH");  // experiment knob: 4 or 8
-        return v && atoi(v) == 8 ? 8 : 4;
+        const char *v = getenv("SC_TC_WIDE_SSH");  // experiment knob: 2, 4 or 8
+        const int k = v ? atoi(v) : 4;
+        return k == 2 || k == 8 ? k : 4;
     }();
     // 256 output rows per tile (measured +2 % on cfg5, +2.7 % on cfg4, +3 %
     // on cfg3 end to end over 128: half the A-operand reads per FLOP) unless
