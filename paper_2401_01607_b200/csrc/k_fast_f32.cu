@@ -130,6 +130,9 @@ __global__ void __launch_bounds__(FT_THREADS, 2) k_fir_f32_fast(FastArgs a) {
             pre_slot = ring_slot(g) * FT_GSTRIDE + (w & 15);
         }
 
+        // ring slots of groups j - c and j - c + 1, stepped down per chunk
+        // (no 64-bit modulo in the inner loop)
+        int sA = ring_slot(j - c0), sB = ring_slot(j - c0 + 1);
 #pragma unroll 1
         for (int cc = 0; cc < FT_CPS; ++cc) {
             const int64_t c = c0 + cc;
@@ -141,8 +144,10 @@ __global__ void __launch_bounds__(FT_THREADS, 2) k_fir_f32_fast(FastArgs a) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) hn[i] = __ldg(h4 + i);
             }
-            const float4 *gA = reinterpret_cast<const float4 *>(ring + ring_slot(j - c) * FT_GSTRIDE);
-            const float4 *gB = reinterpret_cast<const float4 *>(ring + ring_slot(j - c + 1) * FT_GSTRIDE);
+            const float4 *gA = reinterpret_cast<const float4 *>(ring + sA * FT_GSTRIDE);
+            const float4 *gB = reinterpret_cast<const float4 *>(ring + sB * FT_GSTRIDE);
+            sB = sA;
+            sA = sA == 0 ? FT_NG - 1 : sA - 1;
             float2 W[2 * FT_PAIRS];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
