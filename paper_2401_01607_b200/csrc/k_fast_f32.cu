@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(FT_THREADS, 2) k_fir_f32_fast(FastArgs a) {
         // ring slots of groups j - c and j - c + 1, stepped down per chunk
         // (no 64-bit modulo in the inner loop)
         int sA = ring_slot(j - c0), sB = ring_slot(j - c0 + 1);
-#pragma unroll 1
+#pragma unroll 2  // (full unrolling spills at the 128-register cap)
         for (int cc = 0; cc < FT_CPS; ++cc) {
             const int64_t c = c0 + cc;
             // next chunk's taps (padded array: always in bounds up to nh_pad)
