@@ -47,15 +47,16 @@ struct ChainArgs {
 };
 
 // ---------------------------------------------------------------- windowed chain
-// One kernel for every ordered launch.  A CTA of 128 threads owns a tile of
-// 128*R consecutive outputs, thread j the R consecutive outputs tj..tj+R-1
-// (R = 8, 4, 2 or 1, picked per launch so the grid keeps every SM sub-
-// partition busy).  Drive samples go through shared memory in chunks of 128
-// (one per thread), the taps of the chunk x tile in a padded stage (see
-// cw_pos: the stride-R reads of a warp hit distinct banks).  Per 8-sample "u-block" a thread keeps a register
+// One kernel for every ordered launch.  A CTA of TB threads (32 or 128) owns
+// a tile of TB*R consecutive outputs, thread j the R consecutive outputs
+// tj..tj+R-1 (R = 8, 4, 2 or 1, picked per launch so the grid keeps every SM
+// sub-partition busy).  Drive samples go through shared memory in chunks of
+// 128, the taps of the chunk x tile in a padded stage (TapStage: conflict-
+// free 16-byte tap loads).  Per 8-sample "u-block" a thread keeps a register
 // window of R+7 taps; sliding to the next u-block reuses R-1 of them, so a
-// u-block costs 8 tap loads and two (float) / four (double) broadcast
-// vector loads of the drive for 8R MACs.  Interior chunks of a dense drive
+// u-block costs 8 taps (two float / four double 16-byte loads for R >= 4)
+// and two (float) / four (double) broadcast vector loads of the drive for
+// 8R MACs.  Interior chunks of a dense drive
 // (every (output, sample) pair valid, nothing skipped) run a fully unrolled
 // path with no tests; edge u-blocks test validity per thread and only the
 // u-blocks that straddle an edge pay per-MAC predicates.  The next chunk's
@@ -66,23 +67,53 @@ constexpr int CW_U = 8;     // samples per u-block
 constexpr int CW_WIDE = CW_MC < 128 ? CW_MC : 128;  // the wide-CTA variant (SC_CHAIN_TB=128)
 static_assert(32 % CW_U == 0, "a u-block's scatter bits sit in one mask word");
 
-// Tap stage layout: one pad element after every R taps (none for R = 1).
-// Lane l of a warp reads stage index l*R + c, i.e. padded word offset
-// (R+1)*l*(es/4) + ..., which lands on distinct banks for R = 2, 4, 8 (odd
-// strides 3, 5, 9 words for float; for double, 6, 10, 18 words across a
-// half-warp).  Because the thread's base index l*R is a multiple of R, the
-// padded address splits into a per-thread base (R+1)*l plus cw_pos(c) of the
-// compile-time (or 8-aligned) offset c: every tap load is [reg + imm].
-template <int R>
-__host__ __device__ constexpr int cw_pos(int i) {
-    return R == 1 ? i : i + i / R;
-}
+// Tap stage layout: the taps sit in groups of R (the stride between two
+// threads' bases) padded to S elements.  Lane l's base is group l, so every
+// tap address is a per-thread base S*l plus the compile-time (or 8-aligned)
+// offset pos(c): [reg + imm] loads.  For R = 8 and 4 the strides (float 12 /
+// 4, double 10 / 6 elements) are multiples of 16 bytes and put the 8 lanes of
+// each 16-byte-load phase on distinct banks, so a thread reads its 8 new taps
+// per u-block with two (float) or four (double) conflict-free LDS.128.  R = 2
+// and 1 keep scalar loads with odd strides (3 and 1).
+template <typename T, int R>
+struct TapStage {
+    static constexpr int S = R == 8 ? (sizeof(T) == 4 ? 12 : 10) : R == 4 ? (sizeof(T) == 4 ? 4 : 6) : R == 2 ? 3 : 1;
+    static constexpr bool VEC = R >= 4;
+    static constexpr int XV = 16 / (int)sizeof(T);  // elements per 16-byte load
+    __host__ __device__ static constexpr int pos(int i) { return (i / R) * S + i % R; }
+    // w[0..7] = taps c..c+7 of this thread, p = stage + S*l + pos(c), c % 8 == 0
+    __device__ static __forceinline__ void load8(const T *p, T *w) {
+        if constexpr (VEC) {
+#pragma unroll
+            for (int g = 0; g < 8 / R; ++g)
+#pragma unroll
+                for (int v = 0; v < R; v += XV) {
+                    if constexpr (sizeof(T) == 4) {
+                        const float4 f = *reinterpret_cast<const float4 *>(p + g * S + v);
+                        w[g * R + v] = f.x, w[g * R + v + 1] = f.y, w[g * R + v + 2] = f.z, w[g * R + v + 3] = f.w;
+                    } else {
+                        const double2 d = *reinterpret_cast<const double2 *>(p + g * S + v);
+                        w[g * R + v] = d.x, w[g * R + v + 1] = d.y;
+                    }
+                }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) w[q] = p[pos(q)];
+        }
+    }
+};
+static_assert(TapStage<float, 8>::S * 4 % 16 == 0 && TapStage<double, 8>::S * 8 % 16 == 0 &&
+                  TapStage<float, 4>::S * 4 % 16 == 0 && TapStage<double, 4>::S * 8 % 16 == 0,
+              "16-byte aligned tap groups");
 
 template <typename T, int SKIP, int R, bool FUSED, int CW_TB>
 __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB)) k_chain_w(ChainArgs<T> a) {
     constexpr int TILE = CW_TB * R;
     constexpr int HS = TILE + CW_MC - 1;  // taps per stage
-    constexpr int HSP = cw_pos<R>(HS - 1) + 1;
+    using ST = TapStage<T, R>;
+    // + one spare group: the window's initial load reads 8 taps past the
+    // thread's base at chunk offset CW_MC (only R-1 of them are used)
+    constexpr int HSP = (ST::pos(HS + 8) + 4) / 4 * 4;
     constexpr int HPT = (HS + CW_TB - 1) / CW_TB;  // tap loads per thread per chunk
     constexpr int XPT = CW_MC / CW_TB;             // drive samples staged per thread per chunk
     static_assert(CW_MC % CW_TB == 0 && CW_TB % 32 == 0, "chunk staging");
@@ -90,7 +121,7 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
     constexpr int XV = 16 / (int)sizeof(T);  // drive samples per vector load
     __shared__ __align__(16) T xs[2][CW_MC];
     __shared__ unsigned xmask[2][CW_MC / 32];
-    __shared__ T hs[2][HSP];
+    __shared__ __align__(16) T hs[2][HSP];
     if (a.run_if && *a.run_if == 0) return;  // block-uniform
     // channel-local base pointers (the param struct stays in the constant bank)
     const T *xb = a.x + blockIdx.y * a.ldx;
@@ -103,7 +134,7 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
     const int64_t init_len = a.init_len_dev ? a.init_len_dev[blockIdx.y * a.ld_st] : a.init_len;
     const int tid = threadIdx.x;
     // the tap for (r, im) sits at stage index tid*R + (CW_MC - 1) + r - im
-    const int hth = R == 1 ? tid : (R + 1) * tid;  // padded base of this thread
+    const int hth = ST::S * tid;  // padded base of this thread
 
     for (int64_t tb = blockIdx.x; tb < n_tiles; tb += gridDim.x) {
         const int64_t tile0 = a.t0 + tb * TILE;
@@ -158,7 +189,7 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
 #pragma unroll
             for (int j = 0; j < HPT; ++j) {
                 const int i = tid + j * CW_TB;
-                if (i < HS) hs[buf][cw_pos<R>(i)] = ph[j];
+                if (i < HS) hs[buf][ST::pos(i)] = ph[j];
             }
         };
         if (cs < a.nseg) {
@@ -190,15 +221,19 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
             if (full && dense) {
                 // interior: every (output, sample) pair valid, nothing skipped
                 T w[W];
+                {
+                    T nx[8];
+                    ST::load8(hsb + hth + ST::pos(CW_MC - CW_U), w);
+                    ST::load8(hsb + hth + ST::pos(CW_MC), nx);
 #pragma unroll
-                for (int q = 0; q < W; ++q) w[q] = hsb[hth + cw_pos<R>(CW_MC - CW_U + q)];
+                    for (int q = 8; q < W; ++q) w[q] = nx[q - 8];
+                }
 #pragma unroll
                 for (int ub = 0; ub < CW_MC / CW_U; ++ub) {
                     if (ub > 0) {
 #pragma unroll
                         for (int p = R - 2; p >= 0; --p) w[CW_U + p] = w[p];
-#pragma unroll
-                        for (int q = 0; q < CW_U; ++q) w[q] = hsb[hth + cw_pos<R>(CW_MC - CW_U - ub * CW_U + q)];
+                        ST::load8(hsb + hth + ST::pos(CW_MC - CW_U - ub * CW_U), w);
                     }
                     T xv[CW_U];
 #pragma unroll
@@ -228,10 +263,15 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
                 const int nh32 = (int)(nh < INT32_MAX ? nh : INT32_MAX);
                 for (int im0 = (int)ilo; im0 <= (int)ihi; im0 += CW_U) {
                     T w[W];
-                    // c0 = CW_MC - CW_U - im0 is a multiple of 8, so cw_pos(c0 + q) = cw_pos(c0) + cw_pos(q)
-                    const T *hp = hsb + hth + cw_pos<R>(CW_MC - CW_U - im0);
+                    // c0 = CW_MC - CW_U - im0 is a multiple of 8, so pos(c0 + q) = pos(c0) + pos(q)
+                    const T *hp = hsb + hth + ST::pos(CW_MC - CW_U - im0);
+                    {
+                        T nx[8];
+                        ST::load8(hp, w);
+                        ST::load8(hp + ST::pos(8), nx);
 #pragma unroll
-                    for (int q = 0; q < W; ++q) w[q] = hp[cw_pos<R>(q)];
+                        for (int q = 8; q < W; ++q) w[q] = nx[q - 8];
+                    }
                     // samples im0..im0+7 (bits past mcount are 0: m >= bhi)
                     const unsigned bits = (xmask[buf][im0 >> 5] >> (im0 & 31)) & 0xFFu;
                     const int e = (int)(rel - im0);  // |e| < nh + 8 here
@@ -287,21 +327,24 @@ int launch_chain_rf(int R, dim3 grid, cudaStream_t stream, const ChainArgs<T> &a
     return SC_OK;
 }
 
-int chain_tb() {
-    static const int tb = [] {
-        // One-warp CTAs by default: the per-chunk barrier is then a warp
-        // barrier (measured 4-10% faster than 128-thread CTAs on the ordered
-        // workloads).  Experiment knob: SC_CHAIN_TB=128.
+// CTA width.  One-warp CTAs make the per-chunk barrier a warp barrier:
+// 4-10 % faster for float chains and for small float64 launches.  Large
+// float64 launches (at least 4 waves of 128-thread tiles) are FP64-pipe
+// bound and run ~1 % faster on 128-thread CTAs.  SC_CHAIN_TB=32|128 forces.
+int chain_tb(size_t es, int64_t n_out, int64_t channels, int R) {
+    static const int forced = [] {
         const char *v = getenv("SC_CHAIN_TB");
-        return v && atoi(v) == 128 ? CW_WIDE : 32;
+        return v ? atoi(v) : 0;
     }();
-    return tb;
+    if (forced == 32 || forced == CW_WIDE) return forced;
+    if (es == 8 && channels * cdiv(n_out, (int64_t)CW_WIDE * R) >= 4 * (int64_t)sm_count()) return CW_WIDE;
+    return 32;
 }
 
 // float chains are always fused (one instantiation); double picks per call
 template <typename T, int SKIP>
-int launch_chain_r(int R, dim3 grid, cudaStream_t stream, const ChainArgs<T> &a, bool fused) {
-    const bool narrow = chain_tb() == 32;
+int launch_chain_r(int R, int tb, dim3 grid, cudaStream_t stream, const ChainArgs<T> &a, bool fused) {
+    const bool narrow = tb == 32;
     if constexpr (sizeof(T) == 8) {
         if (fused)
             return narrow ? launch_chain_rf<T, SKIP, true, 32>(R, grid, stream, a)
@@ -364,13 +407,14 @@ int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off
     const int R = pick_r(n_out, channels, sizeof(T));
     // Grid-stride over tiles.  A device-gated launch (run_if) is usually a
     // no-op, so it gets a small grid that exits in microseconds.
-    const int64_t cap = run_if ? std::max<int64_t>(1, 4 * (128 / chain_tb()) * (int64_t)sm_count() / channels)
+    const int tb = chain_tb(sizeof(T), n_out, channels, R);
+    const int64_t cap = run_if ? std::max<int64_t>(1, 4 * (128 / tb) * (int64_t)sm_count() / channels)
                                : (int64_t)INT32_MAX - 1;
-    const dim3 grid((unsigned)std::min<int64_t>(cdiv(n_out, (int64_t)chain_tb() * R), cap), (unsigned)channels);
+    const dim3 grid((unsigned)std::min<int64_t>(cdiv(n_out, (int64_t)tb * R), cap), (unsigned)channels);
     switch (skip_mode) {
-        case SC_SKIP_NONE: launch_chain_r<T, SC_SKIP_NONE>(R, grid, stream, a, fused); break;
-        case SC_SKIP_LE: launch_chain_r<T, SC_SKIP_LE>(R, grid, stream, a, fused); break;
-        case SC_SKIP_NOT_GT: launch_chain_r<T, SC_SKIP_NOT_GT>(R, grid, stream, a, fused); break;
+        case SC_SKIP_NONE: launch_chain_r<T, SC_SKIP_NONE>(R, tb, grid, stream, a, fused); break;
+        case SC_SKIP_LE: launch_chain_r<T, SC_SKIP_LE>(R, tb, grid, stream, a, fused); break;
+        case SC_SKIP_NOT_GT: launch_chain_r<T, SC_SKIP_NOT_GT>(R, tb, grid, stream, a, fused); break;
         default: SC_REQUIRE(false, "chain: bad skip_mode %d", skip_mode);
     }
     SC_CHECK_LAUNCH();
