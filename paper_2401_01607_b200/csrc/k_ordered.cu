@@ -162,21 +162,43 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
         bool pbit[XPT];
         T ph[HPT];
         auto fetch = [&](int s, int64_t mc) {
+            // Interior chunks (the whole chunk inside the segment, the whole
+            // tap range inside the IR: block-uniform tests) load without
+            // per-element 64-bit bounds checks, at [reg + imm] addresses.
             const int64_t bhi = seg_hi(s);
+            const T *xp = xb + (mc - a.x_off) + tid;
+            if (mc + CW_MC <= bhi) {
 #pragma unroll
-            for (int k = 0; k < XPT; ++k) {
-                const int64_t m = mc + tid + k * CW_TB;
-                px[k] = m < bhi ? xb[m - a.x_off] : T(0);
-                pbit[k] = m < bhi && !skipped<SKIP>(px[k], a.thr);
+                for (int k = 0; k < XPT; ++k) {
+                    px[k] = xp[k * CW_TB];
+                    pbit[k] = !skipped<SKIP>(px[k], a.thr);
+                }
+            } else {
+                const int rem = (int)(bhi - mc);  // < CW_MC here
+#pragma unroll
+                for (int k = 0; k < XPT; ++k) {
+                    const bool in = tid + k * CW_TB < rem;
+                    px[k] = in ? xp[k * CW_TB] : T(0);
+                    pbit[k] = in && !skipped<SKIP>(px[k], a.thr);
+                }
             }
-            const T *__restrict__ h = static_cast<const T *>(a.seg[s].h) + hoff;
             const int64_t nh = a.seg[s].nh;
             const int64_t kbase = tile0 - mc - CW_MC + 1;
+            const T *__restrict__ hp = static_cast<const T *>(a.seg[s].h) + hoff + kbase + tid;
+            if (kbase >= 0 && kbase + HS <= nh) {
 #pragma unroll
-            for (int j = 0; j < HPT; ++j) {
-                const int i = tid + j * CW_TB;
-                const int64_t k = kbase + i;
-                ph[j] = (i < HS && k >= 0 && k < nh) ? h[k] : T(0);
+                for (int j = 0; j < HPT; ++j)
+                    ph[j] = (j * CW_TB + CW_TB <= HS || tid + j * CW_TB < HS) ? hp[j * CW_TB] : T(0);
+            } else {
+                // k = kbase + i in [0, nh): i in [-kbase, nh - kbase)
+                const int ilo = kbase < 0 ? (int)(-kbase < HS ? -kbase : HS) : 0;
+                const int64_t hi64 = nh - kbase;
+                const int ihi = hi64 < 0 ? 0 : hi64 < HS ? (int)hi64 : HS;
+#pragma unroll
+                for (int j = 0; j < HPT; ++j) {
+                    const int i = tid + j * CW_TB;
+                    ph[j] = (i >= ilo && i < ihi) ? hp[j * CW_TB] : T(0);
+                }
             }
         };
         auto stash = [&](int buf) {

@@ -1,10 +1,12 @@
-# Ordered-chain evidence: float64 big-launch sweep at both CTA widths, the
-# ordered bench lines, and one full ncu capture of k_chain_w (mstream ordered).
+# Ordered-chain evidence: float64 big-launch sweep (A/B of two library builds
+# when given), the ordered bench lines, and one full ncu capture of k_chain_w
+# (mstream ordered).   tools/capture_chain.sh [A.so B.so]
 cd /root/repo
 mkdir -p gpurun_out/prof
-for tb in 128 32; do
-  SC_CHAIN_TB=$tb timeout 600 python -m paper_2401_01607_b200 bench --ir-sweep 200000:400000:200000 --input noise:10 \
-    --reps 1 --csv gpurun_out/prof/rt_tb$tb.csv > gpurun_out/prof/rt_tb$tb.log 2>&1
+for lib in "$@"; do
+  n=$(basename $lib .so)
+  SC_B200_LIB=$PWD/$lib timeout 600 python -m paper_2401_01607_b200 bench --ir-sweep 200000:400000:200000 \
+    --input noise:10 --reps 1 --csv gpurun_out/prof/rt_$n.csv > gpurun_out/prof/rt_$n.log 2>&1
 done
 for c in mstream cfg2; do
   timeout 900 python bench.py --config $c --mode ordered --no-cpu-baseline > gpurun_out/prof/bench_${c}_ordered.json 2>/dev/null
