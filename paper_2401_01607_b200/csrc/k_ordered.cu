@@ -106,6 +106,16 @@ static_assert(TapStage<float, 8>::S * 4 % 16 == 0 && TapStage<double, 8>::S * 8 
                   TapStage<float, 4>::S * 4 % 16 == 0 && TapStage<double, 4>::S * 8 % 16 == 0,
               "16-byte aligned tap groups");
 
+// The per-chunk barrier: a warp barrier for one-warp CTAs (it orders the
+// warp's shared-memory accesses like __syncthreads).
+template <int TB>
+__device__ __forceinline__ void chunk_sync() {
+    if constexpr (TB == 32)
+        __syncwarp();
+    else
+        __syncthreads();
+}
+
 template <typename T, int SKIP, int R, bool FUSED, int CW_TB>
 __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB)) k_chain_w(ChainArgs<T> a) {
     constexpr int TILE = CW_TB * R;
@@ -147,25 +157,47 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
             acc[r] = (initc != nullptr && t < t_end && (t - a.t0) < init_len) ? initc[t - a.t0] : T(0);
         }
         // chunk range of segment s for this tile: [blo, bhi)
-        auto seg_lo = [&](int s) {
-            const int64_t v = tile0 - a.seg[s].nh + 1;
-            return v > a.seg[s].m_lo ? v : a.seg[s].m_lo;
+        // The chunk walk: segment s, chunk start mc, and the segment's
+        // fields cached in registers (hi = end of its drive range for this
+        // tile), so stepping inside a segment is one add and one compare.
+        struct Chunk {
+            int s;
+            int64_t mc, hi, nh;
+            const T *h;
         };
-        auto seg_hi = [&](int s) { return tile_last + 1 < a.seg[s].m_hi ? tile_last + 1 : a.seg[s].m_hi; };
-        // first chunk
-        int cs = 0;
-        int64_t cmc = 0;
-        while (cs < a.nseg && seg_lo(cs) >= seg_hi(cs)) ++cs;
-        if (cs < a.nseg) cmc = seg_lo(cs);
+        auto first_from = [&](int s) {  // first chunk of the first non-empty segment >= s
+            Chunk c{s, 0, 0, 0, nullptr};
+            for (; c.s < a.nseg; ++c.s) {
+                c.nh = a.seg[c.s].nh;
+                const int64_t lo = tile0 - c.nh + 1 > a.seg[c.s].m_lo ? tile0 - c.nh + 1 : a.seg[c.s].m_lo;
+                c.hi = tile_last + 1 < a.seg[c.s].m_hi ? tile_last + 1 : a.seg[c.s].m_hi;
+                if (lo < c.hi) {
+                    c.mc = lo;
+                    c.h = static_cast<const T *>(a.seg[c.s].h) + hoff;
+                    break;
+                }
+            }
+            return c;
+        };
+        auto next_of = [&](const Chunk &c) {
+            if (c.mc + CW_MC < c.hi) {
+                Chunk n = c;
+                n.mc += CW_MC;
+                return n;
+            }
+            return first_from(c.s + 1);
+        };
+        Chunk cur = first_from(0);
         // register prefetch of one chunk
         T px[XPT];
         bool pbit[XPT];
         T ph[HPT];
-        auto fetch = [&](int s, int64_t mc) {
+        auto fetch = [&](const Chunk &c) {
+            const int64_t mc = c.mc;
             // Interior chunks (the whole chunk inside the segment, the whole
             // tap range inside the IR: block-uniform tests) load without
             // per-element 64-bit bounds checks, at [reg + imm] addresses.
-            const int64_t bhi = seg_hi(s);
+            const int64_t bhi = c.hi;
             const T *xp = xb + (mc - a.x_off) + tid;
             if (mc + CW_MC <= bhi) {
 #pragma unroll
@@ -182,9 +214,9 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
                     pbit[k] = in && !skipped<SKIP>(px[k], a.thr);
                 }
             }
-            const int64_t nh = a.seg[s].nh;
+            const int64_t nh = c.nh;
             const int64_t kbase = tile0 - mc - CW_MC + 1;
-            const T *__restrict__ hp = static_cast<const T *>(a.seg[s].h) + hoff + kbase + tid;
+            const T *__restrict__ hp = c.h + kbase + tid;
             if (kbase >= 0 && kbase + HS <= nh) {
 #pragma unroll
                 for (int j = 0; j < HPT; ++j)
@@ -211,28 +243,23 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
 #pragma unroll
             for (int j = 0; j < HPT; ++j) {
                 const int i = tid + j * CW_TB;
-                if (i < HS) hs[buf][ST::pos(i)] = ph[j];
+                // pos(tid + j*TB) = pos(tid) + j*(TB/R)*S since TB % R == 0
+                if (i < HS) hs[buf][ST::pos(tid) + j * (CW_TB / R) * ST::S] = ph[j];
             }
         };
-        if (cs < a.nseg) {
-            fetch(cs, cmc);
+        if (cur.s < a.nseg) {
+            fetch(cur);
             stash(0);
         }
-        __syncthreads();
+        chunk_sync<CW_TB>();
         int buf = 0;
-        while (cs < a.nseg) {
-            // next chunk
-            int ns = cs;
-            int64_t nmc = cmc + CW_MC;
-            if (nmc >= seg_hi(ns)) {
-                ++ns;
-                while (ns < a.nseg && seg_lo(ns) >= seg_hi(ns)) ++ns;
-                if (ns < a.nseg) nmc = seg_lo(ns);
-            }
-            if (ns < a.nseg) fetch(ns, nmc);  // global loads in flight during the compute below
+        while (cur.s < a.nseg) {
+            const Chunk nxt = next_of(cur);
+            if (nxt.s < a.nseg) fetch(nxt);  // global loads in flight during the compute below
 
-            const int64_t nh = a.seg[cs].nh;
-            const int64_t bhi = seg_hi(cs);
+            const int64_t cmc = cur.mc;
+            const int64_t nh = cur.nh;
+            const int64_t bhi = cur.hi;
             const int mcount = (int)(bhi - cmc < CW_MC ? bhi - cmc : CW_MC);
             const T *xsb = xs[buf];
             const T *hsb = hs[buf];
@@ -318,11 +345,10 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
                     }
                 }
             }
-            if (ns < a.nseg) stash(buf ^ 1);
-            __syncthreads();
+            if (nxt.s < a.nseg) stash(buf ^ 1);
+            chunk_sync<CW_TB>();
             buf ^= 1;
-            cs = ns;
-            cmc = nmc;
+            cur = nxt;
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
