@@ -367,7 +367,28 @@ class Work:
         if self.cfg == "cfg4":
             y = convolve_batched(x_pin, h_pin)
             return x_pin.numel() * 4 + h_pin.numel() * 4, y.numel() * 4
-        raise ValueError("e2e only for cfg3/cfg4/cfg5")
+        es = x_pin.element_size()
+        if self.cfg == "cfg1" or self.cfg.startswith("short"):
+            out = scatter_convolve(Signal(x_pin), Signal(h_pin), mode=self.lib_mode)
+            return (x_pin.numel() + h_pin.numel()) * es, (len(out.body) + len(out.tail)) * es
+        if self.cfg in ("cfg2", "mstream"):
+            # the same stream and swap schedule from pinned host memory; body
+            # and flushed tail come back to the host
+            if not hasattr(self, "swaps_pin"):
+                self.swaps_pin = [(b, ir.cpu().pin_memory()) for b, ir in self.swaps]
+            body = self.eng.process_stream(x_pin, 256 if self.cfg == "cfg2" else 8192, self.swaps_pin)
+            tail = self.eng.flush()
+            tail_n = len(tail) if self.cfg == "cfg2" else sum(len(t) for t in tail)
+            h2d = x_pin.numel() * es + sum(ir.numel() for _, ir in self.swaps_pin) * es
+            return h2d, (body.numel() + tail_n) * es
+        raise ValueError(f"no e2e path for {self.cfg}")
+
+
+E2E_API = {
+    "cfg4": "paper_2401_01607_b200.convolve_batched(pinned host [C, N], pinned host [C, Nh])",
+    "cfg2": "ScatterEngine.process_stream(pinned host, 256, pinned-host swaps) + flush()",
+    "mstream": "MultiChannelEngine.process_stream(pinned host [64, N], 8192, pinned-host swaps) + flush()",
+}
 
 
 # ------------------------------------------------------------------ CPU reference
@@ -612,10 +633,13 @@ def main():
 
     # e2e through the public API with pinned host buffers
     e2e = None
-    if not args.no_e2e and args.config in ("cfg3", "cfg4", "cfg5"):
+    if not args.no_e2e:
         if args.config == "cfg4":
             x_pin = torch.from_numpy(work.w.x[work.c0:work.c1]).pin_memory()
             h_pin = torch.from_numpy(work.w.h[work.c0:work.c1]).pin_memory()
+        elif args.config not in ("cfg3", "cfg5"):
+            x_pin = work.xd.cpu().pin_memory()
+            h_pin = work.hd.cpu().pin_memory() if hasattr(work, "hd") else None
         else:
             x_pin = torch.from_numpy(work.x_host).pin_memory()
             h_pin = torch.from_numpy(work.h_host).pin_memory()
@@ -634,7 +658,8 @@ def main():
         e2e = {"value": work.total_macs / t_e2e / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(hb), "d2h_bytes_per_step": int(db),
                "ms_per_step": 1000 * t_e2e,
-               "api": "paper_2401_01607_b200.scatter_convolve(Signal(pinned host tensor))" if world == 1
+               "api": E2E_API.get(args.config, "paper_2401_01607_b200.scatter_convolve(Signal(pinned host tensor))")
+               if world == 1 or args.config not in ("cfg3", "cfg5")
                else "paper_2401_01607_b200.distributed_convolve(pinned host, to_host=True)"}
 
     cpu = None

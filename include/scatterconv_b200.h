@@ -204,6 +204,18 @@ int sc_engine_process_blocks(sc_engine *e, const void *x, int64_t n_total, int64
                              const int64_t *swap_blocks, const void *const *swap_irs,
                              const int64_t *swap_nh, int64_t n_swaps, void *out);
 
+/* The same with x[C][n_total] and out[C][n_total] in HOST memory (pinned for
+ * full PCIe rate; swap IRs on the device).  The stream is processed in
+ * `chunks` runs of whole blocks (0 = automatic: 2..4 by size) whose uploads,
+ * blocks and downloads overlap on three streams; the engine state, and in
+ * ORDERED mode the results bit for bit, are those of one
+ * sc_engine_process_blocks call (FAST: within the FP32 tolerance).  Synchronous: out is filled on
+ * return.  (No reference counterpart: render, engine.py:194-209, over a host
+ * signal, with the transfers hidden behind the blocks.) */
+int sc_engine_process_blocks_host(sc_engine *e, const void *x_host, int64_t n_total, int64_t nb,
+                                  const int64_t *swap_blocks, const void *const *swap_irs,
+                                  const int64_t *swap_nh, int64_t n_swaps, void *out_host, int chunks);
+
 /* ---------------------------------------------------------------- multi-GPU */
 
 /* Whole-signal convolution of a HOST signal x[ne] (pinned or pageable) with

@@ -48,6 +48,31 @@ def as_device(a, npd, device=None):
     return t.from_numpy(arr).to(device=dev)
 
 
+PINNED_STREAM_MIN_BYTES = 1 << 24   # pinned host streams this large are pipelined in the library
+
+
+def host_pipe_chunks() -> int:
+    """Runs per pipelined host stream: 0 = the library's choice (2..4 by
+    size); SC_HOST_PIPE_CHUNKS overrides (experiments)."""
+    import os
+
+    return int(os.environ.get("SC_HOST_PIPE_CHUNKS", "0"))
+
+
+def pinned_rows(x, npd, channels: int):
+    """x as a contiguous [channels, n] pinned CPU tensor of dtype npd when it
+    is one (1-D allowed for one channel) and large enough to pipeline, else
+    None (the caller takes the device path)."""
+    if not (is_tensor(x) and x.device.type == "cpu" and x.is_pinned() and x.is_contiguous()):
+        return None
+    if x.dtype != torch_dtype(npd) or x.numel() * x.element_size() < PINNED_STREAM_MIN_BYTES:
+        return None
+    rows = x[None, :] if x.ndim == 1 and channels == 1 else x
+    if rows.ndim != 2 or rows.shape[0] != channels or rows.shape[1] == 0:
+        return None
+    return rows
+
+
 def like_input(result, *inputs):
     """Return result (a CUDA tensor) in the caller's currency: a CUDA tensor if
     any input was one, a CPU tensor if any input was a tensor, else an ndarray."""

@@ -65,6 +65,8 @@ _SIGNATURES = {
     "sc_engine_current_ir": [_vp, _vp, _i64, _p64],
     "sc_engine_process_blocks": [_vp, _vp, _i64, _i64, _p64, ctypes.POINTER(_vp), _p64, _i64,
                                  _vp],
+    "sc_engine_process_blocks_host": [_vp, _vp, _i64, _i64, _p64, ctypes.POINTER(_vp), _p64, _i64,
+                                      _vp, ctypes.c_int],
 }
 EXPORTS = tuple(_SIGNATURES) + ("sc_last_error", "sc_launch_count")
 

@@ -117,6 +117,8 @@ def mode_code(mode) -> int:
 _PIPELINE_MIN_MACS = 1 << 36   # host-resident inputs this large are streamed in chunks
 _PIPELINE_CHUNK_MACS = 1 << 36   # each pipelined chunk carries at least this much work...
 _PIPELINE_MAX_CHUNKS = 12        # ...up to 12 chunks (cfg3: 4 chunks, cfg5: 12; measured best)
+_PIPELINE_MIN_BYTES = 1 << 25    # transfer-bound inputs (short filters) this large are streamed too,
+_PIPELINE_CHUNK_BYTES = 1 << 24  # in chunks of >= 16 MiB, so upload and download overlap (full duplex)
 _PIPE_STREAMS: dict = {}
 
 
@@ -151,7 +153,7 @@ def _fir_host_pipelined(x_pin, kern, mode):
     for s in (s_in, s_cmp, s_out):
         s.wait_stream(main)   # h upload / allocations are ordered on main
     chunks = int(os.environ.get("SC_PIPE_CHUNKS", "0")) or \
-        max(2, min(_PIPELINE_MAX_CHUNKS, (nout * nh) // _PIPELINE_CHUNK_MACS))
+        max(2, min(_PIPELINE_MAX_CHUNKS, max((nout * nh) // _PIPELINE_CHUNK_MACS, 4 * ne // _PIPELINE_CHUNK_BYTES)))
     per = -(-nout // chunks)
     uploaded = 0
     for c in range(chunks):
@@ -187,7 +189,8 @@ def _fir(drive, kern, *, mode=None, skip_mode=N.SC_SKIP_NONE, threshold=0.0):
     t = _dev.torch()
     if (npd == np.float32 and m != N.SC_MODE_ORDERED and skip_mode == N.SC_SKIP_NONE
             and _dev.is_tensor(drive) and drive.device.type == "cpu" and drive.is_pinned()
-            and drive.dtype == t.float32 and drive.shape[0] * int(np.shape(kern)[0]) >= _PIPELINE_MIN_MACS):
+            and drive.dtype == t.float32 and (drive.shape[0] * int(np.shape(kern)[0]) >= _PIPELINE_MIN_MACS
+                                              or 4 * drive.shape[0] >= _PIPELINE_MIN_BYTES)):
         return _fir_host_pipelined(drive, kern, m)
     x = _dev.as_device(drive, npd)
     h = _dev.as_device(kern, npd, device=x.device)

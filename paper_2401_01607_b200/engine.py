@@ -297,8 +297,6 @@ class ScatterEngine:
         t = _dev.torch()
         with t.cuda.device(self._device):
             xs = x.samples if isinstance(x, Signal) else x
-            xd = self._to_dev(xs)
-            out = t.empty(xd.shape[0], dtype=xd.dtype, device=self._device)
             swaps = sorted(swaps, key=lambda s: s[0])
             irs = [self._to_dev(s[1].samples if isinstance(s[1], Signal) else s[1]) for s in swaps]
             n = len(swaps)
@@ -306,14 +304,28 @@ class ScatterEngine:
             ptrs = (ctypes.c_void_p * max(n, 1))(*[ir.data_ptr() for ir in irs])
             nhs = (ctypes.c_int64 * max(n, 1))(*[ir.shape[0] for ir in irs])
             self._bind_stream()
+            xh = _dev.pinned_rows(xs, self._npd, 1)
+            if xh is not None:
+                # large pinned host stream: transfers overlap the blocks run by
+                # run inside the library (sc_engine_process_blocks_host)
+                out = t.empty(xh.shape[1], dtype=xh.dtype, pin_memory=True)
+                N.check(self._lib.sc_engine_process_blocks_host(self._handle, N.ptr(xh), xh.shape[1], nb,
+                                                                blocks, ptrs, nhs, n, N.ptr(out), _dev.host_pipe_chunks()))
+                self._note_swaps(swaps)
+                return out
+            xd = self._to_dev(xs)
+            out = t.empty(xd.shape[0], dtype=xd.dtype, device=self._device)
             N.check(self._lib.sc_engine_process_blocks(self._handle, N.ptr(xd), xd.shape[0], nb,
                                                        blocks, ptrs, nhs, n, N.ptr(out)))
-            if swaps:
-                last = swaps[-1][1]
-                last = last.samples if isinstance(last, Signal) else last
-                self._ir_like = last[:0]
-                self._nh = len(last)
+            self._note_swaps(swaps)
         return _dev.like_input(out, xs)
+
+    def _note_swaps(self, swaps):
+        if swaps:
+            last = swaps[-1][1]
+            last = last.samples if isinstance(last, Signal) else last
+            self._ir_like = last[:0]
+            self._nh = len(last)
 
     def state_dict(self) -> dict:
         """Snapshot for tests/checkpointing: ring, schedule, read_index, live, consumed."""

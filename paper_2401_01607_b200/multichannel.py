@@ -269,8 +269,6 @@ class MultiChannelEngine:
             h_new, self._pending = self._pending, None
             self.swap_ir(h_new)
         with t.cuda.device(self._device):
-            xd = self._rows(x)
-            out = t.empty_like(xd)
             swaps = sorted(swaps, key=lambda s: s[0])
             irs = [self._ir_rows(s[1]) for s in swaps]
             k = len(swaps)
@@ -278,6 +276,16 @@ class MultiChannelEngine:
             ptrs = (ctypes.c_void_p * max(k, 1))(*[ir.data_ptr() for ir in irs])
             nhs = (ctypes.c_int64 * max(k, 1))(*[ir.shape[1] for ir in irs])
             self._bind()
+            xh = _dev.pinned_rows(x, self._npd, self._C)
+            if xh is not None:
+                # large pinned host stream: uploads / blocks / downloads overlap
+                # run by run inside the library (sc_engine_process_blocks_host)
+                out = t.empty(xh.shape, dtype=xh.dtype, pin_memory=True)
+                N.check(self._lib.sc_engine_process_blocks_host(self._handle, N.ptr(xh), xh.shape[1], nb, blocks,
+                                                                ptrs, nhs, k, N.ptr(out), _dev.host_pipe_chunks()))
+                return out
+            xd = self._rows(x)
+            out = t.empty_like(xd)
             N.check(self._lib.sc_engine_process_blocks(self._handle, N.ptr(xd), xd.shape[1], nb, blocks, ptrs,
                                                        nhs, k, N.ptr(out)))
         return _dev.like_input(out, x)

@@ -132,6 +132,28 @@ def test_pinned_host_pipeline(monkeypatch, mode):
     assert err_frac(y.numpy(), O.scatter_window(x, h, 0, len(y)), x, h) <= 1.0
 
 
+
+@pytest.mark.parametrize("nh", [1, 8, 40])
+def test_pinned_host_pipeline_transfer_bound(monkeypatch, nh):
+    """Short filters on large pinned inputs are streamed by size, not by MACs
+    (upload and download of consecutive chunks overlap)."""
+    import torch
+
+    from paper_2401_01607_b200 import core
+
+    monkeypatch.setattr(core, "_PIPELINE_MIN_BYTES", 4 * 100_000)
+    monkeypatch.setattr(core, "_PIPELINE_CHUNK_BYTES", 4 * 30_000)   # 7 chunks
+    calls = []
+    real = core._fir_host_pipelined
+    monkeypatch.setattr(core, "_fir_host_pipelined", lambda *a: calls.append(1) or real(*a))
+    rng = np.random.default_rng(45 + nh)
+    x = rng.uniform(-1, 1, 210_007).astype(np.float32)
+    h = rng.standard_normal(nh).astype(np.float32)
+    out = scatter_convolve(Signal(torch.from_numpy(x).pin_memory()), Signal(torch.from_numpy(h)))
+    assert calls and out.body.samples.is_pinned()
+    y = out.concatenated().samples
+    assert err_frac(y.numpy(), O.scatter_window(x, h, 0, len(y)), x, h) <= 1.0
+
 def test_tc_deterministic():
     import torch
 
