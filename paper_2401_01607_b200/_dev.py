@@ -48,6 +48,29 @@ def as_device(a, npd, device=None):
     return t.from_numpy(arr).to(device=dev)
 
 
+def as_device_many(arrays, npd, device=None):
+    """as_device of every array; several host arrays go up in ONE copy
+    (packed on the host, split on the device) instead of one small copy each
+    (an IR-swap schedule of 19 host IRs: one ~50 us upload, not 19 dispatches)."""
+    t = torch()
+    host = [a for a in arrays if not (is_tensor(a) and a.is_cuda)]
+    if len(host) < 2 or len(host) != len(arrays) or any(np.ndim(a) == 0 for a in arrays):
+        return [as_device(a, npd, device=device) for a in arrays]
+    td = torch_dtype(npd)
+    shapes = [tuple(a.shape) for a in arrays]
+    sizes = [int(np.prod(sh)) for sh in shapes]
+    if sum(sizes) * np.dtype(npd).itemsize > (64 << 10) * len(arrays):
+        # large arrays: packing costs a host memcpy; one copy each is cheaper
+        return [as_device(a, npd, device=device) for a in arrays]
+    if all(is_tensor(a) for a in arrays):
+        flat = t.empty(sum(sizes), dtype=td, pin_memory=True)
+        t.cat([a.reshape(-1).to(td) for a in arrays], out=flat)
+    else:
+        flat = t.from_numpy(np.concatenate([np.asarray(a, dtype=npd).reshape(-1) for a in arrays]))
+    dflat = as_device(flat, npd, device=device)
+    return [v.view(sh) for v, sh in zip(t.split(dflat, sizes), shapes)]
+
+
 PINNED_STREAM_MIN_BYTES = 1 << 24   # pinned host streams this large are pipelined in the library
 
 

@@ -298,7 +298,8 @@ class ScatterEngine:
         with t.cuda.device(self._device):
             xs = x.samples if isinstance(x, Signal) else x
             swaps = sorted(swaps, key=lambda s: s[0])
-            irs = [self._to_dev(s[1].samples if isinstance(s[1], Signal) else s[1]) for s in swaps]
+            irs = _dev.as_device_many([s[1].samples if isinstance(s[1], Signal) else s[1] for s in swaps],
+                                      self._npd, device=self._device)
             n = len(swaps)
             blocks = (ctypes.c_int64 * max(n, 1))(*[int(s[0]) for s in swaps])
             ptrs = (ctypes.c_void_p * max(n, 1))(*[ir.data_ptr() for ir in irs])

@@ -178,6 +178,18 @@ class MultiChannelEngine:
             raise ValueError("impulse response is empty")
         return self._rows(hd)
 
+    def _ir_rows_many(self, hs):
+        """_ir_rows of a swap schedule, uploaded together (_dev.as_device_many)."""
+        rows = []
+        for h in hs:
+            hd = h if _dev.is_tensor(h) else np.asarray(h)
+            if hd.ndim == 1:
+                hd = hd[None, :].expand(self._C, -1) if _dev.is_tensor(hd) else np.repeat(hd[None, :], self._C, 0)
+            if hd.shape[-1] == 0:
+                raise ValueError("impulse response is empty")
+            rows.append(hd)
+        return [self._rows(d) for d in _dev.as_device_many(rows, self._npd, device=self._device)]
+
     def process_block(self, block):
         """[C, n] in, [C, n] out (engine.py:118-146 per channel)."""
         t = _dev.torch()
@@ -270,7 +282,7 @@ class MultiChannelEngine:
             self.swap_ir(h_new)
         with t.cuda.device(self._device):
             swaps = sorted(swaps, key=lambda s: s[0])
-            irs = [self._ir_rows(s[1]) for s in swaps]
+            irs = self._ir_rows_many([s[1] for s in swaps])
             k = len(swaps)
             blocks = (ctypes.c_int64 * max(k, 1))(*[int(s[0]) for s in swaps])
             ptrs = (ctypes.c_void_p * max(k, 1))(*[ir.data_ptr() for ir in irs])

@@ -156,3 +156,26 @@ def test_host_stream_small_or_pageable_takes_device_path(monkeypatch):
     eng.process_stream(_pinned(x), 100)           # 8 KB: below the threshold
     eng.process_stream(torch.from_numpy(x), 100)  # pageable
     assert seen == []
+
+
+@pytest.mark.parametrize("kind", ["numpy", "pinned", "pageable", "mixed_cuda"])
+def test_as_device_many_packs_small_host_arrays(kind):
+    """A swap schedule's IRs go up in one packed copy; values, shapes and
+    dtype are those of one as_device call per array."""
+    import torch
+
+    rng = np.random.default_rng(95)
+    arrays = [rng.standard_normal(n) for n in (5, 300, 1)] + [rng.standard_normal((3, 40))]
+    if kind == "pinned":
+        arrays = [_pinned(a) for a in arrays]
+    elif kind == "pageable":
+        arrays = [torch.from_numpy(a) for a in arrays]
+    elif kind == "mixed_cuda":
+        arrays = [torch.from_numpy(a).cuda() if i == 1 else a for i, a in enumerate(arrays)]
+    for npd in (np.float64, np.float32):
+        got = _dev.as_device_many(arrays, npd)
+        want = [_dev.as_device(a, npd) for a in arrays]
+        assert len(got) == len(want)
+        for g, w in zip(got, want):
+            assert g.is_cuda and g.dtype == w.dtype and g.shape == w.shape and g.is_contiguous()
+            assert torch.equal(g, w)
