@@ -410,8 +410,11 @@ int pick_r(int64_t n_out, int64_t channels, size_t es) {
         return v ? atoi(v) : 0;
     }();
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
-    (void)es;
-    const int64_t warps_per_sm = 16;
+    // float64 chains run out of FP64-pipe and LDS throughput long before
+    // they run out of warps: more independent chains per thread (larger R)
+    // beat more warps (10 s through 17.6 M taps: R=8 0.946 s, R=4 0.989;
+    // cfg1: R=2 26.5 us, R=1 29.2).  float32 wants ~16 warps per SM.
+    const int64_t warps_per_sm = es == 8 ? 4 : 16;
     const int64_t want_threads = (int64_t)sm_count() * warps_per_sm * 32;
     for (int R = 8; R > 1; R >>= 1)
         if (channels * cdiv(n_out, R) >= want_threads) return R;
