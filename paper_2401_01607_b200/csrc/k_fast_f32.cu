@@ -288,6 +288,32 @@ __global__ void __launch_bounds__(SH_THREADS) k_fir_short(const float *__restric
     const bool interior = n0 - 4 * nkb >= x_lo && n0 + SH_TILE <= x_hi && n0 + SH_TILE <= n_end &&
                           ((reinterpret_cast<uintptr_t>(xt) | reinterpret_cast<uintptr_t>(yc + (n0 - n_begin)) |
                             (uintptr_t)(ldx * 4) | (uintptr_t)(ldy * 4)) & 15) == 0;
+    if (interior && nkb == NKB && nfull == NKB) {
+        // Nh == 4*NKB: the tap-block loop is entirely compile-time (no
+        // per-block tests, the window shift is pure register renaming)
+        const float4 *xp = reinterpret_cast<const float4 *>(xc + (t0 - x_base));
+        float4 g2 = __ldg(xp + 1), g1 = __ldg(xp), g0 = __ldg(xp - 1);
+        const float4 *h4 = reinterpret_cast<const float4 *>(hsm);
+#pragma unroll
+        for (int kb = 0; kb < NKB; ++kb) {
+            const float w[12] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, g2.y, g2.z, g2.w};
+            const float4 hq = h4[kb];
+            const float hk[4] = {hq.x, hq.y, hq.z, hq.w};
+            float4 gn = g0;
+            if (kb + 1 < NKB) gn = __ldg(xp - (kb + 2));  // next window in flight during the FMAs
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int r = 0; r < SH_R; ++r) acc[r] = fmaf(w[r - u + 4], hk[u], acc[r]);
+            g2 = g1;
+            g1 = g0;
+            g0 = gn;
+        }
+        float4 *d = reinterpret_cast<float4 *>(yc + (t0 - n_begin));
+        d[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        d[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        return;
+    }
     if (interior) {
         const float4 *xp = reinterpret_cast<const float4 *>(xc + (t0 - x_base));  // x[t0 .. t0+3]
         float4 g2 = __ldg(xp + 1), g1 = __ldg(xp), g0 = __ldg(xp - 1);        // x[t0-4 .. t0+7]
@@ -392,7 +418,52 @@ __global__ void __launch_bounds__(SM_THREADS) k_fir_short_smem(const float *__re
     const int j16 = threadIdx.x * SM_R;
     const int64_t t0 = n0 + j16;  // this thread's first output
     // output t0+r, tap k reads X(t0 + r - k) = xs[j16 + r - k + nhp]
-    for (int k0 = 0; k0 < nh; k0 += 4) {
+    int k_done = 0;
+    if (!edge) {
+        // Interior tiles: the 20-sample window slides by 4 samples per 4
+        // taps, so each step loads ONE new float4 (into the slot of the
+        // dropped one) plus the broadcast taps: 2 LDS.128 per 64 FFMA
+        // instead of 6.  Five slots in a cycle, unrolled by 5, so the slot
+        // rotation is pure register renaming; whole groups of 20 taps here,
+        // the remainder in the reload loop below (a static tail of slide
+        // steps measured slower: 76 registers).
+        const int b0 = j16 + nhp - 4;
+        const int ngrp = nh / 20;
+        if (ngrp > 0) {
+            float4 S[5];
+#pragma unroll
+            for (int c = 0; c < 5; ++c) S[c] = *reinterpret_cast<const float4 *>(&xs[sh_pos(b0 + 4 * c)]);
+            for (int g = 0; g < ngrp; ++g) {
+                const int k0 = 20 * g;
+#pragma unroll
+                for (int st = 0; st < 5; ++st) {
+                    const int kk = k0 + 4 * st;
+                    float w[20];
+#pragma unroll
+                    for (int c = 0; c < 5; ++c) {
+                        const float4 q = S[(5 - st + c) % 5];
+                        w[4 * c] = q.x;
+                        w[4 * c + 1] = q.y;
+                        w[4 * c + 2] = q.z;
+                        w[4 * c + 3] = q.w;
+                    }
+                    // next lowest float4 (the stage holds nhp+4 samples below
+                    // b0+4, so this stays inside it; unused after the last step)
+                    const float4 nxt = *reinterpret_cast<const float4 *>(&xs[sh_pos(b0 - kk - 4 + (kk + 4 >= nhp ? 4 : 0))]);
+                    const float4 hq = *reinterpret_cast<const float4 *>(&hsm[kk]);
+                    const float hk[4] = {hq.x, hq.y, hq.z, hq.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int r = 0; r < SM_R; ++r) acc[r] = fmaf(w[r - u + 4], hk[u], acc[r]);
+                    S[(9 - st) % 5] = nxt;  // the dropped (highest) slot becomes the new lowest
+                }
+            }
+            k_done = 20 * ngrp;
+        }
+    }
+    // remaining taps (all of them on edge tiles): reload the window per 4 taps
+    for (int k0 = k_done; k0 < nh; k0 += 4) {
         // window: xs[b .. b+20) with b = j16 + nhp - 4 - k0 (a multiple of 4,
         // so both the staging and the window loads are float4-aligned);
         // tap k0+u, output r -> w[r - u + 4]
@@ -487,10 +558,17 @@ int launch_fir_f32_fast(const float *x, int64_t ldx, int64_t x_base, int64_t x_l
         dim3 g((unsigned)tiles, (unsigned)channels);
 #define SC_SHORT(NKB) k_fir_short<NKB><<<g, SH_THREADS, 0, stream>>>(x, ldx, x_base, x_lo, x_hi, h, ldh, (int)nh, \
                                                                    y, ldy, n_begin, n_end, run_if)
-        if (nh <= 4) SC_SHORT(1);
-        else if (nh <= 8) SC_SHORT(2);
-        else if (nh <= 16) SC_SHORT(4);
-        else SC_SHORT(8);
+        // NKB = ceil(Nh/4) exactly for multiples of 4 (the compile-time path)
+        switch ((int)((nh + 3) / 4)) {
+            case 1: SC_SHORT(1); break;
+            case 2: SC_SHORT(2); break;
+            case 3: SC_SHORT(3); break;
+            case 4: SC_SHORT(4); break;
+            case 5: SC_SHORT(5); break;
+            case 6: SC_SHORT(6); break;
+            case 7: SC_SHORT(7); break;
+            default: SC_SHORT(8); break;
+        }
 #undef SC_SHORT
         SC_CHECK_LAUNCH();
         return SC_OK;
