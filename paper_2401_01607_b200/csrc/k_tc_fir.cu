@@ -669,13 +669,20 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     a.channels = channels;
     // Shift-range splits fill idle SMs when whole tiles leave the last wave
     // mostly empty (cfg3: 182 tiles on 148 SMs); each split keeps >= 2 X
-    // windows so its window load stays amortised.
+    // windows so its window load stays amortised -- unless the tiles alone
+    // leave more than half the SMs idle (cfg2's 19 short segments: 38 tiles
+    // of a 40-shift filter), where splits down to one drain period pay.
     const int sms = sm_count();
     const int64_t stages = s8 / SSH;
+    static const bool small_split = [] {
+        const char *v = getenv("SC_TC_SMALL_SPLIT");  // experiment knob: 0 disables
+        return !(v && atoi(v) == 0);
+    }();
+    const int64_t min_stages = (small_split && a.n_tiles * 2 <= sms) ? 1 : WP / SSH;
     int64_t nsplit = 1;
     {
         double best = 0.0;
-        for (int64_t s = 1; s <= 16 && s * (WP / SSH) <= stages; ++s) {
+        for (int64_t s = 1; s <= 16 && s * min_stages <= stages; ++s) {
             const int64_t units = a.n_tiles * s;
             const int64_t waves = (units + sms - 1) / sms;
             const double eff = (double)units / (double)(waves * sms);

@@ -2,7 +2,7 @@
 C enqueue of process_stream and the flush take, versus the device time of
 the whole step (CUDA events).  Diagnostic only.
 
-    python tools/prof_stream_host.py [cfg2|mstream]
+    python tools/prof_stream_host.py [cfg2|mstream] [host] [cprofile]
 """
 import os
 import sys
@@ -35,6 +35,10 @@ else:
     n_blocks = -(-w.ne // nb)
     swaps = [(0, hd), (n_blocks // 2, torch.flip(hd, dims=[1]).contiguous())]
     eng = MultiChannelEngine(hd, EngineConfig(block_size_nb=nb))
+if "host" in sys.argv[2:]:
+    # the e2e path: pinned host stream and pinned host IRs
+    xd = xd.cpu().pin_memory()
+    swaps = [(b, h.cpu().pin_memory()) for b, h in swaps]
 for it in range(6):
     torch.cuda.synchronize()
     e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
@@ -52,7 +56,7 @@ for it in range(6):
           f"device stream {e0.elapsed_time(e1):.3f} ms, device total {e0.elapsed_time(e2):.3f} ms, "
           f"wall {1e3*(t3-t0):.3f} ms")
 
-if len(sys.argv) > 2 and sys.argv[2] == "cprofile":
+if "cprofile" in sys.argv[2:]:
     import cProfile
     import pstats
 
