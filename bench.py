@@ -272,11 +272,13 @@ class Work:
         self.tc_padded_macs = 0
         if self.cfg.startswith("short"):
             # FAST dispatch (capi.cu / k_fast_f32.cu): tensor cores from 80
-            # taps at this size, the streaming k_fir_short up to 32
-            # (HBM-bound), the smem k_fir_short_smem in between (FMA-bound)
+            # taps at this size, the streaming k_fir_short up to 8 taps and
+            # the tap-stationary k_fir_tapreg up to 32 (HBM-bound), the smem
+            # k_fir_short_smem in between (FMA-bound)
             nh = self.w.nh
             use_tc = self.mode == "tc" or (self.mode in ("fast", "auto") and nh >= 80)
-            self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 32 else "k_fir_short_smem")
+            self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 8 else "k_fir_tapreg" if nh <= 32
+                                                     else "k_fir_short_smem")
             self.hbm_bound = nh <= 32 and not use_tc
             if use_tc:
                 self.tc_padded_macs = self.tc_padded([self.w.nout], 1, nh)
@@ -311,7 +313,7 @@ class Work:
             return
         nh = self.w.nh
         use_tc = self.mode == "tc" or (self.mode in ("fast", "auto") and nh >= 256)
-        self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 32 else
+        self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 8 else "k_fir_tapreg" if nh <= 32 else
                                                  "k_fir_short_smem" if nh <= 256 else "k_fir_f32_fast")
         if use_tc:
             if self.cfg == "cfg4":

@@ -29,6 +29,8 @@
 //    to a workspace and a second kernel sums them in fixed split order
 //    (deterministic, no atomics).  grid.z = channel (batched multichannel).
 
+#include <cstdlib>
+
 #include "sc_common.cuh"
 
 namespace sc {
@@ -257,16 +259,19 @@ __global__ void k_pad_taps(const float *__restrict__ h, int64_t ldh, int64_t nh,
 // them cannot leak.  Tiles whose window leaves the valid input range [x_lo,
 // x_hi) (the first and last few) take a guarded scalar path that multiplies
 // only taps whose input exists -- the reference's edge semantics.
+// (16 outputs per thread measured slower at every length: lanes 64 B apart
+// double the L1 wavefronts per LDG.128 along with the FFMAs it feeds.)
 constexpr int SH_THREADS = 256;
 constexpr int SH_R = 8;
-constexpr int SH_TILE = SH_THREADS * SH_R;  // 2048 outputs per CTA
 constexpr int SH_MAXNH = 256;
 
-template <int NKB>
+template <int NKB, int SH_R>
 __global__ void __launch_bounds__(SH_THREADS) k_fir_short(const float *__restrict__ x, int64_t ldx, int64_t x_base,
                                                           int64_t x_lo, int64_t x_hi, const float *__restrict__ h,
                                                           int64_t ldh, int nh, float *__restrict__ y, int64_t ldy,
                                                           int64_t n_begin, int64_t n_end, const unsigned *run_if) {
+    constexpr int SH_TILE = SH_THREADS * SH_R;  // outputs per CTA
+    constexpr int NW = SH_R / 4 + 1;            // float4s in the register window
     __shared__ __align__(16) float hsm[4 * NKB];
     if (run_if && *run_if == 0) return;
     const int ch = blockIdx.y;
@@ -291,41 +296,61 @@ __global__ void __launch_bounds__(SH_THREADS) k_fir_short(const float *__restric
     if (interior && nkb == NKB && nfull == NKB) {
         // Nh == 4*NKB: the tap-block loop is entirely compile-time (no
         // per-block tests, the window shift is pure register renaming)
+        // g[c] = x[t0 - 4 + 4c .. t0 + 4c - 1]: window of taps 4kb..4kb+3
         const float4 *xp = reinterpret_cast<const float4 *>(xc + (t0 - x_base));
-        float4 g2 = __ldg(xp + 1), g1 = __ldg(xp), g0 = __ldg(xp - 1);
+        float4 g[NW];
+#pragma unroll
+        for (int c = 0; c < NW; ++c) g[c] = __ldg(xp + c - 1);
         const float4 *h4 = reinterpret_cast<const float4 *>(hsm);
 #pragma unroll
         for (int kb = 0; kb < NKB; ++kb) {
-            const float w[12] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, g2.y, g2.z, g2.w};
+            float w[4 * NW];
+#pragma unroll
+            for (int c = 0; c < NW; ++c) {
+                w[4 * c] = g[c].x;
+                w[4 * c + 1] = g[c].y;
+                w[4 * c + 2] = g[c].z;
+                w[4 * c + 3] = g[c].w;
+            }
             const float4 hq = h4[kb];
             const float hk[4] = {hq.x, hq.y, hq.z, hq.w};
-            float4 gn = g0;
+            float4 gn = g[0];
             if (kb + 1 < NKB) gn = __ldg(xp - (kb + 2));  // next window in flight during the FMAs
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
                 for (int r = 0; r < SH_R; ++r) acc[r] = fmaf(w[r - u + 4], hk[u], acc[r]);
-            g2 = g1;
-            g1 = g0;
-            g0 = gn;
+#pragma unroll
+            for (int c = NW - 1; c > 0; --c) g[c] = g[c - 1];
+            g[0] = gn;
         }
         float4 *d = reinterpret_cast<float4 *>(yc + (t0 - n_begin));
-        d[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        d[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+#pragma unroll
+        for (int c = 0; c < SH_R / 4; ++c)
+            d[c] = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
         return;
     }
     if (interior) {
         const float4 *xp = reinterpret_cast<const float4 *>(xc + (t0 - x_base));  // x[t0 .. t0+3]
-        float4 g2 = __ldg(xp + 1), g1 = __ldg(xp), g0 = __ldg(xp - 1);        // x[t0-4 .. t0+7]
+        float4 g[NW];                                                             // x[t0-4 .. t0+SH_R-1]
+#pragma unroll
+        for (int c = 0; c < NW; ++c) g[c] = __ldg(xp + c - 1);
         const float4 *h4 = reinterpret_cast<const float4 *>(hsm);
 #pragma unroll
         for (int kb = 0; kb < NKB; ++kb) {
             if (kb < nkb) {
-                const float w[12] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, g2.y, g2.z, g2.w};
+                float w[4 * NW];
+#pragma unroll
+                for (int c = 0; c < NW; ++c) {
+                    w[4 * c] = g[c].x;
+                    w[4 * c + 1] = g[c].y;
+                    w[4 * c + 2] = g[c].z;
+                    w[4 * c + 3] = g[c].w;
+                }
                 const float4 hq = h4[kb];
                 const float hk[4] = {hq.x, hq.y, hq.z, hq.w};
                 // next window (x[t0-4kb-8 .. t0-4kb-5]) in flight during the FMAs
-                const float4 gn = kb + 1 < nkb ? __ldg(xp - (kb + 2)) : g0;
+                const float4 gn = kb + 1 < nkb ? __ldg(xp - (kb + 2)) : g[0];
                 if (kb < nfull) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
@@ -338,14 +363,15 @@ __global__ void __launch_bounds__(SH_THREADS) k_fir_short(const float *__restric
 #pragma unroll
                             for (int r = 0; r < SH_R; ++r) acc[r] = fmaf(w[r - u + 4], hk[u], acc[r]);
                 }
-                g2 = g1;
-                g1 = g0;
-                g0 = gn;
+#pragma unroll
+                for (int c = NW - 1; c > 0; --c) g[c] = g[c - 1];
+                g[0] = gn;
             }
         }
         float4 *d = reinterpret_cast<float4 *>(yc + (t0 - n_begin));
-        d[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        d[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+#pragma unroll
+        for (int c = 0; c < SH_R / 4; ++c)
+            d[c] = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
         return;
     }
     // edge tiles: scalar, only taps whose input exists, k ascending
@@ -360,6 +386,173 @@ __global__ void __launch_bounds__(SH_THREADS) k_fir_short(const float *__restric
 #pragma unroll
     for (int r = 0; r < SH_R; ++r)
         if (t0 + r < n_end) yc[t0 + r - n_begin] = acc[r];
+}
+
+// ---------------------------------------------------------------- short filters, taps in registers (Nh <= 64)
+// Tap-stationary form: every thread holds the whole filter in registers and
+// walks C chunks of 4 consecutive outputs, keeping the last 4*NH4+4 inputs in
+// a register ring of NH4+1 float4 slots (the chunk loop is unrolled by NH4+1,
+// so advancing the window is register renaming).  Per chunk a thread reads
+// ONE float4 of x and writes one float4 of y, both in shared memory, for
+// 4*Nh FFMA: at 32 taps 128 FFMA per LDS.128 + STS.128 (the register-window
+// kernel above needs one L1 wavefront per 4 FFMA there).  The CTA stages its
+// x tile (+ the 4*NH4-sample halo) with coalesced 16-byte loads and copies
+// the y tile out the same way.  Lane stride in smem is C float4s, C odd, so
+// LDS/STS.128 are conflict-free.
+// Each output is one fmaf chain over taps k = 0..Nh-1 ascending from +0 --
+// bit-identical to k_fir_short.  Edge tiles (inputs outside [x_lo, x_hi) or
+// a partial tile) multiply only taps whose input exists.
+constexpr int TR_THREADS = 128;
+
+template <int NH4>
+struct TapReg {
+    // ring of S >= NH4+1 float4 slots, S odd; C = chunks per thread, a
+    // multiple of S (so a whole number of ring cycles) and odd (so the lane
+    // stride in smem is conflict-free for LDS/STS.128)
+    static constexpr int S = (NH4 % 2 == 0) ? NH4 + 1 : NH4 + 2;
+    static constexpr int C = S < 5 ? 3 * S : S;
+    static constexpr int TILE = TR_THREADS * 4 * C;    // outputs per CTA
+    static constexpr int NX4 = TR_THREADS * C + NH4;   // staged x float4s (halo first)
+    static constexpr int SMEM = 16 * (NX4 + TR_THREADS * C);
+};
+
+template <int NH4>
+__device__ __forceinline__ void tapreg_walk(const float4 *xs, float4 *ys, const float (&hr)[4 * NH4], int nh) {
+    using T = TapReg<NH4>;
+    constexpr int S = T::S;
+    const int f0 = threadIdx.x * T::C;  // x float4 of this thread's first window; y float4 of its first chunk
+    float4 W[S];
+#pragma unroll
+    for (int q = 0; q < NH4; ++q) W[q] = xs[f0 + q];
+#pragma unroll 1
+    for (int g = 0; g < T::C / S; ++g) {
+#pragma unroll
+        for (int jj = 0; jj < S; ++jj) {
+            const int j = g * S + jj;
+            // float4 f0+j+q of the window lives in W[(jj+q) % S]; the newest
+            // one (q = NH4) is loaded here
+            W[(jj + NH4) % S] = xs[f0 + j + NH4];
+            float xw[4 * NH4 + 4];
+#pragma unroll
+            for (int q = 0; q <= NH4; ++q) {
+                const float4 v = W[(jj + q) % S];
+                xw[4 * q] = v.x;
+                xw[4 * q + 1] = v.y;
+                xw[4 * q + 2] = v.z;
+                xw[4 * q + 3] = v.w;
+            }
+            // output i of the chunk (n = n_first + 4j + i) times tap k reads
+            // x[n-k] = xw[4*NH4 + i - k]
+            float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+            for (int k = 0; k < 4 * NH4; ++k) {
+                if (k >= 4 * (NH4 - 1) && k >= nh) break;  // taps past Nh are never multiplied
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[i] = fmaf(xw[4 * NH4 + i - k], hr[k], acc[i]);
+            }
+            ys[f0 + j] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        }
+    }
+}
+
+// One tile per CTA (blockIdx.x = tile, blockIdx.y = channel); several CTAs
+// per SM overlap one tile's staging with another's FMAs (a persistent
+// double-buffered loop measured slower: it doubled the registers).
+// Edge tiles: plain runtime loops over the same stage (structurally unlike the
+// unrolled walk, so the compiler cannot merge the two into one predicated
+// body), multiplying only taps whose input exists.
+template <int NH4>
+__device__ __forceinline__ void tapreg_walk_edge(const float4 *xs, float4 *ys, const float *hc, int nh,
+                                                 int64_t n_first, int64_t x_lo, int64_t x_hi) {
+    using T = TapReg<NH4>;
+    const float *xsf = reinterpret_cast<const float *>(xs);
+    const int f0 = threadIdx.x * T::C;
+#pragma unroll 1
+    for (int j = 0; j < T::C; ++j) {
+        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll 1
+        for (int k = 0; k < nh; ++k) {
+            const float hk = __ldg(hc + k);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int64_t m = n_first + 4 * j + i - k;
+                if (m >= x_lo && m < x_hi) acc[i] = fmaf(xsf[4 * (f0 + j) + 4 * NH4 + i - k], hk, acc[i]);
+            }
+        }
+        ys[f0 + j] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    }
+}
+
+template <int NH4>
+__global__ void __launch_bounds__(TR_THREADS) k_fir_tapreg(const float *__restrict__ x, int64_t ldx, int64_t x_base,
+                                                           int64_t x_lo, int64_t x_hi, const float *__restrict__ h,
+                                                           int64_t ldh, int nh, float *__restrict__ y, int64_t ldy,
+                                                           int64_t n_begin, int64_t n_end, const unsigned *run_if) {
+    using T = TapReg<NH4>;
+    extern __shared__ float4 tr_smem[];  // T::SMEM bytes: the x stage, then the y stage
+    float4 *xs = tr_smem;
+    float4 *ys = tr_smem + T::NX4;
+    if (run_if && *run_if == 0) return;
+    const int ch = blockIdx.y;
+    const float *xc = x + (int64_t)ch * ldx;
+    const float *hc = h + (int64_t)ch * ldh;
+    float *yc = y + (int64_t)ch * ldy;
+    float hr[4 * NH4];  // warp-uniform: the compiler keeps them in uniform registers where they fit
+#pragma unroll
+    for (int k = 0; k < 4 * NH4; ++k) hr[k] = k < nh ? __ldg(hc + k) : 0.0f;
+    const int64_t n0 = n_begin + (int64_t)blockIdx.x * T::TILE;
+    const int64_t m0 = n0 - 4 * NH4;  // input index of staged float4 0
+    const float *src = xc + (m0 - x_base);
+    const bool edge = m0 < x_lo || n0 + T::TILE > x_hi || n0 + T::TILE > n_end;
+    if (!edge && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        // 16-byte async copies: the whole stage in flight without registers
+        const uint32_t xs_s = (uint32_t)__cvta_generic_to_shared(xs);
+        for (int f = threadIdx.x; f < T::NX4; f += TR_THREADS)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(xs_s + 16 * f), "l"(src + 4 * f)
+                         : "memory");
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+    } else {
+        float *xsf = reinterpret_cast<float *>(xs);
+        for (int i = threadIdx.x; i < 4 * T::NX4; i += TR_THREADS) {
+            const int64_t m = m0 + i;
+            xsf[i] = (m >= x_lo && m < x_hi) ? __ldg(xc + (m - x_base)) : 0.0f;
+        }
+    }
+    __syncthreads();
+    const int64_t n_first = n0 + (int64_t)threadIdx.x * 4 * T::C;
+    if (!edge)
+        tapreg_walk<NH4>(xs, ys, hr, nh);
+    else
+        tapreg_walk_edge<NH4>(xs, ys, hc, nh, n_first, x_lo, x_hi);
+    __syncthreads();
+    float *dst = yc + (n0 - n_begin);
+    if (!edge && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        float4 *d4 = reinterpret_cast<float4 *>(dst);
+        for (int f = threadIdx.x; f < TR_THREADS * T::C; f += TR_THREADS) d4[f] = ys[f];
+    } else {
+        const float *ysf = reinterpret_cast<const float *>(ys);
+        const int64_t lim = n_end - n0 < T::TILE ? n_end - n0 : T::TILE;
+        for (int i = threadIdx.x; i < lim; i += TR_THREADS) dst[i] = ysf[i];
+    }
+}
+
+constexpr int TR_MAXNH4 = 8;
+
+template <int NH4>
+int launch_tapreg(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi, const float *h,
+                  int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin, int64_t n_end,
+                  int64_t channels, cudaStream_t stream, const unsigned *run_if) {
+    using T = TapReg<NH4>;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(k_fir_tapreg<NH4>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+    SC_REQUIRE(attr == cudaSuccess, "fir: tap-register kernel smem attribute: %s", cudaGetErrorString(attr));
+    const int64_t tiles = cdiv(n_end - n_begin, (int64_t)T::TILE);
+    SC_REQUIRE(tiles < (int64_t)INT32_MAX, "fir: output range too large");
+    dim3 g((unsigned)tiles, (unsigned)channels);
+    k_fir_tapreg<NH4><<<g, TR_THREADS, T::SMEM, stream>>>(x, ldx, x_base, x_lo, x_hi, h, ldh, (int)nh, y, ldy,
+                                                          n_begin, n_end, run_if);
+    SC_CHECK_LAUNCH();
+    return SC_OK;
 }
 
 // ---------------------------------------------------------------- short filters, FMA-bound (32 < Nh <= 256)
@@ -543,6 +736,29 @@ int launch_fir_f32_fast(const float *x, int64_t ldx, int64_t x_base, int64_t x_l
     if (n_len <= 0 || channels <= 0) return SC_OK;
     SC_REQUIRE(nh >= 1, "fir: empty impulse response");
     SC_REQUIRE(channels < 65536, "fir: too many channels");
+    // 9..32 taps: the tap-stationary kernel (16 taps 0.096 vs 0.103 ms, 32 taps
+    // 0.135 vs 0.146 on 2^26 outputs); <= 8 taps the register-window kernel
+    // (HBM-bound, 0.93 of the copy bandwidth; tap-stationary 0.091 ms); 33..256
+    // the smem kernel (tap-stationary with 64 taps in registers: par, and
+    // an FFMA2 pairing of the tap-stationary walk measured slower everywhere)
+    static const int knob_kind = [] {  // experiment knob: 1 = default choice, 0 = never tap-stationary
+        const char *v = getenv("SC_SHORT_KIND");
+        return v ? atoi(v) : 1;
+    }();
+    if (knob_kind == 1 && nh > 8 && nh <= 4 * TR_MAXNH4) {
+        const int nh4 = (int)((nh + 3) / 4);
+        int rc = SC_OK;
+#define SC_TAPREG(N)                                                                                        \
+    case N: rc = launch_tapreg<N>(x, ldx, x_base, x_lo, x_hi, h, ldh, nh, y, ldy, n_begin, n_end, channels, \
+                                  stream, run_if);                                                          \
+        break
+        switch (nh4) {
+            SC_TAPREG(3); SC_TAPREG(4); SC_TAPREG(5); SC_TAPREG(6); SC_TAPREG(7); SC_TAPREG(8);
+            default: SC_REQUIRE(false, "fir: tap-register kernel, bad tap count");
+        }
+#undef SC_TAPREG
+        return rc;
+    }
     if (nh > 32 && nh <= SH_MAXNH) {
         const int64_t tiles = cdiv(n_len, SM_TILE);
         SC_REQUIRE(tiles < (int64_t)INT32_MAX, "fir: output range too large");
@@ -553,21 +769,19 @@ int launch_fir_f32_fast(const float *x, int64_t ldx, int64_t x_base, int64_t x_l
         return SC_OK;
     }
     if (nh <= SH_MAXNH) {
-        const int64_t tiles = cdiv(n_len, SH_TILE);
+        const int64_t tiles = cdiv(n_len, (int64_t)SH_THREADS * SH_R);
         SC_REQUIRE(tiles < (int64_t)INT32_MAX, "fir: output range too large");
         dim3 g((unsigned)tiles, (unsigned)channels);
-#define SC_SHORT(NKB) k_fir_short<NKB><<<g, SH_THREADS, 0, stream>>>(x, ldx, x_base, x_lo, x_hi, h, ldh, (int)nh, \
-                                                                   y, ldy, n_begin, n_end, run_if)
-        // NKB = ceil(Nh/4) exactly for multiples of 4 (the compile-time path)
+#define SC_SHORT(NKB)                                                                                          \
+    case NKB:                                                                                                  \
+        k_fir_short<NKB, SH_R><<<g, SH_THREADS, 0, stream>>>(x, ldx, x_base, x_lo, x_hi, h, ldh, (int)nh, y, ldy, \
+                                                             n_begin, n_end, run_if);                              \
+        break
+        // NKB = ceil(Nh/4) exactly (the compile-time path for multiples of 4)
         switch ((int)((nh + 3) / 4)) {
-            case 1: SC_SHORT(1); break;
-            case 2: SC_SHORT(2); break;
-            case 3: SC_SHORT(3); break;
-            case 4: SC_SHORT(4); break;
-            case 5: SC_SHORT(5); break;
-            case 6: SC_SHORT(6); break;
-            case 7: SC_SHORT(7); break;
-            default: SC_SHORT(8); break;
+            SC_SHORT(1); SC_SHORT(2); SC_SHORT(3); SC_SHORT(4);
+            SC_SHORT(5); SC_SHORT(6); SC_SHORT(7); SC_SHORT(8);
+            default: SC_REQUIRE(false, "fir: short kernel, bad tap count");
         }
 #undef SC_SHORT
         SC_CHECK_LAUNCH();

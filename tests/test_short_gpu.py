@@ -17,7 +17,7 @@ def _tol(x, h):
     return 1e-5 * float(np.max(np.abs(x))) * float(np.sum(np.abs(h)))
 
 
-@pytest.mark.parametrize("nh", [1, 2, 3, 4, 5, 8, 9, 12, 16, 17, 20, 24, 28, 31, 32, 33, 64, 100, 128, 129, 200, 255])
+@pytest.mark.parametrize("nh", [1, 2, 3, 4, 5, 8, 9, 12, 16, 17, 20, 24, 28, 31, 32, 33, 36, 47, 60, 63, 64, 65, 100, 128, 129, 200, 255])
 @pytest.mark.parametrize("ne", [1, 7, 2048, 70_001])
 def test_short_whole_signal(ne, nh):
     from paper_2401_01607_b200.core import Signal, scatter_convolve
@@ -32,7 +32,7 @@ def test_short_whole_signal(ne, nh):
         assert np.max(np.abs(y - ref)) <= _tol(x, h), mode
 
 
-@pytest.mark.parametrize("nh", [8, 64, 250])
+@pytest.mark.parametrize("nh", [8, 13, 20, 32, 64, 250])
 def test_short_shards_and_misaligned_slices(nh):
     import torch
 
