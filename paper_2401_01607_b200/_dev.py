@@ -32,14 +32,35 @@ def torch_dtype(npd):
     return t.float32 if npd == np.float32 else t.float64
 
 
+class device_guard:
+    """`torch.cuda.device(d)` without its Python overhead: switches the current
+    device only when it differs (engine calls are made on their own device
+    almost always)."""
+
+    __slots__ = ("idx", "prev")
+
+    def __init__(self, device):
+        self.idx = device.index if hasattr(device, "index") else int(device)
+
+    def __enter__(self):
+        self.prev = torch()._C._cuda_exchangeDevice(self.idx)
+        return self
+
+    def __exit__(self, *exc):
+        if self.prev != self.idx:
+            torch()._C._cuda_exchangeDevice(self.prev)
+        return False
+
+
 def as_device(a, npd, device=None):
     """Contiguous CUDA tensor of dtype npd holding a (ndarray or tensor)."""
     t = torch()
     td = torch_dtype(npd)
     if is_tensor(a) and a.is_cuda and a.dtype == td and a.is_contiguous():
         # already in place: skip the .to() dispatch (hot in fused streaming calls)
-        want = t.device(device).index if device is not None else t.cuda.current_device()
-        if a.device.index == want:
+        want = device.index if isinstance(device, t.device) else (
+            t.device(device).index if device is not None else t._C._cuda_getDevice())
+        if a.get_device() == want:
             return a
     dev = device if device is not None else t.device("cuda", t.cuda.current_device())
     if is_tensor(a):
@@ -53,6 +74,14 @@ def as_device_many(arrays, npd, device=None):
     (packed on the host, split on the device) instead of one small copy each
     (an IR-swap schedule of 19 host IRs: one ~50 us upload, not 19 dispatches)."""
     t = torch()
+    td = torch_dtype(npd)
+    if arrays and all(isinstance(a, t.Tensor) for a in arrays):
+        # fast path: every array already a contiguous CUDA tensor of the right
+        # dtype on the target device (an IR schedule held on the device)
+        want = device.index if isinstance(device, t.device) else (
+            t.device(device).index if device is not None else t._C._cuda_getDevice())
+        if all(a.get_device() == want and a.dtype == td and a.is_contiguous() for a in arrays):
+            return list(arrays)
     host = [a for a in arrays if not (is_tensor(a) and a.is_cuda)]
     if len(host) < 2 or len(host) != len(arrays) or any(np.ndim(a) == 0 for a in arrays):
         return [as_device(a, npd, device=device) for a in arrays]

@@ -141,10 +141,18 @@ def dtype_code(dtype) -> int:
 
 
 def stream_ptr(stream=None):
+    """cudaStream_t of `stream`, or of the current device's current stream.
+    The default path asks torch's C layer directly (~0.3 us instead of ~10 us
+    through torch.cuda.current_stream(), which dominated small engine calls)."""
     import torch
 
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return ctypes.c_void_p(s.cuda_stream)
+    if stream is not None:
+        return ctypes.c_void_p(stream.cuda_stream)
+    C = torch._C
+    raw = getattr(C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return ctypes.c_void_p(raw(C._cuda_getDevice()))
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
 def ptr(t) -> ctypes.c_void_p:

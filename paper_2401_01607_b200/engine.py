@@ -92,7 +92,7 @@ class ScatterEngine:
         self._pending_ir = None
         self._handle = ctypes.c_void_p()
         hd = self._to_dev(h.samples)
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             N.check(self._lib.sc_engine_create(self._dt, N.ptr(hd), len(h),
                                                int(self.config.block_size_nb),
                                                float(self.config.zero_skip_threshold),
@@ -122,7 +122,7 @@ class ScatterEngine:
         ri, live, cap, cons, nh = (ctypes.c_int64() for _ in range(5))
         pend = ctypes.c_int()
         t = _dev.torch()
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             self._bind_stream()
             N.check(self._lib.sc_engine_state(self._handle, ctypes.byref(ri), ctypes.byref(live),
                                               ctypes.byref(cap), ctypes.byref(cons),
@@ -149,7 +149,7 @@ class ScatterEngine:
         """The impulse response in force (engine.py:91-93): read back from the
         engine's own device copy, in the currency of the IR last given."""
         t = _dev.torch()
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             buf = t.empty(self._nh, dtype=_dev.torch_dtype(self._npd), device=self._device)
             n = ctypes.c_int64()
             self._bind_stream()
@@ -170,7 +170,7 @@ class ScatterEngine:
         """Consume one input sample, return the output sample it completes
         (engine.py:99-116; a pending swap is not applied)."""
         t = _dev.torch()
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             xd = t.tensor([x], dtype=_dev.torch_dtype(self._npd), device=self._device)
             out = t.empty(1, dtype=xd.dtype, device=self._device)
             self._bind_stream()
@@ -196,7 +196,7 @@ class ScatterEngine:
                 f"sample rates differ: block {block.sample_rate} Hz vs engine {self._sample_rate} Hz"
             )
         t = _dev.torch()
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             xd = self._to_dev(block.samples)
             out = t.empty(len(block), dtype=xd.dtype, device=self._device)
             if len(block):
@@ -209,7 +209,7 @@ class ScatterEngine:
         """Emit the pending residue and reset the engine (engine.py:148-161):
         max(len(ir)-1, live) samples in emission order."""
         t = _dev.torch()
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             self._bind_stream()
             cap = ctypes.c_int64()
             N.check(self._lib.sc_engine_tail_bound(self._handle, ctypes.byref(cap)))
@@ -231,7 +231,7 @@ class ScatterEngine:
                 f"vs engine {self._sample_rate} Hz"
             )
         t = _dev.torch()
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             hd = self._to_dev(h_new.samples)
             self._bind_stream()
             N.check(self._lib.sc_engine_swap_ir(self._handle, N.ptr(hd), len(h_new)))
@@ -265,7 +265,7 @@ class ScatterEngine:
     def _schedule_order(self) -> np.ndarray:
         """Ring contents reordered so index 0 is the next slot to emit (engine.py:211-214)."""
         t = _dev.torch()
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             st = self._state()
             buf = t.empty(max(st["cap"], 1), dtype=_dev.torch_dtype(self._npd), device=self._device)
             n = ctypes.c_int64()
@@ -295,7 +295,7 @@ class ScatterEngine:
             h_new, self._pending_ir = self._pending_ir, None
             self.swap_ir(h_new)
         t = _dev.torch()
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             xs = x.samples if isinstance(x, Signal) else x
             swaps = sorted(swaps, key=lambda s: s[0])
             irs = _dev.as_device_many([s[1].samples if isinstance(s[1], Signal) else s[1] for s in swaps],

@@ -137,7 +137,7 @@ class MultiChannelEngine:
         self._pending = None
         h_dev = _dev.as_device(hd, npd, device=self._device).contiguous()
         self._handle = ctypes.c_void_p()
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             N.check(self._lib.sc_engine_create_multi(self._dt, N.ptr(h_dev), h_dev.shape[1], self._C,
                                                      int(self.config.block_size_nb),
                                                      float(self.config.zero_skip_threshold),
@@ -196,7 +196,7 @@ class MultiChannelEngine:
         if self._pending is not None:
             h_new, self._pending = self._pending, None
             self.swap_ir(h_new)
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             xd = self._rows(block)
             n = xd.shape[1]
             if n > self.config.block_size_nb:
@@ -210,7 +210,7 @@ class MultiChannelEngine:
     def process_sample(self, x):
         """One sample per channel ([C]) -> [C] outputs (engine.py:99-116)."""
         t = _dev.torch()
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             xd = _dev.as_device(np.asarray(x, dtype=self._npd).reshape(self._C, 1), self._npd, device=self._device)
             out = t.empty_like(xd)
             self._bind()
@@ -220,7 +220,7 @@ class MultiChannelEngine:
     def swap_ir(self, h_new):
         """Every channel swaps to its row of h_new (or a broadcast mono IR)."""
         t = _dev.torch()
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             hd = self._ir_rows(h_new)
             self._bind()
             N.check(self._lib.sc_engine_swap_ir(self._handle, N.ptr(hd), hd.shape[1]))
@@ -237,7 +237,7 @@ class MultiChannelEngine:
         import ctypes
 
         t = _dev.torch()
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             self._bind()
             cap = ctypes.c_int64()
             N.check(self._lib.sc_engine_tail_bound(self._handle, ctypes.byref(cap)))
@@ -258,7 +258,7 @@ class MultiChannelEngine:
         cons, nh = ctypes.c_int64(), ctypes.c_int64()
         pend = ctypes.c_int()
         t = _dev.torch()
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             self._bind()
             N.check(self._lib.sc_engine_state(self._handle, ri, live, cap, ctypes.byref(cons), ctypes.byref(nh),
                                               ctypes.byref(pend)))
@@ -280,7 +280,7 @@ class MultiChannelEngine:
         if self._pending is not None:
             h_new, self._pending = self._pending, None
             self.swap_ir(h_new)
-        with t.cuda.device(self._device):
+        with _dev.device_guard(self._device):
             swaps = sorted(swaps, key=lambda s: s[0])
             irs = self._ir_rows_many([s[1] for s in swaps])
             k = len(swaps)
