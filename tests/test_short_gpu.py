@@ -66,3 +66,33 @@ def test_short_batched_pitch():
     for c in range(5):
         ref = O.scatter_full(X[c], H[c])
         assert np.max(np.abs(Y[c].astype(np.float64) - ref)) <= _tol(X[c], H[c])
+
+
+@pytest.mark.parametrize("nh", [9, 16, 30, 32])
+def test_tapreg_bit_identical_to_register_window(nh, tmp_path):
+    """k_fir_tapreg (9..32 taps) keeps k_fir_short's per-output chain (fmaf
+    over taps ascending from +0), so both kernels give the same bits.  The
+    kernel choice is read once per process (SC_SHORT_KIND), hence two
+    subprocesses."""
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    prog = (
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {repo!r})\n"
+        "from paper_2401_01607_b200 import Signal, scatter_convolve\n"
+        "rng = np.random.default_rng(77)\n"
+        "x = rng.uniform(-1, 1, 300_001).astype(np.float32)\n"
+        f"h = rng.standard_normal({nh}).astype(np.float32)\n"
+        "y = scatter_convolve(Signal(torch.from_numpy(x).cuda()), Signal(torch.from_numpy(h).cuda()))\n"
+        "np.save(sys.argv[1], y.concatenated().samples.cpu().numpy())\n"
+    )
+    outs = []
+    for kind in ("0", "1"):
+        f = str(tmp_path / f"y{kind}.npy")
+        env = dict(os.environ, SC_SHORT_KIND=kind)
+        subprocess.run([sys.executable, "-c", prog, f], check=True, env=env, timeout=300)
+        outs.append(np.load(f))
+    assert outs[0].dtype == np.float32 and np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
