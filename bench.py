@@ -60,7 +60,34 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0,
                     help="target seconds of CPU work for the cpu_baseline sample")
+    # CPU test mode (SC_BENCH_COMPUTE=oracle): the multi-rank sharding, timing
+    # and reporting logic with the CPU oracle standing in for the kernel, on a
+    # reduced cfg5-law signal -- for tests/test_bench_cpu.py under gloo; never
+    # a GPU number (its line says so)
+    ap.add_argument("--test-ne", type=int, default=0, help=argparse.SUPPRESS)
+    ap.add_argument("--test-nh", type=int, default=0, help=argparse.SUPPRESS)
     return ap.parse_args()
+
+
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch this script as N ranks
+    (one process per GPU) under torch.distributed.run on 127.0.0.1; rank 0
+    prints the JSON line on the shared stdout."""
+    import subprocess
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(REPO / "bench.py"),
+           *sys.argv[1:]]
+    print(f"[bench] spawning {args.gpus} ranks: {' '.join(cmd[2:7])}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
 
 
 def env_rank():
@@ -254,22 +281,10 @@ class Work:
             self.scaling = "weak"
             self.dtype = "f32"
 
-    @staticmethod
-    def tc_padded(n_lens, channels, nh, sms=148):
-        """Padded MMA MACs of one k_tc_fir launch over batches of output
-        lengths n_lens (x channels), mirroring the library's tile choice
-        (256-row tiles when they fill the SMs twice, else 128) and drain
-        period (2 shifts for <= 2-shift filters, else 8)."""
-        s_needed = (nh + 126) // 128 + 1
-        s8 = 2 if s_needed <= 2 else -(-s_needed // 8) * 8
-        wide = sum(-(-n // 32768) for n in n_lens) * channels >= 2 * sms
-        tile = 32768 if wide else 16384
-        return sum(-(-n // tile) for n in n_lens) * channels * tile * 128 * s8
-
     def pick_kernel(self):
-        """Which kernel the library runs for this config/mode (mirrors capi.cu's
-        FAST dispatch) and the padded tensor-core work it issues."""
-        self.tc_padded_macs = 0
+        """Which kernel family the library runs for this config/mode (mirrors
+        capi.cu's FAST dispatch).  The tensor-core work it issues is read from
+        the library itself (sc_tc_stats) around the timed region."""
         if self.cfg.startswith("short"):
             # FAST dispatch (capi.cu / k_fast_f32.cu): tensor cores from 80
             # taps at this size, the streaming k_fir_short up to 8 taps and
@@ -280,8 +295,6 @@ class Work:
             self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 8 else "k_fir_tapreg" if nh <= 32
                                                      else "k_fir_short_smem")
             self.hbm_bound = nh <= 32 and not use_tc
-            if use_tc:
-                self.tc_padded_macs = self.tc_padded([self.w.nout], 1, nh)
             return
         if self.cfg == "cfg2":
             # float32 engine: FAST mode convolves the 19 equal IR segments in one
@@ -289,10 +302,6 @@ class Work:
             fast = self.mode != "ordered"
             self.eng = self._make_engine("fast" if fast else "ordered")
             self.kernel = "k_tc_fir" if fast else "k_chain_w"
-            if fast:
-                nh, seg = self.w.nh, 100 * 256
-                nseg = -(-self.w.ne // seg)
-                self.tc_padded_macs = self.tc_padded([seg + nh - 1] * nseg, 1, nh)
             return
         if self.cfg == "mstream":
             # float32 engine: FAST mode puts each IR segment (2 x 64 ch x 240,000
@@ -301,12 +310,6 @@ class Work:
             fast = self.mode != "ordered"
             self.eng = self._make_engine("fast" if fast else "ordered")
             self.kernel = "k_tc_fir" if fast else "k_chain_w"
-            if fast:
-                nh = self.w.nh
-                half = (-(-self.w.ne // 8192) // 2) * 8192
-                segs = [half, self.w.ne - half]
-                # the two segments are padded to the longer one and batched
-                self.tc_padded_macs = self.tc_padded([max(segs) + nh - 1] * 2, self.w.channels, nh)
             return
         if self.dtype != "f32" or self.cfg not in ("cfg3", "cfg4", "cfg5") or self.mode == "ordered":
             self.kernel = "k_chain_w"   # ordered chain (csrc/k_ordered.cu)
@@ -315,11 +318,6 @@ class Work:
         use_tc = self.mode == "tc" or (self.mode in ("fast", "auto") and nh >= 256)
         self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 8 else "k_fir_tapreg" if nh <= 32 else
                                                  "k_fir_short_smem" if nh <= 256 else "k_fir_f32_fast")
-        if use_tc:
-            if self.cfg == "cfg4":
-                self.tc_padded_macs = self.tc_padded([self.w.nout], self.c1 - self.c0, nh)
-            else:
-                self.tc_padded_macs = self.tc_padded([self.shard.n_out], 1, nh)
 
     def step(self):
         import torch
@@ -495,6 +493,75 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------------ CPU test mode
+
+
+def run_cpu_test_mode(args):
+    """SC_BENCH_COMPUTE=oracle: the same rank/shard/timing/report logic as the
+    GPU path, on CPU under gloo, with the oracle computing each rank's shard
+    of a reduced cfg5-law signal (--test-ne x --test-nh).  Rank 0 gathers the
+    shards (sharded.gather_shards) and checks they cover the full output and
+    equal the oracle's single-pass result.  Test infrastructure: the line
+    carries "compute": "oracle-cpu" and is never a benchmark number."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2401_01607_b200.sharded import gather_shards, shard_plan
+
+    rank, world, _ = env_rank()
+    if world > 1:
+        dist.init_process_group(os.environ.get("SC_DIST_BACKEND", "gloo"))
+    ne = args.test_ne or 40_000
+    nh = args.test_nh or 1_000
+    rng = np.random.default_rng((5, 0))
+    x = rng.uniform(-1, 1, ne).astype(np.float32)
+    h = (np.random.default_rng((5, 1)).standard_normal(nh) * np.exp(-np.arange(nh) / (nh / 6.5))).astype(np.float32)
+    plan = shard_plan(ne, nh, world)
+    sh = plan[rank]
+
+    def step():
+        xx = np.zeros(sh.x_end)
+        xx[sh.x_begin:] = x[sh.x_begin:sh.x_end]   # this rank sees only its slice + halo
+        return torch.from_numpy(O.scatter_window(xx, h, sh.n_begin, sh.n_end))
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        y = step()
+        times.append(time.perf_counter() - t0)
+    ms_local = 1000 * sum(times) / len(times)
+    if world > 1:
+        t = torch.tensor([ms_local], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        full = gather_shards(y, sh, world, dst=0)
+    else:
+        ms, full = ms_local, y
+    if rank == 0:
+        ref = O.scatter_full(x, h)
+        got = full.numpy()
+        line = {
+            "metric": METRIC, "value": (ne + nh - 1) * nh / (ms * 1e-3) / 1e9, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "compute": "oracle-cpu (SC_BENCH_COMPUTE=oracle test mode: no GPU, not a benchmark number)",
+            "config": {"workload": f"cfg5-law {ne}x{nh} (test mode)", "ne": ne, "nh": nh,
+                       "parallelism": f"time-sharded x{world} (output segments + {nh - 1}-sample halo)"},
+            "coverage": {"outputs": int(len(ref)), "gathered": int(len(got)),
+                         "shards": [[p.n_begin, p.n_end] for p in plan],
+                         "max_abs_err": float(np.max(np.abs(got - ref))) if len(got) == len(ref) else None},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 # ------------------------------------------------------------------ main
 
 
@@ -502,6 +569,10 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    if os.environ.get("SC_BENCH_COMPUTE") == "oracle":
+        return run_cpu_test_mode(args)
 
     import torch
     import torch.distributed as dist
@@ -520,8 +591,16 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        # make the communicator visible (and eagerly created): one tiny
+        # all-reduce, then report its rank count
+        probe = torch.ones(1, device=torch.device("cuda", local) if backend == "nccl" else "cpu")
+        dist.all_reduce(probe)
+        comm = {"backend": dist.get_backend(), "nranks": dist.get_world_size(), "allreduce_check": int(probe.item())}
+        print(f"[bench] rank {rank}: {comm['backend']} communicator nranks={comm['nranks']} "
+              f"device=cuda:{local}", file=sys.stderr, flush=True)
     else:
         torch.cuda.set_device(0)
+        comm = {"backend": None, "nranks": 1}
     device = torch.device("cuda", torch.cuda.current_device())
     L = N.lib()
     work = Work(args.config, rank, world, device)
@@ -549,6 +628,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     launches0 = L.sc_launch_count()
+    L.sc_tc_stats_reset()
     with ClockSampler(nvml_index) as clocks:
         t_wall0 = time.perf_counter()
         # ~1 ms of device-side spin ahead of the first step, so the host's
@@ -563,6 +643,7 @@ def main():
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
     launches = L.sc_launch_count() - launches0
+    tc = N.tc_stats()   # the library's own count of the tensor-core work it issued
     barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms_local = sum(step_ms) / len(step_ms)
@@ -580,7 +661,11 @@ def main():
     traffic = None
     tf = REPO / "profiles" / "ncu_traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get(f"{args.config}_{work.kernel}")
+        tt = json.loads(tf.read_text())
+        if work.kernel == "k_tc_fir" and tc["launches"]:
+            traffic = tt.get(f"{args.config}_k_tc_fir<{tc['ssh']},{tc['tile_n']}>")
+        else:
+            traffic = tt.get(f"{args.config}_{work.kernel}")
     if getattr(work, "hbm_bound", False):
         # short filters: the kernel should stream x in and y out at HBM speed
         hbm = float(p.get("hbm_gbs", 6650.0))
@@ -589,20 +674,26 @@ def main():
         roofline = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                     "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                     "alg_bytes_per_launch": alg_bytes, "kernel": work.kernel}
-    elif work.kernel == "k_tc_fir":
-        # tensor work actually issued: 3 fp16 MMAs (hi*hi, lo*hi, hi*lo) over the
-        # padded block-Toeplitz GEMM (whole 32768- or 16384-output tiles x 128 taps x s8 shifts)
+    elif work.kernel == "k_tc_fir" and tc["launches"]:
+        # tensor work actually issued, as the library counts it (sc_tc_stats):
+        # 3 fp16 MMAs (hi*hi, lo*hi, hi*lo) over the padded block-Toeplitz
+        # GEMM -- whole 128 x tile_n-row tiles x 128 taps x drain-padded shifts
         tc_peak = float(p.get("bf16_tflops", 1590.0))
-        achieved = 2 * 3 * work.tc_padded_macs / (ms_local * 1e-3) / 1e12
+        padded = tc["padded_macs"] / args.steps
+        achieved = 2 * 3 * padded / (ms_local * 1e-3) / 1e12
+        tmpl = f"k_tc_fir<{tc['ssh']},{tc['tile_n']}>"
+        work.kernel_template = tmpl
         roofline = {
             "bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
             "frac": achieved / tc_peak, "traffic": traffic,
             "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst, cuBLAS bf16; fp16 MMA runs at "
                            "the same rate)" if "bf16_tflops" in p else "fallback 1.59 PFLOP/s",
-            "achieved_per_launch": f"2 x 3 x {work.tc_padded_macs:.4e} padded MMA MACs / mean step time",
+            "achieved_per_launch": f"2 x 3 x {padded:.6e} padded MMA MACs per step (sc_tc_stats: "
+                                   f"{tc['launches'] / args.steps:g} launches/step) / mean step time",
             "useful_fp32_tflops": useful,
             "useful_frac_of_fp32_fma_peak": useful / fp32_peak,
-            "kernel": "k_tc_fir (tcgen05.mma kind::f16 128x128x16, TMEM accumulators, cp.async.bulk)",
+            "kernel": f"{tmpl} (tcgen05.mma kind::f16 M128 x N{tc['tile_n']} x K16, TMEM accumulators, "
+                      f"TMEM drain every {tc['ssh']} shifts, cp.async.bulk)",
         }
     elif work.dtype == "f64":
         # ordered float64 chain: every MAC is a DMUL and a DADD (separately
@@ -686,11 +777,12 @@ def main():
                        "l2": "256 MiB memset before every timed step (outside the events); "
                              "inputs also exceed L2 at N=1"},
             "pct_fp32_fma_peak": 100.0 * useful / fp32_peak,
-            "kernel": work.kernel,
+            "kernel": getattr(work, "kernel_template", work.kernel),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "comm": comm,
             "clocks": csum,
             "wall_s_timed_region": t_wall,
             "step_ms_rank0": step_ms,

@@ -76,6 +76,15 @@ const char *sc_last_error(void);
  * how many of the library's kernels ran there. */
 int64_t sc_launch_count(void);
 
+/* Tensor-core bookkeeping for the roofline (bench.py): cumulative k_tc_fir
+ * launches and the MACs their MMAs issue over the PADDED block-Toeplitz GEMM
+ * (whole tiles of 128*tile_n outputs x 128 taps x every drain-padded shift;
+ * each padded MAC is 3 fp16 MMA MACs: hi*hi, lo*hi, hi*lo), plus the last
+ * launch's template (drain period in shifts, tile width in output rows).
+ * No reference counterpart (bench instrumentation). */
+int sc_tc_stats(int64_t *launches, int64_t *padded_macs, int *last_ssh, int *last_tile_n);
+void sc_tc_stats_reset(void);
+
 /* ---------------------------------------------------------------- whole signal */
 
 /* Full linear convolution y[0 : ne+nh-1] = x (*) h.
@@ -184,6 +193,16 @@ int sc_engine_flush(sc_engine *e, void *tail, int64_t tail_capacity, int64_t *n_
  * a tail_capacity that always suffices for sc_engine_flush. */
 int sc_engine_tail_bound(sc_engine *e, int64_t *bound);
 
+/* flush (engine.py:148-161) split in two so that all of its device work is
+ * queued before its only host wait: _begin enqueues the tail copy (the
+ * sc_engine_tail_bound prefix of the schedule; samples past a channel's tail
+ * are zero), the state read-back into pinned memory and the reset; _end
+ * waits for the stream and returns each channel's tail length
+ * max(len(ir) - 1, live).  tail_capacity must be >= sc_engine_tail_bound.
+ * No other engine call may come between the two. */
+int sc_engine_flush_begin(sc_engine *e, void *tail, int64_t tail_capacity);
+int sc_engine_flush_end(sc_engine *e, int64_t *n_tail);
+
 /* State (engine.py:83-97): read_index, live, cap (= len(ring)), consumed,
  * current nh, has_pending.  Synchronous. */
 int sc_engine_state(sc_engine *e, int64_t *read_index, int64_t *live, int64_t *cap,
@@ -218,14 +237,31 @@ int sc_engine_process_blocks_host(sc_engine *e, const void *x_host, int64_t n_to
 
 /* ---------------------------------------------------------------- multi-GPU */
 
-/* Whole-signal convolution of a HOST signal x[ne] (pinned or pageable) with
- * h[nh] (host), partitioned by output time segment over ngpu devices
- * (devices[]; repeats allowed): device g computes outputs [a_g, b_g) from
- * its input slice plus the (nh-1)-sample halo -- no MAC repeated, no partial
- * sums exchanged, no reduction (SURVEY.md 8(b) sc_fir_sharded, north_star
- * (4)).  y[ne+nh-1] is a host pointer when gather_device < 0, else a device
- * pointer on gather_device filled by peer copies.  One host thread per shard;
- * synchronous.  mode as sc_fir_full; ORDERED float64 stays bit-identical to
+/* Outputs [n_begin, n_end) of the convolution of a HOST signal x[ne] with
+ * h[nh] (host, or a device pointer on `device`), computed on `device` and
+ * written to the host buffer y_host[n_end - n_begin].  Only inputs
+ * [max(0, n_begin-nh+1), min(ne, n_end)) are uploaded (the range's slice plus
+ * its halo).  The range is cut into `chunks` output chunks (0 = by size:
+ * one per >= 2^36 MACs or 16 MiB of input, 2..12) whose upload, FIR and
+ * download run on three persistent streams, so transfers in both directions
+ * overlap the kernels of neighbouring chunks; device buffers persist across
+ * calls.  Pinned x_host / y_host overlap fully; pageable ones are correct
+ * but serialise.  Synchronous.  mode as sc_fir_full.  The host-I/O leg of
+ * scatter_convolve (core.py:122-131) on one GPU, and one rank's shard in
+ * the time-sharded multi-GPU path. */
+int sc_fir_range_host(int dtype, int mode, const void *x_host, int64_t ne, const void *h, int64_t nh,
+                      void *y_host, int64_t n_begin, int64_t n_end, int device, int chunks);
+
+/* Whole-signal convolution of a HOST signal x[ne] with h[nh] (host),
+ * partitioned by output time segment over ngpu devices (devices[]; repeats
+ * allowed): device g computes outputs [a_g, b_g) from its input slice plus
+ * the (nh-1)-sample halo -- no MAC repeated, no partial sums exchanged, no
+ * reduction (SURVEY.md 8(b) sc_fir_sharded, north_star (4)).  Each device
+ * runs the chunk-pipelined range engine of sc_fir_range_host on its own host
+ * thread.  y[ne+nh-1] is a host pointer when gather_device < 0; else a
+ * device pointer on gather_device that the FIR epilogues store into directly
+ * (peer stores over NVLink; peer copies when peer access is unavailable).
+ * Synchronous.  mode as sc_fir_full; ORDERED float64 stays bit-identical to
  * the reference at any device count (every output's chain runs on one
  * device). */
 int sc_fir_sharded(int dtype, int mode, const void *x_host, int64_t ne, const void *h_host, int64_t nh, void *y,
@@ -260,6 +296,11 @@ int sc_peak_abs(int dtype, const void *x, int64_t n, unsigned long long *peak_bi
  * counters, initialise to 0.  word_bits in [2, 64]. */
 int sc_fixed_quantize(const double *x, int64_t n, int word_bits, int64_t *k, double *xq,
                       unsigned long long *stats, void *stream);
+
+/* t[i] / 2^shift rounded to nearest, ties to even, for int64 device arrays
+ * (0 <= shift <= 63) -- replaces the scalar helper _round_shift_half_even,
+ * quantize.py:145-154 (the requantisation step of both schemes). */
+int sc_fixed_round_shift(const int64_t *t, int64_t n, int shift, int64_t *out, void *stream);
 
 /* Exact-integer convolution of quantised ke[ne], kh[nh] (device) under one
  * requantisation scheme (0 "ideal": one half-even rounding per output;

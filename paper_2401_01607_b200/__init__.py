@@ -16,8 +16,10 @@ plus the B200 additions of the north_star: ``convolve_batched``
 Everything computes in the CUDA library built in-tree under ``_lib`` and
 called through its C ABI (include/scatterconv_b200.h).  There is no CPU
 fallback: without the library or a CUDA device every compute call raises.
-The reference's file I/O, CLI, fixed-point model and timing sweeps are out
-of scope.
+The reference's other public names (WAV I/O, fixed-point simulation, timing
+sweeps; pkg/src/scatterconv/__init__.py:1-85) are re-exported here too, so
+``from scatterconv import read_wav``-style code keeps working; their arithmetic
+runs on the device as well (csrc/k_wav.cu, csrc/k_fixed.cu, CUDA-event sweeps).
 """
 
 from . import configs
@@ -40,6 +42,17 @@ from .sharded import (
     shard_plan,
 )
 
+from .fixed_point import (
+    FixedPointFormat,
+    RequantReport,
+    fixed_point_convolve,
+    ideal_accumulator_bits,
+    ideal_bits_removed,
+    mac_requant_count,
+    quantize,
+    simulate_fixed_point_conv,
+)
+from .wav import WavFormatError, WavSpec, read_wav, write_wav
 from .sweeps import (
     BenchReport,
     BenchRow,
@@ -66,6 +79,18 @@ __all__ = [
     "ConvOutput",
     "DEFAULT_BLOCK_SIZE",
     "EngineConfig",
+    "FixedPointFormat",
+    "RequantReport",
+    "WavFormatError",
+    "WavSpec",
+    "fixed_point_convolve",
+    "ideal_accumulator_bits",
+    "ideal_bits_removed",
+    "mac_requant_count",
+    "quantize",
+    "read_wav",
+    "simulate_fixed_point_conv",
+    "write_wav",
     "MultiChannelEngine",
     "ScatterEngine",
     "Shard",

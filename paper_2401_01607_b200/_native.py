@@ -47,8 +47,11 @@ _SIGNATURES = {
     "sc_engine_tail_bound": [_vp, _p64],
     "sc_fir_sharded": [ctypes.c_int, ctypes.c_int, _vp, _i64, _vp, _i64, _vp, ctypes.c_int,
                        ctypes.POINTER(ctypes.c_int), ctypes.c_int],
+    "sc_fir_range_host": [ctypes.c_int, ctypes.c_int, _vp, _i64, _vp, _i64, _vp, _i64, _i64, ctypes.c_int,
+                          ctypes.c_int],
     "sc_engine_set_mode": [_vp, ctypes.c_int],
     "sc_fixed_quantize": [_vp, _i64, ctypes.c_int, _vp, _vp, _vp, _vp],
+    "sc_fixed_round_shift": [_vp, _i64, ctypes.c_int, _vp, _vp],
     "sc_fixed_convolve": [_vp, _i64, _vp, _i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp],
     "sc_engine_create_multi": [ctypes.c_int, _vp, _i64, _i64, _i64, ctypes.c_double, _vp,
                                ctypes.POINTER(_vp)],
@@ -60,6 +63,8 @@ _SIGNATURES = {
     "sc_engine_swap_ir": [_vp, _vp, _i64],
     "sc_engine_swap_ir_at_next_block": [_vp, _vp, _i64],
     "sc_engine_flush": [_vp, _vp, _i64, _p64],
+    "sc_engine_flush_begin": [_vp, _vp, _i64],
+    "sc_engine_flush_end": [_vp, _vp],
     "sc_engine_state": [_vp, _p64, _p64, _p64, _p64, _p64, _pint],
     "sc_engine_schedule": [_vp, _vp, _i64, _p64],
     "sc_engine_current_ir": [_vp, _vp, _i64, _p64],
@@ -67,8 +72,9 @@ _SIGNATURES = {
                                  _vp],
     "sc_engine_process_blocks_host": [_vp, _vp, _i64, _i64, _p64, ctypes.POINTER(_vp), _p64, _i64,
                                       _vp, ctypes.c_int],
+    "sc_tc_stats": [_p64, _p64, _pint, _pint],
 }
-EXPORTS = tuple(_SIGNATURES) + ("sc_last_error", "sc_launch_count")
+EXPORTS = tuple(_SIGNATURES) + ("sc_last_error", "sc_launch_count", "sc_tc_stats_reset")
 
 _lock = threading.Lock()
 _lib = None
@@ -100,6 +106,8 @@ def load_library() -> ctypes.CDLL:
         L.sc_last_error.restype = ctypes.c_char_p
         L.sc_launch_count.argtypes = []
         L.sc_launch_count.restype = ctypes.c_int64
+        L.sc_tc_stats_reset.argtypes = []
+        L.sc_tc_stats_reset.restype = None
         _lib = L
         return L
 
@@ -157,3 +165,12 @@ def stream_ptr(stream=None):
 
 def ptr(t) -> ctypes.c_void_p:
     return ctypes.c_void_p(t.data_ptr())
+
+
+def tc_stats() -> dict:
+    """Cumulative tensor-core launch bookkeeping (sc_tc_stats)."""
+    L = load_library()
+    n, macs = ctypes.c_int64(), ctypes.c_int64()
+    ssh, tn = ctypes.c_int(), ctypes.c_int()
+    check(L.sc_tc_stats(ctypes.byref(n), ctypes.byref(macs), ctypes.byref(ssh), ctypes.byref(tn)))
+    return {"launches": n.value, "padded_macs": macs.value, "ssh": ssh.value, "tile_n": tn.value}

@@ -9,6 +9,7 @@ travels to the GPU box with the repo snapshot).
 from __future__ import annotations
 
 import argparse
+import concurrent.futures as cf
 import os
 import pathlib
 import shutil
@@ -23,7 +24,7 @@ SOURCES = ["capi.cu", "k_ordered.cu", "k_fast_f32.cu", "k_tc_fir.cu", "engine.cu
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
 
 
@@ -42,21 +43,32 @@ def needs_build() -> bool:
     return any(d.stat().st_mtime > t for d in deps if d.exists())
 
 
-def build(verbose: bool = False, force: bool = False) -> pathlib.Path:
-    if not force and not needs_build():
-        return OUT
-    OUT.parent.mkdir(parents=True, exist_ok=True)
-    tmp = OUT.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
+def _run(cmd, verbose):
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libscatterconv_b200.so")
+        raise RuntimeError(f"nvcc failed: {' '.join(cmd[-3:])}")
     if verbose:
         sys.stderr.write(res.stderr)
+
+
+def build(verbose: bool = False, force: bool = False) -> pathlib.Path:
+    """Every translation unit compiles in parallel (they are independent: no
+    relocatable device code), then one shared-library link."""
+    if not force and not needs_build():
+        return OUT
+    OUT.parent.mkdir(parents=True, exist_ok=True)
+    objdir = OUT.parent / "obj"
+    objdir.mkdir(exist_ok=True)
+    extra = ["-Xptxas=-v"] if verbose else []
+    jobs = [[nvcc(), *NVCC_FLAGS, *extra, "-c", "-o", str(objdir / (s + ".o")), str(CSRC / s)] for s in SOURCES]
+    with cf.ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+        list(ex.map(lambda c: _run(c, verbose), jobs))
+    tmp = OUT.with_suffix(".so.tmp")
+    _run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
+          *[str(objdir / (s + ".o")) for s in SOURCES]], verbose)
     os.replace(tmp, OUT)
     return OUT
 

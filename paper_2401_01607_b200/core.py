@@ -114,11 +114,8 @@ def mode_code(mode) -> int:
     return _MODES[mode]
 
 
-_PIPELINE_MIN_MACS = 1 << 36   # host-resident inputs this large are streamed in chunks
-_PIPELINE_CHUNK_MACS = 1 << 36   # each pipelined chunk carries at least this much work...
-_PIPELINE_MAX_CHUNKS = 12        # ...up to 12 chunks (cfg3: 4 chunks, cfg5: 12; measured best)
-_PIPELINE_MIN_BYTES = 1 << 25    # transfer-bound inputs (short filters) this large are streamed too,
-_PIPELINE_CHUNK_BYTES = 1 << 24  # in chunks of >= 16 MiB, so upload and download overlap (full duplex)
+_PIPELINE_MIN_MACS = 1 << 36   # host-resident inputs this large are streamed in chunks (by the
+_PIPELINE_MIN_BYTES = 1 << 25   # library: one per >= 2^36 MACs or 16 MiB, 2..12), as are transfer-bound ones
 _PIPE_STREAMS: dict = {}
 
 
@@ -133,46 +130,23 @@ def pipe_streams(dev):
 
 
 def _fir_host_pipelined(x_pin, kern, mode):
-    """Pinned-host float32 input: overlap the H2D upload, the FIR and the D2H
-    download chunk by chunk (one stream each, event-chained).  Chunk c owns
-    outputs [a_c, b_c) and needs inputs up to min(Ne, b_c); it is computed with
-    sc_fir_range over the device copy of x (its halo is already there).
-    Returns a pinned host tensor with the full Ne+Nh-1 result."""
+    """Pinned-host float32 input: the native chunk-pipelined range engine
+    (csrc/sharded.cu sc_fir_range_host) over the whole output -- upload,
+    FIR and download of consecutive output chunks overlap on three persistent
+    streams.  Returns a pinned host tensor with the full Ne+Nh-1 result."""
     t = _dev.torch()
-    L = N.lib()
-    dev = t.device("cuda", t.cuda.current_device())
-    ne = x_pin.shape[0]
-    h = _dev.as_device(kern, np.float32, device=dev)
-    nh = h.shape[0]
-    nout = ne + nh - 1
-    out = t.empty(nout, dtype=t.float32, pin_memory=True)
-    xd = t.empty(ne, dtype=t.float32, device=dev)
-    yd = t.empty(nout, dtype=t.float32, device=dev)
-    main = t.cuda.current_stream(dev)
-    s_in, s_cmp, s_out = pipe_streams(dev)
-    for s in (s_in, s_cmp, s_out):
-        s.wait_stream(main)   # h upload / allocations are ordered on main
-    chunks = int(os.environ.get("SC_PIPE_CHUNKS", "0")) or \
-        max(2, min(_PIPELINE_MAX_CHUNKS, max((nout * nh) // _PIPELINE_CHUNK_MACS, 4 * ne // _PIPELINE_CHUNK_BYTES)))
-    per = -(-nout // chunks)
-    uploaded = 0
-    for c in range(chunks):
-        a, b = c * per, min(nout, (c + 1) * per)
-        if a >= b:
-            break
-        need = min(ne, b)
-        if need > uploaded:
-            with t.cuda.stream(s_in):
-                xd[uploaded:need].copy_(x_pin[uploaded:need], non_blocking=True)
-            uploaded = need
-        s_cmp.wait_stream(s_in)
-        xb = max(0, a - nh + 1)
-        N.check(L.sc_fir_range(N.SC_F32, mode, N.ptr(xd[xb:]) if need > xb else None, xb, max(xb, need),
-                               N.ptr(h), nh, N.ptr(yd[a:]), a, b, N.stream_ptr(s_cmp)))
-        s_out.wait_stream(s_cmp)
-        with t.cuda.stream(s_out):
-            out[a:b].copy_(yd[a:b], non_blocking=True)
-    s_out.synchronize()   # the result lives in host memory: wait for the last D2H
+    dev = t.cuda.current_device()
+    h = kern if (_dev.is_tensor(kern) and kern.is_cuda and kern.get_device() == dev
+                 and kern.dtype == t.float32 and kern.is_contiguous()) else None
+    if h is None:
+        h = _dev.as_device(kern, np.float32, device=t.device("cuda", dev))
+    ne, nh = x_pin.shape[0], h.shape[0]
+    out = t.empty(ne + nh - 1, dtype=t.float32, pin_memory=True)
+    # h (and x, when the caller just filled it) are ordered on the current stream
+    t.cuda.current_stream().synchronize()
+    chunks = int(os.environ.get("SC_PIPE_CHUNKS", "0"))
+    N.check(N.lib().sc_fir_range_host(N.SC_F32, mode, N.ptr(x_pin), ne, N.ptr(h), nh, N.ptr(out), 0,
+                                      ne + nh - 1, dev, chunks))
     return out
 
 

@@ -11,6 +11,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
 
 #include "sc_common.cuh"
 
@@ -20,6 +21,16 @@ static thread_local char g_err[512] = "";
 static std::atomic<int64_t> g_launches{0};
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// tensor-core launch bookkeeping (sc_tc_stats): the work k_tc_fir issues
+static std::atomic<int64_t> g_tc_launches{0}, g_tc_padded{0};
+static std::atomic<int> g_tc_last_ssh{0}, g_tc_last_tn{0};
+void note_tc_launch(int ssh, int tile_n, int64_t padded_macs) {
+    g_tc_launches.fetch_add(1, std::memory_order_relaxed);
+    g_tc_padded.fetch_add(padded_macs, std::memory_order_relaxed);
+    g_tc_last_ssh.store(ssh, std::memory_order_relaxed);
+    g_tc_last_tn.store(tile_n, std::memory_order_relaxed);
+}
 
 // FAST mode routes long filters to the tensor-core kernel (validated on B200
 // against the oracle, tests/test_tc_gpu.py).
@@ -44,6 +55,68 @@ int sm_count() {
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
     cache[dev] = n;
     return n;
+}
+
+// Small pinned host blocks (state read-backs; portable and mapped, so any
+// device's kernels may store into them) carved from 256 KB arenas:
+// cudaHostAlloc costs ~1 ms per call, far too much for a per-engine buffer.
+namespace {
+struct PinnedPool {
+    static constexpr size_t kArena = 256 * 1024;
+    std::mutex mu;
+    std::map<size_t, std::vector<void *>> free_lists;  // size class -> blocks
+    std::map<void *, size_t> owner;                     // block -> size class
+    char *arena = nullptr;
+    size_t arena_left = 0;
+};
+PinnedPool &pinned_pool() {
+    static PinnedPool *p = new PinnedPool();  // never destroyed: blocks may outlive static teardown
+    return *p;
+}
+}  // namespace
+
+void *pinned_small(size_t bytes) {
+    if (bytes == 0) return nullptr;
+    PinnedPool &pp = pinned_pool();
+    size_t cls = 64;
+    while (cls < bytes) cls <<= 1;
+    std::lock_guard<std::mutex> lk(pp.mu);
+    auto &fl = pp.free_lists[cls];
+    if (!fl.empty()) {
+        void *p = fl.back();
+        fl.pop_back();
+        return p;
+    }
+    void *p = nullptr;
+    if (cls > PinnedPool::kArena / 4) {
+        if (cudaHostAlloc(&p, cls, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+    } else {
+        if (pp.arena_left < cls) {
+            void *a = nullptr;
+            if (cudaHostAlloc(&a, PinnedPool::kArena, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
+                cudaGetLastError();
+                return nullptr;
+            }
+            pp.arena = static_cast<char *>(a);
+            pp.arena_left = PinnedPool::kArena;
+        }
+        p = pp.arena;
+        pp.arena += cls;
+        pp.arena_left -= cls;
+    }
+    pp.owner[p] = cls;
+    return p;
+}
+
+void pinned_small_free(void *p) {
+    if (!p) return;
+    PinnedPool &pp = pinned_pool();
+    std::lock_guard<std::mutex> lk(pp.mu);
+    auto it = pp.owner.find(p);
+    if (it != pp.owner.end()) pp.free_lists[it->second].push_back(p);  // reused by the next request
 }
 
 void *scratch(size_t bytes, int slot, cudaStream_t stream, int *err) {
@@ -85,7 +158,7 @@ int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_
                    int64_t n_end, int64_t channels, cudaStream_t stream) {
     bool tc = false, guard = false;
     if (mode == SC_MODE_TC) {
-        tc = true;
+        tc = guard = true;
     } else if (mode == SC_MODE_FAST) {
         // tensor cores from 256 taps; from 80 taps too when the launch is big
         // enough to amortise their set-up (short128 on 2^26 outputs: 0.30 ms
@@ -104,7 +177,8 @@ int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_
     int rc = launch_fir_f32_tc(x, ldx, x_base, x_lo, x_hi, h, ldh, nh, y, ldy, n_begin, n_end, channels,
                                stream, &nonfinite);
     if (rc || !guard || !nonfinite) return rc;
-    // FAST mode: NaN/Inf inputs are routed (on the device, no host sync) to
+    // NaN/Inf inputs, and magnitudes whose power-of-two scales leave float
+    // range (k_tc_fir.cu channel_scales), are routed (on the device, no host sync) to
     // the ORDERED kernel, which visits exactly the reference's (m, k) pairs
     // and so reproduces its NaN/Inf pattern (0*Inf included).  Each launch
     // exits immediately when the flag is clear.
@@ -127,6 +201,19 @@ int sc_abi_version(void) { return SC_ABI_VERSION; }
 int64_t sc_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char *sc_last_error(void) { return g_err; }
+
+int sc_tc_stats(int64_t *launches, int64_t *padded_macs, int *last_ssh, int *last_tile_n) {
+    if (launches) *launches = g_tc_launches.load(std::memory_order_relaxed);
+    if (padded_macs) *padded_macs = g_tc_padded.load(std::memory_order_relaxed);
+    if (last_ssh) *last_ssh = g_tc_last_ssh.load(std::memory_order_relaxed);
+    if (last_tile_n) *last_tile_n = g_tc_last_tn.load(std::memory_order_relaxed);
+    return SC_OK;
+}
+
+void sc_tc_stats_reset(void) {
+    g_tc_launches.store(0, std::memory_order_relaxed);
+    g_tc_padded.store(0, std::memory_order_relaxed);
+}
 
 int sc_fir_full(int dtype, int mode, const void *x, int64_t ne, const void *h, int64_t nh,
                 void *y, int skip_mode, double threshold, void *stream) {

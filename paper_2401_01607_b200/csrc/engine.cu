@@ -128,23 +128,55 @@ struct StreamEvents {
 template <typename T>
 __global__ void k_blocks_last_scatter(const T *__restrict__ x, int64_t ldx, int64_t n_total, int64_t nb,
                                       double thr, int64_t n_blocks, int64_t *__restrict__ J) {
+    // The last scattering index: walk the block backwards one CTA-wide tile
+    // at a time and stop at the first tile holding a scattering sample (a
+    // dense drive stops after one tile; only skip-heavy blocks scan further).
     const int64_t b = blockIdx.x;
     const T *xc = x + blockIdx.y * ldx;
     const int64_t s = b * nb;
     const int64_t n = n_total - s < nb ? n_total - s : nb;
     long long j = -1;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
-        if (!skipped<SC_SKIP_NOT_GT>(xc[s + i], thr)) j = i > j ? i : j;
+    for (int64_t top = n; top > 0; top -= blockDim.x) {
+        const int64_t i = top - 1 - threadIdx.x;
+        if (i >= 0 && !skipped<SC_SKIP_NOT_GT>(xc[s + i], thr)) j = i;
+        if (__syncthreads_or(j >= 0)) break;
+    }
     for (int o = 16; o > 0; o >>= 1) {
         const long long v = __shfl_xor_sync(0xffffffffu, j, o);
         j = v > j ? v : j;
     }
-    __shared__ long long sj[8];
+    __shared__ long long sj[32];
     if ((threadIdx.x & 31) == 0) sj[threadIdx.x >> 5] = j;
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) j = sj[w] > j ? sj[w] : j;
         J[blockIdx.y * n_blocks + b] = j;
+    }
+}
+
+// flush (engine.py:148-161) in one launch: per channel row c, copy the
+// schedule prefix [0, n_copy) of the current residue into the tail and zero
+// both residue buffers (each element is read before the same thread zeroes
+// it); CTA (0, c) thread 0 writes channel c's state to the pinned host
+// read-back and resets it (live = ri = 0, cap = nh).
+template <typename T>
+__global__ void k_flush(T *__restrict__ cur, T *__restrict__ other, int64_t res_ld, T *__restrict__ tail,
+                        int64_t tail_ld, int64_t n_copy, int64_t *__restrict__ st, int64_t nh,
+                        int64_t *__restrict__ st_host) {
+    const int64_t c = blockIdx.y;
+    T *rc = cur + c * res_ld;
+    T *ro = other + c * res_ld;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < res_ld; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < n_copy) tail[c * tail_ld + i] = rc[i];
+        rc[i] = T(0);
+        ro[i] = T(0);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        int64_t *sc = st + c * ST_N;
+        for (int k = 0; k < ST_N; ++k) st_host[c * ST_N + k] = sc[k];
+        sc[ST_LIVE] = 0;
+        sc[ST_CAP] = nh;
+        sc[ST_RI] = 0;
     }
 }
 
@@ -430,6 +462,11 @@ struct sc_engine {
     void *hx = nullptr, *hy = nullptr;
     int64_t h_cap = 0;
     cudaStream_t up = nullptr, down = nullptr;
+    // pinned host copy of the state a flush reads back ([C][ST_N]); the
+    // flush enqueues all of its device work before the one host wait
+    int64_t *st_host = nullptr;
+    bool flush_open = false;
+    int64_t flush_cap = 0, flush_nh = 0;
 };
 
 namespace {
@@ -675,13 +712,28 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
     for (int64_t i = 0; i < n_swaps; ++i)
         if (swap_blocks[i] >= 0 && swap_blocks[i] < n_blocks)
             ev.push_back({swap_blocks[i], swap_irs[i], swap_ld ? swap_ld[i] : swap_nh[i], swap_nh[i]});
+    std::stable_sort(ev.begin(), ev.end(), [](const Ev &a, const Ev &b) { return a.block < b.block; });
     if (e->has_pending) {
         size_t pos = 0;
         while (pos < ev.size() && ev[pos].block == 0) ++pos;
         ev.insert(ev.begin() + pos, Ev{0, e->pend, e->pend_ld, e->pend_nh});
         e->has_pending = false;
     }
-    // Too many IR changes for one launch: process consecutive block ranges.
+    // Swaps before the same block: only the last one's IR and cap matter
+    // (swap_ir keeps every live residue sample whatever the cap, engine.py:
+    // 178-183, and live does not change between them), so keep the last.
+    // Afterwards every event has its own block, which bounds the split below.
+    {
+        size_t w = 0;
+        for (size_t r = 0; r < ev.size(); ++r) {
+            if (w > 0 && ev[w - 1].block == ev[r].block) ev[w - 1] = ev[r];
+            else ev[w++] = ev[r];
+        }
+        ev.resize(w);
+    }
+    // Too many IR changes for one launch: process consecutive block ranges
+    // (each range holds <= kMaxEvents events at distinct blocks, so the
+    // recursive call never splits again).
     if ((int64_t)ev.size() > kMaxEvents) {
         int64_t b0 = 0;
         size_t k = 0;
@@ -857,6 +909,7 @@ int sc_engine_destroy(sc_engine *e) {
     cudaFree(e->res[0]);
     cudaFree(e->res[1]);
     cudaFree(e->st);
+    pinned_small_free(e->st_host);
     cudaFree(e->stage);
     cudaFree(e->jbuf);
     cudaFree(e->fx);
@@ -924,8 +977,70 @@ int sc_engine_swap_ir_at_next_block(sc_engine *e, const void *h, int64_t nh) {
     return SC_OK;
 }
 
+int sc_engine_flush_begin(sc_engine *e, void *tail, int64_t tail_capacity) {
+    SC_REQUIRE(e, "sc_engine_flush_begin: null pointer");
+    SC_REQUIRE(!e->flush_open, "sc_engine_flush_begin: previous flush not finished (sc_engine_flush_end)");
+    DeviceGuard g(e->device);
+    // Every channel's tail (max(nh - 1, live) samples, engine.py:155-156) is
+    // a prefix of its schedule; entries past it are zero (beyond its live
+    // slots), so copying the bound cap_ub >= every tail needs no host read of
+    // live first.  The state goes to pinned memory in the same stream order.
+    const int64_t n_copy = e->cap_ub;
+    SC_REQUIRE(tail_capacity >= n_copy && (n_copy <= 0 || tail),
+               "sc_engine_flush_begin: tail buffer below sc_engine_tail_bound (%lld < %lld)",
+               (long long)tail_capacity, (long long)n_copy);
+    if (!e->st_host) {
+        e->st_host = static_cast<int64_t *>(pinned_small(sizeof(int64_t) * ST_N * e->C));
+        SC_REQUIRE(e->st_host, "sc_engine_flush_begin: pinned host allocation failed");
+    }
+    {
+        const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(e->res_ld, 256), 2 * sm_count()));
+        const dim3 g(gx, (unsigned)e->C);
+        if (e->dtype == SC_F64)
+            k_flush<double><<<g, 256, 0, e->stream>>>(static_cast<double *>(e->res[e->cur]),
+                                                      static_cast<double *>(e->res[1 - e->cur]), e->res_ld,
+                                                      static_cast<double *>(tail), tail_capacity, n_copy, e->st,
+                                                      e->nh, e->st_host);
+        else
+            k_flush<float><<<g, 256, 0, e->stream>>>(static_cast<float *>(e->res[e->cur]),
+                                                     static_cast<float *>(e->res[1 - e->cur]), e->res_ld,
+                                                     static_cast<float *>(tail), tail_capacity, n_copy, e->st,
+                                                     e->nh, e->st_host);
+        SC_CHECK_LAUNCH();
+    }
+    e->flush_cap = tail_capacity;
+    e->flush_nh = e->nh;
+    e->cap_ub = e->nh;
+    e->consumed = 0;
+    e->flush_open = true;
+    return SC_OK;
+}
+
+int sc_engine_flush_end(sc_engine *e, int64_t *n_tail) {
+    SC_REQUIRE(e && n_tail, "sc_engine_flush_end: null pointer");
+    SC_REQUIRE(e->flush_open, "sc_engine_flush_end: no flush in flight");
+    DeviceGuard g(e->device);
+    e->flush_open = false;
+    SC_CHECK_CUDA(cudaStreamSynchronize(e->stream));
+    int64_t nt_max = 0;
+    for (int64_t c = 0; c < e->C; ++c) {
+        const int64_t live = e->st_host[c * ST_N + ST_LIVE];
+        n_tail[c] = (e->flush_nh - 1 > live) ? e->flush_nh - 1 : live;  // engine.py:155
+        nt_max = std::max(nt_max, n_tail[c]);
+    }
+    SC_REQUIRE(e->flush_cap >= nt_max, "sc_engine_flush: tail buffer too small (%lld < %lld)",
+               (long long)e->flush_cap, (long long)nt_max);
+    return SC_OK;
+}
+
 int sc_engine_flush(sc_engine *e, void *tail, int64_t tail_capacity, int64_t *n_tail) {
     SC_REQUIRE(e && n_tail, "sc_engine_flush: null pointer");
+    SC_REQUIRE(!e->flush_open, "sc_engine_flush: a split flush is in flight (sc_engine_flush_end)");
+    if (tail_capacity >= e->cap_ub) {  // one launch, one host wait
+        const int rc = sc_engine_flush_begin(e, tail, tail_capacity);
+        return rc ? rc : sc_engine_flush_end(e, n_tail);
+    }
+    // a buffer sized to the exact tail: read live first, copy only the tail
     DeviceGuard g(e->device);
     std::vector<int64_t> hs;
     int rc = read_state(e, hs);

@@ -129,6 +129,13 @@ __global__ void __launch_bounds__(256) k_fixed_conv(const int64_t *__restrict__ 
     }
 }
 
+// Element-wise t / 2^s, half-even (the scalar helper _round_shift_half_even,
+// quantize.py:145-154), through the same rshift_half_even the schemes use.
+__global__ void k_round_shift(const int64_t *__restrict__ t, int64_t n, int s, int64_t *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = s == 0 ? t[i] : (int64_t)rshift_half_even((i128)t[i], s);
+}
+
 }  // namespace
 }  // namespace sc
 
@@ -144,6 +151,17 @@ int sc_fixed_quantize(const double *x, int64_t n, int word_bits, int64_t *k, dou
     SC_REQUIRE(x && k, "sc_fixed_quantize: null pointer");
     const unsigned g = (unsigned)std::min<int64_t>(cdiv(n, 256), 4 * (int64_t)sm_count());
     k_fixed_quantize<<<g, 256, 0, as_stream(stream)>>>(x, n, word_bits - 1, k, xq, stats);
+    SC_CHECK_LAUNCH();
+    return SC_OK;
+}
+
+int sc_fixed_round_shift(const int64_t *t, int64_t n, int shift, int64_t *out, void *stream) {
+    SC_REQUIRE(shift >= 0 && shift <= 63, "shift must be in [0, 63], got %d", shift);
+    SC_REQUIRE(n >= 0, "sc_fixed_round_shift: bad arguments");
+    if (n == 0) return SC_OK;
+    SC_REQUIRE(t && out, "sc_fixed_round_shift: null pointer");
+    const unsigned g = (unsigned)std::min<int64_t>(cdiv(n, 256), 4 * (int64_t)sm_count());
+    k_round_shift<<<g, 256, 0, as_stream(stream)>>>(t, n, shift, out);
     SC_CHECK_LAUNCH();
     return SC_OK;
 }

@@ -439,11 +439,22 @@ __global__ void k_amax2(const float *__restrict__ x, int64_t ldx, int64_t nx, in
 
 // per channel c: exact powers of two that put max|x|, max|h| in [2^14, 2^15):
 // 2^ex, 2^eh, and the epilogue's unscale 2^-(ex+eh).  From amax[2c], [2c+1].
-__device__ __forceinline__ float3 channel_scales(const unsigned *amax, int c) {
+// Magnitudes whose scales would leave float range (max below 2^-100: 2^ex
+// overflows from 2^-113 on; or |ex+eh| > 126: the unscale over/underflows)
+// raise the fallback flag instead, so the ordered kernel computes the launch
+// (flag-gated, like non-finite inputs) rather than returning Inf/NaN/0.
+__device__ __forceinline__ float3 channel_scales(const unsigned *amax, int c, unsigned *fallback) {
     int e[2];
+    bool out_of_range = false;
     for (int i = 0; i < 2; ++i) {
         const float m = __uint_as_float(amax[2 * c + i]);
         e[i] = (m > 0.0f && isfinite(m)) ? 14 - ilogbf(m) : 0;
+        out_of_range |= e[i] > 114;
+    }
+    out_of_range |= e[0] + e[1] > 126 || e[0] + e[1] < -126;
+    if (out_of_range) {
+        if (threadIdx.x == 0) atomicOr(fallback, 1u);
+        e[0] = e[1] = 0;
     }
     return make_float3(ldexpf(1.0f, e[0]), ldexpf(1.0f, e[1]), ldexpf(1.0f, -(e[0] + e[1])));
 }
@@ -544,10 +555,10 @@ __global__ void __launch_bounds__(256) k_tc_prep(const float *__restrict__ x, in
                                                  float *scales, __half *__restrict__ xt_hi,
                                                  __half *__restrict__ xt_lo, int64_t xt_ch,
                                                  __half *__restrict__ h8_hi, __half *__restrict__ h8_lo,
-                                                 int64_t h8_ch) {
+                                                 int64_t h8_ch, unsigned *fallback) {
     __shared__ __align__(16) float s[32][132];
     const int c = blockIdx.y;
-    const float3 sc = channel_scales(amax, c);
+    const float3 sc = channel_scales(amax, c, fallback);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         scales[3 * c] = sc.x;
         scales[3 * c + 1] = sc.y;
@@ -634,7 +645,7 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
         const int gh8 = (int)cdiv(ngroups * 8, 256);
         dim3 g((unsigned)(gsplit + gh8), (unsigned)channels);
         k_tc_prep<<<g, 256, 0, stream>>>(x, ldx, x_base, x_lo, x_hi, n_begin, row_min, nrows, gsplit, h, ldh, nh,
-                                         s8, ngroups, amax, scales, xt_hi, xt_lo, xt_ch, h8_hi, h8_lo, h8_ch);
+                                         s8, ngroups, amax, scales, xt_hi, xt_lo, xt_ch, h8_hi, h8_lo, h8_ch, flag);
         SC_CHECK_LAUNCH();
     }
     // function attributes are per device (context): set on every launch so
@@ -712,6 +723,7 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     else SC_TC_LAUNCH(8, 256);
 #undef SC_TC_LAUNCH
     SC_CHECK_LAUNCH();
+    note_tc_launch(SSH, TNV, a.n_tiles * TTILE * (int64_t)TR * s8);
     if (nsplit > 1) {
         dim3 g((unsigned)cdiv(n_len, 256), (unsigned)channels);
         k_tc_split_reduce<<<g, 256, 0, stream>>>(a.ws, (int)nsplit, (int)channels, n_len, y, ldy, flag);

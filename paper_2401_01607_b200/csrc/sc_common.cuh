@@ -26,6 +26,9 @@ void set_error(const char *fmt, ...);
     } while (0)
 
 void note_launch();  // bumps the sc_launch_count() counter
+// records one k_tc_fir launch for sc_tc_stats (drain period, tile width, and
+// the padded MACs of its MMAs: tiles x 128*tile_n outputs x 128 taps x shifts)
+void note_tc_launch(int ssh, int tile_n, int64_t padded_macs);
 
 #define SC_CHECK_LAUNCH()                                                              \
     do {                                                                               \
@@ -54,6 +57,10 @@ int sm_count();  // of the current device (cached per device)
 // padded taps).  Stream-ordered: a buffer is only reallocated after a
 // cudaStreamSynchronize of the requesting stream.
 void *scratch(size_t bytes, int slot, cudaStream_t stream, int *err);
+
+// Small pinned host blocks from a process-wide pool (nullptr on failure).
+void *pinned_small(size_t bytes);
+void pinned_small_free(void *p);
 
 // ------------------------------------------------------------------ exact arithmetic
 

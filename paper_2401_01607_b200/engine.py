@@ -208,17 +208,26 @@ class ScatterEngine:
     def flush(self) -> Signal:
         """Emit the pending residue and reset the engine (engine.py:148-161):
         max(len(ir)-1, live) samples in emission order."""
+        return self._flush_end(self._flush_begin())
+
+    def _flush_begin(self):
+        """Queue the flush's device work (tail copy, state read-back, reset);
+        returns the tail buffer for _flush_end (csrc sc_engine_flush_begin)."""
         t = _dev.torch()
         with _dev.device_guard(self._device):
             self._bind_stream()
             cap = ctypes.c_int64()
             N.check(self._lib.sc_engine_tail_bound(self._handle, ctypes.byref(cap)))
             tail = t.empty(cap.value, dtype=_dev.torch_dtype(self._npd), device=self._device)
-            n = ctypes.c_int64()
-            N.check(self._lib.sc_engine_flush(self._handle, N.ptr(tail), cap.value, ctypes.byref(n)))
-            tail = tail[:n.value]
-        like = self._ir_like
-        return Signal(_dev.like_input(tail, like), self._sample_rate)
+            N.check(self._lib.sc_engine_flush_begin(self._handle, N.ptr(tail), cap.value))
+        return tail
+
+    def _flush_end(self, tail) -> Signal:
+        """Wait for the queued flush; the tail is max(len(ir)-1, live) long."""
+        n = ctypes.c_int64()
+        with _dev.device_guard(self._device):
+            N.check(self._lib.sc_engine_flush_end(self._handle, ctypes.byref(n)))
+        return Signal(_dev.like_input(tail[:n.value], self._ir_like), self._sample_rate)
 
     def swap_ir(self, h_new: Signal):
         """Replace the impulse response, effective for the very next sample
@@ -291,13 +300,26 @@ class ScatterEngine:
         nb = self.config.block_size_nb if nb is None else int(nb)
         if nb < 1 or nb > self.config.block_size_nb:
             raise ValueError(f"nb must be in [1, block_size_nb={self.config.block_size_nb}]")
-        if self._pending_ir is not None and len(x):
-            h_new, self._pending_ir = self._pending_ir, None
-            self.swap_ir(h_new)
         t = _dev.torch()
         with _dev.device_guard(self._device):
             xs = x.samples if isinstance(x, Signal) else x
-            swaps = sorted(swaps, key=lambda s: s[0])
+            n_blocks = -(-len(xs) // nb)
+            pending = None
+            if self._pending_ir is not None and n_blocks:
+                # the deferred swap acts before block 0, after any explicit
+                # block-0 swap (as swap_ir + process_block would order them):
+                # the library places it (csrc/engine.cu process_blocks_impl)
+                pending, self._pending_ir = self._pending_ir, None
+                if pending.sample_rate != self._sample_rate:
+                    raise ValueError(
+                        f"sample rates differ: new impulse response {pending.sample_rate} Hz "
+                        f"vs engine {self._sample_rate} Hz"
+                    )
+                pd = self._to_dev(pending.samples)
+                self._bind_stream()
+                N.check(self._lib.sc_engine_swap_ir_at_next_block(self._handle, N.ptr(pd), len(pending)))
+            # swaps outside [0, n_blocks) precede no block: the library ignores them
+            swaps = sorted((s for s in swaps if 0 <= int(s[0]) < n_blocks), key=lambda s: s[0])
             irs = _dev.as_device_many([s[1].samples if isinstance(s[1], Signal) else s[1] for s in swaps],
                                       self._npd, device=self._device)
             n = len(swaps)
@@ -312,18 +334,22 @@ class ScatterEngine:
                 out = t.empty(xh.shape[1], dtype=xh.dtype, pin_memory=True)
                 N.check(self._lib.sc_engine_process_blocks_host(self._handle, N.ptr(xh), xh.shape[1], nb,
                                                                 blocks, ptrs, nhs, n, N.ptr(out), _dev.host_pipe_chunks()))
-                self._note_swaps(swaps)
+                self._note_swaps(swaps, pending)
                 return out
             xd = self._to_dev(xs)
             out = t.empty(xd.shape[0], dtype=xd.dtype, device=self._device)
             N.check(self._lib.sc_engine_process_blocks(self._handle, N.ptr(xd), xd.shape[0], nb,
                                                        blocks, ptrs, nhs, n, N.ptr(out)))
-            self._note_swaps(swaps)
+            self._note_swaps(swaps, pending)
         return _dev.like_input(out, xs)
 
-    def _note_swaps(self, swaps):
-        if swaps:
-            last = swaps[-1][1]
+    def _note_swaps(self, swaps, pending=None):
+        """Host copy of the IR now in effect: the last swap of the timeline,
+        where a pending IR follows the block-0 swaps."""
+        last = swaps[-1][1] if swaps else None
+        if pending is not None and (not swaps or int(swaps[-1][0]) == 0):
+            last = pending
+        if last is not None:
             last = last.samples if isinstance(last, Signal) else last
             self._ir_like = last[:0]
             self._nh = len(last)

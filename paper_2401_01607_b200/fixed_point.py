@@ -156,6 +156,23 @@ def quantize(values, fmt: FixedPointFormat):
     return _dev.like_input(xq, values)
 
 
+def _round_shift_half_even(t, shift: int):
+    """t / 2**shift rounded to nearest, ties to even (quantize.py:145-154),
+    evaluated by the device's requantisation step (``sc_fixed_round_shift``).
+    Scalar in, scalar out (as the reference); arrays map element-wise."""
+    tt = _dev.torch()
+    scalar = np.ndim(t) == 0
+    v = np.asarray(t, dtype=object).reshape(-1)
+    if any(not (-(1 << 63) <= int(a) < (1 << 63)) for a in v):
+        raise ValueError("the device requantisation step takes 64-bit integers")
+    src = tt.tensor([int(a) for a in v], dtype=tt.int64).to(tt.device("cuda", tt.cuda.current_device()))
+    out = tt.empty_like(src)
+    with tt.cuda.device(src.device):
+        N.check(N.lib().sc_fixed_round_shift(N.ptr(src), src.shape[0], int(shift), N.ptr(out), N.stream_ptr()))
+    res = [int(a) for a in out.cpu().tolist()]
+    return res[0] if scalar else np.asarray(res, dtype=np.int64)
+
+
 def _check_pair(e: Signal, h: Signal, scheme: str):
     _one_of(scheme, SCHEMES, "scheme")
     if min(len(e), len(h)) == 0:

@@ -277,11 +277,17 @@ class MultiChannelEngine:
         nb = self.config.block_size_nb if nb is None else int(nb)
         if nb < 1 or nb > self.config.block_size_nb:
             raise ValueError(f"nb must be in [1, block_size_nb={self.config.block_size_nb}]")
-        if self._pending is not None:
-            h_new, self._pending = self._pending, None
-            self.swap_ir(h_new)
+        n_total = x.shape[-1]
+        n_blocks = -(-n_total // nb)
         with _dev.device_guard(self._device):
-            swaps = sorted(swaps, key=lambda s: s[0])
+            if self._pending is not None and n_blocks:
+                # after any explicit block-0 swap, as process_block orders it;
+                # the library places it (csrc/engine.cu process_blocks_impl)
+                pd, self._pending = self._ir_rows(self._pending), None
+                self._bind()
+                N.check(self._lib.sc_engine_swap_ir_at_next_block(self._handle, N.ptr(pd), pd.shape[1]))
+            # swaps outside [0, n_blocks) precede no block: the library ignores them
+            swaps = sorted((s for s in swaps if 0 <= int(s[0]) < n_blocks), key=lambda s: s[0])
             irs = self._ir_rows_many([s[1] for s in swaps])
             k = len(swaps)
             blocks = (ctypes.c_int64 * max(k, 1))(*[int(s[0]) for s in swaps])

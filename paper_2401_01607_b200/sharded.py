@@ -124,13 +124,29 @@ def convolve_sharded(x, h, devices=None, gather: str | None = "host"):
     return t.cat([o.to(dst) for o in outs])
 
 
+def _pinned_1d(a, npd):
+    """A contiguous pinned host tensor holding a (host array or tensor): the
+    caller's own tensor when it already is one, else one staging copy (the
+    library's transfers only overlap from pinned memory)."""
+    t = _dev.torch()
+    td = _dev.torch_dtype(npd)
+    if _dev.is_tensor(a):
+        if a.device.type == "cpu" and a.is_pinned() and a.dtype == td and a.is_contiguous():
+            return a
+        return a.detach().to(device="cpu", dtype=td).contiguous().pin_memory()
+    return t.from_numpy(np.ascontiguousarray(a, dtype=npd)).pin_memory()
+
+
 def fir_sharded(x, h, devices=None, *, mode=None, gather_device=None):
     """The C-ABI multi-GPU entry (``sc_fir_sharded``): host x [Ne] and h [Nh]
     (float32 or float64), outputs partitioned over ``devices`` (repeats
-    allowed) by one native host thread per shard.  Returns the full
-    Ne+Nh-1 result as an ndarray, or as a CUDA tensor on ``gather_device``
-    (filled by peer copies).  mode as ``scatter_convolve``: float64 defaults
-    to ORDERED, bit-identical to the reference at any device count."""
+    allowed); each device runs the chunk-pipelined range engine (upload /
+    FIR / download overlapped, persistent buffers) on its own native host
+    thread.  Returns the full Ne+Nh-1 result in pinned host memory (a tensor
+    when x is a tensor, else an ndarray view of it), or as a CUDA tensor on
+    ``gather_device`` (filled by the shards' peer stores).  mode as
+    ``scatter_convolve``: float64 defaults to ORDERED, bit-identical to the
+    reference at any device count."""
     import ctypes
 
     from .core import _MODES, _result_dtype
@@ -138,31 +154,34 @@ def fir_sharded(x, h, devices=None, *, mode=None, gather_device=None):
     t = _dev.torch()
     devices = list(devices) if devices is not None else list(range(t.cuda.device_count()))
     npd = _result_dtype(x, h)
-    xa = np.ascontiguousarray(x.cpu().numpy() if _dev.is_tensor(x) else x, dtype=npd)
-    ha = np.ascontiguousarray(h.cpu().numpy() if _dev.is_tensor(h) else h, dtype=npd)
-    if xa.ndim != 1 or ha.ndim != 1:
+    if np.ndim(x) != 1 or np.ndim(h) != 1:
         raise ValueError("x and h must be 1-D")
-    if len(xa) == 0:
+    if len(x) == 0:
         raise ValueError("input signal is empty")
-    if len(ha) == 0:
+    if len(h) == 0:
         raise ValueError("impulse response is empty")
     if mode not in _MODES:
         raise ValueError(f"mode must be one of {sorted(k for k in _MODES if k)}, got {mode!r}")
     m = _MODES[mode]
     if m is None:
         m = N.SC_MODE_FAST if npd == np.float32 else N.SC_MODE_ORDERED
-    nout = len(xa) + len(ha) - 1
+    xp = _pinned_1d(x, npd)
+    hp = _pinned_1d(h, npd)
+    nout = xp.shape[0] + hp.shape[0] - 1
     if gather_device is None:
-        y = np.empty(nout, dtype=npd)
-        yp, gd = y.ctypes.data, -1
+        y = t.empty(nout, dtype=_dev.torch_dtype(npd), pin_memory=True)
+        gd = -1
     else:
         gd = t.device(gather_device).index if not isinstance(gather_device, int) else gather_device
         y = t.empty(nout, dtype=_dev.torch_dtype(npd), device=t.device("cuda", gd))
-        yp = y.data_ptr()
+        # the shards store from their own streams: the allocation (and any
+        # earlier use of this memory) on the gather device's stream is done first
+        t.cuda.current_stream(y.device).synchronize()
     devs = (ctypes.c_int * len(devices))(*devices)
-    N.check(N.lib().sc_fir_sharded(N.dtype_code(npd), m, ctypes.c_void_p(xa.ctypes.data), len(xa),
-                                   ctypes.c_void_p(ha.ctypes.data), len(ha), ctypes.c_void_p(yp),
-                                   len(devices), devs, gd))
+    N.check(N.lib().sc_fir_sharded(N.dtype_code(npd), m, N.ptr(xp), xp.shape[0], N.ptr(hp), hp.shape[0],
+                                   N.ptr(y), len(devices), devs, gd))
+    if gather_device is None and not _dev.is_tensor(x):
+        return y.numpy()
     return y
 
 
@@ -187,15 +206,22 @@ def distributed_convolve(x, h, *, rank=None, world=None, compute=None, device=No
         return sh, compute(x[sh.x_begin:sh.x_end], sh, h)
     t = _dev.torch()
     dev = device if device is not None else t.device("cuda", t.cuda.current_device())
+    dev = t.device(dev)
+    if to_host:
+        # the chunk-pipelined range engine: this rank's slice + halo goes up
+        # chunk by chunk, overlapped with the FIR and the download of the
+        # outputs into pinned host memory (csrc/sharded.cu sc_fir_range_host)
+        xp = _pinned_1d(x, np.float32)
+        hp = _dev.as_device(h, np.float32, device=dev) if _dev.is_tensor(h) and h.is_cuda else _pinned_1d(h, np.float32)
+        y = t.empty(sh.n_out, dtype=t.float32, pin_memory=True)
+        if sh.n_out:
+            N.check(N.lib().sc_fir_range_host(N.SC_F32, N.SC_MODE_FAST, N.ptr(xp), xp.shape[0], N.ptr(hp),
+                                              hp.shape[0], N.ptr(y), sh.n_begin, sh.n_end, dev.index, 0))
+        return sh, y
     with t.cuda.device(dev):
         xs = _dev.as_device(x[sh.x_begin:sh.x_end], np.float32, device=dev)
         hd = _dev.as_device(h, np.float32, device=dev)
         y = convolve_shard(xs, sh, hd)
-        if to_host:
-            out = t.empty(y.shape, dtype=y.dtype, pin_memory=True)
-            out.copy_(y, non_blocking=True)
-            t.cuda.current_stream(dev).synchronize()
-            y = out
         return sh, y
 
 

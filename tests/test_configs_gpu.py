@@ -116,6 +116,37 @@ def test_cfg2_float32_engine_per_block_within_tolerance():
     assert np.max(np.abs(tail - ref_tail)) <= tol
 
 
+def test_cfg2_float32_fast_fused_stream_full_shape():
+    """The exact path bench.py --config cfg2 times: one float32 FAST
+    process_stream over all 480,000 samples (1,875 blocks of 256) with the 19
+    IRs swapped in every 100 blocks (block 0 re-selecting IR 0, as the bench
+    does), then flush -- every block's 256 outputs and the tail against the
+    float64 oracle engine (engine.py:118-186 restated)."""
+    import torch
+
+    w = configs.cfg2()
+    h0 = torch.from_numpy(w.irs[0]).cuda()
+    eng = ScatterEngine(Signal(h0), EngineConfig(block_size_nb=256))
+    assert eng.mode == "fast"
+    n_blocks = -(-w.ne // 256)
+    swaps = [(0, h0)] + [(b, torch.from_numpy(w.irs[b // 100]).cuda()) for b in range(100, n_blocks, 100)]
+    body = eng.process_stream(torch.from_numpy(w.x).cuda(), 256, swaps).cpu().numpy()
+    tail = eng.flush().samples.cpu().numpy()
+    ref_body, ref_tail = O.stream_with_swaps(w.x, w.irs, 256, 100)
+    assert body.shape == ref_body.shape == (w.ne,)
+    assert len(tail) == len(ref_tail) == w.nh - 1
+    for j in range(len(w.irs)):                     # tolerance of the IR in effect per block
+        blk = slice(j * 100 * 256, min(w.ne, (j + 1) * 100 * 256))
+        tol = configs.tolerance(w.x, w.irs[j], "f32")
+        # a block's outputs also carry the previous IR's residue
+        if j:
+            tol = max(tol, configs.tolerance(w.x, w.irs[j - 1], "f32"))
+        per_block = np.abs(body[blk].astype(np.float64) - ref_body[blk]).reshape(-1, 256).max(axis=1)
+        assert per_block.max() <= tol, (j, per_block.max(), tol)
+    tol_last = max(configs.tolerance(w.x, ir, "f32") for ir in w.irs[-2:])
+    assert np.max(np.abs(tail - ref_tail)) <= tol_last
+
+
 # ---------------------------------------------------------------- cfg3 long reverb
 
 
@@ -172,7 +203,7 @@ def cfg5_full():
 def test_cfg5_full_single_gpu_vs_oracle(cfg5_full):
     w, _, _, y = cfg5_full
     assert y.shape[0] == w.nout
-    pre = int(os.environ.get("SC_CFG5_PREFIX", "200000"))
+    pre = int(os.environ.get("SC_CFG5_PREFIX", "2000000"))   # BASELINE.json configs[4]: 2,000,000
     yh_pre = y[:pre].cpu().numpy()
     check_tol(yh_pre, O.scatter_window(w.x, w.h, 0, pre), w.x, w.h, "cfg5 prefix")
     for s in configs.cfg5_spot_windows(w.nout):

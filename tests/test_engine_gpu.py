@@ -356,3 +356,43 @@ def test_literal_scatter_block_matches_oracle():
         assert got == want
         assert np.array_equal(r1, r2) and np.array_equal(o1, o2)
     _kernels.warm_up()
+
+
+def test_process_stream_pending_swap_follows_block0_swap():
+    """swap_ir_at_next_block(p) then a stream whose schedule swaps at block 0:
+    as swap_ir(ir0) + process_block (which applies p last), p wins."""
+    rng = np.random.default_rng(31)
+    x = rng.uniform(-1, 1, 1000)
+    h0, h1, p = rng.standard_normal(50), rng.standard_normal(70), rng.standard_normal(30)
+    nb = 100
+    ref = O.OracleEngine(h0, nb)
+    ref.swap_ir_at_next_block(p)
+    ref.swap_ir(h1)
+    want = np.concatenate([ref.process_block(x[s:s + nb]) for s in range(0, len(x), nb)] + [ref.flush()])
+    eng = ScatterEngine(sig(h0), EngineConfig(block_size_nb=nb))
+    eng.swap_ir_at_next_block(sig(p))
+    body = eng.process_stream(x, nb, [(0, sig(h1)), (10_000, sig(h1[:3]))])   # out-of-range swap ignored
+    assert eng.current_ir.samples.shape[0] == 30
+    got = np.concatenate([body, eng.flush().samples])
+    assert np.array_equal(got, want)
+
+
+def test_process_stream_many_swaps_before_one_block():
+    """40 swaps before the same block (more than one launch's 31 IR changes):
+    only the last IR and cap matter -- bit-exact vs the oracle applying all."""
+    rng = np.random.default_rng(32)
+    x = rng.uniform(-1, 1, 2000)
+    nb = 64
+    irs = [rng.standard_normal(int(n)) for n in rng.integers(1, 200, 40)]
+    swaps = [(3, sig(h)) for h in irs] + [(0, sig(irs[0])) for _ in range(35)] + [(20, sig(irs[5]))]
+    ref = O.OracleEngine(irs[7], nb)
+    out = []
+    for b, s in enumerate(range(0, len(x), nb)):
+        for sb, h in swaps:
+            if sb == b:
+                ref.swap_ir(h.samples)
+        out.append(ref.process_block(x[s:s + nb]))
+    want = np.concatenate(out + [ref.flush()])
+    eng = ScatterEngine(sig(irs[7]), EngineConfig(block_size_nb=nb))
+    got = np.concatenate([eng.process_stream(x, nb, swaps), eng.flush().samples])
+    assert np.array_equal(got, want)

@@ -48,3 +48,48 @@ def test_sharded_gather_device_and_more_devices_than_outputs():
     assert np.array_equal(y.cpu().numpy(), O.scatter_full(x, h))
     with pytest.raises(ValueError, match="no device"):
         fir_sharded(x, h, devices=[99])
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 7])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_range_host_chunk_pipeline(chunks, dtype):
+    """sc_fir_range_host: output sub-ranges of a host signal, cut into chunks
+    whose upload / FIR / download overlap; float64 ORDERED bit-exact, float32
+    FAST within the FP32 tolerance, pinned and pageable buffers alike."""
+    import torch
+
+    from paper_2401_01607_b200 import _native as N
+
+    rng = np.random.default_rng(chunks)
+    x = rng.uniform(-1, 1, 70_001).astype(dtype)
+    h = rng.standard_normal(2_500).astype(dtype)
+    ref = O.scatter_full(x, h)
+    dt = N.dtype_code(dtype)
+    mode = N.SC_MODE_FAST if dtype == np.float32 else N.SC_MODE_ORDERED
+    tol = 1e-5 * np.max(np.abs(x)) * np.sum(np.abs(h))
+    for a, b in [(0, len(ref)), (1_234, 50_000), (60_000, len(ref))]:
+        for pinned in (True, False):
+            xp = torch.from_numpy(x).pin_memory() if pinned else torch.from_numpy(x)
+            y = torch.empty(b - a, dtype=xp.dtype, pin_memory=pinned)
+            N.check(N.lib().sc_fir_range_host(dt, mode, N.ptr(xp), len(x), N.ptr(torch.from_numpy(h)), len(h),
+                                              N.ptr(y), a, b, 0, chunks))
+            got = y.numpy()
+            if dtype == np.float64:
+                assert np.array_equal(got, ref[a:b]), (a, b, pinned)
+            else:
+                assert np.max(np.abs(got.astype(np.float64) - ref[a:b])) <= tol, (a, b, pinned)
+
+
+def test_distributed_convolve_to_host_shards_concatenate():
+    """distributed_convolve(to_host=True) per rank (rank/world given, no
+    process group): each shard's pinned host segment, concatenated, is the
+    full result."""
+    from paper_2401_01607_b200.sharded import distributed_convolve
+
+    rng = np.random.default_rng(9)
+    x = rng.uniform(-1, 1, 200_000).astype(np.float32)
+    h = rng.standard_normal(3_000).astype(np.float32)
+    parts = [distributed_convolve(x, h, rank=r, world=3, to_host=True)[1].numpy() for r in range(3)]
+    ref = O.scatter_full(x, h)
+    tol = 1e-5 * np.max(np.abs(x)) * np.sum(np.abs(h))
+    assert np.max(np.abs(np.concatenate(parts).astype(np.float64) - ref)) <= tol

@@ -40,7 +40,9 @@ def test_tc_matches_oracle(ne, nh):
     assert err_frac(y, ref, x, h) <= 1.0
 
 
-@pytest.mark.parametrize("xscale,hscale", [(1e-6, 1.0), (1.0, 1e-9), (3e4, 7e3), (1e-30, 1e20)])
+@pytest.mark.parametrize("xscale,hscale", [(1e-6, 1.0), (1.0, 1e-9), (3e4, 7e3), (1e-30, 1e20),
+                                           # scales beyond float range: the ordered fallback
+                                           (1e-36, 1.0), (1.0, 1e-37), (1e25, 1e-30)])
 def test_tc_scaling_is_exact_power_of_two(xscale, hscale):
     rng = np.random.default_rng(5)
     x = (rng.uniform(-1, 1, 30_000) * xscale).astype(np.float32)
@@ -163,3 +165,14 @@ def test_tc_deterministic():
     a = scatter_convolve(Signal(x), Signal(h), mode="tc").concatenated().samples
     b = scatter_convolve(Signal(x), Signal(h), mode="tc").concatenated().samples
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("nh", [300, 4096, 40_000])
+def test_tc_same_sign_inputs(nh):
+    """DC (all-positive) drive through an all-positive decaying filter: no
+    cancellation hides errors in the split products or the drains."""
+    rng = np.random.default_rng(nh)
+    x = rng.uniform(0.5, 1.0, 60_000).astype(np.float32)
+    h = (rng.uniform(0, 1, nh) * np.exp(-np.arange(nh) / (nh / 3))).astype(np.float32)
+    y = np.asarray(scatter_convolve(Signal(x), Signal(h), mode="tc").concatenated().samples)
+    assert err_frac(y, O.scatter_window(x, h, 0, len(y)), x, h) <= 1.0
