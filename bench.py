@@ -690,6 +690,9 @@ def main():
                            "the same rate)" if "bf16_tflops" in p else "fallback 1.59 PFLOP/s",
             "achieved_per_launch": f"2 x 3 x {padded:.6e} padded MMA MACs per step (sc_tc_stats: "
                                    f"{tc['launches'] / args.steps:g} launches/step) / mean step time",
+            "frac_of_nominal_dense_fp16": achieved / 2250.0,
+            "peak_note": "frac > 1 means the kernel's MMA issue rate beats the driver's cuBLAS bf16 "
+                         "measurement; the nominal dense fp16 peak is 2250 TFLOP/s",
             "useful_fp32_tflops": useful,
             "useful_frac_of_fp32_fma_peak": useful / fp32_peak,
             "kernel": f"{tmpl} (tcgen05.mma kind::f16 M128 x N{tc['tile_n']} x K16, TMEM accumulators, "

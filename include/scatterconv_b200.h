@@ -218,10 +218,17 @@ int sc_engine_current_ir(sc_engine *e, void *dst, int64_t capacity, int64_t *nh)
 /* Back-to-back blocks with no host synchronisation (render, engine.py:194-209,
  * plus an IR swap schedule): x[n_total] is cut into blocks of nb; before block
  * b = swap_blocks[i] the engine performs swap_ir(swap_irs[i], swap_nh[i]).
- * Bit-identical to the equivalent sequence of process_block/swap_ir calls. */
+ * Bit-identical to the equivalent sequence of process_block/swap_ir calls.
+ * A call repeated with the same arguments, buffers and engine host state is
+ * captured as a CUDA graph on its second occurrence and replayed from then
+ * on (same kernels, same arguments; SC_ENGINE_GRAPHS=0 disables). */
 int sc_engine_process_blocks(sc_engine *e, const void *x, int64_t n_total, int64_t nb,
                              const int64_t *swap_blocks, const void *const *swap_irs,
                              const int64_t *swap_nh, int64_t n_swaps, void *out);
+
+/* Graph-replay bookkeeping of sc_engine_process_blocks: replays, captures,
+ * and captures that failed (those keys then always run directly). */
+int sc_engine_graph_stats(sc_engine *e, int64_t *hits, int64_t *captures, int64_t *failures);
 
 /* The same with x[C][n_total] and out[C][n_total] in HOST memory (pinned for
  * full PCIe rate; swap IRs on the device).  The stream is processed in

@@ -25,9 +25,27 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 // tensor-core launch bookkeeping (sc_tc_stats): the work k_tc_fir issues
 static std::atomic<int64_t> g_tc_launches{0}, g_tc_padded{0};
 static std::atomic<int> g_tc_last_ssh{0}, g_tc_last_tn{0};
+void note_launches(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+int64_t launches_so_far() { return g_launches.load(std::memory_order_relaxed); }
+
 void note_tc_launch(int ssh, int tile_n, int64_t padded_macs) {
     g_tc_launches.fetch_add(1, std::memory_order_relaxed);
     g_tc_padded.fetch_add(padded_macs, std::memory_order_relaxed);
+    g_tc_last_ssh.store(ssh, std::memory_order_relaxed);
+    g_tc_last_tn.store(tile_n, std::memory_order_relaxed);
+}
+
+void tc_stats_now(int64_t *launches, int64_t *padded, int *ssh, int *tile_n) {
+    *launches = g_tc_launches.load(std::memory_order_relaxed);
+    *padded = g_tc_padded.load(std::memory_order_relaxed);
+    *ssh = g_tc_last_ssh.load(std::memory_order_relaxed);
+    *tile_n = g_tc_last_tn.load(std::memory_order_relaxed);
+}
+
+void note_tc_replay(int64_t launches, int64_t padded, int ssh, int tile_n) {
+    if (launches <= 0) return;
+    g_tc_launches.fetch_add(launches, std::memory_order_relaxed);
+    g_tc_padded.fetch_add(padded, std::memory_order_relaxed);
     g_tc_last_ssh.store(ssh, std::memory_order_relaxed);
     g_tc_last_tn.store(tile_n, std::memory_order_relaxed);
 }
@@ -119,7 +137,22 @@ void pinned_small_free(void *p) {
     if (it != pp.owner.end()) pp.free_lists[it->second].push_back(p);  // reused by the next request
 }
 
+static std::atomic<int64_t> g_scratch_gen{0};
+int64_t scratch_generation() { return g_scratch_gen.load(std::memory_order_relaxed); }
+
+// Graph capture on a private stream stands in for a caller stream: scratch
+// lookups from the capture stream resolve to the caller stream's buffers
+// (the graph is launched there), and nothing may grow while capturing.
+static thread_local cudaStream_t t_alias_from = nullptr, t_alias_to = nullptr;
+static thread_local bool t_capturing = false;
+void scratch_capture_alias(cudaStream_t from, cudaStream_t to, bool on) {
+    t_alias_from = from;
+    t_alias_to = to;
+    t_capturing = on;
+}
+
 void *scratch(size_t bytes, int slot, cudaStream_t stream, int *err) {
+    if (t_capturing && stream == t_alias_from) stream = t_alias_to;
     // Grow-only buffers keyed by (device, stream, slot): concurrent streams
     // (or host threads driving different devices) never share a buffer.
     struct Buf {
@@ -132,6 +165,11 @@ void *scratch(size_t bytes, int slot, cudaStream_t stream, int *err) {
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(mu);
     Buf &b = bufs[std::make_tuple(dev, reinterpret_cast<uintptr_t>(stream), slot)];
+    if (b.n < bytes && t_capturing) {
+        set_error("scratch: would grow during graph capture");
+        *err = SC_ERR_STATE;
+        return nullptr;
+    }
     if (b.n < bytes) {
         if (b.p) {
             // kernels queued on this stream may still read the old buffer
@@ -148,6 +186,7 @@ void *scratch(size_t bytes, int slot, cudaStream_t stream, int *err) {
             return nullptr;
         }
         b.n = want;
+        g_scratch_gen.fetch_add(1, std::memory_order_relaxed);
     }
     *err = 0;
     return b.p;

@@ -29,6 +29,11 @@ void note_launch();  // bumps the sc_launch_count() counter
 // records one k_tc_fir launch for sc_tc_stats (drain period, tile width, and
 // the padded MACs of its MMAs: tiles x 128*tile_n outputs x 128 taps x shifts)
 void note_tc_launch(int ssh, int tile_n, int64_t padded_macs);
+// counters around a CUDA-graph capture, re-applied on every replay
+void note_launches(int64_t k);
+int64_t launches_so_far();
+void tc_stats_now(int64_t *launches, int64_t *padded, int *ssh, int *tile_n);
+void note_tc_replay(int64_t launches, int64_t padded, int ssh, int tile_n);
 
 #define SC_CHECK_LAUNCH()                                                              \
     do {                                                                               \
@@ -57,6 +62,11 @@ int sm_count();  // of the current device (cached per device)
 // padded taps).  Stream-ordered: a buffer is only reallocated after a
 // cudaStreamSynchronize of the requesting stream.
 void *scratch(size_t bytes, int slot, cudaStream_t stream, int *err);
+// bumped whenever a scratch buffer is (re)allocated: cached CUDA graphs that
+// captured scratch addresses are keyed by it
+int64_t scratch_generation();
+// while on: scratch(.., from) resolves to stream `to`'s buffers and never grows
+void scratch_capture_alias(cudaStream_t from, cudaStream_t to, bool on);
 
 // Small pinned host blocks from a process-wide pool (nullptr on failure).
 void *pinned_small(size_t bytes);

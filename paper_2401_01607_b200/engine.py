@@ -65,6 +65,15 @@ def _engine_mode(mode, npd) -> bool:
     return mode == "fast"
 
 
+def _signal(samples, sample_rate):
+    """A Signal around samples the engine just produced (already 1-D, float,
+    in the caller's currency): skips the constructor's coercion and checks."""
+    sig = object.__new__(Signal)
+    sig.samples = samples
+    sig.sample_rate = sample_rate
+    return sig
+
+
 class ScatterEngine:
     """Stateful block- or sample-driven convolution processor on the GPU.
 
@@ -86,11 +95,13 @@ class ScatterEngine:
             device = h.samples.device if (_dev.is_tensor(h.samples) and h.samples.is_cuda) else \
                 t.device("cuda", t.cuda.current_device())
         self._device = t.device(device)
+        self._dev_idx = self._device.index
         self._sample_rate = h.sample_rate
         self._ir_like = h.samples[:0]   # currency of returned signals (host / device / pinned)
         self._nh = len(h)
         self._pending_ir = None
         self._handle = ctypes.c_void_p()
+        self._stream_val = None
         hd = self._to_dev(h.samples)
         with _dev.device_guard(self._device):
             N.check(self._lib.sc_engine_create(self._dt, N.ptr(hd), len(h),
@@ -100,6 +111,10 @@ class ScatterEngine:
             if fast:
                 N.check(self._lib.sc_engine_set_mode(self._handle, N.SC_MODE_FAST))
         self.mode = "fast" if fast else "ordered"
+        # per-block hot path: bound entry point, raw handle, torch dtype
+        self._pb = self._lib.sc_engine_process_block
+        self._hv = self._handle.value
+        self._td = _dev.torch_dtype(self._npd)
 
     # ------------------------------------------------------------- plumbing
 
@@ -107,7 +122,12 @@ class ScatterEngine:
         return _dev.as_device(samples, self._npd, device=self._device)
 
     def _bind_stream(self):
-        N.check(self._lib.sc_engine_set_stream(self._handle, N.stream_ptr()))
+        # the engine queues on the caller's current stream; rebinding only
+        # when it changed keeps a ctypes call off the per-block path
+        sp = N.stream_ptr().value or 0
+        if sp != self._stream_val:
+            N.check(self._lib.sc_engine_set_stream(self._handle, sp))
+            self._stream_val = sp
 
     def __del__(self):
         h = getattr(self, "_handle", None)
@@ -187,7 +207,7 @@ class ScatterEngine:
         if self._pending_ir is not None:
             h_new, self._pending_ir = self._pending_ir, None
             self.swap_ir(h_new)
-        if len(block) > self.config.block_size_nb:
+        if block.samples.shape[0] > self.config.block_size_nb:
             raise ValueError(
                 f"block of {len(block)} samples exceeds block_size_nb={self.config.block_size_nb}"
             )
@@ -195,15 +215,31 @@ class ScatterEngine:
             raise ValueError(
                 f"sample rates differ: block {block.sample_rate} Hz vs engine {self._sample_rate} Hz"
             )
+        samples = block.samples
+        n = samples.shape[0]
         t = _dev.torch()
-        with _dev.device_guard(self._device):
-            xd = self._to_dev(block.samples)
-            out = t.empty(len(block), dtype=xd.dtype, device=self._device)
-            if len(block):
-                self._bind_stream()
-                N.check(self._lib.sc_engine_process_block(self._handle, N.ptr(xd), len(block),
-                                                          N.ptr(out)))
-        return Signal(_dev.like_input(out, block.samples), self._sample_rate)
+        C = t._C
+        prev = C._cuda_exchangeDevice(self._dev_idx)
+        try:
+            if (type(samples) is t.Tensor and samples.is_cuda and samples.dtype is self._td
+                    and samples.get_device() == self._dev_idx and samples.is_contiguous()):
+                xd = samples                  # already in place: the per-block hot path
+            else:
+                xd = self._to_dev(samples)
+            out = t.empty_like(xd)
+            if n:
+                sp = C._cuda_getCurrentRawStream(self._dev_idx)
+                if sp != self._stream_val:
+                    N.check(self._lib.sc_engine_set_stream(self._handle, sp))
+                    self._stream_val = sp
+                rc = self._pb(self._hv, xd.data_ptr(), n, out.data_ptr())
+                if rc:
+                    N.check(rc)
+        finally:
+            if prev != self._dev_idx:
+                C._cuda_exchangeDevice(prev)
+        res = out if samples is xd else _dev.like_input(out, samples)
+        return _signal(res, self._sample_rate)
 
     def flush(self) -> Signal:
         """Emit the pending residue and reset the engine (engine.py:148-161):
