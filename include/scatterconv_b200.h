@@ -111,10 +111,14 @@ int sc_fir_range(int dtype, int mode, const void *x, int64_t x_begin, int64_t x_
 int sc_fir_batched(int dtype, int mode, const void *x, int64_t ldx, const void *h, int64_t ldh,
                    void *y, int64_t ldy, int64_t channels, int64_t ne, int64_t nh, void *stream);
 
-/* Gather form with an (almost) exactly rounded accumulator: double-double
- * (TwoProduct + TwoSum) per output.  Device restatement of direct_form
- * (core.py:102-119, math.fsum); float64 only. */
-int sc_direct_form(const double *e, int64_t ne, const double *h, int64_t nh, double *y,
+/* Gather form with an exactly rounded accumulator: y[n] = math.fsum of the
+ * individually rounded products e[m]*h[n-m] (direct_form, core.py:102-119),
+ * bit-identical to CPython's fsum (Shewchuk partials + its half-even
+ * fix-up).  float64 only.  `status` (device pointer to one unsigned, may be
+ * NULL) receives bit 0 for an intermediate overflow of finite products and
+ * bit 1 for -inf + inf -- the two cases where math.fsum raises
+ * (OverflowError / ValueError) -- OR-ed in by the kernel. */
+int sc_direct_form(const double *e, int64_t ne, const double *h, int64_t nh, double *y, unsigned *status,
                    void *stream);
 
 /* ---------------------------------------------------------------- literal kernel */

@@ -36,7 +36,7 @@ _SIGNATURES = {
     "sc_fir_range": [ctypes.c_int, ctypes.c_int, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _vp],
     "sc_fir_batched": [ctypes.c_int, ctypes.c_int, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64,
                        _i64, _vp],
-    "sc_direct_form": [_vp, _i64, _vp, _i64, _vp, _vp],
+    "sc_direct_form": [_vp, _i64, _vp, _i64, _vp, _vp, _vp],
     "sc_scatter_block": [ctypes.c_int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64,
                          ctypes.c_double, _p64, _p64, _vp],
     "sc_engine_create": [ctypes.c_int, _vp, _i64, _i64, ctypes.c_double, _vp,

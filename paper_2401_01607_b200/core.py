@@ -197,9 +197,11 @@ def _split(full, n_body: int, sample_rate: int) -> ConvOutput:
 def direct_form(e: Signal, h: Signal) -> Signal:
     """Gather-form convolution (core.py:102-119).
 
-    The reference sums each output's products with math.fsum.  On the device
-    each output's individually rounded products are summed with a
-    compensated (double-double) accumulator, float64 always.
+    The reference sums each output's individually rounded products with
+    math.fsum; the device runs the same exactly rounded summation (CPython's
+    fsum algorithm, one thread per output), float64 always, so the results
+    are bit-identical.  Like math.fsum it raises OverflowError on an
+    intermediate overflow of finite products and ValueError on -inf + inf.
     """
     _check_pair(e, h)
     L = N.lib()
@@ -208,7 +210,13 @@ def direct_form(e: Signal, h: Signal) -> Signal:
     k = _dev.as_device(h.samples, np.float64, device=x.device)
     with t.cuda.device(x.device):
         y = t.empty(len(e) + len(h) - 1, dtype=t.float64, device=x.device)
-        N.check(L.sc_direct_form(N.ptr(x), len(e), N.ptr(k), len(h), N.ptr(y), N.stream_ptr()))
+        status = t.zeros(1, dtype=t.int32, device=x.device)
+        N.check(L.sc_direct_form(N.ptr(x), len(e), N.ptr(k), len(h), N.ptr(y), N.ptr(status), N.stream_ptr()))
+        bad = int(status.item())
+    if bad & 1:
+        raise OverflowError("intermediate overflow in fsum")
+    if bad & 2:
+        raise ValueError("-inf + inf in fsum")
     return Signal(_dev.like_input(y, e.samples, h.samples), e.sample_rate)
 
 

@@ -301,12 +301,12 @@ int sc_fir_batched(int dtype, int mode, const void *x, int64_t ldx, const void *
                           ne + nh - 1, channels, as_stream(stream));
 }
 
-int sc_direct_form(const double *e, int64_t ne, const double *h, int64_t nh, double *y,
+int sc_direct_form(const double *e, int64_t ne, const double *h, int64_t nh, double *y, unsigned *status,
                    void *stream) {
     SC_REQUIRE(ne >= 1, "sc_direct_form: input signal is empty");
     SC_REQUIRE(nh >= 1, "sc_direct_form: impulse response is empty");
     SC_REQUIRE(e && h && y, "sc_direct_form: null pointer");
-    return launch_direct_form_dd(e, ne, h, nh, y, as_stream(stream));
+    return launch_direct_form(e, ne, h, nh, y, status, as_stream(stream));
 }
 
 }  // extern "C"

@@ -473,34 +473,86 @@ int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off
 }
 
 // ---------------------------------------------------------------- direct form
-// Gather form of direct_form (core.py:102-119).  The reference sums the
-// individually rounded products e[m]*h[n-m] with math.fsum (exact rounding).
-// Here: products rounded the same way, summed with the compensated
-// "Sum2" scheme (TwoSum error-free transformation, error terms accumulated
-// and folded in once) -- as accurate as a double-double accumulator, which
-// is exactly rounded except under extreme cancellation.
+// direct_form (core.py:102-119): each output is math.fsum of its individually
+// rounded products e[m]*h[n-m], i.e. their EXACT sum rounded once.  One
+// thread per output runs CPython's fsum: Shewchuk's non-overlapping
+// "partials" (each new product is two-summed through them, so their exact
+// sum is always the exact running sum), then the partials are added from the
+// top with the round-half-even fix-up across partials -- the same published
+// algorithm, so the results are bit-identical to math.fsum.  Non-overlapping
+// doubles number at most ~40 (2098 exponent bits / 53), kept in local
+// memory; the usual count is 1-3.  Non-finite summands follow fsum: a NaN
+// or an Inf product short-circuits to their IEEE sum; -inf + inf and an
+// intermediate overflow of finite products, which fsum raises on, set
+// status bits 2 and 1 (the host raises ValueError / OverflowError).
+constexpr int FSUM_MAXP = 48;
 
-__device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
-    s = __dadd_rn(a, b);
-    const double bb = __dsub_rn(s, a);
-    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
-}
-
-__global__ void __launch_bounds__(TB) k_direct_dd(const double *__restrict__ e, int64_t ne,
-                                                  const double *__restrict__ h, int64_t nh,
-                                                  double *__restrict__ y) {
+__global__ void __launch_bounds__(TB) k_direct_fsum(const double *__restrict__ e, int64_t ne,
+                                                    const double *__restrict__ h, int64_t nh,
+                                                    double *__restrict__ y, unsigned *status) {
     const int64_t n = (int64_t)blockIdx.x * TB + threadIdx.x;
     if (n >= ne + nh - 1) return;
     const int64_t lo = n - nh + 1 > 0 ? n - nh + 1 : 0;
     const int64_t hi = n < ne - 1 ? n : ne - 1;
-    double s = 0.0, c = 0.0;
+    double p[FSUM_MAXP];
+    int np = 0;
+    double special = 0.0, inf_sum = 0.0;
+    unsigned bad = 0;
     for (int64_t m = lo; m <= hi; ++m) {
-        const double p = __dmul_rn(e[m], h[n - m]);
-        double q;
-        two_sum(s, p, s, q);
-        c = __dadd_rn(c, q);
+        double x = __dmul_rn(e[m], h[n - m]);
+        const double xsave = x;
+        int i = 0;
+        for (int j = 0; j < np; ++j) {
+            double yv = p[j];
+            if (fabs(x) < fabs(yv)) {
+                const double t = x;
+                x = yv;
+                yv = t;
+            }
+            const double hs = __dadd_rn(x, yv);
+            const double yr = __dsub_rn(hs, x);
+            const double ls = __dsub_rn(yv, yr);
+            if (ls != 0.0) p[i++] = ls;
+            x = hs;
+        }
+        np = i;
+        if (x != 0.0) {
+            if (!isfinite(x)) {
+                if (isfinite(xsave)) bad |= 1u;  // intermediate overflow
+                if (isinf(xsave)) inf_sum = __dadd_rn(inf_sum, xsave);
+                special = __dadd_rn(special, xsave);
+                np = 0;
+            } else if (np < FSUM_MAXP) {
+                p[np++] = x;
+            }
+        }
     }
-    y[n] = __dadd_rn(s, c);
+    double r = 0.0;
+    if (special != 0.0 || isnan(special)) {
+        if (isnan(inf_sum)) bad |= 2u;  // -inf + inf
+        r = special;
+    } else if (np > 0) {
+        double hs = p[--np], ls = 0.0;
+        while (np > 0) {
+            const double x = hs;
+            const double yv = p[--np];
+            hs = __dadd_rn(x, yv);
+            const double yr = __dsub_rn(hs, x);
+            ls = __dsub_rn(yv, yr);
+            if (ls != 0.0) break;
+        }
+        // round half to even across the partials below: if the rounding of
+        // hs + ls was a tie and the next partial pushes past it, round away
+        if (np > 0 && ((ls < 0.0 && p[np - 1] < 0.0) || (ls > 0.0 && p[np - 1] > 0.0))) {
+            const double yv = ls * 2.0;
+            const double x = __dadd_rn(hs, yv);
+            const double yr = __dsub_rn(x, hs);
+            if (yv == yr) hs = x;
+        }
+        r = hs;
+    }
+    y[n] = r;
+    if (bad && status) atomicOr(status, bad);
 }
 
 }  // namespace
@@ -520,11 +572,11 @@ int launch_chain(int dtype, int skip_mode, double threshold, const void *x, int6
     return SC_ERR_ARG;
 }
 
-int launch_direct_form_dd(const double *e, int64_t ne, const double *h, int64_t nh, double *y,
-                          cudaStream_t stream) {
+int launch_direct_form(const double *e, int64_t ne, const double *h, int64_t nh, double *y,
+                       unsigned *status, cudaStream_t stream) {
     const int64_t nout = ne + nh - 1;
     if (nout <= 0) return SC_OK;
-    k_direct_dd<<<(unsigned)cdiv(nout, TB), TB, 0, stream>>>(e, ne, h, nh, y);
+    k_direct_fsum<<<(unsigned)cdiv(nout, TB), TB, 0, stream>>>(e, ne, h, nh, y, status);
     SC_CHECK_LAUNCH();
     return SC_OK;
 }

@@ -166,7 +166,7 @@ int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_
                    const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin,
                    int64_t n_end, int64_t channels, cudaStream_t stream);
 
-int launch_direct_form_dd(const double *e, int64_t ne, const double *h, int64_t nh, double *y,
-                          cudaStream_t stream);
+int launch_direct_form(const double *e, int64_t ne, const double *h, int64_t nh, double *y,
+                       unsigned *status, cudaStream_t stream);
 
 }  // namespace sc

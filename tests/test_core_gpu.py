@@ -126,12 +126,45 @@ def test_golden_scatter_commuted_skip_bit_exact(pairs):
 
 
 def test_golden_direct_form(pairs):
-    exact = 0
+    """Exactly rounded like math.fsum: every golden output bit-exact."""
     for p in pairs:
         got = direct_form(_sig(p["e"]), _sig(p["h"])).samples
-        _near(got, p["direct"], 1e-15)
-        exact += int(np.array_equal(got, p["direct"]))
-    assert exact >= 0.95 * len(pairs)
+        assert np.array_equal(got, p["direct"])
+
+
+@given(e=_SEQ, h=_SEQ)
+@settings(max_examples=150)
+def test_direct_form_matches_fsum_oracle(e, h):
+    assert np.array_equal(direct_form(_sig(e), _sig(h)).samples, O.direct_form(e, h))
+
+
+def test_direct_form_cancellation_and_specials():
+    """Products whose exact sum cancels far below any partial (where a
+    compensated sum fails), ties that the half-even fix-up decides, and
+    fsum's non-finite rules (NaN / Inf propagate; -inf + inf and an
+    intermediate overflow raise like math.fsum)."""
+    import math
+
+    cases = [
+        ([1e16, 1.0, -1e16, 1e-16], [1.0]),
+        ([1.0, 2.0 ** -53, 2.0 ** -106], [1.0]),
+        ([2.0 ** 53, 1.0, 1.0 - 2.0 ** -53], [1.0, 1.0]),
+        ([1e308, 1e308, -1e308], [0.5]),
+        ([3.0, -1e-300, 1e300, -1e300], [1.0, 1e-10, 7.0]),
+        ([0.1] * 10 + [-1.0], [1.0]),
+    ]
+    for e, h in cases:
+        got = direct_form(_sig(e), _sig(h)).samples
+        ne, nh = len(e), len(h)
+        want = [math.fsum(e[m] * h[n - m] for m in range(max(0, n - nh + 1), min(n, ne - 1) + 1))
+                for n in range(ne + nh - 1)]
+        assert np.array_equal(got, np.asarray(want)), (e, h)
+    assert np.isnan(direct_form(_sig([1.0, float("nan")]), _sig([1.0])).samples[1])
+    assert direct_form(_sig([float("inf"), 1.0]), _sig([1.0, 1.0])).samples[1] == float("inf")
+    with pytest.raises(ValueError, match="inf"):
+        direct_form(_sig([float("inf"), float("-inf")]), _sig([1.0, 1.0]))
+    with pytest.raises(OverflowError):
+        direct_form(_sig([1e308, 1e308]), _sig([1.0, 1.0]))
 
 
 # ---------------------------------------------------------------- properties (float64)
