@@ -501,6 +501,7 @@ __global__ void k_stage_irs(StageCopies c, T *__restrict__ stage, int64_t dld) {
 // or, without swaps, ri = (ri0 + n_total) mod cap.  One CTA per channel.
 constexpr int64_t kMaxPlusNegInf = INT64_MIN / 4;
 constexpr int SS_TB = 256;
+constexpr int64_t kFoldLastScatter = 64;  // streams of at most this many blocks: J inside k_stream_state
 
 __device__ __forceinline__ void mp_then(int64_t &A, int64_t &B, int64_t A2, int64_t B2) {
     const int64_t b1 = B <= kMaxPlusNegInf ? kMaxPlusNegInf : B + A2;
@@ -553,11 +554,43 @@ __device__ void mp_reduce(const int64_t *__restrict__ Jc, int64_t lo, int64_t hi
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(SS_TB) k_stream_state(const int64_t *__restrict__ J, int64_t n_blocks, int64_t nb,
-                                                        int64_t n_total, int64_t nh0, StreamEvents ev, int64_t *st) {
+// Last scattering index of every block, by this CTA's warps: each warp takes
+// blocks in turn and scans one backwards 32 samples per ballot (a dense drive
+// is decided by the first ballot).  For the few-block streams where a
+// separate grid-wide pass would cost more launch than work.
+template <typename T>
+__device__ void blocks_last_scatter_cta(const T *__restrict__ xc, int64_t n_total, int64_t nb, int64_t n_blocks,
+                                        double thr, int64_t *__restrict__ Jc) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t b = threadIdx.x >> 5; b < n_blocks; b += SS_TB / 32) {
+        const int64_t base = b * nb;
+        const int64_t n = n_total - base < nb ? n_total - base : nb;
+        long long j = -1;
+        for (int64_t top = n; top > 0; top -= 32) {
+            const int64_t i = top - 1 - lane;
+            const unsigned bits = __ballot_sync(0xffffffffu, i >= 0 && !skipped<SC_SKIP_NOT_GT>(xc[base + i], thr));
+            if (bits) {
+                j = top - 1 - (__ffs(bits) - 1);  // lowest set lane = highest index
+                break;
+            }
+        }
+        if (lane == 0) Jc[b] = j;
+    }
+}
+
+__global__ void __launch_bounds__(SS_TB) k_stream_state(int64_t *__restrict__ J, int64_t n_blocks, int64_t nb,
+                                                        int64_t n_total, int64_t nh0, StreamEvents ev, int64_t *st,
+                                                        const void *x, int64_t ldx, double thr, int x_dtype) {
     const int64_t c = blockIdx.x;
     int64_t *s = st + c * ST_N;
-    const int64_t *Jc = J + c * n_blocks;
+    int64_t *Jc = J + c * n_blocks;
+    if (x) {  // J not computed by an earlier pass: find it here first
+        if (x_dtype == SC_F64)
+            blocks_last_scatter_cta(static_cast<const double *>(x) + c * ldx, n_total, nb, n_blocks, thr, Jc);
+        else
+            blocks_last_scatter_cta(static_cast<const float *>(x) + c * ldx, n_total, nb, n_blocks, thr, Jc);
+        __syncthreads();
+    }
     int last = -1;  // last event that precedes a processed block
     for (int k = 0; k < ev.n; ++k)
         if (ev.block[k] < n_blocks) last = k;
@@ -812,7 +845,7 @@ bool fast_stream_worth(const sc_engine *e, const ChainSeg *segs, int nseg) {
 
 // Also fills e->jbuf (last scattering index per block) from its mask pass.
 int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64_t nb, int64_t ub,
-                const ChainSeg *segs, int nseg, void *rin, void *rout, void *out, int64_t ldo) {
+                const ChainSeg *segs, int nseg, int64_t hld, void *rin, void *rout, void *out, int64_t ldo) {
     const int64_t n_blocks = cdiv(n_total, nb);
     int64_t L, NH;
     const bool batched = uniform_segs(segs, nseg, &L, &NH) && e->C * nseg < 65536;
@@ -861,7 +894,7 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
         StageCopies cp{};
         cp.n = nseg;
         for (int j = 0; j < nseg; ++j)
-            cp.src[j] = segs[j].h, cp.sld[j] = e->stage_ld, cp.off[j] = j * NH, cp.nh[j] = NH;
+            cp.src[j] = segs[j].h, cp.sld[j] = hld, cp.off[j] = j * NH, cp.nh[j] = NH;
         const dim3 gs((unsigned)std::min<int64_t>(cdiv(NH, 256), 64), (unsigned)nseg, (unsigned)e->C);
         k_stage_irs<float><<<gs, 256, 0, e->stream>>>(cp, static_cast<float *>(e->fh), nseg * NH);
         SC_CHECK_LAUNCH();
@@ -872,7 +905,7 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
         for (int j = 0; j < nseg; ++j) {
             // outputs [m_lo, m_hi + nh - 1) of segment j's drive samples
             rc = launch_fir_f32(SC_MODE_FAST, xm, xpitch, 0, segs[j].m_lo, segs[j].m_hi,
-                                static_cast<const float *>(segs[j].h), e->stage_ld, segs[j].nh, fy + sg.off[j],
+                                static_cast<const float *>(segs[j].h), hld, segs[j].nh, fy + sg.off[j],
                                 ypitch, segs[j].m_lo, segs[j].m_hi + segs[j].nh - 1, e->C, e->stream);
             if (rc) return rc;
         }
@@ -950,13 +983,16 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
     }
     // Stage every IR of the timeline in engine-owned memory (the kernels run
     // after this call returns; callers may free their buffers): [C][stage_ld].
+    // (A call without IR changes reads the engine's own copy directly.)
+    const bool staged = !ev.empty();
     int64_t tot = e->nh;
     for (const Ev &v : ev) tot += v.nh;
-    int rc = ensure_2d(&e->stage, &e->stage_ld, tot, e->es, e->C, 0, e->stream);
+    int rc = staged ? ensure_2d(&e->stage, &e->stage_ld, tot, e->es, e->C, 0, e->stream) : SC_OK;
     if (rc) return rc;
     rc = ensure_2d(reinterpret_cast<void **>(&e->jbuf), &e->jbuf_ld, n_blocks * e->C, 8, 1, 0, e->stream);
     if (rc) return rc;
-    char *stage = static_cast<char *>(e->stage);
+    char *stage = staged ? static_cast<char *>(e->stage) : static_cast<char *>(e->ir);
+    const int64_t hld = staged ? e->stage_ld : e->ir_ld;  // row pitch of every segment's taps
     StageCopies cp{};
     int64_t max_nh = e->nh;
     cp.src[0] = e->ir, cp.sld[0] = e->ir_ld, cp.off[0] = 0, cp.nh[0] = e->nh, cp.n = 1;
@@ -984,7 +1020,7 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
         off += v.nh;
         ub = v.nh > ub ? v.nh : ub;
     }
-    {
+    if (staged) {
         const dim3 gs((unsigned)std::min<int64_t>(cdiv(max_nh, 256), 64), (unsigned)cp.n, (unsigned)e->C);
         if (e->dtype == SC_F64)
             k_stage_irs<double><<<gs, 256, 0, e->stream>>>(cp, static_cast<double *>(e->stage), e->stage_ld);
@@ -998,14 +1034,18 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
     // in ascending order across blocks and IR segments -- the same chain as
     // block-by-block processing (bit-identical), continued from the residue.
     void *rin = e->res[e->cur], *rout = e->res[1 - e->cur];
+    bool j_from_x = false;
     if (fast_stream_worth(e, segs, nseg)) {
-        rc = fast_stream(e, x, ldx, n_total, nb, ub, segs, nseg, rin, rout, out, ldo);
+        rc = fast_stream(e, x, ldx, n_total, nb, ub, segs, nseg, hld, rin, rout, out, ldo);
         if (rc) return rc;
     } else {
-        ChainBatch batch{e->C, ldx, e->stage_ld, ldo, e->res_ld, e->res_ld, ST_N};
+        ChainBatch batch{e->C, ldx, hld, ldo, e->res_ld, e->res_ld, ST_N};
         rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, x, 0, segs, nseg, rin, 0, e->st + ST_CAP, 0,
                           n_total + ub, out, n_total, rout, e->stream, nullptr, &batch, fused_chain(e));
         if (rc) return rc;
+        if (n_blocks <= kFoldLastScatter) {
+            j_from_x = true;  // the state kernel finds J itself
+        } else {
         const dim3 gj((unsigned)n_blocks, (unsigned)e->C);
         if (e->dtype == SC_F64)
             k_blocks_last_scatter<double><<<gj, 256, 0, e->stream>>>(static_cast<const double *>(x), ldx, n_total,
@@ -1014,12 +1054,14 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
             k_blocks_last_scatter<float><<<gj, 256, 0, e->stream>>>(static_cast<const float *>(x), ldx, n_total,
                                                                    nb, e->thr, n_blocks, e->jbuf);
         SC_CHECK_LAUNCH();
+        }
     }
-    k_stream_state<<<(unsigned)e->C, SS_TB, 0, e->stream>>>(e->jbuf, n_blocks, nb, n_total, e->nh, sev, e->st);
+    k_stream_state<<<(unsigned)e->C, SS_TB, 0, e->stream>>>(e->jbuf, n_blocks, nb, n_total, e->nh, sev, e->st,
+                                                            j_from_x ? x : nullptr, ldx, e->thr, e->dtype);
     SC_CHECK_LAUNCH();
     // host-side bookkeeping: the last IR becomes current (engine-owned copy)
     const ChainSeg &last = segs[nseg - 1];
-    if (last.h != stage) {
+    if (staged && last.h != stage) {
         rc = ensure_2d(&e->ir, &e->ir_ld, last.nh, e->es, e->C, 0, e->stream);
         if (rc) return rc;
         rc = copy_rows(e, e->ir, e->ir_ld, last.h, e->stage_ld, last.nh);

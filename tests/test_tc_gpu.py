@@ -123,7 +123,7 @@ def test_pinned_host_pipeline(monkeypatch, mode):
     from paper_2401_01607_b200 import core
 
     monkeypatch.setattr(core, "_PIPELINE_MIN_MACS", 0)
-    monkeypatch.setattr(core, "_PIPELINE_CHUNK_MACS", 70_001 * 3_333 // 5)   # 5 chunks
+    monkeypatch.setenv("SC_PIPE_CHUNKS", "5")   # the native range engine's chunk count
     rng = np.random.default_rng(44)
     x = rng.uniform(-1, 1, 70_001).astype(np.float32)
     h = rng.standard_normal(3_333).astype(np.float32)
@@ -144,7 +144,7 @@ def test_pinned_host_pipeline_transfer_bound(monkeypatch, nh):
     from paper_2401_01607_b200 import core
 
     monkeypatch.setattr(core, "_PIPELINE_MIN_BYTES", 4 * 100_000)
-    monkeypatch.setattr(core, "_PIPELINE_CHUNK_BYTES", 4 * 30_000)   # 7 chunks
+    monkeypatch.setenv("SC_PIPE_CHUNKS", "7")
     calls = []
     real = core._fir_host_pipelined
     monkeypatch.setattr(core, "_fir_host_pipelined", lambda *a: calls.append(1) or real(*a))
