@@ -185,6 +185,21 @@ int sc_engine_swap_ir(sc_engine *e, const void *h, int64_t nh);
 /* swap_ir_at_next_block (engine.py:188-192).  Async (h is copied). */
 int sc_engine_swap_ir_at_next_block(sc_engine *e, const void *h, int64_t nh);
 
+/* Independent channels (engine.py:60-66: one ScatterEngine per channel, each
+ * with its own IR, length and swap times).  h is [C][ldh] (device);
+ * channel c swaps to its row's first nh_per_channel[c] taps when that is
+ * >= 1 and keeps its IR otherwise (nh_per_channel is a HOST array of C
+ * lengths).  Channels may then hold IRs of different lengths: every
+ * channel's live / cap / read_index / tail length follows its own
+ * (engine.py:163-192 per channel).  _at_next_block is the per-channel
+ * pending swap (a uniform pending swap becomes per-channel, the named
+ * channels replacing theirs). */
+int sc_engine_swap_ir_channels(sc_engine *e, const void *h, int64_t ldh, const int64_t *nh_per_channel);
+int sc_engine_swap_ir_at_next_block_channels(sc_engine *e, const void *h, int64_t ldh,
+                                             const int64_t *nh_per_channel);
+/* Host copy of every channel's current IR length (C values). */
+int sc_engine_channel_nh(sc_engine *e, int64_t *nh_per_channel);
+
 /* flush (engine.py:148-161): writes max(nh-1, live) tail samples in emission
  * order to tail (device, capacity tail_capacity; per channel for a
  * multichannel engine), returns the count(s) in n_tail and resets the engine
@@ -233,6 +248,16 @@ int sc_engine_process_blocks(sc_engine *e, const void *x, int64_t n_total, int64
 /* Graph-replay bookkeeping of sc_engine_process_blocks: replays, captures,
  * and captures that failed (those keys then always run directly). */
 int sc_engine_graph_stats(sc_engine *e, int64_t *hits, int64_t *captures, int64_t *failures);
+
+/* process_blocks with a per-channel swap schedule: before block
+ * swap_blocks[i], channel c swaps to row c of swap_irs[i] ([C][swap_ld[i]],
+ * swap_ld may be NULL = the longest length of that swap) with length
+ * swap_nh[i*C + c], or keeps its IR when that is <= 0.  Blocks run one
+ * launch each (one engine per channel semantics; bit-identical to the
+ * equivalent sequence of per-channel swaps and process_block calls). */
+int sc_engine_process_blocks_channels(sc_engine *e, const void *x, int64_t n_total, int64_t nb,
+                                      const int64_t *swap_blocks, const void *const *swap_irs,
+                                      const int64_t *swap_ld, const int64_t *swap_nh, int64_t n_swaps, void *out);
 
 /* The same with x[C][n_total] and out[C][n_total] in HOST memory (pinned for
  * full PCIe rate; swap IRs on the device).  The stream is processed in

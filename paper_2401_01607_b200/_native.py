@@ -74,6 +74,11 @@ _SIGNATURES = {
                                       _vp, ctypes.c_int],
     "sc_tc_stats": [_p64, _p64, _pint, _pint],
     "sc_engine_graph_stats": [_vp, _p64, _p64, _p64],
+    "sc_engine_swap_ir_channels": [_vp, _vp, _i64, _p64],
+    "sc_engine_swap_ir_at_next_block_channels": [_vp, _vp, _i64, _p64],
+    "sc_engine_channel_nh": [_vp, _p64],
+    "sc_engine_process_blocks_channels": [_vp, _vp, _i64, _i64, _p64, ctypes.POINTER(_vp), _p64, _p64, _i64,
+                                          _vp],
 }
 EXPORTS = tuple(_SIGNATURES) + ("sc_last_error", "sc_launch_count", "sc_tc_stats_reset")
 

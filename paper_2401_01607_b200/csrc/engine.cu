@@ -37,7 +37,10 @@
 namespace sc {
 namespace {
 
-enum { ST_LIVE = 0, ST_CAP = 1, ST_RI = 2, ST_N = 4 };
+// per-channel device state: live, cap, read_index, and the channel's current
+// IR length (channels may hold IRs of different lengths: one engine per
+// channel, engine.py:60-66)
+enum { ST_LIVE = 0, ST_CAP = 1, ST_RI = 2, ST_NH = 3, ST_N = 4 };
 
 // live/read_index after a block (derivation in DESIGN.md): with J = last
 // index whose sample scatters (-1 if none),
@@ -60,6 +63,7 @@ __global__ void k_block_epilogue(const T *__restrict__ x, int64_t ldx, int64_t n
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) J = sj[w] > J ? sj[w] : J;
+        if (nh <= 0) nh = s[ST_NH];  // channels with their own IR lengths
         int64_t live = s[ST_LIVE] - n;
         if (live < 0) live = 0;
         if (J >= 0 && nh - n + J > live) live = nh - n + J;
@@ -75,14 +79,29 @@ __global__ void k_swap_state(int64_t *st, int64_t nh_new, int64_t C) {
     const int64_t live = s[ST_LIVE];
     s[ST_CAP] = nh_new > live ? nh_new : live;  // engine.py:179
     s[ST_RI] = 0;                               // engine.py:184
+    s[ST_NH] = nh_new;
 }
 
+// per-channel swap: channels with nh_new[c] > 0 swap (to that length), the
+// others keep their IR and state untouched
+__global__ void k_swap_state_ch(int64_t *st, const int64_t *__restrict__ nh_new, int64_t C) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C || nh_new[c] <= 0) return;
+    int64_t *s = st + c * ST_N;
+    const int64_t live = s[ST_LIVE];
+    s[ST_CAP] = nh_new[c] > live ? nh_new[c] : live;
+    s[ST_RI] = 0;
+    s[ST_NH] = nh_new[c];
+}
+
+// nh <= 0: every channel keeps its own IR length (cap = that length)
 __global__ void k_reset_state(int64_t *st, int64_t nh, int64_t C) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= C) return;
     int64_t *s = st + c * ST_N;
     s[ST_LIVE] = 0;
-    s[ST_CAP] = nh;
+    if (nh > 0) s[ST_NH] = nh;
+    s[ST_CAP] = s[ST_NH];
     s[ST_RI] = 0;
 }
 
@@ -143,6 +162,7 @@ struct BlockStepArgs {
     int64_t *st;
     double thr;
     int slot_ctas;
+    int ragged;  // channels hold IRs of different lengths: nh = st[ST_NH] per channel
 };
 
 __device__ __forceinline__ void cp_async_elem(void *smem, const void *gmem, int bytes) {
@@ -179,9 +199,10 @@ __global__ void __launch_bounds__(BS_TB) k_block_step(BlockStepArgs a) {
         __syncthreads();
         if (threadIdx.x == 0) {
             for (int w = 1; w < BS_TB / 32; ++w) J = sj[w] > J ? sj[w] : J;
+            const int64_t nh = a.ragged ? st[ST_NH] : a.nh;
             int64_t live = st[ST_LIVE] - a.n;
             if (live < 0) live = 0;
-            if (J >= 0 && a.nh - a.n + J > live) live = a.nh - a.n + J;
+            if (J >= 0 && nh - a.n + J > live) live = nh - a.n + J;
             st[ST_LIVE] = live;
             st[ST_RI] = (st[ST_RI] + a.n) % st[ST_CAP];
         }
@@ -192,16 +213,20 @@ __global__ void __launch_bounds__(BS_TB) k_block_step(BlockStepArgs a) {
     T *hs = reinterpret_cast<T *>(xm + BS_MAX_N / 32);
     const int64_t t0 = (int64_t)blockIdx.x * BS_TB;
     const int64_t t = t0 + threadIdx.x;
+    asm volatile("griddepcontrol.launch_dependents;\n" ::);
+    // a ragged engine's per-channel IR length lives in the device state:
+    // read after this grid's predecessors are done
+    if (a.ragged) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    const int64_t nhc = a.ragged ? st[ST_NH] : a.nh;
     // taps k = t - m for this CTA's slots: [k0, k1)
     const int64_t k0 = t0 - (n - 1) > 0 ? t0 - (n - 1) : 0;
-    const int64_t k1 = t0 + BS_TB < a.nh ? t0 + BS_TB : a.nh;
+    const int64_t k1 = t0 + BS_TB < nhc ? t0 + BS_TB : nhc;
     const T *__restrict__ hc = static_cast<const T *>(a.h) + (int64_t)c * a.ldh;
     // Programmatic dependent launch: the next block's kernel may start now
     // (its CTAs fit beside ours); it stages its taps -- engine-owned, only
     // ever written by swaps, which are stream-ordered before any kernel they
     // precede -- and then waits for this grid before touching the residue,
     // the state or its block.
-    asm volatile("griddepcontrol.launch_dependents;\n" ::);
     for (int64_t k = k0 + threadIdx.x; k < k1; k += BS_TB) cp_async_elem(hs + (k - k0), hc + k, (int)sizeof(T));
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -229,7 +254,7 @@ __global__ void __launch_bounds__(BS_TB) k_block_step(BlockStepArgs a) {
     if (t >= a.n_slots) return;
     T acc = t < cap ? r0 : T(0);
     // m in [max(0, t - nh + 1), min(n - 1, t)]
-    const int64_t mlo64 = t - a.nh + 1 > 0 ? t - a.nh + 1 : 0;
+    const int64_t mlo64 = t - nhc + 1 > 0 ? t - nhc + 1 : 0;
     const int mlo = (int)(mlo64 < n ? mlo64 : n);
     const int mhi = (int)(t < n - 1 ? t : n - 1);
     const T *hb = hs + (t - k0);  // tap k = t - m at hb[-m]
@@ -346,7 +371,7 @@ __global__ void k_flush(T *__restrict__ cur, T *__restrict__ other, int64_t res_
         int64_t *sc = st + c * ST_N;
         for (int k = 0; k < ST_N; ++k) st_host[c * ST_N + k] = sc[k];
         sc[ST_LIVE] = 0;
-        sc[ST_CAP] = nh;
+        sc[ST_CAP] = nh > 0 ? nh : sc[ST_NH];  // ring of len(ir) (engine.py:157), per channel when ragged
         sc[ST_RI] = 0;
     }
 }
@@ -613,6 +638,7 @@ __global__ void __launch_bounds__(SS_TB) k_stream_state(int64_t *__restrict__ J,
             const int64_t nh_last = ev.nh[last];
             cap = nh_last > live ? nh_last : live;
             ri = since % cap;
+            s[ST_NH] = nh_last;
         } else {
             ri = (ri + since) % cap;
         }
@@ -673,6 +699,17 @@ struct sc_engine {
     cudaStream_t cap_stream = nullptr;  // private stream the graphs are captured on
     bool flush_open = false;
     int64_t flush_cap = 0, flush_nh = 0;
+    // Channels with IRs of their own (per-channel swaps, engine.py:60-66's one
+    // engine per channel): host copy of every channel's IR length; `ragged`
+    // when they differ (the kernels then read each channel's length from the
+    // device state).  A per-channel pending swap keeps its lengths in pend_nh_c
+    // (<= 0: that channel has none).  nh_arg: device copy of one swap's
+    // per-channel lengths for k_swap_state_ch.
+    int64_t *nh_host = nullptr;
+    bool ragged = false;
+    int64_t *pend_nh_c = nullptr;
+    bool pend_ch = false;
+    int64_t *nh_arg = nullptr;
 };
 
 namespace {
@@ -735,9 +772,63 @@ int do_swap(sc_engine *e, const void *h, int64_t h_ld, int64_t nh) {
     if (rc) return rc;
     e->cap_ub = ub;
     e->nh = nh;
+    for (int64_t c = 0; c < e->C; ++c) e->nh_host[c] = nh;
+    e->ragged = false;
     k_swap_state<<<cgrid(e->C), 128, 0, e->stream>>>(e->st, nh, e->C);
     SC_CHECK_LAUNCH();
     return SC_OK;
+}
+
+// Per-channel swap_ir: channel c with nh_new[c] > 0 takes row c of h (pitch
+// h_ld) as its new IR, the others keep theirs (one engine per channel,
+// engine.py:163-186 each).  Rows are zero-padded past their length.
+int do_swap_ch(sc_engine *e, const void *h, int64_t h_ld, const int64_t *nh_new) {
+    int64_t mx = 0;
+    for (int64_t c = 0; c < e->C; ++c) {
+        const int64_t keep = nh_new[c] > 0 ? nh_new[c] : e->nh_host[c];
+        mx = keep > mx ? keep : mx;
+    }
+    int rc = SC_OK;
+    if (h != e->ir) {
+        // the untouched channels' taps must survive a wider buffer
+        rc = ensure_2d(&e->ir, &e->ir_ld, mx, e->es, e->C, e->nh, e->stream);
+        if (rc) return rc;
+        for (int64_t c = 0; c < e->C; ++c) {
+            if (nh_new[c] <= 0) continue;
+            char *dst = static_cast<char *>(e->ir) + (size_t)(c * e->ir_ld) * e->es;
+            SC_CHECK_CUDA(cudaMemcpyAsync(dst, static_cast<const char *>(h) + (size_t)(c * h_ld) * e->es,
+                                          (size_t)nh_new[c] * e->es, cudaMemcpyDeviceToDevice, e->stream));
+            if (e->ir_ld > nh_new[c])
+                SC_CHECK_CUDA(cudaMemsetAsync(dst + (size_t)nh_new[c] * e->es, 0,
+                                              (size_t)(e->ir_ld - nh_new[c]) * e->es, e->stream));
+        }
+    }
+    const int64_t ub = mx > e->cap_ub ? mx : e->cap_ub;
+    rc = grow_residue(e, ub);
+    if (rc) return rc;
+    e->cap_ub = ub;
+    // the lengths go to the device in stream order (a pageable source is
+    // staged by the copy call itself, so nh_new need not outlive it)
+    SC_CHECK_CUDA(cudaMemcpyAsync(e->nh_arg, nh_new, sizeof(int64_t) * e->C, cudaMemcpyHostToDevice, e->stream));
+    bool uniform = true;
+    for (int64_t c = 0; c < e->C; ++c) {
+        if (nh_new[c] > 0) e->nh_host[c] = nh_new[c];
+        uniform = uniform && e->nh_host[c] == e->nh_host[0];
+    }
+    e->nh = mx;
+    e->ragged = !uniform;
+    k_swap_state_ch<<<cgrid(e->C), 128, 0, e->stream>>>(e->st, e->nh_arg, e->C);
+    SC_CHECK_LAUNCH();
+    return SC_OK;
+}
+
+int run_pending_swap(sc_engine *e) {
+    e->has_pending = false;
+    if (e->pend_ch) {
+        e->pend_ch = false;
+        return do_swap_ch(e, e->pend, e->pend_ld, e->pend_nh_c);
+    }
+    return do_swap(e, e->pend, e->pend_ld, e->pend_nh);
 }
 
 // One block of n samples per channel: block/out are [C][ld].
@@ -746,8 +837,7 @@ bool fused_chain(const sc_engine *e) { return e->dtype == SC_F64 && e->mode == S
 
 int do_block(sc_engine *e, const void *block, int64_t ldx, int64_t n, void *out, int64_t ldo, bool apply_pending) {
     if (apply_pending && e->has_pending) {
-        e->has_pending = false;
-        int rc = do_swap(e, e->pend, e->pend_ld, e->pend_nh);
+        int rc = run_pending_swap(e);
         if (rc) return rc;
     }
     SC_REQUIRE(n <= e->nb, "block of %lld samples exceeds block_size_nb=%lld", (long long)n,
@@ -765,18 +855,35 @@ int do_block(sc_engine *e, const void *block, int64_t ldx, int64_t n, void *out,
         a.st = e->st;
         a.thr = e->thr;
         a.slot_ctas = (int)cdiv(a.n_slots, BS_TB);
+        a.ragged = e->ragged ? 1 : 0;
         int rc = launch_block_step(a, e->dtype, fused_chain(e), e->C, e->stream);
         if (rc) return rc;
         e->cur = 1 - e->cur;
         e->consumed += n;
         return SC_OK;
     }
-    ChainSeg seg{e->ir, e->nh, 0, n};
-    ChainBatch batch{e->C, ldx, e->ir_ld, ldo, e->res_ld, e->res_ld, ST_N};
-    int rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, block, 0, &seg, 1, rin, 0, e->st + ST_CAP, 0,
+    int rc = SC_OK;
+    if (e->ragged) {
+        // channels with their own IR lengths: one ordered launch per channel
+        for (int64_t c = 0; c < e->C; ++c) {
+            const size_t es = e->es;
+            ChainSeg seg{static_cast<const char *>(e->ir) + (size_t)(c * e->ir_ld) * es, e->nh_host[c], 0, n};
+            ChainBatch batch{1, ldx, e->ir_ld, ldo, e->res_ld, e->res_ld, ST_N};
+            rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, static_cast<const char *>(block) + (size_t)(c * ldx) * es,
+                              0, &seg, 1, static_cast<const char *>(rin) + (size_t)(c * e->res_ld) * es, 0,
+                              e->st + c * ST_N + ST_CAP, 0, n + e->cap_ub, static_cast<char *>(out) + (size_t)(c * ldo) * es,
+                              n, static_cast<char *>(rout) + (size_t)(c * e->res_ld) * es, e->stream, nullptr, &batch,
+                              fused_chain(e));
+            if (rc) return rc;
+        }
+    } else {
+        ChainSeg seg{e->ir, e->nh, 0, n};
+        ChainBatch batch{e->C, ldx, e->ir_ld, ldo, e->res_ld, e->res_ld, ST_N};
+        rc = launch_chain(e->dtype, SC_SKIP_NOT_GT, e->thr, block, 0, &seg, 1, rin, 0, e->st + ST_CAP, 0,
                           n + e->cap_ub, out, n, rout, e->stream, nullptr, &batch, fused_chain(e));
+    }
     if (rc) return rc;
-    rc = launch_epilogue(e->dtype, block, ldx, n, e->thr, e->nh, e->st, e->C, e->stream);
+    rc = launch_epilogue(e->dtype, block, ldx, n, e->thr, e->ragged ? 0 : e->nh, e->st, e->C, e->stream);
     if (rc) return rc;
     e->cur = 1 - e->cur;
     e->consumed += n;
@@ -919,10 +1026,52 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
     return SC_OK;
 }
 
+// Block-by-block execution of a stream: for engines whose channels hold IRs
+// of their own (or a per-channel swap schedule).  Swaps scheduled before
+// block b run in schedule order, then the block (a pending swap at block 0,
+// after the explicit ones, as process_block orders it).  nh_stride 0: swap i
+// gives every channel length swap_nh[i]; nh_stride C: channel c's length is
+// swap_nh[i*C + c] (<= 0 keeps that channel's IR).
+int process_blocks_stepwise(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64_t nb,
+                            const int64_t *swap_blocks, const void *const *swap_irs, const int64_t *swap_ld,
+                            const int64_t *swap_nh, int64_t nh_stride, int64_t n_swaps, void *out, int64_t ldo) {
+    const int64_t n_blocks = cdiv(n_total, nb);
+    std::vector<int64_t> order;
+    for (int64_t i = 0; i < n_swaps; ++i)
+        if (swap_blocks[i] >= 0 && swap_blocks[i] < n_blocks) order.push_back(i);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int64_t a, int64_t b) { return swap_blocks[a] < swap_blocks[b]; });
+    size_t k = 0;
+    for (int64_t b = 0; b < n_blocks; ++b) {
+        for (; k < order.size() && swap_blocks[order[k]] == b; ++k) {
+            const int64_t i = order[k];
+            const int64_t ld = swap_ld ? swap_ld[i] : (nh_stride ? 0 : swap_nh[i]);
+            int rc;
+            if (nh_stride) {
+                int64_t ldm = ld;
+                if (!ldm)
+                    for (int64_t c = 0; c < e->C; ++c) ldm = swap_nh[i * nh_stride + c] > ldm ? swap_nh[i * nh_stride + c] : ldm;
+                rc = do_swap_ch(e, swap_irs[i], ldm, swap_nh + i * nh_stride);
+            } else {
+                rc = do_swap(e, swap_irs[i], ld, swap_nh[i]);
+            }
+            if (rc) return rc;
+        }
+        const int64_t s0 = b * nb, n = n_total - s0 < nb ? n_total - s0 : nb;
+        int rc = do_block(e, static_cast<const char *>(x) + (size_t)s0 * e->es, ldx, n,
+                          static_cast<char *>(out) + (size_t)s0 * e->es, ldo, b == 0);
+        if (rc) return rc;
+    }
+    return SC_OK;
+}
+
 int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64_t nb,
                         const int64_t *swap_blocks, const void *const *swap_irs, const int64_t *swap_nh,
                         const int64_t *swap_ld, int64_t n_swaps, void *out, int64_t ldo) {
     if (n_total == 0) return SC_OK;
+    if (e->ragged || e->pend_ch)
+        return process_blocks_stepwise(e, x, ldx, n_total, nb, swap_blocks, swap_irs, swap_ld, swap_nh, 0, n_swaps,
+                                       out, ldo);
     const int64_t n_blocks = cdiv(n_total, nb);
     // IR timeline: (block, h [C][nh], nh); a pending deferred swap acts right
     // before block 0, after any explicit swap scheduled there (engine.py:124-126).
@@ -1069,6 +1218,7 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
         e->nh = last.nh;
     }
     e->cap_ub = ub;
+    for (int64_t c = 0; c < e->C; ++c) e->nh_host[c] = e->nh;
     e->cur = 1 - e->cur;
     e->consumed += n_total;
     return SC_OK;
@@ -1152,7 +1302,7 @@ int process_blocks_graphed(sc_engine *e, const void *x, int64_t n_total, int64_t
         return process_blocks_impl(e, x, n_total, n_total, nb, swap_blocks, swap_irs, swap_nh, nullptr, n_swaps, out,
                                    n_total);
     };
-    if (!graphs_enabled() || n_total == 0) return direct();
+    if (!graphs_enabled() || n_total == 0 || e->ragged || e->pend_ch) return direct();
     if (!e->gc) e->gc = new GraphCache();
     GraphCache *gc = e->gc;
     const int64_t key_gen = scratch_generation();
@@ -1182,6 +1332,7 @@ int process_blocks_graphed(sc_engine *e, const void *x, int64_t n_total, int64_t
         note_tc_replay(g.tc_launches, g.tc_padded, g.tc_ssh, g.tc_tn);
         e->has_pending = false;
         e->nh = g.post_nh;
+        for (int64_t c = 0; c < e->C; ++c) e->nh_host[c] = e->nh;
         e->cap_ub = g.post_cap_ub;
         e->cur = g.post_cur;
         e->consumed = consumed + n_total;
@@ -1249,6 +1400,7 @@ int process_blocks_graphed(sc_engine *e, const void *x, int64_t n_total, int64_t
     const int64_t consumed_now = pre.consumed;
     e->has_pending = pre.has_pending;
     e->nh = pre.nh;
+    for (int64_t c = 0; c < e->C; ++c) e->nh_host[c] = e->nh;
     e->cap_ub = pre.cap_ub;
     e->cur = pre.cur;
     e->consumed = consumed_now;
@@ -1283,6 +1435,19 @@ int sc_engine_create_multi(int dtype, const void *h, int64_t nh, int64_t channel
     e->thr = threshold;
     int rc = SC_OK;
     if (cudaMalloc(&e->st, sizeof(int64_t) * ST_N * channels) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("sc_engine_create: cudaMalloc failed");
+        rc = SC_ERR_ALLOC;
+    }
+    e->nh_host = new (std::nothrow) int64_t[channels];
+    e->pend_nh_c = new (std::nothrow) int64_t[channels];
+    if (!e->nh_host || !e->pend_nh_c) {
+        set_error("sc_engine_create: out of host memory");
+        rc = SC_ERR_ALLOC;
+    } else {
+        for (int64_t c = 0; c < channels; ++c) e->nh_host[c] = nh, e->pend_nh_c[c] = 0;
+    }
+    if (!rc && cudaMalloc(reinterpret_cast<void **>(&e->nh_arg), sizeof(int64_t) * channels) != cudaSuccess) {
         cudaGetLastError();
         set_error("sc_engine_create: cudaMalloc failed");
         rc = SC_ERR_ALLOC;
@@ -1325,6 +1490,9 @@ int sc_engine_destroy(sc_engine *e) {
     cudaFree(e->res[1]);
     cudaFree(e->st);
     pinned_small_free(e->st_host);
+    cudaFree(e->nh_arg);
+    delete[] e->nh_host;
+    delete[] e->pend_nh_c;
     delete e->gc;
     if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
     cudaFree(e->stage);
@@ -1361,7 +1529,7 @@ int sc_engine_process_block(sc_engine *e, const void *block, int64_t n, void *ou
     // the channels, with the IR that will be in force) goes through the fused
     // path as a one-block stream (same state updates, pending swap included)
     const int64_t nh_next = e->has_pending ? e->pend_nh : e->nh;
-    if (n > 0 && n <= e->nb && e->mode == SC_MODE_FAST && e->dtype == SC_F32 &&
+    if (n > 0 && n <= e->nb && e->mode == SC_MODE_FAST && e->dtype == SC_F32 && !e->ragged && !e->pend_ch &&
         (double)e->C * (double)n * (double)nh_next >= 1073741824.0)
         return process_blocks_impl(e, block, n, n, n, nullptr, nullptr, nullptr, nullptr, 0, out, n);
     return do_block(e, block, n, n, out, n, true);
@@ -1391,7 +1559,66 @@ int sc_engine_swap_ir_at_next_block(sc_engine *e, const void *h, int64_t nh) {
     if (rc) return rc;
     e->pend_nh = nh;
     e->has_pending = true;
+    e->pend_ch = false;
     return SC_OK;
+}
+
+int sc_engine_swap_ir_channels(sc_engine *e, const void *h, int64_t ldh, const int64_t *nh_per_channel) {
+    SC_REQUIRE(e && h && nh_per_channel, "sc_engine_swap_ir_channels: null pointer");
+    DeviceGuard g(e->device);
+    int64_t mx = 0;
+    for (int64_t c = 0; c < e->C; ++c) mx = nh_per_channel[c] > mx ? nh_per_channel[c] : mx;
+    SC_REQUIRE(mx >= 1, "sc_engine_swap_ir_channels: no channel swaps");
+    SC_REQUIRE(ldh >= mx, "sc_engine_swap_ir_channels: row pitch below the longest IR");
+    return do_swap_ch(e, h, ldh, nh_per_channel);
+}
+
+int sc_engine_swap_ir_at_next_block_channels(sc_engine *e, const void *h, int64_t ldh,
+                                             const int64_t *nh_per_channel) {
+    SC_REQUIRE(e && h && nh_per_channel, "sc_engine_swap_ir_at_next_block_channels: null pointer");
+    DeviceGuard g(e->device);
+    int64_t mx = 0;
+    for (int64_t c = 0; c < e->C; ++c) mx = nh_per_channel[c] > mx ? nh_per_channel[c] : mx;
+    SC_REQUIRE(mx >= 1, "sc_engine_swap_ir_at_next_block_channels: no channel swaps");
+    SC_REQUIRE(ldh >= mx, "sc_engine_swap_ir_at_next_block_channels: row pitch below the longest IR");
+    // a uniform pending swap becomes per-channel: the channels named here
+    // replace theirs (engine.py:188-192, per channel)
+    if (e->has_pending && !e->pend_ch)
+        for (int64_t c = 0; c < e->C; ++c) e->pend_nh_c[c] = e->pend_nh;
+    if (!e->has_pending)
+        for (int64_t c = 0; c < e->C; ++c) e->pend_nh_c[c] = 0;
+    const int64_t keep_n = e->has_pending ? e->pend_ld : 0;
+    int rc = ensure_2d(&e->pend, &e->pend_ld, mx, e->es, e->C, keep_n, e->stream);
+    if (rc) return rc;
+    for (int64_t c = 0; c < e->C; ++c) {
+        if (nh_per_channel[c] <= 0) continue;
+        SC_CHECK_CUDA(cudaMemcpyAsync(static_cast<char *>(e->pend) + (size_t)(c * e->pend_ld) * e->es,
+                                      static_cast<const char *>(h) + (size_t)(c * ldh) * e->es,
+                                      (size_t)nh_per_channel[c] * e->es, cudaMemcpyDeviceToDevice, e->stream));
+        e->pend_nh_c[c] = nh_per_channel[c];
+    }
+    e->has_pending = true;
+    e->pend_ch = true;
+    return SC_OK;
+}
+
+int sc_engine_channel_nh(sc_engine *e, int64_t *nh_per_channel) {
+    SC_REQUIRE(e && nh_per_channel, "sc_engine_channel_nh: null pointer");
+    for (int64_t c = 0; c < e->C; ++c) nh_per_channel[c] = e->nh_host[c];
+    return SC_OK;
+}
+
+int sc_engine_process_blocks_channels(sc_engine *e, const void *x, int64_t n_total, int64_t nb,
+                                      const int64_t *swap_blocks, const void *const *swap_irs,
+                                      const int64_t *swap_ld, const int64_t *swap_nh, int64_t n_swaps, void *out) {
+    SC_REQUIRE(e, "null engine");
+    SC_REQUIRE(nb >= 1 && nb <= e->nb, "sc_engine_process_blocks_channels: nb must be in [1, block_size_nb]");
+    SC_REQUIRE(n_total >= 0 && (n_total == 0 || (x && out)), "sc_engine_process_blocks_channels: bad input");
+    SC_REQUIRE(n_swaps == 0 || (swap_blocks && swap_irs && swap_nh), "sc_engine_process_blocks_channels: bad swaps");
+    DeviceGuard g(e->device);
+    if (n_total == 0) return SC_OK;
+    return process_blocks_stepwise(e, x, n_total, n_total, nb, swap_blocks, swap_irs, swap_ld, swap_nh, e->C, n_swaps,
+                                   out, n_total);
 }
 
 int sc_engine_flush_begin(sc_engine *e, void *tail, int64_t tail_capacity) {
@@ -1417,12 +1644,12 @@ int sc_engine_flush_begin(sc_engine *e, void *tail, int64_t tail_capacity) {
             k_flush<double><<<g, 256, 0, e->stream>>>(static_cast<double *>(e->res[e->cur]),
                                                       static_cast<double *>(e->res[1 - e->cur]), e->res_ld,
                                                       static_cast<double *>(tail), tail_capacity, n_copy, e->st,
-                                                      e->nh, e->st_host);
+                                                      e->ragged ? 0 : e->nh, e->st_host);
         else
             k_flush<float><<<g, 256, 0, e->stream>>>(static_cast<float *>(e->res[e->cur]),
                                                      static_cast<float *>(e->res[1 - e->cur]), e->res_ld,
                                                      static_cast<float *>(tail), tail_capacity, n_copy, e->st,
-                                                     e->nh, e->st_host);
+                                                     e->ragged ? 0 : e->nh, e->st_host);
         SC_CHECK_LAUNCH();
     }
     e->flush_cap = tail_capacity;
@@ -1442,7 +1669,8 @@ int sc_engine_flush_end(sc_engine *e, int64_t *n_tail) {
     int64_t nt_max = 0;
     for (int64_t c = 0; c < e->C; ++c) {
         const int64_t live = e->st_host[c * ST_N + ST_LIVE];
-        n_tail[c] = (e->flush_nh - 1 > live) ? e->flush_nh - 1 : live;  // engine.py:155
+        const int64_t nhc = e->nh_host[c];
+        n_tail[c] = (nhc - 1 > live) ? nhc - 1 : live;  // engine.py:155
         nt_max = std::max(nt_max, n_tail[c]);
     }
     SC_REQUIRE(e->flush_cap >= nt_max, "sc_engine_flush: tail buffer too small (%lld < %lld)",
@@ -1465,7 +1693,8 @@ int sc_engine_flush(sc_engine *e, void *tail, int64_t tail_capacity, int64_t *n_
     int64_t nt_max = 0;
     for (int64_t c = 0; c < e->C; ++c) {
         const int64_t live = hs[c * ST_N + ST_LIVE];
-        n_tail[c] = (e->nh - 1 > live) ? e->nh - 1 : live;  // engine.py:155
+        const int64_t nhc = e->nh_host[c];
+        n_tail[c] = (nhc - 1 > live) ? nhc - 1 : live;  // engine.py:155
         nt_max = std::max(nt_max, n_tail[c]);
     }
     SC_REQUIRE(tail_capacity >= nt_max && (nt_max == 0 || tail), "sc_engine_flush: tail buffer too small (%lld < %lld)",
@@ -1476,7 +1705,7 @@ int sc_engine_flush(sc_engine *e, void *tail, int64_t tail_capacity, int64_t *n_
     // reset (engine.py:157-160): zero ring of len(ir), ri = live = consumed = 0
     SC_CHECK_CUDA(cudaMemsetAsync(e->res[0], 0, (size_t)e->res_ld * e->es * e->C, e->stream));
     SC_CHECK_CUDA(cudaMemsetAsync(e->res[1], 0, (size_t)e->res_ld * e->es * e->C, e->stream));
-    k_reset_state<<<cgrid(e->C), 128, 0, e->stream>>>(e->st, e->nh, e->C);
+    k_reset_state<<<cgrid(e->C), 128, 0, e->stream>>>(e->st, e->ragged ? 0 : e->nh, e->C);
     SC_CHECK_LAUNCH();
     e->cap_ub = e->nh;
     e->consumed = 0;

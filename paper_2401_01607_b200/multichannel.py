@@ -120,6 +120,20 @@ class MultiChannelEngine:
 
         t = _dev.torch()
         self.config = config if config is not None else EngineConfig()
+        ragged = None
+        if isinstance(h, (list, tuple)):
+            # one IR per channel, lengths may differ (one engine per channel)
+            if channels is not None and channels != len(h):
+                raise ValueError(f"{len(h)} impulse responses for channels={channels}")
+            ragged = list(h)
+            npd0 = (np.float32 if all(_dev.np_dtype(a) == np.float32 for a in ragged
+                                      if _dev.is_tensor(a) or np.asarray(a).dtype in (np.float32, np.float64))
+                    else np.float64)
+            if any(len(a) == 0 for a in ragged):
+                raise ValueError("impulse response is empty")
+            h = np.zeros((len(ragged), max(len(a) for a in ragged)), dtype=npd0)
+            for c, a in enumerate(ragged):
+                h[c, :len(a)] = a.cpu().numpy() if _dev.is_tensor(a) else np.asarray(a)
         hd = h if _dev.is_tensor(h) else np.asarray(h)
         npd = _dev.np_dtype(hd) if (_dev.is_tensor(hd) or hd.dtype in (np.float32, np.float64)) else np.float64
         if hd.ndim == 1:
@@ -134,7 +148,6 @@ class MultiChannelEngine:
         self._device = t.device(device) if device is not None else t.device("cuda", t.cuda.current_device())
         self._lib = N.lib()
         self._C = int(hd.shape[0])
-        self._pending = None
         h_dev = _dev.as_device(hd, npd, device=self._device).contiguous()
         self._handle = ctypes.c_void_p()
         with _dev.device_guard(self._device):
@@ -145,6 +158,10 @@ class MultiChannelEngine:
             if fast:
                 N.check(self._lib.sc_engine_set_mode(self._handle, N.SC_MODE_FAST))
         self.mode = "fast" if fast else "ordered"
+        if ragged is not None and len({len(a) for a in ragged}) > 1:
+            # channels start on IRs of their own lengths: a per-channel swap on
+            # the fresh state is exactly a fresh engine per channel
+            self.swap_ir(ragged)
 
     def __del__(self):
         h = getattr(self, "_handle", None)
@@ -191,20 +208,16 @@ class MultiChannelEngine:
         return [self._rows(d) for d in _dev.as_device_many(rows, self._npd, device=self._device)]
 
     def process_block(self, block):
-        """[C, n] in, [C, n] out (engine.py:118-146 per channel)."""
+        """[C, n] in, [C, n] out (engine.py:118-146 per channel).  A pending
+        swap (uniform or per channel) is applied first, inside the library."""
         t = _dev.torch()
-        if self._pending is not None:
-            h_new, self._pending = self._pending, None
-            self.swap_ir(h_new)
         with _dev.device_guard(self._device):
             xd = self._rows(block)
             n = xd.shape[1]
-            if n > self.config.block_size_nb:
-                raise ValueError(f"block of {n} samples exceeds block_size_nb={self.config.block_size_nb}")
             out = t.empty_like(xd)
-            if n:
-                self._bind()
-                N.check(self._lib.sc_engine_process_block(self._handle, N.ptr(xd), n, N.ptr(out)))
+            self._bind()   # an empty block still applies a pending swap (engine.py:124-126)
+            N.check(self._lib.sc_engine_process_block(self._handle, N.ptr(xd) if n else None, n,
+                                                      N.ptr(out) if n else None))
         return _dev.like_input(out, block)
 
     def process_sample(self, x):
@@ -217,17 +230,92 @@ class MultiChannelEngine:
             N.check(self._lib.sc_engine_process_sample(self._handle, N.ptr(xd), N.ptr(out)))
             return out[:, 0].cpu().numpy()
 
-    def swap_ir(self, h_new):
-        """Every channel swaps to its row of h_new (or a broadcast mono IR)."""
-        t = _dev.torch()
-        with _dev.device_guard(self._device):
-            hd = self._ir_rows(h_new)
-            self._bind()
-            N.check(self._lib.sc_engine_swap_ir(self._handle, N.ptr(hd), hd.shape[1]))
+    def _channel_irs(self, h_new, channels):
+        """(rows [C, L] on the device, per-channel lengths (0 = keep)) for a
+        per-channel swap.  h_new: a mono IR (1-D) for the selected channels,
+        [C, n] rows, or a list of C per-channel IRs (None = keep); channels:
+        indices or a boolean mask of the channels that swap (default: every
+        channel given an IR)."""
+        C = self._C
+        if isinstance(h_new, (list, tuple)):
+            if len(h_new) != C:
+                raise ValueError(f"expected {C} per-channel impulse responses, got {len(h_new)}")
+            per = [None if a is None else (a.cpu().numpy() if _dev.is_tensor(a) else np.asarray(a)) for a in h_new]
+        else:
+            hd = h_new.cpu().numpy() if _dev.is_tensor(h_new) else np.asarray(h_new)
+            if hd.ndim == 1:
+                per = [hd] * C
+            elif hd.ndim == 2 and hd.shape[0] == C:
+                per = list(hd)
+            else:
+                raise ValueError(f"expected a mono IR, [channels={C}, n] rows or {C} IRs, got shape {hd.shape}")
+        if channels is not None:
+            sel = np.zeros(C, dtype=bool)
+            ch = np.asarray(channels)
+            if ch.dtype == bool:
+                if ch.shape != (C,):
+                    raise ValueError(f"channel mask must have {C} entries")
+                sel = ch
+            else:
+                sel[ch.astype(np.int64)] = True
+            per = [a if sel[c] else None for c, a in enumerate(per)]
+        if any(a is not None and len(a) == 0 for a in per):
+            raise ValueError("impulse response is empty")
+        lengths = np.array([0 if a is None else len(a) for a in per], dtype=np.int64)
+        if not lengths.any():
+            raise ValueError("no channel swaps")
+        rows = np.zeros((C, int(lengths.max())), dtype=self._npd)
+        for c, a in enumerate(per):
+            if a is not None:
+                rows[c, :len(a)] = a
+        return _dev.as_device(rows, self._npd, device=self._device), lengths
 
-    def swap_ir_at_next_block(self, h_new):
-        self._ir_rows(h_new)  # validate now (engine.py:188-192)
-        self._pending = h_new
+    def _uniform(self, h_new, channels) -> bool:
+        if channels is not None or isinstance(h_new, (list, tuple)):
+            return False
+        return True
+
+    def swap_ir(self, h_new, channels=None):
+        """Swap impulse responses (engine.py:163-186, per channel).  Every
+        channel to its row of h_new (or a broadcast mono IR); with
+        ``channels`` (indices or mask) or a list of per-channel IRs (None =
+        keep), only those channels swap and lengths may differ -- the
+        semantics of one engine per channel."""
+        import ctypes
+
+        with _dev.device_guard(self._device):
+            self._bind()
+            if self._uniform(h_new, channels):
+                hd = self._ir_rows(h_new)
+                N.check(self._lib.sc_engine_swap_ir(self._handle, N.ptr(hd), hd.shape[1]))
+                return
+            rows, lengths = self._channel_irs(h_new, channels)
+            nh = (ctypes.c_int64 * self._C)(*lengths.tolist())
+            N.check(self._lib.sc_engine_swap_ir_channels(self._handle, N.ptr(rows), rows.shape[1], nh))
+
+    def swap_ir_at_next_block(self, h_new, channels=None):
+        """Deferred swap applied by the next process_block (engine.py:188-192),
+        for every channel or (``channels`` / per-channel list) some of them."""
+        import ctypes
+
+        with _dev.device_guard(self._device):
+            self._bind()
+            if self._uniform(h_new, channels):
+                hd = self._ir_rows(h_new)   # validated now
+                N.check(self._lib.sc_engine_swap_ir_at_next_block(self._handle, N.ptr(hd), hd.shape[1]))
+                return
+            rows, lengths = self._channel_irs(h_new, channels)
+            nh = (ctypes.c_int64 * self._C)(*lengths.tolist())
+            N.check(self._lib.sc_engine_swap_ir_at_next_block_channels(self._handle, N.ptr(rows), rows.shape[1], nh))
+
+    @property
+    def ir_lengths(self) -> list:
+        """Every channel's current impulse-response length."""
+        import ctypes
+
+        nh = (ctypes.c_int64 * self._C)()
+        N.check(self._lib.sc_engine_channel_nh(self._handle, nh))
+        return list(nh)
 
     def flush(self, *, on_device: bool = False):
         """Per-channel tails (max(len(ir)-1, live_c) samples each) as a list of
@@ -263,7 +351,7 @@ class MultiChannelEngine:
             N.check(self._lib.sc_engine_state(self._handle, ri, live, cap, ctypes.byref(cons), ctypes.byref(nh),
                                               ctypes.byref(pend)))
         return {"read_index": list(ri), "live": list(live), "cap": list(cap), "consumed": cons.value,
-                "nh": nh.value}
+                "nh": nh.value, "nh_per_channel": self.ir_lengths}
 
     def process_stream(self, x, nb=None, swaps=()):
         """[C, N] through back-to-back blocks of nb with an IR-swap schedule
@@ -280,14 +368,10 @@ class MultiChannelEngine:
         n_total = x.shape[-1]
         n_blocks = -(-n_total // nb)
         with _dev.device_guard(self._device):
-            if self._pending is not None and n_blocks:
-                # after any explicit block-0 swap, as process_block orders it;
-                # the library places it (csrc/engine.cu process_blocks_impl)
-                pd, self._pending = self._ir_rows(self._pending), None
-                self._bind()
-                N.check(self._lib.sc_engine_swap_ir_at_next_block(self._handle, N.ptr(pd), pd.shape[1]))
             # swaps outside [0, n_blocks) precede no block: the library ignores them
             swaps = sorted((s for s in swaps if 0 <= int(s[0]) < n_blocks), key=lambda s: s[0])
+            if any(len(s) > 2 or isinstance(s[1], (list, tuple)) for s in swaps):
+                return self._process_stream_channels(x, nb, swaps)
             irs = self._ir_rows_many([s[1] for s in swaps])
             k = len(swaps)
             blocks = (ctypes.c_int64 * max(k, 1))(*[int(s[0]) for s in swaps])
@@ -306,4 +390,29 @@ class MultiChannelEngine:
             out = t.empty_like(xd)
             N.check(self._lib.sc_engine_process_blocks(self._handle, N.ptr(xd), xd.shape[1], nb, blocks, ptrs,
                                                        nhs, k, N.ptr(out)))
+        return _dev.like_input(out, x)
+
+    def _process_stream_channels(self, x, nb, swaps):
+        """Per-channel swap schedule: entries (block, IR) swap every channel,
+        (block, IR, channels) or (block, [per-channel IRs]) only some; the
+        library runs the blocks one launch each (sc_engine_process_blocks_channels)."""
+        import ctypes
+
+        t = _dev.torch()
+        C = self._C
+        rows_list, flat = [], []
+        for s in swaps:
+            rows, lengths = self._channel_irs(s[1], s[2] if len(s) > 2 else None)
+            rows_list.append(rows)
+            flat.extend(lengths.tolist())
+        k = len(swaps)
+        blocks = (ctypes.c_int64 * max(k, 1))(*[int(s[0]) for s in swaps])
+        ptrs = (ctypes.c_void_p * max(k, 1))(*[r.data_ptr() for r in rows_list])
+        lds = (ctypes.c_int64 * max(k, 1))(*[r.shape[1] for r in rows_list])
+        nhs = (ctypes.c_int64 * max(k * C, 1))(*flat)
+        xd = self._rows(x)
+        out = t.empty_like(xd)
+        self._bind()
+        N.check(self._lib.sc_engine_process_blocks_channels(self._handle, N.ptr(xd), xd.shape[1], nb, blocks, ptrs,
+                                                            lds, nhs, k, N.ptr(out)))
         return _dev.like_input(out, x)

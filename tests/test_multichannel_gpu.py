@@ -121,3 +121,97 @@ def test_batched_pinned_host_pipeline(monkeypatch):
         ref = O.scatter_full(X[c], H[c])
         tol = 1e-5 * np.max(np.abs(X[c])) * np.sum(np.abs(H[c]))
         assert np.max(np.abs(y[c].numpy().astype(np.float64) - ref)) <= tol
+
+
+# ---------------------------------------------------------------- independent channels
+
+
+def _ir(rng, n):
+    return rng.standard_normal(n) * np.exp(-np.arange(n) / max(1.0, n / 4))
+
+
+@pytest.mark.parametrize("nb", [37, 300, 3000])
+def test_independent_channels_staggered_swaps_bit_exact(nb):
+    """One engine per channel (engine.py:60-66): every channel has its own IR
+    length from the start, swaps at its own blocks (some channels never),
+    takes per-channel deferred swaps, and drains its own live/tail -- float64
+    bit-exact against C independent oracle engines.  nb = 3000 exercises the
+    multi-launch path for blocks above the one-launch kernel's limit."""
+    rng = np.random.default_rng(50 + nb)
+    C = 5
+    n = 9000
+    lens0 = [33, 700, 1, 260, 1500]
+    h0 = [_ir(rng, L) for L in lens0]
+    x = _inputs(rng, C, n, np.float64)
+    eng = MultiChannelEngine(h0, EngineConfig(block_size_nb=nb, zero_skip_threshold=0.01))
+    assert eng.ir_lengths == lens0
+    refs = [O.OracleEngine(h0[c], nb, 0.01) for c in range(C)]
+    n_blocks = -(-n // nb)
+    plan = {}                                   # block -> [(kind, channel, ir)]
+    for c in range(C):
+        if c == 2:
+            continue                            # channel 2 never swaps
+        for b in sorted(rng.choice(np.arange(1, n_blocks), size=min(3, n_blocks - 1), replace=False)):
+            kind = "now" if (c + int(b)) % 2 else "next"
+            plan.setdefault(int(b), []).append((kind, c, _ir(rng, int(rng.integers(1, 2000)))))
+    got, want = [], [[] for _ in range(C)]
+    for b, s in enumerate(range(0, n, nb)):
+        for kind, c, h in plan.get(b, []):
+            per = [None] * C
+            per[c] = h
+            if kind == "now":
+                eng.swap_ir(per)
+                refs[c].swap_ir(h)
+            else:
+                eng.swap_ir_at_next_block(h, channels=[c])
+                refs[c].swap_ir_at_next_block(h)
+        got.append(np.asarray(eng.process_block(x[:, s:s + nb])))
+        for c in range(C):
+            want[c].append(refs[c].process_block(x[c, s:s + nb]))
+        if b == n_blocks // 2:
+            st = eng.state()
+            assert st["live"] == [r.live for r in refs]
+            assert st["read_index"] == [r.read_index for r in refs]
+            assert st["nh_per_channel"] == [len(r.ir) for r in refs]
+    tails = eng.flush()
+    body = np.concatenate(got, axis=1)
+    for c in range(C):
+        assert np.array_equal(body[c], np.concatenate(want[c])), c
+        wt = refs[c].flush()
+        assert len(tails[c]) == len(wt) and np.array_equal(tails[c], wt), c
+
+
+def test_independent_channels_stream_schedule():
+    """process_stream with a per-channel schedule ((block, IR, channels) and
+    (block, [per-channel IRs]) entries) equals the block-by-block calls of
+    independent oracle engines, bit for bit (float64)."""
+    import torch
+
+    rng = np.random.default_rng(61)
+    C, nb, n = 3, 64, 64 * 30 + 11
+    h0 = [_ir(rng, L) for L in (50, 120, 7)]
+    x = _inputs(rng, C, n, np.float64)
+    a, b2 = _ir(rng, 300), _ir(rng, 20)
+    swaps = [(3, a, [1]), (5, [b2, None, _ir(rng, 90)]), (5, _ir(rng, 40), [0]), (17, a, [0, 2]), (22, np.stack([a[:64]] * 3))]
+    eng = MultiChannelEngine(h0, EngineConfig(block_size_nb=nb))
+    body = eng.process_stream(torch.from_numpy(x).cuda(), nb, swaps).cpu().numpy()
+    tails = eng.flush()
+    for c in range(C):
+        ref = O.OracleEngine(h0[c], nb)
+        out = []
+        for blk, s in enumerate(range(0, n, nb)):
+            for sw in swaps:
+                if sw[0] != blk:
+                    continue
+                irs = sw[1]
+                if len(sw) > 2:
+                    if c in sw[2]:
+                        ref.swap_ir(irs)
+                elif isinstance(irs, list):
+                    if irs[c] is not None:
+                        ref.swap_ir(irs[c])
+                else:
+                    ref.swap_ir(irs[c])
+            out.append(ref.process_block(x[c, s:s + nb]))
+        assert np.array_equal(body[c], np.concatenate(out)), c
+        assert np.array_equal(tails[c], ref.flush()), c
