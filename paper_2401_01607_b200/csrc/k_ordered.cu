@@ -131,6 +131,8 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
     constexpr int XV = 16 / (int)sizeof(T);  // drive samples per vector load
     __shared__ __align__(16) T xs[2][CW_MC];
     __shared__ unsigned xmask[2][CW_MC / 32];
+    // per chunk and warp: every staged drive sample and tap finite
+    __shared__ unsigned xfin[2][CW_TB / 32];
     __shared__ __align__(16) T hs[2][HSP];
     if (a.run_if && *a.run_if == 0) return;  // block-uniform
     // channel-local base pointers (the param struct stays in the constant bank)
@@ -234,12 +236,23 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
             }
         };
         auto stash = [&](int buf) {
+            // Skipped samples are stored as zero: when every staged sample
+            // and tap of the chunk is finite, adding x*h for a zeroed sample
+            // or a zero (out-of-range) tap adds +-0, which leaves a chain
+            // value unchanged (chains start at +0 or a residue and are never
+            // -0), so the unpredicated path can run the whole chunk.
+            bool fin = true;
 #pragma unroll
             for (int k = 0; k < XPT; ++k) {
-                xs[buf][tid + k * CW_TB] = px[k];
+                xs[buf][tid + k * CW_TB] = pbit[k] ? px[k] : T(0);
+                fin = fin && (!pbit[k] || isfinite((double)px[k]));
                 const unsigned bits = __ballot_sync(0xffffffffu, pbit[k]);
                 if ((tid & 31) == 0) xmask[buf][(tid + k * CW_TB) >> 5] = bits;
             }
+#pragma unroll
+            for (int j = 0; j < HPT; ++j) fin = fin && isfinite((double)ph[j]);
+            const bool wfin = __all_sync(0xffffffffu, fin);
+            if ((tid & 31) == 0) xfin[buf][tid >> 5] = wfin ? 1u : 0u;
 #pragma unroll
             for (int j = 0; j < HPT; ++j) {
                 const int i = tid + j * CW_TB;
@@ -265,9 +278,12 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
             const T *hsb = hs[buf];
             const bool full = (cmc >= tile_last - nh + 1) && (cmc + mcount - 1 <= tile0);
             bool dense = mcount == CW_MC;
+            bool finite = true;
+#pragma unroll
+            for (int w = 0; w < CW_TB / 32; ++w) finite = finite && xfin[buf][w] != 0;
 #pragma unroll
             for (int q = 0; q < CW_MC / 32; ++q) dense = dense && xmask[buf][q] == ~0u;
-            if (full && dense) {
+            if ((full && dense) || finite) {
                 // interior: every (output, sample) pair valid, nothing skipped
                 T w[W];
                 {
