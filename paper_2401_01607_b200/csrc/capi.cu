@@ -194,7 +194,7 @@ void *scratch(size_t bytes, int slot, cudaStream_t stream, int *err) {
 
 int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
                    const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin,
-                   int64_t n_end, int64_t channels, cudaStream_t stream) {
+                   int64_t n_end, int64_t channels, cudaStream_t stream, const TcPre *pre) {
     bool tc = false, guard = false;
     if (mode == SC_MODE_TC) {
         tc = guard = true;
@@ -214,7 +214,7 @@ int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_
                                    channels, stream);
     const unsigned *nonfinite = nullptr;
     int rc = launch_fir_f32_tc(x, ldx, x_base, x_lo, x_hi, h, ldh, nh, y, ldy, n_begin, n_end, channels,
-                               stream, &nonfinite);
+                               stream, &nonfinite, pre);
     if (rc || !guard || !nonfinite) return rc;
     // NaN/Inf inputs, and magnitudes whose power-of-two scales leave float
     // range (k_tc_fir.cu channel_scales), are routed (on the device, no host sync) to

@@ -401,20 +401,47 @@ struct SegMap {
     int64_t m_lo[kMaxSegs], dst[kMaxSegs];
 };
 
+// Extras of the mask pass for the batched tensor-core FIR: per (channel,
+// segment) max |masked x| into amax[2*(c*nseg + j)] (the TC kernel's power-
+// of-two scales; float bits, atomicMax), a flag for Inf samples (NaN is
+// skipped by the engine rule, so masked samples are otherwise finite), the
+// residue length (cap) of every channel snapshotted before the state replay
+// -- which runs concurrently on a side stream -- rewrites it, and the zero
+// padding of the shorter segments (grid.x CTAs past the blocks).
+struct MaskExtras {
+    unsigned *amax;    // nullptr: no amax (per-segment FIR path)
+    unsigned *flag;
+    int64_t *cap_snap;
+    const int64_t *st;
+    int nseg;
+    int64_t L;         // padded segment length (batched layout)
+    int64_t len[kMaxSegs];
+};
+
 __global__ void k_mask_skip(const float *__restrict__ x, int64_t ldx, int64_t n_total, int64_t nb, float keep,
                             float *__restrict__ xm, int64_t ldm, int64_t n_blocks, int64_t *__restrict__ J,
-                            bool vec4, SegMap sm) {
+                            bool vec4, SegMap sm, MaskExtras mx) {
     const int64_t b = blockIdx.x;
+    if (b >= n_blocks) {
+        // zero [len_j, L) of segment j's padded row
+        const int j = (int)(b - n_blocks);
+        float *row = xm + blockIdx.y * ldm + (int64_t)j * mx.L;
+        for (int64_t i = mx.len[j] + threadIdx.x; i < mx.L; i += blockDim.x) row[i] = 0.0f;
+        return;
+    }
+    if (b == 0 && threadIdx.x == 0 && mx.cap_snap) mx.cap_snap[blockIdx.y] = mx.st[blockIdx.y * ST_N + ST_CAP];
     const float *xc = x + blockIdx.y * ldx + b * nb;
     int64_t dst = b * nb;
+    int seg = 0;
     if (sm.n > 0) {
-        int j = 0;
-        while (j + 1 < sm.n && sm.m_lo[j + 1] <= b * nb) ++j;
-        dst = sm.dst[j] + (b * nb - sm.m_lo[j]);
+        while (seg + 1 < sm.n && sm.m_lo[seg + 1] <= b * nb) ++seg;
+        dst = sm.dst[seg] + (b * nb - sm.m_lo[seg]);
     }
     float *mc = xm + blockIdx.y * ldm + dst;
     const int64_t n = n_total - b * nb < nb ? n_total - b * nb : nb;
     long long j = -1;
+    float amx = 0.0f;
+    bool inf = false;
     int64_t i0 = 0;
     if (vec4) {
         const int64_t n4 = n >> 2;
@@ -424,6 +451,8 @@ __global__ void k_mask_skip(const float *__restrict__ x, int64_t ldx, int64_t n_
                        k3 = fabsf(v.w) >= keep;
             v.x = k0 ? v.x : 0.0f, v.y = k1 ? v.y : 0.0f, v.z = k2 ? v.z : 0.0f, v.w = k3 ? v.w : 0.0f;
             reinterpret_cast<float4 *>(mc)[q] = v;
+            amx = fmaxf(amx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+            inf |= isinf(v.x) || isinf(v.y) || isinf(v.z) || isinf(v.w);
             const long long base = 4 * q;
             if (k3) j = base + 3;
             else if (k2) j = base + 2;
@@ -435,38 +464,39 @@ __global__ void k_mask_skip(const float *__restrict__ x, int64_t ldx, int64_t n_
     for (int64_t i = i0 + threadIdx.x; i < n; i += blockDim.x) {
         const float v = xc[i];
         const bool keepv = fabsf(v) >= keep;
-        mc[i] = keepv ? v : 0.0f;
+        const float w = keepv ? v : 0.0f;
+        mc[i] = w;
+        amx = fmaxf(amx, fabsf(w));
+        inf |= isinf(w);
         if (keepv) j = i;
     }
     for (int o = 16; o > 0; o >>= 1) {
         const long long v = __shfl_xor_sync(0xffffffffu, j, o);
         j = v > j ? v : j;
+        amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
     }
     __shared__ long long sj[32];
-    if ((threadIdx.x & 31) == 0) sj[threadIdx.x >> 5] = j;
+    __shared__ float sa[32];
+    if ((threadIdx.x & 31) == 0) sj[threadIdx.x >> 5] = j, sa[threadIdx.x >> 5] = amx;
+    if (mx.amax && __syncthreads_or(inf) && threadIdx.x == 0) atomicOr(mx.flag, 1u);
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) j = sj[w] > j ? sj[w] : j;
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) j = sj[w] > j ? sj[w] : j, amx = fmaxf(amx, sa[w]);
         J[blockIdx.y * n_blocks + b] = j;
+        // IEEE order of non-negative floats == order of their bit patterns
+        if (mx.amax) atomicMax(mx.amax + 2 * (blockIdx.y * mx.nseg + seg), __float_as_uint(amx));
     }
 }
 
-// zero [len_j, L) of every padded segment j of the masked copy (grid nseg x C)
-__global__ void k_zero_tails(float *__restrict__ xm, int64_t ldm, int64_t L, FastSegs sg) {
-    const int j = blockIdx.x;
-    const int64_t len = sg.m_hi[j] - sg.m_lo[j];
-    float *row = xm + blockIdx.y * ldm + (int64_t)j * L;
-    for (int64_t i = len + threadIdx.x; i < L; i += blockDim.x) row[i] = 0.0f;
-}
 
 // 4 consecutive slots per thread; segments that miss the 4 slots are skipped
 // with one test.
 __global__ void k_fast_combine(FastSegs sg, const float *__restrict__ fy, int64_t fy_ld,
-                               const float *__restrict__ rin, int64_t res_ld, const int64_t *__restrict__ st,
+                               const float *__restrict__ rin, int64_t res_ld, const int64_t *__restrict__ cap_snap,
                                int64_t n_total, int64_t n_slots, float *__restrict__ out, int64_t ldo,
                                float *__restrict__ rout) {
     const int64_t c = blockIdx.y;
-    const int64_t cap = st[c * ST_N + ST_CAP];
+    const int64_t cap = cap_snap[c];
     const float *yc = fy + c * fy_ld;
     for (int64_t t4 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; t4 < n_slots;
          t4 += (int64_t)gridDim.x * blockDim.x * 4) {
@@ -510,6 +540,27 @@ __global__ void k_stage_irs(StageCopies c, T *__restrict__ stage, int64_t dld) {
     T *dst = stage + ch * dld + c.off[j];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.nh[j]; i += (int64_t)gridDim.x * blockDim.x)
         dst[i] = src[i];
+}
+
+// k_stage_irs for the batched FIR's taps, also taking max |h| per (channel,
+// segment) into amax[2*(ch*nseg + j) + 1] and flagging non-finite taps
+__global__ void k_stage_irs_amax(StageCopies c, float *__restrict__ stage, int64_t dld, unsigned *amax,
+                                 unsigned *flag) {
+    const int j = blockIdx.y;
+    const int64_t ch = blockIdx.z;
+    const float *src = static_cast<const float *>(c.src[j]) + ch * c.sld[j];
+    float *dst = stage + ch * dld + c.off[j];
+    float amx = 0.0f;
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.nh[j]; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = src[i];
+        dst[i] = v;
+        amx = fmaxf(amx, fabsf(v));
+        bad |= !isfinite(v);
+    }
+    for (int o = 16; o > 0; o >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(amax + 2 * (ch * c.n + j) + 1, __float_as_uint(amx));
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
 // Replays engine.py's bookkeeping over all blocks of the call: each swap
@@ -697,6 +748,12 @@ struct sc_engine {
     int64_t *st_host = nullptr;
     struct GraphCache *gc = nullptr;  // CUDA graphs of repeated process_blocks calls
     cudaStream_t cap_stream = nullptr;  // private stream the graphs are captured on
+    // FAST fused streams: side stream for the state replay (overlaps the FIR)
+    // and the per-call scratch of the mask pass (amax / flag / cap snapshot)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    void *tcpre = nullptr;
+    int64_t tcpre_cap = 0;
     bool flush_open = false;
     int64_t flush_cap = 0, flush_nh = 0;
     // Channels with IRs of their own (per-channel swaps, engine.py:60-66's one
@@ -950,9 +1007,13 @@ bool fast_stream_worth(const sc_engine *e, const ChainSeg *segs, int nseg) {
     return each;
 }
 
-// Also fills e->jbuf (last scattering index per block) from its mask pass.
+// Also fills e->jbuf (last scattering index per block) from its mask pass and
+// replays the engine state (k_stream_state) on a side stream that overlaps
+// the FIR: the combine reads each channel's residue length from the mask
+// pass's snapshot, so the replay may rewrite the state meanwhile.
 int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64_t nb, int64_t ub,
-                const ChainSeg *segs, int nseg, int64_t hld, void *rin, void *rout, void *out, int64_t ldo) {
+                const ChainSeg *segs, const int64_t *seg_ld, int nseg, void *rin, void *rout, void *out, int64_t ldo,
+                const StreamEvents &sev) {
     const int64_t n_blocks = cdiv(n_total, nb);
     int64_t L, NH;
     const bool batched = uniform_segs(segs, nseg, &L, &NH) && e->C * nseg < 65536;
@@ -973,27 +1034,53 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
     if (rc) return rc;
     rc = ensure_2d(&e->fy, &e->fy_cap, e->C * ypitch, 4, 1, 0, e->stream);
     if (rc) return rc;
+    // [amax 2*C*nseg u32 | flag u32 | pad] [cap snapshot C x i64]
+    const int64_t amax_bytes = ((8 * e->C * nseg + 4 + 15) / 16) * 16;
+    rc = ensure_2d(&e->tcpre, &e->tcpre_cap, amax_bytes + 8 * e->C, 1, 1, 0, e->stream);
+    if (rc) return rc;
+    if (!e->side) {
+        SC_CHECK_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+        SC_CHECK_CUDA(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+        SC_CHECK_CUDA(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
+    }
+    unsigned *amax = static_cast<unsigned *>(e->tcpre);
+    unsigned *flag = amax + 2 * e->C * nseg;
+    int64_t *cap_snap = reinterpret_cast<int64_t *>(static_cast<char *>(e->tcpre) + amax_bytes);
     float *xm = static_cast<float *>(e->fx), *fy = static_cast<float *>(e->fy);
     {
-        const dim3 g((unsigned)n_blocks, (unsigned)e->C);
+        if (batched) SC_CHECK_CUDA(cudaMemsetAsync(amax, 0, 8 * e->C * nseg + 4, e->stream));
         // smallest float strictly above thr (thr >= 0): |x| > thr <=> |x| >= keep
         float keep = (float)e->thr;
         if ((double)keep <= e->thr) keep = nextafterf(keep, INFINITY);
         SegMap sm{};
+        MaskExtras mx{};
+        mx.cap_snap = cap_snap;
+        mx.st = e->st;
+        mx.nseg = nseg;
+        int tails = 0;
         if (batched) {
             sm.n = nseg;
             for (int j = 0; j < nseg; ++j) sm.m_lo[j] = segs[j].m_lo, sm.dst[j] = j * L;
+            mx.amax = amax;
+            mx.flag = flag;
+            mx.L = L;
+            for (int j = 0; j < nseg; ++j) mx.len[j] = segs[j].m_hi - segs[j].m_lo;
+            if (xpitch > n_total) tails = nseg;  // zero padding of the shorter segments
         }
         const bool vec4 = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(xm)) & 15) == 0 &&
                           ldx % 4 == 0 && xpitch % 4 == 0 && nb % 4 == 0 && (!batched || L % 4 == 0);
+        const dim3 g((unsigned)(n_blocks + tails), (unsigned)e->C);
         k_mask_skip<<<g, 256, 0, e->stream>>>(static_cast<const float *>(x), ldx, n_total, nb, keep, xm, xpitch,
-                                              n_blocks, e->jbuf, vec4, sm);
+                                              n_blocks, e->jbuf, vec4, sm, mx);
         SC_CHECK_LAUNCH();
-        if (batched && xpitch > n_total) {  // zero padding of the shorter segments
-            k_zero_tails<<<dim3((unsigned)nseg, (unsigned)e->C), 256, 0, e->stream>>>(xm, xpitch, L, sg);
-            SC_CHECK_LAUNCH();
-        }
     }
+    // the state replay needs only J (and the state): fork it off
+    SC_CHECK_CUDA(cudaEventRecord(e->ev_fork, e->stream));
+    SC_CHECK_CUDA(cudaStreamWaitEvent(e->side, e->ev_fork, 0));
+    k_stream_state<<<(unsigned)e->C, SS_TB, 0, e->side>>>(e->jbuf, n_blocks, nb, n_total, e->nh, sev, e->st, nullptr,
+                                                          ldx, e->thr, e->dtype);
+    SC_CHECK_LAUNCH();
+    SC_CHECK_CUDA(cudaEventRecord(e->ev_join, e->side));
     // NaN/Inf in x or h: launch_fir_f32's device-gated ordered fallback
     if (batched) {
         rc = ensure_2d(&e->fh, &e->fh_cap, e->C * nseg * NH, 4, 1, 0, e->stream);
@@ -1001,37 +1088,33 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
         StageCopies cp{};
         cp.n = nseg;
         for (int j = 0; j < nseg; ++j)
-            cp.src[j] = segs[j].h, cp.sld[j] = hld, cp.off[j] = j * NH, cp.nh[j] = NH;
+            cp.src[j] = segs[j].h, cp.sld[j] = seg_ld[j], cp.off[j] = j * NH, cp.nh[j] = NH;
         const dim3 gs((unsigned)std::min<int64_t>(cdiv(NH, 256), 64), (unsigned)nseg, (unsigned)e->C);
-        k_stage_irs<float><<<gs, 256, 0, e->stream>>>(cp, static_cast<float *>(e->fh), nseg * NH);
+        k_stage_irs_amax<<<gs, 256, 0, e->stream>>>(cp, static_cast<float *>(e->fh), nseg * NH, amax, flag);
         SC_CHECK_LAUNCH();
+        const TcPre pre{amax, flag};
         rc = launch_fir_f32(SC_MODE_FAST, xm, L, 0, 0, L, static_cast<const float *>(e->fh), NH, NH, fy, Lo, 0, Lo,
-                            e->C * nseg, e->stream);
+                            e->C * nseg, e->stream, &pre);
         if (rc) return rc;
     } else {
         for (int j = 0; j < nseg; ++j) {
             // outputs [m_lo, m_hi + nh - 1) of segment j's drive samples
             rc = launch_fir_f32(SC_MODE_FAST, xm, xpitch, 0, segs[j].m_lo, segs[j].m_hi,
-                                static_cast<const float *>(segs[j].h), hld, segs[j].nh, fy + sg.off[j],
+                                static_cast<const float *>(segs[j].h), seg_ld[j], segs[j].nh, fy + sg.off[j],
                                 ypitch, segs[j].m_lo, segs[j].m_hi + segs[j].nh - 1, e->C, e->stream);
             if (rc) return rc;
         }
     }
     const int64_t n_slots = n_total + ub;
     const dim3 g((unsigned)std::min<int64_t>(cdiv(n_slots, 1024), 4096), (unsigned)e->C);
-    k_fast_combine<<<g, 256, 0, e->stream>>>(sg, fy, ypitch, static_cast<const float *>(rin), e->res_ld, e->st,
+    k_fast_combine<<<g, 256, 0, e->stream>>>(sg, fy, ypitch, static_cast<const float *>(rin), e->res_ld, cap_snap,
                                              n_total, n_slots, static_cast<float *>(out), ldo,
                                              static_cast<float *>(rout));
     SC_CHECK_LAUNCH();
+    SC_CHECK_CUDA(cudaStreamWaitEvent(e->stream, e->ev_join, 0));
     return SC_OK;
 }
 
-// Block-by-block execution of a stream: for engines whose channels hold IRs
-// of their own (or a per-channel swap schedule).  Swaps scheduled before
-// block b run in schedule order, then the block (a pending swap at block 0,
-// after the explicit ones, as process_block orders it).  nh_stride 0: swap i
-// gives every channel length swap_nh[i]; nh_stride C: channel c's length is
-// swap_nh[i*C + c] (<= 0 keeps that channel's IR).
 int process_blocks_stepwise(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64_t nb,
                             const int64_t *swap_blocks, const void *const *swap_irs, const int64_t *swap_ld,
                             const int64_t *swap_nh, int64_t nh_stride, int64_t n_swaps, void *out, int64_t ldo) {
@@ -1130,62 +1213,76 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
         }
         return SC_OK;
     }
-    // Stage every IR of the timeline in engine-owned memory (the kernels run
-    // after this call returns; callers may free their buffers): [C][stage_ld].
-    // (A call without IR changes reads the engine's own copy directly.)
-    const bool staged = !ev.empty();
-    int64_t tot = e->nh;
-    for (const Ev &v : ev) tot += v.nh;
-    int rc = staged ? ensure_2d(&e->stage, &e->stage_ld, tot, e->es, e->C, 0, e->stream) : SC_OK;
-    if (rc) return rc;
-    rc = ensure_2d(reinterpret_cast<void **>(&e->jbuf), &e->jbuf_ld, n_blocks * e->C, 8, 1, 0, e->stream);
-    if (rc) return rc;
-    char *stage = staged ? static_cast<char *>(e->stage) : static_cast<char *>(e->ir);
-    const int64_t hld = staged ? e->stage_ld : e->ir_ld;  // row pitch of every segment's taps
-    StageCopies cp{};
+    // The IR timeline as segments of drive samples, each with its taps' source
+    // (the engine's copy, the pending buffer or the caller's IR; row pitch
+    // seg_ld).  The FAST path reads the sources directly (stream-ordered, like
+    // any kernel given the caller's buffers); the ordered chain wants one row
+    // pitch for all segments, so it stages them in engine memory [C][stage_ld].
     int64_t max_nh = e->nh;
-    cp.src[0] = e->ir, cp.sld[0] = e->ir_ld, cp.off[0] = 0, cp.nh[0] = e->nh, cp.n = 1;
     ChainSeg segs[kMaxSegs];
+    int64_t seg_ld[kMaxSegs];
     int nseg = 0;
-    segs[nseg++] = ChainSeg{stage, e->nh, 0, n_total};
-    int64_t off = e->nh, ub = e->cap_ub;
+    segs[nseg] = ChainSeg{e->ir, e->nh, 0, n_total};
+    seg_ld[nseg++] = e->ir_ld;
+    int64_t ub = e->cap_ub;
     StreamEvents sev{};
     sev.n = 0;
     for (const Ev &v : ev) {
-        char *dst = stage + (size_t)off * e->es;
-        cp.src[cp.n] = v.h, cp.sld[cp.n] = v.ld, cp.off[cp.n] = off, cp.nh[cp.n] = v.nh, ++cp.n;
         max_nh = v.nh > max_nh ? v.nh : max_nh;
         const int64_t m = v.block * nb;
         if (segs[nseg - 1].m_lo == m) {
-            segs[nseg - 1].h = dst;  // a later swap before the same block wins
+            segs[nseg - 1].h = v.h;  // a later swap before the same block wins
             segs[nseg - 1].nh = v.nh;
+            seg_ld[nseg - 1] = v.ld;
         } else {
             segs[nseg - 1].m_hi = m;
-            segs[nseg++] = ChainSeg{dst, v.nh, m, n_total};
+            segs[nseg] = ChainSeg{v.h, v.nh, m, n_total};
+            seg_ld[nseg++] = v.ld;
         }
         sev.block[sev.n] = v.block;
         sev.nh[sev.n] = v.nh;
         ++sev.n;
-        off += v.nh;
         ub = v.nh > ub ? v.nh : ub;
     }
-    if (staged) {
+    int rc = ensure_2d(reinterpret_cast<void **>(&e->jbuf), &e->jbuf_ld, n_blocks * e->C, 8, 1, 0, e->stream);
+    if (rc) return rc;
+    rc = grow_residue(e, ub);
+    if (rc) return rc;
+    const bool fast = fast_stream_worth(e, segs, nseg);
+    int64_t hld = e->ir_ld;  // ordered path: the common row pitch of the segments' taps
+    if (!fast && !(nseg == 1 && segs[0].h == e->ir)) {
+        int64_t tot = 0;
+        for (int j = 0; j < nseg; ++j) tot += segs[j].nh;
+        rc = ensure_2d(&e->stage, &e->stage_ld, tot, e->es, e->C, 0, e->stream);
+        if (rc) return rc;
+        StageCopies cp{};
+        int64_t off = 0;
+        for (int j = 0; j < nseg; ++j) {
+            cp.src[j] = segs[j].h, cp.sld[j] = seg_ld[j], cp.off[j] = off, cp.nh[j] = segs[j].nh;
+            segs[j].h = static_cast<char *>(e->stage) + (size_t)off * e->es;
+            off += segs[j].nh;
+        }
+        cp.n = nseg;
         const dim3 gs((unsigned)std::min<int64_t>(cdiv(max_nh, 256), 64), (unsigned)cp.n, (unsigned)e->C);
         if (e->dtype == SC_F64)
             k_stage_irs<double><<<gs, 256, 0, e->stream>>>(cp, static_cast<double *>(e->stage), e->stage_ld);
         else
             k_stage_irs<float><<<gs, 256, 0, e->stream>>>(cp, static_cast<float *>(e->stage), e->stage_ld);
         SC_CHECK_LAUNCH();
+        hld = e->stage_ld;
     }
-    rc = grow_residue(e, ub);
-    if (rc) return rc;
+    // the IR in force after the call (becomes the engine's copy)
+    const void *last_src = fast ? ev.empty() ? e->ir : ev.back().h : segs[nseg - 1].h;
+    const int64_t last_ld = fast ? ev.empty() ? e->ir_ld : ev.back().ld : hld;
+    const int64_t last_nh = segs[nseg - 1].nh;
     // One ordered launch for every block: slot t accumulates its drive samples
     // in ascending order across blocks and IR segments -- the same chain as
     // block-by-block processing (bit-identical), continued from the residue.
     void *rin = e->res[e->cur], *rout = e->res[1 - e->cur];
     bool j_from_x = false;
-    if (fast_stream_worth(e, segs, nseg)) {
-        rc = fast_stream(e, x, ldx, n_total, nb, ub, segs, nseg, hld, rin, rout, out, ldo);
+    if (fast) {
+        // (the FAST path also replays the state, on a side stream)
+        rc = fast_stream(e, x, ldx, n_total, nb, ub, segs, seg_ld, nseg, rin, rout, out, ldo, sev);
         if (rc) return rc;
     } else {
         ChainBatch batch{e->C, ldx, hld, ldo, e->res_ld, e->res_ld, ST_N};
@@ -1205,17 +1302,18 @@ int process_blocks_impl(sc_engine *e, const void *x, int64_t ldx, int64_t n_tota
         SC_CHECK_LAUNCH();
         }
     }
+    if (!fast) {
     k_stream_state<<<(unsigned)e->C, SS_TB, 0, e->stream>>>(e->jbuf, n_blocks, nb, n_total, e->nh, sev, e->st,
                                                             j_from_x ? x : nullptr, ldx, e->thr, e->dtype);
     SC_CHECK_LAUNCH();
+    }
     // host-side bookkeeping: the last IR becomes current (engine-owned copy)
-    const ChainSeg &last = segs[nseg - 1];
-    if (staged && last.h != stage) {
-        rc = ensure_2d(&e->ir, &e->ir_ld, last.nh, e->es, e->C, 0, e->stream);
+    if (last_src != e->ir) {
+        rc = ensure_2d(&e->ir, &e->ir_ld, last_nh, e->es, e->C, 0, e->stream);
         if (rc) return rc;
-        rc = copy_rows(e, e->ir, e->ir_ld, last.h, e->stage_ld, last.nh);
+        rc = copy_rows(e, e->ir, e->ir_ld, last_src, last_ld, last_nh);
         if (rc) return rc;
-        e->nh = last.nh;
+        e->nh = last_nh;
     }
     e->cap_ub = ub;
     for (int64_t c = 0; c < e->C; ++c) e->nh_host[c] = e->nh;
@@ -1284,7 +1382,8 @@ std::vector<int64_t> graph_key(const sc_engine *e, const void *x, int64_t ldx, i
                        P(e->ir), e->nh, e->ir_ld, (int64_t)e->has_pending, e->has_pending ? P(e->pend) : 0,
                        e->has_pending ? e->pend_nh : 0, e->has_pending ? e->pend_ld : 0, P(e->res[0]), P(e->res[1]),
                        (int64_t)e->cur, e->res_ld, e->cap_ub, P(e->st), P(e->stage), e->stage_ld, P(e->jbuf),
-                       e->jbuf_ld, P(e->fx), P(e->fy), P(e->fh), e->fx_cap, e->fy_cap, e->fh_cap});
+                       e->jbuf_ld, P(e->fx), P(e->fy), P(e->fh), e->fx_cap, e->fy_cap, e->fh_cap, P(e->tcpre),
+                       e->tcpre_cap, P(e->side)});
     int64_t thr_bits;
     std::memcpy(&thr_bits, &e->thr, sizeof thr_bits);
     k.push_back(thr_bits);
@@ -1495,6 +1594,10 @@ int sc_engine_destroy(sc_engine *e) {
     delete[] e->pend_nh_c;
     delete e->gc;
     if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+    if (e->side) cudaStreamDestroy(e->side);
+    if (e->ev_fork) cudaEventDestroy(e->ev_fork);
+    if (e->ev_join) cudaEventDestroy(e->ev_join);
+    cudaFree(e->tcpre);
     cudaFree(e->stage);
     cudaFree(e->jbuf);
     cudaFree(e->fx);

@@ -576,7 +576,8 @@ bool tc_fir_supported(int64_t nh) { return nh >= 2 * TR; }
 
 int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
                       const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin,
-                      int64_t n_end, int64_t channels, cudaStream_t stream, const unsigned **nonfinite_out) {
+                      int64_t n_end, int64_t channels, cudaStream_t stream, const unsigned **nonfinite_out,
+                      const TcPre *pre) {
     if (nonfinite_out) *nonfinite_out = nullptr;
     const int64_t n_len = n_end - n_begin;
     if (n_len <= 0 || channels <= 0) return SC_OK;
@@ -602,10 +603,17 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     const int64_t s8_wide = cdiv(s_needed, ssh_wide) * ssh_wide;
     const int64_t wide_units = cdiv(n_len, (int64_t)TR * 256) * channels * std::max<int64_t>(1, s8_wide / wp_wide);
     const int TNV = tnv_env == 128 ? 128 : tnv_env == 256 ? 256 : (wide_units >= sm_count() ? 256 : 128);
-    const int SSH = TNV == 256 ? ssh_wide : (s_needed <= 2 ? 2 : 8);  // drain period: see TcStage
+    // 128-row tiles (small launches, e.g. cfg2's 19 segments) drain every 8
+    // shifts; SC_TC_SSH128=4 drains every 4 (less shift padding, but measured
+    // slower on cfg2: 0.102 vs 0.095 ms)
+    static const int ssh128 = [] {
+        const char *v = getenv("SC_TC_SSH128");
+        return v && atoi(v) == 4 ? 4 : 8;
+    }();
+    const int SSH = TNV == 256 ? ssh_wide : (s_needed <= 2 ? 2 : ssh128);  // drain period: see TcStage
     const int64_t s8 = cdiv(s_needed, SSH) * SSH;
     const int64_t TN = TNV, TTILE = (int64_t)TR * TNV;
-    const int WP = TNV == 128 ? (SSH == 2 ? TcStage<2, 128>::WP : TcStage<8, 128>::WP)
+    const int WP = TNV == 128 ? (SSH == 2 ? TcStage<2, 128>::WP : SSH == 4 ? TcStage<4, 128>::WP : TcStage<8, 128>::WP)
                               : (SSH == 2 ? TcStage<2, 256>::WP : SSH == 4 ? TcStage<4, 256>::WP : TcStage<8, 256>::WP);
     const int64_t tiles_per_ch = cdiv(n_len, TTILE);
     const int64_t row_min = -((s8 + WP + 7) / 8) * 8;
@@ -620,8 +628,9 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     int err = 0;
     char *ws = static_cast<char *>(scratch(bytes, 3, stream, &err));
     if (err) return err;
-    unsigned *amax = reinterpret_cast<unsigned *>(ws);
-    unsigned *flag = reinterpret_cast<unsigned *>(ws + 8 * channels);
+    unsigned *amax_own = reinterpret_cast<unsigned *>(ws);
+    const unsigned *amax = pre ? pre->amax : amax_own;
+    unsigned *flag = pre ? pre->flag : reinterpret_cast<unsigned *>(ws + 8 * channels);
     float *scales = reinterpret_cast<float *>(ws + 8 * channels + 16);
     if (nonfinite_out) *nonfinite_out = flag;
     __half *xt_hi = reinterpret_cast<__half *>(ws + head);
@@ -629,7 +638,8 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     __half *h8_hi = xt_lo + xt_ch * channels;
     __half *h8_lo = h8_hi + h8_ch * channels;
 
-    SC_CHECK_CUDA(cudaMemsetAsync(amax, 0, 8 * channels + 4, stream));
+    if (!pre) {  // the caller's pass already took the maxima and the flag
+    SC_CHECK_CUDA(cudaMemsetAsync(amax_own, 0, 8 * channels + 4, stream));
     {
         // ~8 resident CTAs per SM across all channels for x, float4 per thread
         const int64_t xn = x_hi - x_lo;
@@ -637,8 +647,9 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
         const int gx = xn > 0 ? (int)std::min<int64_t>(cdiv(xn, 1024), per_ch) : 0;
         const int gh = (int)std::min<int64_t>(cdiv(nh, 1024), std::max<int64_t>(1, per_ch / 4));
         dim3 g((unsigned)(gx + gh), (unsigned)channels);
-        k_amax2<<<g, 256, 0, stream>>>(x + (x_lo - x_base), ldx, xn, gx, h, ldh, nh, amax, flag);
+        k_amax2<<<g, 256, 0, stream>>>(x + (x_lo - x_base), ldx, xn, gx, h, ldh, nh, amax_own, flag);
         SC_CHECK_LAUNCH();
+    }
     }
     {
         const int gsplit = (int)cdiv(nrows, 32);
@@ -654,6 +665,7 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir<S, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                        TcStage<S, N>::SM_TOTAL))
     if (TNV == 128 && SSH == 2) SC_TC_ATTR(2, 128);
+    else if (TNV == 128 && SSH == 4) SC_TC_ATTR(4, 128);
     else if (TNV == 128) SC_TC_ATTR(8, 128);
     else if (SSH == 2) SC_TC_ATTR(2, 256);
     else if (SSH == 4) SC_TC_ATTR(4, 256);
@@ -717,6 +729,7 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     const int grid = (int)std::min<int64_t>(a.n_units, sms);
 #define SC_TC_LAUNCH(S, N) k_tc_fir<S, N><<<grid, TcGeo<N>::THREADS, TcStage<S, N>::SM_TOTAL, stream>>>(a)
     if (TNV == 128 && SSH == 2) SC_TC_LAUNCH(2, 128);
+    else if (TNV == 128 && SSH == 4) SC_TC_LAUNCH(4, 128);
     else if (TNV == 128) SC_TC_LAUNCH(8, 128);
     else if (SSH == 2) SC_TC_LAUNCH(2, 256);
     else if (SSH == 4) SC_TC_LAUNCH(4, 256);

@@ -151,6 +151,15 @@ int launch_fir_f32_fast(const float *x, int64_t ldx, int64_t x_base, int64_t x_l
                         int64_t n_begin, int64_t n_end, int64_t channels, cudaStream_t stream,
                         const unsigned *run_if = nullptr);
 
+// Per-channel max |x| / max |h| (float bit patterns at amax[2c], amax[2c+1])
+// and the non-finite flag of a tensor-core FIR launch, computed by the caller
+// in a pass it makes anyway (the engine's mask pass): the launch then skips
+// its own max pass.
+struct TcPre {
+    const unsigned *amax;
+    unsigned *flag;
+};
+
 // Tensor-core (tcgen05, FP16 hi/lo split, 3 MMAs) FP32-accurate FIR (k_tc_fir.cu).
 // *nonfinite_out receives a device flag that is nonzero when an input sample
 // is NaN/Inf; the tensor-core kernel then writes nothing and the caller's
@@ -159,12 +168,12 @@ bool tc_fir_supported(int64_t nh);
 int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
                       const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin,
                       int64_t n_end, int64_t channels, cudaStream_t stream,
-                      const unsigned **nonfinite_out);
+                      const unsigned **nonfinite_out, const TcPre *pre = nullptr);
 
 // FAST-mode dispatch: tensor cores for long filters, FFMA2 kernel otherwise.
 int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
                    const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin,
-                   int64_t n_end, int64_t channels, cudaStream_t stream);
+                   int64_t n_end, int64_t channels, cudaStream_t stream, const TcPre *pre = nullptr);
 
 int launch_direct_form(const double *e, int64_t ne, const double *h, int64_t nh, double *y,
                        unsigned *status, cudaStream_t stream);
