@@ -286,15 +286,18 @@ class Work:
         capi.cu's FAST dispatch).  The tensor-core work it issues is read from
         the library itself (sc_tc_stats) around the timed region."""
         if self.cfg.startswith("short"):
-            # FAST dispatch (capi.cu / k_fast_f32.cu): tensor cores from 80
-            # taps at this size, the streaming k_fir_short up to 8 taps and
-            # the tap-stationary k_fir_tapreg up to 32 (HBM-bound), the smem
-            # k_fir_short_smem in between (FMA-bound)
+            # FAST dispatch (capi.cu / k_fast_f32.cu): tensor cores from 48
+            # taps at this size (the fused-split k_tc_fir_fs), the streaming
+            # k_fir_short up to 8 taps and the tap-stationary k_fir_tapreg up
+            # to 32 (HBM-bound), the smem k_fir_short_smem in between
+            # (FMA-bound).  Filters of at most two 128-tap shifts on tensor
+            # cores are HBM-bound too: 2 shifts of MMAs take less than moving
+            # 8 B per output
             nh = self.w.nh
-            use_tc = self.mode == "tc" or (self.mode in ("fast", "auto") and nh >= 80)
+            use_tc = self.mode == "tc" or (self.mode in ("fast", "auto") and nh >= 48)
             self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 8 else "k_fir_tapreg" if nh <= 32
                                                      else "k_fir_short_smem")
-            self.hbm_bound = nh <= 32 and not use_tc
+            self.hbm_bound = (nh <= 32 and not use_tc) or (use_tc and nh <= 255)
             return
         if self.cfg == "cfg2":
             # float32 engine: FAST mode convolves the 19 equal IR segments in one
@@ -674,6 +677,12 @@ def main():
         roofline = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                     "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                     "alg_bytes_per_launch": alg_bytes, "kernel": work.kernel}
+        if work.kernel == "k_tc_fir" and tc["launches"]:
+            tc_peak = float(p.get("bf16_tflops", 1590.0))
+            tflops = 2 * 3 * tc["padded_macs"] / args.steps / (ms_local * 1e-3) / 1e12
+            roofline["kernel"] = f"k_tc_fir_fs<{tc['ssh']},{tc['tile_n']}> (fused split: x read as FP32)"
+            roofline["tensor"] = {"achieved_tflops": tflops, "frac": tflops / tc_peak,
+                                  "note": "the tensor roof is not the binding one at <= 2 shifts"}
     elif work.kernel == "k_tc_fir" and tc["launches"]:
         # tensor work actually issued, as the library counts it (sc_tc_stats):
         # 3 fp16 MMAs (hi*hi, lo*hi, hi*lo) over the padded block-Toeplitz

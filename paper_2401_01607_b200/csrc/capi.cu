@@ -199,11 +199,13 @@ int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_
     if (mode == SC_MODE_TC) {
         tc = guard = true;
     } else if (mode == SC_MODE_FAST) {
-        // tensor cores from 256 taps; from 80 taps too when the launch is big
-        // enough to amortise their set-up (short128 on 2^26 outputs: 0.30 ms
-        // on tensor cores vs 0.51 ms on the CUDA-core short-filter kernel)
+        // tensor cores from 256 taps; from 48 taps too when the launch is big
+        // enough to amortise their set-up: with the fused-split kernel
+        // (k_tc_fir_fs, no split image in HBM) 2^26 outputs take 0.19 ms at
+        // 64 or 128 taps, against 0.25 ms (64) on the CUDA-core short-filter
+        // kernel, whose time grows with the taps (crossover ~50)
         const double macs = (double)(n_end - n_begin) * (double)nh * (double)channels;
-        tc = g_fast_uses_tc && (tc_fir_supported(nh) || (nh >= 80 && macs >= 1073741824.0));
+        tc = g_fast_uses_tc && (tc_fir_supported(nh) || (nh >= 48 && macs >= 1073741824.0));
         guard = tc;
     } else if (mode != SC_MODE_FFMA) {
         set_error("fir: bad mode %d", mode);

@@ -570,6 +570,478 @@ __global__ void __launch_bounds__(256) k_tc_prep(const float *__restrict__ x, in
         build_h8_part(h, ldh, nh, s8, ngroups, sc.y, h8_hi, h8_lo, h8_ch, (int64_t)blockIdx.x - gsplit);
 }
 
+// ---------------------------------------------------------------- fused split
+// Short and medium filters (at most FsGeo::WPF shifts): the tensor-core FIR
+// reads x as FP32 straight from the signal -- no split image in HBM.  Every
+// work unit (tile, shift range) needs one window of TN + shifts - 1 rows;
+// four converter warps load it (coalesced float4), take its max |x|, pick
+// the unit's own power-of-two scale, split it into the fp16 hi/lo K-group-
+// major layout the UMMA descriptors read, and hand it to the MMA warp.  Two
+// window slots: the next unit's conversion overlaps this unit's MMAs.  The
+// epilogue unscales by 2^-(ex_unit + eh_channel).  HBM traffic: 4 B per input
+// sample (plus the halo rows) and 4 B per output, against 16 B + 4 B for the
+// image path (max pass, image write, image read).
+// ONE: every unit is one drain stage (filters of at most SSH shifts, no
+// shift splits) -- the epilogue streams each accumulator straight out (no
+// per-thread sum over stages), which frees the registers for 8 converter
+// warps instead of 4.
+template <int SSH, bool ONE = false>
+struct FsGeo {
+    static constexpr int TN = 128;                                  // output rows per tile (UMMA N)
+    static constexpr int NEPI = 4, NCONV = ONE ? 8 : 4;
+    static constexpr int THREADS = 64 + 32 * (NEPI + NCONV);
+    static constexpr int SGROUPS = 2 * KG - 1 + KG * (SSH - 1);
+    static constexpr uint32_t HST_PART = SGROUPS * 128;
+    static constexpr int WROWS_FIT = (int)((SMEM_MAX - 256 - NHSLOT * 2 * HST_PART) / (2 * 2 * KG * 16));
+    static constexpr int WPF = ((WROWS_FIT - 1 - TN) / 8) * 8;      // most shifts per unit
+    // rows per window slot; WROWS = 1 (mod 8) puts the K-group stride at 16
+    // (mod 128) bytes, so the converters' 16-byte accesses -- consecutive
+    // threads on consecutive K-groups of one row -- are bank-conflict free
+    static constexpr int WROWS = TN + WPF + 1;
+    static constexpr uint32_t XPART = WROWS * KG * 16;              // one slot, one part (hi or lo)
+    static constexpr uint32_t SM_HST = 4 * XPART;                   // slot s, part p at (2s + p) * XPART
+    static constexpr uint32_t SM_BAR = SM_HST + NHSLOT * 2 * HST_PART;
+    static constexpr uint32_t SM_TOTAL = SM_BAR + 256;
+    static constexpr uint32_t IDESC = TcGeo<TN>::IDESC;
+    static_assert(WPF >= SSH && WPF % SSH == 0, "window");
+    static_assert(SM_TOTAL <= SMEM_MAX, "smem");
+};
+
+struct FsArgs {
+    const float *x;
+    int64_t ldx, x_base, x_lo, x_hi;  // channel c's sample m at x[c*ldx + m - x_base], zero outside [x_lo, x_hi)
+    const __half *h8[2];
+    int64_t h8_ch;
+    const int *eh;                    // per channel: h scale exponent
+    int64_t s8, tiles_per_ch, n_tiles, n_begin, n_end, nsplit, sps, n_units, channels;
+    float *y;
+    int64_t ldy;
+    float *ws;
+    unsigned *flag;
+};
+
+template <int NT>
+__device__ __forceinline__ void conv_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NT) : "memory"); }
+
+template <int SSH, bool ONE>
+__global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArgs a) {
+    using G = FsGeo<SSH, ONE>;
+    // converter groups of 4 warps; with two groups each takes every other
+    // unit (its own window slot), so two windows' loads are in flight
+    constexpr int TN = G::TN, WROWS = G::WROWS, NEPI = G::NEPI, NCONV = 4, NGRP = G::NCONV / 4, NCT = 128;
+    constexpr uint32_t XPART = G::XPART, SM_HST = G::SM_HST, HST_PART = G::HST_PART, SM_BAR = G::SM_BAR;
+    constexpr int64_t TTILE = (int64_t)TR * TN;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    if (*a.flag) return;  // non-finite taps (found by the H8 build): the gated fallback computes the launch
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t bar_xfull = sbase + SM_BAR + 0;    // + 8*slot
+    const uint32_t bar_xempty = sbase + SM_BAR + 16;  // + 8*slot
+    const uint32_t bar_hfull = sbase + SM_BAR + 32;   // + 8*slot
+    const uint32_t bar_hempty = sbase + SM_BAR + 48;  // + 8*slot
+    const uint32_t bar_tfull = sbase + SM_BAR + 64;   // + 8*acc
+    const uint32_t bar_tempty = sbase + SM_BAR + 80;  // + 8*acc
+    const uint32_t bar_exfull = sbase + SM_BAR + 96;  // + 8*k, k = unit % 4
+    int *ex_ring = reinterpret_cast<int *>(smem + SM_BAR + 128);   // [4]
+    float *cmax = reinterpret_cast<float *>(smem + SM_BAR + 144);  // [NCONV <= 8]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + SM_BAR + 176);
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(bar_xfull + 8 * i, 1);
+            mbar_init(bar_xempty + 8 * i, 1);
+            mbar_init(bar_hfull + 8 * i, 1);
+            mbar_init(bar_hempty + 8 * i, 1);
+            mbar_init(bar_tfull + 8 * i, 1);
+            mbar_init(bar_tempty + 8 * i, NEPI);
+        }
+        for (int k = 0; k < 4; ++k) mbar_init(bar_exfull + 8 * k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"((uint32_t)(2 * TN)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    auto unit_of = [&](int64_t u, int64_t &tile, int64_t &sb, int64_t &se, int64_t &ch, int64_t &i0) {
+        tile = u / a.nsplit;
+        sb = (u - tile * a.nsplit) * a.sps;
+        se = sb + a.sps < a.s8 ? sb + a.sps : a.s8;
+        ch = tile / a.tiles_per_ch;
+        i0 = (tile - ch * a.tiles_per_ch) * TN;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------------------ producer: H8 stages
+            uint32_t hsc = 0;
+            for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+                int64_t tile, sb, se, ch, i0;
+                unit_of(u, tile, sb, se, ch, i0);
+                const __half *h80 = a.h8[0] + ch * a.h8_ch, *h81 = a.h8[1] + ch * a.h8_ch;
+                for (int64_t sg = sb; sg < se; sg += SSH) {
+                    const uint32_t slot = hsc % NHSLOT;
+                    if (hsc >= NHSLOT) mbar_wait(bar_hempty + 8 * slot, ((hsc / NHSLOT) - 1) & 1);
+                    mbar_expect_tx(bar_hfull + 8 * slot, 2 * HST_PART);
+                    const int64_t glo = (a.s8 - 1 - (sg + SSH - 1)) * KG;
+                    for (int p = 0; p < 2; ++p)
+                        bulk_g2s(sbase + SM_HST + (slot * 2 + p) * HST_PART, (p ? h81 : h80) + glo * 64, HST_PART,
+                                 bar_hfull + 8 * slot);
+                    ++hsc;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ------------------------------------------------------------ MMA issuer
+            uint32_t uc = 0, hsc = 0, dc = 0;
+            for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++uc) {
+                int64_t tile, sb, se, ch, i0;
+                unit_of(u, tile, sb, se, ch, i0);
+                const uint32_t xs = uc & 1;
+                mbar_wait(bar_xfull + 8 * xs, (uc >> 1) & 1);
+                for (int64_t sg = sb; sg < se; sg += SSH) {
+                    const uint32_t slot = hsc % NHSLOT;
+                    mbar_wait(bar_hfull + 8 * slot, (hsc / NHSLOT) & 1);
+                    ++hsc;
+                    const uint32_t acc = dc & 1;
+                    if (dc >= 2) mbar_wait(bar_tempty + 8 * acc, ((dc >> 1) - 1) & 1);
+                    tc_fence_after();
+                    const uint32_t d_tmem = tmem + acc * TN;
+                    uint32_t accumulate = 0;
+#pragma unroll 1
+                    for (int ss = 0; ss < SSH; ++ss) {
+                        const int64_t s = sg + ss;
+                        const uint32_t a_hi = sbase + SM_HST + (slot * 2 + 0) * HST_PART + (SSH - 1 - ss) * KG * 128;
+                        const uint32_t a_lo = a_hi + HST_PART;
+                        // output row i of shift s reads window row i + (se - 1 - s)
+                        const uint32_t b_hi = sbase + (2 * xs) * XPART + (uint32_t)(se - 1 - s) * 16;
+                        const uint32_t b_lo = b_hi + XPART;
+#pragma unroll
+                        for (int kk = 0; kk < KG / 2; ++kk) {
+                            const uint64_t ah = sdesc(a_hi + kk * 256, 128, 128);
+                            const uint64_t al = sdesc(a_lo + kk * 256, 128, 128);
+                            const uint64_t bh = sdesc(b_hi + kk * 2 * (WROWS * 16), WROWS * 16, 128);
+                            const uint64_t bl = sdesc(b_lo + kk * 2 * (WROWS * 16), WROWS * 16, 128);
+                            umma_f16(d_tmem, ah, bh, G::IDESC, accumulate);
+                            accumulate = 1;
+                            umma_f16(d_tmem, al, bh, G::IDESC, 1);
+                            umma_f16(d_tmem, ah, bl, G::IDESC, 1);
+                        }
+                    }
+                    umma_commit(bar_hempty + 8 * slot);
+                    umma_commit(bar_tfull + 8 * acc);
+                    ++dc;
+                }
+                umma_commit(bar_xempty + 8 * xs);
+            }
+        }
+    } else if (warp < 2 + NEPI) {
+        // ---------------------------------------------------------------- epilogue
+        const int q = warp & 3;          // TMEM lane quarter
+        const int rp = q * 32 + lane;    // phase r' = 127 - r
+        uint32_t dc = 0, uc = 0;
+        for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++uc) {
+            int64_t tile, sb, se, ch, i0;
+            unit_of(u, tile, sb, se, ch, i0);
+            const int64_t sp = u - tile * a.nsplit;
+            const int64_t n_stages = (se - sb) / SSH;
+            float *yc = a.nsplit == 1 ? a.y + ch * a.ldy : a.ws + (sp * a.channels + ch) * (a.n_end - a.n_begin);
+            const int64_t nb = a.n_begin + i0 * TR + (TR - 1 - rp);
+            if constexpr (ONE) {
+                // one stage: the unit's x scale first, then stream the accumulator out
+                mbar_wait(bar_exfull + 8 * (uc & 3), (uc >> 2) & 1);
+                const int e = ex_ring[uc & 3] + a.eh[ch];
+                const float inv = __int_as_float((127 - e) << 23);
+                const uint32_t acc = dc & 1;
+                mbar_wait(bar_tfull + 8 * acc, (dc >> 1) & 1);
+                tc_fence_after();
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * TN;
+#pragma unroll
+                for (int c = 0; c < TN; c += 32) {
+                    float v[32];
+                    tmem_ld32(taddr + c, v);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int64_t n = nb + (int64_t)(c + i) * TR;
+                        if (n < a.n_end) yc[n - a.n_begin] = v[i] * inv;
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
+                ++dc;
+                continue;
+            }
+            float sum[TN];
+#pragma unroll
+            for (int i = 0; i < TN; ++i) sum[i] = 0.0f;
+#pragma unroll 1
+            for (int64_t st = 0; st < n_stages; ++st, ++dc) {
+                const uint32_t acc = dc & 1;
+                mbar_wait(bar_tfull + 8 * acc, (dc >> 1) & 1);
+                tc_fence_after();
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * TN;
+#pragma unroll
+                for (int c = 0; c < TN; c += 32) {
+                    float v[32];
+                    tmem_ld32(taddr + c, v);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) sum[c + i] += v[i];
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
+            }
+            // the unit's x scale (written by the converters before this arrive)
+            mbar_wait(bar_exfull + 8 * (uc & 3), (uc >> 2) & 1);
+            const int e = ex_ring[uc & 3] + a.eh[ch];
+            const float inv = __int_as_float((127 - e) << 23);  // 2^-e, |e| <= 126 (checked)
+#pragma unroll
+            for (int i = 0; i < TN; ++i) {
+                const int64_t n = nb + (int64_t)i * TR;
+                if (n < a.n_end) yc[n - a.n_begin] = sum[i] * inv;
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- converters
+        // Work item = (window row w, K-group j): 8 consecutive samples.  The
+        // raw FP32 samples land IN PLACE in the item's two 16-byte slots (hi
+        // part, lo part) by cp.async -- every load of the window in flight at
+        // once, no registers held -- then each thread takes the max over its
+        // own items and, once the unit's scale is known, overwrites them with
+        // the fp16 hi / lo split.
+        const int cg = (threadIdx.x - 32 * (2 + NEPI)) / NCT;  // converter group
+        const int ct = (threadIdx.x - 32 * (2 + NEPI)) % NCT;  // 0..127 within the group
+        const int cw = ct >> 5;
+        float *gmax = cmax + 4 * cg;
+        uint32_t uc = 0;
+        for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++uc) {
+            if ((int)(uc % NGRP) != cg) continue;
+            int64_t tile, sb, se, ch, i0;
+            unit_of(u, tile, sb, se, ch, i0);
+            const uint32_t xs = uc & 1;
+            if (uc >= 2) mbar_wait(bar_xempty + 8 * xs, ((uc >> 1) - 1) & 1);
+            // window row w <-> global row i0 - (se - 1) + w; samples m0 + 128 w + v
+            const int nrows = TN + (int)(se - sb) - 1;
+            const int items = nrows * KG;
+            const int64_t m0 = a.n_begin + (i0 - (se - 1)) * TR;
+            const float *xc = a.x + ch * a.ldx - a.x_base;
+            const int64_t lo = a.x_lo, hi = a.x_hi;
+            // interior window: every sample inside [lo, hi) and 16-byte aligned
+            const bool interior = m0 >= lo && m0 + (int64_t)nrows * TR <= hi &&
+                                  ((reinterpret_cast<uintptr_t>(xc + m0) & 15) == 0);
+            uint8_t *xhi = smem + (2 * xs) * XPART, *xlo = xhi + XPART;
+            if (interior) {
+                // unrolled: every copy's addresses in their own registers, so
+                // the copies issue back to back (no waits on reused sources)
+                const uint32_t shi = smem_u32(xhi), slo = smem_u32(xlo);
+                for (int it0 = ct; it0 < items; it0 += 8 * NCT) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int it = it0 + k * NCT;
+                        if (it < items) {
+                            const float *src = xc + m0 + (int64_t)(it >> 4) * TR + (it & 15) * 8;
+                            const uint32_t off = ((uint32_t)(it & 15) * WROWS + (uint32_t)(it >> 4)) * 16;
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(shi + off), "l"(src));
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(slo + off), "l"(src + 4));
+                        }
+                    }
+                }
+            } else for (int it = ct; it < items; it += NCT) {
+                const int64_t m = m0 + (int64_t)(it >> 4) * TR + (it & 15) * 8;
+                const uint32_t off = ((uint32_t)(it & 15) * WROWS + (uint32_t)(it >> 4)) * 16;
+                {
+                    float v[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) v[e] = (m + e >= lo && m + e < hi) ? xc[m + e] : 0.0f;
+                    *reinterpret_cast<float4 *>(xhi + off) = make_float4(v[0], v[1], v[2], v[3]);
+                    *reinterpret_cast<float4 *>(xlo + off) = make_float4(v[4], v[5], v[6], v[7]);
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            // max |x| over this thread's own items (it wrote them itself)
+            float mx = 0.0f;
+            bool bad = false;
+            for (int it = ct; it < items; it += NCT) {
+                const uint32_t off = ((uint32_t)(it & 15) * WROWS + (uint32_t)(it >> 4)) * 16;
+                const float4 p0 = *reinterpret_cast<const float4 *>(xhi + off);
+                const float4 p1 = *reinterpret_cast<const float4 *>(xlo + off);
+                mx = fmaxf(mx, fmaxf(fmaxf(fabsf(p0.x), fabsf(p0.y)), fmaxf(fabsf(p0.z), fabsf(p0.w))));
+                mx = fmaxf(mx, fmaxf(fmaxf(fabsf(p1.x), fabsf(p1.y)), fmaxf(fabsf(p1.z), fabsf(p1.w))));
+                bad |= !(isfinite(p0.x) && isfinite(p0.y) && isfinite(p0.z) && isfinite(p0.w) && isfinite(p1.x) &&
+                         isfinite(p1.y) && isfinite(p1.z) && isfinite(p1.w));
+            }
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 1u);
+            if (lane == 0) gmax[cw] = mx;
+            conv_bar<NCT>(1 + cg);
+#pragma unroll
+            for (int w = 0; w < NCONV; ++w) mx = fmaxf(mx, gmax[w]);
+            // the unit's exact power-of-two scale: max |x| into [2^14, 2^15);
+            // scales (or the unscale with the taps' exponent) leaving float
+            // range raise the fallback flag (the gated ordered launch)
+            int ex = (mx > 0.0f && isfinite(mx)) ? 14 - ilogbf(mx) : 0;
+            const int e_tot = ex + a.eh[ch];
+            if (ex > 114 || e_tot > 126 || e_tot < -126) {
+                if (ct == 0) atomicOr(a.flag, 1u);
+                ex = 0;
+            }
+            const float sc = __int_as_float((127 + ex) << 23);  // 2^ex
+            for (int it = ct; it < items; it += NCT) {
+                const uint32_t off = ((uint32_t)(it & 15) * WROWS + (uint32_t)(it >> 4)) * 16;
+                const float4 p0 = *reinterpret_cast<const float4 *>(xhi + off);
+                const float4 p1 = *reinterpret_cast<const float4 *>(xlo + off);
+                const float v[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+                __align__(16) __half hv[8], lv[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) split16(v[e] * sc, hv[e], lv[e]);
+                *reinterpret_cast<uint4 *>(xhi + off) = *reinterpret_cast<const uint4 *>(hv);
+                *reinterpret_cast<uint4 *>(xlo + off) = *reinterpret_cast<const uint4 *>(lv);
+            }
+            // generic-proxy stores -> visible to the tensor core's async proxy
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            conv_bar<NCT>(1 + cg);
+            if (ct == 0) {
+                ex_ring[uc & 3] = ex;
+                mbar_arrive(bar_exfull + 8 * (uc & 3));
+                mbar_arrive(bar_xfull + 8 * xs);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(2 * TN)));
+    }
+}
+
+// H8 images for the fused-split kernel with each channel's own h scale:
+// every CTA takes max |h_c| over the whole (short) IR itself, so no separate
+// max pass runs; CTA (0, c) publishes the exponent, non-finite taps raise
+// the fallback flag.
+__global__ void __launch_bounds__(256) k_h8_fs(const float *__restrict__ h, int64_t ldh, int64_t nh, int64_t s8,
+                                               int64_t ngroups, __half *__restrict__ h8_hi,
+                                               __half *__restrict__ h8_lo, int64_t h8_ch, int *eh, unsigned *flag) {
+    const int c = blockIdx.y;
+    const float *hc = h + (int64_t)c * ldh;
+    float mx = 0.0f;
+    bool bad = false;
+    for (int64_t i = threadIdx.x; i < nh; i += blockDim.x) {
+        const float v = hc[i];
+        mx = fmaxf(mx, fabsf(v));
+        bad |= !isfinite(v);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __shared__ float wm[8];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mx;
+    bad = __syncthreads_or(bad);
+    mx = wm[0];
+    for (int w = 1; w < 8; ++w) mx = fmaxf(mx, wm[w]);
+    int e = (mx > 0.0f && isfinite(mx)) ? 14 - ilogbf(mx) : 0;
+    if (e > 114) {  // taps this small leave the split's range: ordered fallback
+        if (threadIdx.x == 0) atomicOr(flag, 1u);
+        e = 0;
+    }
+    if (bad && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flag, 1u);
+    if (blockIdx.x == 0 && threadIdx.x == 0) eh[c] = e;
+    build_h8_part(h, ldh, nh, s8, ngroups, __int_as_float((127 + e) << 23), h8_hi, h8_lo, h8_ch, blockIdx.x);
+}
+
+}  // namespace
+
+// Fused-split launch (see k_tc_fir_fs); returns SC_ERR_STATE when the filter
+// has more shifts than one window holds (the image path then runs).
+int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi, const float *h,
+                         int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin, int64_t n_end,
+                         int64_t channels, cudaStream_t stream, const unsigned **nonfinite_out, const TcPre *pre) {
+    constexpr int SSH = 2;
+    using G = FsGeo<SSH>;
+    const int64_t n_len = n_end - n_begin;
+    const int64_t s_needed = (nh + TR - 2) / TR + 1;
+    const int64_t s8 = cdiv(s_needed, SSH) * SSH;
+    // Short filters on launches with several tiles per SM (the converters of
+    // the next tile then overlap this one's MMAs): measured 0.21 vs 0.28 ms
+    // (128 taps, 2^26 outputs).  Longer filters and small launches keep the
+    // image path (cfg2: 0.094 vs 0.108 ms).
+    if (s8 > 8 || cdiv(n_len, (int64_t)TR * G::TN) * channels < 2 * (int64_t)sm_count()) return SC_ERR_STATE;
+    const int64_t ngroups = KG * s8 + KG - 1;
+    const int64_t h8_ch = ngroups * 64;
+    const int64_t tiles_per_ch = cdiv(n_len, (int64_t)TR * G::TN);
+    const int64_t n_tiles = tiles_per_ch * channels;
+    // scratch: [flag u32 | eh i32 x C] [h8 hi | h8 lo]
+    const size_t head = (size_t)cdiv(4 * channels + 64, 256) * 256;
+    int err = 0;
+    char *ws = static_cast<char *>(scratch(head + 2 * (size_t)h8_ch * channels * 2 + 1024, 3, stream, &err));
+    if (err) return err;
+    unsigned *flag = pre ? pre->flag : reinterpret_cast<unsigned *>(ws);
+    int *eh = reinterpret_cast<int *>(ws + 16);
+    __half *h8_hi = reinterpret_cast<__half *>(ws + head);
+    __half *h8_lo = h8_hi + h8_ch * channels;
+    if (nonfinite_out) *nonfinite_out = flag;
+    if (!pre) SC_CHECK_CUDA(cudaMemsetAsync(flag, 0, 4, stream));
+    {
+        dim3 g((unsigned)cdiv(ngroups * 8, 256), (unsigned)channels);
+        k_h8_fs<<<g, 256, 0, stream>>>(h, ldh, nh, s8, ngroups, h8_hi, h8_lo, h8_ch, eh, flag);
+        SC_CHECK_LAUNCH();
+    }
+    FsArgs a;
+    a.x = x, a.ldx = ldx, a.x_base = x_base, a.x_lo = x_lo, a.x_hi = x_hi;
+    a.h8[0] = h8_hi, a.h8[1] = h8_lo, a.h8_ch = h8_ch, a.eh = eh;
+    a.s8 = s8, a.tiles_per_ch = tiles_per_ch, a.n_tiles = n_tiles, a.n_begin = n_begin, a.n_end = n_end;
+    a.channels = channels, a.y = y, a.ldy = ldy, a.flag = flag;
+    // shift-range splits when the tiles leave SMs idle (fixed-order reduce)
+    const int sms = sm_count();
+    const int64_t stages = s8 / SSH;
+    int64_t nsplit = 1;
+    {
+        double best = 0.0;
+        for (int64_t sp = 1; sp <= 16 && sp <= stages; ++sp) {
+            const int64_t units = n_tiles * sp;
+            const int64_t waves = (units + sms - 1) / sms;
+            const double eff = (double)units / (double)(waves * sms);
+            if (eff > best + 0.03) best = eff, nsplit = sp;
+            if (best > 0.95) break;
+        }
+    }
+    const int64_t sps = cdiv(stages, nsplit) * SSH;
+    nsplit = cdiv(s8, sps);
+    a.nsplit = nsplit, a.sps = sps, a.n_units = n_tiles * nsplit;
+    a.ws = nullptr;
+    if (nsplit > 1) {
+        a.ws = static_cast<float *>(scratch(sizeof(float) * (size_t)n_len * channels * nsplit, 4, stream, &err));
+        if (err) return err;
+    }
+    const int grid = (int)std::min<int64_t>(a.n_units, sms);
+    if (nsplit == 1 && s8 == SSH) {
+        using G1 = FsGeo<SSH, true>;
+        SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir_fs<SSH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           G1::SM_TOTAL));
+        k_tc_fir_fs<SSH, true><<<grid, G1::THREADS, G1::SM_TOTAL, stream>>>(a);
+    } else {
+        SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir_fs<SSH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           G::SM_TOTAL));
+        k_tc_fir_fs<SSH, false><<<grid, G::THREADS, G::SM_TOTAL, stream>>>(a);
+    }
+    SC_CHECK_LAUNCH();
+    note_tc_launch(SSH, G::TN, n_tiles * (int64_t)TR * G::TN * (int64_t)TR * s8);
+    if (nsplit > 1) {
+        dim3 g((unsigned)cdiv(n_len, 256), (unsigned)channels);
+        k_tc_split_reduce<<<g, 256, 0, stream>>>(a.ws, (int)nsplit, (int)channels, n_len, y, ldy, flag);
+        SC_CHECK_LAUNCH();
+    }
+    return SC_OK;
+}
+
+namespace {
 }  // namespace
 
 bool tc_fir_supported(int64_t nh) { return nh >= 2 * TR; }
@@ -583,6 +1055,17 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     if (n_len <= 0 || channels <= 0) return SC_OK;
     SC_REQUIRE(nh >= 1, "tc fir: empty impulse response");
     SC_REQUIRE(channels < 65536, "tc fir: too many channels");
+    // Filters whose shifts fit one converter window skip the split image
+    // (k_tc_fir_fs); SC_TC_FUSED=0 forces the image path.
+    static const bool fused = [] {
+        const char *v = getenv("SC_TC_FUSED");
+        return !(v && atoi(v) == 0);
+    }();
+    if (fused) {
+        const int rc = launch_fir_f32_tc_fs(x, ldx, x_base, x_lo, x_hi, h, ldh, nh, y, ldy, n_begin, n_end, channels,
+                                            stream, nonfinite_out, pre);
+        if (rc != SC_ERR_STATE) return rc;
+    }
     const int64_t s_needed = (nh + TR - 2) / TR + 1;
     static const int wide_ssh = [] {
         const char *v = getenv("SC_TC_WIDE_SSH");  // experiment knob: 2, 4 or 8
