@@ -9,9 +9,13 @@ arithmetic runs in the CUDA library (csrc/), never on the host:
   kernel: each output is a single chain over input index ascending with
   separately rounded multiply and add -- bit-identical to the reference.
 * float32 signals (arrays or tensors; ``Signal`` keeps float32 instead of
-  upcasting) use the FAST register-tiled FFMA2 kernel, within
-  1e-5*max|x|*||h||_1 of the reference; ``mode="ordered"`` selects the
-  ordered chain in float32.
+  upcasting) use the FAST path, within 1e-5*max|x|*||h||_1 of the
+  reference: the tcgen05 tensor-core FIR (fp16 hi/lo split, 3 MMAs) for
+  filters of >= 256 taps (>= 48 on large launches), the CUDA-core
+  short-filter kernels below that; ``mode="ffma"`` forces the FFMA2
+  register-tiled kernel, ``mode="tc"`` the tensor cores, and
+  ``mode="ordered"`` the ordered chain in float32.
+* ``direct_form`` is exactly rounded like the reference's math.fsum.
 
 Samples may be numpy arrays (results come back as arrays) or torch tensors
 (CUDA tensors stay on the device; no host synchronisation).

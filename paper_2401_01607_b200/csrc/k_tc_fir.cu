@@ -18,7 +18,7 @@
 //    dense 128x128 Toeplitz block.  Consecutive shifts slide by 16 groups.
 //  * X (B operand) is stored K-group-major ([j][row][8]) so rows are 16 B
 //    apart: moving to the next shift (one row down) is just start address
-//    - 16 B.  One 192-row window serves 64 consecutive shifts.
+//    - 16 B.  One window of N + WP rows serves WP consecutive shifts.
 //
 // FP32 accuracy from FP16 tensor cores: x = x_hi + x_lo, h = h_hi + h_lo
 // (each fp16, after exact power-of-two scaling of x and h into fp16 range),
@@ -26,14 +26,19 @@
 // are exact in the FP32 accumulator).  Per-product relative error <= ~3*2^-22,
 // i.e. worst case ~7% of the 1e-5*max|x|*||h||_1 tolerance.
 //
-// Pipeline (one persistent CTA per SM, 192 threads):
-//   warp 0 lane 0 : producer -- cp.async.bulk of X windows and H8 stages
-//                   (8 shifts each) into smem, mbarrier complete_tx
-//   warp 1 lane 0 : MMA issuer -- tcgen05.mma kind::f16, 128x128x16, FP32
-//                   accumulators in TMEM (two 128-column buffers),
-//                   tcgen05.commit releases smem slots / publishes tiles
-//   warps 2..5    : epilogue -- tcgen05.ld 32x32b, unscale, coalesced stores
-//                   while the MMA warp already works on the next tile.
+// Pipeline (one persistent CTA per SM): warp 0 lane 0 is the producer
+// (cp.async.bulk of X windows and H8 stages into smem, mbarrier
+// complete_tx); warp 1 lane 0 issues tcgen05.mma kind::f16 (M128 x N x K16,
+// FP32 accumulators in TMEM: two N-column buffers) and tcgen05.commit
+// releases smem slots / publishes a drained stage; the epilogue warps (4 at
+// N = 128, 8 at N = 256) tcgen05.ld, accumulate in FP32, unscale and store
+// while the MMA warp works on the next stage.  N = 256-row tiles with
+// 4-shift drains and 112-shift X windows for launches that fill the SMs;
+// N = 128 with 8-shift drains (or 2 for <= 2-shift filters) otherwise.
+//
+// k_tc_fir_fs (end of file) is the fused-split variant for short filters:
+// converter warps read x as FP32 and build each unit's hi/lo window in
+// shared memory, so no split image goes through HBM.
 
 #include <cuda_fp16.h>
 
