@@ -597,14 +597,18 @@ struct FsGeo {
     static constexpr int THREADS = 64 + 32 * (NEPI + NCONV);
     static constexpr int SGROUPS = 2 * KG - 1 + KG * (SSH - 1);
     static constexpr uint32_t HST_PART = SGROUPS * 128;
-    static constexpr int WROWS_FIT = (int)((SMEM_MAX - 256 - NHSLOT * 2 * HST_PART) / (2 * 2 * KG * 16));
-    static constexpr int WPF = ((WROWS_FIT - 1 - TN) / 8) * 8;      // most shifts per unit
+    // ONE: the unit's FP32 window (TN + SSH - 1 rows, contiguous in x) is
+    // staged row-major by one bulk copy into RAW, then converted into the slot
+    static constexpr uint32_t RAW = ONE ? (uint32_t)(TN + SSH - 1) * TR * 4 : 0;
+    static constexpr int WROWS_FIT = (int)((SMEM_MAX - 256 - RAW - NHSLOT * 2 * HST_PART) / (2 * 2 * KG * 16));
+    static constexpr int WPF = ONE ? SSH : ((WROWS_FIT - 1 - TN) / 8) * 8;  // most shifts per unit
     // rows per window slot; WROWS = 1 (mod 8) puts the K-group stride at 16
     // (mod 128) bytes, so the converters' 16-byte accesses -- consecutive
     // threads on consecutive K-groups of one row -- are bank-conflict free
-    static constexpr int WROWS = TN + WPF + 1;
+    static constexpr int WROWS = ((TN + WPF - 1 + 6) / 8) * 8 + 1;
     static constexpr uint32_t XPART = WROWS * KG * 16;              // one slot, one part (hi or lo)
-    static constexpr uint32_t SM_HST = 4 * XPART;                   // slot s, part p at (2s + p) * XPART
+    static constexpr uint32_t SM_RAW = 4 * XPART;                   // slot s, part p at (2s + p) * XPART
+    static constexpr uint32_t SM_HST = SM_RAW + RAW;
     static constexpr uint32_t SM_BAR = SM_HST + NHSLOT * 2 * HST_PART;
     static constexpr uint32_t SM_TOTAL = SM_BAR + 256;
     static constexpr uint32_t IDESC = TcGeo<TN>::IDESC;
@@ -623,7 +627,18 @@ struct FsArgs {
     int64_t ldy;
     float *ws;
     unsigned *flag;
+    unsigned long long *trace;  // debug (SC_FS_TRACE): per CTA 0 unit timestamps
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define FS_TRACE(field)                                                                  \
+    do {                                                                                 \
+        if (a.trace && blockIdx.x == 0 && uc < 32) a.trace[uc * 8 + (field)] = gtime(); \
+    } while (0)
 
 template <int NT>
 __device__ __forceinline__ void conv_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NT) : "memory"); }
@@ -633,7 +648,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
     using G = FsGeo<SSH, ONE>;
     // converter groups of 4 warps; with two groups each takes every other
     // unit (its own window slot), so two windows' loads are in flight
-    constexpr int TN = G::TN, WROWS = G::WROWS, NEPI = G::NEPI, NCONV = 4, NGRP = G::NCONV / 4, NCT = 128;
+    constexpr int TN = G::TN, WROWS = G::WROWS, NEPI = G::NEPI, NCONV = 4, NGRP = ONE ? 1 : G::NCONV / 4, NCT = 128;
     constexpr uint32_t XPART = G::XPART, SM_HST = G::SM_HST, HST_PART = G::HST_PART, SM_BAR = G::SM_BAR;
     constexpr int64_t TTILE = (int64_t)TR * TN;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -648,9 +663,11 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
     const uint32_t bar_tfull = sbase + SM_BAR + 64;   // + 8*acc
     const uint32_t bar_tempty = sbase + SM_BAR + 80;  // + 8*acc
     const uint32_t bar_exfull = sbase + SM_BAR + 96;  // + 8*k, k = unit % 4
-    int *ex_ring = reinterpret_cast<int *>(smem + SM_BAR + 128);   // [4]
-    float *cmax = reinterpret_cast<float *>(smem + SM_BAR + 144);  // [NCONV <= 8]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + SM_BAR + 176);
+    const uint32_t bar_rawfull = sbase + SM_BAR + 128;
+    const uint32_t bar_rawempty = sbase + SM_BAR + 136;
+    int *ex_ring = reinterpret_cast<int *>(smem + SM_BAR + 144);   // [4]
+    float *cmax = reinterpret_cast<float *>(smem + SM_BAR + 160);  // [NCONV <= 8]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + SM_BAR + 192);
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -662,6 +679,8 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             mbar_init(bar_tempty + 8 * i, NEPI);
         }
         for (int k = 0; k < 4; ++k) mbar_init(bar_exfull + 8 * k, 1);
+        mbar_init(bar_rawfull, 1);
+        mbar_init(bar_rawempty, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -681,16 +700,44 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
         ch = tile / a.tiles_per_ch;
         i0 = (tile - ch * a.tiles_per_ch) * TN;
     };
+    // a unit's window: samples [m0, m0 + 128*nrows) of channel ch; interior =
+    // all of them inside [x_lo, x_hi) and 16-byte aligned (one bulk copy)
+    auto window_of = [&](int64_t sb, int64_t se, int64_t ch, int64_t i0, int64_t &m0, int &nrows, bool &interior) {
+        nrows = TN + (int)(se - sb) - 1;
+        m0 = a.n_begin + (i0 - (se - 1)) * TR;
+        const float *xc = a.x + ch * a.ldx - a.x_base;
+        interior = m0 >= a.x_lo && m0 + (int64_t)nrows * TR <= a.x_hi &&
+                   ((reinterpret_cast<uintptr_t>(xc + m0) & 15) == 0);
+    };
 
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------------------ producer: H8 stages
-            uint32_t hsc = 0;
-            for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+            // A stage already in the previous slot (same channel and shift
+            // range: every unit of a one-stage, one-channel launch) is not
+            // loaded again -- the MMA warp keeps using it.
+            uint32_t hsc = 0, rc = 0;
+            int64_t last_key = -1;
+            for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++rc) {
                 int64_t tile, sb, se, ch, i0;
                 unit_of(u, tile, sb, se, ch, i0);
+                if constexpr (ONE) {
+                    // the unit's FP32 window, one bulk copy (edge windows: the
+                    // converters fill RAW themselves after this arrive)
+                    int64_t m0;
+                    int nrows;
+                    bool interior;
+                    window_of(sb, se, ch, i0, m0, nrows, interior);
+                    if (rc > 0) mbar_wait(bar_rawempty, (rc - 1) & 1);
+                    const uint32_t bytes = interior ? (uint32_t)nrows * TR * 4 : 0;
+                    mbar_expect_tx(bar_rawfull, bytes);
+                    if (interior) bulk_g2s(sbase + G::SM_RAW, a.x + ch * a.ldx - a.x_base + m0, bytes, bar_rawfull);
+                }
                 const __half *h80 = a.h8[0] + ch * a.h8_ch, *h81 = a.h8[1] + ch * a.h8_ch;
                 for (int64_t sg = sb; sg < se; sg += SSH) {
+                    const int64_t key = ch * a.s8 + sg;
+                    if (key == last_key) continue;
+                    last_key = key;
                     const uint32_t slot = hsc % NHSLOT;
                     if (hsc >= NHSLOT) mbar_wait(bar_hempty + 8 * slot, ((hsc / NHSLOT) - 1) & 1);
                     mbar_expect_tx(bar_hfull + 8 * slot, 2 * HST_PART);
@@ -706,15 +753,25 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
         if (lane == 0) {
             // ------------------------------------------------------------ MMA issuer
             uint32_t uc = 0, hsc = 0, dc = 0;
+            int64_t last_key = -1;
+            uint32_t slot = 0;
             for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++uc) {
                 int64_t tile, sb, se, ch, i0;
                 unit_of(u, tile, sb, se, ch, i0);
                 const uint32_t xs = uc & 1;
                 mbar_wait(bar_xfull + 8 * xs, (uc >> 1) & 1);
+                FS_TRACE(3);
                 for (int64_t sg = sb; sg < se; sg += SSH) {
-                    const uint32_t slot = hsc % NHSLOT;
-                    mbar_wait(bar_hfull + 8 * slot, (hsc / NHSLOT) & 1);
-                    ++hsc;
+                    const int64_t key = ch * a.s8 + sg;
+                    if (key != last_key) {
+                        // leaving the previous stage: its slot is free once
+                        // the MMAs issued so far complete
+                        if (hsc > 0) umma_commit(bar_hempty + 8 * slot);
+                        last_key = key;
+                        slot = hsc % NHSLOT;
+                        mbar_wait(bar_hfull + 8 * slot, (hsc / NHSLOT) & 1);
+                        ++hsc;
+                    }
                     const uint32_t acc = dc & 1;
                     if (dc >= 2) mbar_wait(bar_tempty + 8 * acc, ((dc >> 1) - 1) & 1);
                     tc_fence_after();
@@ -740,11 +797,11 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                             umma_f16(d_tmem, ah, bl, G::IDESC, 1);
                         }
                     }
-                    umma_commit(bar_hempty + 8 * slot);
                     umma_commit(bar_tfull + 8 * acc);
                     ++dc;
                 }
                 umma_commit(bar_xempty + 8 * xs);
+                FS_TRACE(4);
             }
         }
     } else if (warp < 2 + NEPI) {
@@ -766,6 +823,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                 const float inv = __int_as_float((127 - e) << 23);
                 const uint32_t acc = dc & 1;
                 mbar_wait(bar_tfull + 8 * acc, (dc >> 1) & 1);
+                if (threadIdx.x == 64) FS_TRACE(5);
                 tc_fence_after();
                 const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * TN;
 #pragma unroll
@@ -778,6 +836,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                         if (n < a.n_end) yc[n - a.n_begin] = v[i] * inv;
                     }
                 }
+                if (threadIdx.x == 64) FS_TRACE(6);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
@@ -816,6 +875,100 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
         }
     } else {
         // ---------------------------------------------------------------- converters
+        if constexpr (ONE) {
+            // The window arrived row-major in RAW by one bulk copy (or, at the
+            // signal's edges, is filled here).  Pass 1: max |x| (float4 per
+            // thread, contiguous); pass 2: each thread turns 4 samples into
+            // 8 bytes of hi and 8 of lo in the slot's K-group-major layout.
+            // RAW is released as soon as pass 2 has read it, so the next
+            // window's copy overlaps this unit's MMAs.
+            constexpr int NT1 = 32 * G::NCONV;  // converter threads
+            const int ct = threadIdx.x - 32 * (2 + NEPI);  // 0..NT1-1
+            const int cw = ct >> 5;
+            const float4 *raw4 = reinterpret_cast<const float4 *>(smem + G::SM_RAW);
+            uint32_t uc = 0;
+            for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++uc) {
+                int64_t tile, sb, se, ch, i0, m0;
+                int nrows;
+                bool interior;
+                unit_of(u, tile, sb, se, ch, i0);
+                window_of(sb, se, ch, i0, m0, nrows, interior);
+                const uint32_t xs = uc & 1;
+                mbar_wait(bar_rawfull, uc & 1);
+                if (ct == 0) FS_TRACE(0);
+                const int n4 = nrows * (TR / 4);
+                if (!interior) {
+                    const float *xc = a.x + ch * a.ldx - a.x_base;
+                    float4 *w4 = reinterpret_cast<float4 *>(smem + G::SM_RAW);
+                    for (int q = ct; q < n4; q += NT1) {
+                        const int64_t m = m0 + 4 * (int64_t)q;
+                        float v[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) v[e] = (m + e >= a.x_lo && m + e < a.x_hi) ? xc[m + e] : 0.0f;
+                        w4[q] = make_float4(v[0], v[1], v[2], v[3]);
+                    }
+                    conv_bar<NT1>(1);
+                }
+                // RAW -> registers (<= 33 float4 per thread), then RAW is free
+                // for the next window's copy while this unit converts
+                constexpr int Q = (((TN + SSH - 1) * (TR / 4)) + NT1 - 1) / NT1;
+                float4 r[Q];
+                float mx = 0.0f;
+                bool bad = false;
+#pragma unroll
+                for (int k = 0; k < Q; ++k) {
+                    const int q = ct + NT1 * k;
+                    r[k] = q < n4 ? raw4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(r[k].x), fabsf(r[k].y)), fmaxf(fabsf(r[k].z), fabsf(r[k].w))));
+                    bad |= !(isfinite(r[k].x) && isfinite(r[k].y) && isfinite(r[k].z) && isfinite(r[k].w));
+                }
+                if (ct == 0) FS_TRACE(1);
+                for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 1u);
+                if (lane == 0) cmax[cw] = mx;
+                conv_bar<NT1>(1);   // also: every thread has read RAW
+                if (ct == 0) mbar_arrive(bar_rawempty);
+#pragma unroll
+                for (int w = 0; w < G::NCONV; ++w) mx = fmaxf(mx, cmax[w]);
+                int ex = (mx > 0.0f && isfinite(mx)) ? 14 - ilogbf(mx) : 0;
+                const int e_tot = ex + a.eh[ch];
+                if (ex > 114 || e_tot > 126 || e_tot < -126) {
+                    if (ct == 0) atomicOr(a.flag, 1u);
+                    ex = 0;
+                }
+                const float sc = __int_as_float((127 + ex) << 23);  // 2^ex
+                if (uc >= 2) mbar_wait(bar_xempty + 8 * xs, ((uc >> 1) - 1) & 1);
+                uint8_t *xhi = smem + (2 * xs) * XPART, *xlo = xhi + XPART;
+#pragma unroll
+                for (int k = 0; k < Q; ++k) {
+                    const int q = ct + NT1 * k;
+                    if (q < n4) {
+                        const int w = q >> 5, j = (q >> 1) & 15, half = q & 1;
+                        // packed: two samples per conversion instruction
+                        const float2 a01 = make_float2(r[k].x * sc, r[k].y * sc);
+                        const float2 a23 = make_float2(r[k].z * sc, r[k].w * sc);
+                        const __half2 h01 = __float22half2_rn(a01), h23 = __float22half2_rn(a23);
+                        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+                        const __half2 l01 = __float22half2_rn(make_float2(a01.x - f01.x, a01.y - f01.y));
+                        const __half2 l23 = __float22half2_rn(make_float2(a23.x - f23.x, a23.y - f23.y));
+                        const uint32_t off = ((uint32_t)j * WROWS + (uint32_t)w) * 16 + half * 8;
+                        *reinterpret_cast<uint2 *>(xhi + off) =
+                            make_uint2(*reinterpret_cast<const uint32_t *>(&h01), *reinterpret_cast<const uint32_t *>(&h23));
+                        *reinterpret_cast<uint2 *>(xlo + off) =
+                            make_uint2(*reinterpret_cast<const uint32_t *>(&l01), *reinterpret_cast<const uint32_t *>(&l23));
+                    }
+                }
+                // generic-proxy stores -> visible to the tensor core's async proxy
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                conv_bar<NT1>(1);
+                if (ct == 0) {
+                    ex_ring[uc & 3] = ex;
+                    mbar_arrive(bar_exfull + 8 * (uc & 3));
+                    mbar_arrive(bar_xfull + 8 * xs);
+                    FS_TRACE(2);
+                }
+            }
+        } else {
         // Work item = (window row w, K-group j): 8 consecutive samples.  The
         // raw FP32 samples land IN PLACE in the item's two 16-byte slots (hi
         // part, lo part) by cp.async -- every load of the window in flight at
@@ -833,6 +986,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             unit_of(u, tile, sb, se, ch, i0);
             const uint32_t xs = uc & 1;
             if (uc >= 2) mbar_wait(bar_xempty + 8 * xs, ((uc >> 1) - 1) & 1);
+            if (ct == 0) FS_TRACE(0);
             // window row w <-> global row i0 - (se - 1) + w; samples m0 + 128 w + v
             const int nrows = TN + (int)(se - sb) - 1;
             const int items = nrows * KG;
@@ -872,6 +1026,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             }
             asm volatile("cp.async.commit_group;\n" ::);
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            if (ct == 0) FS_TRACE(1);
             // max |x| over this thread's own items (it wrote them itself)
             float mx = 0.0f;
             bool bad = false;
@@ -918,8 +1073,10 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                 ex_ring[uc & 3] = ex;
                 mbar_arrive(bar_exfull + 8 * (uc & 3));
                 mbar_arrive(bar_xfull + 8 * xs);
+                FS_TRACE(2);
             }
         }
+    }
     }
     tc_fence_before();
     __syncthreads();
@@ -1021,6 +1178,12 @@ int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_
     nsplit = cdiv(s8, sps);
     a.nsplit = nsplit, a.sps = sps, a.n_units = n_tiles * nsplit;
     a.ws = nullptr;
+    static const bool trace = getenv("SC_FS_TRACE") != nullptr;
+    a.trace = nullptr;
+    if (trace) {
+        SC_CHECK_CUDA(cudaMalloc(&a.trace, 32 * 8 * 8));
+        SC_CHECK_CUDA(cudaMemset(a.trace, 0, 32 * 8 * 8));
+    }
     if (nsplit > 1) {
         a.ws = static_cast<float *>(scratch(sizeof(float) * (size_t)n_len * channels * nsplit, 4, stream, &err));
         if (err) return err;
@@ -1037,6 +1200,17 @@ int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_
         k_tc_fir_fs<SSH, false><<<grid, G::THREADS, G::SM_TOTAL, stream>>>(a);
     }
     SC_CHECK_LAUNCH();
+    if (a.trace) {
+        unsigned long long h[32 * 8];
+        cudaMemcpy(h, a.trace, sizeof h, cudaMemcpyDeviceToHost);
+        cudaFree(a.trace);
+        const unsigned long long t0 = h[0];
+        for (int k = 0; k < 32 && h[k * 8]; ++k)
+            fprintf(stderr, "[fs] unit %2d conv %7.2f load %7.2f ready %7.2f | mma %7.2f issued %7.2f | epi %7.2f done %7.2f us\n",
+                    k, (h[k * 8 + 0] - t0) * 1e-3, (h[k * 8 + 1] - t0) * 1e-3, (h[k * 8 + 2] - t0) * 1e-3,
+                    (h[k * 8 + 3] - t0) * 1e-3, (h[k * 8 + 4] - t0) * 1e-3, (h[k * 8 + 5] - t0) * 1e-3,
+                    (h[k * 8 + 6] - t0) * 1e-3);
+    }
     note_tc_launch(SSH, G::TN, n_tiles * (int64_t)TR * G::TN * (int64_t)TR * s8);
     if (nsplit > 1) {
         dim3 g((unsigned)cdiv(n_len, 256), (unsigned)channels);
