@@ -253,3 +253,40 @@ def test_unequal_segments_padded_batched_path():
         tol = max(_tol(xc, ir[c]) for ir in irs)
         assert np.max(np.abs(body[c] - ref_body)) <= tol, c
         assert len(tails[c]) == len(ref_tail) and np.max(np.abs(tails[c] - ref_tail)) <= tol, c
+
+
+def test_fast_stream_graph_replay_identical():
+    """The FAST fused stream (batched tensor-core FIR, state replay forked on a
+    side stream) captured as a CUDA graph and replayed: every replay equals
+    the first, direct call bit for bit, and the graph is actually used."""
+    import ctypes
+
+    import torch
+
+    from paper_2401_01607_b200 import _native as N
+    from paper_2401_01607_b200.core import Signal
+    from paper_2401_01607_b200.engine import EngineConfig, ScatterEngine
+
+    rng = np.random.default_rng(77)
+    n, nh, nb, every = 256 * 600, 4096, 256, 100
+    x = torch.from_numpy(rng.uniform(-1, 1, n).astype(np.float32)).cuda()
+    irs = [torch.from_numpy((rng.standard_normal(nh) * np.exp(-np.arange(nh) / 800)).astype(np.float32)).cuda()
+           for _ in range(6)]
+    swaps = [(0, irs[0])] + [(b, irs[b // every]) for b in range(every, n // nb, every)]
+    eng = ScatterEngine(Signal(irs[0]), EngineConfig(block_size_nb=nb))
+    assert eng.mode == "fast"
+    res = []
+    for _ in range(12):
+        body = eng.process_stream(x, nb, swaps)
+        tail = eng.flush().samples
+        res.append((body.cpu().numpy().copy(), tail.cpu().numpy().copy()))
+    hits, caps, fails = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    N.check(N.lib().sc_engine_graph_stats(eng._handle, ctypes.byref(hits), ctypes.byref(caps), ctypes.byref(fails)))
+    assert fails.value == 0 and caps.value >= 1 and hits.value >= 3, (hits.value, caps.value, fails.value)
+    for body, tail in res[1:]:
+        assert np.array_equal(body, res[0][0]) and np.array_equal(tail, res[0][1])
+    # and within the FP32 tolerance of the float64 oracle engine
+    ref_body, ref_tail = _oracle_stream(x.cpu().numpy(), {b: h.cpu().numpy() for b, h in swaps}, nb)
+    tol = max(_tol(x.cpu().numpy(), h.cpu().numpy()) for h in irs)
+    assert np.max(np.abs(res[0][0] - ref_body)) <= tol
+    assert np.max(np.abs(res[0][1] - ref_tail)) <= tol
