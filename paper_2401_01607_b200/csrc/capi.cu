@@ -215,9 +215,10 @@ int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_
         return launch_fir_f32_fast(x, ldx, x_base, x_lo, x_hi, h, ldh, nh, y, ldy, n_begin, n_end,
                                    channels, stream);
     const unsigned *nonfinite = nullptr;
+    bool folded = false;  // a split reduce already computes the flagged case
     int rc = launch_fir_f32_tc(x, ldx, x_base, x_lo, x_hi, h, ldh, nh, y, ldy, n_begin, n_end, channels,
-                               stream, &nonfinite, pre);
-    if (rc || !guard || !nonfinite) return rc;
+                               stream, &nonfinite, pre, &folded);
+    if (rc || !guard || !nonfinite || folded) return rc;
     // NaN/Inf inputs, and magnitudes whose power-of-two scales leave float
     // range (k_tc_fir.cu channel_scales), are routed (on the device, no host sync) to
     // the ORDERED kernel, which visits exactly the reference's (m, k) pairs

@@ -401,6 +401,16 @@ struct SegMap {
     int64_t m_lo[kMaxSegs], dst[kMaxSegs];
 };
 
+// Staging of every IR of a fused call in ONE launch (instead of one
+// cudaMemcpy2DAsync per IR): copy j moves [C][nh_j] from src_j (row pitch
+// sld_j) to stage + off_j (row pitch dld).  grid (x: 256-sample chunks of
+// the longest IR, y: copy, z: channel).
+struct StageCopies {
+    int n;
+    const void *src[kMaxSegs];
+    int64_t sld[kMaxSegs], off[kMaxSegs], nh[kMaxSegs];
+};
+
 // Extras of the mask pass for the batched tensor-core FIR: per (channel,
 // segment) max |masked x| into amax[2*(c*nseg + j)] (the TC kernel's power-
 // of-two scales; float bits, atomicMax), a flag for Inf samples (NaN is
@@ -416,12 +426,39 @@ struct MaskExtras {
     int nseg;
     int64_t L;         // padded segment length (batched layout)
     int64_t len[kMaxSegs];
+    // the batched FIR's IR staging (one copy per segment, taking max |h|), CTAs past the
+    // zero-padding ones: copy j of `stage` in `parts` 256-sample strides
+    float *fh;
+    int64_t fh_ld;
+    int parts;
 };
 
 __global__ void k_mask_skip(const float *__restrict__ x, int64_t ldx, int64_t n_total, int64_t nb, float keep,
                             float *__restrict__ xm, int64_t ldm, int64_t n_blocks, int64_t *__restrict__ J,
-                            bool vec4, SegMap sm, MaskExtras mx) {
+                            bool vec4, SegMap sm, MaskExtras mx, StageCopies stage) {
+    pdl_begin();
     const int64_t b = blockIdx.x;
+    const int64_t n_stage = mx.fh ? (int64_t)mx.parts * stage.n : 0;
+    if (b >= (int64_t)gridDim.x - n_stage) {
+        // IR staging for the batched FIR, taking max |h| and flagging non-finite taps
+        const int64_t q = b - ((int64_t)gridDim.x - n_stage);
+        const int j = (int)(q / mx.parts), part = (int)(q % mx.parts);
+        const int64_t ch = blockIdx.y;
+        const float *src = static_cast<const float *>(stage.src[j]) + ch * stage.sld[j];
+        float *dst = mx.fh + ch * mx.fh_ld + stage.off[j];
+        float amx = 0.0f;
+        bool bad = false;
+        for (int64_t i = (int64_t)part * blockDim.x + threadIdx.x; i < stage.nh[j]; i += (int64_t)mx.parts * blockDim.x) {
+            const float v = src[i];
+            dst[i] = v;
+            amx = fmaxf(amx, fabsf(v));
+            bad |= !isfinite(v);
+        }
+        for (int o = 16; o > 0; o >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+        if ((threadIdx.x & 31) == 0) atomicMax(mx.amax + 2 * (ch * stage.n + j) + 1, __float_as_uint(amx));
+        if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(mx.flag, 1u);
+        return;
+    }
     if (b >= n_blocks) {
         // zero [len_j, L) of segment j's padded row
         const int j = (int)(b - n_blocks);
@@ -494,9 +531,15 @@ __global__ void k_mask_skip(const float *__restrict__ x, int64_t ldx, int64_t n_
 __global__ void k_fast_combine(FastSegs sg, const float *__restrict__ fy, int64_t fy_ld,
                                const float *__restrict__ rin, int64_t res_ld, const int64_t *__restrict__ cap_snap,
                                int64_t n_total, int64_t n_slots, float *__restrict__ out, int64_t ldo,
-                               float *__restrict__ rout) {
+                               float *__restrict__ rout, unsigned *zero_next, int64_t zero_words) {
+    pdl_begin();
     const int64_t c = blockIdx.y;
     const int64_t cap = cap_snap[c];
+    // the next call's max / flag words start at zero (they were consumed by
+    // this call's FIR, which precedes this kernel)
+    if (zero_next && blockIdx.y == 0)
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < zero_words; i += (int64_t)gridDim.x * blockDim.x)
+            zero_next[i] = 0u;
     const float *yc = fy + c * fy_ld;
     for (int64_t t4 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; t4 < n_slots;
          t4 += (int64_t)gridDim.x * blockDim.x * 4) {
@@ -522,15 +565,6 @@ __global__ void k_fast_combine(FastSegs sg, const float *__restrict__ fy, int64_
     }
 }
 
-// Staging of every IR of a fused call in ONE launch (instead of one
-// cudaMemcpy2DAsync per IR): copy j moves [C][nh_j] from src_j (row pitch
-// sld_j) to stage + off_j (row pitch dld).  grid (x: 256-sample chunks of
-// the longest IR, y: copy, z: channel).
-struct StageCopies {
-    int n;
-    const void *src[kMaxSegs];
-    int64_t sld[kMaxSegs], off[kMaxSegs], nh[kMaxSegs];
-};
 
 template <typename T>
 __global__ void k_stage_irs(StageCopies c, T *__restrict__ stage, int64_t dld) {
@@ -542,26 +576,6 @@ __global__ void k_stage_irs(StageCopies c, T *__restrict__ stage, int64_t dld) {
         dst[i] = src[i];
 }
 
-// k_stage_irs for the batched FIR's taps, also taking max |h| per (channel,
-// segment) into amax[2*(ch*nseg + j) + 1] and flagging non-finite taps
-__global__ void k_stage_irs_amax(StageCopies c, float *__restrict__ stage, int64_t dld, unsigned *amax,
-                                 unsigned *flag) {
-    const int j = blockIdx.y;
-    const int64_t ch = blockIdx.z;
-    const float *src = static_cast<const float *>(c.src[j]) + ch * c.sld[j];
-    float *dst = stage + ch * dld + c.off[j];
-    float amx = 0.0f;
-    bool bad = false;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.nh[j]; i += (int64_t)gridDim.x * blockDim.x) {
-        const float v = src[i];
-        dst[i] = v;
-        amx = fmaxf(amx, fabsf(v));
-        bad |= !isfinite(v);
-    }
-    for (int o = 16; o > 0; o >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(amax + 2 * (ch * c.n + j) + 1, __float_as_uint(amx));
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
-}
 
 // Replays engine.py's bookkeeping over all blocks of the call: each swap
 // (cap = max(nh, live), ri = 0; engine.py:179-184) and each block
@@ -1048,7 +1062,8 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
     int64_t *cap_snap = reinterpret_cast<int64_t *>(static_cast<char *>(e->tcpre) + amax_bytes);
     float *xm = static_cast<float *>(e->fx), *fy = static_cast<float *>(e->fy);
     {
-        if (batched) SC_CHECK_CUDA(cudaMemsetAsync(amax, 0, 8 * e->C * nseg + 4, e->stream));
+        // amax / flag are zero here: a fresh buffer is zero-filled, and every
+        // batched call's combine zeroes them for the next one
         // smallest float strictly above thr (thr >= 0): |x| > thr <=> |x| >= keep
         float keep = (float)e->thr;
         if ((double)keep <= e->thr) keep = nextafterf(keep, INFINITY);
@@ -1069,10 +1084,23 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
         }
         const bool vec4 = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(xm)) & 15) == 0 &&
                           ldx % 4 == 0 && xpitch % 4 == 0 && nb % 4 == 0 && (!batched || L % 4 == 0);
-        const dim3 g((unsigned)(n_blocks + tails), (unsigned)e->C);
-        k_mask_skip<<<g, 256, 0, e->stream>>>(static_cast<const float *>(x), ldx, n_total, nb, keep, xm, xpitch,
-                                              n_blocks, e->jbuf, vec4, sm, mx);
-        SC_CHECK_LAUNCH();
+        // the batched FIR's IR staging rides in the same launch (extra CTAs)
+        StageCopies cp{};
+        int parts = 0;
+        if (batched) {
+            rc = ensure_2d(&e->fh, &e->fh_cap, e->C * nseg * NH, 4, 1, 0, e->stream);
+            if (rc) return rc;
+            cp.n = nseg;
+            for (int j = 0; j < nseg; ++j)
+                cp.src[j] = segs[j].h, cp.sld[j] = seg_ld[j], cp.off[j] = j * NH, cp.nh[j] = NH;
+            parts = (int)std::min<int64_t>(cdiv(NH, 256), 64);
+            mx.fh = static_cast<float *>(e->fh);
+            mx.fh_ld = nseg * NH;
+            mx.parts = parts;
+        }
+        const dim3 g((unsigned)(n_blocks + tails + (int64_t)parts * (batched ? nseg : 0)), (unsigned)e->C);
+        SC_LAUNCH_PDL(k_mask_skip, g, dim3(256), 0, e->stream, static_cast<const float *>(x), ldx, n_total, nb, keep,
+                      xm, xpitch, n_blocks, e->jbuf, vec4, sm, mx, cp);
     }
     // the state replay needs only J (and the state): fork it off
     SC_CHECK_CUDA(cudaEventRecord(e->ev_fork, e->stream));
@@ -1083,15 +1111,6 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
     SC_CHECK_CUDA(cudaEventRecord(e->ev_join, e->side));
     // NaN/Inf in x or h: launch_fir_f32's device-gated ordered fallback
     if (batched) {
-        rc = ensure_2d(&e->fh, &e->fh_cap, e->C * nseg * NH, 4, 1, 0, e->stream);
-        if (rc) return rc;
-        StageCopies cp{};
-        cp.n = nseg;
-        for (int j = 0; j < nseg; ++j)
-            cp.src[j] = segs[j].h, cp.sld[j] = seg_ld[j], cp.off[j] = j * NH, cp.nh[j] = NH;
-        const dim3 gs((unsigned)std::min<int64_t>(cdiv(NH, 256), 64), (unsigned)nseg, (unsigned)e->C);
-        k_stage_irs_amax<<<gs, 256, 0, e->stream>>>(cp, static_cast<float *>(e->fh), nseg * NH, amax, flag);
-        SC_CHECK_LAUNCH();
         const TcPre pre{amax, flag};
         rc = launch_fir_f32(SC_MODE_FAST, xm, L, 0, 0, L, static_cast<const float *>(e->fh), NH, NH, fy, Lo, 0, Lo,
                             e->C * nseg, e->stream, &pre);
@@ -1107,10 +1126,10 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
     }
     const int64_t n_slots = n_total + ub;
     const dim3 g((unsigned)std::min<int64_t>(cdiv(n_slots, 1024), 4096), (unsigned)e->C);
-    k_fast_combine<<<g, 256, 0, e->stream>>>(sg, fy, ypitch, static_cast<const float *>(rin), e->res_ld, cap_snap,
-                                             n_total, n_slots, static_cast<float *>(out), ldo,
-                                             static_cast<float *>(rout));
-    SC_CHECK_LAUNCH();
+    SC_LAUNCH_PDL(k_fast_combine, g, dim3(256), 0, e->stream, sg, static_cast<const float *>(fy), ypitch,
+                  static_cast<const float *>(rin), e->res_ld, static_cast<const int64_t *>(cap_snap), n_total, n_slots,
+                  static_cast<float *>(out), ldo, static_cast<float *>(rout), batched ? amax : nullptr,
+                  (int64_t)(batched ? 2 * e->C * nseg + 1 : 0));
     SC_CHECK_CUDA(cudaStreamWaitEvent(e->stream, e->ev_join, 0));
     return SC_OK;
 }

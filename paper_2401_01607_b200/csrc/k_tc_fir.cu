@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(TcGeo<TNV>::THREADS, 1) k_tc_fir(TcArgs a) {
     constexpr uint32_t HST_PART = S::HST_PART;
     constexpr uint32_t SM_BAR = S::SM_BAR;
     extern __shared__ __align__(1024) uint8_t smem[];
+    pdl_begin();
     if (*a.nonfinite) return;  // block-uniform: the FFMA kernel handles this input
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -518,11 +519,35 @@ __device__ __forceinline__ void split_x_tile(const float *__restrict__ x, int64_
 
 // H8[c][g][b][e] = split(scale_c * h_c[C - 8g - b - e]), C = 128*s8 - 1
 // y = sum of the split partials in ascending split order (deterministic).
+// The launch's inputs, for the flagged (NaN/Inf or out-of-range scale) case:
+// the reduce kernel then computes every output as the ordered FP32 chain
+// itself -- the reference's (m, k) pairs in ascending m, one fused
+// multiply-add per step, exactly what the gated k_chain_w launch would do --
+// so a launch with shift splits needs no separate fallback kernel.
+struct TcFallback {
+    const float *x;
+    int64_t ldx, x_base, x_lo, x_hi;
+    const float *h;
+    int64_t ldh, nh, n_begin;
+};
+
 __global__ void k_tc_split_reduce(const float *__restrict__ ws, int nsplit, int channels, int64_t n_len,
-                                  float *__restrict__ y, int64_t ldy, const unsigned *nonfinite) {
+                                  float *__restrict__ y, int64_t ldy, const unsigned *nonfinite, TcFallback fb) {
+    pdl_begin();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int ch = blockIdx.y;
-    if (i >= n_len || *nonfinite) return;
+    if (i >= n_len) return;
+    if (*nonfinite) {
+        const int64_t n = fb.n_begin + i;
+        const int64_t m_lo = n - fb.nh + 1 > fb.x_lo ? n - fb.nh + 1 : fb.x_lo;
+        const int64_t m_hi = n + 1 < fb.x_hi ? n + 1 : fb.x_hi;
+        const float *xc = fb.x + ch * fb.ldx - fb.x_base;
+        const float *hc = fb.h + ch * fb.ldh;
+        float acc = 0.0f;
+        for (int64_t m = m_lo; m < m_hi; ++m) acc = __fmaf_rn(xc[m], hc[n - m], acc);
+        y[(int64_t)ch * ldy + i] = acc;
+        return;
+    }
     float s = ws[(int64_t)ch * n_len + i];
     for (int k = 1; k < nsplit; ++k) s += ws[((int64_t)k * channels + ch) * n_len + i];
     y[(int64_t)ch * ldy + i] = s;
@@ -561,6 +586,7 @@ __global__ void __launch_bounds__(256) k_tc_prep(const float *__restrict__ x, in
                                                  __half *__restrict__ xt_lo, int64_t xt_ch,
                                                  __half *__restrict__ h8_hi, __half *__restrict__ h8_lo,
                                                  int64_t h8_ch, unsigned *fallback) {
+    pdl_begin();
     __shared__ __align__(16) float s[32][132];
     const int c = blockIdx.y;
     const float3 sc = channel_scales(amax, c, fallback);
@@ -652,6 +678,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
     constexpr uint32_t XPART = G::XPART, SM_HST = G::SM_HST, HST_PART = G::HST_PART, SM_BAR = G::SM_BAR;
     constexpr int64_t TTILE = (int64_t)TR * TN;
     extern __shared__ __align__(1024) uint8_t smem[];
+    pdl_begin();
     if (*a.flag) return;  // non-finite taps (found by the H8 build): the gated fallback computes the launch
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -1093,6 +1120,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
 __global__ void __launch_bounds__(256) k_h8_fs(const float *__restrict__ h, int64_t ldh, int64_t nh, int64_t s8,
                                                int64_t ngroups, __half *__restrict__ h8_hi,
                                                __half *__restrict__ h8_lo, int64_t h8_ch, int *eh, unsigned *flag) {
+    pdl_begin();
     const int c = blockIdx.y;
     const float *hc = h + (int64_t)c * ldh;
     float mx = 0.0f;
@@ -1124,7 +1152,8 @@ __global__ void __launch_bounds__(256) k_h8_fs(const float *__restrict__ h, int6
 // has more shifts than one window holds (the image path then runs).
 int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi, const float *h,
                          int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin, int64_t n_end,
-                         int64_t channels, cudaStream_t stream, const unsigned **nonfinite_out, const TcPre *pre) {
+                         int64_t channels, cudaStream_t stream, const unsigned **nonfinite_out, const TcPre *pre,
+                         bool *fallback_folded) {
     constexpr int SSH = 2;
     using G = FsGeo<SSH>;
     const int64_t n_len = n_end - n_begin;
@@ -1152,8 +1181,7 @@ int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_
     if (!pre) SC_CHECK_CUDA(cudaMemsetAsync(flag, 0, 4, stream));
     {
         dim3 g((unsigned)cdiv(ngroups * 8, 256), (unsigned)channels);
-        k_h8_fs<<<g, 256, 0, stream>>>(h, ldh, nh, s8, ngroups, h8_hi, h8_lo, h8_ch, eh, flag);
-        SC_CHECK_LAUNCH();
+        SC_LAUNCH_PDL(k_h8_fs, g, dim3(256), 0, stream, h, ldh, nh, s8, ngroups, h8_hi, h8_lo, h8_ch, eh, flag);
     }
     FsArgs a;
     a.x = x, a.ldx = ldx, a.x_base = x_base, a.x_lo = x_lo, a.x_hi = x_hi;
@@ -1193,13 +1221,12 @@ int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_
         using G1 = FsGeo<SSH, true>;
         SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir_fs<SSH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            G1::SM_TOTAL));
-        k_tc_fir_fs<SSH, true><<<grid, G1::THREADS, G1::SM_TOTAL, stream>>>(a);
+        SC_LAUNCH_PDL(k_tc_fir_fs<SSH, true>, dim3(grid), dim3(G1::THREADS), G1::SM_TOTAL, stream, a);
     } else {
         SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir_fs<SSH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            G::SM_TOTAL));
-        k_tc_fir_fs<SSH, false><<<grid, G::THREADS, G::SM_TOTAL, stream>>>(a);
+        SC_LAUNCH_PDL(k_tc_fir_fs<SSH, false>, dim3(grid), dim3(G::THREADS), G::SM_TOTAL, stream, a);
     }
-    SC_CHECK_LAUNCH();
     if (a.trace) {
         unsigned long long h[32 * 8];
         cudaMemcpy(h, a.trace, sizeof h, cudaMemcpyDeviceToHost);
@@ -1214,8 +1241,10 @@ int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_
     note_tc_launch(SSH, G::TN, n_tiles * (int64_t)TR * G::TN * (int64_t)TR * s8);
     if (nsplit > 1) {
         dim3 g((unsigned)cdiv(n_len, 256), (unsigned)channels);
-        k_tc_split_reduce<<<g, 256, 0, stream>>>(a.ws, (int)nsplit, (int)channels, n_len, y, ldy, flag);
-        SC_CHECK_LAUNCH();
+        SC_LAUNCH_PDL(k_tc_split_reduce, g, dim3(256), 0, stream, static_cast<const float *>(a.ws), (int)nsplit,
+                      (int)channels, n_len, y, ldy, static_cast<const unsigned *>(flag),
+                      TcFallback{x, ldx, x_base, x_lo, x_hi, h, ldh, nh, n_begin});
+        if (fallback_folded) *fallback_folded = true;
     }
     return SC_OK;
 }
@@ -1228,8 +1257,9 @@ bool tc_fir_supported(int64_t nh) { return nh >= 2 * TR; }
 int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
                       const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin,
                       int64_t n_end, int64_t channels, cudaStream_t stream, const unsigned **nonfinite_out,
-                      const TcPre *pre) {
+                      const TcPre *pre, bool *fallback_folded) {
     if (nonfinite_out) *nonfinite_out = nullptr;
+    if (fallback_folded) *fallback_folded = false;
     const int64_t n_len = n_end - n_begin;
     if (n_len <= 0 || channels <= 0) return SC_OK;
     SC_REQUIRE(nh >= 1, "tc fir: empty impulse response");
@@ -1242,7 +1272,7 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     }();
     if (fused) {
         const int rc = launch_fir_f32_tc_fs(x, ldx, x_base, x_lo, x_hi, h, ldh, nh, y, ldy, n_begin, n_end, channels,
-                                            stream, nonfinite_out, pre);
+                                            stream, nonfinite_out, pre, fallback_folded);
         if (rc != SC_ERR_STATE) return rc;
     }
     const int64_t s_needed = (nh + TR - 2) / TR + 1;
@@ -1317,9 +1347,8 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
         const int gsplit = (int)cdiv(nrows, 32);
         const int gh8 = (int)cdiv(ngroups * 8, 256);
         dim3 g((unsigned)(gsplit + gh8), (unsigned)channels);
-        k_tc_prep<<<g, 256, 0, stream>>>(x, ldx, x_base, x_lo, x_hi, n_begin, row_min, nrows, gsplit, h, ldh, nh,
-                                         s8, ngroups, amax, scales, xt_hi, xt_lo, xt_ch, h8_hi, h8_lo, h8_ch, flag);
-        SC_CHECK_LAUNCH();
+        SC_LAUNCH_PDL(k_tc_prep, g, dim3(256), 0, stream, x, ldx, x_base, x_lo, x_hi, n_begin, row_min, nrows, gsplit,
+                      h, ldh, nh, s8, ngroups, amax, scales, xt_hi, xt_lo, xt_ch, h8_hi, h8_lo, h8_ch, flag);
     }
     // function attributes are per device (context): set on every launch so
     // multi-GPU drivers (one host thread per device) never miss it
@@ -1389,7 +1418,8 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
         if (err) return err;
     }
     const int grid = (int)std::min<int64_t>(a.n_units, sms);
-#define SC_TC_LAUNCH(S, N) k_tc_fir<S, N><<<grid, TcGeo<N>::THREADS, TcStage<S, N>::SM_TOTAL, stream>>>(a)
+#define SC_TC_LAUNCH(S, N) \
+    SC_LAUNCH_PDL(k_tc_fir<S, N>, dim3(grid), dim3(TcGeo<N>::THREADS), TcStage<S, N>::SM_TOTAL, stream, a)
     if (TNV == 128 && SSH == 2) SC_TC_LAUNCH(2, 128);
     else if (TNV == 128 && SSH == 4) SC_TC_LAUNCH(4, 128);
     else if (TNV == 128) SC_TC_LAUNCH(8, 128);
@@ -1397,12 +1427,13 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     else if (SSH == 4) SC_TC_LAUNCH(4, 256);
     else SC_TC_LAUNCH(8, 256);
 #undef SC_TC_LAUNCH
-    SC_CHECK_LAUNCH();
     note_tc_launch(SSH, TNV, a.n_tiles * TTILE * (int64_t)TR * s8);
     if (nsplit > 1) {
         dim3 g((unsigned)cdiv(n_len, 256), (unsigned)channels);
-        k_tc_split_reduce<<<g, 256, 0, stream>>>(a.ws, (int)nsplit, (int)channels, n_len, y, ldy, flag);
-        SC_CHECK_LAUNCH();
+        SC_LAUNCH_PDL(k_tc_split_reduce, g, dim3(256), 0, stream, static_cast<const float *>(a.ws), (int)nsplit,
+                      (int)channels, n_len, y, ldy, static_cast<const unsigned *>(flag),
+                      TcFallback{x, ldx, x_base, x_lo, x_hi, h, ldh, nh, n_begin});
+        if (fallback_folded) *fallback_folded = true;
     }
     return SC_OK;
 }

@@ -109,6 +109,45 @@ __device__ __forceinline__ bool skipped(T x, double thr) {
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Kernels on a dependent chain (the FAST fused stream, the tensor-core FIR's
+// prep -> MMA -> reduce) are launched with programmatic stream
+// serialisation: the next kernel's launch and prologue overlap this one's
+// tail.  Every such kernel calls pdl_begin() first: it lets its own
+// successor launch and waits for its predecessors' memory (a no-op when the
+// kernel was launched without the attribute).
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+#define SC_LAUNCH_PDL(...)                                                                  \
+    do {                                                                                    \
+        cudaError_t _e = ::sc::launch_pdl(__VA_ARGS__);                                     \
+        if (_e != cudaSuccess) {                                                            \
+            ::sc::set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e),     \
+                            __FILE__, __LINE__);                                            \
+            return SC_ERR_CUDA;                                                             \
+        }                                                                                   \
+        ::sc::note_launch();                                                                \
+    } while (0)
+
 }  // namespace sc
 
 // ------------------------------------------------------------------ internal launchers
@@ -168,7 +207,8 @@ bool tc_fir_supported(int64_t nh);
 int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
                       const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin,
                       int64_t n_end, int64_t channels, cudaStream_t stream,
-                      const unsigned **nonfinite_out, const TcPre *pre = nullptr);
+                      const unsigned **nonfinite_out, const TcPre *pre = nullptr,
+                      bool *fallback_folded = nullptr);
 
 // FAST-mode dispatch: tensor cores for long filters, FFMA2 kernel otherwise.
 int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
