@@ -176,3 +176,72 @@ def test_tc_same_sign_inputs(nh):
     h = (rng.uniform(0, 1, nh) * np.exp(-np.arange(nh) / (nh / 3))).astype(np.float32)
     y = np.asarray(scatter_convolve(Signal(x), Signal(h), mode="tc").concatenated().samples)
     assert err_frac(y, O.scatter_window(x, h, 0, len(y)), x, h) <= 1.0
+
+
+# ---------------------------------------------------------------- fused split (k_tc_fir_fs)
+# Taken for filters of <= 8 shifts on launches of >= 2 tiles per SM (>= 296
+# tiles of 16,384 outputs): one-stage units (<= 255 taps) on the bulk-copy
+# path, 3-8 shifts on the in-place cp.async path.
+
+
+def _fs_check(x, h, y, seeds=6):
+    n = len(x) + len(h) - 1
+    wins = [0, n - 512, min(len(x) - 256, n - 512)] + [int(s) for s in np.random.default_rng(seeds).integers(0, n - 512, seeds)]
+    for s in wins:
+        ref = O.scatter_window(x, h, s, s + 512)
+        assert err_frac(np.asarray(y[s:s + 512]), ref, x, h) <= 1.0, s
+
+
+@pytest.mark.parametrize("nh", [48, 128, 255, 700, 900])
+def test_fused_split_large_launch(nh):
+    import torch
+
+    rng = np.random.default_rng(900 + nh)
+    ne = (1 << 23) + 12_345                       # 512+ tiles: the fused-split kernel
+    x = rng.uniform(-1, 1, ne).astype(np.float32)
+    h = (rng.standard_normal(nh) * np.exp(-np.arange(nh) / (nh / 4 + 1))).astype(np.float32)
+    y = scatter_convolve(Signal(torch.from_numpy(x).cuda()), Signal(torch.from_numpy(h).cuda()))
+    y = y.concatenated().samples.cpu().numpy()
+    assert len(y) == ne + nh - 1
+    _fs_check(x, h, y)
+
+
+def test_fused_split_batched_channels_and_shards():
+    import torch
+
+    rng = np.random.default_rng(77)
+    C, ne, nh = 8, 700_001, 131
+    x = rng.uniform(-1, 1, (C, ne)).astype(np.float32)
+    h = rng.standard_normal((C, nh)).astype(np.float32)
+    y = convolve_batched(torch.from_numpy(x).cuda(), torch.from_numpy(h).cuda()).cpu().numpy()
+    for c in (0, 3, 7):
+        _fs_check(x[c], h[c], y[c], seeds=2)
+    # a shard whose input slice starts unaligned (edge windows take the slow fill)
+    xs = rng.uniform(-1, 1, 5_000_003).astype(np.float32)
+    hs = rng.standard_normal(100).astype(np.float32)
+    plan = shard_plan(len(xs), len(hs), 3)
+    hd = torch.from_numpy(hs).cuda()
+    for sh in plan[1:]:
+        ys = convolve_shard(torch.from_numpy(xs[sh.x_begin:sh.x_end]).cuda(), sh, hd).cpu().numpy()
+        for s in (0, sh.n_out - 300):
+            ref = O.scatter_window(xs, hs, sh.n_begin + s, sh.n_begin + s + 300)
+            assert err_frac(ys[s:s + 300], ref, xs, hs) <= 1.0
+
+
+def test_fused_split_nonfinite_falls_back():
+    import torch
+
+    rng = np.random.default_rng(78)
+    ne, nh = (1 << 23), 128
+    x = rng.uniform(-1, 1, ne).astype(np.float32)
+    x[4_000_000] = np.inf
+    x[6_000_123] = np.nan
+    h = rng.standard_normal(nh).astype(np.float32)
+    y = scatter_convolve(Signal(torch.from_numpy(x).cuda()), Signal(torch.from_numpy(h).cuda()))
+    y = y.concatenated().samples.cpu().numpy()
+    for s in (3_999_900, 6_000_000, 100_000):
+        ref = O.scatter_window(x, h, s, s + 400)
+        got = y[s:s + 400].astype(np.float64)
+        assert np.array_equal(np.isnan(got), np.isnan(ref)) and np.array_equal(np.isinf(got), np.isinf(ref)), s
+        fin = np.isfinite(ref)
+        assert np.max(np.abs(got[fin] - ref[fin]), initial=0) <= configs.tolerance(x[np.isfinite(x)], h, "f32")
