@@ -315,7 +315,9 @@ class Work:
             self.kernel = "k_tc_fir" if fast else "k_chain_w"
             return
         if self.dtype != "f32" or self.cfg not in ("cfg3", "cfg4", "cfg5") or self.mode == "ordered":
-            self.kernel = "k_chain_w"   # ordered chain (csrc/k_ordered.cu)
+            # ordered chain (csrc/k_ordered.cu): strict float64 with one IR of
+            # <= 2,048 taps runs the latency kernel k_chain_small
+            self.kernel = "k_chain_small" if self.dtype == "f64" and self.w.nh <= 2048 else "k_chain_w"
             return
         nh = self.w.nh
         use_tc = self.mode == "tc" or (self.mode in ("fast", "auto") and nh >= 256)

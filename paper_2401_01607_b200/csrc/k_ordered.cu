@@ -437,6 +437,180 @@ int pick_r(int64_t n_out, int64_t channels, size_t es) {
     return 1;
 }
 
+// ---------------------------------------------------------------- small strict float64
+// k_chain_small: the latency kernel for small single-IR float64 strict
+// launches (cfg1: 48,000 x 1,024 taps, 49,023 chains of 1,024 dependent
+// DMUL+DADD steps).  Such launches cannot fill the FP64 pipe: there are only
+// ~83 chains per SM sub-partition, so the time per step is set by how many
+// chains share a sub-partition's 16-lane FP64 pipe and by how well one warp
+// hides its own latencies.  Measured (tools/ubench/chain_small.cu): 3
+// consecutive outputs per thread in one-warp CTAs (96 chains per warp, at
+// most one warp per sub-partition at cfg1) beat 2 (two warps on some
+// sub-partitions) and 4 (idle sub-partitions); k_chain_w's chunked,
+// windowed form took 22.6 us at cfg1.
+//
+// Every output t runs one chain over a fixed step count nhp = nh rounded up
+// to 8: step j takes drive sample m = t - nhp + 1 + j and tap hs[nhp-1-j]
+// (taps ascending in shared memory, zero beyond nh), the drive zero outside
+// [m_lo, m_hi).  The steps the reference does not take add x*0 or 0*h = +-0,
+// which leaves the chain unchanged when the operands are finite (chains start
+// at +0 and never become -0), so the result is bit-identical to k_chain_w's
+// and the reference's.  A CTA whose padded steps would meet a non-finite
+// operand runs the bounded per-output loop instead (same products, same
+// order, no padded terms).
+//
+// Staging: the CTA's drive window (TILE + nhp - 1 samples) and the taps
+// arrive by cp.async.bulk on one mbarrier, issued by one thread while the
+// warp writes the zero padding.  (Splitting the staging into per-128-step
+// chunks so the chain could start earlier measured slower: the first chunk
+// landed later than the whole window does in one transfer.)
+constexpr int CS_R = 3;
+constexpr int CS_TB = 32;
+constexpr int CS_MAX_NH = 2048;                  // <= 34 KB of shared memory
+
+__device__ __forceinline__ void cs_bulk(void *dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+template <int R, int TB>
+__global__ void __launch_bounds__(TB) k_chain_small(const double *__restrict__ x, int64_t x_off, int64_t m_lo,
+                                                    int64_t m_hi, const double *__restrict__ h, int nh, int64_t t0,
+                                                    int64_t n_out, double *__restrict__ y) {
+    extern __shared__ __align__(16) unsigned char cs_smem[];
+    constexpr int TILE = TB * R;
+    const int nhp = (nh + 7) & ~7;
+    const int P = nhp - nh;
+    const int nxs = TILE + nhp - 1;
+    const int64_t tile0 = t0 + (int64_t)blockIdx.x * TILE;
+    const int64_t g0 = tile0 - nhp + 1;  // drive index m of xs[0]
+    // 16-byte aligned drive samples m share one parity; shift xs by one
+    // element when needed so they land 16-byte aligned in shared memory
+    const uintptr_t xa = reinterpret_cast<uintptr_t>(x) - (uintptr_t)(x_off * 8);  // address of m = 0
+    const int apar = (int)((xa >> 3) & 1);
+    const int sx = (int)((apar - g0) & 1);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(cs_smem);
+    double *hs = reinterpret_cast<double *>(cs_smem + 16);  // nhp taps ascending
+    double *xs = hs + nhp + sx;                               // nxs drive samples
+    const bool h_bulk = (reinterpret_cast<uintptr_t>(h) & 15) == 0;
+    const int tid = threadIdx.x;
+    const uint32_t bb = (uint32_t)__cvta_generic_to_shared(bar);
+    // drive indices inside the signal: [a, b); bulk part [a16, a16 + n16)
+    const int64_t a = max(g0, m_lo), b = min(g0 + nxs, m_hi);
+    const int64_t a16 = a + ((int)(a & 1) != apar);
+    const int64_t n16 = b > a16 ? (b - a16) & ~(int64_t)1 : 0;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bb), "r"(1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        const uint32_t xbytes = (uint32_t)(n16 * 8), hbytes = h_bulk ? (uint32_t)(nh & ~1) * 8 : 0;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(xbytes + hbytes)
+                     : "memory");
+        if (xbytes) cs_bulk(xs + (a16 - g0), x + (a16 - x_off), xbytes, bb);
+        if (hbytes) cs_bulk(hs, h, hbytes, bb);
+    }
+    // plain stores: zero drive outside [m_lo, m_hi) (edge CTAs), the (at
+    // most two) unaligned ends of the bulk range, zero taps past nh, and
+    // every tap when h is not 16-byte aligned
+    const bool edge = g0 < m_lo || g0 + nxs > m_hi;
+    if (edge)
+        for (int i = tid; i < nxs; i += TB) {
+            const int64_t m = g0 + i;
+            if (m < m_lo || m >= m_hi) xs[i] = 0.0;
+        }
+    if (tid == 0 && a < b) {
+        if (a16 > a) xs[a - g0] = x[a - x_off];
+        for (int64_t m = a16 + n16; m < b; ++m) xs[m - g0] = x[m - x_off];
+    }
+    for (int k = nh + tid; k < nhp; k += TB) hs[k] = 0.0;
+    if (!h_bulk)
+        for (int k = tid; k < nh; k += TB) hs[k] = h[k];
+    else if ((nh & 1) && tid == 0)
+        hs[nh - 1] = h[nh - 1];
+    __syncthreads();  // plain stores visible; the mbarrier init too
+    {
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+                " selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(done)
+                : "r"(bb)
+                : "memory");
+    }
+    // Padded steps are exact only with finite operands: x meets a zero tap in
+    // the P front steps (drive xs[0, TILE+P-1)), and a real tap meets zero
+    // drive only in edge CTAs, which check the taps.
+    bool fin = true;
+    if (P > 0)
+        for (int i = tid; i < TILE + P - 1; i += TB) fin &= isfinite(xs[i]);
+    if (edge)
+        for (int k = tid; k < nh; k += TB) fin &= isfinite(hs[k]);
+    fin = TB == 32 ? __all_sync(0xffffffffu, fin) : __syncthreads_and(fin);
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    const double *xb = xs + tid * R;  // xs index of (output r, step j) = tid*R + r + j
+    if (fin) {
+        double wx[R + 7];
+#pragma unroll
+        for (int k = 0; k < R - 1; ++k) wx[k] = xb[k];
+#pragma unroll 4
+        for (int jq = 0; jq < nhp; jq += 8) {  // steps jq..jq+7
+            double hv[8];
+#pragma unroll
+            for (int k = 0; k < 8; k += 2) {  // their taps, descending in memory
+                const double2 d = *reinterpret_cast<const double2 *>(hs + nhp - 8 - jq + k);
+                hv[7 - k] = d.x, hv[6 - k] = d.y;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) wx[R - 1 + k] = xb[jq + R - 1 + k];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int r = 0; r < R; ++r) acc[r] = __dadd_rn(acc[r], __dmul_rn(wx[u + r], hv[u]));
+#pragma unroll
+            for (int k = 0; k < R - 1; ++k) wx[k] = wx[8 + k];
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t t = tile0 + tid * R + r;
+            // tap t-m in [0, nh) <=> j >= P; drive m in [m_lo, m_hi)
+            const int64_t lo = max((int64_t)P, m_lo - t + nhp - 1);
+            const int64_t hi = min((int64_t)nhp, m_hi - t + nhp - 1);
+            for (int64_t j = lo; j < hi; ++j) acc[r] = __dadd_rn(acc[r], __dmul_rn(xb[r + j], hs[nhp - 1 - j]));
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = (int64_t)blockIdx.x * TILE + tid * R + r;
+        if (i < n_out) y[i] = acc[r];
+    }
+}
+
+size_t chain_small_smem(int nh) {
+    const int nhp = (nh + 7) & ~7;
+    return 16 + sizeof(double) * (size_t)(2 * nhp + CS_TB * CS_R);
+}
+
+// Strict float64 launches of one IR of at most 2,048 taps (sc_fir_full,
+// shards) take k_chain_small at every size: it also beats k_chain_w on
+// large launches
+// (tools/ubench/cfg1_lib.cu, one launch after an L2 flush: 8 M x 1,024 taps
+// 1.01 ms vs 1.96 ms; 2 M x 2,048 0.57 vs 0.77; 4 M x 64 45 us vs 562).
+// SC_CHAIN_SMALL=0 turns it off (A/B and tests).
+bool chain_small_ok(int64_t n_out, int64_t nh) {
+    static const int forced = [] {
+        const char *v = getenv("SC_CHAIN_SMALL");
+        return v ? atoi(v) : -1;
+    }();
+    (void)n_out;
+    return forced != 0 && nh >= 1 && nh <= CS_MAX_NH;
+}
+
 template <typename T>
 int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off,
                    const ChainSeg *segs, int nseg, const void *init, int64_t init_len,
@@ -470,6 +644,18 @@ int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off
         a.ld_outb = batch->ld_outb;
         a.ld_st = batch->ld_st;
         SC_REQUIRE(channels >= 1 && channels < 65536, "chain: bad batch");
+    }
+    if constexpr (sizeof(T) == 8) {
+        if (!fused && skip_mode == SC_SKIP_NONE && nseg == 1 && !init && !init_len_dev && !out_b && !run_if &&
+            !batch && n_a >= n_out && chain_small_ok(n_out, segs[0].nh)) {
+            const int nh = (int)segs[0].nh;
+            const dim3 grid((unsigned)cdiv(n_out, (int64_t)CS_TB * CS_R));
+            k_chain_small<CS_R, CS_TB><<<grid, CS_TB, chain_small_smem(nh), stream>>>(
+                static_cast<const double *>(x), x_off, segs[0].m_lo, segs[0].m_hi,
+                static_cast<const double *>(segs[0].h), nh, t0, n_out, static_cast<double *>(out_a));
+            SC_CHECK_LAUNCH();
+            return SC_OK;
+        }
     }
     const int R = pick_r(n_out, channels, sizeof(T));
     // Grid-stride over tiles.  A device-gated launch (run_if) is usually a
