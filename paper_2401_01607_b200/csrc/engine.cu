@@ -433,15 +433,82 @@ struct MaskExtras {
     int parts;
 };
 
+// Blocks of at most kMaskWarpNb samples take one WARP each (8 per CTA):
+// with a CTA per 256-sample block, cfg2's 1,875 blocks were 2 waves of
+// CTAs that each did one load, two barriers and an atomic (~10 us).
+constexpr int64_t kMaskWarpNb = 1024;
+constexpr int kMaskBpc = 8;  // blocks per CTA in warp mode (256 threads)
+
+__device__ __forceinline__ void mask_block_warp(const float *__restrict__ x, int64_t ldx, int64_t n_total, int64_t nb,
+                                                float keep, float *__restrict__ xm, int64_t ldm, int64_t n_blocks,
+                                                int64_t *__restrict__ J, bool vec4, const SegMap &sm,
+                                                const MaskExtras &mx, int64_t b) {
+    const int lane = threadIdx.x & 31;
+    if (b == 0 && lane == 0 && mx.cap_snap) mx.cap_snap[blockIdx.y] = mx.st[blockIdx.y * ST_N + ST_CAP];
+    const float *xc = x + blockIdx.y * ldx + b * nb;
+    int64_t dst = b * nb;
+    int seg = 0;
+    if (sm.n > 0) {
+        while (seg + 1 < sm.n && sm.m_lo[seg + 1] <= b * nb) ++seg;
+        dst = sm.dst[seg] + (b * nb - sm.m_lo[seg]);
+    }
+    float *mc = xm + blockIdx.y * ldm + dst;
+    const int64_t n = n_total - b * nb < nb ? n_total - b * nb : nb;
+    long long j = -1;
+    float amx = 0.0f;
+    bool inf = false;
+    int64_t i0 = 0;
+    if (vec4) {
+        const int64_t n4 = n >> 2;
+        for (int64_t q = lane; q < n4; q += 32) {
+            float4 v = reinterpret_cast<const float4 *>(xc)[q];
+            const bool k0 = fabsf(v.x) >= keep, k1 = fabsf(v.y) >= keep, k2 = fabsf(v.z) >= keep,
+                       k3 = fabsf(v.w) >= keep;
+            v.x = k0 ? v.x : 0.0f, v.y = k1 ? v.y : 0.0f, v.z = k2 ? v.z : 0.0f, v.w = k3 ? v.w : 0.0f;
+            reinterpret_cast<float4 *>(mc)[q] = v;
+            amx = fmaxf(amx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+            inf |= isinf(v.x) || isinf(v.y) || isinf(v.z) || isinf(v.w);
+            const long long base = 4 * q;
+            if (k3) j = base + 3;
+            else if (k2) j = base + 2;
+            else if (k1) j = base + 1;
+            else if (k0) j = base;
+        }
+        i0 = n4 << 2;
+    }
+    for (int64_t i = i0 + lane; i < n; i += 32) {
+        const float v = xc[i];
+        const bool keepv = fabsf(v) >= keep;
+        const float w = keepv ? v : 0.0f;
+        mc[i] = w;
+        amx = fmaxf(amx, fabsf(w));
+        inf |= isinf(w);
+        if (keepv) j = i;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long v = __shfl_xor_sync(0xffffffffu, j, o);
+        j = v > j ? v : j;
+        amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+    }
+    if (mx.amax && __any_sync(0xffffffffu, inf) && lane == 0) atomicOr(mx.flag, 1u);
+    if (lane == 0) {
+        J[blockIdx.y * n_blocks + b] = j;
+        if (mx.amax) atomicMax(mx.amax + 2 * (blockIdx.y * mx.nseg + seg), __float_as_uint(amx));
+    }
+}
+
 __global__ void k_mask_skip(const float *__restrict__ x, int64_t ldx, int64_t n_total, int64_t nb, float keep,
                             float *__restrict__ xm, int64_t ldm, int64_t n_blocks, int64_t *__restrict__ J,
-                            bool vec4, SegMap sm, MaskExtras mx, StageCopies stage) {
+                            bool vec4, SegMap sm, MaskExtras mx, StageCopies stage, int bpc) {
     pdl_begin();
-    const int64_t b = blockIdx.x;
+    // CTAs: [0, nbc) blocks (bpc per CTA), then nseg zero-padding CTAs, then
+    // the IR staging CTAs
+    const int64_t nbc = (n_blocks + bpc - 1) / bpc;
+    const int64_t bx = blockIdx.x;
     const int64_t n_stage = mx.fh ? (int64_t)mx.parts * stage.n : 0;
-    if (b >= (int64_t)gridDim.x - n_stage) {
+    if (bx >= (int64_t)gridDim.x - n_stage) {
         // IR staging for the batched FIR, taking max |h| and flagging non-finite taps
-        const int64_t q = b - ((int64_t)gridDim.x - n_stage);
+        const int64_t q = bx - ((int64_t)gridDim.x - n_stage);
         const int j = (int)(q / mx.parts), part = (int)(q % mx.parts);
         const int64_t ch = blockIdx.y;
         const float *src = static_cast<const float *>(stage.src[j]) + ch * stage.sld[j];
@@ -459,13 +526,19 @@ __global__ void k_mask_skip(const float *__restrict__ x, int64_t ldx, int64_t n_
         if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(mx.flag, 1u);
         return;
     }
-    if (b >= n_blocks) {
+    if (bx >= nbc) {
         // zero [len_j, L) of segment j's padded row
-        const int j = (int)(b - n_blocks);
+        const int j = (int)(bx - nbc);
         float *row = xm + blockIdx.y * ldm + (int64_t)j * mx.L;
         for (int64_t i = mx.len[j] + threadIdx.x; i < mx.L; i += blockDim.x) row[i] = 0.0f;
         return;
     }
+    if (bpc > 1) {
+        const int64_t bw = bx * bpc + (threadIdx.x >> 5);
+        if (bw < n_blocks) mask_block_warp(x, ldx, n_total, nb, keep, xm, ldm, n_blocks, J, vec4, sm, mx, bw);
+        return;
+    }
+    const int64_t b = bx;
     if (b == 0 && threadIdx.x == 0 && mx.cap_snap) mx.cap_snap[blockIdx.y] = mx.st[blockIdx.y * ST_N + ST_CAP];
     const float *xc = x + blockIdx.y * ldx + b * nb;
     int64_t dst = b * nb;
@@ -1098,9 +1171,11 @@ int fast_stream(sc_engine *e, const void *x, int64_t ldx, int64_t n_total, int64
             mx.fh_ld = nseg * NH;
             mx.parts = parts;
         }
-        const dim3 g((unsigned)(n_blocks + tails + (int64_t)parts * (batched ? nseg : 0)), (unsigned)e->C);
+        const int bpc = nb <= kMaskWarpNb ? kMaskBpc : 1;
+        const dim3 g((unsigned)(cdiv(n_blocks, (int64_t)bpc) + tails + (int64_t)parts * (batched ? nseg : 0)),
+                     (unsigned)e->C);
         SC_LAUNCH_PDL(k_mask_skip, g, dim3(256), 0, e->stream, static_cast<const float *>(x), ldx, n_total, nb, keep,
-                      xm, xpitch, n_blocks, e->jbuf, vec4, sm, mx, cp);
+                      xm, xpitch, n_blocks, e->jbuf, vec4, sm, mx, cp, bpc);
     }
     // the state replay needs only J (and the state): fork it off
     SC_CHECK_CUDA(cudaEventRecord(e->ev_fork, e->stream));

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 from dataclasses import dataclass
+from operator import is_ as _is
 
 import numpy as np
 
@@ -103,6 +104,7 @@ class ScatterEngine:
         self._handle = ctypes.c_void_p()
         self._stream_val = None
         self._sched_cache = None
+        self._stream_fast = None  # see _process_stream_fast
         hd = self._to_dev(h.samples)
         with _dev.device_guard(self._device):
             N.check(self._lib.sc_engine_create(self._dt, N.ptr(hd), len(h),
@@ -335,6 +337,11 @@ class ScatterEngine:
         Returns the body (device tensor if x is a CUDA tensor, else ndarray).
         """
         nb = self.config.block_size_nb if nb is None else int(nb)
+        fp = self._stream_fast
+        if fp is not None and self._pending_ir is None:
+            out = self._process_stream_fast(fp, x, nb, swaps)
+            if out is not None:
+                return out
         if nb < 1 or nb > self.config.block_size_nb:
             raise ValueError(f"nb must be in [1, block_size_nb={self.config.block_size_nb}]")
         t = _dev.torch()
@@ -394,7 +401,37 @@ class ScatterEngine:
             if rc:
                 N.check(rc)
             self._note_swaps(swaps, pending)
+            if xd is xs and pending is None and type(xs) is t.Tensor and xs.dim() == 1:
+                # args[1] keeps the device IRs (and the C arrays) alive
+                self._stream_fast = (nb, xs.shape[0], xs.dtype, self._device.index, self._sched_cache[2],
+                                     self._sched_cache[1], (self._ir_like, self._nh) if swaps else None)
         return out if xd is xs else _dev.like_input(out, xs)
+
+    def _process_stream_fast(self, fp, x, nb, swaps):
+        """process_stream's repeat call: the same device tensor shape and
+        dtype, the same nb and the same swap schedule (the very same
+        (block, IR) tuples as the call that built the cached C arrays), no
+        pending swap, on the same device and stream -- straight to the C call
+        (~3 us of Python instead of ~12: the fused stream's GPU work starts
+        that much earlier).  None when any of it differs."""
+        f_nb, f_len, f_dtype, f_dev, f_keep, args, note = fp
+        t = _dev.torch()
+        if (nb != f_nb or type(x) is not t.Tensor or x.dtype is not f_dtype or x.dim() != 1
+                or x.shape[0] != f_len or not x.is_cuda or x.get_device() != f_dev or not x.is_contiguous()
+                or len(swaps) != len(f_keep) or not all(map(_is, swaps, f_keep))):
+            return None
+        C = t._C
+        if C._cuda_getDevice() != f_dev or C._cuda_getCurrentRawStream(f_dev) != self._stream_val:
+            return None
+        _, _, blocks, ptrs, nhs, n = args
+        out = x.new_empty(f_len)
+        rc = self._lib.sc_engine_process_blocks(self._handle, x.data_ptr(), f_len, f_nb, blocks, ptrs, nhs, n,
+                                                out.data_ptr())
+        if rc:
+            N.check(rc)
+        if note is not None:
+            self._ir_like, self._nh = note
+        return out
 
     def _note_swaps(self, swaps, pending=None):
         """Host copy of the IR now in effect: the last swap of the timeline,
