@@ -616,10 +616,14 @@ __global__ void __launch_bounds__(256) k_tc_prep(const float *__restrict__ x, in
 // shift splits) -- the epilogue streams each accumulator straight out (no
 // per-thread sum over stages), which frees the registers for 8 converter
 // warps instead of 4.
+// converter warps of the one-stage kernel (env knob for A/B at build time)
+#ifndef FS_NCONV1
+#define FS_NCONV1 16
+#endif
 template <int SSH, bool ONE = false>
 struct FsGeo {
     static constexpr int TN = 128;                                  // output rows per tile (UMMA N)
-    static constexpr int NEPI = 4, NCONV = ONE ? 8 : 4;
+    static constexpr int NEPI = 4, NCONV = ONE ? FS_NCONV1 : 4;
     static constexpr int THREADS = 64 + 32 * (NEPI + NCONV);
     static constexpr int SGROUPS = 2 * KG - 1 + KG * (SSH - 1);
     static constexpr uint32_t HST_PART = SGROUPS * 128;
@@ -693,8 +697,9 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
     const uint32_t bar_rawfull = sbase + SM_BAR + 128;
     const uint32_t bar_rawempty = sbase + SM_BAR + 136;
     int *ex_ring = reinterpret_cast<int *>(smem + SM_BAR + 144);   // [4]
-    float *cmax = reinterpret_cast<float *>(smem + SM_BAR + 160);  // [NCONV <= 8]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + SM_BAR + 192);
+    float *cmax = reinterpret_cast<float *>(smem + SM_BAR + 160);  // [NCONV <= 16]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + SM_BAR + 224);
+    static_assert(G::NCONV <= 16, "cmax slots");
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -924,21 +929,38 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                 mbar_wait(bar_rawfull, uc & 1);
                 if (ct == 0) FS_TRACE(0);
                 const int n4 = nrows * (TR / 4);
+                constexpr int Q = (((TN + SSH - 1) * (TR / 4)) + NT1 - 1) / NT1;
                 if (!interior) {
+                    // edge (or unaligned) window: every thread's loads in
+                    // flight at once (unrolled, non-coherent), then the
+                    // stores -- a loop of dependent load/store rounds took
+                    // ~14 us per window, on the critical path of the CTA
+                    // that owns the signal's first window
                     const float *xc = a.x + ch * a.ldx - a.x_base;
                     float4 *w4 = reinterpret_cast<float4 *>(smem + G::SM_RAW);
-                    for (int q = ct; q < n4; q += NT1) {
-                        const int64_t m = m0 + 4 * (int64_t)q;
-                        float v[4];
+                    constexpr int QB = 8;  // float4 per batch: 32 loads in flight per thread
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) v[e] = (m + e >= a.x_lo && m + e < a.x_hi) ? xc[m + e] : 0.0f;
-                        w4[q] = make_float4(v[0], v[1], v[2], v[3]);
+                    for (int k0 = 0; k0 < Q; k0 += QB) {
+                        float v[QB][4];
+#pragma unroll
+                        for (int k = 0; k < QB; ++k) {
+                            const int q = ct + NT1 * (k0 + k);
+                            const int64_t m = m0 + 4 * (int64_t)q;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                v[k][e] = (k0 + k < Q && q < n4 && m + e >= a.x_lo && m + e < a.x_hi)
+                                              ? __ldg(xc + m + e) : 0.0f;
+                        }
+#pragma unroll
+                        for (int k = 0; k < QB; ++k) {
+                            const int q = ct + NT1 * (k0 + k);
+                            if (k0 + k < Q && q < n4) w4[q] = make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
+                        }
                     }
                     conv_bar<NT1>(1);
                 }
                 // RAW -> registers (<= 33 float4 per thread), then RAW is free
                 // for the next window's copy while this unit converts
-                constexpr int Q = (((TN + SSH - 1) * (TR / 4)) + NT1 - 1) / NT1;
                 float4 r[Q];
                 float mx = 0.0f;
                 bool bad = false;
@@ -1040,15 +1062,28 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                         }
                     }
                 }
-            } else for (int it = ct; it < items; it += NCT) {
-                const int64_t m = m0 + (int64_t)(it >> 4) * TR + (it & 15) * 8;
-                const uint32_t off = ((uint32_t)(it & 15) * WROWS + (uint32_t)(it >> 4)) * 16;
-                {
-                    float v[8];
+            } else {
+                // edge (or unaligned) window: 4 items' loads in flight per
+                // round (non-coherent), then their stores
+                for (int it0 = ct; it0 < items; it0 += 4 * NCT) {
+                    float v[4][8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) v[e] = (m + e >= lo && m + e < hi) ? xc[m + e] : 0.0f;
-                    *reinterpret_cast<float4 *>(xhi + off) = make_float4(v[0], v[1], v[2], v[3]);
-                    *reinterpret_cast<float4 *>(xlo + off) = make_float4(v[4], v[5], v[6], v[7]);
+                    for (int k = 0; k < 4; ++k) {
+                        const int it = it0 + k * NCT;
+                        const int64_t m = m0 + (int64_t)(it >> 4) * TR + (it & 15) * 8;
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            v[k][e] = (it < items && m + e >= lo && m + e < hi) ? __ldg(xc + m + e) : 0.0f;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int it = it0 + k * NCT;
+                        if (it < items) {
+                            const uint32_t off = ((uint32_t)(it & 15) * WROWS + (uint32_t)(it >> 4)) * 16;
+                            *reinterpret_cast<float4 *>(xhi + off) = make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
+                            *reinterpret_cast<float4 *>(xlo + off) = make_float4(v[k][4], v[k][5], v[k][6], v[k][7]);
+                        }
+                    }
                 }
             }
             asm volatile("cp.async.commit_group;\n" ::);

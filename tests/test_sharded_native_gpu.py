@@ -50,19 +50,22 @@ def test_sharded_gather_device_and_more_devices_than_outputs():
         fir_sharded(x, h, devices=[99])
 
 
+@pytest.mark.parametrize("nh", [2_500, 1_501])
 @pytest.mark.parametrize("chunks", [1, 3, 7])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-def test_range_host_chunk_pipeline(chunks, dtype):
+def test_range_host_chunk_pipeline(chunks, dtype, nh):
     """sc_fir_range_host: output sub-ranges of a host signal, cut into chunks
     whose upload / FIR / download overlap; float64 ORDERED bit-exact, float32
-    FAST within the FP32 tolerance, pinned and pageable buffers alike."""
+    FAST within the FP32 tolerance, pinned and pageable buffers alike.  (In
+    float64, 1,501 taps run k_chain_small with a nonzero drive offset, drive
+    window and first output; 2,500 taps the windowed chain.)"""
     import torch
 
     from paper_2401_01607_b200 import _native as N
 
     rng = np.random.default_rng(chunks)
     x = rng.uniform(-1, 1, 70_001).astype(dtype)
-    h = rng.standard_normal(2_500).astype(dtype)
+    h = rng.standard_normal(nh).astype(dtype)
     ref = O.scatter_full(x, h)
     dt = N.dtype_code(dtype)
     mode = N.SC_MODE_FAST if dtype == np.float32 else N.SC_MODE_ORDERED
