@@ -164,6 +164,16 @@ __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// One elected lane of a converged warp (the lowest active: lane 0 here).
+// Issuing tcgen05.mma under elect.sync from a warp-wide loop lets ptxas keep
+// the descriptors in uniform registers; a lane-0-only loop made it wrap
+// every MMA in an elect / R2UR waterfall.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                  : "memory");
@@ -203,7 +213,7 @@ __global__ void __launch_bounds__(TcGeo<TNV>::THREADS, 1) k_tc_fir(TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     pdl_begin();
     if (*a.nonfinite) return;  // block-uniform: the FFMA kernel handles this input
-    const int warp = threadIdx.x >> 5;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform, provably
     const int lane = threadIdx.x & 31;
     const uint32_t sbase = smem_u32(smem);
     const uint32_t bar_xfull = sbase + SM_BAR + 0;
@@ -235,7 +245,7 @@ __global__ void __launch_bounds__(TcGeo<TNV>::THREADS, 1) k_tc_fir(TcArgs a) {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform for the MMA operands
 
     // Work unit u = (tile, split): the split's shift range [sb, se) of that
     // tile (splits > 1 only when tiles alone leave SMs idle, e.g. cfg3).
@@ -281,24 +291,27 @@ __global__ void __launch_bounds__(TcGeo<TNV>::THREADS, 1) k_tc_fir(TcArgs a) {
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ------------------------------------------------------------ MMA issuer
-            // Every H8 stage (8 shifts) accumulates into a fresh TMEM buffer
-            // (alternating), which the epilogue drains into FP32 registers.
-            // The tensor core's FP32 accumulation truncates; bounding each
-            // accumulator's chain to 8 shifts x 8 K-steps x 3 MMAs keeps the
-            // truncation drift ~1e-6 relative (it reached ~1.5e-3 over a full
-            // 262k-tap chain).
+        // ---------------------------------------------------------------- MMA issuer
+        // Every H8 stage (SSH shifts) accumulates into a fresh TMEM buffer
+        // (alternating), which the epilogue drains into FP32 registers.
+        // The tensor core's FP32 accumulation truncates; bounding each
+        // accumulator's chain to a stage of shifts x 8 K-steps x 3 MMAs keeps
+        // the truncation drift ~1e-6 relative (it reached ~1.5e-3 over a full
+        // 262k-tap chain).  The whole warp walks the schedule in 32-bit
+        // arithmetic and elect.sync issues (see elect_one): the descriptors
+        // stay in uniform registers, no per-MMA R2UR waterfall.
+        {
+            const int nsplit = (int)a.nsplit, sps = (int)a.sps, s8 = (int)a.s8, n_units = (int)a.n_units;
             uint32_t xw = 0, hsc = 0, dc = 0;
-            for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x) {
-                const int64_t tile = u / a.nsplit;
-                const int64_t sb = (u - tile * a.nsplit) * a.sps;
-                const int64_t se = sb + a.sps < a.s8 ? sb + a.sps : a.s8;
-                for (int64_t s0 = sb; s0 < se; s0 += WP) {
-                    const int64_t s1 = s0 + WP < se ? s0 + WP : se;
+            for (int u = (int)blockIdx.x; u < n_units; u += (int)gridDim.x) {
+                const int tile = u / nsplit;
+                const int sb = (u - tile * nsplit) * sps;
+                const int se = sb + sps < s8 ? sb + sps : s8;
+                for (int s0 = sb; s0 < se; s0 += WP) {
+                    const int s1 = s0 + WP < se ? s0 + WP : se;
                     mbar_wait(bar_xfull, xw & 1);
                     ++xw;
-                    for (int64_t sg = s0; sg < s1; sg += SSH) {
+                    for (int sg = s0; sg < s1; sg += SSH) {
                         const uint32_t slot = hsc % NHSLOT;
                         mbar_wait(bar_hfull + 8 * slot, (hsc / NHSLOT) & 1);
                         ++hsc;
@@ -309,30 +322,38 @@ __global__ void __launch_bounds__(TcGeo<TNV>::THREADS, 1) k_tc_fir(TcArgs a) {
                         uint32_t accumulate = 0;
 #pragma unroll 1
                         for (int ss = 0; ss < SSH; ++ss) {
-                            const int64_t s = sg + ss;
+                            const int s = sg + ss;
                             // A: T_s starts at group offset (SSH-1-ss)*KG inside the stage
                             const uint32_t a_hi = sbase + SM_HST + (slot * 2 + 0) * HST_PART + (SSH - 1 - ss) * KG * 128;
                             const uint32_t a_lo = a_hi + HST_PART;
                             // B: rows of shift s start WP + s0 - s rows into the window
                             const uint32_t b_hi = sbase + SM_XWIN + (uint32_t)(WP + s0 - s) * 16;
                             const uint32_t b_lo = b_hi + XWIN_PART;
+                            const uint64_t ah0 = sdesc(a_hi, 128, 128), al0 = sdesc(a_lo, 128, 128);
+                            const uint64_t bh0 = sdesc(b_hi, WROWS * 16, 128), bl0 = sdesc(b_lo, WROWS * 16, 128);
 #pragma unroll
                             for (int kk = 0; kk < KG / 2; ++kk) {
-                                const uint64_t ah = sdesc(a_hi + kk * 256, 128, 128);
-                                const uint64_t al = sdesc(a_lo + kk * 256, 128, 128);
-                                const uint64_t bh = sdesc(b_hi + kk * 2 * (WROWS * 16), WROWS * 16, 128);
-                                const uint64_t bl = sdesc(b_lo + kk * 2 * (WROWS * 16), WROWS * 16, 128);
-                                umma_f16(d_tmem, ah, bh, IDESC, accumulate);
+                                // descriptor start addresses are in 16-byte units (low bits)
+                                const uint64_t da = (uint64_t)((kk * 256) >> 4);
+                                const uint64_t db = (uint64_t)((kk * 2 * (WROWS * 16)) >> 4);
+                                if (elect_one()) {
+                                    umma_f16(d_tmem, ah0 + da, bh0 + db, IDESC, accumulate);
+                                    umma_f16(d_tmem, al0 + da, bh0 + db, IDESC, 1);
+                                    umma_f16(d_tmem, ah0 + da, bl0 + db, IDESC, 1);
+                                }
+                                __syncwarp();
                                 accumulate = 1;
-                                umma_f16(d_tmem, al, bh, IDESC, 1);
-                                umma_f16(d_tmem, ah, bl, IDESC, 1);
                             }
                         }
-                        umma_commit(bar_hempty + 8 * slot);
-                        umma_commit(bar_tfull + 8 * acc);
+                        if (elect_one()) {
+                            umma_commit(bar_hempty + 8 * slot);
+                            umma_commit(bar_tfull + 8 * acc);
+                        }
+                        __syncwarp();
                         ++dc;
                     }
-                    umma_commit(bar_xempty);
+                    if (elect_one()) umma_commit(bar_xempty);
+                    __syncwarp();
                 }
             }
         }
@@ -684,7 +705,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
     extern __shared__ __align__(1024) uint8_t smem[];
     pdl_begin();
     if (*a.flag) return;  // non-finite taps (found by the H8 build): the gated fallback computes the launch
-    const int warp = threadIdx.x >> 5;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform, provably
     const int lane = threadIdx.x & 31;
     const uint32_t sbase = smem_u32(smem);
     const uint32_t bar_xfull = sbase + SM_BAR + 0;    // + 8*slot
@@ -723,7 +744,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
     auto unit_of = [&](int64_t u, int64_t &tile, int64_t &sb, int64_t &se, int64_t &ch, int64_t &i0) {
         tile = u / a.nsplit;
@@ -782,23 +803,35 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ------------------------------------------------------------ MMA issuer
+        // ---------------------------------------------------------------- MMA issuer
+        // The whole warp walks the schedule (so the descriptors are
+        // warp-uniform values the compiler keeps in uniform registers) and
+        // lane 0 issues: a single-thread loop made ptxas wrap every
+        // tcgen05.mma in an elect / R2UR waterfall, ~110 clk per MMA against
+        // the 64-clk floor of an M128 x N128 x K16 MMA.
+        {
+            // 32-bit unit arithmetic (n_units < 2^31, checked at launch): a
+            // 64-bit division is a call whose results ptxas cannot treat as
+            // warp-uniform
+            const int nsplit = (int)a.nsplit, sps = (int)a.sps, s8 = (int)a.s8;
+            const int n_units = (int)a.n_units;
             uint32_t uc = 0, hsc = 0, dc = 0;
-            int64_t last_key = -1;
+            int last_key = -1;
             uint32_t slot = 0;
-            for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++uc) {
-                int64_t tile, sb, se, ch, i0;
-                unit_of(u, tile, sb, se, ch, i0);
+            for (int u = (int)blockIdx.x; u < n_units; u += (int)gridDim.x, ++uc) {
+                const int tile = u / nsplit;
+                const int sb = (u - tile * nsplit) * sps;
+                const int se = sb + sps < s8 ? sb + sps : s8;
+                const int ch = tile / (int)a.tiles_per_ch;
                 const uint32_t xs = uc & 1;
                 mbar_wait(bar_xfull + 8 * xs, (uc >> 1) & 1);
-                FS_TRACE(3);
-                for (int64_t sg = sb; sg < se; sg += SSH) {
-                    const int64_t key = ch * a.s8 + sg;
+                if (lane == 0) FS_TRACE(3);
+                for (int sg = sb; sg < se; sg += SSH) {
+                    const int key = ch * s8 + sg;
                     if (key != last_key) {
                         // leaving the previous stage: its slot is free once
                         // the MMAs issued so far complete
-                        if (hsc > 0) umma_commit(bar_hempty + 8 * slot);
+                        if (hsc > 0 && elect_one()) umma_commit(bar_hempty + 8 * slot);
                         last_key = key;
                         slot = hsc % NHSLOT;
                         mbar_wait(bar_hfull + 8 * slot, (hsc / NHSLOT) & 1);
@@ -811,29 +844,35 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                     uint32_t accumulate = 0;
 #pragma unroll 1
                     for (int ss = 0; ss < SSH; ++ss) {
-                        const int64_t s = sg + ss;
+                        const int s = sg + ss;
                         const uint32_t a_hi = sbase + SM_HST + (slot * 2 + 0) * HST_PART + (SSH - 1 - ss) * KG * 128;
                         const uint32_t a_lo = a_hi + HST_PART;
                         // output row i of shift s reads window row i + (se - 1 - s)
                         const uint32_t b_hi = sbase + (2 * xs) * XPART + (uint32_t)(se - 1 - s) * 16;
                         const uint32_t b_lo = b_hi + XPART;
+                        const uint64_t ah0 = sdesc(a_hi, 128, 128), al0 = sdesc(a_lo, 128, 128);
+                        const uint64_t bh0 = sdesc(b_hi, WROWS * 16, 128), bl0 = sdesc(b_lo, WROWS * 16, 128);
 #pragma unroll
                         for (int kk = 0; kk < KG / 2; ++kk) {
-                            const uint64_t ah = sdesc(a_hi + kk * 256, 128, 128);
-                            const uint64_t al = sdesc(a_lo + kk * 256, 128, 128);
-                            const uint64_t bh = sdesc(b_hi + kk * 2 * (WROWS * 16), WROWS * 16, 128);
-                            const uint64_t bl = sdesc(b_lo + kk * 2 * (WROWS * 16), WROWS * 16, 128);
-                            umma_f16(d_tmem, ah, bh, G::IDESC, accumulate);
+                            // descriptor start addresses are in 16-byte units (low bits)
+                            const uint64_t da = (uint64_t)((kk * 256) >> 4);
+                            const uint64_t db = (uint64_t)((kk * 2 * (WROWS * 16)) >> 4);
+                            if (elect_one()) {
+                                umma_f16(d_tmem, ah0 + da, bh0 + db, G::IDESC, accumulate);
+                                umma_f16(d_tmem, al0 + da, bh0 + db, G::IDESC, 1);
+                                umma_f16(d_tmem, ah0 + da, bl0 + db, G::IDESC, 1);
+                            }
+                            __syncwarp();
                             accumulate = 1;
-                            umma_f16(d_tmem, al, bh, G::IDESC, 1);
-                            umma_f16(d_tmem, ah, bl, G::IDESC, 1);
                         }
                     }
-                    umma_commit(bar_tfull + 8 * acc);
+                    if (elect_one()) umma_commit(bar_tfull + 8 * acc);
+                    __syncwarp();
                     ++dc;
                 }
-                umma_commit(bar_xempty + 8 * xs);
-                FS_TRACE(4);
+                if (elect_one()) umma_commit(bar_xempty + 8 * xs);
+                __syncwarp();
+                if (lane == 0) FS_TRACE(4);
             }
         }
     } else if (warp < 2 + NEPI) {
@@ -1240,6 +1279,7 @@ int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_
     const int64_t sps = cdiv(stages, nsplit) * SSH;
     nsplit = cdiv(s8, sps);
     a.nsplit = nsplit, a.sps = sps, a.n_units = n_tiles * nsplit;
+    SC_REQUIRE(a.n_units < (int64_t)INT32_MAX && a.s8 < (int64_t)INT32_MAX, "fir: too many work units");
     a.ws = nullptr;
     static const bool trace = getenv("SC_FS_TRACE") != nullptr;
     a.trace = nullptr;
@@ -1447,6 +1487,7 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     a.nsplit = nsplit;
     a.sps = sps;
     a.n_units = a.n_tiles * nsplit;
+    SC_REQUIRE(a.n_units < (int64_t)INT32_MAX && a.s8 < (int64_t)INT32_MAX, "fir: too many work units");
     a.ws = nullptr;
     if (nsplit > 1) {
         a.ws = static_cast<float *>(scratch(sizeof(float) * (size_t)n_len * channels * nsplit, 4, stream, &err));
