@@ -651,6 +651,7 @@ struct FsGeo {
     // ONE: the unit's FP32 window (TN + SSH - 1 rows, contiguous in x) is
     // staged row-major by one bulk copy into RAW, then converted into the slot
     static constexpr uint32_t RAW = ONE ? (uint32_t)(TN + SSH - 1) * TR * 4 : 0;
+    static constexpr int RAW_ROWS_A = 64;  // rows of RAW's first half (see the converters)
     static constexpr int WROWS_FIT = (int)((SMEM_MAX - 256 - RAW - NHSLOT * 2 * HST_PART) / (2 * 2 * KG * 16));
     static constexpr int WPF = ONE ? SSH : ((WROWS_FIT - 1 - TN) / 8) * 8;  // most shifts per unit
     // rows per window slot; WROWS = 1 (mod 8) puts the K-group stride at 16
@@ -715,8 +716,13 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
     const uint32_t bar_tfull = sbase + SM_BAR + 64;   // + 8*acc
     const uint32_t bar_tempty = sbase + SM_BAR + 80;  // + 8*acc
     const uint32_t bar_exfull = sbase + SM_BAR + 96;  // + 8*k, k = unit % 4
+    // RAW is filled and drained in two halves (rows [0, RAW_ROWS_A) and the
+    // rest), so the next window's first half is in flight while this one's
+    // second half is read
     const uint32_t bar_rawfull = sbase + SM_BAR + 128;
     const uint32_t bar_rawempty = sbase + SM_BAR + 136;
+    const uint32_t bar_rawfull2 = sbase + SM_BAR + 232;
+    const uint32_t bar_rawempty2 = sbase + SM_BAR + 240;
     int *ex_ring = reinterpret_cast<int *>(smem + SM_BAR + 144);   // [4]
     float *cmax = reinterpret_cast<float *>(smem + SM_BAR + 160);  // [NCONV <= 16]
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + SM_BAR + 224);
@@ -734,6 +740,8 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
         for (int k = 0; k < 4; ++k) mbar_init(bar_exfull + 8 * k, 1);
         mbar_init(bar_rawfull, 1);
         mbar_init(bar_rawempty, 1);
+        mbar_init(bar_rawfull2, 1);
+        mbar_init(bar_rawempty2, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -781,10 +789,18 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                     int nrows;
                     bool interior;
                     window_of(sb, se, ch, i0, m0, nrows, interior);
+                    const float *src = a.x + ch * a.ldx - a.x_base + m0;
+                    const int rows_a = nrows < G::RAW_ROWS_A ? nrows : G::RAW_ROWS_A;
                     if (rc > 0) mbar_wait(bar_rawempty, (rc - 1) & 1);
-                    const uint32_t bytes = interior ? (uint32_t)nrows * TR * 4 : 0;
-                    mbar_expect_tx(bar_rawfull, bytes);
-                    if (interior) bulk_g2s(sbase + G::SM_RAW, a.x + ch * a.ldx - a.x_base + m0, bytes, bar_rawfull);
+                    const uint32_t bytes_a = interior ? (uint32_t)rows_a * TR * 4 : 0;
+                    mbar_expect_tx(bar_rawfull, bytes_a);
+                    if (bytes_a) bulk_g2s(sbase + G::SM_RAW, src, bytes_a, bar_rawfull);
+                    if (rc > 0) mbar_wait(bar_rawempty2, (rc - 1) & 1);
+                    const uint32_t bytes_b = interior ? (uint32_t)(nrows - rows_a) * TR * 4 : 0;
+                    mbar_expect_tx(bar_rawfull2, bytes_b);
+                    if (bytes_b)
+                        bulk_g2s(sbase + G::SM_RAW + (uint32_t)rows_a * TR * 4, src + (int64_t)rows_a * TR, bytes_b,
+                                 bar_rawfull2);
                 }
                 const __half *h80 = a.h8[0] + ch * a.h8_ch, *h81 = a.h8[1] + ch * a.h8_ch;
                 for (int64_t sg = sb; sg < se; sg += SSH) {
@@ -969,7 +985,10 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                 if (ct == 0) FS_TRACE(0);
                 const int n4 = nrows * (TR / 4);
                 constexpr int Q = (((TN + SSH - 1) * (TR / 4)) + NT1 - 1) / NT1;
+                constexpr int QA = G::RAW_ROWS_A * (TR / 4) / NT1;  // float4 rounds in half A
+                static_assert(QA * NT1 == G::RAW_ROWS_A * (TR / 4) && QA < Q, "RAW halves");
                 if (!interior) {
+                    mbar_wait(bar_rawfull2, uc & 1);  // the previous window's half B is released too
                     // edge (or unaligned) window: every thread's loads in
                     // flight at once (unrolled, non-coherent), then the
                     // stores -- a loop of dependent load/store rounds took
@@ -1005,6 +1024,12 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                 bool bad = false;
 #pragma unroll
                 for (int k = 0; k < Q; ++k) {
+                    if (k == QA) {
+                        // half A read by every converter: release it, then half B
+                        conv_bar<NT1>(1);
+                        if (ct == 0) mbar_arrive(bar_rawempty);
+                        mbar_wait(bar_rawfull2, uc & 1);
+                    }
                     const int q = ct + NT1 * k;
                     r[k] = q < n4 ? raw4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
                     mx = fmaxf(mx, fmaxf(fmaxf(fabsf(r[k].x), fabsf(r[k].y)), fmaxf(fabsf(r[k].z), fabsf(r[k].w))));
@@ -1014,8 +1039,8 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                 for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
                 if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 1u);
                 if (lane == 0) cmax[cw] = mx;
-                conv_bar<NT1>(1);   // also: every thread has read RAW
-                if (ct == 0) mbar_arrive(bar_rawempty);
+                conv_bar<NT1>(1);   // also: every thread has read RAW half B
+                if (ct == 0) mbar_arrive(bar_rawempty2);
 #pragma unroll
                 for (int w = 0; w < G::NCONV; ++w) mx = fmaxf(mx, cmax[w]);
                 int ex = (mx > 0.0f && isfinite(mx)) ? 14 - ilogbf(mx) : 0;
@@ -1191,9 +1216,13 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
 // every CTA takes max |h_c| over the whole (short) IR itself, so no separate
 // max pass runs; CTA (0, c) publishes the exponent, non-finite taps raise
 // the fallback flag.
+// set_flag (one channel, no caller-owned flag): every CTA has seen all the
+// taps, so each STORES the same flag value (no memset launch before this
+// one); otherwise the flag is only raised (atomicOr).
 __global__ void __launch_bounds__(256) k_h8_fs(const float *__restrict__ h, int64_t ldh, int64_t nh, int64_t s8,
                                                int64_t ngroups, __half *__restrict__ h8_hi,
-                                               __half *__restrict__ h8_lo, int64_t h8_ch, int *eh, unsigned *flag) {
+                                               __half *__restrict__ h8_lo, int64_t h8_ch, int *eh, unsigned *flag,
+                                               bool set_flag) {
     pdl_begin();
     const int c = blockIdx.y;
     const float *hc = h + (int64_t)c * ldh;
@@ -1211,11 +1240,14 @@ __global__ void __launch_bounds__(256) k_h8_fs(const float *__restrict__ h, int6
     mx = wm[0];
     for (int w = 1; w < 8; ++w) mx = fmaxf(mx, wm[w]);
     int e = (mx > 0.0f && isfinite(mx)) ? 14 - ilogbf(mx) : 0;
-    if (e > 114) {  // taps this small leave the split's range: ordered fallback
-        if (threadIdx.x == 0) atomicOr(flag, 1u);
-        e = 0;
+    const bool small = e > 114;  // taps this small leave the split's range: ordered fallback
+    if (small) e = 0;
+    if (set_flag) {
+        if (threadIdx.x == 0) *flag = (bad || small) ? 1u : 0u;
+    } else {
+        if (small && threadIdx.x == 0) atomicOr(flag, 1u);
+        if (bad && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flag, 1u);
     }
-    if (bad && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flag, 1u);
     if (blockIdx.x == 0 && threadIdx.x == 0) eh[c] = e;
     build_h8_part(h, ldh, nh, s8, ngroups, __int_as_float((127 + e) << 23), h8_hi, h8_lo, h8_ch, blockIdx.x);
 }
@@ -1252,10 +1284,13 @@ int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_
     __half *h8_hi = reinterpret_cast<__half *>(ws + head);
     __half *h8_lo = h8_hi + h8_ch * channels;
     if (nonfinite_out) *nonfinite_out = flag;
-    if (!pre) SC_CHECK_CUDA(cudaMemsetAsync(flag, 0, 4, stream));
+    // one channel: k_h8_fs stores the flag itself (no memset node in the chain)
+    const bool set_flag = !pre && channels == 1;
+    if (!pre && !set_flag) SC_CHECK_CUDA(cudaMemsetAsync(flag, 0, 4, stream));
     {
         dim3 g((unsigned)cdiv(ngroups * 8, 256), (unsigned)channels);
-        SC_LAUNCH_PDL(k_h8_fs, g, dim3(256), 0, stream, h, ldh, nh, s8, ngroups, h8_hi, h8_lo, h8_ch, eh, flag);
+        SC_LAUNCH_PDL(k_h8_fs, g, dim3(256), 0, stream, h, ldh, nh, s8, ngroups, h8_hi, h8_lo, h8_ch, eh, flag,
+                      set_flag);
     }
     FsArgs a;
     a.x = x, a.ldx = ldx, a.x_base = x_base, a.x_lo = x_lo, a.x_hi = x_hi;
