@@ -286,15 +286,14 @@ class Work:
         capi.cu's FAST dispatch).  The tensor-core work it issues is read from
         the library itself (sc_tc_stats) around the timed region."""
         if self.cfg.startswith("short"):
-            # FAST dispatch (capi.cu / k_fast_f32.cu): tensor cores from 48
+            # FAST dispatch (capi.cu / k_fast_f32.cu): tensor cores from 26
             # taps at this size (the fused-split k_tc_fir_fs), the streaming
-            # k_fir_short up to 8 taps and the tap-stationary k_fir_tapreg up
-            # to 32 (HBM-bound), the smem k_fir_short_smem in between
-            # (FMA-bound).  Filters of at most two 128-tap shifts on tensor
+            # k_fir_short up to 8 taps and the tap-stationary k_fir_tapreg
+            # below 26 (HBM-bound).  Filters of at most two 128-tap shifts on tensor
             # cores are HBM-bound too: 2 shifts of MMAs take less than moving
             # 8 B per output
             nh = self.w.nh
-            use_tc = self.mode == "tc" or (self.mode in ("fast", "auto") and nh >= 48)
+            use_tc = self.mode == "tc" or (self.mode in ("fast", "auto") and nh >= 26)   # capi.cu kTcShortMinTaps
             self.kernel = "k_tc_fir" if use_tc else ("k_fir_short" if nh <= 8 else "k_fir_tapreg" if nh <= 32
                                                      else "k_fir_short_smem")
             self.hbm_bound = (nh <= 32 and not use_tc) or (use_tc and nh <= 255)

@@ -11,7 +11,7 @@ arithmetic runs in the CUDA library (csrc/), never on the host:
 * float32 signals (arrays or tensors; ``Signal`` keeps float32 instead of
   upcasting) use the FAST path, within 1e-5*max|x|*||h||_1 of the
   reference: the tcgen05 tensor-core FIR (fp16 hi/lo split, 3 MMAs) for
-  filters of >= 256 taps (>= 48 on large launches), the CUDA-core
+  filters of >= 256 taps (>= 26 on launches of >= 2^30 MACs), the CUDA-core
   short-filter kernels below that; ``mode="ffma"`` forces the FFMA2
   register-tiled kernel, ``mode="tc"`` the tensor cores, and
   ``mode="ordered"`` the ordered chain in float32.

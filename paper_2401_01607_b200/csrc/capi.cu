@@ -192,6 +192,8 @@ void *scratch(size_t bytes, int slot, cudaStream_t stream, int *err) {
     return b.p;
 }
 
+constexpr int64_t kTcShortMinTaps = 26;  // see launch_fir_f32
+
 int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
                    const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin,
                    int64_t n_end, int64_t channels, cudaStream_t stream, const TcPre *pre) {
@@ -199,13 +201,14 @@ int launch_fir_f32(int mode, const float *x, int64_t ldx, int64_t x_base, int64_
     if (mode == SC_MODE_TC) {
         tc = guard = true;
     } else if (mode == SC_MODE_FAST) {
-        // tensor cores from 256 taps; from 48 taps too when the launch is big
-        // enough to amortise their set-up: with the fused-split kernel
-        // (k_tc_fir_fs, no split image in HBM) 2^26 outputs take 0.19 ms at
-        // 64 or 128 taps, against 0.25 ms (64) on the CUDA-core short-filter
-        // kernel, whose time grows with the taps (crossover ~50)
+        // tensor cores from 256 taps; from 26 taps too when the launch is big
+        // enough to amortise their set-up: the fused-split kernel
+        // (k_tc_fir_fs, no split image in HBM) takes a flat ~0.12 ms for
+        // 2^26 outputs at any tap count up to 255 (HBM-bound), while the
+        // CUDA-core short-filter kernels grow ~2.5 us per tap from 0.095 ms
+        // at 16 taps (32 taps: 0.135 vs 0.120 ms on tensor cores)
         const double macs = (double)(n_end - n_begin) * (double)nh * (double)channels;
-        tc = g_fast_uses_tc && (tc_fir_supported(nh) || (nh >= 48 && macs >= 1073741824.0));
+        tc = g_fast_uses_tc && (tc_fir_supported(nh) || (nh >= kTcShortMinTaps && macs >= 1073741824.0));
         guard = tc;
     } else if (mode != SC_MODE_FFMA) {
         set_error("fir: bad mode %d", mode);
