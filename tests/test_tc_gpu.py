@@ -206,6 +206,22 @@ def test_fused_split_large_launch(nh):
     _fs_check(x, h, y)
 
 
+@pytest.mark.parametrize("nh", [26, 33, 47])
+def test_fused_split_short_filters_from_26_taps(nh):
+    """FAST dispatch takes the fused-split tensor cores from 26 taps on
+    launches of >= 2^30 MACs (capi.cu kTcShortMinTaps)."""
+    import torch
+
+    rng = np.random.default_rng(300 + nh)
+    ne = (1 << 30) // nh + 4_321
+    x = rng.uniform(-1, 1, ne).astype(np.float32)
+    h = rng.standard_normal(nh).astype(np.float32)
+    y = scatter_convolve(Signal(torch.from_numpy(x).cuda()), Signal(torch.from_numpy(h).cuda()))
+    y = y.concatenated().samples.cpu().numpy()
+    assert len(y) == ne + nh - 1
+    _fs_check(x, h, y)
+
+
 def test_fused_split_batched_channels_and_shards():
     import torch
 
@@ -245,3 +261,10 @@ def test_fused_split_nonfinite_falls_back():
         assert np.array_equal(np.isnan(got), np.isnan(ref)) and np.array_equal(np.isinf(got), np.isinf(ref)), s
         fin = np.isfinite(ref)
         assert np.max(np.abs(got[fin] - ref[fin]), initial=0) <= configs.tolerance(x[np.isfinite(x)], h, "f32")
+    # the next (finite) call of the same shape: the launch's flag starts clear
+    # again (one-channel launches store it in the H8 kernel, no memset)
+    x2 = rng.uniform(-1, 1, ne).astype(np.float32)
+    y2 = scatter_convolve(Signal(torch.from_numpy(x2).cuda()), Signal(torch.from_numpy(h).cuda()))
+    y2 = y2.concatenated().samples.cpu().numpy()
+    assert np.all(np.isfinite(y2))
+    _fs_check(x2, h, y2, seeds=2)
