@@ -134,6 +134,12 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
     // per chunk and warp: every staged drive sample and tap finite
     __shared__ unsigned xfin[2][CW_TB / 32];
     __shared__ __align__(16) T hs[2][HSP];
+    // A gated launch (run_if: the tensor-core path's non-finite fallback) is
+    // launched with programmatic stream serialisation: its CTAs become
+    // resident while the tensor-core kernel runs and wait here for it (a
+    // no-op for launches without the attribute), which hides this launch's
+    // ~3 us of set-up behind that kernel.
+    if (a.run_if) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (a.run_if && *a.run_if == 0) return;  // block-uniform
     // channel-local base pointers (the param struct stays in the constant bank)
     const T *xb = a.x + blockIdx.y * a.ldx;
@@ -382,12 +388,21 @@ __global__ void __launch_bounds__(CW_TB, (sizeof(T) == 4 ? 6 : 4) * (128 / CW_TB
 
 template <typename T, int SKIP, bool FUSED, int TB>
 int launch_chain_rf(int R, dim3 grid, cudaStream_t stream, const ChainArgs<T> &a) {
+    auto go = [&](auto kern) -> cudaError_t {
+        if (!a.run_if) {
+            kern<<<grid, TB, 0, stream>>>(a);
+            return cudaGetLastError();
+        }
+        return launch_pdl(kern, grid, dim3(TB), 0, stream, a);  // gated: see k_chain_w
+    };
+    cudaError_t e;
     switch (R) {
-        case 8: k_chain_w<T, SKIP, 8, FUSED, TB><<<grid, TB, 0, stream>>>(a); break;
-        case 4: k_chain_w<T, SKIP, 4, FUSED, TB><<<grid, TB, 0, stream>>>(a); break;
-        case 2: k_chain_w<T, SKIP, 2, FUSED, TB><<<grid, TB, 0, stream>>>(a); break;
-        default: k_chain_w<T, SKIP, 1, FUSED, TB><<<grid, TB, 0, stream>>>(a); break;
+        case 8: e = go(k_chain_w<T, SKIP, 8, FUSED, TB>); break;
+        case 4: e = go(k_chain_w<T, SKIP, 4, FUSED, TB>); break;
+        case 2: e = go(k_chain_w<T, SKIP, 2, FUSED, TB>); break;
+        default: e = go(k_chain_w<T, SKIP, 1, FUSED, TB>); break;
     }
+    SC_REQUIRE(e == cudaSuccess, "chain: kernel launch failed: %s", cudaGetErrorString(e));
     return SC_OK;
 }
 
