@@ -416,7 +416,8 @@ class ScatterEngine:
         that much earlier).  None when any of it differs."""
         f_nb, f_len, f_dtype, f_dev, f_keep, args, note = fp
         t = _dev.torch()
-        if (nb != f_nb or type(x) is not t.Tensor or x.dtype is not f_dtype or x.dim() != 1
+        if (nb != f_nb or type(x) is not t.Tensor or type(swaps) not in (list, tuple)
+                or x.dtype is not f_dtype or x.dim() != 1
                 or x.shape[0] != f_len or not x.is_cuda or x.get_device() != f_dev or not x.is_contiguous()
                 or len(swaps) != len(f_keep) or not all(map(_is, swaps, f_keep))):
             return None

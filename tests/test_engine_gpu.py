@@ -441,3 +441,45 @@ def test_repeated_process_stream_replays_graph_identically(dtype):
     if dtype == np.float64 or eng.mode == "ordered":
         assert np.array_equal(np.concatenate(pieces), results[0][0])
         assert np.array_equal(want_tail, results[0][1])
+
+
+def test_process_stream_repeat_calls_follow_schedule_changes():
+    """process_stream's repeat-call fast path (engine.py _process_stream_fast)
+    must only reuse the cached schedule when the caller passes the very same
+    (block, IR) tuples: an edited list, an iterator and a pending deferred
+    swap all take the full path.  Checked bit for bit (float64, ordered)
+    against an engine driven block by block (swap_ir + process_block)."""
+    import torch
+
+    from paper_2401_01607_b200.core import Signal
+    from paper_2401_01607_b200.engine import EngineConfig, ScatterEngine
+
+    rng = np.random.default_rng(31)
+    nb, n = 64, 64 * 20
+    x = torch.from_numpy(rng.uniform(-1, 1, n)).cuda()
+    irs = [torch.from_numpy(rng.standard_normal(k)).cuda() for k in (40, 90, 17)]
+    eng = ScatterEngine(Signal(irs[0]), EngineConfig(block_size_nb=nb))
+    ref = ScatterEngine(Signal(irs[0]), EngineConfig(block_size_nb=nb))
+
+    def ref_stream(sw):
+        out = []
+        for b in range(n // nb):
+            for blk, ir in sw:
+                if blk == b:
+                    ref.swap_ir(Signal(ir))
+            out.append(ref.process_block(Signal(x[b * nb:(b + 1) * nb])).samples.cpu().numpy())
+        return np.concatenate(out)
+
+    swaps = [(0, irs[1]), (5, irs[2])]
+    for call in range(6):
+        sw = swaps
+        if call == 2:
+            swaps[1] = (5, irs[0])          # same list object, one tuple replaced
+        if call == 3:
+            sw = iter(swaps)                 # an iterator, not a list
+        if call == 4:
+            eng.swap_ir_at_next_block(Signal(irs[2]))
+            ref.swap_ir_at_next_block(Signal(irs[2]))
+        got = eng.process_stream(x, nb, sw).cpu().numpy()
+        assert np.array_equal(got, ref_stream(swaps)), call
+    assert np.array_equal(eng.flush().samples.cpu().numpy(), ref.flush().samples.cpu().numpy())
