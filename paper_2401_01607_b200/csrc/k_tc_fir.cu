@@ -44,6 +44,9 @@
 
 #include <algorithm>
 
+#include <map>
+#include <mutex>
+
 #include "sc_common.cuh"
 
 namespace sc {
@@ -680,7 +683,31 @@ struct FsArgs {
     float *ws;
     unsigned *flag;
     unsigned long long *trace;  // debug (SC_FS_TRACE): per CTA 0 unit timestamps
+    // fold (one-stage, one channel): the kernel builds its H8 stage from the
+    // taps itself and runs the non-finite fallback after a grid barrier
+    int fold;
+    const float *h;
+    int64_t nh;
+    unsigned long long *gbar;  // grid barrier word (generation << 32 | arrivals)
 };
+
+// Sense-reversing grid barrier for a cooperative (co-resident) grid: the
+// last arrival clears the count and bumps the generation the others wait on.
+__device__ __forceinline__ void fs_grid_barrier(unsigned long long *w) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long old = atomicAdd(w, 1ull);
+        const unsigned gen = (unsigned)(old >> 32);
+        if ((unsigned)(old & 0xffffffffull) + 1u == gridDim.x) {
+            atomicExch(w, (unsigned long long)(gen + 1u) << 32);
+        } else {
+            while ((unsigned)(atomicAdd(w, 0ull) >> 32) == gen) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
 
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -705,7 +732,8 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
     constexpr int64_t TTILE = (int64_t)TR * TN;
     extern __shared__ __align__(1024) uint8_t smem[];
     pdl_begin();
-    if (*a.flag) return;  // non-finite taps (found by the H8 build): the gated fallback computes the launch
+    // non-finite taps (found by the H8 build): the gated fallback computes the launch
+    if (!(ONE && a.fold) && *a.flag) return;
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform, provably
     const int lane = threadIdx.x & 31;
     const uint32_t sbase = smem_u32(smem);
@@ -754,6 +782,56 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
     tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
+    // fold: every warp takes max |h| over the (<= 255) taps itself, the CTA
+    // builds H8 stage 0 in slot 0 (what k_h8_fs + the producer's bulk copy
+    // would have put there), and taps that are non-finite or too small skip
+    // straight to the fallback
+    bool fold_skip = false;
+    int fold_eh = 0;
+    if constexpr (ONE) {
+        if (a.fold) {
+            float mx = 0.0f;
+            bool bad = false;
+            for (int64_t k = lane; k < a.nh; k += 32) {
+                const float v = a.h[k];
+                mx = fmaxf(mx, fabsf(v));
+                bad |= !isfinite(v);
+            }
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            bad = __any_sync(0xffffffffu, bad);
+            int e = (mx > 0.0f && isfinite(mx)) ? 14 - ilogbf(mx) : 0;
+            const bool small = e > 114;
+            if (small) e = 0;
+            fold_eh = e;
+            fold_skip = bad || small;
+            if (fold_skip) {
+                if (threadIdx.x == 0) atomicOr(a.flag, 1u);
+            } else {
+                const float sc = __int_as_float((127 + e) << 23);
+                const int64_t cc = (int64_t)TR * a.s8 - 1;
+                for (int idx = threadIdx.x; idx < G::SGROUPS * 8; idx += blockDim.x) {
+                    const int g = idx >> 3, b = idx & 7;
+                    __align__(16) __half hv[8], lv[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int64_t k = cc - 8 * g - b - q;
+                        const float v = (k >= 0 && k < a.nh) ? a.h[k] * sc : 0.0f;
+                        split16(v, hv[q], lv[q]);
+                    }
+                    *reinterpret_cast<uint4 *>(smem + SM_HST + idx * 16) = *reinterpret_cast<const uint4 *>(hv);
+                    *reinterpret_cast<uint4 *>(smem + SM_HST + HST_PART + idx * 16) =
+                        *reinterpret_cast<const uint4 *>(lv);
+                }
+                // generic-proxy stores -> visible to the tensor core's async proxy
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            __syncthreads();
+            if (threadIdx.x == 0 && !fold_skip) mbar_arrive(bar_hfull);  // slot 0 holds stage 0
+        }
+    }
+    const int64_t NU = fold_skip ? 0 : a.n_units;
+    auto EH = [&](int64_t ch) { return (ONE && a.fold) ? fold_eh : a.eh[ch]; };
+
     auto unit_of = [&](int64_t u, int64_t &tile, int64_t &sb, int64_t &se, int64_t &ch, int64_t &i0) {
         tile = u / a.nsplit;
         sb = (u - tile * a.nsplit) * a.sps;
@@ -779,7 +857,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             // loaded again -- the MMA warp keeps using it.
             uint32_t hsc = 0, rc = 0;
             int64_t last_key = -1;
-            for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++rc) {
+            for (int64_t u = blockIdx.x; u < NU; u += gridDim.x, ++rc) {
                 int64_t tile, sb, se, ch, i0;
                 unit_of(u, tile, sb, se, ch, i0);
                 if constexpr (ONE) {
@@ -802,6 +880,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                         bulk_g2s(sbase + G::SM_RAW + (uint32_t)rows_a * TR * 4, src + (int64_t)rows_a * TR, bytes_b,
                                  bar_rawfull2);
                 }
+                if (ONE && a.fold) continue;  // stage 0 was built in slot 0 by the CTA
                 const __half *h80 = a.h8[0] + ch * a.h8_ch, *h81 = a.h8[1] + ch * a.h8_ch;
                 for (int64_t sg = sb; sg < se; sg += SSH) {
                     const int64_t key = ch * a.s8 + sg;
@@ -830,7 +909,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             // 64-bit division is a call whose results ptxas cannot treat as
             // warp-uniform
             const int nsplit = (int)a.nsplit, sps = (int)a.sps, s8 = (int)a.s8;
-            const int n_units = (int)a.n_units;
+            const int n_units = (int)NU;
             uint32_t uc = 0, hsc = 0, dc = 0;
             int last_key = -1;
             uint32_t slot = 0;
@@ -896,7 +975,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
         const int q = warp & 3;          // TMEM lane quarter
         const int rp = q * 32 + lane;    // phase r' = 127 - r
         uint32_t dc = 0, uc = 0;
-        for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++uc) {
+        for (int64_t u = blockIdx.x; u < NU; u += gridDim.x, ++uc) {
             int64_t tile, sb, se, ch, i0;
             unit_of(u, tile, sb, se, ch, i0);
             const int64_t sp = u - tile * a.nsplit;
@@ -906,7 +985,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             if constexpr (ONE) {
                 // one stage: the unit's x scale first, then stream the accumulator out
                 mbar_wait(bar_exfull + 8 * (uc & 3), (uc >> 2) & 1);
-                const int e = ex_ring[uc & 3] + a.eh[ch];
+                const int e = ex_ring[uc & 3] + EH(ch);
                 const float inv = __int_as_float((127 - e) << 23);
                 const uint32_t acc = dc & 1;
                 mbar_wait(bar_tfull + 8 * acc, (dc >> 1) & 1);
@@ -952,7 +1031,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             }
             // the unit's x scale (written by the converters before this arrive)
             mbar_wait(bar_exfull + 8 * (uc & 3), (uc >> 2) & 1);
-            const int e = ex_ring[uc & 3] + a.eh[ch];
+            const int e = ex_ring[uc & 3] + EH(ch);
             const float inv = __int_as_float((127 - e) << 23);  // 2^-e, |e| <= 126 (checked)
 #pragma unroll
             for (int i = 0; i < TN; ++i) {
@@ -974,7 +1053,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             const int cw = ct >> 5;
             const float4 *raw4 = reinterpret_cast<const float4 *>(smem + G::SM_RAW);
             uint32_t uc = 0;
-            for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++uc) {
+            for (int64_t u = blockIdx.x; u < NU; u += gridDim.x, ++uc) {
                 int64_t tile, sb, se, ch, i0, m0;
                 int nrows;
                 bool interior;
@@ -1044,7 +1123,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
 #pragma unroll
                 for (int w = 0; w < G::NCONV; ++w) mx = fmaxf(mx, cmax[w]);
                 int ex = (mx > 0.0f && isfinite(mx)) ? 14 - ilogbf(mx) : 0;
-                const int e_tot = ex + a.eh[ch];
+                const int e_tot = ex + EH(ch);
                 if (ex > 114 || e_tot > 126 || e_tot < -126) {
                     if (ct == 0) atomicOr(a.flag, 1u);
                     ex = 0;
@@ -1093,7 +1172,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
         const int cw = ct >> 5;
         float *gmax = cmax + 4 * cg;
         uint32_t uc = 0;
-        for (int64_t u = blockIdx.x; u < a.n_units; u += gridDim.x, ++uc) {
+        for (int64_t u = blockIdx.x; u < NU; u += gridDim.x, ++uc) {
             if ((int)(uc % NGRP) != cg) continue;
             int64_t tile, sb, se, ch, i0;
             unit_of(u, tile, sb, se, ch, i0);
@@ -1175,7 +1254,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             // scales (or the unscale with the taps' exponent) leaving float
             // range raise the fallback flag (the gated ordered launch)
             int ex = (mx > 0.0f && isfinite(mx)) ? 14 - ilogbf(mx) : 0;
-            const int e_tot = ex + a.eh[ch];
+            const int e_tot = ex + EH(ch);
             if (ex > 114 || e_tot > 126 || e_tot < -126) {
                 if (ct == 0) atomicOr(a.flag, 1u);
                 ex = 0;
@@ -1209,6 +1288,30 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
     if (warp == 0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(2 * TN)));
+    }
+    if constexpr (ONE) {
+        if (a.fold) {
+            // Every unit is written (and every non-finite sample has raised
+            // the flag) once the whole grid is here.  Flagged launches then
+            // recompute every output as the ordered FP32 chain -- the
+            // reference's (m, k) pairs in ascending m, one fused multiply-add
+            // each, exactly the gated k_chain_w launch this replaces -- and
+            // clear the flag for the next launch.
+            fs_grid_barrier(a.gbar);
+            if (*reinterpret_cast<volatile unsigned *>(a.flag)) {
+                const float *xc = a.x - a.x_base;
+                for (int64_t n = a.n_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < a.n_end;
+                     n += (int64_t)gridDim.x * blockDim.x) {
+                    const int64_t m_lo = n - a.nh + 1 > a.x_lo ? n - a.nh + 1 : a.x_lo;
+                    const int64_t m_hi = n + 1 < a.x_hi ? n + 1 : a.x_hi;
+                    float acc = 0.0f;
+                    for (int64_t m = m_lo; m < m_hi; ++m) acc = __fmaf_rn(xc[m], a.h[n - m], acc);
+                    a.y[n - a.n_begin] = acc;
+                }
+                fs_grid_barrier(a.gbar);
+                if (blockIdx.x == 0 && threadIdx.x == 0) *a.flag = 0u;
+            }
+        }
     }
 }
 
@@ -1254,6 +1357,34 @@ __global__ void __launch_bounds__(256) k_h8_fs(const float *__restrict__ h, int6
 
 }  // namespace
 
+// Fold control words (non-finite flag, grid-barrier word) of one (device,
+// stream): zeroed once at creation; every folded launch leaves them clear.
+struct FsCtl {
+    unsigned flag, pad;
+    unsigned long long gbar;
+};
+
+FsCtl *fs_ctl(cudaStream_t stream, int *err) {
+    static std::mutex mu;
+    static std::map<std::pair<int, uintptr_t>, FsCtl *> ctls;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    FsCtl *&c = ctls[std::make_pair(dev, reinterpret_cast<uintptr_t>(stream))];
+    if (!c) {
+        void *p = nullptr;
+        if (cudaMalloc(&p, sizeof(FsCtl)) != cudaSuccess || cudaMemsetAsync(p, 0, sizeof(FsCtl), stream) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("fir: fold control block allocation failed");
+            *err = SC_ERR_ALLOC;
+            return nullptr;
+        }
+        c = static_cast<FsCtl *>(p);
+    }
+    *err = 0;
+    return c;
+}
+
 // Fused-split launch (see k_tc_fir_fs); returns SC_ERR_STATE when the filter
 // has more shifts than one window holds (the image path then runs).
 int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi, const float *h,
@@ -1274,29 +1405,6 @@ int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_
     const int64_t h8_ch = ngroups * 64;
     const int64_t tiles_per_ch = cdiv(n_len, (int64_t)TR * G::TN);
     const int64_t n_tiles = tiles_per_ch * channels;
-    // scratch: [flag u32 | eh i32 x C] [h8 hi | h8 lo]
-    const size_t head = (size_t)cdiv(4 * channels + 64, 256) * 256;
-    int err = 0;
-    char *ws = static_cast<char *>(scratch(head + 2 * (size_t)h8_ch * channels * 2 + 1024, 3, stream, &err));
-    if (err) return err;
-    unsigned *flag = pre ? pre->flag : reinterpret_cast<unsigned *>(ws);
-    int *eh = reinterpret_cast<int *>(ws + 16);
-    __half *h8_hi = reinterpret_cast<__half *>(ws + head);
-    __half *h8_lo = h8_hi + h8_ch * channels;
-    if (nonfinite_out) *nonfinite_out = flag;
-    // one channel: k_h8_fs stores the flag itself (no memset node in the chain)
-    const bool set_flag = !pre && channels == 1;
-    if (!pre && !set_flag) SC_CHECK_CUDA(cudaMemsetAsync(flag, 0, 4, stream));
-    {
-        dim3 g((unsigned)cdiv(ngroups * 8, 256), (unsigned)channels);
-        SC_LAUNCH_PDL(k_h8_fs, g, dim3(256), 0, stream, h, ldh, nh, s8, ngroups, h8_hi, h8_lo, h8_ch, eh, flag,
-                      set_flag);
-    }
-    FsArgs a;
-    a.x = x, a.ldx = ldx, a.x_base = x_base, a.x_lo = x_lo, a.x_hi = x_hi;
-    a.h8[0] = h8_hi, a.h8[1] = h8_lo, a.h8_ch = h8_ch, a.eh = eh;
-    a.s8 = s8, a.tiles_per_ch = tiles_per_ch, a.n_tiles = n_tiles, a.n_begin = n_begin, a.n_end = n_end;
-    a.channels = channels, a.y = y, a.ldy = ldy, a.flag = flag;
     // shift-range splits when the tiles leave SMs idle (fixed-order reduce)
     const int sms = sm_count();
     const int64_t stages = s8 / SSH;
@@ -1313,6 +1421,79 @@ int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_
     }
     const int64_t sps = cdiv(stages, nsplit) * SSH;
     nsplit = cdiv(s8, sps);
+    // One-stage, one-channel launches fold the H8 build and the non-finite
+    // fallback into the tensor-core kernel (one launch instead of three;
+    // a cooperative launch, for the grid barrier before the fallback).
+    // SC_FS_FOLD=0 keeps the three launches.
+    static const bool fold_on = [] {
+        const char *v = getenv("SC_FS_FOLD");
+        return !(v && atoi(v) == 0);
+    }();
+    const bool one = nsplit == 1 && s8 == SSH;
+    bool fold = fold_on && one && channels == 1 && !pre && !getenv("SC_FS_TRACE");
+    FsArgs a;
+    a.fold = 0, a.h = h, a.nh = nh, a.gbar = nullptr;
+    int err = 0;
+    if (fold) {
+        FsCtl *ctl = fs_ctl(stream, &err);
+        if (err) return err;
+        if (nonfinite_out) *nonfinite_out = &ctl->flag;
+        if (fallback_folded) *fallback_folded = true;
+        a.x = x, a.ldx = ldx, a.x_base = x_base, a.x_lo = x_lo, a.x_hi = x_hi;
+        a.h8[0] = a.h8[1] = nullptr, a.h8_ch = 0, a.eh = nullptr;
+        a.s8 = s8, a.tiles_per_ch = tiles_per_ch, a.n_tiles = n_tiles, a.n_begin = n_begin, a.n_end = n_end;
+        a.channels = channels, a.y = y, a.ldy = ldy, a.flag = &ctl->flag;
+        a.nsplit = nsplit, a.sps = sps, a.n_units = n_tiles * nsplit;
+        SC_REQUIRE(a.n_units < (int64_t)INT32_MAX, "fir: too many work units");
+        a.ws = nullptr, a.trace = nullptr, a.fold = 1, a.gbar = &ctl->gbar;
+        using G1 = FsGeo<SSH, true>;
+        SC_CHECK_CUDA(cudaFuncSetAttribute(k_tc_fir_fs<SSH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           G1::SM_TOTAL));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)std::min<int64_t>(a.n_units, sms));
+        cfg.blockDim = dim3(G1::THREADS);
+        cfg.dynamicSmemBytes = G1::SM_TOTAL;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        at[1].id = cudaLaunchAttributeCooperative;
+        at[1].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        const cudaError_t le = cudaLaunchKernelEx(&cfg, k_tc_fir_fs<SSH, true>, a);
+        if (le == cudaSuccess) {
+            note_launch();
+            note_tc_launch(SSH, G::TN, n_tiles * (int64_t)TR * G::TN * (int64_t)TR * s8);
+            return SC_OK;
+        }
+        // the grid cannot be co-resident here (e.g. a partitioned device):
+        // the three-launch form below
+        cudaGetLastError();
+        if (fallback_folded) *fallback_folded = false;
+        a.fold = 0;
+    }
+    // scratch: [flag u32 | eh i32 x C] [h8 hi | h8 lo]
+    const size_t head = (size_t)cdiv(4 * channels + 64, 256) * 256;
+    char *ws = static_cast<char *>(scratch(head + 2 * (size_t)h8_ch * channels * 2 + 1024, 3, stream, &err));
+    if (err) return err;
+    unsigned *flag = pre ? pre->flag : reinterpret_cast<unsigned *>(ws);
+    int *eh = reinterpret_cast<int *>(ws + 16);
+    __half *h8_hi = reinterpret_cast<__half *>(ws + head);
+    __half *h8_lo = h8_hi + h8_ch * channels;
+    if (nonfinite_out) *nonfinite_out = flag;
+    // one channel: k_h8_fs stores the flag itself (no memset node in the chain)
+    const bool set_flag = !pre && channels == 1;
+    if (!pre && !set_flag) SC_CHECK_CUDA(cudaMemsetAsync(flag, 0, 4, stream));
+    {
+        dim3 g((unsigned)cdiv(ngroups * 8, 256), (unsigned)channels);
+        SC_LAUNCH_PDL(k_h8_fs, g, dim3(256), 0, stream, h, ldh, nh, s8, ngroups, h8_hi, h8_lo, h8_ch, eh, flag,
+                      set_flag);
+    }
+    a.x = x, a.ldx = ldx, a.x_base = x_base, a.x_lo = x_lo, a.x_hi = x_hi;
+    a.h8[0] = h8_hi, a.h8[1] = h8_lo, a.h8_ch = h8_ch, a.eh = eh;
+    a.s8 = s8, a.tiles_per_ch = tiles_per_ch, a.n_tiles = n_tiles, a.n_begin = n_begin, a.n_end = n_end;
+    a.channels = channels, a.y = y, a.ldy = ldy, a.flag = flag;
     a.nsplit = nsplit, a.sps = sps, a.n_units = n_tiles * nsplit;
     SC_REQUIRE(a.n_units < (int64_t)INT32_MAX && a.s8 < (int64_t)INT32_MAX, "fir: too many work units");
     a.ws = nullptr;
