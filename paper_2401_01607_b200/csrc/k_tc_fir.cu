@@ -848,6 +848,21 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
         interior = m0 >= a.x_lo && m0 + (int64_t)nrows * TR <= a.x_hi &&
                    ((reinterpret_cast<uintptr_t>(xc + m0) & 15) == 0);
     };
+    // Rows [r_lo, r_hi) of a window lie wholly inside [x_lo, x_hi): the one-
+    // stage path bulk-copies them even in an edge window (16-byte aligned
+    // rows only) and the converters fill just the rest.
+    auto bulk_rows = [&](int64_t ch, int64_t m0, int nrows, int &r_lo, int &r_hi) {
+        const float *xc = a.x + ch * a.ldx - a.x_base;
+        if ((reinterpret_cast<uintptr_t>(xc + m0) & 15) != 0) {
+            r_lo = r_hi = 0;
+            return;
+        }
+        const int64_t lo = a.x_lo - m0 > 0 ? (a.x_lo - m0 + TR - 1) / TR : 0;
+        const int64_t hi = a.x_hi - m0 >= 0 ? (a.x_hi - m0) / TR : 0;
+        r_lo = (int)(lo < nrows ? lo : nrows);
+        r_hi = (int)(hi < nrows ? hi : nrows);
+        if (r_hi < r_lo) r_hi = r_lo;
+    };
 
     if (warp == 0) {
         if (lane == 0) {
@@ -869,15 +884,22 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                     window_of(sb, se, ch, i0, m0, nrows, interior);
                     const float *src = a.x + ch * a.ldx - a.x_base + m0;
                     const int rows_a = nrows < G::RAW_ROWS_A ? nrows : G::RAW_ROWS_A;
+                    int r_lo = 0, r_hi = nrows;  // bulk-copied rows
+                    if (!interior) bulk_rows(ch, m0, nrows, r_lo, r_hi);
+                    // half A: rows [0, rows_a), half B: [rows_a, nrows)
+                    const int a0 = r_lo, a1 = r_hi < rows_a ? r_hi : rows_a;
+                    const int b0 = r_lo > rows_a ? r_lo : rows_a, b1 = r_hi;
                     if (rc > 0) mbar_wait(bar_rawempty, (rc - 1) & 1);
-                    const uint32_t bytes_a = interior ? (uint32_t)rows_a * TR * 4 : 0;
+                    const uint32_t bytes_a = a1 > a0 ? (uint32_t)(a1 - a0) * TR * 4 : 0;
                     mbar_expect_tx(bar_rawfull, bytes_a);
-                    if (bytes_a) bulk_g2s(sbase + G::SM_RAW, src, bytes_a, bar_rawfull);
+                    if (bytes_a)
+                        bulk_g2s(sbase + G::SM_RAW + (uint32_t)a0 * TR * 4, src + (int64_t)a0 * TR, bytes_a,
+                                 bar_rawfull);
                     if (rc > 0) mbar_wait(bar_rawempty2, (rc - 1) & 1);
-                    const uint32_t bytes_b = interior ? (uint32_t)(nrows - rows_a) * TR * 4 : 0;
+                    const uint32_t bytes_b = b1 > b0 ? (uint32_t)(b1 - b0) * TR * 4 : 0;
                     mbar_expect_tx(bar_rawfull2, bytes_b);
                     if (bytes_b)
-                        bulk_g2s(sbase + G::SM_RAW + (uint32_t)rows_a * TR * 4, src + (int64_t)rows_a * TR, bytes_b,
+                        bulk_g2s(sbase + G::SM_RAW + (uint32_t)b0 * TR * 4, src + (int64_t)b0 * TR, bytes_b,
                                  bar_rawfull2);
                 }
                 if (ONE && a.fold) continue;  // stage 0 was built in slot 0 by the CTA
@@ -1068,6 +1090,9 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                 static_assert(QA * NT1 == G::RAW_ROWS_A * (TR / 4) && QA < Q, "RAW halves");
                 if (!interior) {
                     mbar_wait(bar_rawfull2, uc & 1);  // the previous window's half B is released too
+                    int r_lo, r_hi;                   // rows the producer bulk-copied (see bulk_rows)
+                    bulk_rows(ch, m0, nrows, r_lo, r_hi);
+                    const int q_lo = r_lo * (TR / 4), q_hi = r_hi * (TR / 4);
                     // edge (or unaligned) window: every thread's loads in
                     // flight at once (unrolled, non-coherent), then the
                     // stores -- a loop of dependent load/store rounds took
@@ -1085,13 +1110,15 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                             const int64_t m = m0 + 4 * (int64_t)q;
 #pragma unroll
                             for (int e = 0; e < 4; ++e)
-                                v[k][e] = (k0 + k < Q && q < n4 && m + e >= a.x_lo && m + e < a.x_hi)
+                                v[k][e] = (k0 + k < Q && q < n4 && (q < q_lo || q >= q_hi) && m + e >= a.x_lo &&
+                                       m + e < a.x_hi)
                                               ? __ldg(xc + m + e) : 0.0f;
                         }
 #pragma unroll
                         for (int k = 0; k < QB; ++k) {
                             const int q = ct + NT1 * (k0 + k);
-                            if (k0 + k < Q && q < n4) w4[q] = make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
+                            if (k0 + k < Q && q < n4 && (q < q_lo || q >= q_hi))
+                                w4[q] = make_float4(v[k][0], v[k][1], v[k][2], v[k][3]);
                         }
                     }
                     conv_bar<NT1>(1);
