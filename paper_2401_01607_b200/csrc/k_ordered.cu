@@ -459,10 +459,12 @@ int pick_r(int64_t n_out, int64_t channels, size_t es) {
 // ~83 chains per SM sub-partition, so the time per step is set by how many
 // chains share a sub-partition's 16-lane FP64 pipe and by how well one warp
 // hides its own latencies.  Measured (tools/ubench/chain_small.cu): 3
-// consecutive outputs per thread in one-warp CTAs (96 chains per warp, at
-// most one warp per sub-partition at cfg1) beat 2 (two warps on some
-// sub-partitions) and 4 (idle sub-partitions); k_chain_w's chunked,
-// windowed form took 22.6 us at cfg1.
+// consecutive outputs per thread (96 chains per warp) beat 2 (two warps on
+// some sub-partitions) and 4 (idle sub-partitions); 4-warp CTAs (one warp
+// per sub-partition of the SM that holds the CTA; cfg1: 128 CTAs) beat 1-
+// and 3-warp CTAs (cfg1 per bench step: 15.5 vs 16.6 and 22.4 us; large
+// launches 1-3 % faster too); k_chain_w's chunked, windowed form took
+// 22.6 us at cfg1.
 //
 // Every output t runs one chain over a fixed step count nhp = nh rounded up
 // to 8: step j takes drive sample m = t - nhp + 1 + j and tap hs[nhp-1-j]
@@ -480,7 +482,7 @@ int pick_r(int64_t n_out, int64_t channels, size_t es) {
 // chunks so the chain could start earlier measured slower: the first chunk
 // landed later than the whole window does in one transfer.)
 constexpr int CS_R = 3;
-constexpr int CS_TB = 32;
+constexpr int CS_TB = 128;
 constexpr int CS_MAX_NH = 2048;                  // <= 34 KB of shared memory
 
 __device__ __forceinline__ void cs_bulk(void *dst, const void *src, uint32_t bytes, uint32_t bar) {
