@@ -493,10 +493,15 @@ __device__ __forceinline__ void cs_bulk(void *dst, const void *src, uint32_t byt
         : "memory");
 }
 
-template <int R, int TB>
+// Skip modes (scatter_convolve_skip_zeros, core.py:150-167): samples the
+// reference skips are zeroed in the staged window, so a skipped sample adds
+// x*0... = +-0 like a padded step -- exact when every tap is finite (checked
+// by every CTA in skip mode); otherwise the bounded loop reads the drive from
+// memory and skips those samples itself.
+template <int R, int TB, int SKIP>
 __global__ void __launch_bounds__(TB) k_chain_small(const double *__restrict__ x, int64_t x_off, int64_t m_lo,
                                                     int64_t m_hi, const double *__restrict__ h, int nh, int64_t t0,
-                                                    int64_t n_out, double *__restrict__ y) {
+                                                    int64_t n_out, double *__restrict__ y, double thr) {
     extern __shared__ __align__(16) unsigned char cs_smem[];
     constexpr int TILE = TB * R;
     const int nhp = (nh + 7) & ~7;
@@ -559,12 +564,18 @@ __global__ void __launch_bounds__(TB) k_chain_small(const double *__restrict__ x
     }
     // Padded steps are exact only with finite operands: x meets a zero tap in
     // the P front steps (drive xs[0, TILE+P-1)), and a real tap meets zero
-    // drive only in edge CTAs, which check the taps.
+    // drive only in edge CTAs -- or, in skip mode, at any skipped sample --
+    // which check the taps.
     bool fin = true;
     if (P > 0)
         for (int i = tid; i < TILE + P - 1; i += TB) fin &= isfinite(xs[i]);
-    if (edge)
+    if (edge || SKIP != SC_SKIP_NONE)
         for (int k = tid; k < nh; k += TB) fin &= isfinite(hs[k]);
+    if constexpr (SKIP != SC_SKIP_NONE) {
+        __syncthreads();  // the front check read xs before it is masked
+        for (int i = tid; i < nxs; i += TB)
+            if (skipped<SKIP>(xs[i], thr)) xs[i] = 0.0;
+    }
     fin = TB == 32 ? __all_sync(0xffffffffu, fin) : __syncthreads_and(fin);
     double acc[R];
 #pragma unroll
@@ -601,7 +612,16 @@ __global__ void __launch_bounds__(TB) k_chain_small(const double *__restrict__ x
             // tap t-m in [0, nh) <=> j >= P; drive m in [m_lo, m_hi)
             const int64_t lo = max((int64_t)P, m_lo - t + nhp - 1);
             const int64_t hi = min((int64_t)nhp, m_hi - t + nhp - 1);
-            for (int64_t j = lo; j < hi; ++j) acc[r] = __dadd_rn(acc[r], __dmul_rn(xb[r + j], hs[nhp - 1 - j]));
+            if constexpr (SKIP == SC_SKIP_NONE) {
+                for (int64_t j = lo; j < hi; ++j)
+                    acc[r] = __dadd_rn(acc[r], __dmul_rn(xb[r + j], hs[nhp - 1 - j]));
+            } else {
+                // the staged window is masked: read the drive itself
+                for (int64_t j = lo; j < hi; ++j) {
+                    const double xv = x[t - nhp + 1 + j - x_off];
+                    if (!skipped<SKIP>(xv, thr)) acc[r] = __dadd_rn(acc[r], __dmul_rn(xv, hs[nhp - 1 - j]));
+                }
+            }
         }
     }
 #pragma unroll
@@ -666,13 +686,29 @@ int launch_chain_t(int skip_mode, double threshold, const void *x, int64_t x_off
         SC_REQUIRE(channels >= 1 && channels < 65536, "chain: bad batch");
     }
     if constexpr (sizeof(T) == 8) {
-        if (!fused && skip_mode == SC_SKIP_NONE && nseg == 1 && !init && !init_len_dev && !out_b && !run_if &&
-            !batch && n_a >= n_out && chain_small_ok(n_out, segs[0].nh)) {
+        if (!fused && nseg == 1 && !init && !init_len_dev && !out_b && !run_if && !batch && n_a >= n_out &&
+            chain_small_ok(n_out, segs[0].nh)) {
             const int nh = (int)segs[0].nh;
             const dim3 grid((unsigned)cdiv(n_out, (int64_t)CS_TB * CS_R));
-            k_chain_small<CS_R, CS_TB><<<grid, CS_TB, chain_small_smem(nh), stream>>>(
-                static_cast<const double *>(x), x_off, segs[0].m_lo, segs[0].m_hi,
-                static_cast<const double *>(segs[0].h), nh, t0, n_out, static_cast<double *>(out_a));
+            const size_t sm = chain_small_smem(nh);
+            const double *xd = static_cast<const double *>(x), *hd = static_cast<const double *>(segs[0].h);
+            double *yd = static_cast<double *>(out_a);
+            const int64_t lo = segs[0].m_lo, hi = segs[0].m_hi;
+            switch (skip_mode) {
+                case SC_SKIP_NONE:
+                    k_chain_small<CS_R, CS_TB, SC_SKIP_NONE><<<grid, CS_TB, sm, stream>>>(xd, x_off, lo, hi, hd, nh,
+                                                                                           t0, n_out, yd, threshold);
+                    break;
+                case SC_SKIP_LE:
+                    k_chain_small<CS_R, CS_TB, SC_SKIP_LE><<<grid, CS_TB, sm, stream>>>(xd, x_off, lo, hi, hd, nh,
+                                                                                         t0, n_out, yd, threshold);
+                    break;
+                case SC_SKIP_NOT_GT:
+                    k_chain_small<CS_R, CS_TB, SC_SKIP_NOT_GT><<<grid, CS_TB, sm, stream>>>(
+                        xd, x_off, lo, hi, hd, nh, t0, n_out, yd, threshold);
+                    break;
+                default: SC_REQUIRE(false, "chain: bad skip_mode %d", skip_mode);
+            }
             SC_CHECK_LAUNCH();
             return SC_OK;
         }

@@ -95,3 +95,27 @@ def test_small_chain_matches_windowed_chain(tmp_path):
     env = dict(os.environ, SC_CHAIN_SMALL="0")
     subprocess.run([sys.executable, "-c", code], check=True, env=env)
     _bits_equal(_conv(x, h), np.load(tmp_path / "y.npy"))
+
+
+@pytest.mark.parametrize("thr", [0.0, 0.3])
+@pytest.mark.parametrize("case", ["plain", "x_nonfinite", "h_inf"])
+def test_small_chain_skip_zeros_bit_exact(thr, case):
+    """scatter_convolve_skip_zeros (core.py:150-167, skip |x| <= threshold,
+    NaN not skipped) through k_chain_small: skipped samples are zeroed in the
+    staged window (exact with finite taps); a non-finite tap sends every CTA
+    to the bounded loop, which reads and skips the drive itself."""
+    from paper_2401_01607_b200.core import scatter_convolve_skip_zeros
+
+    rng = np.random.default_rng(17)
+    ne, nh = 5000, 777
+    x = rng.uniform(-1, 1, ne)
+    x[::5] = 0.0
+    x[1::9] = -0.0
+    h = rng.standard_normal(nh)
+    if case == "x_nonfinite":
+        x[3] = np.inf        # |inf| > thr: scatters
+        x[2500] = np.nan     # NaN is not skipped here: propagates
+    if case == "h_inf":
+        h[100] = np.inf
+    got = np.asarray(scatter_convolve_skip_zeros(Signal(x), Signal(h), threshold=thr).concatenated().samples)
+    _bits_equal(got, O.scatter_full(x, h, skip_mode=O.SKIP_LE, threshold=thr))
