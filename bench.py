@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="cfg5",
                     choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "short8", "short16", "short32",
-                             "short64", "short128", "mstream"])
+                             "short64", "short128", "short256", "short512", "short1024", "mstream"])
     ap.add_argument("--mode", default="auto", choices=["auto", "fast", "ffma", "tc", "ordered"],
                     help="auto = the library default (float32: fast, tensor cores for long filters; "
                          "float64: ordered, bit-exact); fast on a float64 config = fused-FMA chain; "

@@ -655,7 +655,10 @@ struct FsGeo {
     // staged row-major by one bulk copy into RAW, then converted into the slot
     static constexpr uint32_t RAW = ONE ? (uint32_t)(TN + SSH - 1) * TR * 4 : 0;
     static constexpr int RAW_ROWS_A = 64;  // rows of RAW's first half (see the converters)
-    static constexpr int WROWS_FIT = (int)((SMEM_MAX - 256 - RAW - NHSLOT * 2 * HST_PART) / (2 * 2 * KG * 16));
+    // H8 stage slots: one-stage units keep their single stage resident (one
+    // slot; a multi-channel launch reloads it when the channel changes)
+    static constexpr int NHS = ONE ? 1 : NHSLOT;
+    static constexpr int WROWS_FIT = (int)((SMEM_MAX - 256 - RAW - NHS * 2 * HST_PART) / (2 * 2 * KG * 16));
     static constexpr int WPF = ONE ? SSH : ((WROWS_FIT - 1 - TN) / 8) * 8;  // most shifts per unit
     // rows per window slot; WROWS = 1 (mod 8) puts the K-group stride at 16
     // (mod 128) bytes, so the converters' 16-byte accesses -- consecutive
@@ -664,7 +667,7 @@ struct FsGeo {
     static constexpr uint32_t XPART = WROWS * KG * 16;              // one slot, one part (hi or lo)
     static constexpr uint32_t SM_RAW = 4 * XPART;                   // slot s, part p at (2s + p) * XPART
     static constexpr uint32_t SM_HST = SM_RAW + RAW;
-    static constexpr uint32_t SM_BAR = SM_HST + NHSLOT * 2 * HST_PART;
+    static constexpr uint32_t SM_BAR = SM_HST + NHS * 2 * HST_PART;
     static constexpr uint32_t SM_TOTAL = SM_BAR + 256;
     static constexpr uint32_t IDESC = TcGeo<TN>::IDESC;
     static_assert(WPF >= SSH && WPF % SSH == 0, "window");
@@ -908,8 +911,8 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                     const int64_t key = ch * a.s8 + sg;
                     if (key == last_key) continue;
                     last_key = key;
-                    const uint32_t slot = hsc % NHSLOT;
-                    if (hsc >= NHSLOT) mbar_wait(bar_hempty + 8 * slot, ((hsc / NHSLOT) - 1) & 1);
+                    const uint32_t slot = hsc % G::NHS;
+                    if (hsc >= (uint32_t)G::NHS) mbar_wait(bar_hempty + 8 * slot, ((hsc / G::NHS) - 1) & 1);
                     mbar_expect_tx(bar_hfull + 8 * slot, 2 * HST_PART);
                     const int64_t glo = (a.s8 - 1 - (sg + SSH - 1)) * KG;
                     for (int p = 0; p < 2; ++p)
@@ -950,8 +953,8 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                         // the MMAs issued so far complete
                         if (hsc > 0 && elect_one()) umma_commit(bar_hempty + 8 * slot);
                         last_key = key;
-                        slot = hsc % NHSLOT;
-                        mbar_wait(bar_hfull + 8 * slot, (hsc / NHSLOT) & 1);
+                        slot = hsc % G::NHS;
+                        mbar_wait(bar_hfull + 8 * slot, (hsc / G::NHS) & 1);
                         ++hsc;
                     }
                     const uint32_t acc = dc & 1;
@@ -1414,11 +1417,10 @@ FsCtl *fs_ctl(cudaStream_t stream, int *err) {
 
 // Fused-split launch (see k_tc_fir_fs); returns SC_ERR_STATE when the filter
 // has more shifts than one window holds (the image path then runs).
-int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi, const float *h,
-                         int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin, int64_t n_end,
-                         int64_t channels, cudaStream_t stream, const unsigned **nonfinite_out, const TcPre *pre,
-                         bool *fallback_folded) {
-    constexpr int SSH = 2;
+template <int SSH>
+int launch_fs_impl(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi, const float *h,
+                   int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin, int64_t n_end, int64_t channels,
+                   cudaStream_t stream, const unsigned **nonfinite_out, const TcPre *pre, bool *fallback_folded) {
     using G = FsGeo<SSH>;
     const int64_t n_len = n_end - n_begin;
     const int64_t s_needed = (nh + TR - 2) / TR + 1;
@@ -1571,6 +1573,25 @@ namespace {
 }  // namespace
 
 bool tc_fir_supported(int64_t nh) { return nh >= 2 * TR; }
+
+// Filters of 3-4 shifts (256-511 taps) run one-stage units with 4-shift
+// drains (k_tc_fir_fs<4, true>: one accumulator per unit, the streaming
+// epilogue); shorter ones 2-shift drains; 5-8 shifts the multi-stage units.
+int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi, const float *h,
+                         int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin, int64_t n_end,
+                         int64_t channels, cudaStream_t stream, const unsigned **nonfinite_out, const TcPre *pre,
+                         bool *fallback_folded) {
+    const int64_t s_needed = (nh + TR - 2) / TR + 1;
+    static const bool one4 = [] {
+        const char *v = getenv("SC_FS_SSH4");  // 0: 3-4 shift filters keep the multi-stage units (A/B)
+        return !(v && atoi(v) == 0);
+    }();
+    if (one4 && s_needed > 2 && s_needed <= 4)
+        return launch_fs_impl<4>(x, ldx, x_base, x_lo, x_hi, h, ldh, nh, y, ldy, n_begin, n_end, channels, stream,
+                                 nonfinite_out, pre, fallback_folded);
+    return launch_fs_impl<2>(x, ldx, x_base, x_lo, x_hi, h, ldh, nh, y, ldy, n_begin, n_end, channels, stream,
+                             nonfinite_out, pre, fallback_folded);
+}
 
 int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi,
                       const float *h, int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin,

@@ -192,7 +192,7 @@ def _fs_check(x, h, y, seeds=6):
         assert err_frac(np.asarray(y[s:s + 512]), ref, x, h) <= 1.0, s
 
 
-@pytest.mark.parametrize("nh", [48, 128, 255, 700, 900])
+@pytest.mark.parametrize("nh", [48, 128, 255, 256, 300, 511, 512, 700, 900])
 def test_fused_split_large_launch(nh):
     import torch
 
@@ -244,11 +244,12 @@ def test_fused_split_batched_channels_and_shards():
             assert err_frac(ys[s:s + 300], ref, xs, hs) <= 1.0
 
 
-def test_fused_split_nonfinite_falls_back():
+@pytest.mark.parametrize("nh", [128, 300])
+def test_fused_split_nonfinite_falls_back(nh):
     import torch
 
     rng = np.random.default_rng(78)
-    ne, nh = (1 << 23), 128
+    ne = 1 << 23
     x = rng.uniform(-1, 1, ne).astype(np.float32)
     x[4_000_000] = np.inf
     x[6_000_123] = np.nan
