@@ -222,11 +222,14 @@ def test_fused_split_short_filters_from_26_taps(nh):
     _fs_check(x, h, y)
 
 
-def test_fused_split_batched_channels_and_shards():
+@pytest.mark.parametrize("nh", [131, 300])
+def test_fused_split_batched_channels_and_shards(nh):
+    """Several channels in one launch (the one resident H8 stage is reloaded
+    when the channel changes; 300 taps: 4-shift units), and shards."""
     import torch
 
     rng = np.random.default_rng(77)
-    C, ne, nh = 8, 700_001, 131
+    C, ne = 8, 700_001
     x = rng.uniform(-1, 1, (C, ne)).astype(np.float32)
     h = rng.standard_normal((C, nh)).astype(np.float32)
     y = convolve_batched(torch.from_numpy(x).cuda(), torch.from_numpy(h).cuda()).cpu().numpy()
