@@ -667,7 +667,7 @@ def main():
     if tf.exists():
         tt = json.loads(tf.read_text())
         if work.kernel == "k_tc_fir" and tc["launches"]:
-            traffic = tt.get(f"{args.config}_k_tc_fir<{tc['ssh']},{tc['tile_n']}>")
+            traffic = tt.get(f"{args.config}_{tc['kernel'] or 'k_tc_fir'}<{tc['ssh']},{tc['tile_n']}>")
         else:
             traffic = tt.get(f"{args.config}_{work.kernel}")
     if getattr(work, "hbm_bound", False):
@@ -681,7 +681,9 @@ def main():
         if work.kernel == "k_tc_fir" and tc["launches"]:
             tc_peak = float(p.get("bf16_tflops", 1590.0))
             tflops = 2 * 3 * tc["padded_macs"] / args.steps / (ms_local * 1e-3) / 1e12
-            roofline["kernel"] = f"k_tc_fir_fs<{tc['ssh']},{tc['tile_n']}> (fused split: x read as FP32)"
+            roofline["kernel"] = (f"k_tc_fir_fs<{tc['ssh']},{tc['tile_n']}> (fused split: x read as FP32)"
+                                  if tc["kernel"] == "k_tc_fir_fs" else
+                                  f"k_tc_fir<{tc['ssh']},{tc['tile_n']}> (fp16 hi/lo operand image in HBM)")
             roofline["tensor"] = {"achieved_tflops": tflops, "frac": tflops / tc_peak,
                                   "note": "the tensor roof is not the binding one at <= 2 shifts"}
     elif work.kernel == "k_tc_fir" and tc["launches"]:
@@ -691,7 +693,9 @@ def main():
         tc_peak = float(p.get("bf16_tflops", 1590.0))
         padded = tc["padded_macs"] / args.steps
         achieved = 2 * 3 * padded / (ms_local * 1e-3) / 1e12
-        tmpl = f"k_tc_fir<{tc['ssh']},{tc['tile_n']}>"
+        # the library names the kernel that issued the MMAs (sc_tc_last_kernel):
+        # k_tc_fir (operand image) or k_tc_fir_fs (fused split, medium filters)
+        tmpl = f"{tc['kernel'] or 'k_tc_fir'}<{tc['ssh']},{tc['tile_n']}>"
         work.kernel_template = tmpl
         roofline = {
             "bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
@@ -706,7 +710,9 @@ def main():
             "useful_fp32_tflops": useful,
             "useful_frac_of_fp32_fma_peak": useful / fp32_peak,
             "kernel": f"{tmpl} (tcgen05.mma kind::f16 M128 x N{tc['tile_n']} x K16, TMEM accumulators, "
-                      f"TMEM drain every {tc['ssh']} shifts, cp.async.bulk)",
+                      f"TMEM drain every {tc['ssh']} shifts, "
+                      + ("x read as FP32 and split to fp16 hi/lo in shared memory)" if tc["kernel"] == "k_tc_fir_fs"
+                         else "cp.async.bulk of the fp16 hi/lo operand image)"),
         }
     elif work.dtype == "f64":
         # ordered float64 chain: every MAC is a DMUL and a DADD (separately

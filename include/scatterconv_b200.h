@@ -84,6 +84,16 @@ int64_t sc_launch_count(void);
  * No reference counterpart (bench instrumentation). */
 int sc_tc_stats(int64_t *launches, int64_t *padded_macs, int *last_ssh, int *last_tile_n);
 void sc_tc_stats_reset(void);
+/* Which tensor-core kernel issued the last counted launch (graph replays keep
+ * the kernel their capture recorded): SC_TC_KERNEL_IMAGE = k_tc_fir (fp16
+ * hi/lo operand image in HBM), SC_TC_KERNEL_FUSED_SPLIT = k_tc_fir_fs (x
+ * read as FP32 and split in shared memory), SC_TC_KERNEL_NONE before any.
+ * Not reset by sc_tc_stats_reset.  No reference counterpart (bench
+ * instrumentation: the roofline names the kernel the library ran). */
+#define SC_TC_KERNEL_NONE 0
+#define SC_TC_KERNEL_IMAGE 1
+#define SC_TC_KERNEL_FUSED_SPLIT 2
+int sc_tc_last_kernel(void);
 
 /* ---------------------------------------------------------------- whole signal */
 

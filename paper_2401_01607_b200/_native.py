@@ -80,7 +80,8 @@ _SIGNATURES = {
     "sc_engine_process_blocks_channels": [_vp, _vp, _i64, _i64, _p64, ctypes.POINTER(_vp), _p64, _p64, _i64,
                                           _vp],
 }
-EXPORTS = tuple(_SIGNATURES) + ("sc_last_error", "sc_launch_count", "sc_tc_stats_reset")
+EXPORTS = tuple(_SIGNATURES) + ("sc_last_error", "sc_launch_count", "sc_tc_stats_reset", "sc_tc_last_kernel")
+TC_KERNEL_NAMES = {0: None, 1: "k_tc_fir", 2: "k_tc_fir_fs"}   # SC_TC_KERNEL_* (include/scatterconv_b200.h)
 
 _lock = threading.Lock()
 _lib = None
@@ -114,6 +115,8 @@ def load_library() -> ctypes.CDLL:
         L.sc_launch_count.restype = ctypes.c_int64
         L.sc_tc_stats_reset.argtypes = []
         L.sc_tc_stats_reset.restype = None
+        L.sc_tc_last_kernel.argtypes = []
+        L.sc_tc_last_kernel.restype = ctypes.c_int
         _lib = L
         return L
 
@@ -179,4 +182,5 @@ def tc_stats() -> dict:
     n, macs = ctypes.c_int64(), ctypes.c_int64()
     ssh, tn = ctypes.c_int(), ctypes.c_int()
     check(L.sc_tc_stats(ctypes.byref(n), ctypes.byref(macs), ctypes.byref(ssh), ctypes.byref(tn)))
-    return {"launches": n.value, "padded_macs": macs.value, "ssh": ssh.value, "tile_n": tn.value}
+    return {"launches": n.value, "padded_macs": macs.value, "ssh": ssh.value, "tile_n": tn.value,
+            "kernel": TC_KERNEL_NAMES.get(L.sc_tc_last_kernel())}

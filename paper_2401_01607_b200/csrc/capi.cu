@@ -24,11 +24,12 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // tensor-core launch bookkeeping (sc_tc_stats): the work k_tc_fir issues
 static std::atomic<int64_t> g_tc_launches{0}, g_tc_padded{0};
-static std::atomic<int> g_tc_last_ssh{0}, g_tc_last_tn{0};
+static std::atomic<int> g_tc_last_ssh{0}, g_tc_last_tn{0}, g_tc_last_kernel{SC_TC_KERNEL_NONE};
 void note_launches(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 int64_t launches_so_far() { return g_launches.load(std::memory_order_relaxed); }
 
-void note_tc_launch(int ssh, int tile_n, int64_t padded_macs) {
+void note_tc_launch(int ssh, int tile_n, int64_t padded_macs, int kernel) {
+    g_tc_last_kernel.store(kernel, std::memory_order_relaxed);
     g_tc_launches.fetch_add(1, std::memory_order_relaxed);
     g_tc_padded.fetch_add(padded_macs, std::memory_order_relaxed);
     g_tc_last_ssh.store(ssh, std::memory_order_relaxed);
@@ -254,6 +255,8 @@ int sc_tc_stats(int64_t *launches, int64_t *padded_macs, int *last_ssh, int *las
     if (last_tile_n) *last_tile_n = g_tc_last_tn.load(std::memory_order_relaxed);
     return SC_OK;
 }
+
+int sc_tc_last_kernel(void) { return g_tc_last_kernel.load(std::memory_order_relaxed); }
 
 void sc_tc_stats_reset(void) {
     g_tc_launches.store(0, std::memory_order_relaxed);

@@ -1493,7 +1493,7 @@ int launch_fs_impl(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, in
         const cudaError_t le = cudaLaunchKernelEx(&cfg, k_tc_fir_fs<SSH, true>, a);
         if (le == cudaSuccess) {
             note_launch();
-            note_tc_launch(SSH, G::TN, n_tiles * (int64_t)TR * G::TN * (int64_t)TR * s8);
+            note_tc_launch(SSH, G::TN, n_tiles * (int64_t)TR * G::TN * (int64_t)TR * s8, SC_TC_KERNEL_FUSED_SPLIT);
             return SC_OK;
         }
         // the grid cannot be co-resident here (e.g. a partitioned device):
@@ -1558,7 +1558,7 @@ int launch_fs_impl(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, in
                     (h[k * 8 + 3] - t0) * 1e-3, (h[k * 8 + 4] - t0) * 1e-3, (h[k * 8 + 5] - t0) * 1e-3,
                     (h[k * 8 + 6] - t0) * 1e-3);
     }
-    note_tc_launch(SSH, G::TN, n_tiles * (int64_t)TR * G::TN * (int64_t)TR * s8);
+    note_tc_launch(SSH, G::TN, n_tiles * (int64_t)TR * G::TN * (int64_t)TR * s8, SC_TC_KERNEL_FUSED_SPLIT);
     if (nsplit > 1) {
         dim3 g((unsigned)cdiv(n_len, 256), (unsigned)channels);
         SC_LAUNCH_PDL(k_tc_split_reduce, g, dim3(256), 0, stream, static_cast<const float *>(a.ws), (int)nsplit,
@@ -1767,7 +1767,7 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
     else if (SSH == 4) SC_TC_LAUNCH(4, 256);
     else SC_TC_LAUNCH(8, 256);
 #undef SC_TC_LAUNCH
-    note_tc_launch(SSH, TNV, a.n_tiles * TTILE * (int64_t)TR * s8);
+    note_tc_launch(SSH, TNV, a.n_tiles * TTILE * (int64_t)TR * s8, SC_TC_KERNEL_IMAGE);
     if (nsplit > 1) {
         dim3 g((unsigned)cdiv(n_len, 256), (unsigned)channels);
         SC_LAUNCH_PDL(k_tc_split_reduce, g, dim3(256), 0, stream, static_cast<const float *>(a.ws), (int)nsplit,

@@ -28,7 +28,8 @@ void set_error(const char *fmt, ...);
 void note_launch();  // bumps the sc_launch_count() counter
 // records one k_tc_fir launch for sc_tc_stats (drain period, tile width, and
 // the padded MACs of its MMAs: tiles x 128*tile_n outputs x 128 taps x shifts)
-void note_tc_launch(int ssh, int tile_n, int64_t padded_macs);
+// and which kernel issued them (SC_TC_KERNEL_IMAGE / SC_TC_KERNEL_FUSED_SPLIT)
+void note_tc_launch(int ssh, int tile_n, int64_t padded_macs, int kernel);
 // counters around a CUDA-graph capture, re-applied on every replay
 void note_launches(int64_t k);
 int64_t launches_so_far();

@@ -272,3 +272,23 @@ def test_fused_split_nonfinite_falls_back(nh):
     y2 = y2.concatenated().samples.cpu().numpy()
     assert np.all(np.isfinite(y2))
     _fs_check(x2, h, y2, seeds=2)
+
+
+@pytest.mark.parametrize("ne,nh,kernel", [((1 << 23) + 7, 128, "k_tc_fir_fs"), ((1 << 23) + 7, 300, "k_tc_fir_fs"),
+                                          (1 << 20, 4096, "k_tc_fir")])
+def test_tc_last_kernel_names_the_kernel_that_ran(ne, nh, kernel):
+    """sc_tc_last_kernel (bench.py's roofline label) reports which tensor-core
+    kernel issued the MMAs; sc_tc_stats counts the launch."""
+    import torch
+
+    from paper_2401_01607_b200 import _native as N
+
+    rng = np.random.default_rng(nh)
+    x = torch.from_numpy(rng.uniform(-1, 1, ne).astype(np.float32)).cuda()
+    h = torch.from_numpy(rng.standard_normal(nh).astype(np.float32)).cuda()
+    N.lib().sc_tc_stats_reset()
+    scatter_convolve(Signal(x), Signal(h))
+    torch.cuda.synchronize()
+    st = N.tc_stats()
+    assert st["launches"] >= 1 and st["padded_macs"] >= ne * nh
+    assert st["kernel"] == kernel
