@@ -75,6 +75,15 @@ def _signal(samples, sample_rate):
     return sig
 
 
+def _is_dev_ir(ir, device, npd) -> bool:
+    """An IR the library can read in place: a contiguous CUDA tensor of the
+    engine's dtype on its device (a Signal holding one counts)."""
+    t = _dev.torch()
+    a = ir.samples if isinstance(ir, Signal) else ir
+    return (type(a) is t.Tensor and a.is_cuda and a.get_device() == device.index and a.is_contiguous()
+            and a.dtype == _dev.torch_dtype(npd))
+
+
 class ScatterEngine:
     """Stateful block- or sample-driven convolution processor on the GPU.
 
@@ -96,6 +105,8 @@ class ScatterEngine:
             device = h.samples.device if (_dev.is_tensor(h.samples) and h.samples.is_cuda) else \
                 t.device("cuda", t.cuda.current_device())
         self._device = t.device(device)
+        if self._device.index is None:
+            self._device = t.device("cuda", t.cuda.current_device())
         self._dev_idx = self._device.index
         self._sample_rate = h.sample_rate
         self._ir_like = h.samples[:0]   # currency of returned signals (host / device / pinned)
@@ -366,12 +377,16 @@ class ScatterEngine:
             # reused while the caller passes the same IR objects at the same
             # blocks -- a render loop replaying one schedule pays no
             # per-swap Python (the cache keeps the objects alive, so their
-            # identities cannot be recycled).
+            # identities cannot be recycled).  Only for schedules whose IRs
+            # are all device tensors (the library reads them in place): host
+            # IRs are uploaded again on every call, so an IR edited in place
+            # between calls is seen, as the reference reads it per call.
             if not isinstance(swaps, (list, tuple)):
                 swaps = list(swaps)
-            sig = (n_blocks, tuple((s[0], id(s[1])) for s in swaps))
+            on_dev = all(_is_dev_ir(s[1], self._device, self._npd) for s in swaps)
+            sig = (n_blocks, tuple((s[0], id(s[1])) for s in swaps)) if on_dev else None
             cached = self._sched_cache
-            if cached is not None and cached[0] == sig:
+            if sig is not None and cached is not None and cached[0] == sig:
                 swaps, irs, blocks, ptrs, nhs, n = cached[1]
             else:
                 keep = list(swaps)
@@ -401,7 +416,7 @@ class ScatterEngine:
             if rc:
                 N.check(rc)
             self._note_swaps(swaps, pending)
-            if xd is xs and pending is None and type(xs) is t.Tensor and xs.dim() == 1:
+            if xd is xs and pending is None and type(xs) is t.Tensor and xs.dim() == 1 and on_dev:
                 # args[1] keeps the device IRs (and the C arrays) alive
                 self._stream_fast = (nb, xs.shape[0], xs.dtype, self._device.index, self._sched_cache[2],
                                      self._sched_cache[1], (self._ir_like, self._nh) if swaps else None)

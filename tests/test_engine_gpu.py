@@ -483,3 +483,38 @@ def test_process_stream_repeat_calls_follow_schedule_changes():
         got = eng.process_stream(x, nb, sw).cpu().numpy()
         assert np.array_equal(got, ref_stream(swaps)), call
     assert np.array_equal(eng.flush().samples.cpu().numpy(), ref.flush().samples.cpu().numpy())
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_process_stream_host_irs_edited_in_place_are_seen(dtype):
+    """A schedule of HOST IRs is uploaded on every call: editing an IR in
+    place between two process_stream calls changes the second call's output
+    exactly as a fresh engine given the edited IR (the reference reads the IR
+    on every call); device-tensor schedules are read in place."""
+    import torch
+
+    from paper_2401_01607_b200.core import Signal as S
+    from paper_2401_01607_b200.engine import EngineConfig as EC, ScatterEngine as SE
+
+    rng = np.random.default_rng(77)
+    nb = 64
+    h0 = rng.standard_normal(40).astype(dtype)
+    irs = [rng.standard_normal(50).astype(dtype), rng.standard_normal(30).astype(dtype)]
+    x = torch.from_numpy(rng.uniform(-1, 1, 20 * nb).astype(dtype)).cuda()
+    swaps = [(3, irs[0]), (11, irs[1])]
+
+    def run(sched):
+        eng = SE(S(h0.copy()), EC(block_size_nb=nb))
+        a = eng.process_stream(x, nb, sched).cpu().numpy()
+        return a, np.asarray(eng.flush().samples)
+
+    eng = SE(S(h0.copy()), EC(block_size_nb=nb))
+    first = eng.process_stream(x, nb, swaps).cpu().numpy()
+    irs[0][:] = rng.standard_normal(50).astype(dtype)   # edited in place, same object
+    eng.flush()
+    eng2_body = eng.process_stream(x, nb, swaps).cpu().numpy()
+    want_body, _ = run([(3, irs[0].copy()), (11, irs[1].copy())])
+    # the second call starts from the flushed engine's IR (irs[1]); its first
+    # three blocks' residue reaches at most 39 samples into block 3
+    np.testing.assert_array_equal(eng2_body[4 * nb:], want_body[4 * nb:])
+    assert not np.array_equal(first[4 * nb:12 * nb], eng2_body[4 * nb:12 * nb])
