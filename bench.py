@@ -43,15 +43,23 @@ METRIC = json.loads((REPO / "BASELINE.json").read_text())["metric"] if (REPO / "
 UNIT = "GMAC/s"
 
 
+
+def _config_name(v: str) -> str:
+    import argparse
+    import re
+
+    if v in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "mstream") or re.fullmatch(r"short[1-9][0-9]*", v):
+        return v
+    raise argparse.ArgumentTypeError(f"unknown config {v!r} (cfg1..cfg5, mstream or shortN)")
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="cfg5",
-                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "short8", "short16", "short32",
-                             "short64", "short128", "short256", "short512", "short1024", "mstream"])
+    ap.add_argument("--config", default="cfg5", type=_config_name,
+                    help="cfg1..cfg5, mstream, or shortN (2^26 samples x N taps, N >= 1)")
     ap.add_argument("--mode", default="auto", choices=["auto", "fast", "ffma", "tc", "ordered"],
                     help="auto = the library default (float32: fast, tensor cores for long filters; "
                          "float64: ordered, bit-exact); fast on a float64 config = fused-FMA chain; "
