@@ -1615,11 +1615,19 @@ int launch_fir_f32_tc(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo,
         if (rc != SC_ERR_STATE) return rc;
     }
     const int64_t s_needed = (nh + TR - 2) / TR + 1;
-    static const int wide_ssh = [] {
-        const char *v = getenv("SC_TC_WIDE_SSH");  // experiment knob: 2, 4 or 8
-        const int k = v ? atoi(v) : 4;
-        return k == 2 || k == 8 ? k : 4;
+    static const int wide_ssh_env = [] {
+        const char *v = getenv("SC_TC_WIDE_SSH");  // experiment knob: 2, 4 or 8 (0 = by padding)
+        const int k = v ? atoi(v) : 0;
+        return k == 2 || k == 4 || k == 8 ? k : 0;
     }();
+    // Drain period at 256-row tiles: 4 shifts, unless draining every 2 saves
+    // >= 3 % of the padded shifts (short filters: 9 shifts pad to 12 vs 10).
+    // Measured on 2^26-sample launches (profiles/r02_medium_ssh.txt): 2-shift
+    // drains cost ~2 % of MMA throughput, so 1,024 taps 0.529 -> 0.485 ms,
+    // 2,048 taps 0.740 -> 0.697, 4,096 taps 1.175 -> 1.128; cfg3/cfg4/cfg5
+    // (751 / 129 / 2,049 shifts: <= 1.5 % padding either way) keep 4.
+    const int wide_ssh = wide_ssh_env ? wide_ssh_env
+                                      : (cdiv(s_needed, 4) * 4 * 100 >= cdiv(s_needed, 2) * 2 * 103 ? 2 : 4);
     // 256 output rows per tile (measured +2 % on cfg5, +2.7 % on cfg4, +3 %
     // on cfg3 end to end over 128: half the A-operand reads per FLOP) unless
     // the launch is too small to fill the SMs with 256-row work units (tiles
