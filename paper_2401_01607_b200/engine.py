@@ -116,6 +116,7 @@ class ScatterEngine:
         self._stream_val = None
         self._sched_cache = None
         self._stream_fast = None  # see _process_stream_fast
+        self._ir_stage = None     # see _stage_irs
         hd = self._to_dev(h.samples)
         with _dev.device_guard(self._device):
             N.check(self._lib.sc_engine_create(self._dt, N.ptr(hd), len(h),
@@ -134,6 +135,60 @@ class ScatterEngine:
 
     def _to_dev(self, samples):
         return _dev.as_device(samples, self._npd, device=self._device)
+
+    def _stage_irs(self, arrs):
+        """Device copies of a swap schedule's IRs for one call.  Host IRs are
+        packed into an engine-owned pinned buffer and go up in ONE copy into
+        an engine-owned device buffer, so their device addresses are the same
+        on every call (the library's CUDA-graph cache keys on them: a render
+        loop with host IRs replays one graph) while the data is fresh
+        (edited-in-place IRs are seen).  Device IRs of the engine's dtype are
+        read in place; others are converted."""
+        t = _dev.torch()
+        td = _dev.torch_dtype(self._npd)
+        out = [None] * len(arrs)
+        host = []
+        for i, a in enumerate(arrs):
+            if _is_dev_ir(a, self._device, self._npd):
+                out[i] = a
+            elif _dev.is_tensor(a) and a.is_cuda:
+                out[i] = _dev.as_device(a, self._npd, device=self._device)
+            else:
+                host.append(i)
+        if not host:
+            return out
+        sizes = [int(np.shape(arrs[i])[0]) for i in host]
+        total = sum(sizes)
+        st = self._ir_stage
+        if st is None or st[0].numel() < total:
+            if st is not None:
+                st[2].synchronize()
+            st = (t.empty(total, dtype=td, device=self._device), t.empty(total, dtype=td, pin_memory=True),
+                  t.cuda.Event(), t.cuda.Event())
+            self._ir_stage = st
+        dbuf, hbuf, ev_copy, ev_used = st
+        ev_copy.synchronize()   # the previous call's upload has left hbuf
+        off = 0
+        hv = hbuf.numpy()
+        for i, n in zip(host, sizes):
+            a = arrs[i]
+            if _dev.is_tensor(a):
+                hbuf[off:off + n].copy_(a.reshape(-1))
+            else:
+                hv[off:off + n] = np.asarray(a, dtype=self._npd).reshape(-1)
+            out[i] = dbuf[off:off + n]
+            off += n
+        cur = t.cuda.current_stream(self._device)
+        cur.wait_event(ev_used)   # kernels of the previous call (any stream) done with dbuf
+        dbuf[:total].copy_(hbuf[:total], non_blocking=True)
+        ev_copy.record(cur)
+        return out
+
+    def _staged_irs_used(self, on_dev):
+        """Mark the staged IR buffer as read by the work just queued (the next
+        call's upload into it waits for that work on the device)."""
+        if not on_dev and self._ir_stage is not None:
+            self._ir_stage[3].record(_dev.torch().cuda.current_stream(self._device))
 
     def _bind_stream(self):
         # the engine queues on the caller's current stream; rebinding only
@@ -392,13 +447,14 @@ class ScatterEngine:
                 keep = list(swaps)
                 # swaps outside [0, n_blocks) precede no block: the library ignores them
                 swaps = sorted((s for s in keep if 0 <= int(s[0]) < n_blocks), key=lambda s: s[0])
-                irs = _dev.as_device_many([s[1].samples if isinstance(s[1], Signal) else s[1] for s in swaps],
-                                          self._npd, device=self._device)
+                arrs = [s[1].samples if isinstance(s[1], Signal) else s[1] for s in swaps]
+                irs = arrs if on_dev else self._stage_irs(arrs)
                 n = len(swaps)
                 blocks = (ctypes.c_int64 * max(n, 1))(*[int(s[0]) for s in swaps])
                 ptrs = (ctypes.c_void_p * max(n, 1))(*[ir.data_ptr() for ir in irs])
                 nhs = (ctypes.c_int64 * max(n, 1))(*[ir.shape[0] for ir in irs])
-                self._sched_cache = (sig, (swaps, irs, blocks, ptrs, nhs, n), keep)
+                # host schedules are staged again on the next call: nothing to keep
+                self._sched_cache = (sig, (swaps, irs, blocks, ptrs, nhs, n), keep) if on_dev else None
             self._bind_stream()
             xh = _dev.pinned_rows(xs, self._npd, 1)
             if xh is not None:
@@ -407,6 +463,7 @@ class ScatterEngine:
                 out = t.empty(xh.shape[1], dtype=xh.dtype, pin_memory=True)
                 N.check(self._lib.sc_engine_process_blocks_host(self._handle, N.ptr(xh), xh.shape[1], nb,
                                                                 blocks, ptrs, nhs, n, N.ptr(out), _dev.host_pipe_chunks()))
+                self._staged_irs_used(on_dev)
                 self._note_swaps(swaps, pending)
                 return out
             xd = self._to_dev(xs)
@@ -415,6 +472,7 @@ class ScatterEngine:
                                                     nhs, n, out.data_ptr())
             if rc:
                 N.check(rc)
+            self._staged_irs_used(on_dev)
             self._note_swaps(swaps, pending)
             if xd is xs and pending is None and type(xs) is t.Tensor and xs.dim() == 1 and on_dev:
                 # args[1] keeps the device IRs (and the C arrays) alive
