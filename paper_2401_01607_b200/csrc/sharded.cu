@@ -160,30 +160,10 @@ int run_range(RangeJob &j, int dtype, int mode, const void *x_host, int64_t ne, 
     }
     char *ybuf = direct ? direct : static_cast<char *>(p.yd);
     const int64_t chunks = j.chunks > 0 ? j.chunks : pick_chunks(nx, ny, nh, es);
-    // Chunk boundaries.  Only the first chunk's upload and the last chunk's
-    // download are not hidden behind another chunk's FIR, so when chunks are
-    // big enough to keep the tensor cores full at a quarter of the size
-    // (>= 2^36 MACs), the first and last chunks are a quarter of the others:
-    // cfg5 (12 chunks of 4.8 M outputs) exposes 2 x 87 us of copies instead
-    // of 2 x 350 us.
-    std::vector<int64_t> cuts{j.a};
-    {
-        const double quarter = (double)ny / ((double)(chunks - 2) + 0.5) / 4.0;
-        if (chunks >= 3 && quarter * (double)nh >= 68719476736.0) {
-            const int64_t q = (int64_t)quarter;
-            const int64_t mid = ny - 2 * q;
-            cuts.push_back(j.a + q);
-            for (int64_t k = 1; k <= chunks - 2; ++k) cuts.push_back(j.a + q + mid * k / (chunks - 2));
-        } else {
-            const int64_t per = (ny + chunks - 1) / chunks;
-            for (int64_t c = j.a + per; c < j.b; c += per) cuts.push_back(c);
-        }
-        cuts.push_back(j.b);
-    }
+    const int64_t per = (ny + chunks - 1) / chunks;
     int64_t uploaded = xb;
-    for (size_t ci = 0; ci + 1 < cuts.size(); ++ci) {
-        const int64_t c0 = cuts[ci], c1 = cuts[ci + 1];
-        if (c1 <= c0) continue;
+    for (int64_t c0 = j.a; c0 < j.b; c0 += per) {
+        const int64_t c1 = std::min(j.b, c0 + per);
         const int64_t need = std::min(xe, c1);  // outputs < c1 read inputs < c1
         if (need > uploaded) {
             SC_CHECK_CUDA(cudaMemcpyAsync(static_cast<char *>(p.xd) + (size_t)(uploaded - xb) * es,

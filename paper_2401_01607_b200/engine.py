@@ -173,9 +173,10 @@ class ScatterEngine:
         for i, n in zip(host, sizes):
             a = arrs[i]
             if _dev.is_tensor(a):
-                hbuf[off:off + n].copy_(a.reshape(-1))
-            else:
-                hv[off:off + n] = np.asarray(a, dtype=self._npd).reshape(-1)
+                # numpy views of CPU tensors: a slice assignment per IR (~1 us),
+                # not a torch copy_ dispatch
+                a = a.numpy() if (a.dtype == td and not a.requires_grad) else a.detach().to(td).numpy()
+            hv[off:off + n] = a if getattr(a, "ndim", 0) == 1 else np.asarray(a, dtype=self._npd).reshape(-1)
             out[i] = dbuf[off:off + n]
             off += n
         cur = t.cuda.current_stream(self._device)

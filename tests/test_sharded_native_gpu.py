@@ -96,38 +96,3 @@ def test_distributed_convolve_to_host_shards_concatenate():
     ref = O.scatter_full(x, h)
     tol = 1e-5 * np.max(np.abs(x)) * np.sum(np.abs(h))
     assert np.max(np.abs(np.concatenate(parts).astype(np.float64) - ref)) <= tol
-
-
-@pytest.mark.parametrize("chunks", [3, 5])
-def test_range_host_tapered_chunks(chunks):
-    """Chunks of >= 2^36 MACs at a quarter size: the range engine cuts the
-    first and last chunks to a quarter of the others (sharded.cu run_range).
-    Windows across every cut vs the oracle, and the whole output vs the
-    device-resident path, within the FP32 tolerance."""
-    import torch
-
-    from paper_2401_01607_b200 import _native as N
-    from paper_2401_01607_b200.core import Signal, scatter_convolve
-
-    rng = np.random.default_rng(40 + chunks)
-    ne, nh = 7_000_000 if chunks == 3 else 12_000_000, 65_536
-    x = rng.uniform(-1, 1, ne).astype(np.float32)
-    h = (rng.standard_normal(nh) * np.exp(-np.arange(nh) / 9_000.0)).astype(np.float32)
-    ny = ne + nh - 1
-    quarter = int(ny / ((chunks - 2) + 0.5) / 4.0)
-    assert quarter * nh >= 1 << 36
-    xp = torch.from_numpy(x).pin_memory()
-    y = torch.empty(ny, dtype=torch.float32, pin_memory=True)
-    N.check(N.lib().sc_fir_range_host(N.SC_F32, N.SC_MODE_FAST, N.ptr(xp), ne, N.ptr(torch.from_numpy(h)), nh,
-                                      N.ptr(y), 0, ny, 0, chunks))
-    got = y.numpy()
-    tol = 1e-5 * np.max(np.abs(x)) * np.sum(np.abs(h))
-    mid = ny - 2 * quarter
-    cuts = [quarter + mid * k // (chunks - 2) for k in range(chunks - 1)]
-    for c in [0] + cuts + [ny - 300]:
-        a, b = max(0, c - 300), min(ny, c + 300)
-        ref = O.scatter_window(x, h, a, b)
-        assert np.max(np.abs(got[a:b].astype(np.float64) - ref)) <= tol, c
-    dev = scatter_convolve(Signal(torch.from_numpy(x).cuda()), Signal(torch.from_numpy(h).cuda()))
-    dev = dev.concatenated().samples.cpu().numpy()
-    assert np.max(np.abs(dev.astype(np.float64) - got)) <= 2 * tol

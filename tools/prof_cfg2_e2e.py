@@ -51,3 +51,30 @@ for _ in range(3):
     body = eng.process_stream(xd, nb, swaps); torch.cuda.synchronize(); t1 = time.perf_counter()
     eng.flush(); t2 = time.perf_counter()
     print(f"device x, host IRs: process_stream {1e3*(t1-t0):.3f} ms, flush {1e3*(t2-t1):.3f} ms, graphs {stats()}")
+
+# copy primitives
+d = torch.empty_like(x, device="cuda")
+hp = torch.empty_like(x).pin_memory()
+for name, fn in [("sync only", lambda: None),
+                 ("x.to(cuda) 1.9 MB", lambda: x.to("cuda", non_blocking=True)),
+                 ("d.copy_(x) 1.9 MB", lambda: d.copy_(x, non_blocking=True)),
+                 ("hp.copy_(d) 1.9 MB", lambda: hp.copy_(d, non_blocking=True)),
+                 ("stage irs", lambda: eng._stage_irs([s[1] for s in swaps]))]:
+    ts = []
+    for _ in range(20):
+        torch.cuda.synchronize(); t0 = time.perf_counter(); fn(); torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    ts.sort()
+    print(f"{name}: median {1e3*ts[10]:.3f} ms, min {1e3*ts[0]:.3f} ms")
+
+# the library's host-stream path for this small stream too
+from paper_2401_01607_b200 import _dev  # noqa: E402
+_dev.PINNED_STREAM_MIN_BYTES = 1
+for it in range(8):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    body = eng.process_stream(x, nb, swaps)
+    t1 = time.perf_counter()
+    tail = eng.flush()
+    t2 = time.perf_counter()
+    print(f"host-stream path iter {it}: process_stream {1e3*(t1-t0):.3f} ms, flush {1e3*(t2-t1):.3f} ms, graphs {stats()}")
