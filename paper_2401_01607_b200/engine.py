@@ -137,27 +137,34 @@ class ScatterEngine:
         return _dev.as_device(samples, self._npd, device=self._device)
 
     def _stage_irs(self, arrs):
-        """Device copies of a swap schedule's IRs for one call.  Host IRs are
-        packed into an engine-owned pinned buffer and go up in ONE copy into
-        an engine-owned device buffer, so their device addresses are the same
-        on every call (the library's CUDA-graph cache keys on them: a render
-        loop with host IRs replays one graph) while the data is fresh
-        (edited-in-place IRs are seen).  Device IRs of the engine's dtype are
-        read in place; others are converted."""
+        """(device pointer, length) of each IR of a swap schedule, for one
+        call.  Host IRs are packed into an engine-owned pinned buffer and go
+        up in ONE copy into an engine-owned device buffer, so their device
+        addresses are the same on every call (the library's CUDA-graph cache
+        keys on them: a render loop with host IRs replays one graph) while the
+        data is fresh (edited-in-place IRs are seen).  Device IRs of the
+        engine's dtype are read in place; others are converted (kept alive
+        in the returned list's third element).  Runs under the engine's
+        device guard: events record / wait on the current stream."""
         t = _dev.torch()
         td = _dev.torch_dtype(self._npd)
-        out = [None] * len(arrs)
+        ptrs = [0] * len(arrs)
+        nhs = [0] * len(arrs)
+        keep = []
         host = []
         for i, a in enumerate(arrs):
             if _is_dev_ir(a, self._device, self._npd):
-                out[i] = a
+                ptrs[i], nhs[i] = a.data_ptr(), a.shape[0]
             elif _dev.is_tensor(a) and a.is_cuda:
-                out[i] = _dev.as_device(a, self._npd, device=self._device)
+                d = _dev.as_device(a, self._npd, device=self._device)
+                keep.append(d)
+                ptrs[i], nhs[i] = d.data_ptr(), d.shape[0]
             else:
                 host.append(i)
         if not host:
-            return out
-        sizes = [int(np.shape(arrs[i])[0]) for i in host]
+            return ptrs, nhs, keep
+        harr = [arrs[i] for i in host]
+        sizes = [len(a) for a in harr]
         total = sum(sizes)
         st = self._ir_stage
         if st is None or st[0].numel() < total:
@@ -168,28 +175,35 @@ class ScatterEngine:
             self._ir_stage = st
         dbuf, hbuf, ev_copy, ev_used = st
         ev_copy.synchronize()   # the previous call's upload has left hbuf
-        off = 0
-        hv = hbuf.numpy()
-        for i, n in zip(host, sizes):
-            a = arrs[i]
-            if _dev.is_tensor(a):
-                # numpy views of CPU tensors: a slice assignment per IR (~1 us),
-                # not a torch copy_ dispatch
-                a = a.numpy() if (a.dtype == td and not a.requires_grad) else a.detach().to(td).numpy()
-            hv[off:off + n] = a if getattr(a, "ndim", 0) == 1 else np.asarray(a, dtype=self._npd).reshape(-1)
-            out[i] = dbuf[off:off + n]
-            off += n
-        cur = t.cuda.current_stream(self._device)
-        cur.wait_event(ev_used)   # kernels of the previous call (any stream) done with dbuf
+        # one packing op where the IRs allow it (the per-IR ops cost ~2 us
+        # each in Python): torch.cat for CPU tensors of the engine's dtype,
+        # np.concatenate for arrays
+        if all(type(a) is t.Tensor and a.dtype == td and a.dim() == 1 and not a.requires_grad for a in harr):
+            t.cat(harr, out=hbuf[:total])
+        elif all(type(a) is np.ndarray and a.ndim == 1 for a in harr):
+            np.concatenate(harr, out=hbuf.numpy()[:total], casting="unsafe")
+        else:
+            hv = hbuf.numpy()
+            off = 0
+            for a, n in zip(harr, sizes):
+                if _dev.is_tensor(a):
+                    a = a.detach().to(td).numpy()
+                hv[off:off + n] = np.asarray(a, dtype=self._npd).reshape(-1)
+                off += n
+        ev_used.wait()   # the current stream: kernels of the previous call are done with dbuf
         dbuf[:total].copy_(hbuf[:total], non_blocking=True)
-        ev_copy.record(cur)
-        return out
+        ev_copy.record()
+        base, es, off = dbuf.data_ptr(), dbuf.element_size(), 0
+        for i, n in zip(host, sizes):
+            ptrs[i], nhs[i] = base + off * es, n
+            off += n
+        return ptrs, nhs, keep
 
     def _staged_irs_used(self, on_dev):
         """Mark the staged IR buffer as read by the work just queued (the next
         call's upload into it waits for that work on the device)."""
         if not on_dev and self._ir_stage is not None:
-            self._ir_stage[3].record(_dev.torch().cuda.current_stream(self._device))
+            self._ir_stage[3].record()
 
     def _bind_stream(self):
         # the engine queues on the caller's current stream; rebinding only
@@ -449,11 +463,15 @@ class ScatterEngine:
                 # swaps outside [0, n_blocks) precede no block: the library ignores them
                 swaps = sorted((s for s in keep if 0 <= int(s[0]) < n_blocks), key=lambda s: s[0])
                 arrs = [s[1].samples if isinstance(s[1], Signal) else s[1] for s in swaps]
-                irs = arrs if on_dev else self._stage_irs(arrs)
+                if on_dev:
+                    irs = arrs
+                    p_list, n_list = [ir.data_ptr() for ir in irs], [ir.shape[0] for ir in irs]
+                else:
+                    p_list, n_list, irs = self._stage_irs(arrs)
                 n = len(swaps)
                 blocks = (ctypes.c_int64 * max(n, 1))(*[int(s[0]) for s in swaps])
-                ptrs = (ctypes.c_void_p * max(n, 1))(*[ir.data_ptr() for ir in irs])
-                nhs = (ctypes.c_int64 * max(n, 1))(*[ir.shape[0] for ir in irs])
+                ptrs = (ctypes.c_void_p * max(n, 1))(*p_list)
+                nhs = (ctypes.c_int64 * max(n, 1))(*n_list)
                 # host schedules are staged again on the next call: nothing to keep
                 self._sched_cache = (sig, (swaps, irs, blocks, ptrs, nhs, n), keep) if on_dev else None
             self._bind_stream()
