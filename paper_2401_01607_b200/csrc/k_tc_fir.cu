@@ -1429,7 +1429,18 @@ int launch_fs_impl(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, in
     // the next tile then overlap this one's MMAs): measured 0.21 vs 0.28 ms
     // (128 taps, 2^26 outputs).  Longer filters and small launches keep the
     // image path (cfg2: 0.094 vs 0.108 ms).
-    if (s8 > 8 || cdiv(n_len, (int64_t)TR * G::TN) * channels < 2 * (int64_t)sm_count()) return SC_ERR_STATE;
+    static const int64_t fs_max_s8 = [] {
+        // Most (padded) shifts on this path: everything one window holds
+        // (WPF = 72 at 2-shift drains: filters up to ~9,000 taps).  Measured on
+        // 2^26 samples against the image path (profiles/r02_fs_max.txt):
+        // 1,024 taps 0.481 -> 0.375 ms, 2,048 0.694 -> 0.607, 4,096 1.119 ->
+        // 1.073, 8,192 2.007 -> 2.004 (the x image's extra HBM passes stop
+        // mattering there).  SC_FS_MAX_S8=8 restores the round-2 bound (A/B).
+        const char *v = getenv("SC_FS_MAX_S8");
+        const int k = v ? atoi(v) : 0;
+        return (int64_t)(k >= 2 && k <= G::WPF ? k : G::WPF);
+    }();
+    if (s8 > fs_max_s8 || cdiv(n_len, (int64_t)TR * G::TN) * channels < 2 * (int64_t)sm_count()) return SC_ERR_STATE;
     const int64_t ngroups = KG * s8 + KG - 1;
     const int64_t h8_ch = ngroups * 64;
     const int64_t tiles_per_ch = cdiv(n_len, (int64_t)TR * G::TN);
@@ -1576,7 +1587,7 @@ bool tc_fir_supported(int64_t nh) { return nh >= 2 * TR; }
 
 // Filters of 3-4 shifts (256-511 taps) run one-stage units with 4-shift
 // drains (k_tc_fir_fs<4, true>: one accumulator per unit, the streaming
-// epilogue); shorter ones 2-shift drains; 5-8 shifts the multi-stage units.
+// epilogue); shorter ones 2-shift drains; 5-72 shifts the multi-stage units.
 int launch_fir_f32_tc_fs(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, int64_t x_hi, const float *h,
                          int64_t ldh, int64_t nh, float *y, int64_t ldy, int64_t n_begin, int64_t n_end,
                          int64_t channels, cudaStream_t stream, const unsigned **nonfinite_out, const TcPre *pre,

@@ -179,9 +179,9 @@ def test_tc_same_sign_inputs(nh):
 
 
 # ---------------------------------------------------------------- fused split (k_tc_fir_fs)
-# Taken for filters of <= 8 shifts on launches of >= 2 tiles per SM (>= 296
-# tiles of 16,384 outputs): one-stage units (<= 255 taps) on the bulk-copy
-# path, 3-8 shifts on the in-place cp.async path.
+# Taken for filters of <= 72 padded shifts (~9,000 taps) on launches of >= 2
+# tiles per SM (>= 296 tiles of 16,384 outputs): one-stage units (<= 255 taps)
+# on the bulk-copy path, 3-72 shifts on the in-place cp.async path.
 
 
 def _fs_check(x, h, y, seeds=6):
@@ -192,7 +192,7 @@ def _fs_check(x, h, y, seeds=6):
         assert err_frac(np.asarray(y[s:s + 512]), ref, x, h) <= 1.0, s
 
 
-@pytest.mark.parametrize("nh", [48, 128, 255, 256, 300, 511, 512, 700, 900])
+@pytest.mark.parametrize("nh", [48, 128, 255, 256, 300, 511, 512, 700, 900, 1024, 1100, 2049, 4096, 8191, 9000])
 def test_fused_split_large_launch(nh):
     import torch
 
@@ -247,7 +247,7 @@ def test_fused_split_batched_channels_and_shards(nh):
             assert err_frac(ys[s:s + 300], ref, xs, hs) <= 1.0
 
 
-@pytest.mark.parametrize("nh", [128, 300])
+@pytest.mark.parametrize("nh", [128, 300, 2048])
 def test_fused_split_nonfinite_falls_back(nh):
     import torch
 
@@ -274,7 +274,8 @@ def test_fused_split_nonfinite_falls_back(nh):
     _fs_check(x2, h, y2, seeds=2)
 
 
-@pytest.mark.parametrize("ne,nh,kernel", [((1 << 23) + 7, 128, "k_tc_fir_fs"), ((1 << 23) + 7, 300, "k_tc_fir_fs"),
+@pytest.mark.parametrize("ne,nh,kernel", [((1 << 23) + 7, 128, "k_tc_fir_fs"), ((1 << 23) + 7, 300, "k_tc_fir_fs"), ((1 << 23) + 7, 2048, "k_tc_fir_fs"),
+                                          ((1 << 23) + 7, 9300, "k_tc_fir"),
                                           (1 << 20, 4096, "k_tc_fir")])
 def test_tc_last_kernel_names_the_kernel_that_ran(ne, nh, kernel):
     """sc_tc_last_kernel (bench.py's roofline label) reports which tensor-core
