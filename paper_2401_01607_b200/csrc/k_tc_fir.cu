@@ -658,7 +658,14 @@ struct FsGeo {
     // H8 stage slots: one-stage units keep their single stage resident (one
     // slot; a multi-channel launch reloads it when the channel changes)
     static constexpr int NHS = ONE ? 1 : NHSLOT;
-    static constexpr int WROWS_FIT = (int)((SMEM_MAX - 256 - RAW - NHS * 2 * HST_PART) / (2 * 2 * KG * 16));
+    // TMEM accumulators: multi-stage units run four deep (all 512 columns), so
+    // the MMA warp keeps issuing through a unit's output store
+#ifndef FS_NACC_MULTI
+#define FS_NACC_MULTI 4
+#endif
+    static constexpr int NACC = ONE ? 2 : FS_NACC_MULTI;
+    static constexpr uint32_t BAR_BYTES = 320;
+    static constexpr int WROWS_FIT = (int)((SMEM_MAX - BAR_BYTES - RAW - NHS * 2 * HST_PART) / (2 * 2 * KG * 16));
     static constexpr int WPF = ONE ? SSH : ((WROWS_FIT - 1 - TN) / 8) * 8;  // most shifts per unit
     // rows per window slot; WROWS = 1 (mod 8) puts the K-group stride at 16
     // (mod 128) bytes, so the converters' 16-byte accesses -- consecutive
@@ -668,7 +675,7 @@ struct FsGeo {
     static constexpr uint32_t SM_RAW = 4 * XPART;                   // slot s, part p at (2s + p) * XPART
     static constexpr uint32_t SM_HST = SM_RAW + RAW;
     static constexpr uint32_t SM_BAR = SM_HST + NHS * 2 * HST_PART;
-    static constexpr uint32_t SM_TOTAL = SM_BAR + 256;
+    static constexpr uint32_t SM_TOTAL = SM_BAR + BAR_BYTES;
     static constexpr uint32_t IDESC = TcGeo<TN>::IDESC;
     static_assert(WPF >= SSH && WPF % SSH == 0, "window");
     static_assert(SM_TOTAL <= SMEM_MAX, "smem");
@@ -744,8 +751,9 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
     const uint32_t bar_xempty = sbase + SM_BAR + 16;  // + 8*slot
     const uint32_t bar_hfull = sbase + SM_BAR + 32;   // + 8*slot
     const uint32_t bar_hempty = sbase + SM_BAR + 48;  // + 8*slot
-    const uint32_t bar_tfull = sbase + SM_BAR + 64;   // + 8*acc
-    const uint32_t bar_tempty = sbase + SM_BAR + 80;  // + 8*acc
+    constexpr int NACC = G::NACC;                       // TMEM accumulators in the ring
+    const uint32_t bar_tfull = sbase + SM_BAR + 256;  // + 8*acc
+    const uint32_t bar_tempty = sbase + SM_BAR + 288; // + 8*acc
     const uint32_t bar_exfull = sbase + SM_BAR + 96;  // + 8*k, k = unit % 4
     // RAW is filled and drained in two halves (rows [0, RAW_ROWS_A) and the
     // rest), so the next window's first half is in flight while this one's
@@ -765,6 +773,8 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             mbar_init(bar_xempty + 8 * i, 1);
             mbar_init(bar_hfull + 8 * i, 1);
             mbar_init(bar_hempty + 8 * i, 1);
+        }
+        for (int i = 0; i < NACC; ++i) {
             mbar_init(bar_tfull + 8 * i, 1);
             mbar_init(bar_tempty + 8 * i, NEPI);
         }
@@ -777,7 +787,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"((uint32_t)(2 * TN)));
+                     "r"((uint32_t)(NACC * TN)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -957,8 +967,8 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                         mbar_wait(bar_hfull + 8 * slot, (hsc / G::NHS) & 1);
                         ++hsc;
                     }
-                    const uint32_t acc = dc & 1;
-                    if (dc >= 2) mbar_wait(bar_tempty + 8 * acc, ((dc >> 1) - 1) & 1);
+                    const uint32_t acc = dc % NACC;
+                    if (dc >= NACC) mbar_wait(bar_tempty + 8 * acc, ((dc / NACC) - 1) & 1);
                     tc_fence_after();
                     const uint32_t d_tmem = tmem + acc * TN;
                     uint32_t accumulate = 0;
@@ -1012,8 +1022,8 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                 mbar_wait(bar_exfull + 8 * (uc & 3), (uc >> 2) & 1);
                 const int e = ex_ring[uc & 3] + EH(ch);
                 const float inv = __int_as_float((127 - e) << 23);
-                const uint32_t acc = dc & 1;
-                mbar_wait(bar_tfull + 8 * acc, (dc >> 1) & 1);
+                const uint32_t acc = dc % NACC;
+                mbar_wait(bar_tfull + 8 * acc, (dc / NACC) & 1);
                 if (threadIdx.x == 64) FS_TRACE(5);
                 tc_fence_after();
                 const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * TN;
@@ -1039,8 +1049,9 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             for (int i = 0; i < TN; ++i) sum[i] = 0.0f;
 #pragma unroll 1
             for (int64_t st = 0; st < n_stages; ++st, ++dc) {
-                const uint32_t acc = dc & 1;
-                mbar_wait(bar_tfull + 8 * acc, (dc >> 1) & 1);
+                const uint32_t acc = dc % NACC;
+                mbar_wait(bar_tfull + 8 * acc, (dc / NACC) & 1);
+                if (st == 0 && threadIdx.x == 64) FS_TRACE(5);
                 tc_fence_after();
                 const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * TN;
 #pragma unroll
@@ -1058,11 +1069,20 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             mbar_wait(bar_exfull + 8 * (uc & 3), (uc >> 2) & 1);
             const int e = ex_ring[uc & 3] + EH(ch);
             const float inv = __int_as_float((127 - e) << 23);  // 2^-e, |e| <= 126 (checked)
+            if (threadIdx.x == 64) FS_TRACE(7);
+            if (nb + (int64_t)(TN - 1) * TR < a.n_end) {
+                // whole tile in range: immediate-offset stores, no per-element bound
+                float *yp = yc + (nb - a.n_begin);
 #pragma unroll
-            for (int i = 0; i < TN; ++i) {
-                const int64_t n = nb + (int64_t)i * TR;
-                if (n < a.n_end) yc[n - a.n_begin] = sum[i] * inv;
+                for (int i = 0; i < TN; ++i) yp[i * TR] = sum[i] * inv;
+            } else {
+#pragma unroll
+                for (int i = 0; i < TN; ++i) {
+                    const int64_t n = nb + (int64_t)i * TR;
+                    if (n < a.n_end) yc[n - a.n_begin] = sum[i] * inv;
+                }
             }
+            if (threadIdx.x == 64) FS_TRACE(6);
         }
     } else {
         // ---------------------------------------------------------------- converters
@@ -1317,7 +1337,7 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(2 * TN)));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(NACC * TN)));
     }
     if constexpr (ONE) {
         if (a.fold) {
@@ -1564,10 +1584,10 @@ int launch_fs_impl(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, in
         cudaFree(a.trace);
         const unsigned long long t0 = h[0];
         for (int k = 0; k < 32 && h[k * 8]; ++k)
-            fprintf(stderr, "[fs] unit %2d conv %7.2f load %7.2f ready %7.2f | mma %7.2f issued %7.2f | epi %7.2f done %7.2f us\n",
+            fprintf(stderr, "[fs] unit %2d conv %7.2f load %7.2f ready %7.2f | mma %7.2f issued %7.2f | epi %7.2f store %7.2f done %7.2f us\n",
                     k, (h[k * 8 + 0] - t0) * 1e-3, (h[k * 8 + 1] - t0) * 1e-3, (h[k * 8 + 2] - t0) * 1e-3,
                     (h[k * 8 + 3] - t0) * 1e-3, (h[k * 8 + 4] - t0) * 1e-3, (h[k * 8 + 5] - t0) * 1e-3,
-                    (h[k * 8 + 6] - t0) * 1e-3);
+                    h[k * 8 + 7] ? (h[k * 8 + 7] - t0) * 1e-3 : 0.0, (h[k * 8 + 6] - t0) * 1e-3);
     }
     note_tc_launch(SSH, G::TN, n_tiles * (int64_t)TR * G::TN * (int64_t)TR * s8, SC_TC_KERNEL_FUSED_SPLIT);
     if (nsplit > 1) {
