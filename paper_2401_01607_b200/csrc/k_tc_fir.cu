@@ -647,7 +647,16 @@ __global__ void __launch_bounds__(256) k_tc_prep(const float *__restrict__ x, in
 template <int SSH, bool ONE = false>
 struct FsGeo {
     static constexpr int TN = 128;                                  // output rows per tile (UMMA N)
-    static constexpr int NEPI = 4, NCONV = ONE ? FS_NCONV1 : 4;
+    // multi-stage units: FS_NEPI_MULTI epilogue warps (8 = two per TMEM lane
+    // quarter, half the accumulator's columns each) and FS_NCONV_MULTI
+    // converter warps (8 = two groups of four on alternating units)
+#ifndef FS_NEPI_MULTI
+#define FS_NEPI_MULTI 4
+#endif
+#ifndef FS_NCONV_MULTI
+#define FS_NCONV_MULTI 4
+#endif
+    static constexpr int NEPI = ONE ? 4 : FS_NEPI_MULTI, NCONV = ONE ? FS_NCONV1 : FS_NCONV_MULTI;
     static constexpr int THREADS = 64 + 32 * (NEPI + NCONV);
     static constexpr int SGROUPS = 2 * KG - 1 + KG * (SSH - 1);
     static constexpr uint32_t HST_PART = SGROUPS * 128;
@@ -1044,18 +1053,21 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
                 ++dc;
                 continue;
             }
-            float sum[TN];
+            // NEPI = 8: warps 2..5 take columns [0, TN/2), warps 6..9 the rest
+            constexpr int CPW = TN / (NEPI / 4);
+            const int c0 = ((warp - 2) >> 2) * CPW;
+            float sum[CPW];
 #pragma unroll
-            for (int i = 0; i < TN; ++i) sum[i] = 0.0f;
+            for (int i = 0; i < CPW; ++i) sum[i] = 0.0f;
 #pragma unroll 1
             for (int64_t st = 0; st < n_stages; ++st, ++dc) {
                 const uint32_t acc = dc % NACC;
                 mbar_wait(bar_tfull + 8 * acc, (dc / NACC) & 1);
                 if (st == 0 && threadIdx.x == 64) FS_TRACE(5);
                 tc_fence_after();
-                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * TN;
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * TN + c0;
 #pragma unroll
-                for (int c = 0; c < TN; c += 32) {
+                for (int c = 0; c < CPW; c += 32) {
                     float v[32];
                     tmem_ld32(taddr + c, v);
 #pragma unroll
@@ -1072,13 +1084,13 @@ __global__ void __launch_bounds__(FsGeo<SSH, ONE>::THREADS, 1) k_tc_fir_fs(FsArg
             if (threadIdx.x == 64) FS_TRACE(7);
             if (nb + (int64_t)(TN - 1) * TR < a.n_end) {
                 // whole tile in range: immediate-offset stores, no per-element bound
-                float *yp = yc + (nb - a.n_begin);
+                float *yp = yc + (nb - a.n_begin) + (int64_t)c0 * TR;
 #pragma unroll
-                for (int i = 0; i < TN; ++i) yp[i * TR] = sum[i] * inv;
+                for (int i = 0; i < CPW; ++i) yp[i * TR] = sum[i] * inv;
             } else {
 #pragma unroll
-                for (int i = 0; i < TN; ++i) {
-                    const int64_t n = nb + (int64_t)i * TR;
+                for (int i = 0; i < CPW; ++i) {
+                    const int64_t n = nb + (int64_t)(c0 + i) * TR;
                     if (n < a.n_end) yc[n - a.n_begin] = sum[i] * inv;
                 }
             }
