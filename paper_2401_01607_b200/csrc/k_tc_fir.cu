@@ -1472,7 +1472,24 @@ int launch_fs_impl(const float *x, int64_t ldx, int64_t x_base, int64_t x_lo, in
         const int k = v ? atoi(v) : 0;
         return (int64_t)(k >= 2 && k <= G::WPF ? k : G::WPF);
     }();
-    if (s8 > fs_max_s8 || cdiv(n_len, (int64_t)TR * G::TN) * channels < 2 * (int64_t)sm_count()) return SC_ERR_STATE;
+    static const int64_t fs_min_tiles_x2 = [] {
+        const char *v = getenv("SC_FS_MIN_TILES_X2");  // A/B knob: least tiles per SM, in halves (default 4 = 2 per SM)
+        return (int64_t)(v ? atoi(v) : 4);
+    }();
+    // One-wave launches (a quarter to all of the SMs busy with one tile each)
+    // of 512-1,024-tap filters also run here: measured against the image path
+    // (profiles/r02_fs_small_launch.txt) 2^20 samples x 512 / 1,024 taps
+    // 0.036 -> 0.032 / 0.038 -> 0.034 ms, 2^21 samples 0.038 -> 0.032 / 0.046
+    // -> 0.036 ms; longer filters and 1-2 wave launches are mixed (wave
+    // quantisation) and keep the image path.  SC_FS_SMALL=0 disables (A/B).
+    static const bool fs_small = [] {
+        const char *v = getenv("SC_FS_SMALL");
+        return !(v && atoi(v) == 0);
+    }();
+    const int64_t tiles_all = cdiv(n_len, (int64_t)TR * G::TN) * channels;
+    const bool small_ok = fs_small && s_needed > 4 && s8 <= 10 && 4 * tiles_all >= (int64_t)sm_count() &&
+                          tiles_all <= (int64_t)sm_count();
+    if (s8 > fs_max_s8 || (2 * tiles_all < fs_min_tiles_x2 * (int64_t)sm_count() && !small_ok)) return SC_ERR_STATE;
     const int64_t ngroups = KG * s8 + KG - 1;
     const int64_t h8_ch = ngroups * 64;
     const int64_t tiles_per_ch = cdiv(n_len, (int64_t)TR * G::TN);

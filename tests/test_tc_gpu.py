@@ -206,6 +206,25 @@ def test_fused_split_large_launch(nh):
     _fs_check(x, h, y)
 
 
+@pytest.mark.parametrize("ne,nh", [((1 << 20) + 777, 600), (1 << 21, 1024), (700_001, 1000)])
+def test_fused_split_one_wave_launch(ne, nh):
+    """One-wave launches (37..148 tiles) of 512-1,024-tap filters take the
+    multi-stage fused-split units with shift-range splits."""
+    import torch
+
+    from paper_2401_01607_b200 import _native as N
+
+    rng = np.random.default_rng(ne % 1000 + nh)
+    x = rng.uniform(-1, 1, ne).astype(np.float32)
+    h = (rng.standard_normal(nh) * np.exp(-np.arange(nh) / (nh / 4 + 1))).astype(np.float32)
+    N.lib().sc_tc_stats_reset()
+    y = scatter_convolve(Signal(torch.from_numpy(x).cuda()), Signal(torch.from_numpy(h).cuda()))
+    y = y.concatenated().samples.cpu().numpy()
+    assert N.tc_stats()["kernel"] == "k_tc_fir_fs"
+    assert len(y) == ne + nh - 1
+    _fs_check(x, h, y)
+
+
 @pytest.mark.parametrize("nh", [26, 33, 47])
 def test_fused_split_short_filters_from_26_taps(nh):
     """FAST dispatch takes the fused-split tensor cores from 26 taps on
