@@ -36,9 +36,11 @@
 // 4-shift drains and 112-shift X windows for launches that fill the SMs;
 // N = 128 with 8-shift drains (or 2 for <= 2-shift filters) otherwise.
 //
-// k_tc_fir_fs (end of file) is the fused-split variant for short filters:
-// converter warps read x as FP32 and build each unit's hi/lo window in
-// shared memory, so no split image goes through HBM.
+// k_tc_fir_fs (end of file) is the fused-split variant for short and medium
+// filters (up to 72 padded shifts, ~9,000 taps, on launches of >= 2 tiles per
+// SM or one wave of 512-1,024-tap work): converter warps read x as FP32 and
+// build each unit's hi/lo window in shared memory, so no split image goes
+// through HBM; multi-stage units ring through four TMEM accumulators.
 
 #include <cuda_fp16.h>
 
